@@ -1,0 +1,163 @@
+/*
+ * halfwave_b200.h — C ABI of the B200 (sm_100a) staggered-grid leapfrog hot path.
+ *
+ * This is the drop-in boundary for the reference package's solver entry points
+ * (reference: /root/reference/pkg/src/halfwave, "halfwave"):
+ *
+ *   AcousticSolver.__init__ / .run / .step_baseline / .step_compensated
+ *       acoustic.py:56-97, 113-128, 185-236
+ *   ElasticSolver.__init__ / .run / .step_baseline / .step_compensated
+ *       elastic.py:63-113, 132-147, 242-296
+ *
+ * The reference has no FFI of its own (pure Python/numpy); these entry points are
+ * what its Python classes would bind with ctypes, one call per run()/step_*().
+ * The whole `for n in range(nt)` loop (acoustic.py:210-226, elastic.py:271-286)
+ * runs behind hw_run(); the host crosses the boundary once per call.
+ *
+ * Plain C types only: pointers, sizes, fixed-width integers, IEEE doubles.
+ * No C++ exceptions cross this boundary; every entry point returns an hw_status.
+ *
+ * Axis naming is generic so one descriptor covers 2D and 3D:
+ *   x   — fastest axis (reference 2D "x", periodic)
+ *   mid — 3D only (3D "y"); nm == 1 in 2D
+ *   slow— slab / slowest axis (reference 2D "y", 3D "z"); free surfaces live here
+ * Arrays are row-major with x fastest ([s][m][x]), matching grids.py:3.
+ */
+#ifndef HALFWAVE_B200_H
+#define HALFWAVE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HW_ABI_VERSION 1
+
+typedef enum hw_status {
+    HW_OK = 0,
+    HW_RANGE_FAILURE = 1, /* RangeFailureError (diagnostics.py:24-32); state holds the failing step */
+    HW_EINVAL = 2,        /* bad argument (ValueError in the reference) */
+    HW_ECUDA = 3,         /* CUDA runtime error */
+    HW_ENCCL = 4          /* NCCL error (multi-GPU halo exchange) */
+} hw_status;
+
+enum hw_equation { HW_EQ_ACOUSTIC = 0, HW_EQ_ELASTIC = 1 };        /* MediumKind, grids.py:126-128 */
+enum hw_lane { HW_FP16 = 16, HW_FP32 = 32, HW_FP64 = 64 };         /* Precision, precision.py:35-41 */
+enum hw_variant { HW_NAIVE = 0, HW_OP3 = 3, HW_OP6 = 6 };          /* None / Variant.OP3 / OP6, efsum.py:30-37 */
+enum hw_bc { HW_BC_PERIODIC = 0, HW_BC_FREE_SURFACE = 1 };         /* Boundary, grids.py:59-64 */
+enum hw_source {
+    HW_SRC_NONE = 0,
+    HW_SRC_PRESSURE = 1,  /* SourceKind.PRESSURE_POINT, acoustic.py:176-181 */
+    HW_SRC_VSLOW = 2,     /* SourceKind.VY_POINT (2D vy / 3D vz), elastic.py:196-205 */
+    HW_SRC_EXPLOSIVE = 3  /* extension: into every normal-stress increment at (n+1/2) dt */
+};
+
+/* fp64 medium planes, already materialised on the host exactly as the reference
+ * builds them (extend_rows grids.py:321-331; lam + 2.0*mu, elastic.py:104;
+ * 4.0*mu*(lam+mu)/(lam+2.0*mu), elastic.py:110-113).  Each plane has the shape of
+ * the field it feeds (noted).  The library rounds each into its lane once
+ * (UpdatePipeline.update_plane / stencil_plane, stepping.py:47-56) and keeps the
+ * fp64 copies for the energy functionals (diagnostics.py:76-162). */
+enum hw_plane {
+    HW_PL_RHO_X = 0, /* shape of vx;  acoustic + elastic; U lane */
+    HW_PL_RHO_S = 1, /* shape of v_slow */
+    HW_PL_RHO_M = 2, /* shape of v_mid (3D only) */
+    HW_PL_BETA = 3,  /* shape of p (acoustic) */
+    HW_PL_LAM = 4,   /* shape of sxx (elastic); S lane + energy */
+    HW_PL_MU = 5,    /* shape of sxx (cell mu, energy only) */
+    HW_PL_STIFF = 6, /* shape of sxx: lam + 2 mu; S lane */
+    HW_PL_MU_N = 7,  /* shape of the shear stresses (node/edge mu reuses cell mu); S lane + energy */
+    HW_PL_EP = 8,    /* [2][nx]: plane-stress modulus on the top / bottom surface rows (free surface) */
+    HW_NPLANES = 9
+};
+
+typedef struct hw_desc {
+    int32_t abi_version;  /* HW_ABI_VERSION */
+    int32_t equation;     /* hw_equation */
+    int32_t ndim;         /* 2 or 3 */
+    int32_t order;        /* 4 (reference, stencil.py:34) or 2 (extension: inner tap pair only) */
+    int32_t bc_slow;      /* hw_bc on the slow axis; x and mid are periodic */
+    int32_t lane_s;       /* stencil precision */
+    int32_t lane_u;       /* update precision */
+    int32_t src_kind;     /* hw_source */
+    int64_t nx, nm, ns;   /* cells along x, mid (1 in 2D), slow */
+    double dx;            /* GridSpec.dx */
+    double dt;            /* GridSpec.dt, raw fp64; rounded into U by the library (stepping.py:30) */
+    double taps[4];       /* c1..c4 of StencilSpec.make, already rounded into lane_s (stencil.py:52-56) */
+    const double* plane[HW_NPLANES];
+    int64_t src_x, src_m, src_s;  /* source cell on its field's sub-grid */
+    const int64_t* receivers;     /* n_receivers triples (x, m, s); trace field is p (acoustic) or v_slow (elastic) */
+    int32_t n_receivers;
+    int32_t world_size;           /* slab decomposition over the slow axis; 1 = single GPU */
+    int32_t rank;
+    int32_t device;               /* CUDA device ordinal for this rank */
+    const void* nccl_unique_id;   /* 128-byte ncclUniqueId when world_size > 1 */
+    int64_t energy_every;         /* AcousticSolver(energy_every=...), >= 1 */
+} hw_desc;
+
+typedef struct hw_solver hw_solver; /* opaque; owns device state, medium, streams, NCCL comm */
+
+/* Number of state fields (solution + residual) and their external order:
+ *   acoustic 2D: p vx vy rp rvx rvy                       (AcousticState, acoustic.py:35-50)
+ *   acoustic 3D: p vx vy vz rp rvx rvy rvz
+ *   elastic 2D : vx vy sxx syy sxy rvx rvy rsxx rsyy rsxy (ElasticState, elastic.py:43-57)
+ *   elastic 3D : vx vy vz sxx syy szz sxy sxz syz + 9 residuals
+ * fail_field from hw_run indexes this list (check_finite order, acoustic.py:154-160). */
+int hw_num_fields(int32_t equation, int32_t ndim);
+
+/* Shape of external field f as (slow, mid, x) extents. */
+int hw_field_shape(const hw_desc* d, int32_t field, int64_t shape[3]);
+
+/* Validate the descriptor, allocate device state (zeros) and materialise the medium.
+ * Mirrors the solver constructors (acoustic.py:56-97, elastic.py:63-113).  The host
+ * side has already done the reference's ValueError validation; this re-checks the
+ * invariants the kernels depend on.  The handle is bound to desc->device. */
+int hw_create(const hw_desc* desc, hw_solver** out);
+int hw_destroy(hw_solver* h);
+
+/* Upload / download every state field in external order.  Each pointer addresses a
+ * row-major host array of lane_u storage (uint16 fp16 bits, float, or double) with
+ * the field's full (global) shape; a rank > 0 of a multi-GPU job reads/writes only
+ * its own slab rows.  Mirrors _load_work / _flush_work (acoustic.py:137-152). */
+int hw_set_state(hw_solver* h, const void* const* fields);
+int hw_get_state(hw_solver* h, void* const* fields);
+
+/* March nt steps from step index step0 (AcousticSolver.run, acoustic.py:185-236;
+ * ElasticSolver.run, elastic.py:242-296) on the device-resident state.
+ *   variant     hw_variant
+ *   src_samples nt fp64 samples sample_source(t_n) (sources.py:57-69), NULL if no source
+ *   traces      [n_receivers][nt] fp64 receiver samples recorded after each step
+ *   e_times, e_vals  capacity 1 + nt/energy_every; E(t=0) first, then every sample step
+ *   n_energy    number of energy samples written
+ *   fail_step, fail_field  set on HW_RANGE_FAILURE (first non-finite field in
+ *               check_finite order at the first failing step; state stops after it).
+ * Any of the output pointers may be NULL.  Blocks until the device is done. */
+int hw_run(hw_solver* h, int32_t variant, int64_t step0, int64_t nt, const double* src_samples,
+           double* traces, double* e_times, double* e_vals, int64_t* n_energy,
+           int64_t* fail_step, int32_t* fail_field);
+
+/* Device-resident timing helper for benchmarks: same as hw_run but outputs stay on
+ * the device (no host copies).  Returns the device time of the marched steps in ms
+ * (CUDA events on the solver's stream) through *ms. */
+int hw_run_device(hw_solver* h, int32_t variant, int64_t step0, int64_t nt,
+                  const double* src_samples, float* ms);
+
+/* Kernel launches issued by the last hw_run / hw_run_device (evidence for bench.py). */
+int64_t hw_last_launch_count(const hw_solver* h);
+
+/* Average duration (ms) of the dominant (fused step) kernel in the last
+ * hw_run_device, measured with CUDA events on the launching stream; 0 if unknown. */
+double hw_last_kernel_ms(const hw_solver* h);
+
+/* Thread-local message for the last non-OK status. */
+const char* hw_last_error(void);
+
+/* Library build identity (sm arch, ABI version). */
+const char* hw_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HALFWAVE_B200_H */

@@ -1,0 +1,118 @@
+"""ctypes binding of the C ABI in include/halfwave_b200.h.
+
+The shared library is built in-tree (``make`` or ``__graft_entry__.build()``) to
+``paper_2310_00236_b200/lib/libhalfwave_b200.so`` for sm_100a.  There is no CPU
+fallback: if the library is missing, or no CUDA device is usable, every solver
+call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libhalfwave_b200.so"
+
+ABI_VERSION = 1
+
+# hw_status
+OK, RANGE_FAILURE, EINVAL, ECUDA, ENCCL = 0, 1, 2, 3, 4
+# hw_equation
+EQ_ACOUSTIC, EQ_ELASTIC = 0, 1
+# hw_variant
+NAIVE, OP3, OP6 = 0, 3, 6
+# hw_bc
+BC_PERIODIC, BC_FREE_SURFACE = 0, 1
+# hw_source
+SRC_NONE, SRC_PRESSURE, SRC_VSLOW, SRC_EXPLOSIVE = 0, 1, 2, 3
+# hw_plane
+PL_RHO_X, PL_RHO_S, PL_RHO_M, PL_BETA, PL_LAM, PL_MU, PL_STIFF, PL_MU_N, PL_EP = range(9)
+NPLANES = 9
+
+EXPORTED = (
+    "hw_num_fields", "hw_field_shape", "hw_create", "hw_destroy", "hw_set_state",
+    "hw_get_state", "hw_run", "hw_run_device", "hw_last_launch_count",
+    "hw_last_kernel_ms", "hw_last_error", "hw_version",
+)
+
+
+class Desc(ctypes.Structure):
+    """Mirror of ``hw_desc``; field order and types must match the header."""
+
+    _fields_ = [
+        ("abi_version", ctypes.c_int32),
+        ("equation", ctypes.c_int32),
+        ("ndim", ctypes.c_int32),
+        ("order", ctypes.c_int32),
+        ("bc_slow", ctypes.c_int32),
+        ("lane_s", ctypes.c_int32),
+        ("lane_u", ctypes.c_int32),
+        ("src_kind", ctypes.c_int32),
+        ("nx", ctypes.c_int64),
+        ("nm", ctypes.c_int64),
+        ("ns", ctypes.c_int64),
+        ("dx", ctypes.c_double),
+        ("dt", ctypes.c_double),
+        ("taps", ctypes.c_double * 4),
+        ("plane", ctypes.POINTER(ctypes.c_double) * NPLANES),
+        ("src_x", ctypes.c_int64),
+        ("src_m", ctypes.c_int64),
+        ("src_s", ctypes.c_int64),
+        ("receivers", ctypes.POINTER(ctypes.c_int64)),
+        ("n_receivers", ctypes.c_int32),
+        ("world_size", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("nccl_unique_id", ctypes.c_void_p),
+        ("energy_every", ctypes.c_int64),
+    ]
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load the sm_100a library once; raise loudly if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build the CUDA library first "
+            "(`make` or `python -c 'import __graft_entry__ as g; g.build()'`); "
+            "there is no CPU fallback"
+        )
+    lib = ctypes.CDLL(str(LIB_PATH))
+    P = ctypes.POINTER
+    vp = ctypes.c_void_p
+    i32, i64, dbl = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    lib.hw_num_fields.argtypes = [i32, i32]
+    lib.hw_num_fields.restype = ctypes.c_int
+    lib.hw_field_shape.argtypes = [P(Desc), i32, P(i64)]
+    lib.hw_create.argtypes = [P(Desc), P(vp)]
+    lib.hw_destroy.argtypes = [vp]
+    lib.hw_set_state.argtypes = [vp, P(vp)]
+    lib.hw_get_state.argtypes = [vp, P(vp)]
+    lib.hw_run.argtypes = [vp, i32, i64, i64, P(dbl), P(dbl), P(dbl), P(dbl), P(i64), P(i64), P(i32)]
+    lib.hw_run_device.argtypes = [vp, i32, i64, i64, P(dbl), P(ctypes.c_float)]
+    lib.hw_last_launch_count.argtypes = [vp]
+    lib.hw_last_launch_count.restype = i64
+    lib.hw_last_kernel_ms.argtypes = [vp]
+    lib.hw_last_kernel_ms.restype = dbl
+    lib.hw_last_error.argtypes = []
+    lib.hw_last_error.restype = ctypes.c_char_p
+    lib.hw_version.argtypes = []
+    lib.hw_version.restype = ctypes.c_char_p
+    for name in ("hw_create", "hw_destroy", "hw_set_state", "hw_get_state", "hw_run", "hw_run_device"):
+        getattr(lib, name).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    return load().hw_last_error().decode()
+
+
+def check(status: int, what: str) -> None:
+    if status != OK:
+        raise RuntimeError(f"{what} failed (status {status}): {last_error()}")

@@ -1,0 +1,229 @@
+// hw_common.cuh — device data layout and shared step machinery.
+//
+// HBM layout:
+//   * every field is [rows + 2G][nm][pitch] in its update-lane storage type, with
+//     G = 2 ghost slabs on each end of the slow axis and pitch a multiple of 32
+//     elements (64 B rows for fp16); `base` points at (s=0, m=0, x=0).
+//   * x and mid are periodic through index arithmetic; the slow axis reads its
+//     ghost slabs, which encode the boundary condition and are kept current by the
+//     kernel that writes the field ("write-through ghosts": periodic wrap copies or
+//     free-surface image rows with a parity sign flip, stencil.py:121-144), or by
+//     the NCCL halo exchange at slab boundaries of a multi-GPU job.
+//   * medium planes are strided views: constant (0,0,0), slow-layered (1,0,0) or
+//     full (nm*nx, nx, 1), so layered media cost no HBM traffic per cell.
+#pragma once
+#include <stdint.h>
+#include "hw_lanes.cuh"
+
+namespace hw {
+
+constexpr int G = 2;          // ghost slabs per side (4th-order staggered reach)
+constexpr int NCOMP = 5;      // energy partial components per block
+constexpr int BLOCK = 256;    // threads per block for the phase kernels
+
+enum GhostMode { GHOST_NONE = 0, GHOST_PERIODIC = 1, GHOST_IMAGE = 2 };
+
+struct FieldView {
+    void* base;       // element (s=0, m=0, x=0)
+    int64_t rows;     // slow-axis extent (ns or ns+1)
+    int32_t gmode;    // GhostMode for write-through
+    int32_t half_s;   // field sits on the half-offset slow sub-grid
+    int32_t odd;      // free-surface parity: image rows are negated
+    int32_t bit;      // external field index (check_finite order) for failure masks
+};
+
+struct Geom {
+    int64_t nx, nm, pitch;
+    int64_t slab;     // elements per slow index = nm * pitch
+};
+
+struct PlaneView {    // lane-rounded medium plane (storage type of its lane)
+    const void* p;
+    int64_t ss, sm, sx;
+};
+
+struct Plane64 {      // fp64 medium plane for the energy functionals
+    const double* p;
+    int64_t ss, sm, sx;
+};
+
+struct Ctrl {         // device-side run control
+    int64_t fail_step;      // first local step index with a non-finite write (INT64_MAX if none)
+    unsigned int fail_mask; // external field bits recorded at that step
+    unsigned int pad;
+};
+
+template <typename T>
+__device__ __forceinline__ T* frow(const FieldView& f, const Geom& g, int64_t s, int64_t m) {
+    return reinterpret_cast<T*>(f.base) + s * g.slab + m * g.pitch;
+}
+
+template <int L, int W>
+__device__ __forceinline__ vec<L, W> pload(const PlaneView& pv, int64_t s, int64_t m, int64_t x) {
+    using T = typename lane<L>::T;
+    const T* p = reinterpret_cast<const T*>(pv.p) + s * pv.ss + m * pv.sm;
+    if (pv.sx == 0) return vsplat<L, W>(p[0]);
+    return vload<L, W>(p + x);
+}
+
+__device__ __forceinline__ double p64(const Plane64& pv, int64_t s, int64_t m, int64_t x) {
+    return pv.p[s * pv.ss + m * pv.sm + x * pv.sx];
+}
+
+__device__ __forceinline__ int64_t wrap(int64_t i, int64_t n) {
+    return i < 0 ? i + n : (i >= n ? i - n : i);
+}
+
+// Four x taps around the W cells starting at x (periodic x, ddx_work stencil.py:98-107).
+// to_int: input on the half grid, shifts (-2,-1,0,1); else (-1,0,1,2).
+template <int LU, int W>
+__device__ __forceinline__ void xtaps(const typename lane<LU>::T* row, int64_t x, int64_t nx, bool to_int,
+                                      vec<LU, W> t[4]) {
+    if constexpr (W == 2) {
+        vec<LU, W> a = vload<LU, W>(row + wrap(x - 2, nx));
+        vec<LU, W> b = vload<LU, W>(row + x);
+        vec<LU, W> c = vload<LU, W>(row + wrap(x + 2, nx));
+        if (to_int) {
+            t[0] = a; t[1] = vshift(a, b); t[2] = b; t[3] = vshift(b, c);
+        } else {
+            t[0] = vshift(a, b); t[1] = b; t[2] = vshift(b, c); t[3] = c;
+        }
+    } else {
+        int64_t b0 = to_int ? x - 2 : x - 1;
+#pragma unroll
+        for (int j = 0; j < 4; j++) t[j].e[0] = row[wrap(b0 + j, nx)];
+    }
+}
+
+// Fixed fold (stencil.py:72-79) in the stencil lane; order 2 keeps the inner pair.
+// Taps arrive in the update lane and enter the stencil lane through one rounding
+// (UpdatePipeline.to_stencil, stepping.py:39-41; identity when the lanes agree).
+template <int LS, int LU, int W>
+__device__ __forceinline__ vec<LS, W> fold(const typename lane<LS>::T c[4], const vec<LU, W> tu[4], int order) {
+    using O = vops<LS, W>;
+    vec<LS, W> t1 = vcvt<LS, LU, W>(tu[1]), t2 = vcvt<LS, LU, W>(tu[2]);
+    vec<LS, W> inner = O::add(O::mul(vsplat<LS, W>(c[1]), t1), O::mul(vsplat<LS, W>(c[2]), t2));
+    if (order == 2) return inner;
+    vec<LS, W> t0 = vcvt<LS, LU, W>(tu[0]), t3 = vcvt<LS, LU, W>(tu[3]);
+    vec<LS, W> outer = O::add(O::mul(vsplat<LS, W>(c[0]), t0), O::mul(vsplat<LS, W>(c[3]), t3));
+    return O::add(inner, outer);
+}
+
+// Slow-axis taps of field f landing on row s (ghost slabs hold wrap / images).
+template <int LU, int W>
+__device__ __forceinline__ void staps(const FieldView& f, const Geom& g, int64_t s, int64_t m, int64_t x,
+                                      bool to_int, int order, vec<LU, W> t[4]) {
+    using T = typename lane<LU>::T;
+    int64_t b0 = to_int ? s - 2 : s - 1;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        if (order == 2 && (j == 0 || j == 3)) continue;
+        t[j] = vload<LU, W>(frow<T>(f, g, b0 + j, m) + x);
+    }
+    if (order == 2) { t[0] = t[1]; t[3] = t[2]; }
+}
+
+// Mid-axis taps (3D, periodic).
+template <int LU, int W>
+__device__ __forceinline__ void mtaps(const FieldView& f, const Geom& g, int64_t s, int64_t m, int64_t x,
+                                      bool to_int, int order, vec<LU, W> t[4]) {
+    using T = typename lane<LU>::T;
+    int64_t b0 = to_int ? m - 2 : m - 1;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        if (order == 2 && (j == 0 || j == 3)) continue;
+        t[j] = vload<LU, W>(frow<T>(f, g, s, wrap(b0 + j, g.nm)) + x);
+    }
+    if (order == 2) { t[0] = t[1]; t[3] = t[2]; }
+}
+
+// UpdatePipeline.increment (stepping.py:58-80) + .advance (stepping.py:82-98,
+// efsum.py:100-121) for W cells.  src_lane >= 0 marks the element holding the
+// point source, injected as round_U(src) before the division when src != 0.
+template <int LS, int LU, int W>
+__device__ __forceinline__ void finish(vec<LS, W> rhs, bool has_div, vec<LU, W> divisor,
+                                       typename lane<LU>::T dt, int variant, int src_lane, double src,
+                                       vec<LU, W>& u, vec<LU, W>& t) {
+    using O = vops<LU, W>;
+    using ln = lane<LU>;
+    vec<LU, W> x = vcvt<LU, LS, W>(rhs);
+    if (src_lane >= 0 && src != 0.0) {
+#pragma unroll
+        for (int i = 0; i < W; i++)
+            if (i == src_lane) x.e[i] = ln::add(x.e[i], ln::from_f64(src));
+    }
+    if (has_div) x = O::div(x, divisor);
+    x = O::mul(x, vsplat<LU, W>(dt));
+    if (variant == 0) {
+        u = O::add(u, x);
+        return;
+    }
+    vec<LU, W> r = O::add(t, x);
+    vec<LU, W> s = O::add(u, r);
+    if (variant == 3) {
+        vec<LU, W> z = O::sub(s, u);
+        t = O::sub(r, z);
+    } else {
+        vec<LU, W> pa = O::sub(s, r);
+        vec<LU, W> pb = O::sub(s, pa);
+        vec<LU, W> da = O::sub(u, pa);
+        vec<LU, W> db = O::sub(r, pb);
+        t = O::add(da, db);
+    }
+    u = s;
+}
+
+// Store W cells of field f at (s, m, x) and keep its ghost slabs current.
+template <int LU, int W>
+__device__ __forceinline__ void store_field(const FieldView& f, const Geom& g, int64_t s, int64_t m, int64_t x,
+                                            vec<LU, W> v) {
+    using T = typename lane<LU>::T;
+    vstore<LU, W>(frow<T>(f, g, s, m) + x, v);
+    if (f.gmode == GHOST_NONE) return;
+    int64_t n = f.rows;
+    if (f.gmode == GHOST_PERIODIC) {
+        if (s < G) vstore<LU, W>(frow<T>(f, g, n + s, m) + x, v);
+        if (s >= n - G) vstore<LU, W>(frow<T>(f, g, s - n, m) + x, v);
+        return;
+    }
+    vec<LU, W> w = f.odd ? vneg<LU, W>(v) : v;
+    int64_t k1, k2;
+    if (f.half_s) { k1 = -s - 1; k2 = 2 * n - 1 - s; }
+    else { k1 = -s; k2 = 2 * n - 2 - s; }
+    if (k1 < 0 && k1 >= -G) vstore<LU, W>(frow<T>(f, g, k1, m) + x, w);
+    if (k2 >= n && k2 < n + G) vstore<LU, W>(frow<T>(f, g, k2, m) + x, w);
+}
+
+// Warp-aggregated failure record: first failing step + external field bits.
+__device__ __forceinline__ void record_failure(Ctrl* ctrl, int64_t n, unsigned int mask) {
+    unsigned int any = __reduce_or_sync(0xffffffffu, mask);
+    if (any && (threadIdx.x & 31) == 0) {
+        atomicMin(reinterpret_cast<unsigned long long*>(&ctrl->fail_step), (unsigned long long)n);
+        atomicOr(&ctrl->fail_mask, any);
+    }
+}
+
+__device__ __forceinline__ bool halted(const Ctrl* ctrl, int64_t n) {
+    return *reinterpret_cast<const volatile int64_t*>(&ctrl->fail_step) < n;
+}
+
+// Block-wide fp64 sum of NCOMP components; thread 0 writes the block partial.
+__device__ __forceinline__ void block_partials(double v[NCOMP], double* out) {
+    __shared__ double red[BLOCK / 32][NCOMP];
+    int lane_id = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int c = 0; c < NCOMP; c++) {
+        double a = v[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+        if (lane_id == 0) red[warp][c] = a;
+    }
+    __syncthreads();
+    if (threadIdx.x < NCOMP) {
+        double a = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) a += red[w][threadIdx.x];
+        out[blockIdx.x * NCOMP + threadIdx.x] = a;
+    }
+}
+
+}  // namespace hw

@@ -1,0 +1,81 @@
+// hw_params.h — kernel parameter blocks shared by the launch layer and kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include "hw_common.cuh"
+
+// compile-time dispatch over lanes / vector width
+#define HW_DISPATCH_LU(LU, ...)                              \
+    switch (LU) {                                            \
+        case 16: { constexpr int LU_ = 16; __VA_ARGS__; } break; \
+        case 32: { constexpr int LU_ = 32; __VA_ARGS__; } break; \
+        default: { constexpr int LU_ = 64; __VA_ARGS__; } break; \
+    }
+#define HW_DISPATCH_LS(LS, ...)                              \
+    switch (LS) {                                            \
+        case 16: { constexpr int LS_ = 16; __VA_ARGS__; } break; \
+        case 32: { constexpr int LS_ = 32; __VA_ARGS__; } break; \
+        default: { constexpr int LS_ = 64; __VA_ARGS__; } break; \
+    }
+#define HW_DISPATCH_W(W, ...)                                \
+    if ((W) == 2) { constexpr int W_ = 2; __VA_ARGS__; }     \
+    else { constexpr int W_ = 1; __VA_ARGS__; }
+
+namespace hw {
+
+// Acoustic p-v leapfrog (acoustic.py:162-181), generic 2D / 3D.
+struct AcParams {
+    Geom g;
+    FieldView p, vx, vs, vm, rp, rvx, rvs, rvm;
+    PlaneView rho_x, rho_s, rho_m, beta;      // update lane (stepping.py:47-52)
+    Plane64 e_beta, e_rho_x, e_rho_s, e_rho_m; // fp64 (diagnostics.py:76-87)
+    double taps[4];                            // stencil-lane values
+    double dt_u;                               // update-lane value of dt
+    int32_t order, variant, d3, has_src;
+    int64_t src_x, src_m, src_s;
+    Ctrl* ctrl;
+    double* partials;                          // [nblocks][NCOMP]
+};
+
+// Elastic velocity-stress leapfrog (elastic.py:176-238), generic 2D / 3D.
+struct ElParams {
+    Geom g;
+    FieldView vx, vs, vm, sxx, sss, smm, sxs, sxm, sms;
+    FieldView rvx, rvs, rvm, rsxx, rsss, rsmm, rsxs, rsxm, rsms;
+    PlaneView rho_x, rho_s, rho_m;             // update lane
+    PlaneView stiff, lam, mu_n, ep;            // stencil lane; ep rows: 0 top, 1 bottom
+    Plane64 e_rho_x, e_rho_s, e_rho_m, e_lam, e_mu, e_mu_n;
+    double taps[4];
+    double dt_u;
+    int32_t order, variant, d3, fs;
+    int32_t src_kind;                          // HW_SRC_VSLOW / HW_SRC_EXPLOSIVE / none
+    int32_t pad;
+    int64_t src_x, src_m, src_s;
+    Ctrl* ctrl;
+    double* partials;
+};
+
+struct EpParams {      // per-step epilogue: receiver traces + energy finalisation
+    const void* trace_base; // field base for traces
+    const int64_t* rec_off; // element offsets from trace_base
+    int32_t n_rec;
+    int32_t nblocks;        // partial rows to reduce
+    double* traces;         // [n_rec][nt]
+    int64_t nt;
+    double* e_vals;
+    double scale;           // 0.5 dx^2 (2D) or 0.5 dx^3 (3D)
+    const double* partials;
+    const Ctrl* ctrl;
+};
+
+// launchers (one instantiation per lane pair and vector width)
+void launch_ac_vel(int LS, int LU, int W, const AcParams& P, int64_t n, int64_t nblocks, cudaStream_t st);
+void launch_ac_pres(int LS, int LU, int W, const AcParams& P, int64_t n, double src, int sample, int64_t nblocks,
+                    cudaStream_t st);
+void launch_ac_energy(int LU, int W, const AcParams& P, int64_t nblocks, cudaStream_t st);
+void launch_el_vel(int LS, int LU, int W, const ElParams& P, int64_t n, double src, int64_t nblocks, cudaStream_t st);
+void launch_el_stress(int LS, int LU, int W, const ElParams& P, int64_t n, double src, int sample, int64_t nblocks,
+                      cudaStream_t st);
+void launch_el_energy(int LU, int W, const ElParams& P, int64_t nblocks, cudaStream_t st);
+void launch_epilogue(int LU, const EpParams& E, int64_t n, int sample, int64_t eidx, cudaStream_t st);
+
+}  // namespace hw
