@@ -17,13 +17,11 @@ __global__ void __launch_bounds__(BLOCK) k_ac_vel(AcParams P, int64_t n) {
     using TS = typename lane<LS>::T;
     const Geom& g = P.g;
     const int64_t nxv = g.nx / W;
-    const int64_t tid = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
-    const int64_t total = nxv * g.nm * P.p.rows;
+    const int64_t xv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t m = blockIdx.y, s = blockIdx.z;
     unsigned int mask = 0;
-    if (tid < total) {
-        const int64_t x = (tid % nxv) * W;
-        const int64_t r = tid / nxv;
-        const int64_t m = r % g.nm, s = r / g.nm;
+    if (xv < nxv && s < P.p.rows) {
+        const int64_t x = xv * W;
         TS c[4];
 #pragma unroll
         for (int j = 0; j < 4; j++) c[j] = lane<LS>::from_f64(P.taps[j]);
@@ -82,14 +80,12 @@ __global__ void __launch_bounds__(BLOCK) k_ac_pres(AcParams P, int64_t n, double
     using TS = typename lane<LS>::T;
     const Geom& g = P.g;
     const int64_t nxv = g.nx / W;
-    const int64_t tid = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
-    const int64_t total = nxv * g.nm * P.p.rows;
+    const int64_t xv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t m = blockIdx.y, s = blockIdx.z;
     unsigned int mask = 0;
     double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    if (tid < total) {
-        const int64_t x = (tid % nxv) * W;
-        const int64_t r = tid / nxv;
-        const int64_t m = r % g.nm, s = r / g.nm;
+    if (xv < nxv && s < P.p.rows) {
+        const int64_t x = xv * W;
         TS c[4];
 #pragma unroll
         for (int j = 0; j < 4; j++) c[j] = lane<LS>::from_f64(P.taps[j]);
@@ -144,13 +140,11 @@ __global__ void __launch_bounds__(BLOCK) k_ac_energy(AcParams P) {
     using TU = typename lane<LU>::T;
     const Geom& g = P.g;
     const int64_t nxv = g.nx / W;
-    const int64_t tid = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
-    const int64_t total = nxv * g.nm * P.p.rows;
+    const int64_t xv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t m = blockIdx.y, s = blockIdx.z;
     double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    if (tid < total) {
-        const int64_t x = (tid % nxv) * W;
-        const int64_t r = tid / nxv;
-        const int64_t m = r % g.nm, s = r / g.nm;
+    if (xv < nxv && s < P.p.rows) {
+        const int64_t x = xv * W;
         vec<LU, W> p = vload<LU, W>(frow<TU>(P.p, g, s, m) + x);
         vec<LU, W> vx = vload<LU, W>(frow<TU>(P.vx, g, s, m) + x);
         vec<LU, W> vs = vload<LU, W>(frow<TU>(P.vs, g, s, m) + x);
@@ -178,14 +172,14 @@ __global__ void __launch_bounds__(BLOCK) k_ac_energy(AcParams P) {
 // ------------------------------------------------------------------ launchers
 
 void launch_ac_vel(int LS, int LU, int W, const AcParams& P, int64_t n, int64_t nblocks, cudaStream_t st) {
-    HW_DISPATCH_LS(LS, HW_DISPATCH_LU(LU, HW_DISPATCH_W(W, k_ac_vel<LS_, LU_, W_><<<nblocks, BLOCK, 0, st>>>(P, n))))
+    HW_DISPATCH_LS(LS, HW_DISPATCH_LU(LU, HW_DISPATCH_W(W, k_ac_vel<LS_, LU_, W_><<<grid3(P.g, W, nblocks), block3(P.g, W), 0, st>>>(P, n))))
 }
 void launch_ac_pres(int LS, int LU, int W, const AcParams& P, int64_t n, double src, int sample, int64_t nblocks,
                     cudaStream_t st) {
-    HW_DISPATCH_LS(LS, HW_DISPATCH_LU(LU, HW_DISPATCH_W(W, k_ac_pres<LS_, LU_, W_><<<nblocks, BLOCK, 0, st>>>(P, n, src, sample))))
+    HW_DISPATCH_LS(LS, HW_DISPATCH_LU(LU, HW_DISPATCH_W(W, k_ac_pres<LS_, LU_, W_><<<grid3(P.g, W, nblocks), block3(P.g, W), 0, st>>>(P, n, src, sample))))
 }
 void launch_ac_energy(int LU, int W, const AcParams& P, int64_t nblocks, cudaStream_t st) {
-    HW_DISPATCH_LU(LU, HW_DISPATCH_W(W, k_ac_energy<LU_, W_><<<nblocks, BLOCK, 0, st>>>(P)))
+    HW_DISPATCH_LU(LU, HW_DISPATCH_W(W, k_ac_energy<LU_, W_><<<grid3(P.g, W, nblocks), block3(P.g, W), 0, st>>>(P)))
 }
 
 }  // namespace hw

@@ -170,6 +170,7 @@ struct hw_solver {
     Ctrl* ctrl = nullptr;
     double* partials = nullptr;
     int64_t nblocks = 0;
+    int64_t max_rows = 0;
     double* traces = nullptr;
     int64_t traces_cap = 0;
     double* evals = nullptr;
@@ -397,8 +398,8 @@ int hw_create(const hw_desc* desc, hw_solver** out) {
     for (int pl = 0; pl < HW_NPLANES; pl++)
         if ((rc = upload_plane(h, pl))) return cleanup(rc);
     if (cudaMalloc(&h->ctrl, sizeof(Ctrl)) != cudaSuccess) return cleanup(fail(HW_ECUDA, "ctrl alloc"));
-    int64_t nxv = desc->nx / h->W;
-    h->nblocks = (nxv * desc->nm * max_rows + BLOCK - 1) / BLOCK;
+    h->max_rows = max_rows;
+    h->nblocks = grid_blocks(h->g, h->W, max_rows);
     if (cudaMalloc(&h->partials, h->nblocks * NCOMP * sizeof(double)) != cudaSuccess)
         return cleanup(fail(HW_ECUDA, "partials alloc"));
     if (desc->n_receivers > 0) {
@@ -532,7 +533,7 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
     else fill_params(h, L);
     A.variant = L.variant = variant;
     const int LS = h->LS, LU = h->LU, W = h->W;
-    const int64_t nb = h->nblocks;
+    const int64_t nb = h->max_rows;  // launchers take the slow extent of the grid
     const int64_t every = h->d.energy_every;
     const int sk = h->d.src_kind;
     int64_t launches = 0;

@@ -222,8 +222,26 @@ __device__ __forceinline__ void block_partials(double v[NCOMP], double* out) {
     if (threadIdx.x < NCOMP) {
         double a = 0.0;
         for (int w = 0; w < (int)(blockDim.x >> 5); w++) a += red[w][threadIdx.x];
-        out[blockIdx.x * NCOMP + threadIdx.x] = a;
+        const int64_t bid = ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        out[bid * NCOMP + threadIdx.x] = a;
     }
+}
+
+// Launch shape of the phase kernels: x vectors across blockIdx.x (one row segment
+// per block), mid index on blockIdx.y, slow index on blockIdx.z — no integer division.
+inline int block_threads(int64_t nxv) {
+    int64_t b = (nxv + 31) / 32 * 32;
+    return (int)(b > BLOCK ? BLOCK : (b < 32 ? 32 : b));
+}
+inline dim3 block3(const Geom& g, int W) { return dim3(block_threads(g.nx / W)); }
+inline dim3 grid3(const Geom& g, int W, int64_t rows) {
+    int64_t nxv = g.nx / W;
+    int bt = block_threads(nxv);
+    return dim3((unsigned)((nxv + bt - 1) / bt), (unsigned)g.nm, (unsigned)rows);
+}
+inline int64_t grid_blocks(const Geom& g, int W, int64_t rows) {
+    dim3 gr = grid3(g, W, rows);
+    return (int64_t)gr.x * gr.y * gr.z;
 }
 
 }  // namespace hw

@@ -37,12 +37,11 @@ __global__ void __launch_bounds__(BLOCK) k_el_vel(ElParams P, int64_t n, double 
     const Geom& g = P.g;
     const int64_t nxv = g.nx / W;
     const int64_t rows = P.vx.rows > P.vs.rows ? P.vx.rows : P.vs.rows;
-    const int64_t tid = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
+    const int64_t xv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t m = blockIdx.y, s = blockIdx.z;
     unsigned int mask = 0;
-    if (tid < nxv * g.nm * rows) {
-        const int64_t x = (tid % nxv) * W;
-        const int64_t r = tid / nxv;
-        const int64_t m = r % g.nm, s = r / g.nm;
+    if (xv < nxv && s < rows) {
+        const int64_t x = xv * W;
         TS c[4];
 #pragma unroll
         for (int j = 0; j < 4; j++) c[j] = lane<LS>::from_f64(P.taps[j]);
@@ -105,13 +104,12 @@ __global__ void __launch_bounds__(BLOCK) k_el_stress(ElParams P, int64_t n, doub
     const Geom& g = P.g;
     const int64_t nxv = g.nx / W;
     const int64_t rows = P.sxx.rows > P.sxs.rows ? P.sxx.rows : P.sxs.rows;
-    const int64_t tid = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
+    const int64_t xv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t m = blockIdx.y, s = blockIdx.z;
     unsigned int mask = 0;
     double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    if (tid < nxv * g.nm * rows) {
-        const int64_t x = (tid % nxv) * W;
-        const int64_t r = tid / nxv;
-        const int64_t m = r % g.nm, s = r / g.nm;
+    if (xv < nxv && s < rows) {
+        const int64_t x = xv * W;
         TS c[4];
 #pragma unroll
         for (int j = 0; j < 4; j++) c[j] = lane<LS>::from_f64(P.taps[j]);
@@ -274,12 +272,11 @@ __global__ void __launch_bounds__(BLOCK) k_el_energy(ElParams P) {
     const Geom& g = P.g;
     const int64_t nxv = g.nx / W;
     const int64_t rows = P.sxx.rows > P.sxs.rows ? P.sxx.rows : P.sxs.rows;
-    const int64_t tid = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
+    const int64_t xv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t m = blockIdx.y, s = blockIdx.z;
     double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    if (tid < nxv * g.nm * rows) {
-        const int64_t x = (tid % nxv) * W;
-        const int64_t r = tid / nxv;
-        const int64_t m = r % g.nm, s = r / g.nm;
+    if (xv < nxv && s < rows) {
+        const int64_t x = xv * W;
         if (s < P.sxx.rows) {
             const bool surf = P.fs && (s == 0 || s == P.sxx.rows - 1);
             const double w = surf ? 0.5 : 1.0;
@@ -343,14 +340,14 @@ __global__ void __launch_bounds__(BLOCK) k_el_energy(ElParams P) {
 }
 
 void launch_el_vel(int LS, int LU, int W, const ElParams& P, int64_t n, double src, int64_t nblocks, cudaStream_t st) {
-    HW_DISPATCH_LS(LS, HW_DISPATCH_LU(LU, HW_DISPATCH_W(W, k_el_vel<LS_, LU_, W_><<<nblocks, BLOCK, 0, st>>>(P, n, src))))
+    HW_DISPATCH_LS(LS, HW_DISPATCH_LU(LU, HW_DISPATCH_W(W, k_el_vel<LS_, LU_, W_><<<grid3(P.g, W, nblocks), block3(P.g, W), 0, st>>>(P, n, src))))
 }
 void launch_el_stress(int LS, int LU, int W, const ElParams& P, int64_t n, double src, int sample, int64_t nblocks,
                       cudaStream_t st) {
-    HW_DISPATCH_LS(LS, HW_DISPATCH_LU(LU, HW_DISPATCH_W(W, k_el_stress<LS_, LU_, W_><<<nblocks, BLOCK, 0, st>>>(P, n, src, sample))))
+    HW_DISPATCH_LS(LS, HW_DISPATCH_LU(LU, HW_DISPATCH_W(W, k_el_stress<LS_, LU_, W_><<<grid3(P.g, W, nblocks), block3(P.g, W), 0, st>>>(P, n, src, sample))))
 }
 void launch_el_energy(int LU, int W, const ElParams& P, int64_t nblocks, cudaStream_t st) {
-    HW_DISPATCH_LU(LU, HW_DISPATCH_W(W, k_el_energy<LU_, W_><<<nblocks, BLOCK, 0, st>>>(P)))
+    HW_DISPATCH_LU(LU, HW_DISPATCH_W(W, k_el_energy<LU_, W_><<<grid3(P.g, W, nblocks), block3(P.g, W), 0, st>>>(P)))
 }
 
 }  // namespace hw
