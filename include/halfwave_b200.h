@@ -151,6 +151,12 @@ int64_t hw_last_launch_count(const hw_solver* h);
  * hw_run_device, measured with CUDA events on the launching stream; 0 if unknown. */
 double hw_last_kernel_ms(const hw_solver* h);
 
+/* Self-test: compare the branch-free binary16 division used for medium divisors
+ * against the IEEE path (__fdiv_rn, then one RNE to binary16) for all 2^16 x
+ * (2^16 - 2050) operand pairs on `device`.  *mismatches receives the count;
+ * *first_pair the first failing (a << 16 | b) bit patterns. */
+int hw_selftest_div16(int32_t device, uint64_t* mismatches, uint32_t* first_pair);
+
 /* Thread-local message for the last non-OK status. */
 const char* hw_last_error(void);
 

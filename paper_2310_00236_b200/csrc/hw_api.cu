@@ -57,6 +57,31 @@ double round_lane(int lane_bits, double x) {
 
 int lane_bytes(int L) { return L == 16 ? 2 : (L == 32 ? 4 : 8); }
 
+// binary16 bit pattern of a value already exactly representable in binary16.
+uint16_t half_bits(double v) {
+    uint16_t sign = std::signbit(v) ? 0x8000 : 0;
+    double a = std::fabs(v);
+    if (a == 0.0) return sign;
+    if (std::isinf(a)) return sign | 0x7c00;
+    if (std::isnan(a)) return 0x7e00;
+    int e;
+    double m = std::frexp(a, &e);  // a = m 2^e, m in [0.5, 1)
+    int E = e - 1;
+    if (E >= -14) return sign | (uint16_t)((E + 15) << 10) | (uint16_t)std::lround((m * 2.0 - 1.0) * 1024.0);
+    return sign | (uint16_t)std::lround(std::ldexp(a, 24));
+}
+
+LaneConsts make_consts(const double taps[4], double dt_u) {
+    LaneConsts c;
+    for (int j = 0; j < 5; j++) {
+        double v = j < 4 ? taps[j] : dt_u;
+        c.h[j] = half_bits(v);
+        c.f[j] = (float)v;
+        c.d[j] = v;
+    }
+    return c;
+}
+
 // internal field ids (generic axes) and their staggers (half_x, half_m, half_s)
 enum { F_P, F_VX, F_VS, F_VM, F_SXX, F_SSS, F_SMM, F_SXS, F_SXM, F_SMS, F_N };
 const int HALF_S[F_N] = {0, 0, 1, 0, 0, 0, 0, 1, 0, 1};
@@ -147,6 +172,28 @@ __global__ void k_epilogue(EpParams E, int64_t n, int sample, int64_t eidx) {
     }
 }
 
+// Exhaustive check of the branch-free binary16 division against the IEEE one:
+// every binary16 a (incl. inf/NaN/zero/subnormal) x every finite nonzero b.
+__global__ void k_selftest_div16(unsigned long long* bad, unsigned int* first) {
+    const unsigned int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= 65536u) return;
+    const __half ha = __ushort_as_half((unsigned short)a);
+    unsigned long long nbad = 0;
+    for (unsigned int b = 0; b < 65536u; b++) {
+        if ((b & 0x7fffu) == 0 || (b & 0x7c00u) == 0x7c00u) continue;
+        const __half hb = __ushort_as_half((unsigned short)b);
+        const unsigned short x = __half_as_ushort(lane<16>::div(ha, hb));
+        const unsigned short y = __half_as_ushort(lane<16>::div_ieee(ha, hb));
+        const bool xn = (x & 0x7c00u) == 0x7c00u && (x & 0x3ffu);
+        const bool yn = (y & 0x7c00u) == 0x7c00u && (y & 0x3ffu);
+        if (x != y && !(xn && yn)) {
+            nbad++;
+            atomicCAS(first, 0xffffffffu, (a << 16) | b);
+        }
+    }
+    if (nbad) atomicAdd(bad, nbad);
+}
+
 }  // namespace
 
 namespace hw {
@@ -214,7 +261,7 @@ int64_t plane_rows(const hw_solver* h, int pl) {
 // Upload one fp64 plane, compressed to constant / slow-layered / full, plus its lane copy.
 int upload_plane(hw_solver* h, int pl) {
     int64_t rows = plane_rows(h, pl);
-    h->lp[pl] = PlaneView{nullptr, 0, 0, 0};
+    h->lp[pl] = PlaneView{nullptr, 0, 0, 0, 0, 0};
     h->ep64[pl] = Plane64{nullptr, 0, 0, 0};
     if (!rows) return HW_OK;
     const double* src = h->d.plane[pl];
@@ -255,7 +302,12 @@ int upload_plane(hw_solver* h, int pl) {
         else if (L == 32) k_round_plane<float><<<nb, 256>>>(d64, (float*)dl, cnt, L);
         else k_round_plane<double><<<nb, 256>>>(d64, (double*)dl, cnt, L);
         CU(cudaGetLastError());
-        h->lp[pl] = PlaneView{dl, ss, sm, sx};
+        bool fast = true;  // every lane value finite and nonzero (binary16 subnormals allowed)
+        for (double v : packed) {
+            double r = round_lane(L, v);
+            if (!(r != 0.0 && std::isfinite(r))) fast = false;
+        }
+        h->lp[pl] = PlaneView{dl, ss, sm, sx, fast ? 1 : 0, 0};
     }
     return HW_OK;
 }
@@ -269,8 +321,7 @@ void fill_params(const hw_solver* h, AcParams& P) {
     P.beta = h->lp[HW_PL_BETA];
     P.e_beta = h->ep64[HW_PL_BETA]; P.e_rho_x = h->ep64[HW_PL_RHO_X];
     P.e_rho_s = h->ep64[HW_PL_RHO_S]; P.e_rho_m = h->ep64[HW_PL_RHO_M];
-    for (int j = 0; j < 4; j++) P.taps[j] = h->d.taps[j];
-    P.dt_u = h->dt_u;
+    P.k = make_consts(h->d.taps, h->dt_u);
     P.order = h->d.order;
     P.d3 = h->d3;
     P.has_src = h->d.src_kind == HW_SRC_PRESSURE;
@@ -292,8 +343,7 @@ void fill_params(const hw_solver* h, ElParams& P) {
     P.stiff = h->lp[HW_PL_STIFF]; P.lam = h->lp[HW_PL_LAM]; P.mu_n = h->lp[HW_PL_MU_N]; P.ep = h->lp[HW_PL_EP];
     P.e_rho_x = h->ep64[HW_PL_RHO_X]; P.e_rho_s = h->ep64[HW_PL_RHO_S]; P.e_rho_m = h->ep64[HW_PL_RHO_M];
     P.e_lam = h->ep64[HW_PL_LAM]; P.e_mu = h->ep64[HW_PL_MU]; P.e_mu_n = h->ep64[HW_PL_MU_N];
-    for (int j = 0; j < 4; j++) P.taps[j] = h->d.taps[j];
-    P.dt_u = h->dt_u;
+    P.k = make_consts(h->d.taps, h->dt_u);
     P.order = h->d.order;
     P.d3 = h->d3;
     P.fs = h->fs;
@@ -620,6 +670,27 @@ int64_t hw_last_launch_count(const hw_solver* h) { return h ? h->launches : 0; }
 double hw_last_kernel_ms(const hw_solver* h) { return h ? h->kernel_ms : 0.0; }
 
 const char* hw_last_error(void) { return g_err.c_str(); }
+
+int hw_selftest_div16(int32_t device, uint64_t* mismatches, uint32_t* first_pair) {
+    CU(cudaSetDevice(device));
+    unsigned long long* bad = nullptr;
+    unsigned int* first = nullptr;
+    CU(cudaMalloc(&bad, 8));
+    CU(cudaMalloc(&first, 4));
+    cudaMemset(bad, 0, 8);
+    cudaMemset(first, 0xff, 4);
+    k_selftest_div16<<<256, 256>>>(bad, first);
+    CU(cudaGetLastError());
+    unsigned long long nb = 0;
+    unsigned int fp = 0;
+    CU(cudaMemcpy(&nb, bad, 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(&fp, first, 4, cudaMemcpyDeviceToHost));
+    cudaFree(bad);
+    cudaFree(first);
+    if (mismatches) *mismatches = nb;
+    if (first_pair) *first_pair = fp;
+    return HW_OK;
+}
 
 const char* hw_version(void) { return "halfwave_b200 abi=1 arch=sm_100a"; }
 

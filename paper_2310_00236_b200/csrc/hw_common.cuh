@@ -40,7 +40,24 @@ struct Geom {
 struct PlaneView {    // lane-rounded medium plane (storage type of its lane)
     const void* p;
     int64_t ss, sm, sx;
+    int32_t fast_div;  // every value finite and nonzero: the branch-free exact division applies
+    int32_t pad;
 };
+
+// Lane constants converted once on the host (exact: the values are already
+// rounded into their lane): taps c1..c4 in the stencil lane, dt in the update lane.
+struct LaneConsts {
+    uint16_t h[5];
+    float f[5];
+    double d[5];
+};
+
+template <int L>
+__device__ __forceinline__ typename lane<L>::T lconst(const LaneConsts& c, int i) {
+    if constexpr (L == 16) return __ushort_as_half(c.h[i]);
+    else if constexpr (L == 32) return c.f[i];
+    else return c.d[i];
+}
 
 struct Plane64 {      // fp64 medium plane for the energy functionals
     const double* p;
@@ -141,7 +158,7 @@ __device__ __forceinline__ void mtaps(const FieldView& f, const Geom& g, int64_t
 // efsum.py:100-121) for W cells.  src_lane >= 0 marks the element holding the
 // point source, injected as round_U(src) before the division when src != 0.
 template <int LS, int LU, int W>
-__device__ __forceinline__ void finish(vec<LS, W> rhs, bool has_div, vec<LU, W> divisor,
+__device__ __forceinline__ void finish(vec<LS, W> rhs, int has_div, vec<LU, W> divisor,
                                        typename lane<LU>::T dt, int variant, int src_lane, double src,
                                        vec<LU, W>& u, vec<LU, W>& t) {
     using O = vops<LU, W>;
@@ -152,7 +169,8 @@ __device__ __forceinline__ void finish(vec<LS, W> rhs, bool has_div, vec<LU, W> 
         for (int i = 0; i < W; i++)
             if (i == src_lane) x.e[i] = ln::add(x.e[i], ln::from_f64(src));
     }
-    if (has_div) x = O::div(x, divisor);
+    if (has_div == 1) x = O::div(x, divisor);        // fast exact path (finite nonzero divisors)
+    else if (has_div == 2) x = O::div_ieee(x, divisor);
     x = O::mul(x, vsplat<LU, W>(dt));
     if (variant == 0) {
         u = O::add(u, x);

@@ -22,7 +22,23 @@ template <> struct lane<16> {
     static __device__ __forceinline__ T add(T a, T b) { return __hadd_rn(a, b); }
     static __device__ __forceinline__ T sub(T a, T b) { return __hsub_rn(a, b); }
     static __device__ __forceinline__ T mul(T a, T b) { return __hmul_rn(a, b); }
+    // Correctly rounded binary16 quotient without the IEEE-division slow path:
+    // q0 = a * rcp(b), one exact FMA residual, one FMA correction, then a single
+    // RNE to binary16.  Exhaustively verified bit-identical to
+    // __float2half_rn(__fdiv_rn(a, b)) for every binary16 a and every finite
+    // nonzero binary16 b (hw_selftest_div16, tests/test_gpu_parity.py); zero or
+    // non-finite divisors take div_ieee (the host picks per medium plane).
     static __device__ __forceinline__ T div(T a, T b) {
+        const float fa = __half2float(a), fb = __half2float(b);
+        float r;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(fb));
+        const float q0 = __fmul_rn(fa, r);
+        const float e = __fmaf_rn(-fb, q0, fa);
+        const float q1 = __fmaf_rn(e, r, q0);
+        const bool keep = (e == 0.0f) || !(fabsf(q0) < INFINITY);
+        return __float2half_rn(keep ? q0 : q1);
+    }
+    static __device__ __forceinline__ T div_ieee(T a, T b) {
         return __float2half_rn(__fdiv_rn(__half2float(a), __half2float(b)));
     }
     static __device__ __forceinline__ bool finite(T a) {
@@ -40,6 +56,7 @@ template <> struct lane<32> {
     static __device__ __forceinline__ T sub(T a, T b) { return __fsub_rn(a, b); }
     static __device__ __forceinline__ T mul(T a, T b) { return __fmul_rn(a, b); }
     static __device__ __forceinline__ T div(T a, T b) { return __fdiv_rn(a, b); }
+    static __device__ __forceinline__ T div_ieee(T a, T b) { return __fdiv_rn(a, b); }
     static __device__ __forceinline__ bool finite(T a) {
         return (__float_as_uint(a) & 0x7f800000u) != 0x7f800000u;
     }
@@ -55,6 +72,7 @@ template <> struct lane<64> {
     static __device__ __forceinline__ T sub(T a, T b) { return __dsub_rn(a, b); }
     static __device__ __forceinline__ T mul(T a, T b) { return __dmul_rn(a, b); }
     static __device__ __forceinline__ T div(T a, T b) { return __ddiv_rn(a, b); }
+    static __device__ __forceinline__ T div_ieee(T a, T b) { return __ddiv_rn(a, b); }
     static __device__ __forceinline__ bool finite(T a) {
         return (__double_as_longlong(a) & 0x7ff0000000000000ll) != 0x7ff0000000000000ll;
     }
@@ -92,6 +110,20 @@ __device__ __forceinline__ typename lane<LT>::T cvt(typename lane<LF>::T a) { re
 template <int L, int W> struct vec {
     typename lane<L>::T e[W];
 };
+// binary16 pairs live in one 32-bit register as __half2 so the packed ALU ops
+// need no repacking; e[] aliases the two halves for per-element access.
+template <> struct vec<16, 2> {
+    union {
+        __half2 h2;
+        __half e[2];
+    };
+    __device__ __forceinline__ vec() { *reinterpret_cast<unsigned int*>(&h2) = 0u; }
+    __device__ __forceinline__ vec(const vec& o) { *reinterpret_cast<unsigned int*>(&h2) = *reinterpret_cast<const unsigned int*>(&o.h2); }
+    __device__ __forceinline__ vec& operator=(const vec& o) {
+        *reinterpret_cast<unsigned int*>(&h2) = *reinterpret_cast<const unsigned int*>(&o.h2);
+        return *this;
+    }
+};
 
 template <int L, int W> struct vops {
     using V = vec<L, W>;
@@ -100,25 +132,36 @@ template <int L, int W> struct vops {
     static __device__ __forceinline__ V sub(V a, V b) { V r; _Pragma("unroll") for (int i = 0; i < W; i++) r.e[i] = ln::sub(a.e[i], b.e[i]); return r; }
     static __device__ __forceinline__ V mul(V a, V b) { V r; _Pragma("unroll") for (int i = 0; i < W; i++) r.e[i] = ln::mul(a.e[i], b.e[i]); return r; }
     static __device__ __forceinline__ V div(V a, V b) { V r; _Pragma("unroll") for (int i = 0; i < W; i++) r.e[i] = ln::div(a.e[i], b.e[i]); return r; }
+    static __device__ __forceinline__ V div_ieee(V a, V b) { V r; _Pragma("unroll") for (int i = 0; i < W; i++) r.e[i] = ln::div_ieee(a.e[i], b.e[i]); return r; }
 };
 
 template <> struct vops<16, 2> {
     using V = vec<16, 2>;
-    static __device__ __forceinline__ __half2 h2(V a) { return __halves2half2(a.e[0], a.e[1]); }
-    static __device__ __forceinline__ V unh2(__half2 x) { V r; r.e[0] = __low2half(x); r.e[1] = __high2half(x); return r; }
-    static __device__ __forceinline__ V add(V a, V b) { return unh2(__hadd2_rn(h2(a), h2(b))); }
-    static __device__ __forceinline__ V sub(V a, V b) { return unh2(__hsub2_rn(h2(a), h2(b))); }
-    static __device__ __forceinline__ V mul(V a, V b) { return unh2(__hmul2_rn(h2(a), h2(b))); }
+    static __device__ __forceinline__ V mk(__half2 x) { V r; r.h2 = x; return r; }
+    static __device__ __forceinline__ V add(V a, V b) { return mk(__hadd2_rn(a.h2, b.h2)); }
+    static __device__ __forceinline__ V sub(V a, V b) { return mk(__hsub2_rn(a.h2, b.h2)); }
+    static __device__ __forceinline__ V mul(V a, V b) { return mk(__hmul2_rn(a.h2, b.h2)); }
     static __device__ __forceinline__ V div(V a, V b) {
         V r;
         r.e[0] = lane<16>::div(a.e[0], b.e[0]);
         r.e[1] = lane<16>::div(a.e[1], b.e[1]);
         return r;
     }
+    static __device__ __forceinline__ V div_ieee(V a, V b) {
+        V r;
+        r.e[0] = lane<16>::div_ieee(a.e[0], b.e[0]);
+        r.e[1] = lane<16>::div_ieee(a.e[1], b.e[1]);
+        return r;
+    }
 };
 
 template <int L, int W>
 __device__ __forceinline__ vec<L, W> vsplat(typename lane<L>::T x) {
+    if constexpr (L == 16 && W == 2) {
+        vec<16, 2> r;
+        r.h2 = __half2half2(x);
+        return r;
+    }
     vec<L, W> r;
 #pragma unroll
     for (int i = 0; i < W; i++) r.e[i] = x;
@@ -135,6 +178,11 @@ __device__ __forceinline__ vec<LT, W> vcvt(vec<LF, W> a) {
 
 template <int L, int W>
 __device__ __forceinline__ vec<L, W> vneg(vec<L, W> a) {
+    if constexpr (L == 16 && W == 2) {
+        vec<16, 2> r;
+        r.h2 = __halves2half2(lane<16>::neg(__low2half(a.h2)), lane<16>::neg(__high2half(a.h2)));
+        return r;
+    }
     vec<L, W> r;
 #pragma unroll
     for (int i = 0; i < W; i++) r.e[i] = lane<L>::neg(a.e[i]);
@@ -144,6 +192,11 @@ __device__ __forceinline__ vec<L, W> vneg(vec<L, W> a) {
 // (a.e[W-1], b.e[0], ...): the vector shifted by one cell between neighbours a|b
 template <int L, int W>
 __device__ __forceinline__ vec<L, W> vshift(vec<L, W> a, vec<L, W> b) {
+    if constexpr (L == 16 && W == 2) {
+        vec<16, 2> r;
+        r.h2 = __halves2half2(__high2half(a.h2), __low2half(b.h2));  // one PRMT
+        return r;
+    }
     vec<L, W> r;
     r.e[0] = a.e[W - 1];
 #pragma unroll
@@ -154,6 +207,10 @@ __device__ __forceinline__ vec<L, W> vshift(vec<L, W> a, vec<L, W> b) {
 // per-element non-finite mask bit
 template <int L, int W>
 __device__ __forceinline__ bool vfinite(vec<L, W> a) {
+    if constexpr (L == 16 && W == 2) {
+        const unsigned int b = *reinterpret_cast<const unsigned int*>(&a.h2);
+        return ((b & 0x7c00u) != 0x7c00u) && ((b & 0x7c000000u) != 0x7c000000u);
+    }
     bool ok = true;
 #pragma unroll
     for (int i = 0; i < W; i++) ok = ok && lane<L>::finite(a.e[i]);
@@ -166,9 +223,7 @@ __device__ __forceinline__ vec<L, W> vload(const typename lane<L>::T* p) {
     if constexpr (W == 1) {
         r.e[0] = p[0];
     } else if constexpr (L == 16) {
-        __half2 x = *reinterpret_cast<const __half2*>(p);
-        r.e[0] = __low2half(x);
-        r.e[1] = __high2half(x);
+        r.h2 = *reinterpret_cast<const __half2*>(p);
     } else if constexpr (L == 32) {
         float2 x = *reinterpret_cast<const float2*>(p);
         r.e[0] = x.x;
@@ -186,7 +241,7 @@ __device__ __forceinline__ void vstore(typename lane<L>::T* p, vec<L, W> v) {
     if constexpr (W == 1) {
         p[0] = v.e[0];
     } else if constexpr (L == 16) {
-        *reinterpret_cast<__half2*>(p) = __halves2half2(v.e[0], v.e[1]);
+        *reinterpret_cast<__half2*>(p) = v.h2;
     } else if constexpr (L == 32) {
         *reinterpret_cast<float2*>(p) = make_float2(v.e[0], v.e[1]);
     } else {

@@ -28,8 +28,7 @@ struct AcParams {
     FieldView p, vx, vs, vm, rp, rvx, rvs, rvm;
     PlaneView rho_x, rho_s, rho_m, beta;      // update lane (stepping.py:47-52)
     Plane64 e_beta, e_rho_x, e_rho_s, e_rho_m; // fp64 (diagnostics.py:76-87)
-    double taps[4];                            // stencil-lane values
-    double dt_u;                               // update-lane value of dt
+    LaneConsts k;                              // taps (stencil lane) + dt (update lane)
     int32_t order, variant, d3, has_src;
     int64_t src_x, src_m, src_s;
     Ctrl* ctrl;
@@ -44,8 +43,7 @@ struct ElParams {
     PlaneView rho_x, rho_s, rho_m;             // update lane
     PlaneView stiff, lam, mu_n, ep;            // stencil lane; ep rows: 0 top, 1 bottom
     Plane64 e_rho_x, e_rho_s, e_rho_m, e_lam, e_mu, e_mu_n;
-    double taps[4];
-    double dt_u;
+    LaneConsts k;
     int32_t order, variant, d3, fs;
     int32_t src_kind;                          // HW_SRC_VSLOW / HW_SRC_EXPLOSIVE / none
     int32_t pad;

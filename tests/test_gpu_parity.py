@@ -182,3 +182,14 @@ def test_gpu_free_surface_syy_rows_bit_zero():
         assert np.all(rows[0].view(np.uint16) == 0)
         assert np.all(rows[-1].view(np.uint16) == 0)
     assert np.any(st.syy.values[1:-1] != 0.0)
+
+
+def test_gpu_fast_fp16_division_exhaustive():
+    """The branch-free binary16 division equals the IEEE path on all 2^16 x (2^16-2050) pairs."""
+    import ctypes
+
+    from paper_2310_00236_b200 import _abi
+
+    bad, first = ctypes.c_uint64(0), ctypes.c_uint32(0)
+    _abi.check(_abi.load().hw_selftest_div16(0, ctypes.byref(bad), ctypes.byref(first)), "selftest")
+    assert bad.value == 0, f"{bad.value} mismatches; first a,b = {first.value >> 16:#06x},{first.value & 0xffff:#06x}"
