@@ -19,6 +19,8 @@
 
 using namespace hw;
 
+#include "hw_fused2d.h"
+
 namespace {
 
 thread_local std::string g_err;
@@ -223,12 +225,17 @@ struct hw_solver {
     double* evals = nullptr;
     int64_t evals_cap = 0;
     int64_t* rec_off = nullptr;
+    int64_t* rec_xyz = nullptr;
     unsigned int res_bad = 0;   // residual fields holding non-finite values at upload
     cudaStream_t st = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int64_t launches = 0;
     double kernel_ms = 0.0;
     double dt_u = 0.0;
+    // fused single-pass path (2D acoustic, binary16): ping-pong partner buffers
+    bool fused = false;
+    int fused_blocks = 0;
+    void* mem_b[2 * F_N] = {};
 };
 
 namespace {
@@ -447,6 +454,27 @@ int hw_create(const hw_desc* desc, hw_solver** out) {
     }
     for (int pl = 0; pl < HW_NPLANES; pl++)
         if ((rc = upload_plane(h, pl))) return cleanup(rc);
+    {
+        const char* path = getenv("HALFWAVE_PATH");
+        bool want = !(path && strcmp(path, "generic") == 0);
+        int dev_smem = 0, nsm = 0;
+        cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, desc->device);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, desc->device);
+        if (want && h->ac && !h->d3 && h->LS == 16 && h->LU == 16 && desc->world_size == 1 &&
+            fused2d_eligible(desc->nx, dev_smem)) {
+            for (int j = 0; j < 2 * h->nsol; j++) {
+                int f = h->ext[j % h->nsol];
+                size_t bytes = (size_t)(field_rows(h, f) + 2 * G) * h->g.slab * esz;
+                if (cudaMalloc(&h->mem_b[j], bytes) != cudaSuccess) return cleanup(fail(HW_ECUDA, "out of memory (B)"));
+                cudaMemset(h->mem_b[j], 0, bytes);
+            }
+            if (fused2d_prepare(desc->nx) != cudaSuccess) return cleanup(fail(HW_ECUDA, "fused kernel setup failed"));
+            int64_t nbf = desc->ns / 4;
+            if (nbf < 1) nbf = 1;
+            h->fused_blocks = (int)(nbf < nsm ? nbf : nsm);
+            h->fused = true;
+        }
+    }
     if (cudaMalloc(&h->ctrl, sizeof(Ctrl)) != cudaSuccess) return cleanup(fail(HW_ECUDA, "ctrl alloc"));
     h->max_rows = max_rows;
     h->nblocks = grid_blocks(h->g, h->W, max_rows);
@@ -463,6 +491,8 @@ int hw_create(const hw_desc* desc, hw_solver** out) {
         }
         if (cudaMalloc(&h->rec_off, off.size() * 8) != cudaSuccess) return cleanup(fail(HW_ECUDA, "rec alloc"));
         cudaMemcpy(h->rec_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice);
+        if (cudaMalloc(&h->rec_xyz, off.size() * 24) != cudaSuccess) return cleanup(fail(HW_ECUDA, "rec alloc"));
+        cudaMemcpy(h->rec_xyz, desc->receivers, off.size() * 24, cudaMemcpyHostToDevice);
     }
     if (cudaDeviceSynchronize() != cudaSuccess) return cleanup(fail(HW_ECUDA, "setup failed"));
     *out = h;
@@ -473,12 +503,14 @@ int hw_destroy(hw_solver* h) {
     if (!h) return HW_OK;
     cudaSetDevice(h->d.device);
     for (void* p : h->mem) if (p) cudaFree(p);
+    for (void* p : h->mem_b) if (p) cudaFree(p);
     for (void* p : h->plane_mem) cudaFree(p);
     if (h->ctrl) cudaFree(h->ctrl);
     if (h->partials) cudaFree(h->partials);
     if (h->traces) cudaFree(h->traces);
     if (h->evals) cudaFree(h->evals);
     if (h->rec_off) cudaFree(h->rec_off);
+    if (h->rec_xyz) cudaFree(h->rec_xyz);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->st) cudaStreamDestroy(h->st);
@@ -594,6 +626,48 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
         launches += 2;
     }
     if (timed) CU(cudaEventRecord(h->ev0, h->st));
+    if (h->fused) {  // one fused kernel per step, ping-pong A <-> B
+        AcFusedParams F;
+        memset(&F, 0, sizeof(F));
+        F.nx = h->d.nx;
+        F.ns = h->d.ns;
+        F.pitch = h->g.pitch;
+        const int64_t ghost = (int64_t)G * h->g.slab * 2;  // bytes before row 0
+        __half* bufs[2][FUSED_NSTREAM];
+        // external order p vx vy rp rvx rvy == fused stream order
+        for (int j = 0; j < FUSED_NSTREAM; j++) {
+            bufs[0][j] = (__half*)((char*)h->mem[j] + ghost);
+            bufs[1][j] = (__half*)((char*)h->mem_b[j] + ghost);
+        }
+        F.rho_x = h->lp[HW_PL_RHO_X]; F.rho_s = h->lp[HW_PL_RHO_S]; F.beta = h->lp[HW_PL_BETA];
+        F.e_beta = h->ep64[HW_PL_BETA]; F.e_rho_x = h->ep64[HW_PL_RHO_X]; F.e_rho_s = h->ep64[HW_PL_RHO_S];
+        F.k = make_consts(h->d.taps, h->dt_u);
+        F.has_src = sk == HW_SRC_PRESSURE;
+        F.src_x = h->d.src_x;
+        F.src_s = h->d.src_s;
+        F.n_rec = (int32_t)nrec;
+        F.rec = h->rec_xyz;
+        F.traces = h->traces;
+        F.nt = nt;
+        F.ctrl = h->ctrl;
+        F.partials = h->partials;
+        F.e_vals = h->evals;
+        F.scale = E.scale;
+        for (int64_t n = 0; n < nt; n++) {
+            const int sample = energy && ((n + 1) % every == 0);
+            for (int j = 0; j < FUSED_NSTREAM; j++) {
+                F.in[j] = bufs[n & 1][j];
+                F.out[j] = bufs[(n + 1) & 1][j];
+            }
+            launch_ac2d_fused(variant, h->d.order, F, h->fused_blocks, n, src ? src[n] : 0.0, sample,
+                              (n + 1) / every, h->st);
+            launches++;
+        }
+        if (timed) CU(cudaEventRecord(h->ev1, h->st));
+        CU(cudaGetLastError());
+        h->launches = launches;
+        return HW_OK;
+    }
     for (int64_t n = 0; n < nt; n++) {
         const int sample = energy && ((n + 1) % every == 0);
         const double s = src ? src[n] : 0.0;
@@ -613,6 +687,20 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
     if (timed) CU(cudaEventRecord(h->ev1, h->st));
     CU(cudaGetLastError());
     h->launches = launches;
+    return HW_OK;
+}
+
+// After `executed` fused steps the newest state sits in buffer B when the count is
+// odd: copy it home so buffer A is always current between calls.
+static int fused_copy_back(hw_solver* h, int64_t executed, int32_t variant) {
+    if (!h->fused || (executed & 1) == 0) return HW_OK;
+    const int nf = variant == HW_NAIVE ? h->nsol : 2 * h->nsol;  // naive runs never touch residuals
+    for (int j = 0; j < nf; j++) {
+        int f = h->ext[j % h->nsol];
+        size_t bytes = (size_t)(field_rows(h, f) + 2 * G) * h->g.slab * lane_bytes(h->LU);
+        CU(cudaMemcpyAsync(h->mem[j], h->mem_b[j], bytes, cudaMemcpyDeviceToDevice, h->st));
+    }
+    CU(cudaStreamSynchronize(h->st));
     return HW_OK;
 }
 
@@ -636,6 +724,7 @@ int hw_run(hw_solver* h, int32_t variant, int64_t step0, int64_t nt, const doubl
         if (fail_field) *fail_field = bit;
         g_err = "non-finite value after step " + std::to_string(step0 + c.fail_step);
     }
+    if ((rc = fused_copy_back(h, done, variant))) return rc;
     int64_t nrec = h->d.n_receivers;
     if (traces && nrec > 0 && nt > 0) CU(cudaMemcpy(traces, h->traces, nrec * nt * sizeof(double), cudaMemcpyDeviceToHost));
     // energy samples of completed steps only: E0 + one per sample step before the failure
@@ -660,6 +749,9 @@ int hw_run_device(hw_solver* h, int32_t variant, int64_t step0, int64_t nt, cons
     CU(cudaEventSynchronize(h->ev1));
     float t = 0.f;
     CU(cudaEventElapsedTime(&t, h->ev0, h->ev1));
+    Ctrl c;
+    CU(cudaMemcpy(&c, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+    if ((rc = fused_copy_back(h, c.fail_step != INT64_MAX ? c.fail_step + 1 : nt, variant))) return rc;
     if (ms) *ms = t;
     h->kernel_ms = nt > 0 ? t / nt : 0.0;
     return HW_OK;

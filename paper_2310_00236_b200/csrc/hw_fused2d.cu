@@ -1,0 +1,351 @@
+// hw_fused2d.cu — single-pass fused leapfrog step for the 2D acoustic solver,
+// binary16 state (the BASELINE config-2 hot path), sm_100a.
+//
+// One kernel per time step does both phases of AcousticSolver._step_work
+// (acoustic.py:162-181): velocities from p^n, then p from div v^{n+1/2}, with
+// the reference's exact operation order (same device helpers as the phase
+// kernels, so the bits are identical).
+//
+// Work decomposition:
+//   * CTA b owns output rows [y0, y1) and the FULL row width: periodic x wraps
+//     inside the CTA, so no x halo is recomputed.  One CTA per SM.
+//   * The CTA streams rows f = y0-3 .. y1+2 top to bottom.  Input rows arrive
+//     in shared memory through 1D TMA bulk copies (cp.async.bulk + mbarrier
+//     complete_tx), FR ring slots, prefetched FR-1 rows ahead by one thread.
+//   * At front row f a thread (8 x cells, 4 half2) computes vx[f] (x taps from
+//     the smem row), vy[f-2] (slow taps from its register queue of p rows
+//     f-3..f), d/dx vx[f] (from a shared row, queued 3 rows) and finally p[f-3]
+//     (div = queued d/dx vx + slow taps of its vy queue), so every input byte
+//     is read from HBM once (plus a 6-row p / 3-row vy halo per CTA) and every
+//     output byte written once: 24 B per cell-step.
+//   * New state goes to the ping-pong buffer (no intra-step hazards between
+//     CTAs); energy partials (diagnostics.py:76-87), receiver traces and the
+//     non-finite flag are fused; the last CTA reduces the energy partials in a
+//     fixed order (deterministic).
+#include <cuda_runtime.h>
+
+#include "hw_fused2d.h"
+#include "hw_params.h"
+#include "hw_tma.cuh"
+
+namespace hw {
+
+constexpr int FCPT = 8;  // cells per thread
+constexpr int FR = 3;    // TMA ring slots (prefetch distance FR-1)
+constexpr int NSTREAM = FUSED_NSTREAM;
+enum { S_P = 0, S_VX = 1, S_VS = 2, S_RP = 3, S_RVX = 4, S_RVS = 5 };
+
+using H2 = vec<16, 2>;
+using O2 = vops<16, 2>;
+
+struct V8 {
+    H2 q[4];
+};
+
+__device__ __forceinline__ V8 lds8(const __half* p) {
+    V8 r;
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    *reinterpret_cast<unsigned int*>(&r.q[0].h2) = u.x;
+    *reinterpret_cast<unsigned int*>(&r.q[1].h2) = u.y;
+    *reinterpret_cast<unsigned int*>(&r.q[2].h2) = u.z;
+    *reinterpret_cast<unsigned int*>(&r.q[3].h2) = u.w;
+    return r;
+}
+
+__device__ __forceinline__ void st8(__half* p, const V8& v) {
+    uint4 u;
+    u.x = *reinterpret_cast<const unsigned int*>(&v.q[0].h2);
+    u.y = *reinterpret_cast<const unsigned int*>(&v.q[1].h2);
+    u.z = *reinterpret_cast<const unsigned int*>(&v.q[2].h2);
+    u.w = *reinterpret_cast<const unsigned int*>(&v.q[3].h2);
+    *reinterpret_cast<uint4*>(p) = u;
+}
+
+__device__ __forceinline__ H2 ld2(const __half* p) {
+    H2 r;
+    r.h2 = *reinterpret_cast<const __half2*>(p);
+    return r;
+}
+
+template <int ORDER>
+__device__ __forceinline__ H2 fold2(const __half c[4], H2 t0, H2 t1, H2 t2, H2 t3) {
+    H2 inner = O2::add(O2::mul(vsplat<16, 2>(c[1]), t1), O2::mul(vsplat<16, 2>(c[2]), t2));
+    if (ORDER == 2) return inner;
+    H2 outer = O2::add(O2::mul(vsplat<16, 2>(c[0]), t0), O2::mul(vsplat<16, 2>(c[3]), t3));
+    return O2::add(inner, outer);
+}
+
+// x derivative of 8 cells from the pair sequence Q[-1..4] (Q[0..3] = own cells).
+// to_int: shifts (-2,-1,0,1); else (-1,0,1,2)  (stencil.py:39-40).
+template <int ORDER>
+__device__ __forceinline__ V8 xfold8(const __half c[4], H2 left, const V8& own, H2 right, bool to_int) {
+    H2 Q[6];
+    Q[0] = left;
+#pragma unroll
+    for (int j = 0; j < 4; j++) Q[j + 1] = own.q[j];
+    Q[5] = right;
+    H2 S[5];  // S[j] = cells (x+2j-1, x+2j)
+#pragma unroll
+    for (int j = 0; j < 5; j++) S[j] = vshift<16, 2>(Q[j], Q[j + 1]);
+    V8 r;
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+        r.q[j] = to_int ? fold2<ORDER>(c, Q[j], S[j], Q[j + 1], S[j + 1]) : fold2<ORDER>(c, S[j], Q[j + 1], S[j + 1], Q[j + 2]);
+    return r;
+}
+
+__device__ __forceinline__ H2 plane2(const PlaneView& pv, int64_t s, int64_t x) {
+    return pload<16, 2>(pv, s, 0, x);
+}
+
+__device__ __forceinline__ unsigned int nonfinite8(const V8& v) {
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < 4; j++) ok = ok && vfinite<16, 2>(v.q[j]);
+    return ok ? 0u : 1u;
+}
+
+template <int V, int ORDER>
+__global__ void __launch_bounds__(512, 1)
+    k_ac2d_fused(AcFusedParams P, int64_t n, double src, int sample, int64_t eidx) {
+    if (halted(P.ctrl, n)) return;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    __half* ring = reinterpret_cast<__half*>(smem + 128);
+    const int64_t nx = P.nx, ns = P.ns, pitch = P.pitch;
+    __half* xrow = ring + (int64_t)FR * NSTREAM * nx;
+    const int nb = gridDim.x, b = blockIdx.x;
+    const int64_t y0 = (int64_t)b * ns / nb, y1 = (int64_t)(b + 1) * ns / nb;
+    const int64_t F0 = y0 - 3;
+    const int64_t NI = (y1 + 3) - F0;
+    const int tid = threadIdx.x;
+    const int64_t x = (int64_t)tid * FCPT;
+    constexpr bool comp = V != 0;
+    const uint32_t rb = (uint32_t)(nx * sizeof(__half));
+
+    auto slot_row = [&](int slot, int st) { return ring + ((int64_t)slot * NSTREAM + st) * nx; };
+    auto wrap_row = [&](int64_t r) {
+        r %= ns;
+        return r < 0 ? r + ns : r;
+    };
+    auto issue = [&](int64_t i) {  // TMA loads of iteration i (front row F0 + i)
+        const int64_t f = F0 + i;
+        const int slot = (int)(i % FR);
+        const bool lvx = f >= y0 && f < y1;
+        const bool lvs = f >= y0 && f < y1 + 3;
+        const bool lrp = comp && f >= y0 + 3 && f < y1 + 3;
+        const uint32_t rows = 1 + (lvx ? (comp ? 2 : 1) : 0) + (lvs ? (comp ? 2 : 1) : 0) + (lrp ? 1 : 0);
+        mbar_arrive_expect_tx(&bar[slot], rows * rb);
+        tma_load_1d(slot_row(slot, S_P), P.in[S_P] + wrap_row(f) * pitch, rb, &bar[slot]);
+        if (lvx) {
+            tma_load_1d(slot_row(slot, S_VX), P.in[S_VX] + f * pitch, rb, &bar[slot]);
+            if (comp) tma_load_1d(slot_row(slot, S_RVX), P.in[S_RVX] + f * pitch, rb, &bar[slot]);
+        }
+        if (lvs) {
+            const int64_t r = wrap_row(f - 2);
+            tma_load_1d(slot_row(slot, S_VS), P.in[S_VS] + r * pitch, rb, &bar[slot]);
+            if (comp) tma_load_1d(slot_row(slot, S_RVS), P.in[S_RVS] + r * pitch, rb, &bar[slot]);
+        }
+        if (lrp) tma_load_1d(slot_row(slot, S_RP), P.in[S_RP] + (f - 3) * pitch, rb, &bar[slot]);
+    };
+
+    if (tid == 0) {
+        for (int s = 0; s < FR; s++) mbar_init(&bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int64_t i = 0; i < FR - 1 && i < NI; i++) issue(i);
+
+    __half c[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) c[j] = lconst<16>(P.k, j);
+    const __half dt = lconst<16>(P.k, 4);
+    const int dmode_x = P.rho_x.fast_div ? 1 : 2, dmode_s = P.rho_s.fast_div ? 1 : 2,
+              dmode_b = P.beta.fast_div ? 1 : 2;
+    const int64_t xl = x == 0 ? nx - 2 : x - 2;          // left neighbour pair
+    const int64_t xr = x + FCPT >= nx ? 0 : x + FCPT;     // right neighbour pair
+
+    V8 pq0, pq1, pq2, pq3;  // p rows f, f-1, f-2, f-3 (own cells)
+    V8 vq0, vq1, vq2, vq3;  // vy_new rows f-2, f-3, f-4, f-5
+    V8 gq0, gq1, gq2, gq3;  // d/dx vx_new rows f, f-1, f-2, f-3
+    unsigned int mask = 0;
+    double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
+
+    for (int64_t i = 0; i < NI; i++) {
+        const int64_t f = F0 + i;
+        const int slot = (int)(i % FR);
+        if (tid == 0 && i + FR - 1 < NI) {
+            fence_proxy_async_smem();
+            issue(i + FR - 1);
+        }
+        mbar_wait(&bar[slot], (uint32_t)((i / FR) & 1));
+        const __half* prow = slot_row(slot, S_P);
+        pq3 = pq2; pq2 = pq1; pq1 = pq0;
+        pq0 = lds8(prow + x);
+        V8 vxn;
+        const bool do_vx = f >= y0 && f < y1;
+        if (do_vx) {  // vx[f] = advance(fl(fl(ddx p / rho_x) dt)) (acoustic.py:167-168)
+            V8 d = xfold8<ORDER>(c, ld2(prow + xl), pq0, ld2(prow + xr), false);
+            vxn = lds8(slot_row(slot, S_VX) + x);
+            V8 r = comp ? lds8(slot_row(slot, S_RVX) + x) : V8{};
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+                finish<16, 16, 2>(d.q[j], dmode_x, plane2(P.rho_x, f, x + 2 * j), dt, V, -1, 0.0, vxn.q[j], r.q[j]);
+            st8(P.out[S_VX] + f * pitch + x, vxn);
+            mask |= nonfinite8(vxn) << 1;
+            if (comp) {
+                st8(P.out[S_RVX] + f * pitch + x, r);
+                mask |= nonfinite8(r) << 4;
+            }
+            st8(xrow + x, vxn);
+            if (sample) {
+#pragma unroll
+                for (int j = 0; j < FCPT; j++) {
+                    const double v = (double)__half2float(vxn.q[j >> 1].e[j & 1]);
+                    e[1] += p64(P.e_rho_x, f, 0, x + j) * (v * v);
+                }
+            }
+        }
+        if (f >= y0 && f < y1 + 3) {  // vy[r = f-2] from p rows f-3..f (acoustic.py:169-170)
+            const int64_t r = f - 2;
+            V8 vsn = lds8(slot_row(slot, S_VS) + x);
+            V8 rr = comp ? lds8(slot_row(slot, S_RVS) + x) : V8{};
+            const int64_t rw = wrap_row(r);
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                H2 d = fold2<ORDER>(c, pq3.q[j], pq2.q[j], pq1.q[j], pq0.q[j]);
+                finish<16, 16, 2>(d, dmode_s, plane2(P.rho_s, rw, x + 2 * j), dt, V, -1, 0.0, vsn.q[j], rr.q[j]);
+            }
+            if (r >= y0 && r < y1) {
+                st8(P.out[S_VS] + r * pitch + x, vsn);
+                mask |= nonfinite8(vsn) << 2;
+                if (comp) {
+                    st8(P.out[S_RVS] + r * pitch + x, rr);
+                    mask |= nonfinite8(rr) << 5;
+                }
+                if (sample) {
+#pragma unroll
+                    for (int j = 0; j < FCPT; j++) {
+                        const double v = (double)__half2float(vsn.q[j >> 1].e[j & 1]);
+                        e[2] += p64(P.e_rho_s, r, 0, x + j) * (v * v);
+                    }
+                }
+            }
+            vq3 = vq2; vq2 = vq1; vq1 = vq0; vq0 = vsn;
+        }
+        __syncthreads();  // xrow holds vx_new[f]
+        gq3 = gq2; gq2 = gq1; gq1 = gq0;
+        if (do_vx) gq0 = xfold8<ORDER>(c, ld2(xrow + xl), vxn, ld2(xrow + xr), true);
+        const int64_t k = f - 3;
+        if (k >= y0 && k < y1) {  // p[k]: div = fl(ddx vx + ddy vy) (+src) / beta * dt (acoustic.py:172-181)
+            const V8 pold = pq3;
+            V8 pn = pold;
+            V8 rp = comp ? lds8(slot_row(slot, S_RP) + x) : V8{};
+            int src_j = -1, src_lane = -1;
+            if (P.has_src && k == P.src_s && P.src_x >= x && P.src_x < x + FCPT) {
+                src_j = (int)((P.src_x - x) >> 1);
+                src_lane = (int)((P.src_x - x) & 1);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                H2 gs = fold2<ORDER>(c, vq3.q[j], vq2.q[j], vq1.q[j], vq0.q[j]);
+                H2 dv = O2::add(gq3.q[j], gs);
+                finish<16, 16, 2>(dv, dmode_b, plane2(P.beta, k, x + 2 * j), dt, V, j == src_j ? src_lane : -1, src,
+                                  pn.q[j], rp.q[j]);
+            }
+            st8(P.out[S_P] + k * pitch + x, pn);
+            mask |= nonfinite8(pn);
+            if (comp) {
+                st8(P.out[S_RP] + k * pitch + x, rp);
+                mask |= nonfinite8(rp) << 3;
+            }
+            if (sample) {
+#pragma unroll
+                for (int j = 0; j < FCPT; j++) {
+                    const double a = (double)__half2float(pold.q[j >> 1].e[j & 1]);
+                    const double bb = (double)__half2float(pn.q[j >> 1].e[j & 1]);
+                    e[0] += p64(P.e_beta, k, 0, x + j) * (a * bb);
+                }
+            }
+            for (int q = 0; q < P.n_rec; q++) {  // receiver traces (acoustic.py:217-218)
+                const int64_t* rc = P.rec + 3 * q;
+                if (rc[2] == k && rc[0] >= x && rc[0] < x + FCPT) {
+                    const int o = (int)(rc[0] - x);
+                    P.traces[q * P.nt + n] = (double)__half2float(pn.q[o >> 1].e[o & 1]);
+                }
+            }
+        }
+        __syncthreads();  // ring slot and xrow free for reuse
+    }
+    record_failure(P.ctrl, n, mask);
+    if (!sample) return;
+    block_partials(e, P.partials);
+    __threadfence();
+    __syncthreads();
+    __shared__ unsigned int is_last;
+    if (tid == 0) is_last = atomicAdd(&P.ctrl->pad, 1u) == (unsigned int)(nb - 1);
+    __syncthreads();
+    if (!is_last) return;
+    __shared__ double tot[NCOMP];
+    if (tid < NCOMP) {
+        double a = 0.0;
+        for (int bi = 0; bi < nb; bi++) a += __ldcg(&P.partials[(int64_t)bi * NCOMP + tid]);
+        tot[tid] = a;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double t = tot[0];
+        for (int q = 1; q < NCOMP; q++) t += tot[q];
+        P.e_vals[eidx] = P.scale * t;
+        P.ctrl->pad = 0u;
+    }
+}
+
+size_t fused2d_smem_bytes(int64_t nx) { return 128 + ((size_t)FR * NSTREAM + 1) * nx * sizeof(__half); }
+
+int fused2d_threads(int64_t nx) { return (int)(nx / FCPT); }
+
+bool fused2d_eligible(int64_t nx, int max_smem) {
+    if (nx % 256 != 0 || nx / FCPT > 512) return false;
+    return fused2d_smem_bytes(nx) <= (size_t)max_smem;
+}
+
+#define FUSED_INST(V, ORD) (void*)k_ac2d_fused<V, ORD>
+static void* fused_fn(int variant, int order) {
+    if (order == 2) {
+        if (variant == 0) return FUSED_INST(0, 2);
+        if (variant == 3) return FUSED_INST(3, 2);
+        return FUSED_INST(6, 2);
+    }
+    if (variant == 0) return FUSED_INST(0, 4);
+    if (variant == 3) return FUSED_INST(3, 4);
+    return FUSED_INST(6, 4);
+}
+
+cudaError_t fused2d_prepare(int64_t nx) {
+    const int bytes = (int)fused2d_smem_bytes(nx);
+    for (int v : {0, 3, 6})
+        for (int o : {2, 4}) {
+            cudaError_t e = cudaFuncSetAttribute(fused_fn(v, o), cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+            if (e != cudaSuccess) return e;
+        }
+    return cudaSuccess;
+}
+
+void launch_ac2d_fused(int variant, int order, const AcFusedParams& P, int nblocks, int64_t n, double src, int sample,
+                       int64_t eidx, cudaStream_t st) {
+    const int threads = fused2d_threads(P.nx);
+    const size_t bytes = fused2d_smem_bytes(P.nx);
+    if (order == 2) {
+        if (variant == 0) k_ac2d_fused<0, 2><<<nblocks, threads, bytes, st>>>(P, n, src, sample, eidx);
+        else if (variant == 3) k_ac2d_fused<3, 2><<<nblocks, threads, bytes, st>>>(P, n, src, sample, eidx);
+        else k_ac2d_fused<6, 2><<<nblocks, threads, bytes, st>>>(P, n, src, sample, eidx);
+    } else {
+        if (variant == 0) k_ac2d_fused<0, 4><<<nblocks, threads, bytes, st>>>(P, n, src, sample, eidx);
+        else if (variant == 3) k_ac2d_fused<3, 4><<<nblocks, threads, bytes, st>>>(P, n, src, sample, eidx);
+        else k_ac2d_fused<6, 4><<<nblocks, threads, bytes, st>>>(P, n, src, sample, eidx);
+    }
+}
+
+}  // namespace hw

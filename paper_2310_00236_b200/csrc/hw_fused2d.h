@@ -1,0 +1,32 @@
+// hw_fused2d.h — host-side interface of the fused 2D acoustic step (hw_fused2d.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hw_common.cuh"
+
+namespace hw {
+constexpr int FUSED_NSTREAM = 6;
+struct AcFusedParams {
+    int64_t nx, ns, pitch;
+    const __half* in[FUSED_NSTREAM];  // p vx vy rp rvx rvy
+    __half* out[FUSED_NSTREAM];
+    PlaneView rho_x, rho_s, beta;
+    Plane64 e_beta, e_rho_x, e_rho_s;
+    LaneConsts k;
+    int32_t has_src, n_rec;
+    int64_t src_x, src_s;
+    const int64_t* rec;
+    double* traces;
+    int64_t nt;
+    Ctrl* ctrl;
+    double* partials;
+    double* e_vals;
+    double scale;
+};
+size_t fused2d_smem_bytes(int64_t nx);
+bool fused2d_eligible(int64_t nx, int max_smem);
+cudaError_t fused2d_prepare(int64_t nx);
+void launch_ac2d_fused(int variant, int order, const AcFusedParams& P, int nblocks, int64_t n, double src, int sample,
+                       int64_t eidx, cudaStream_t st);
+}  // namespace hw

@@ -1,0 +1,105 @@
+"""The fused single-pass 2D acoustic kernel (csrc/hw_fused2d.cu) against the CPU
+oracle and against the two-phase kernels: bit-exact fields and traces, energy
+within 1e-12 (its fixed-order block reduction differs from the phase kernels')."""
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2310_00236_b200 as hw
+from golden_cases import assert_same_bits
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(nx, ny, nt, *, order=4, amp=2.0, every=5, seed=0, src_row=3, layered=True):
+    rng = np.random.default_rng(seed)
+    dx = 1.0 / nx
+    med = (hw.build_layered_acoustic(nx, ny, [(0.5, 1.0, 1.0), (1.0, 1.5, 2.25)]) if layered
+           else hw.build_homogeneous_acoustic(nx, ny, 1.0, 1.0))
+    dt = float(np.float16(0.5 * dx / med.c_max()))
+    if dt > 0.5 * dx / med.c_max():
+        dt = float(np.nextafter(np.float16(dt), np.float16(0)))
+    grid = hw.GridSpec(nx, ny, dx, dt, nt, order=order)
+    src = hw.SourceSpec(hw.SourceKind.PRESSURE_POINT, nx // 2 + 1, src_row,
+                        hw.RickerSpec(f_center=1.0 / (10 * dx), amplitude=amp))
+    recs = ((nx // 2 + 1, src_row), (0, 0), (nx - 1, ny - 1), (7, ny // 2))
+    s = hw.AcousticSolver(grid, med, src, stencil_precision=hw.Precision.FP16, receivers=recs,
+                          energy_every=every)
+    st = s.new_state()
+    yy, xx = np.mgrid[0:ny, 0:nx] / nx
+    p0 = np.exp(-((xx - 0.5) ** 2 + (yy - 0.3) ** 2) / 0.01) + rng.uniform(-1e-3, 1e-3, (ny, nx))
+    st.p.values = p0.astype(np.float16)
+    st.vx.values = rng.uniform(-0.05, 0.05, (ny, nx)).astype(np.float16)
+    return s, st
+
+
+def _check(s, st, out, ref):
+    for j, n in enumerate(s.FIELDS):
+        assert_same_bits(getattr(st, n).values, ref["fields"][j], n)
+    np.testing.assert_array_equal(np.array([t.samples for t in out.traces]), ref["traces"])
+    np.testing.assert_array_equal(out.energy.times, ref["e_times"])
+    np.testing.assert_allclose(out.energy.values, ref["e_vals"], rtol=1e-12)
+
+
+@pytest.mark.parametrize("variant", [None, hw.Variant.OP3, hw.Variant.OP6])
+@pytest.mark.parametrize("order", [2, 4])
+def test_fused_matches_oracle(variant, order):
+    s, st = _case(512, 300, 37, order=order)  # odd nt: result copied home from the B buffer
+    ref = oracle.run_solver(s, variant, st)
+    out = s.run(variant, st)
+    _check(s, st, out, ref)
+
+
+@pytest.mark.parametrize("ny", [8, 13, 64, 600])
+def test_fused_row_bands_and_wrap(ny):
+    s, st = _case(256, ny, 24, layered=False, src_row=min(3, ny - 1))
+    ref = oracle.run_solver(s, hw.Variant.OP3, st)
+    out = s.run(hw.Variant.OP3, st)
+    _check(s, st, out, ref)
+
+
+def test_fused_equals_two_phase_kernels(monkeypatch):
+    s1, st1 = _case(1024, 256, 40)
+    out1 = s1.run(hw.Variant.OP3, st1)
+    monkeypatch.setenv("HALFWAVE_PATH", "generic")
+    s2, st2 = _case(1024, 256, 40)
+    out2 = s2.run(hw.Variant.OP3, st2)
+    for n in s1.FIELDS:
+        assert_same_bits(getattr(st1, n).values, getattr(st2, n).values, n)
+    np.testing.assert_array_equal(np.array([t.samples for t in out1.traces]),
+                                  np.array([t.samples for t in out2.traces]))
+    np.testing.assert_allclose(out1.energy.values, out2.energy.values, rtol=1e-12)
+
+
+def test_fused_range_failure_matches_oracle():
+    s, st = _case(256, 64, 400, amp=1e9, layered=False)
+    ref = oracle.run_solver(s, None, st)
+    assert ref["fail"] is not None
+    with pytest.raises(hw.RangeFailureError) as err:
+        s.run(None, st)
+    assert err.value.step == ref["fail"][0]
+    assert err.value.field_name == s._fail_name(ref["fail"][1])
+    assert st.step == ref["fail"][0] + 1
+    for j, n in enumerate(s.FIELDS):
+        assert_same_bits(getattr(st, n).values, ref["fields"][j], n)
+
+
+def test_fused_single_steps_and_resume():
+    s, st = _case(256, 40, 3)
+    ref = oracle.run_solver(s, hw.Variant.OP6, st, nt=8)
+    s.step_compensated(st, hw.Variant.OP6)
+    s.run(hw.Variant.OP6, st)
+    s.step_compensated(st, hw.Variant.OP6)
+    s.run(hw.Variant.OP6, st)
+    assert st.step == 8
+    for j, n in enumerate(s.FIELDS):
+        assert_same_bits(getattr(st, n).values, ref["fields"][j], n)
+
+
+def test_fused_path_is_selected():
+    s, st = _case(4096, 64, 2)
+    s.run(hw.Variant.OP3, st)
+    assert s.last_launch_count() == 2 + 2  # E0 kernel + finalize, then one fused launch per step
