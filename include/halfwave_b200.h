@@ -157,6 +157,15 @@ double hw_last_kernel_ms(const hw_solver* h);
  * *first_pair the first failing (a << 16 | b) bit patterns. */
 int hw_selftest_div16(int32_t device, uint64_t* mismatches, uint32_t* first_pair);
 
+/* The exhaustive per-divisor table behind the cheap binary16 division: bit b of
+ * the 1024 words is set iff fl16(fl32(a * rcp_rn(b))) == fl16(a / b) for every
+ * binary16 a (b = positive finite binary16 bit pattern).  Computed on `device`. */
+int hw_cheap_div_table(int32_t device, uint32_t* bits1024);
+
+/* Division mode the solver picked for a divisor plane (0 none, 1 fast exact,
+ * 2 IEEE, 3 cheap table-verified); -1 on bad arguments. */
+int hw_plane_div_mode(const hw_solver* h, int32_t plane);
+
 /* Thread-local message for the last non-OK status. */
 const char* hw_last_error(void);
 

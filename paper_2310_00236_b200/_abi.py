@@ -33,6 +33,7 @@ EXPORTED = (
     "hw_num_fields", "hw_field_shape", "hw_create", "hw_destroy", "hw_set_state",
     "hw_get_state", "hw_run", "hw_run_device", "hw_last_launch_count",
     "hw_last_kernel_ms", "hw_last_error", "hw_version", "hw_selftest_div16",
+    "hw_cheap_div_table", "hw_plane_div_mode",
 )
 
 
@@ -103,6 +104,10 @@ def load() -> ctypes.CDLL:
     lib.hw_last_error.restype = ctypes.c_char_p
     lib.hw_selftest_div16.argtypes = [i32, P(ctypes.c_uint64), P(ctypes.c_uint32)]
     lib.hw_selftest_div16.restype = ctypes.c_int
+    lib.hw_cheap_div_table.argtypes = [i32, P(ctypes.c_uint32)]
+    lib.hw_cheap_div_table.restype = ctypes.c_int
+    lib.hw_plane_div_mode.argtypes = [vp, i32]
+    lib.hw_plane_div_mode.restype = ctypes.c_int
     lib.hw_version.argtypes = []
     lib.hw_version.restype = ctypes.c_char_p
     for name in ("hw_create", "hw_destroy", "hw_set_state", "hw_get_state", "hw_run", "hw_run_device"):

@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(BLOCK) k_ac_vel(AcParams P, int64_t n) {
             vec<LS, W> d = fold<LS, LU, W>(c, t, P.order);
             vec<LU, W> u = vload<LU, W>(frow<TU>(P.vx, g, s, m) + x);
             vec<LU, W> rr = comp ? vload<LU, W>(frow<TU>(P.rvx, g, s, m) + x) : vec<LU, W>{};
-            finish<LS, LU, W>(d, P.rho_x.fast_div ? 1 : 2, pload<LU, W>(P.rho_x, s, m, x), dt, P.variant, -1, 0.0, u, rr);
+            finish<LS, LU, W>(d, &P.rho_x, s, m, x, dt, P.variant, -1, 0.0, u, rr);
             store_field<LU, W>(P.vx, g, s, m, x, u);
             if (!vfinite<LU, W>(u)) mask |= 1u << P.vx.bit;
             if (comp) {
@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(BLOCK) k_ac_vel(AcParams P, int64_t n) {
             vec<LS, W> d = fold<LS, LU, W>(c, t, P.order);
             vec<LU, W> u = vload<LU, W>(frow<TU>(P.vs, g, s, m) + x);
             vec<LU, W> rr = comp ? vload<LU, W>(frow<TU>(P.rvs, g, s, m) + x) : vec<LU, W>{};
-            finish<LS, LU, W>(d, P.rho_s.fast_div ? 1 : 2, pload<LU, W>(P.rho_s, s, m, x), dt, P.variant, -1, 0.0, u, rr);
+            finish<LS, LU, W>(d, &P.rho_s, s, m, x, dt, P.variant, -1, 0.0, u, rr);
             store_field<LU, W>(P.vs, g, s, m, x, u);
             if (!vfinite<LU, W>(u)) mask |= 1u << P.vs.bit;
             if (comp) {
@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(BLOCK) k_ac_vel(AcParams P, int64_t n) {
             vec<LS, W> d = fold<LS, LU, W>(c, t, P.order);
             vec<LU, W> u = vload<LU, W>(frow<TU>(P.vm, g, s, m) + x);
             vec<LU, W> rr = comp ? vload<LU, W>(frow<TU>(P.rvm, g, s, m) + x) : vec<LU, W>{};
-            finish<LS, LU, W>(d, P.rho_m.fast_div ? 1 : 2, pload<LU, W>(P.rho_m, s, m, x), dt, P.variant, -1, 0.0, u, rr);
+            finish<LS, LU, W>(d, &P.rho_m, s, m, x, dt, P.variant, -1, 0.0, u, rr);
             store_field<LU, W>(P.vm, g, s, m, x, u);
             if (!vfinite<LU, W>(u)) mask |= 1u << P.vm.bit;
             if (comp) {
@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(BLOCK) k_ac_pres(AcParams P, int64_t n, double
         const vec<LU, W> p_old = vload<LU, W>(frow<TU>(P.p, g, s, m) + x);
         vec<LU, W> u = p_old;
         vec<LU, W> rr = comp ? vload<LU, W>(frow<TU>(P.rp, g, s, m) + x) : vec<LU, W>{};
-        finish<LS, LU, W>(div, P.beta.fast_div ? 1 : 2, pload<LU, W>(P.beta, s, m, x), dt, P.variant, src_lane, src, u, rr);
+        finish<LS, LU, W>(div, &P.beta, s, m, x, dt, P.variant, src_lane, src, u, rr);
         store_field<LU, W>(P.p, g, s, m, x, u);
         if (!vfinite<LU, W>(u)) mask |= 1u << P.p.bit;
         if (comp) {

@@ -174,6 +174,31 @@ __global__ void k_epilogue(EpParams E, int64_t n, int sample, int64_t eidx) {
     }
 }
 
+// For every positive finite binary16 divisor b: does fl16(fl32(a * __frcp_rn(b)))
+// equal the correctly rounded fl16(a / b) for ALL 65536 binary16 a?  One CTA per b.
+__global__ void k_cheap_div_table(unsigned int* ok) {
+    const unsigned int b = blockIdx.x + 1;
+    if (b > 0x7bffu) return;
+    const __half hb = __ushort_as_half((unsigned short)b);
+    const float r = __frcp_rn(__half2float(hb));
+    bool good = true;
+    for (unsigned int a = threadIdx.x; a < 65536u; a += blockDim.x) {
+        const __half ha = __ushort_as_half((unsigned short)a);
+        const unsigned short x = __half_as_ushort(__float2half_rn(__fmul_rn(__half2float(ha), r)));
+        const unsigned short y = __half_as_ushort(lane<16>::div_ieee(ha, hb));
+        const bool xn = (x & 0x7c00u) == 0x7c00u && (x & 0x3ffu);
+        const bool yn = (y & 0x7c00u) == 0x7c00u && (y & 0x3ffu);
+        if (x != y && !(xn && yn)) good = false;
+    }
+    good = __syncthreads_and(good);
+    if (threadIdx.x == 0 && good) atomicOr(&ok[b >> 5], 1u << (b & 31));
+}
+
+__global__ void k_rcp_plane(const __half* in, float* out, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = __frcp_rn(__half2float(in[i]));
+}
+
 // Exhaustive check of the branch-free binary16 division against the IEEE one:
 // every binary16 a (incl. inf/NaN/zero/subnormal) x every finite nonzero b.
 __global__ void k_selftest_div16(unsigned long long* bad, unsigned int* first) {
@@ -196,6 +221,27 @@ __global__ void k_selftest_div16(unsigned long long* bad, unsigned int* first) {
     if (nbad) atomicAdd(bad, nbad);
 }
 
+}  // namespace
+
+namespace {
+std::vector<uint32_t> g_cheap_table[64];
+
+int cheap_div_table(int device, const std::vector<uint32_t>** out) {
+    if (device < 0 || device >= 64) return fail(HW_EINVAL, "device ordinal out of range");
+    if (g_cheap_table[device].empty()) {
+        unsigned int* ok = nullptr;
+        CU(cudaMalloc(&ok, 1024 * 4));
+        CU(cudaMemset(ok, 0, 1024 * 4));
+        k_cheap_div_table<<<0x7bff, 256>>>(ok);
+        CU(cudaGetLastError());
+        std::vector<uint32_t> t(1024);
+        CU(cudaMemcpy(t.data(), ok, 1024 * 4, cudaMemcpyDeviceToHost));
+        cudaFree(ok);
+        g_cheap_table[device] = t;
+    }
+    *out = &g_cheap_table[device];
+    return HW_OK;
+}
 }  // namespace
 
 namespace hw {
@@ -268,7 +314,7 @@ int64_t plane_rows(const hw_solver* h, int pl) {
 // Upload one fp64 plane, compressed to constant / slow-layered / full, plus its lane copy.
 int upload_plane(hw_solver* h, int pl) {
     int64_t rows = plane_rows(h, pl);
-    h->lp[pl] = PlaneView{nullptr, 0, 0, 0, 0, 0};
+    h->lp[pl] = PlaneView{nullptr, nullptr, 0, 0, 0, 0, 0};
     h->ep64[pl] = Plane64{nullptr, 0, 0, 0};
     if (!rows) return HW_OK;
     const double* src = h->d.plane[pl];
@@ -309,12 +355,37 @@ int upload_plane(hw_solver* h, int pl) {
         else if (L == 32) k_round_plane<float><<<nb, 256>>>(d64, (float*)dl, cnt, L);
         else k_round_plane<double><<<nb, 256>>>(d64, (double*)dl, cnt, L);
         CU(cudaGetLastError());
-        bool fast = true;  // every lane value finite and nonzero (binary16 subnormals allowed)
-        for (double v : packed) {
-            double r = round_lane(L, v);
-            if (!(r != 0.0 && std::isfinite(r))) fast = false;
+        int mode = DIV_NONE;
+        const float* rcp = nullptr;
+        const bool divisor = pl == HW_PL_RHO_X || pl == HW_PL_RHO_S || pl == HW_PL_RHO_M || pl == HW_PL_BETA;
+        if (divisor) {
+            mode = DIV_IEEE;
+            if (L == 16) {
+                const std::vector<uint32_t>* tab = nullptr;
+                int trc = cheap_div_table(h->d.device, &tab);
+                if (trc) return trc;
+                bool fast = true, cheap = true;  // every lane value finite and nonzero / table-verified
+                for (double v : packed) {
+                    double r = round_lane(16, v);
+                    if (!(r != 0.0 && std::isfinite(r))) fast = false;
+                    uint16_t hb = half_bits(r);
+                    if (hb == 0 || hb > 0x7bff || !(((*tab)[hb >> 5] >> (hb & 31)) & 1u)) cheap = false;
+                }
+                const char* env = getenv("HALFWAVE_DIV");
+                if (env && strcmp(env, "ieee") == 0) fast = cheap = false;
+                if (env && strcmp(env, "fast") == 0) cheap = false;
+                mode = cheap ? DIV_CHEAP : (fast ? DIV_FAST : DIV_IEEE);
+                if (cheap) {
+                    float* dr = nullptr;
+                    CU(cudaMalloc(&dr, cnt * sizeof(float) + 16));
+                    h->plane_mem.push_back(dr);
+                    k_rcp_plane<<<(cnt + 255) / 256, 256>>>((const __half*)dl, dr, cnt);
+                    CU(cudaGetLastError());
+                    rcp = dr;
+                }
+            }
         }
-        h->lp[pl] = PlaneView{dl, ss, sm, sx, fast ? 1 : 0, 0};
+        h->lp[pl] = PlaneView{dl, rcp, ss, sm, sx, mode, 0};
     }
     return HW_OK;
 }
@@ -782,6 +853,20 @@ int hw_selftest_div16(int32_t device, uint64_t* mismatches, uint32_t* first_pair
     if (mismatches) *mismatches = nb;
     if (first_pair) *first_pair = fp;
     return HW_OK;
+}
+
+int hw_cheap_div_table(int32_t device, uint32_t* bits1024) {
+    CU(cudaSetDevice(device));
+    const std::vector<uint32_t>* tab = nullptr;
+    int rc = cheap_div_table(device, &tab);
+    if (rc) return rc;
+    memcpy(bits1024, tab->data(), 1024 * 4);
+    return HW_OK;
+}
+
+int hw_plane_div_mode(const hw_solver* h, int32_t plane) {
+    if (!h || plane < 0 || plane >= HW_NPLANES) return -1;
+    return h->lp[plane].div_mode;
 }
 
 const char* hw_version(void) { return "halfwave_b200 abi=1 arch=sm_100a"; }

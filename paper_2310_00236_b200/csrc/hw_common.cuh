@@ -37,10 +37,19 @@ struct Geom {
     int64_t slab;     // elements per slow index = nm * pitch
 };
 
+// Division mode of a divisor plane (chosen on the host per plane, see hw_api.cu):
+enum DivMode {
+    DIV_NONE = 0,
+    DIV_FAST = 1,   // branch-free exact binary16 division (finite nonzero divisors)
+    DIV_IEEE = 2,   // __fdiv_rn / __ddiv_rn path
+    DIV_CHEAP = 3,  // binary16: fl16(a * rcp), every plane value verified exhaustively
+};
+
 struct PlaneView {    // lane-rounded medium plane (storage type of its lane)
     const void* p;
+    const float* rcp; // __frcp_rn of each binary16 value (same strides), DIV_CHEAP planes
     int64_t ss, sm, sx;
-    int32_t fast_div;  // every value finite and nonzero: the branch-free exact division applies
+    int32_t div_mode;
     int32_t pad;
 };
 
@@ -73,6 +82,18 @@ struct Ctrl {         // device-side run control
 template <typename T>
 __device__ __forceinline__ T* frow(const FieldView& f, const Geom& g, int64_t s, int64_t m) {
     return reinterpret_cast<T*>(f.base) + s * g.slab + m * g.pitch;
+}
+
+template <int W>
+__device__ __forceinline__ void prcp(const PlaneView& pv, int64_t s, int64_t m, int64_t x, float r[W]) {
+    const float* p = pv.rcp + s * pv.ss + m * pv.sm;
+    if (pv.sx == 0) {
+#pragma unroll
+        for (int i = 0; i < W; i++) r[i] = p[0];
+    } else {
+#pragma unroll
+        for (int i = 0; i < W; i++) r[i] = p[x + i];
+    }
 }
 
 template <int L, int W>
@@ -158,37 +179,50 @@ __device__ __forceinline__ void mtaps(const FieldView& f, const Geom& g, int64_t
 // efsum.py:100-121) for W cells.  src_lane >= 0 marks the element holding the
 // point source, injected as round_U(src) before the division when src != 0.
 template <int LS, int LU, int W>
-__device__ __forceinline__ void finish(vec<LS, W> rhs, int has_div, vec<LU, W> divisor,
+__device__ __forceinline__ void finish(vec<LS, W> rhs, const PlaneView* div, int64_t s, int64_t m, int64_t x,
                                        typename lane<LU>::T dt, int variant, int src_lane, double src,
                                        vec<LU, W>& u, vec<LU, W>& t) {
     using O = vops<LU, W>;
     using ln = lane<LU>;
-    vec<LU, W> x = vcvt<LU, LS, W>(rhs);
+    vec<LU, W> xv = vcvt<LU, LS, W>(rhs);
     if (src_lane >= 0 && src != 0.0) {
 #pragma unroll
         for (int i = 0; i < W; i++)
-            if (i == src_lane) x.e[i] = ln::add(x.e[i], ln::from_f64(src));
+            if (i == src_lane) xv.e[i] = ln::add(xv.e[i], ln::from_f64(src));
     }
-    if (has_div == 1) x = O::div(x, divisor);        // fast exact path (finite nonzero divisors)
-    else if (has_div == 2) x = O::div_ieee(x, divisor);
-    x = O::mul(x, vsplat<LU, W>(dt));
+    if (div) {
+        if constexpr (LU == 16) {
+            if (div->div_mode == DIV_CHEAP) {
+                float r[W];
+                prcp<W>(*div, s, m, x, r);
+                xv = vdiv_cheap<W>(xv, r);
+            } else if (div->div_mode == DIV_FAST) {
+                xv = O::div(xv, pload<LU, W>(*div, s, m, x));
+            } else {
+                xv = O::div_ieee(xv, pload<LU, W>(*div, s, m, x));
+            }
+        } else {
+            xv = O::div_ieee(xv, pload<LU, W>(*div, s, m, x));
+        }
+    }
+    xv = O::mul(xv, vsplat<LU, W>(dt));
     if (variant == 0) {
-        u = O::add(u, x);
+        u = O::add(u, xv);
         return;
     }
-    vec<LU, W> r = O::add(t, x);
-    vec<LU, W> s = O::add(u, r);
+    vec<LU, W> r = O::add(t, xv);
+    vec<LU, W> sm_ = O::add(u, r);
     if (variant == 3) {
-        vec<LU, W> z = O::sub(s, u);
+        vec<LU, W> z = O::sub(sm_, u);
         t = O::sub(r, z);
     } else {
-        vec<LU, W> pa = O::sub(s, r);
-        vec<LU, W> pb = O::sub(s, pa);
+        vec<LU, W> pa = O::sub(sm_, r);
+        vec<LU, W> pb = O::sub(sm_, pa);
         vec<LU, W> da = O::sub(u, pa);
         vec<LU, W> db = O::sub(r, pb);
         t = O::add(da, db);
     }
-    u = s;
+    u = sm_;
 }
 
 // Store W cells of field f at (s, m, x) and keep its ghost slabs current.

@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(BLOCK) k_el_vel(ElParams P, int64_t n, double 
             }
             vec<LU, W> u = ld<LU, W>(P.vx, g, s, m, x);
             vec<LU, W> rr = comp ? ld<LU, W>(P.rvx, g, s, m, x) : vec<LU, W>{};
-            finish<LS, LU, W>(a, P.rho_x.fast_div ? 1 : 2, pload<LU, W>(P.rho_x, s, m, x), dt, P.variant, -1, 0.0, u, rr);
+            finish<LS, LU, W>(a, &P.rho_x, s, m, x, dt, P.variant, -1, 0.0, u, rr);
             upd_store<LU, W>(P.vx, P.rvx, g, s, m, x, u, rr, comp, mask);
         }
         if (s < P.vs.rows) {  // vy: fl(fl(ddx sxy + dds syy) + ddm sms) (+ src) / rho_y (elastic.py:196-205)
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(BLOCK) k_el_vel(ElParams P, int64_t n, double 
                 src_lane = (int)(P.src_x - x);
             vec<LU, W> u = ld<LU, W>(P.vs, g, s, m, x);
             vec<LU, W> rr = comp ? ld<LU, W>(P.rvs, g, s, m, x) : vec<LU, W>{};
-            finish<LS, LU, W>(a, P.rho_s.fast_div ? 1 : 2, pload<LU, W>(P.rho_s, s, m, x), dt, P.variant, src_lane, src, u, rr);
+            finish<LS, LU, W>(a, &P.rho_s, s, m, x, dt, P.variant, src_lane, src, u, rr);
             upd_store<LU, W>(P.vs, P.rvs, g, s, m, x, u, rr, comp, mask);
             if (P.d3) {  // v_mid: fl(fl(ddx sxm + dds sms) + ddm smm) / rho_m
                 xtaps<LU, W>(frow<TU>(P.sxm, g, s, m), x, g.nx, true, t);
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(BLOCK) k_el_vel(ElParams P, int64_t n, double 
                 b = OS::add(b, fold<LS, LU, W>(c, t, P.order));
                 vec<LU, W> um = ld<LU, W>(P.vm, g, s, m, x);
                 vec<LU, W> rm = comp ? ld<LU, W>(P.rvm, g, s, m, x) : vec<LU, W>{};
-                finish<LS, LU, W>(b, P.rho_m.fast_div ? 1 : 2, pload<LU, W>(P.rho_m, s, m, x), dt, P.variant, -1, 0.0, um, rm);
+                finish<LS, LU, W>(b, &P.rho_m, s, m, x, dt, P.variant, -1, 0.0, um, rm);
                 upd_store<LU, W>(P.vm, P.rvm, g, s, m, x, um, rm, comp, mask);
             }
         }
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(BLOCK) k_el_stress(ElParams P, int64_t n, doub
             const vec<LU, W> sxx_old = ld<LU, W>(P.sxx, g, s, m, x);
             vec<LU, W> u = sxx_old;
             vec<LU, W> rr = comp ? ld<LU, W>(P.rsxx, g, s, m, x) : vec<LU, W>{};
-            finish<LS, LU, W>(a, 0, vec<LU, W>{}, dt, P.variant, src_lane, src, u, rr);
+            finish<LS, LU, W>(a, nullptr, s, m, x, dt, P.variant, src_lane, src, u, rr);
             upd_store<LU, W>(P.sxx, P.rsxx, g, s, m, x, u, rr, comp, mask);
             const vec<LU, W> sxx_new = u;
             // s_slow: fl(fl(lam dvx) + fl(stiff dvs)) [+ fl(lam dvm)]; surface rows: zero increment (elastic.py:223-230)
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(BLOCK) k_el_stress(ElParams P, int64_t n, doub
             const vec<LU, W> sss_old = ld<LU, W>(P.sss, g, s, m, x);
             u = sss_old;
             rr = comp ? ld<LU, W>(P.rsss, g, s, m, x) : vec<LU, W>{};
-            finish<LS, LU, W>(a, 0, vec<LU, W>{}, dt, P.variant, src_lane, src, u, rr);
+            finish<LS, LU, W>(a, nullptr, s, m, x, dt, P.variant, src_lane, src, u, rr);
             upd_store<LU, W>(P.sss, P.rsss, g, s, m, x, u, rr, comp, mask);
             const vec<LU, W> sss_new = u;
             vec<LU, W> smm_old{}, smm_new{};
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(BLOCK) k_el_stress(ElParams P, int64_t n, doub
                 smm_old = ld<LU, W>(P.smm, g, s, m, x);
                 u = smm_old;
                 rr = comp ? ld<LU, W>(P.rsmm, g, s, m, x) : vec<LU, W>{};
-                finish<LS, LU, W>(a, 0, vec<LU, W>{}, dt, P.variant, src_lane, src, u, rr);
+                finish<LS, LU, W>(a, nullptr, s, m, x, dt, P.variant, src_lane, src, u, rr);
                 upd_store<LU, W>(P.smm, P.rsmm, g, s, m, x, u, rr, comp, mask);
                 smm_new = u;
             }
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(BLOCK) k_el_stress(ElParams P, int64_t n, doub
             old[0] = ld<LU, W>(P.sxs, g, s, m, x);
             vec<LU, W> u = old[0];
             vec<LU, W> rr = comp ? ld<LU, W>(P.rsxs, g, s, m, x) : vec<LU, W>{};
-            finish<LS, LU, W>(a, 0, vec<LU, W>{}, dt, P.variant, -1, 0.0, u, rr);
+            finish<LS, LU, W>(a, nullptr, s, m, x, dt, P.variant, -1, 0.0, u, rr);
             upd_store<LU, W>(P.sxs, P.rsxs, g, s, m, x, u, rr, comp, mask);
             nw[0] = u;
             if (P.d3) {
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(BLOCK) k_el_stress(ElParams P, int64_t n, doub
                 old[1] = ld<LU, W>(P.sxm, g, s, m, x);
                 u = old[1];
                 rr = comp ? ld<LU, W>(P.rsxm, g, s, m, x) : vec<LU, W>{};
-                finish<LS, LU, W>(a, 0, vec<LU, W>{}, dt, P.variant, -1, 0.0, u, rr);
+                finish<LS, LU, W>(a, nullptr, s, m, x, dt, P.variant, -1, 0.0, u, rr);
                 upd_store<LU, W>(P.sxm, P.rsxm, g, s, m, x, u, rr, comp, mask);
                 nw[1] = u;
                 // s_ms: fl(mu fl(dds vm + ddm vs))
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(BLOCK) k_el_stress(ElParams P, int64_t n, doub
                 old[2] = ld<LU, W>(P.sms, g, s, m, x);
                 u = old[2];
                 rr = comp ? ld<LU, W>(P.rsms, g, s, m, x) : vec<LU, W>{};
-                finish<LS, LU, W>(a, 0, vec<LU, W>{}, dt, P.variant, -1, 0.0, u, rr);
+                finish<LS, LU, W>(a, nullptr, s, m, x, dt, P.variant, -1, 0.0, u, rr);
                 upd_store<LU, W>(P.sms, P.rsms, g, s, m, x, u, rr, comp, mask);
                 nw[2] = u;
             }

@@ -161,8 +161,6 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
     for (int j = 0; j < 4; j++) c[j] = lconst<16>(P.k, j);
     const __half dt = lconst<16>(P.k, 4);
-    const int dmode_x = P.rho_x.fast_div ? 1 : 2, dmode_s = P.rho_s.fast_div ? 1 : 2,
-              dmode_b = P.beta.fast_div ? 1 : 2;
     const int64_t xl = x == 0 ? nx - 2 : x - 2;          // left neighbour pair
     const int64_t xr = x + FCPT >= nx ? 0 : x + FCPT;     // right neighbour pair
 
@@ -191,7 +189,7 @@ __global__ void __launch_bounds__(512, 1)
             V8 r = comp ? lds8(slot_row(slot, S_RVX) + x) : V8{};
 #pragma unroll
             for (int j = 0; j < 4; j++)
-                finish<16, 16, 2>(d.q[j], dmode_x, plane2(P.rho_x, f, x + 2 * j), dt, V, -1, 0.0, vxn.q[j], r.q[j]);
+                finish<16, 16, 2>(d.q[j], &P.rho_x, f, 0, x + 2 * j, dt, V, -1, 0.0, vxn.q[j], r.q[j]);
             st8(P.out[S_VX] + f * pitch + x, vxn);
             mask |= nonfinite8(vxn) << 1;
             if (comp) {
@@ -215,7 +213,7 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
             for (int j = 0; j < 4; j++) {
                 H2 d = fold2<ORDER>(c, pq3.q[j], pq2.q[j], pq1.q[j], pq0.q[j]);
-                finish<16, 16, 2>(d, dmode_s, plane2(P.rho_s, rw, x + 2 * j), dt, V, -1, 0.0, vsn.q[j], rr.q[j]);
+                finish<16, 16, 2>(d, &P.rho_s, rw, 0, x + 2 * j, dt, V, -1, 0.0, vsn.q[j], rr.q[j]);
             }
             if (r >= y0 && r < y1) {
                 st8(P.out[S_VS] + r * pitch + x, vsn);
@@ -251,8 +249,8 @@ __global__ void __launch_bounds__(512, 1)
             for (int j = 0; j < 4; j++) {
                 H2 gs = fold2<ORDER>(c, vq3.q[j], vq2.q[j], vq1.q[j], vq0.q[j]);
                 H2 dv = O2::add(gq3.q[j], gs);
-                finish<16, 16, 2>(dv, dmode_b, plane2(P.beta, k, x + 2 * j), dt, V, j == src_j ? src_lane : -1, src,
-                                  pn.q[j], rp.q[j]);
+                finish<16, 16, 2>(dv, &P.beta, k, 0, x + 2 * j, dt, V, j == src_j ? src_lane : -1, src, pn.q[j],
+                                  rp.q[j]);
             }
             st8(P.out[S_P] + k * pitch + x, pn);
             mask |= nonfinite8(pn);

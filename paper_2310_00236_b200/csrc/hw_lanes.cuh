@@ -155,6 +155,22 @@ template <> struct vops<16, 2> {
     }
 };
 
+// Binary16 division by a divisor whose reciprocal rcp = __frcp_rn(b) makes
+// fl16(fl32(a * rcp)) == fl16(a / b) for EVERY binary16 a; which divisors qualify
+// is decided exhaustively on the device (k_cheap_div_table in hw_api.cu).
+template <int W>
+__device__ __forceinline__ vec<16, W> vdiv_cheap(vec<16, W> a, const float* rcp) {
+    vec<16, W> r;
+    if constexpr (W == 2) {
+        const float2 f = __half22float2(a.h2);
+        r.h2 = __floats2half2_rn(__fmul_rn(f.x, rcp[0]), __fmul_rn(f.y, rcp[1]));
+    } else {
+#pragma unroll
+        for (int i = 0; i < W; i++) r.e[i] = __float2half_rn(__fmul_rn(__half2float(a.e[i]), rcp[i]));
+    }
+    return r;
+}
+
 template <int L, int W>
 __device__ __forceinline__ vec<L, W> vsplat(typename lane<L>::T x) {
     if constexpr (L == 16 && W == 2) {

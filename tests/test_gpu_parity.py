@@ -22,8 +22,16 @@ def _run_names():
     return [n for n in names() if not Case(n).d["steps_api"]]
 
 
+@pytest.fixture(params=["auto", "fast", "ieee"])
+def div_mode(request, monkeypatch):
+    """Run under each binary16 division path: table-verified cheap (auto), branch-free exact, IEEE."""
+    if request.param != "auto":
+        monkeypatch.setenv("HALFWAVE_DIV", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("name", _run_names())
-def test_gpu_run_matches_reference_golden(name):
+def test_gpu_run_matches_reference_golden(name, div_mode):
     case = Case(name)
     solver = case.solver()
     st = case.initial_state(solver)
@@ -193,3 +201,42 @@ def test_gpu_fast_fp16_division_exhaustive():
     bad, first = ctypes.c_uint64(0), ctypes.c_uint32(0)
     _abi.check(_abi.load().hw_selftest_div16(0, ctypes.byref(bad), ctypes.byref(first)), "selftest")
     assert bad.value == 0, f"{bad.value} mismatches; first a,b = {first.value >> 16:#06x},{first.value & 0xffff:#06x}"
+
+
+def test_gpu_cheap_division_table_verified_on_cpu():
+    """Independently re-check, with numpy on the CPU, the device's exhaustive table of
+    divisors for which fl16(fl32(a * rcp(b))) is the correctly rounded quotient."""
+    import ctypes
+
+    from paper_2310_00236_b200 import _abi
+
+    words = (ctypes.c_uint32 * 1024)()
+    _abi.check(_abi.load().hw_cheap_div_table(0, words), "table")
+    bits = np.array(words, dtype=np.uint32)
+    member = lambda b: bool((bits[b >> 5] >> (b & 31)) & 1)
+    for b in (0x3c00, 0x3e00, 0x4080):  # 1.0, 1.5, 2.25 (the layered media): must qualify
+        assert member(b)
+    rng = np.random.default_rng(0)
+    a = np.arange(65536, dtype=np.uint16).view(np.float16)
+    finite = np.isfinite(a)
+    checked = {True: 0, False: 0}
+    for b in rng.integers(1, 0x7c00, 120):
+        hb = np.uint16(b).view(np.float16)
+        rcp = np.float32(1.0) / np.float32(hb)
+        with np.errstate(all="ignore"):
+            cheap = (a.astype(np.float32) * rcp).astype(np.float16)
+            exact = (a.astype(np.float64) / np.float64(hb)).astype(np.float16)
+        same = (cheap.view(np.uint16) == exact.view(np.uint16)) | (np.isnan(cheap) & np.isnan(exact))
+        assert bool(same.all()) == member(int(b)), f"table disagrees for b={int(b):#06x}"
+        checked[member(int(b))] += 1
+    assert checked[True] > 0
+
+
+def test_gpu_layered_media_use_cheap_division():
+    s, st = _acoustic(256, 64, 2, hw.Precision.FP16, layered=True)
+    s.run(hw.Variant.OP3, st)
+    from paper_2310_00236_b200 import _abi
+
+    lib = _abi.load()
+    for pl in (_abi.PL_RHO_X, _abi.PL_RHO_S, _abi.PL_BETA):
+        assert lib.hw_plane_div_mode(s._lib_handle(), pl) == 3
