@@ -31,7 +31,7 @@
 namespace hw {
 
 constexpr int FCPT = 8;  // cells per thread
-constexpr int FR = 3;    // TMA ring slots (prefetch distance FR-1)
+constexpr int FR = 4;    // TMA ring slots (prefetch distance FR-1); also the unroll factor
 constexpr int NSTREAM = FUSED_NSTREAM;
 enum { S_P = 0, S_VX = 1, S_VS = 2, S_RP = 3, S_RVX = 4, S_RVS = 5 };
 
@@ -98,20 +98,51 @@ __device__ __forceinline__ H2 plane2(const PlaneView& pv, int64_t s, int64_t x) 
     return pload<16, 2>(pv, s, 0, x);
 }
 
-__device__ __forceinline__ unsigned int nonfinite8(const V8& v) {
-    bool ok = true;
+// running max(|x|) with NaN propagation: the field went non-finite iff the
+// accumulator ends at inf/NaN (one VHMNMX.NAN per two half2 values)
+__device__ __forceinline__ void track(__half2& acc, const V8& v) {
 #pragma unroll
-    for (int j = 0; j < 4; j++) ok = ok && vfinite<16, 2>(v.q[j]);
-    return ok ? 0u : 1u;
+    for (int j = 0; j < 4; j++) acc = __hmax2_nan(acc, __habs2(v.q[j].h2));
 }
 
-template <int V, int ORDER>
+__device__ __forceinline__ unsigned int nonfinite_acc(__half2 acc) {
+    const unsigned int b = *reinterpret_cast<const unsigned int*>(&acc);
+    return (((b & 0x7c00u) == 0x7c00u) || ((b & 0x7c000000u) == 0x7c000000u)) ? 1u : 0u;
+}
+
+// increment (stepping.py:58-80) + advance (efsum.py:100-121) for one half2 pair,
+// division by a row-uniform divisor through its verified reciprocal (DIV_CHEAP)
+template <int V>
+__device__ __forceinline__ void finish_row(H2 rhs, float rcp, __half2 dt2, int src_lane, __half srch, H2& u, H2& t) {
+    if (src_lane == 0) rhs.e[0] = __hadd_rn(rhs.e[0], srch);
+    else if (src_lane == 1) rhs.e[1] = __hadd_rn(rhs.e[1], srch);
+    const float2 fx = __half22float2(rhs.h2);
+    H2 x;
+    x.h2 = __hmul2_rn(__floats2half2_rn(__fmul_rn(fx.x, rcp), __fmul_rn(fx.y, rcp)), dt2);
+    if (V == 0) {
+        u.h2 = __hadd2_rn(u.h2, x.h2);
+        return;
+    }
+    const __half2 r = __hadd2_rn(t.h2, x.h2);
+    const __half2 s = __hadd2_rn(u.h2, r);
+    if (V == 3) {
+        t.h2 = __hsub2_rn(r, __hsub2_rn(s, u.h2));
+    } else {
+        const __half2 pa = __hsub2_rn(s, r);
+        const __half2 pb = __hsub2_rn(s, pa);
+        t.h2 = __hadd2_rn(__hsub2_rn(u.h2, pa), __hsub2_rn(r, pb));
+    }
+    u.h2 = s;
+}
+
+template <int V, int ORDER, bool ROWMED>
 __global__ void __launch_bounds__(512, 1)
     k_ac2d_fused(AcFusedParams P, int64_t n, double src, int sample, int64_t eidx) {
     if (halted(P.ctrl, n)) return;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-    __half* ring = reinterpret_cast<__half*>(smem + 128);
+    int* rec_local = reinterpret_cast<int*>(smem + 64);  // up to 8 (row, x, j) triples
+    __half* ring = reinterpret_cast<__half*>(smem + 256);
     const int64_t nx = P.nx, ns = P.ns, pitch = P.pitch;
     __half* xrow = ring + (int64_t)FR * NSTREAM * nx;
     const int nb = gridDim.x, b = blockIdx.x;
@@ -119,18 +150,17 @@ __global__ void __launch_bounds__(512, 1)
     const int64_t F0 = y0 - 3;
     const int64_t NI = (y1 + 3) - F0;
     const int tid = threadIdx.x;
-    const int64_t x = (int64_t)tid * FCPT;
+    const int x = tid * FCPT;
     constexpr bool comp = V != 0;
     const uint32_t rb = (uint32_t)(nx * sizeof(__half));
 
-    auto slot_row = [&](int slot, int st) { return ring + ((int64_t)slot * NSTREAM + st) * nx; };
+    auto slot_row = [&](int slot, int st) { return ring + (slot * NSTREAM + st) * nx; };
     auto wrap_row = [&](int64_t r) {
         r %= ns;
         return r < 0 ? r + ns : r;
     };
-    auto issue = [&](int64_t i) {  // TMA loads of iteration i (front row F0 + i)
+    auto issue = [&](int64_t i, int slot) {  // TMA loads of iteration i (front row F0 + i)
         const int64_t f = F0 + i;
-        const int slot = (int)(i % FR);
         const bool lvx = f >= y0 && f < y1;
         const bool lvs = f >= y0 && f < y1 + 3;
         const bool lrp = comp && f >= y0 + 3 && f < y1 + 3;
@@ -152,130 +182,177 @@ __global__ void __launch_bounds__(512, 1)
     if (tid == 0) {
         for (int s = 0; s < FR; s++) mbar_init(&bar[s], 1);
         fence_mbar_init();
+        int cnt = 0;  // receivers on this CTA's rows
+        for (int q = 0; q < P.n_rec && cnt < 8; q++) {
+            const int64_t* rc = P.rec + 3 * q;
+            if (rc[2] >= y0 && rc[2] < y1) {
+                rec_local[1 + 3 * cnt] = (int)rc[2];
+                rec_local[2 + 3 * cnt] = (int)rc[0];
+                rec_local[3 + 3 * cnt] = q;
+                cnt++;
+            }
+        }
+        rec_local[0] = cnt;
     }
     __syncthreads();
     if (tid == 0)
-        for (int64_t i = 0; i < FR - 1 && i < NI; i++) issue(i);
+        for (int64_t i = 0; i < FR - 1 && i < NI; i++) issue(i, (int)i);
+    const int n_local = rec_local[0];
 
     __half c[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) c[j] = lconst<16>(P.k, j);
-    const __half dt = lconst<16>(P.k, 4);
-    const int64_t xl = x == 0 ? nx - 2 : x - 2;          // left neighbour pair
-    const int64_t xr = x + FCPT >= nx ? 0 : x + FCPT;     // right neighbour pair
+    const __half2 dt2 = __half2half2(lconst<16>(P.k, 4));
+    const __half srch = __double2half(src);
+    const int xl = x == 0 ? (int)nx - 2 : x - 2;                // left neighbour pair
+    const int xr = x + FCPT >= (int)nx ? 0 : x + FCPT;          // right neighbour pair
+    const bool src_here = P.has_src && src != 0.0 && P.src_x >= x && P.src_x < x + FCPT;
+    const int src_j = (int)((P.src_x - x) >> 1), src_lane = (int)((P.src_x - x) & 1);
 
-    V8 pq0, pq1, pq2, pq3;  // p rows f, f-1, f-2, f-3 (own cells)
-    V8 vq0, vq1, vq2, vq3;  // vy_new rows f-2, f-3, f-4, f-5
-    V8 gq0, gq1, gq2, gq3;  // d/dx vx_new rows f, f-1, f-2, f-3
-    unsigned int mask = 0;
+    V8 pq[4], vq[4], gq[4];  // p rows, vy_new rows, d/dx vx_new rows (indexed by iteration mod 4)
+    __half2 acc[NSTREAM];
+#pragma unroll
+    for (int q = 0; q < NSTREAM; q++) acc[q] = __float2half2_rn(0.f);
     double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
 
-    for (int64_t i = 0; i < NI; i++) {
-        const int64_t f = F0 + i;
-        const int slot = (int)(i % FR);
-        if (tid == 0 && i + FR - 1 < NI) {
-            fence_proxy_async_smem();
-            issue(i + FR - 1);
-        }
-        mbar_wait(&bar[slot], (uint32_t)((i / FR) & 1));
-        const __half* prow = slot_row(slot, S_P);
-        pq3 = pq2; pq2 = pq1; pq1 = pq0;
-        pq0 = lds8(prow + x);
-        V8 vxn;
-        const bool do_vx = f >= y0 && f < y1;
-        if (do_vx) {  // vx[f] = advance(fl(fl(ddx p / rho_x) dt)) (acoustic.py:167-168)
-            V8 d = xfold8<ORDER>(c, ld2(prow + xl), pq0, ld2(prow + xr), false);
-            vxn = lds8(slot_row(slot, S_VX) + x);
-            V8 r = comp ? lds8(slot_row(slot, S_RVX) + x) : V8{};
+    for (int64_t i0 = 0; i0 < NI; i0 += FR) {
+        const uint32_t par = (uint32_t)((i0 / FR) & 1);
 #pragma unroll
-            for (int j = 0; j < 4; j++)
-                finish<16, 16, 2>(d.q[j], &P.rho_x, f, 0, x + 2 * j, dt, V, -1, 0.0, vxn.q[j], r.q[j]);
-            st8(P.out[S_VX] + f * pitch + x, vxn);
-            mask |= nonfinite8(vxn) << 1;
-            if (comp) {
-                st8(P.out[S_RVX] + f * pitch + x, r);
-                mask |= nonfinite8(r) << 4;
-            }
-            st8(xrow + x, vxn);
-            if (sample) {
-#pragma unroll
-                for (int j = 0; j < FCPT; j++) {
-                    const double v = (double)__half2float(vxn.q[j >> 1].e[j & 1]);
-                    e[1] += p64(P.e_rho_x, f, 0, x + j) * (v * v);
+        for (int u = 0; u < FR; u++) {
+            const int64_t i = i0 + u;
+            if (i < NI) {
+                const int64_t f = F0 + i;
+                if (tid == 0 && i + FR - 1 < NI) {
+                    fence_proxy_async_smem();
+                    issue(i + FR - 1, (u + FR - 1) % FR);
                 }
-            }
-        }
-        if (f >= y0 && f < y1 + 3) {  // vy[r = f-2] from p rows f-3..f (acoustic.py:169-170)
-            const int64_t r = f - 2;
-            V8 vsn = lds8(slot_row(slot, S_VS) + x);
-            V8 rr = comp ? lds8(slot_row(slot, S_RVS) + x) : V8{};
-            const int64_t rw = wrap_row(r);
+                mbar_wait(&bar[u], par);
+                const __half* prow = slot_row(u, S_P);
+                pq[u] = lds8(prow + x);
+                const bool do_vx = f >= y0 && f < y1;
+                if (do_vx) {  // vx[f] (acoustic.py:167-168)
+                    V8 d = xfold8<ORDER>(c, ld2(prow + xl), pq[u], ld2(prow + xr), false);
+                    V8 vxn = lds8(slot_row(u, S_VX) + x);
+                    V8 r = comp ? lds8(slot_row(u, S_RVX) + x) : V8{};
+                    if constexpr (ROWMED) {
+                        const float rc = __ldg(P.rho_x.rcp + f * P.rho_x.ss);
 #pragma unroll
-            for (int j = 0; j < 4; j++) {
-                H2 d = fold2<ORDER>(c, pq3.q[j], pq2.q[j], pq1.q[j], pq0.q[j]);
-                finish<16, 16, 2>(d, &P.rho_s, rw, 0, x + 2 * j, dt, V, -1, 0.0, vsn.q[j], rr.q[j]);
-            }
-            if (r >= y0 && r < y1) {
-                st8(P.out[S_VS] + r * pitch + x, vsn);
-                mask |= nonfinite8(vsn) << 2;
-                if (comp) {
-                    st8(P.out[S_RVS] + r * pitch + x, rr);
-                    mask |= nonfinite8(rr) << 5;
-                }
-                if (sample) {
+                        for (int j = 0; j < 4; j++) finish_row<V>(d.q[j], rc, dt2, -1, srch, vxn.q[j], r.q[j]);
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < FCPT; j++) {
-                        const double v = (double)__half2float(vsn.q[j >> 1].e[j & 1]);
-                        e[2] += p64(P.e_rho_s, r, 0, x + j) * (v * v);
+                        for (int j = 0; j < 4; j++)
+                            finish<16, 16, 2>(d.q[j], &P.rho_x, f, 0, x + 2 * j, dt2.x, V, -1, 0.0, vxn.q[j], r.q[j]);
+                    }
+                    st8(P.out[S_VX] + f * pitch + x, vxn);
+                    track(acc[S_VX], vxn);
+                    if (comp) {
+                        st8(P.out[S_RVX] + f * pitch + x, r);
+                        track(acc[S_RVX], r);
+                    }
+                    st8(xrow + x, vxn);
+                    if (sample) {
+#pragma unroll
+                        for (int j = 0; j < FCPT; j++) {
+                            const double v = (double)__half2float(vxn.q[j >> 1].e[j & 1]);
+                            e[1] += p64(P.e_rho_x, f, 0, x + j) * (v * v);
+                        }
                     }
                 }
-            }
-            vq3 = vq2; vq2 = vq1; vq1 = vq0; vq0 = vsn;
-        }
-        __syncthreads();  // xrow holds vx_new[f]
-        gq3 = gq2; gq2 = gq1; gq1 = gq0;
-        if (do_vx) gq0 = xfold8<ORDER>(c, ld2(xrow + xl), vxn, ld2(xrow + xr), true);
-        const int64_t k = f - 3;
-        if (k >= y0 && k < y1) {  // p[k]: div = fl(ddx vx + ddy vy) (+src) / beta * dt (acoustic.py:172-181)
-            const V8 pold = pq3;
-            V8 pn = pold;
-            V8 rp = comp ? lds8(slot_row(slot, S_RP) + x) : V8{};
-            int src_j = -1, src_lane = -1;
-            if (P.has_src && k == P.src_s && P.src_x >= x && P.src_x < x + FCPT) {
-                src_j = (int)((P.src_x - x) >> 1);
-                src_lane = (int)((P.src_x - x) & 1);
-            }
+                if (f >= y0 && f < y1 + 3) {  // vy[f-2] from p rows f-3..f (acoustic.py:169-170)
+                    const int64_t r = f - 2;
+                    const int64_t rw = wrap_row(r);
+                    V8 vsn = lds8(slot_row(u, S_VS) + x);
+                    V8 rr = comp ? lds8(slot_row(u, S_RVS) + x) : V8{};
+                    const V8& t0 = pq[(u + 1) % FR];
+                    const V8& t1 = pq[(u + 2) % FR];
+                    const V8& t2 = pq[(u + 3) % FR];
+                    if constexpr (ROWMED) {
+                        const float rc = __ldg(P.rho_s.rcp + rw * P.rho_s.ss);
 #pragma unroll
-            for (int j = 0; j < 4; j++) {
-                H2 gs = fold2<ORDER>(c, vq3.q[j], vq2.q[j], vq1.q[j], vq0.q[j]);
-                H2 dv = O2::add(gq3.q[j], gs);
-                finish<16, 16, 2>(dv, &P.beta, k, 0, x + 2 * j, dt, V, j == src_j ? src_lane : -1, src, pn.q[j],
-                                  rp.q[j]);
-            }
-            st8(P.out[S_P] + k * pitch + x, pn);
-            mask |= nonfinite8(pn);
-            if (comp) {
-                st8(P.out[S_RP] + k * pitch + x, rp);
-                mask |= nonfinite8(rp) << 3;
-            }
-            if (sample) {
+                        for (int j = 0; j < 4; j++)
+                            finish_row<V>(fold2<ORDER>(c, t0.q[j], t1.q[j], t2.q[j], pq[u].q[j]), rc, dt2, -1, srch,
+                                          vsn.q[j], rr.q[j]);
+                    } else {
 #pragma unroll
-                for (int j = 0; j < FCPT; j++) {
-                    const double a = (double)__half2float(pold.q[j >> 1].e[j & 1]);
-                    const double bb = (double)__half2float(pn.q[j >> 1].e[j & 1]);
-                    e[0] += p64(P.e_beta, k, 0, x + j) * (a * bb);
+                        for (int j = 0; j < 4; j++)
+                            finish<16, 16, 2>(fold2<ORDER>(c, t0.q[j], t1.q[j], t2.q[j], pq[u].q[j]), &P.rho_s, rw, 0,
+                                              x + 2 * j, dt2.x, V, -1, 0.0, vsn.q[j], rr.q[j]);
+                    }
+                    if (r >= y0 && r < y1) {
+                        st8(P.out[S_VS] + r * pitch + x, vsn);
+                        track(acc[S_VS], vsn);
+                        if (comp) {
+                            st8(P.out[S_RVS] + r * pitch + x, rr);
+                            track(acc[S_RVS], rr);
+                        }
+                        if (sample) {
+#pragma unroll
+                            for (int j = 0; j < FCPT; j++) {
+                                const double v = (double)__half2float(vsn.q[j >> 1].e[j & 1]);
+                                e[2] += p64(P.e_rho_s, r, 0, x + j) * (v * v);
+                            }
+                        }
+                    }
+                    vq[u] = vsn;
                 }
-            }
-            for (int q = 0; q < P.n_rec; q++) {  // receiver traces (acoustic.py:217-218)
-                const int64_t* rc = P.rec + 3 * q;
-                if (rc[2] == k && rc[0] >= x && rc[0] < x + FCPT) {
-                    const int o = (int)(rc[0] - x);
-                    P.traces[q * P.nt + n] = (double)__half2float(pn.q[o >> 1].e[o & 1]);
+                __syncthreads();  // xrow holds vx_new[f]
+                if (do_vx) gq[u] = xfold8<ORDER>(c, ld2(xrow + xl), lds8(xrow + x), ld2(xrow + xr), true);
+                const int64_t k = f - 3;
+                if (k >= y0 && k < y1) {  // p[k] (acoustic.py:172-181)
+                    const V8& pold = pq[(u + 1) % FR];
+                    V8 pn = pold;
+                    V8 rp = comp ? lds8(slot_row(u, S_RP) + x) : V8{};
+                    const V8& g = gq[(u + 1) % FR];
+                    const V8& a0 = vq[(u + 1) % FR];
+                    const V8& a1 = vq[(u + 2) % FR];
+                    const V8& a2 = vq[(u + 3) % FR];
+                    const bool sk = src_here && k == P.src_s;
+                    if constexpr (ROWMED) {
+                        const float rc = __ldg(P.beta.rcp + k * P.beta.ss);
+#pragma unroll
+                        for (int j = 0; j < 4; j++) {
+                            H2 dv = O2::add(g.q[j], fold2<ORDER>(c, a0.q[j], a1.q[j], a2.q[j], vq[u].q[j]));
+                            finish_row<V>(dv, rc, dt2, (sk && j == src_j) ? src_lane : -1, srch, pn.q[j], rp.q[j]);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 4; j++) {
+                            H2 dv = O2::add(g.q[j], fold2<ORDER>(c, a0.q[j], a1.q[j], a2.q[j], vq[u].q[j]));
+                            finish<16, 16, 2>(dv, &P.beta, k, 0, x + 2 * j, dt2.x, V, (sk && j == src_j) ? src_lane : -1,
+                                              src, pn.q[j], rp.q[j]);
+                        }
+                    }
+                    st8(P.out[S_P] + k * pitch + x, pn);
+                    track(acc[S_P], pn);
+                    if (comp) {
+                        st8(P.out[S_RP] + k * pitch + x, rp);
+                        track(acc[S_RP], rp);
+                    }
+                    if (sample) {
+#pragma unroll
+                        for (int j = 0; j < FCPT; j++) {
+                            const double a = (double)__half2float(pold.q[j >> 1].e[j & 1]);
+                            const double bb = (double)__half2float(pn.q[j >> 1].e[j & 1]);
+                            e[0] += p64(P.e_beta, k, 0, x + j) * (a * bb);
+                        }
+                    }
+                    for (int q = 0; q < n_local; q++) {  // receiver traces (acoustic.py:217-218)
+                        const int rx = rec_local[2 + 3 * q];
+                        if (rec_local[1 + 3 * q] == k && rx >= x && rx < x + FCPT) {
+                            const int o = rx - x;
+                            P.traces[(int64_t)rec_local[3 + 3 * q] * P.nt + n] =
+                                (double)__half2float(pn.q[o >> 1].e[o & 1]);
+                        }
+                    }
                 }
+                __syncthreads();  // ring slot and xrow free for reuse
             }
         }
-        __syncthreads();  // ring slot and xrow free for reuse
     }
+    unsigned int mask = 0;
+    // bit order = external field order p vx vy rp rvx rvy == stream order
+#pragma unroll
+    for (int q = 0; q < NSTREAM; q++) mask |= nonfinite_acc(acc[q]) << q;
     record_failure(P.ctrl, n, mask);
     if (!sample) return;
     block_partials(e, P.partials);
@@ -300,7 +377,7 @@ __global__ void __launch_bounds__(512, 1)
     }
 }
 
-size_t fused2d_smem_bytes(int64_t nx) { return 128 + ((size_t)FR * NSTREAM + 1) * nx * sizeof(__half); }
+size_t fused2d_smem_bytes(int64_t nx) { return 256 + ((size_t)FR * NSTREAM + 1) * nx * sizeof(__half); }
 
 int fused2d_threads(int64_t nx) { return (int)(nx / FCPT); }
 
@@ -309,41 +386,41 @@ bool fused2d_eligible(int64_t nx, int max_smem) {
     return fused2d_smem_bytes(nx) <= (size_t)max_smem;
 }
 
-#define FUSED_INST(V, ORD) (void*)k_ac2d_fused<V, ORD>
+template <bool RM>
 static void* fused_fn(int variant, int order) {
     if (order == 2) {
-        if (variant == 0) return FUSED_INST(0, 2);
-        if (variant == 3) return FUSED_INST(3, 2);
-        return FUSED_INST(6, 2);
+        if (variant == 0) return (void*)k_ac2d_fused<0, 2, RM>;
+        if (variant == 3) return (void*)k_ac2d_fused<3, 2, RM>;
+        return (void*)k_ac2d_fused<6, 2, RM>;
     }
-    if (variant == 0) return FUSED_INST(0, 4);
-    if (variant == 3) return FUSED_INST(3, 4);
-    return FUSED_INST(6, 4);
+    if (variant == 0) return (void*)k_ac2d_fused<0, 4, RM>;
+    if (variant == 3) return (void*)k_ac2d_fused<3, 4, RM>;
+    return (void*)k_ac2d_fused<6, 4, RM>;
 }
 
 cudaError_t fused2d_prepare(int64_t nx) {
     const int bytes = (int)fused2d_smem_bytes(nx);
     for (int v : {0, 3, 6})
-        for (int o : {2, 4}) {
-            cudaError_t e = cudaFuncSetAttribute(fused_fn(v, o), cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-            if (e != cudaSuccess) return e;
-        }
+        for (int o : {2, 4})
+            for (void* fn : {fused_fn<false>(v, o), fused_fn<true>(v, o)}) {
+                cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+                if (e != cudaSuccess) return e;
+            }
     return cudaSuccess;
+}
+
+bool fused2d_rowmed(const AcFusedParams& P) {
+    auto ok = [](const PlaneView& v) { return v.div_mode == DIV_CHEAP && v.sx == 0 && v.sm == 0; };
+    return ok(P.rho_x) && ok(P.rho_s) && ok(P.beta);
 }
 
 void launch_ac2d_fused(int variant, int order, const AcFusedParams& P, int nblocks, int64_t n, double src, int sample,
                        int64_t eidx, cudaStream_t st) {
     const int threads = fused2d_threads(P.nx);
     const size_t bytes = fused2d_smem_bytes(P.nx);
-    if (order == 2) {
-        if (variant == 0) k_ac2d_fused<0, 2><<<nblocks, threads, bytes, st>>>(P, n, src, sample, eidx);
-        else if (variant == 3) k_ac2d_fused<3, 2><<<nblocks, threads, bytes, st>>>(P, n, src, sample, eidx);
-        else k_ac2d_fused<6, 2><<<nblocks, threads, bytes, st>>>(P, n, src, sample, eidx);
-    } else {
-        if (variant == 0) k_ac2d_fused<0, 4><<<nblocks, threads, bytes, st>>>(P, n, src, sample, eidx);
-        else if (variant == 3) k_ac2d_fused<3, 4><<<nblocks, threads, bytes, st>>>(P, n, src, sample, eidx);
-        else k_ac2d_fused<6, 4><<<nblocks, threads, bytes, st>>>(P, n, src, sample, eidx);
-    }
+    void* fn = fused2d_rowmed(P) ? fused_fn<true>(variant, order) : fused_fn<false>(variant, order);
+    void* args[] = {(void*)&P, (void*)&n, (void*)&src, (void*)&sample, (void*)&eidx};
+    cudaLaunchKernel(fn, dim3(nblocks), dim3(threads), args, bytes, st);
 }
 
 }  // namespace hw
