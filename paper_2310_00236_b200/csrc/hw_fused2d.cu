@@ -144,11 +144,11 @@ __global__ void __launch_bounds__(512, 1)
     int* rec_local = reinterpret_cast<int*>(smem + 64);  // up to 8 (row, x, j) triples
     __half* ring = reinterpret_cast<__half*>(smem + 256);
     const int64_t nx = P.nx, ns = P.ns, pitch = P.pitch;
-    __half* xrow = ring + (int64_t)FR * NSTREAM * nx;
+    __half* xrows = ring + (int64_t)FR * NSTREAM * nx;  // two rows, alternating by iteration parity
     const int nb = gridDim.x, b = blockIdx.x;
-    const int64_t y0 = (int64_t)b * ns / nb, y1 = (int64_t)(b + 1) * ns / nb;
-    const int64_t F0 = y0 - 3;
-    const int64_t NI = (y1 + 3) - F0;
+    const int y0 = (int)((int64_t)b * ns / nb), y1 = (int)((int64_t)(b + 1) * ns / nb);
+    const int F0 = y0 - 3;
+    const int NI = (y1 + 3) - F0;
     const int tid = threadIdx.x;
     const int x = tid * FCPT;
     constexpr bool comp = V != 0;
@@ -215,13 +215,14 @@ __global__ void __launch_bounds__(512, 1)
     for (int q = 0; q < NSTREAM; q++) acc[q] = __float2half2_rn(0.f);
     double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
 
-    for (int64_t i0 = 0; i0 < NI; i0 += FR) {
+    for (int i0 = 0; i0 < NI; i0 += FR) {
         const uint32_t par = (uint32_t)((i0 / FR) & 1);
 #pragma unroll
         for (int u = 0; u < FR; u++) {
-            const int64_t i = i0 + u;
+            const int i = i0 + u;
             if (i < NI) {
-                const int64_t f = F0 + i;
+                const int f = F0 + i;
+                __half* xrow = xrows + (u & 1) * nx;  // FR is even: parity of i == parity of u
                 if (tid == 0 && i + FR - 1 < NI) {
                     fence_proxy_async_smem();
                     issue(i + FR - 1, (u + FR - 1) % FR);
@@ -258,9 +259,12 @@ __global__ void __launch_bounds__(512, 1)
                         }
                     }
                 }
+                const int k = f - 3;
+                const bool do_p = k >= y0 && k < y1;
+                V8 rp = (comp && do_p) ? lds8(slot_row(u, S_RP) + x) : V8{};  // all ring reads before the barrier
                 if (f >= y0 && f < y1 + 3) {  // vy[f-2] from p rows f-3..f (acoustic.py:169-170)
-                    const int64_t r = f - 2;
-                    const int64_t rw = wrap_row(r);
+                    const int r = f - 2;
+                    const int rw = (int)wrap_row(r);
                     V8 vsn = lds8(slot_row(u, S_VS) + x);
                     V8 rr = comp ? lds8(slot_row(u, S_RVS) + x) : V8{};
                     const V8& t0 = pq[(u + 1) % FR];
@@ -295,13 +299,14 @@ __global__ void __launch_bounds__(512, 1)
                     }
                     vq[u] = vsn;
                 }
-                __syncthreads();  // xrow holds vx_new[f]
+                // One barrier per row: xrow[f&1] now holds vx_new[f] and every thread is past
+                // its ring-slot reads, so the producer may refill this slot next iteration;
+                // xrow[f&1] is rewritten two iterations later, after another barrier.
+                __syncthreads();
                 if (do_vx) gq[u] = xfold8<ORDER>(c, ld2(xrow + xl), lds8(xrow + x), ld2(xrow + xr), true);
-                const int64_t k = f - 3;
-                if (k >= y0 && k < y1) {  // p[k] (acoustic.py:172-181)
+                if (do_p) {  // p[k] (acoustic.py:172-181)
                     const V8& pold = pq[(u + 1) % FR];
                     V8 pn = pold;
-                    V8 rp = comp ? lds8(slot_row(u, S_RP) + x) : V8{};
                     const V8& g = gq[(u + 1) % FR];
                     const V8& a0 = vq[(u + 1) % FR];
                     const V8& a1 = vq[(u + 2) % FR];
@@ -345,7 +350,6 @@ __global__ void __launch_bounds__(512, 1)
                         }
                     }
                 }
-                __syncthreads();  // ring slot and xrow free for reuse
             }
         }
     }
@@ -377,7 +381,7 @@ __global__ void __launch_bounds__(512, 1)
     }
 }
 
-size_t fused2d_smem_bytes(int64_t nx) { return 256 + ((size_t)FR * NSTREAM + 1) * nx * sizeof(__half); }
+size_t fused2d_smem_bytes(int64_t nx) { return 256 + ((size_t)FR * NSTREAM + 2) * nx * sizeof(__half); }
 
 int fused2d_threads(int64_t nx) { return (int)(nx / FCPT); }
 
