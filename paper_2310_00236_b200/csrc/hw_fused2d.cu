@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(512, 1)
     if (halted(P.ctrl, n)) return;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);       // FR "row landed" barriers (TMA tx)
-    uint64_t* empty = full + FR;                              // FR "slot consumed" barriers (one arrive per warp)
+    unsigned int* released = reinterpret_cast<unsigned int*>(full + FR);  // per-slot count of warps done with it
     int* rec_local = reinterpret_cast<int*>(smem + 128);      // up to 8 (row, x, j) triples
     __half* ring = reinterpret_cast<__half*>(smem + 256);
     const int64_t nx = P.nx, ns = P.ns, pitch = P.pitch;
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(512, 1)
     if (tid == 0) {
         for (int s = 0; s < FR; s++) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], (uint32_t)nwarps_c);
+            released[s] = 0u;
         }
         fence_mbar_init();
         int cnt = 0;  // receivers on this CTA's rows
@@ -226,9 +226,8 @@ __global__ void __launch_bounds__(512, 1)
         }
         if (lrp) tma_load_1d(slot_row(slot, S_RP), P.in[S_RP] + (int64_t)(f - 3) * pitch, rb, &full[slot]);
     };
-    int next = 0;  // producer (thread 0): next iteration to issue
     if (tid == 0)
-        for (; next < FR && next < NI; next++) issue(next);  // slots start empty
+        for (int j = 0; j < FR && j < NI; j++) issue(j);  // slots start empty
     {
         // ---------------- consumer warps: independent 256-column strips
         const int n_local = rec_local[0];
@@ -253,19 +252,6 @@ __global__ void __launch_bounds__(512, 1)
                 const int i = i0 + u;
                 if (i < NI) {
                     const int f = F0 + i;
-                    if (tid == 0) {
-                        // Producer duty of warp 0 / lane 0: refill slots as soon as every warp has
-                        // released them (non-blocking), blocking only for the row needed right now.
-                        // Slot reuse for iteration j waits on all warps finishing iteration j - FR.
-                        for (; next < NI && next < i + FR; next++) {
-                            const uint32_t ph = (uint32_t)(((next / FR) - 1) & 1);
-                            if (!mbar_try_wait(&empty[next % FR], ph)) {
-                                if (next > i) break;
-                                mbar_wait(&empty[next % FR], ph);
-                            }
-                            issue(next);
-                        }
-                    }
                     mbar_wait(&full[u], par);
                     const __half* prow = slot_row(u, S_P);
                     pq[u] = lds8(prow + x);
@@ -352,8 +338,17 @@ __global__ void __launch_bounds__(512, 1)
                         }
                         vq[u] = vsn;
                     }
-                    __syncwarp();  // this warp is done with ring slot u
-                    if (lane == 0) mbar_arrive(&empty[u]);
+                    // Release ring slot u; the last warp to release it refills it with
+                    // iteration i + FR right away (no producer warp, no block barrier).
+                    __syncwarp();
+                    if (lane == 0) {
+                        __threadfence_block();
+                        if (atomicAdd(&released[u], 1u) == (unsigned int)(nwarps_c - 1)) {
+                            released[u] = 0u;
+                            __threadfence_block();
+                            if (i + FR < NI) issue(i + FR);
+                        }
+                    }
                     if (do_p) {  // p[k] (acoustic.py:172-181)
                         const V8& pold = pq[(u + 1) % FR];
                         V8 pn = pold;
