@@ -135,44 +135,21 @@ __device__ __forceinline__ void finish_row(H2 rhs, float rcp, __half2 dt2, int s
     u.h2 = s;
 }
 
-// vx_new for the single pair at x-offset xp (periodic), used by lanes 0 / 31 to
-// recompute the one halo pair their shuffle neighbour lives in another warp for.
-template <int V, int ORDER, bool ROWMED>
-__device__ __forceinline__ H2 vx_halo_pair(const AcFusedParams& P, const __half c[4], const __half* prow,
-                                           const __half* vxrow, const __half* rvxrow, int xp, int nx, int f,
-                                           float rc, __half2 dt2, __half srch) {
-    const int xm = xp == 0 ? nx - 2 : xp - 2, xq = xp + 2 >= nx ? 0 : xp + 2;
-    const H2 a = ld2(prow + xm), m = ld2(prow + xp), b = ld2(prow + xq);
-    // to-half taps (-1,0,1,2): (x-1,x) (x,x+1) (x+1,x+2) (x+2,x+3)
-    H2 d = fold2<ORDER>(c, vshift<16, 2>(a, m), m, vshift<16, 2>(m, b), b);
-    H2 u = ld2(vxrow + xp);
-    H2 t;
-    if (V != 0) t = ld2(rvxrow + xp);
-    if constexpr (ROWMED) {
-        finish_row<V>(d, rc, dt2, -1, srch, u, t);
-    } else {
-        finish<16, 16, 2>(d, &P.rho_x, f, 0, xp, dt2.x, V, -1, 0.0, u, t);
-    }
-    return u;
-}
-
 template <int V, int ORDER, bool ROWMED>
 __global__ void __launch_bounds__(512, 1)
     k_ac2d_fused(AcFusedParams P, int64_t n, double src, int sample, int64_t eidx) {
     if (halted(P.ctrl, n)) return;
     extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem);       // FR "row landed" barriers (TMA tx)
-    unsigned int* released = reinterpret_cast<unsigned int*>(full + FR);  // per-slot count of warps done with it
-    int* rec_local = reinterpret_cast<int*>(smem + 128);      // up to 8 (row, x, j) triples
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
+    int* rec_local = reinterpret_cast<int*>(smem + 64);  // up to 8 (row, x, j) triples
     __half* ring = reinterpret_cast<__half*>(smem + 256);
     const int64_t nx = P.nx, ns = P.ns, pitch = P.pitch;
+    __half* xrows = ring + (int64_t)FR * NSTREAM * nx;  // two rows, alternating by iteration parity
     const int nb = gridDim.x, b = blockIdx.x;
     const int y0 = (int)((int64_t)b * ns / nb), y1 = (int)((int64_t)(b + 1) * ns / nb);
     const int F0 = y0 - 3;
     const int NI = (y1 + 3) - F0;
     const int tid = threadIdx.x;
-    const int nwarps_c = (int)(blockDim.x / 32);
-    const int lane = tid & 31;
     const int x = tid * FCPT;
     constexpr bool comp = V != 0;
     const uint32_t rb = (uint32_t)(nx * sizeof(__half));
@@ -182,12 +159,28 @@ __global__ void __launch_bounds__(512, 1)
         r %= ns;
         return r < 0 ? r + ns : r;
     };
+    auto issue = [&](int64_t i, int slot) {  // TMA loads of iteration i (front row F0 + i)
+        const int64_t f = F0 + i;
+        const bool lvx = f >= y0 && f < y1;
+        const bool lvs = f >= y0 && f < y1 + 3;
+        const bool lrp = comp && f >= y0 + 3 && f < y1 + 3;
+        const uint32_t rows = 1 + (lvx ? (comp ? 2 : 1) : 0) + (lvs ? (comp ? 2 : 1) : 0) + (lrp ? 1 : 0);
+        mbar_arrive_expect_tx(&bar[slot], rows * rb);
+        tma_load_1d(slot_row(slot, S_P), P.in[S_P] + wrap_row(f) * pitch, rb, &bar[slot]);
+        if (lvx) {
+            tma_load_1d(slot_row(slot, S_VX), P.in[S_VX] + f * pitch, rb, &bar[slot]);
+            if (comp) tma_load_1d(slot_row(slot, S_RVX), P.in[S_RVX] + f * pitch, rb, &bar[slot]);
+        }
+        if (lvs) {
+            const int64_t r = wrap_row(f - 2);
+            tma_load_1d(slot_row(slot, S_VS), P.in[S_VS] + r * pitch, rb, &bar[slot]);
+            if (comp) tma_load_1d(slot_row(slot, S_RVS), P.in[S_RVS] + r * pitch, rb, &bar[slot]);
+        }
+        if (lrp) tma_load_1d(slot_row(slot, S_RP), P.in[S_RP] + (f - 3) * pitch, rb, &bar[slot]);
+    };
 
     if (tid == 0) {
-        for (int s = 0; s < FR; s++) {
-            mbar_init(&full[s], 1);
-            released[s] = 0u;
-        }
+        for (int s = 0; s < FR; s++) mbar_init(&bar[s], 1);
         fence_mbar_init();
         int cnt = 0;  // receivers on this CTA's rows
         for (int q = 0; q < P.n_rec && cnt < 8; q++) {
@@ -202,206 +195,168 @@ __global__ void __launch_bounds__(512, 1)
         rec_local[0] = cnt;
     }
     __syncthreads();
-
-    double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    unsigned int mask = 0;
-    auto issue = [&](int i) {  // TMA loads of iteration i (front row F0 + i) into slot i % FR
-        const int slot = i % FR;
-        fence_proxy_async_smem();
-        const int f = F0 + i;
-        const bool lvx = f >= y0 && f < y1;
-        const bool lvs = f >= y0 && f < y1 + 3;
-        const bool lrp = comp && f >= y0 + 3 && f < y1 + 3;
-        const uint32_t rows = 1 + (lvx ? (comp ? 2 : 1) : 0) + (lvs ? (comp ? 2 : 1) : 0) + (lrp ? 1 : 0);
-        mbar_arrive_expect_tx(&full[slot], rows * rb);
-        tma_load_1d(slot_row(slot, S_P), P.in[S_P] + wrap_row(f) * pitch, rb, &full[slot]);
-        if (lvx) {
-            tma_load_1d(slot_row(slot, S_VX), P.in[S_VX] + (int64_t)f * pitch, rb, &full[slot]);
-            if (comp) tma_load_1d(slot_row(slot, S_RVX), P.in[S_RVX] + (int64_t)f * pitch, rb, &full[slot]);
-        }
-        if (lvs) {
-            const int64_t r = wrap_row(f - 2);
-            tma_load_1d(slot_row(slot, S_VS), P.in[S_VS] + r * pitch, rb, &full[slot]);
-            if (comp) tma_load_1d(slot_row(slot, S_RVS), P.in[S_RVS] + r * pitch, rb, &full[slot]);
-        }
-        if (lrp) tma_load_1d(slot_row(slot, S_RP), P.in[S_RP] + (int64_t)(f - 3) * pitch, rb, &full[slot]);
-    };
     if (tid == 0)
-        for (int j = 0; j < FR && j < NI; j++) issue(j);  // slots start empty
-    {
-        // ---------------- consumer warps: independent 256-column strips
-        const int n_local = rec_local[0];
-        __half c[4];
-#pragma unroll
-        for (int j = 0; j < 4; j++) c[j] = lconst<16>(P.k, j);
-        const __half2 dt2 = __half2half2(lconst<16>(P.k, 4));
-        const __half srch = __double2half(src);
-        const int xl = x == 0 ? (int)nx - 2 : x - 2;        // left neighbour pair (p row taps)
-        const int xr = x + FCPT >= (int)nx ? 0 : x + FCPT;  // right neighbour pair
-        const bool src_here = P.has_src && src != 0.0 && P.src_x >= x && P.src_x < x + FCPT;
-        const int src_j = (int)((P.src_x - x) >> 1), src_lane = (int)((P.src_x - x) & 1);
-        V8 pq[4], vq[4], gq[4];  // p rows, vy_new rows, d/dx vx_new rows (indexed by iteration mod 4)
-        __half2 acc[NSTREAM];
-#pragma unroll
-        for (int q = 0; q < NSTREAM; q++) acc[q] = __float2half2_rn(0.f);
+        for (int64_t i = 0; i < FR - 1 && i < NI; i++) issue(i, (int)i);
+    const int n_local = rec_local[0];
 
-        for (int i0 = 0; i0 < NI; i0 += FR) {
-            const uint32_t par = (uint32_t)((i0 / FR) & 1);
+    __half c[4];
 #pragma unroll
-            for (int u = 0; u < FR; u++) {
-                const int i = i0 + u;
-                if (i < NI) {
-                    const int f = F0 + i;
-                    mbar_wait(&full[u], par);
-                    const __half* prow = slot_row(u, S_P);
-                    pq[u] = lds8(prow + x);
-                    const int k = f - 3;
-                    const bool do_p = k >= y0 && k < y1;
-                    V8 rp = (comp && do_p) ? lds8(slot_row(u, S_RP) + x) : V8{};
-                    const bool do_vx = f >= y0 && f < y1;
-                    if (do_vx) {  // vx[f] (acoustic.py:167-168)
-                        const __half* vxrow = slot_row(u, S_VX);
-                        const __half* rvxrow = slot_row(u, S_RVX);
-                        V8 d = xfold8<ORDER>(c, ld2(prow + xl), pq[u], ld2(prow + xr), false);
-                        V8 vxn = lds8(vxrow + x);
-                        V8 r = comp ? lds8(rvxrow + x) : V8{};
-                        float rc = 0.f;
-                        if constexpr (ROWMED) {
-                            rc = __ldg(P.rho_x.rcp + (int64_t)f * P.rho_x.ss);
+    for (int j = 0; j < 4; j++) c[j] = lconst<16>(P.k, j);
+    const __half2 dt2 = __half2half2(lconst<16>(P.k, 4));
+    const __half srch = __double2half(src);
+    const int xl = x == 0 ? (int)nx - 2 : x - 2;                // left neighbour pair
+    const int xr = x + FCPT >= (int)nx ? 0 : x + FCPT;          // right neighbour pair
+    const bool src_here = P.has_src && src != 0.0 && P.src_x >= x && P.src_x < x + FCPT;
+    const int src_j = (int)((P.src_x - x) >> 1), src_lane = (int)((P.src_x - x) & 1);
+
+    V8 pq[4], vq[4], gq[4];  // p rows, vy_new rows, d/dx vx_new rows (indexed by iteration mod 4)
+    __half2 acc[NSTREAM];
 #pragma unroll
-                            for (int j = 0; j < 4; j++) finish_row<V>(d.q[j], rc, dt2, -1, srch, vxn.q[j], r.q[j]);
-                        } else {
+    for (int q = 0; q < NSTREAM; q++) acc[q] = __float2half2_rn(0.f);
+    double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
+
+    for (int i0 = 0; i0 < NI; i0 += FR) {
+        const uint32_t par = (uint32_t)((i0 / FR) & 1);
 #pragma unroll
-                            for (int j = 0; j < 4; j++)
-                                finish<16, 16, 2>(d.q[j], &P.rho_x, f, 0, x + 2 * j, dt2.x, V, -1, 0.0, vxn.q[j], r.q[j]);
+        for (int u = 0; u < FR; u++) {
+            const int i = i0 + u;
+            if (i < NI) {
+                const int f = F0 + i;
+                __half* xrow = xrows + (u & 1) * nx;  // FR is even: parity of i == parity of u
+                if (tid == 0 && i + FR - 1 < NI) {
+                    fence_proxy_async_smem();
+                    issue(i + FR - 1, (u + FR - 1) % FR);
+                }
+                mbar_wait(&bar[u], par);
+                const __half* prow = slot_row(u, S_P);
+                pq[u] = lds8(prow + x);
+                const bool do_vx = f >= y0 && f < y1;
+                if (do_vx) {  // vx[f] (acoustic.py:167-168)
+                    V8 d = xfold8<ORDER>(c, ld2(prow + xl), pq[u], ld2(prow + xr), false);
+                    V8 vxn = lds8(slot_row(u, S_VX) + x);
+                    V8 r = comp ? lds8(slot_row(u, S_RVX) + x) : V8{};
+                    if constexpr (ROWMED) {
+                        const float rc = __ldg(P.rho_x.rcp + f * P.rho_x.ss);
+#pragma unroll
+                        for (int j = 0; j < 4; j++) finish_row<V>(d.q[j], rc, dt2, -1, srch, vxn.q[j], r.q[j]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 4; j++)
+                            finish<16, 16, 2>(d.q[j], &P.rho_x, f, 0, x + 2 * j, dt2.x, V, -1, 0.0, vxn.q[j], r.q[j]);
+                    }
+                    st8(P.out[S_VX] + f * pitch + x, vxn);
+                    track(acc[S_VX], vxn);
+                    if (comp) {
+                        st8(P.out[S_RVX] + f * pitch + x, r);
+                        track(acc[S_RVX], r);
+                    }
+                    st8(xrow + x, vxn);
+                    if (sample) {
+#pragma unroll
+                        for (int j = 0; j < FCPT; j++) {
+                            const double v = (double)__half2float(vxn.q[j >> 1].e[j & 1]);
+                            e[1] += p64(P.e_rho_x, f, 0, x + j) * (v * v);
                         }
-                        st8(P.out[S_VX] + (int64_t)f * pitch + x, vxn);
-                        track(acc[S_VX], vxn);
+                    }
+                }
+                const int k = f - 3;
+                const bool do_p = k >= y0 && k < y1;
+                V8 rp = (comp && do_p) ? lds8(slot_row(u, S_RP) + x) : V8{};  // all ring reads before the barrier
+                if (f >= y0 && f < y1 + 3) {  // vy[f-2] from p rows f-3..f (acoustic.py:169-170)
+                    const int r = f - 2;
+                    const int rw = (int)wrap_row(r);
+                    V8 vsn = lds8(slot_row(u, S_VS) + x);
+                    V8 rr = comp ? lds8(slot_row(u, S_RVS) + x) : V8{};
+                    const V8& t0 = pq[(u + 1) % FR];
+                    const V8& t1 = pq[(u + 2) % FR];
+                    const V8& t2 = pq[(u + 3) % FR];
+                    if constexpr (ROWMED) {
+                        const float rc = __ldg(P.rho_s.rcp + rw * P.rho_s.ss);
+#pragma unroll
+                        for (int j = 0; j < 4; j++)
+                            finish_row<V>(fold2<ORDER>(c, t0.q[j], t1.q[j], t2.q[j], pq[u].q[j]), rc, dt2, -1, srch,
+                                          vsn.q[j], rr.q[j]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 4; j++)
+                            finish<16, 16, 2>(fold2<ORDER>(c, t0.q[j], t1.q[j], t2.q[j], pq[u].q[j]), &P.rho_s, rw, 0,
+                                              x + 2 * j, dt2.x, V, -1, 0.0, vsn.q[j], rr.q[j]);
+                    }
+                    if (r >= y0 && r < y1) {
+                        st8(P.out[S_VS] + r * pitch + x, vsn);
+                        track(acc[S_VS], vsn);
                         if (comp) {
-                            st8(P.out[S_RVX] + (int64_t)f * pitch + x, r);
-                            track(acc[S_RVX], r);
-                        }
-                        // x neighbours of vx_new for d/dx vx: shuffles inside the warp, one
-                        // recomputed halo pair at each strip edge
-                        H2 left, right;
-                        *reinterpret_cast<unsigned int*>(&left.h2) =
-                            __shfl_up_sync(0xffffffffu, *reinterpret_cast<unsigned int*>(&vxn.q[3].h2), 1);
-                        *reinterpret_cast<unsigned int*>(&right.h2) =
-                            __shfl_down_sync(0xffffffffu, *reinterpret_cast<unsigned int*>(&vxn.q[0].h2), 1);
-                        if (lane == 0)
-                            left = vx_halo_pair<V, ORDER, ROWMED>(P, c, prow, vxrow, rvxrow, xl, (int)nx, f, rc, dt2, srch);
-                        if (lane == 31)
-                            right = vx_halo_pair<V, ORDER, ROWMED>(P, c, prow, vxrow, rvxrow, xr, (int)nx, f, rc, dt2, srch);
-                        gq[u] = xfold8<ORDER>(c, left, vxn, right, true);
-                        if (sample) {
-#pragma unroll
-                            for (int j = 0; j < FCPT; j++) {
-                                const double v = (double)__half2float(vxn.q[j >> 1].e[j & 1]);
-                                e[1] += p64(P.e_rho_x, f, 0, x + j) * (v * v);
-                            }
-                        }
-                    }
-                    if (f >= y0 && f < y1 + 3) {  // vy[f-2] from p rows f-3..f (acoustic.py:169-170)
-                        const int r = f - 2;
-                        const int rw = (int)wrap_row(r);
-                        V8 vsn = lds8(slot_row(u, S_VS) + x);
-                        V8 rr = comp ? lds8(slot_row(u, S_RVS) + x) : V8{};
-                        const V8& t0 = pq[(u + 1) % FR];
-                        const V8& t1 = pq[(u + 2) % FR];
-                        const V8& t2 = pq[(u + 3) % FR];
-                        if constexpr (ROWMED) {
-                            const float rc = __ldg(P.rho_s.rcp + (int64_t)rw * P.rho_s.ss);
-#pragma unroll
-                            for (int j = 0; j < 4; j++)
-                                finish_row<V>(fold2<ORDER>(c, t0.q[j], t1.q[j], t2.q[j], pq[u].q[j]), rc, dt2, -1, srch,
-                                              vsn.q[j], rr.q[j]);
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 4; j++)
-                                finish<16, 16, 2>(fold2<ORDER>(c, t0.q[j], t1.q[j], t2.q[j], pq[u].q[j]), &P.rho_s, rw, 0,
-                                                  x + 2 * j, dt2.x, V, -1, 0.0, vsn.q[j], rr.q[j]);
-                        }
-                        if (r >= y0 && r < y1) {
-                            st8(P.out[S_VS] + (int64_t)r * pitch + x, vsn);
-                            track(acc[S_VS], vsn);
-                            if (comp) {
-                                st8(P.out[S_RVS] + (int64_t)r * pitch + x, rr);
-                                track(acc[S_RVS], rr);
-                            }
-                            if (sample) {
-#pragma unroll
-                                for (int j = 0; j < FCPT; j++) {
-                                    const double v = (double)__half2float(vsn.q[j >> 1].e[j & 1]);
-                                    e[2] += p64(P.e_rho_s, r, 0, x + j) * (v * v);
-                                }
-                            }
-                        }
-                        vq[u] = vsn;
-                    }
-                    // Release ring slot u; the last warp to release it refills it with
-                    // iteration i + FR right away (no producer warp, no block barrier).
-                    __syncwarp();
-                    if (lane == 0) {
-                        __threadfence_block();
-                        if (atomicAdd(&released[u], 1u) == (unsigned int)(nwarps_c - 1)) {
-                            released[u] = 0u;
-                            __threadfence_block();
-                            if (i + FR < NI) issue(i + FR);
-                        }
-                    }
-                    if (do_p) {  // p[k] (acoustic.py:172-181)
-                        const V8& pold = pq[(u + 1) % FR];
-                        V8 pn = pold;
-                        const V8& g = gq[(u + 1) % FR];
-                        const V8& a0 = vq[(u + 1) % FR];
-                        const V8& a1 = vq[(u + 2) % FR];
-                        const V8& a2 = vq[(u + 3) % FR];
-                        const bool sk = src_here && k == P.src_s;
-                        if constexpr (ROWMED) {
-                            const float rc = __ldg(P.beta.rcp + (int64_t)k * P.beta.ss);
-#pragma unroll
-                            for (int j = 0; j < 4; j++) {
-                                H2 dv = O2::add(g.q[j], fold2<ORDER>(c, a0.q[j], a1.q[j], a2.q[j], vq[u].q[j]));
-                                finish_row<V>(dv, rc, dt2, (sk && j == src_j) ? src_lane : -1, srch, pn.q[j], rp.q[j]);
-                            }
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 4; j++) {
-                                H2 dv = O2::add(g.q[j], fold2<ORDER>(c, a0.q[j], a1.q[j], a2.q[j], vq[u].q[j]));
-                                finish<16, 16, 2>(dv, &P.beta, k, 0, x + 2 * j, dt2.x, V,
-                                                  (sk && j == src_j) ? src_lane : -1, src, pn.q[j], rp.q[j]);
-                            }
-                        }
-                        st8(P.out[S_P] + (int64_t)k * pitch + x, pn);
-                        track(acc[S_P], pn);
-                        if (comp) {
-                            st8(P.out[S_RP] + (int64_t)k * pitch + x, rp);
-                            track(acc[S_RP], rp);
+                            st8(P.out[S_RVS] + r * pitch + x, rr);
+                            track(acc[S_RVS], rr);
                         }
                         if (sample) {
 #pragma unroll
                             for (int j = 0; j < FCPT; j++) {
-                                const double a = (double)__half2float(pold.q[j >> 1].e[j & 1]);
-                                const double bb = (double)__half2float(pn.q[j >> 1].e[j & 1]);
-                                e[0] += p64(P.e_beta, k, 0, x + j) * (a * bb);
+                                const double v = (double)__half2float(vsn.q[j >> 1].e[j & 1]);
+                                e[2] += p64(P.e_rho_s, r, 0, x + j) * (v * v);
                             }
                         }
-                        for (int q = 0; q < n_local; q++) {  // receiver traces (acoustic.py:217-218)
-                            const int rx = rec_local[2 + 3 * q];
-                            if (rec_local[1 + 3 * q] == k && rx >= x && rx < x + FCPT) {
-                                const int o = rx - x;
-                                P.traces[(int64_t)rec_local[3 + 3 * q] * P.nt + n] =
-                                    (double)__half2float(pn.q[o >> 1].e[o & 1]);
-                            }
+                    }
+                    vq[u] = vsn;
+                }
+                // One barrier per row: xrow[f&1] now holds vx_new[f] and every thread is past
+                // its ring-slot reads, so the producer may refill this slot next iteration;
+                // xrow[f&1] is rewritten two iterations later, after another barrier.
+                __syncthreads();
+                if (do_vx) gq[u] = xfold8<ORDER>(c, ld2(xrow + xl), lds8(xrow + x), ld2(xrow + xr), true);
+                if (do_p) {  // p[k] (acoustic.py:172-181)
+                    const V8& pold = pq[(u + 1) % FR];
+                    V8 pn = pold;
+                    const V8& g = gq[(u + 1) % FR];
+                    const V8& a0 = vq[(u + 1) % FR];
+                    const V8& a1 = vq[(u + 2) % FR];
+                    const V8& a2 = vq[(u + 3) % FR];
+                    const bool sk = src_here && k == P.src_s;
+                    if constexpr (ROWMED) {
+                        const float rc = __ldg(P.beta.rcp + k * P.beta.ss);
+#pragma unroll
+                        for (int j = 0; j < 4; j++) {
+                            H2 dv = O2::add(g.q[j], fold2<ORDER>(c, a0.q[j], a1.q[j], a2.q[j], vq[u].q[j]));
+                            finish_row<V>(dv, rc, dt2, (sk && j == src_j) ? src_lane : -1, srch, pn.q[j], rp.q[j]);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 4; j++) {
+                            H2 dv = O2::add(g.q[j], fold2<ORDER>(c, a0.q[j], a1.q[j], a2.q[j], vq[u].q[j]));
+                            finish<16, 16, 2>(dv, &P.beta, k, 0, x + 2 * j, dt2.x, V, (sk && j == src_j) ? src_lane : -1,
+                                              src, pn.q[j], rp.q[j]);
+                        }
+                    }
+                    st8(P.out[S_P] + k * pitch + x, pn);
+                    track(acc[S_P], pn);
+                    if (comp) {
+                        st8(P.out[S_RP] + k * pitch + x, rp);
+                        track(acc[S_RP], rp);
+                    }
+                    if (sample) {
+#pragma unroll
+                        for (int j = 0; j < FCPT; j++) {
+                            const double a = (double)__half2float(pold.q[j >> 1].e[j & 1]);
+                            const double bb = (double)__half2float(pn.q[j >> 1].e[j & 1]);
+                            e[0] += p64(P.e_beta, k, 0, x + j) * (a * bb);
+                        }
+                    }
+                    for (int q = 0; q < n_local; q++) {  // receiver traces (acoustic.py:217-218)
+                        const int rx = rec_local[2 + 3 * q];
+                        if (rec_local[1 + 3 * q] == k && rx >= x && rx < x + FCPT) {
+                            const int o = rx - x;
+                            P.traces[(int64_t)rec_local[3 + 3 * q] * P.nt + n] =
+                                (double)__half2float(pn.q[o >> 1].e[o & 1]);
                         }
                     }
                 }
             }
         }
-        // bit order = external field order p vx vy rp rvx rvy == stream order
-#pragma unroll
-        for (int q = 0; q < NSTREAM; q++) mask |= nonfinite_acc(acc[q]) << q;
     }
+    unsigned int mask = 0;
+    // bit order = external field order p vx vy rp rvx rvy == stream order
+#pragma unroll
+    for (int q = 0; q < NSTREAM; q++) mask |= nonfinite_acc(acc[q]) << q;
     record_failure(P.ctrl, n, mask);
     if (!sample) return;
     block_partials(e, P.partials);
@@ -426,7 +381,7 @@ __global__ void __launch_bounds__(512, 1)
     }
 }
 
-size_t fused2d_smem_bytes(int64_t nx) { return 256 + (size_t)FR * NSTREAM * nx * sizeof(__half); }
+size_t fused2d_smem_bytes(int64_t nx) { return 256 + ((size_t)FR * NSTREAM + 2) * nx * sizeof(__half); }
 
 int fused2d_threads(int64_t nx) { return (int)(nx / FCPT); }
 
