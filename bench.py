@@ -112,30 +112,25 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_baseline(hw, seconds_target=15.0):
-    """The CPU oracle port (oracle/halfwave_oracle.c, OpenMP) on a bounded sample of
-    the same workload: 4096^2 cells, a few leapfrog steps of config 2."""
+def cpu_baseline(hw, steps=40):
+    """The CPU oracle port (oracle/halfwave_oracle.c, OpenMP over rows, all host
+    threads) on a bounded sample of the same workload: `steps` leapfrog steps of
+    config 2 at 4096^2 with energy every 10.  Steady-state rate: the one-off setup
+    (lane rounding of the medium planes) is timed with nt=0 and subtracted."""
     import oracle
+    from paper_2310_00236_b200.efsum import variant_code
 
     s = make_solver(hw, nt=1)
     st = s.new_state()
     cores = os.cpu_count() or 1
-    oracle.run_solver(s, hw.Variant.OP3, st, nt=1, energy=False, nthreads=cores)  # warm
-    steps, elapsed = 0, 0.0
-    arrays = [getattr(st, n).values for n in s.FIELDS]
-    from paper_2310_00236_b200.efsum import variant_code
-
-    while elapsed < seconds_target and steps < 200:
-        t0 = time.perf_counter()
-        out = oracle.run_desc(s.desc, arrays, variant_code(hw.Variant.OP3), steps, 1,
-                              s.source_samples(steps, 1), energy=False, nthreads=cores)
-        elapsed += time.perf_counter() - t0
-        arrays = out["fields"]
-        steps += 1
-    v = N * N * steps / elapsed
-    return {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{steps} leapfrog steps of config 2 at 4096x4096 (fp16 op3, no energy), "
-                      f"oracle/halfwave_oracle.c with {cores} OpenMP threads"}
+    arrays = [np.ascontiguousarray(getattr(st, n).values, dtype=np.float64) for n in s.FIELDS]
+    v = variant_code(hw.Variant.OP3)
+    t_setup = oracle.timed_steps(s.desc, arrays, v, 0, 0, None, cores, energy=True)
+    t_run = oracle.timed_steps(s.desc, arrays, v, 0, steps, s.source_samples(0, steps), cores, energy=True)
+    el = max(t_run - t_setup, 1e-9)
+    return {"value": N * N * steps / el, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{steps} leapfrog steps of config 2 at 4096x4096 (fp16 op3, energy every 10), "
+                      f"oracle/halfwave_oracle.c, {cores} OpenMP threads, {el:.1f} s"}
 
 
 def dist_env():
@@ -158,27 +153,26 @@ def run_reference(args):
     s = make_solver(hw, nt=1)
     st = s.new_state()
     cores = os.cpu_count() or 1
-    arrays = [getattr(st, n).values for n in s.FIELDS]
-    per_step = 2  # leapfrog steps per bench step (bounded sample of the 5000-step run)
+    arrays = [np.ascontiguousarray(getattr(st, n).values, dtype=np.float64) for n in s.FIELDS]
+    per_step = 10  # leapfrog steps per bench step (a bounded sample of the 5000-step run)
+    v = variant_code(hw.Variant.OP3)
+    t_setup = oracle.timed_steps(s.desc, arrays, v, 0, 0, None, cores, energy=True)
     step_idx = 0
 
     def one():
-        nonlocal arrays, step_idx
-        out = oracle.run_desc(s.desc, arrays, variant_code(hw.Variant.OP3), step_idx, per_step,
-                              s.source_samples(step_idx, per_step), energy=True, nthreads=cores)
-        arrays = out["fields"]
+        nonlocal step_idx
+        t = oracle.timed_steps(s.desc, arrays, v, step_idx, per_step, s.source_samples(step_idx, per_step),
+                               cores, energy=True)
         step_idx += per_step
+        return max(t - t_setup, 1e-9)
 
     for _ in range(args.warmup):
         one()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        one()
-    el = time.perf_counter() - t0
+    el = sum(one() for _ in range(args.steps))
     v = N * N * per_step * args.steps / el
     cb = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
           "sample": f"{per_step} leapfrog steps of config 2 at 4096x4096 per bench step (fp16 op3, energy "
-                    f"every 10 logged), oracle/halfwave_oracle.c with {cores} OpenMP threads"}
+                    f"every 10), oracle/halfwave_oracle.c, {cores} OpenMP threads, setup excluded"}
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16",
@@ -247,10 +241,17 @@ def main():
     peak, peak_src = peak_hbm()
     per_leap_ms = ms_total / (args.steps * args.nt)
     achieved = B_ALG * cells / (per_leap_ms / 1e3) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"  # dram bytes per launch from the committed ncu --set full capture
+    if tf.exists():
+        tj = json.loads(tf.read_text())
+        traffic = {"bytes_per_launch": tj["dram_bytes_per_launch"], "source": tj["source"],
+                   "bytes_per_cell_step": tj["dram_bytes_per_launch"] / cells}
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "peak_source": peak_src,
+                "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_cell_step": B_ALG,
-                "kernel": "one leapfrog step (velocity + pressure phase kernels + epilogue), 4096^2 cells"}
+                "kernel": "k_ac2d_fused (one launch per leapfrog step of 4096^2 cells); achieved uses the "
+                          "CUDA-event time of the whole step loop (launch gaps included)"}
 
     # ---------------------------------------------------------- end to end through the public API
     import torch as _t

@@ -115,3 +115,24 @@ def run_solver(solver, variant, state=None, nt=None, energy=True, nthreads=0) ->
                    energy=energy, nthreads=nthreads)
     out["step0"] = state.step
     return out
+
+
+def timed_steps(desc, arrays64, variant: int, step0: int, nt: int, src=None, nthreads: int = 0,
+                energy: bool = False) -> float:
+    """Advance binary64-container state arrays in place by nt steps; return the wall
+    seconds of the C call alone (CPU-baseline timing, no Python conversions)."""
+    import time
+
+    lib = load()
+    P = ctypes.POINTER(ctypes.c_double)
+    ptrs = (P * len(arrays64))(*[a.ctypes.data_as(P) for a in arrays64])
+    srcp = None
+    if src is not None:
+        src = np.ascontiguousarray(src, dtype=np.float64)
+        srcp = src.ctypes.data_as(P)
+    cap = 1 + nt // desc.energy_every
+    e = np.zeros(cap) if energy else None
+    t0 = time.perf_counter()
+    lib.hwo_run(ctypes.addressof(desc), ptrs, variant, step0, nt, srcp, None,
+                e.ctypes.data_as(P) if energy else None, None, None, None, None, nthreads)
+    return time.perf_counter() - t0
