@@ -1,0 +1,72 @@
+"""Device-resident throughput of the BASELINE configs on one GPU (short runs):
+python tools/measure_configs.py [nt] -> one JSON line per config."""
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import paper_2310_00236_b200 as hw  # noqa: E402
+
+NT = int(sys.argv[1]) if len(sys.argv) > 1 else 50
+F16 = hw.Precision.FP16
+
+
+def timed(name, s, variant, bytes_per_cell, cells, nt=NT):
+    st = s.new_state()
+    s.upload(st)
+    s.run_device(variant, 0, 3)
+    ms = s.run_device(variant, 3, nt)
+    rate = cells * nt / (ms / 1e3)
+    print(json.dumps({"config": name, "cell_steps_per_s": rate, "us_per_step": 1e3 * ms / nt,
+                      "B_alg": bytes_per_cell, "GBps": rate * bytes_per_cell / 1e9,
+                      "frac_of_6551": rate * bytes_per_cell / 6551.7e9, "launches": s.last_launch_count()}), flush=True)
+
+
+def cfg1(order):  # 2D acoustic 256^2, CFL 0.5 (4th order twin: reference-native periodic)
+    n = 256
+    dx = 1.0 / n
+    g = hw.GridSpec(n, n, dx, 0.5 * dx if order == 2 else 0.5 * dx, NT, order=order)
+    return hw.AcousticSolver(g, hw.build_homogeneous_acoustic(n, n, 1.0, 1.0), stencil_precision=F16, energy_every=1)
+
+
+def cfg3():  # 3D acoustic 512^3, 2nd order, full beta plane
+    n = 512
+    rng = np.random.default_rng(0)
+    c = 1.5 + 3.0 * rng.random((n, n, n))
+    med = hw.build_acoustic_from_velocity(c)
+    dx = 1.0 / n
+    g = hw.GridSpec(n, n, dx, float(np.float16(0.5 * dx / (med.c_max() * np.sqrt(3)))), NT, nz=n, order=2)
+    return hw.AcousticSolver(g, med, stencil_precision=F16, energy_every=10)
+
+
+def cfg4():  # 2D elastic 4096^2, free surface
+    n = 4096
+    med = hw.build_layered_elastic(n, n, [(1.0, 1.0, 2.0, 1.0)])
+    dx = 1.0 / n
+    g = hw.GridSpec(n, n, dx, float(np.float16(0.4 * dx / 2)), NT, bc_y=hw.Boundary.FREE_SURFACE)
+    src = hw.SourceSpec(hw.SourceKind.EXPLOSIVE, n // 2, 16, hw.RickerSpec(1 / (10 * dx), amplitude=1.0))
+    return hw.ElasticSolver(g, med, src, stencil_precision=F16, energy_every=10)
+
+
+def cfg5():  # 3D elastic 512^3 per GPU, 2nd order, layered
+    n = 512
+    med = hw.build_layered_elastic(n, n, [(0.3, 1.0, 2.0, 1.0), (0.7, 1.4, 2.6, 1.3), (1.0, 1.8, 3.0, 1.6)], nz=n)
+    dx = 1.0 / n
+    g = hw.GridSpec(n, n, dx, float(np.float16(0.4 * dx / 3.0)), NT, nz=n, order=2)
+    return hw.ElasticSolver(g, med, stencil_precision=F16, energy_every=10)
+
+
+if __name__ == "__main__":
+    which = sys.argv[2].split(",") if len(sys.argv) > 2 else ["1", "3", "4", "5"]
+    if "1" in which:
+        timed("1: 2D acoustic 256^2 4th-order periodic fp16 op3", cfg1(4), hw.Variant.OP3, 24, 256 * 256)
+    if "3" in which:
+        timed("3: 3D acoustic 512^3 2nd order fp16 op3 (beta plane)", cfg3(), hw.Variant.OP3, 34, 512 ** 3)
+    if "4" in which:
+        timed("4: 2D elastic 4096^2 free surface fp16 op6", cfg4(), hw.Variant.OP6, 40, 4096 * 4097)
+    if "5" in which:
+        timed("5: 3D elastic 512^3 2nd order fp16 op6", cfg5(), hw.Variant.OP6, 72, 512 ** 3)
