@@ -117,6 +117,23 @@ int hw_field_shape(const hw_desc* d, int32_t field, int64_t shape[3]);
 int hw_create(const hw_desc* desc, hw_solver** out);
 int hw_destroy(hw_solver* h);
 
+/* Slab decomposition over the slow axis.  Two transports:
+ *  - one process per GPU: desc->world_size > 1, desc->rank, desc->device and a
+ *    128-byte ncclUniqueId (from hw_nccl_unique_id on rank 0, broadcast by the
+ *    host) -> hw_create; halo slabs move by NCCL send/recv after each phase and
+ *    hw_run returns the combined energy history and traces on every rank;
+ *  - one process driving nslabs slabs (on one GPU or several NVLink peers):
+ *    hw_create_group creates the nslabs handles (devices[r], or desc->device for
+ *    all when devices is NULL) and hw_run_group marches them in lockstep with
+ *    peer copies of the halo slabs.  Destroying any handle releases the group.
+ * Slab r owns global slow rows [r*ns/N, (r+1)*ns/N) (+ the extra free-surface row
+ * on the last slab); hw_set_state / hw_get_state take the global host arrays. */
+int hw_nccl_unique_id(void* out128);
+int hw_create_group(const hw_desc* desc, int32_t nslabs, const int32_t* devices, hw_solver** out);
+int hw_run_group(hw_solver* const* handles, int32_t nslabs, int32_t variant, int64_t step0, int64_t nt,
+                 const double* src_samples, double* traces, double* e_times, double* e_vals,
+                 int64_t* n_energy, int64_t* fail_step, int32_t* fail_field);
+
 /* Upload / download every state field in external order.  Each pointer addresses a
  * row-major host array of lane_u storage (uint16 fp16 bits, float, or double) with
  * the field's full (global) shape; a rank > 0 of a multi-GPU job reads/writes only

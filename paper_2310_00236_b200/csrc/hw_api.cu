@@ -113,23 +113,27 @@ __global__ void k_round_plane(const double* in, T* out, int64_t n, int lane_bits
     else out[i] = in[i];
 }
 
-// Initial ghost fill (write-through keeps them current afterwards).
+// Initial ghost fill of the write-through slabs (periodic wrap or global free-surface
+// images); slabs facing another rank are filled by the halo exchange.
 template <typename T>
-__global__ void k_fill_ghosts(FieldView f, Geom g, int esize) {
+__global__ void k_fill_ghosts(FieldView f, Geom g) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t per = g.nm * g.nx;
     if (i >= 2 * G * per) return;
     int64_t q = i / per, rem = i % per;
     int64_t m = rem / g.nx, x = rem % g.nx;
-    int64_t n = f.rows;
-    int64_t k = q < G ? q - G : n + (q - G);  // -2,-1, n, n+1
+    const int64_t n = f.rows;
+    const int64_t k = q < G ? q - G : n + (q - G);  // -2,-1, n, n+1
+    const int mode = k < 0 ? f.gtop : f.gbot;
+    if (mode == GHOST_NONE) return;
     int64_t src;
     bool neg = false;
-    if (f.gmode == GHOST_PERIODIC) {
+    if (mode == GHOST_PERIODIC) {
         src = k < 0 ? k + n : k - n;
     } else {
-        if (f.half_s) src = k < 0 ? -k - 1 : 2 * n - 1 - k;
-        else src = k < 0 ? -k : 2 * n - 2 - k;
+        const int64_t kg = f.row0 + k, ng = f.nglob;
+        const int64_t sg = f.half_s ? (kg < 0 ? -kg - 1 : 2 * ng - 1 - kg) : (kg < 0 ? -kg : 2 * ng - 2 - kg);
+        src = sg - f.row0;
         neg = f.odd;
     }
     T* base = reinterpret_cast<T*>(f.base);
@@ -140,7 +144,6 @@ __global__ void k_fill_ghosts(FieldView f, Geom g, int esize) {
         else v = lane<64>::neg(v);
     }
     base[k * g.slab + m * g.pitch + x] = v;
-    (void)esize;
 }
 
 // Per-step epilogue: receiver traces (acoustic.py:217-218) and the fixed-order
@@ -151,8 +154,8 @@ __global__ void k_epilogue(EpParams E, int64_t n, int sample, int64_t eidx) {
     using TU = typename lane<LU>::T;
     if (n >= 0) {
         const TU* b = reinterpret_cast<const TU*>(E.trace_base);
-        for (int j = threadIdx.x; j < E.n_rec; j += blockDim.x)
-            E.traces[(int64_t)j * E.nt + n] = lane<LU>::to_f64(b[E.rec_off[j]]);
+        for (int j = threadIdx.x; j < E.n_rec; j += blockDim.x)  // receivers of this slab only
+            if (E.rec_off[j] >= 0) E.traces[(int64_t)j * E.nt + n] = lane<LU>::to_f64(b[E.rec_off[j]]);
     }
     if (!sample) return;
     __shared__ double red[NCOMP][256];
@@ -250,7 +253,53 @@ void launch_epilogue(int LU, const EpParams& E, int64_t n, int sample, int64_t e
 }
 }  // namespace hw
 
+// ---------------------------------------------------------------- NCCL (loaded on demand)
+// Multi-process runs exchange halo slabs with NCCL send/recv over NVLink.  The
+// library resolves NCCL with dlopen only when world_size > 1, so single-GPU and
+// in-process slab groups carry no NCCL dependency.
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace {
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+    ncclResult_t (*CommDestroy)(ncclComm_t);
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    ncclResult_t (*GroupStart)();
+    ncclResult_t (*GroupEnd)();
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t);
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+    const char* (*GetErrorString)(ncclResult_t);
+};
+NcclApi g_nccl;
+
+int nccl_load() {
+    if (g_nccl.ok) return HW_OK;
+    void* lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) return fail(HW_ENCCL, std::string("cannot load libnccl.so.2: ") + dlerror());
+#define SYM(name) *(void**)(&g_nccl.name) = dlsym(lib, "nccl" #name); if (!g_nccl.name) return fail(HW_ENCCL, "missing nccl" #name)
+    SYM(GetUniqueId); SYM(CommInitRank); SYM(CommDestroy); SYM(Send); SYM(Recv); SYM(GroupStart);
+    SYM(GroupEnd); SYM(AllReduce); SYM(AllGather); SYM(Broadcast); SYM(GetErrorString);
+#undef SYM
+    g_nccl.ok = true;
+    return HW_OK;
+}
+
+#define NC(call)                                                                              \
+    do {                                                                                      \
+        ncclResult_t r_ = (call);                                                             \
+        if (r_ != ncclSuccess) return fail(HW_ENCCL, std::string(#call) + ": " + g_nccl.GetErrorString(r_)); \
+    } while (0)
+}  // namespace
+
 // ---------------------------------------------------------------- the handle
+
+struct hw_group;
 
 struct hw_solver {
     hw_desc d;
@@ -263,6 +312,7 @@ struct hw_solver {
     PlaneView lp[HW_NPLANES];
     Plane64 ep64[HW_NPLANES];
     Ctrl* ctrl = nullptr;
+    bool owns_ctrl = true;
     double* partials = nullptr;
     int64_t nblocks = 0;
     int64_t max_rows = 0;
@@ -275,6 +325,7 @@ struct hw_solver {
     unsigned int res_bad = 0;   // residual fields holding non-finite values at upload
     cudaStream_t st = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev_phase = nullptr, ev_copied = nullptr;
     int64_t launches = 0;
     double kernel_ms = 0.0;
     double dt_u = 0.0;
@@ -282,11 +333,38 @@ struct hw_solver {
     bool fused = false;
     int fused_blocks = 0;
     void* mem_b[2 * F_N] = {};
+    // slab decomposition over the slow axis
+    int world = 1, rank = 0;
+    int64_t r0 = 0, ns_loc = 0;
+    int transport = 0;  // 0 single domain, 1 in-process slab group, 2 NCCL
+    hw_group* group = nullptr;
+    ncclComm_t nccl = nullptr;
+    int src_active = 0;
+    int64_t src_s_loc = 0;
+    std::vector<int> rec_owned;  // receiver j lives on this slab
+};
+
+struct hw_group {
+    std::vector<hw_solver*> ranks;
 };
 
 namespace {
 
-int64_t field_rows(const hw_solver* h, int f) { return h->d.ns + ((h->fs && !HALF_S[f]) ? 1 : 0); }
+int64_t nglob_rows(const hw_solver* h, int f) { return h->d.ns + ((h->fs && !HALF_S[f]) ? 1 : 0); }
+
+int64_t field_rows(const hw_solver* h, int f) {
+    return h->ns_loc + ((h->fs && !HALF_S[f] && h->rank == h->world - 1) ? 1 : 0);
+}
+
+// fields read by a slow-axis derivative: they need ghost slabs (stencil.py ddy_*)
+bool needs_ghosts(const hw_solver* h, int f) {
+    if (h->ac) return f == F_P || f == F_VS;
+    return f == F_VX || f == F_VS || f == F_VM || f == F_SXS || f == F_SSS || f == F_SMS;
+}
+bool is_velocity(int f) { return f == F_VX || f == F_VS || f == F_VM; }
+
+int prev_rank(const hw_solver* h) { return h->rank > 0 ? h->rank - 1 : (h->fs ? -1 : h->world - 1); }
+int next_rank(const hw_solver* h) { return h->rank < h->world - 1 ? h->rank + 1 : (h->fs ? -1 : 0); }
 
 int plane_lane(const hw_solver* h, int pl) {
     switch (pl) {
@@ -296,7 +374,7 @@ int plane_lane(const hw_solver* h, int pl) {
     }
 }
 
-// rows of the field each plane is shaped like (0 = plane unused)
+// local rows of the field each plane is shaped like (0 = plane unused)
 int64_t plane_rows(const hw_solver* h, int pl) {
     bool el = !h->ac;
     switch (pl) {
@@ -311,16 +389,17 @@ int64_t plane_rows(const hw_solver* h, int pl) {
     return 0;
 }
 
-// Upload one fp64 plane, compressed to constant / slow-layered / full, plus its lane copy.
+// Upload this slab's rows of one fp64 plane, compressed to constant / slow-layered /
+// full, plus its lane copy and (binary16 divisors) its division mode.
 int upload_plane(hw_solver* h, int pl) {
     int64_t rows = plane_rows(h, pl);
     h->lp[pl] = PlaneView{nullptr, nullptr, 0, 0, 0, 0, 0};
     h->ep64[pl] = Plane64{nullptr, 0, 0, 0};
     if (!rows) return HW_OK;
-    const double* src = h->d.plane[pl];
-    if (!src) return fail(HW_EINVAL, "medium plane " + std::to_string(pl) + " missing");
     int64_t nm = pl == HW_PL_EP ? 1 : h->d.nm, nx = h->d.nx;
     int64_t per = nm * nx, n = rows * per;
+    if (!h->d.plane[pl]) return fail(HW_EINVAL, "medium plane " + std::to_string(pl) + " missing");
+    const double* src = h->d.plane[pl] + (pl == HW_PL_EP ? 0 : h->r0 * per);
     bool cst = true, layered = true;
     for (int64_t i = 1; i < n && cst; i++) cst = memcmp(&src[i], &src[0], 8) == 0;
     if (!cst)
@@ -402,8 +481,8 @@ void fill_params(const hw_solver* h, AcParams& P) {
     P.k = make_consts(h->d.taps, h->dt_u);
     P.order = h->d.order;
     P.d3 = h->d3;
-    P.has_src = h->d.src_kind == HW_SRC_PRESSURE;
-    P.src_x = h->d.src_x; P.src_m = h->d.src_m; P.src_s = h->d.src_s;
+    P.has_src = h->d.src_kind == HW_SRC_PRESSURE && h->src_active;
+    P.src_x = h->d.src_x; P.src_m = h->d.src_m; P.src_s = h->src_s_loc;
     P.ctrl = h->ctrl;
     P.partials = h->partials;
 }
@@ -425,8 +504,8 @@ void fill_params(const hw_solver* h, ElParams& P) {
     P.order = h->d.order;
     P.d3 = h->d3;
     P.fs = h->fs;
-    P.src_kind = h->d.src_kind;
-    P.src_x = h->d.src_x; P.src_m = h->d.src_m; P.src_s = h->d.src_s;
+    P.src_kind = h->src_active ? h->d.src_kind : HW_SRC_NONE;
+    P.src_x = h->d.src_x; P.src_m = h->d.src_m; P.src_s = h->src_s_loc;
     P.ctrl = h->ctrl;
     P.partials = h->partials;
 }
@@ -446,9 +525,227 @@ int check_desc(const hw_desc* d) {
     if (d->bc_slow != HW_BC_PERIODIC && d->bc_slow != HW_BC_FREE_SURFACE) return fail(HW_EINVAL, "bad bc");
     if (d->energy_every < 1) return fail(HW_EINVAL, "energy_every must be at least 1");
     if (!(d->dx > 0.0) || !(d->dt > 0.0)) return fail(HW_EINVAL, "dx and dt must be positive");
-    if (d->world_size != 1) return fail(HW_EINVAL, "world_size > 1 requires the NCCL build");
+    if (d->world_size < 1 || d->rank < 0 || d->rank >= d->world_size) return fail(HW_EINVAL, "bad world_size/rank");
+    if (d->world_size > 1 && d->ns / d->world_size < 4) return fail(HW_EINVAL, "slabs need at least 4 rows per rank");
     if (d->n_receivers < 0 || (d->n_receivers > 0 && !d->receivers)) return fail(HW_EINVAL, "bad receivers");
     return HW_OK;
+}
+
+// The slab's field buffers, ghost policies, medium, source and receivers.
+int setup_handle(hw_solver* h) {
+    const hw_desc* desc = &h->d;
+    int rc;
+    CU(cudaSetDevice(desc->device));
+    h->LS = desc->lane_s;
+    h->LU = desc->lane_u;
+    h->W = (desc->nx % 2 == 0) ? 2 : 1;
+    h->d3 = desc->ndim == 3;
+    h->fs = desc->bc_slow == HW_BC_FREE_SURFACE;
+    h->ac = desc->equation == HW_EQ_ACOUSTIC;
+    h->ext = ext_order(desc->equation, desc->ndim, &h->nsol);
+    h->dt_u = round_lane(h->LU, desc->dt);
+    h->r0 = (int64_t)h->rank * desc->ns / h->world;
+    h->ns_loc = (int64_t)(h->rank + 1) * desc->ns / h->world - h->r0;
+    int64_t pitch = (desc->nx + 31) / 32 * 32;
+    h->g = Geom{desc->nx, desc->nm, pitch, desc->nm * pitch};
+    CU(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking));
+    CU(cudaEventCreate(&h->ev0));
+    CU(cudaEventCreate(&h->ev1));
+    CU(cudaEventCreateWithFlags(&h->ev_phase, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&h->ev_copied, cudaEventDisableTiming));
+    const int esz = lane_bytes(h->LU);
+    int64_t max_rows = 0;
+    const bool top_image = h->fs && h->rank == 0, bot_image = h->fs && h->rank == h->world - 1;
+    for (int j = 0; j < 2 * h->nsol; j++) {
+        int f = h->ext[j % h->nsol];
+        bool resid = j >= h->nsol;
+        int64_t rows = field_rows(h, f);
+        max_rows = rows > max_rows ? rows : max_rows;
+        size_t bytes = (size_t)(rows + 2 * G) * h->g.slab * esz;
+        void* p = nullptr;
+        if (cudaMalloc(&p, bytes) != cudaSuccess) return fail(HW_ECUDA, "out of device memory for fields");
+        CU(cudaMemset(p, 0, bytes));
+        h->mem[j] = p;
+        FieldView fv;
+        memset(&fv, 0, sizeof(fv));
+        fv.base = (char*)p + (size_t)G * h->g.slab * esz;
+        fv.rows = rows;
+        fv.row0 = h->r0;
+        fv.nglob = nglob_rows(h, f);
+        fv.half_s = HALF_S[f];
+        fv.bit = j;
+        fv.gtop = fv.gbot = GHOST_NONE;
+        if (!resid && needs_ghosts(h, f)) {
+            // parity of the image: odd for sxy/syy (elastic.py:186-189), even for vx/vy (:210-236)
+            fv.odd = (f == F_SXS || f == F_SSS) ? 1 : 0;
+            if (h->world == 1 && !h->fs) fv.gtop = fv.gbot = GHOST_PERIODIC;
+            if (top_image) fv.gtop = GHOST_IMAGE;
+            if (bot_image) fv.gbot = GHOST_IMAGE;
+        }
+        (resid ? h->rv : h->fv)[f] = fv;
+    }
+    for (int pl = 0; pl < HW_NPLANES; pl++)
+        if ((rc = upload_plane(h, pl))) return rc;
+    {
+        const char* path = getenv("HALFWAVE_PATH");
+        bool want = !(path && strcmp(path, "generic") == 0);
+        int dev_smem = 0, nsm = 0;
+        cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, desc->device);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, desc->device);
+        if (want && h->ac && !h->d3 && h->LS == 16 && h->LU == 16 && h->world == 1 &&
+            fused2d_eligible(desc->nx, dev_smem)) {
+            for (int j = 0; j < 2 * h->nsol; j++) {
+                int f = h->ext[j % h->nsol];
+                size_t bytes = (size_t)(field_rows(h, f) + 2 * G) * h->g.slab * esz;
+                if (cudaMalloc(&h->mem_b[j], bytes) != cudaSuccess) return fail(HW_ECUDA, "out of memory (B)");
+                CU(cudaMemset(h->mem_b[j], 0, bytes));
+            }
+            if (fused2d_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "fused kernel setup failed");
+            int64_t nbf = desc->ns / 4;
+            if (nbf < 1) nbf = 1;
+            h->fused_blocks = (int)(nbf < nsm ? nbf : nsm);
+            h->fused = true;
+        }
+    }
+    if (!h->ctrl) CU(cudaMalloc(&h->ctrl, sizeof(Ctrl)));
+    h->max_rows = max_rows;
+    h->nblocks = grid_blocks(h->g, h->W, max_rows);
+    CU(cudaMalloc(&h->partials, h->nblocks * NCOMP * sizeof(double)));
+    // the point source belongs to the slab holding its row
+    int srcf = desc->src_kind == HW_SRC_PRESSURE ? F_P : (desc->src_kind == HW_SRC_VSLOW ? F_VS : F_SXX);
+    if (desc->src_kind != HW_SRC_NONE && desc->src_s >= h->r0 && desc->src_s < h->r0 + field_rows(h, srcf)) {
+        h->src_active = 1;
+        h->src_s_loc = desc->src_s - h->r0;
+    }
+    if (desc->n_receivers > 0) {
+        int f = h->ac ? F_P : F_VS;
+        std::vector<int64_t> off(desc->n_receivers), xyz(3 * desc->n_receivers);
+        h->rec_owned.assign(desc->n_receivers, 0);
+        for (int j = 0; j < desc->n_receivers; j++) {
+            const int64_t* r = desc->receivers + 3 * j;
+            if (r[0] < 0 || r[0] >= desc->nx || r[1] < 0 || r[1] >= desc->nm || r[2] < 0 || r[2] >= nglob_rows(h, f))
+                return fail(HW_EINVAL, "receiver outside the grid");
+            const int64_t sl = r[2] - h->r0;
+            const bool own = sl >= 0 && sl < field_rows(h, f);
+            h->rec_owned[j] = own;
+            off[j] = own ? sl * h->g.slab + r[1] * h->g.pitch + r[0] : -1;
+            xyz[3 * j] = r[0];
+            xyz[3 * j + 1] = r[1];
+            xyz[3 * j + 2] = own ? sl : -1000000;
+        }
+        CU(cudaMalloc(&h->rec_off, off.size() * 8));
+        CU(cudaMemcpy(h->rec_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
+        CU(cudaMalloc(&h->rec_xyz, xyz.size() * 8));
+        CU(cudaMemcpy(h->rec_xyz, xyz.data(), xyz.size() * 8, cudaMemcpyHostToDevice));
+    }
+    CU(cudaDeviceSynchronize());
+    return HW_OK;
+}
+
+void release_handle(hw_solver* h) {
+    cudaSetDevice(h->d.device);
+    for (void* p : h->mem) if (p) cudaFree(p);
+    for (void* p : h->mem_b) if (p) cudaFree(p);
+    for (void* p : h->plane_mem) cudaFree(p);
+    if (h->ctrl && h->owns_ctrl) cudaFree(h->ctrl);
+    if (h->partials) cudaFree(h->partials);
+    if (h->traces) cudaFree(h->traces);
+    if (h->evals) cudaFree(h->evals);
+    if (h->rec_off) cudaFree(h->rec_off);
+    if (h->rec_xyz) cudaFree(h->rec_xyz);
+    if (h->ev0) cudaEventDestroy(h->ev0);
+    if (h->ev1) cudaEventDestroy(h->ev1);
+    if (h->ev_phase) cudaEventDestroy(h->ev_phase);
+    if (h->ev_copied) cudaEventDestroy(h->ev_copied);
+    if (h->st) cudaStreamDestroy(h->st);
+    if (h->nccl && g_nccl.ok) g_nccl.CommDestroy(h->nccl);
+    delete h;
+}
+
+// ---------------------------------------------------------------- halo exchange
+// Phase 0 (after the velocity kernels) ships the velocity fields with slow-axis
+// derivatives, phase 1 (after the pressure / stress kernels) the rest.  Each field
+// sends its G boundary slabs: bottom rows -> next rank's top ghosts, top rows ->
+// previous rank's bottom ghosts (free surfaces: the global ends keep their images).
+struct Xfer {
+    void* src_bottom;  // rows [n-G, n)
+    void* src_top;     // rows [0, G)
+    void* dst_top;     // ghost rows [-G, 0)
+    void* dst_bottom;  // ghost rows [n, n+G)
+    size_t bytes;
+};
+
+std::vector<Xfer> xfers(const hw_solver* h, int phase) {
+    std::vector<Xfer> out;
+    const size_t esz = lane_bytes(h->LU);
+    for (int j = 0; j < h->nsol; j++) {
+        const int f = h->ext[j];
+        if (!needs_ghosts(h, f) || is_velocity(f) != (phase == 0)) continue;
+        const FieldView& fv = h->fv[f];
+        const size_t row = (size_t)h->g.slab * esz;
+        char* b = (char*)fv.base;
+        out.push_back(Xfer{b + (fv.rows - G) * row, b, b - G * row, b + fv.rows * row, G * row});
+    }
+    return out;
+}
+
+int exchange_nccl(hw_solver* h, int phase) {
+    const int pv = prev_rank(h), nx_ = next_rank(h);
+    std::vector<Xfer> xs = xfers(h, phase);
+    NC(g_nccl.GroupStart());
+    for (const Xfer& x : xs) {  // canonical order: bottom->next / top ghost<-prev, then the reverse
+        if (nx_ >= 0) NC(g_nccl.Send(x.src_bottom, x.bytes, ncclInt8, nx_, h->nccl, h->st));
+        if (pv >= 0) NC(g_nccl.Recv(x.dst_top, x.bytes, ncclInt8, pv, h->nccl, h->st));
+    }
+    for (const Xfer& x : xs) {
+        if (pv >= 0) NC(g_nccl.Send(x.src_top, x.bytes, ncclInt8, pv, h->nccl, h->st));
+        if (nx_ >= 0) NC(g_nccl.Recv(x.dst_bottom, x.bytes, ncclInt8, nx_, h->nccl, h->st));
+    }
+    NC(g_nccl.GroupEnd());
+    return HW_OK;
+}
+
+// In-process slab group: every rank pulls its ghosts from its neighbours' slabs with
+// peer copies ordered by events (works on one GPU or across NVLink peers).
+int exchange_group(hw_group* grp, int phase) {
+    for (hw_solver* h : grp->ranks) {
+        CU(cudaSetDevice(h->d.device));
+        CU(cudaEventRecord(h->ev_phase, h->st));
+    }
+    for (hw_solver* b : grp->ranks) {
+        CU(cudaSetDevice(b->d.device));
+        const int pv = prev_rank(b), nx_ = next_rank(b);
+        std::vector<Xfer> mine = xfers(b, phase);
+        if (pv >= 0) {
+            hw_solver* a = grp->ranks[pv];
+            CU(cudaStreamWaitEvent(b->st, a->ev_phase, 0));
+            std::vector<Xfer> theirs = xfers(a, phase);
+            for (size_t k = 0; k < mine.size(); k++)
+                CU(cudaMemcpyPeerAsync(mine[k].dst_top, b->d.device, theirs[k].src_bottom, a->d.device, mine[k].bytes, b->st));
+        }
+        if (nx_ >= 0) {
+            hw_solver* a = grp->ranks[nx_];
+            CU(cudaStreamWaitEvent(b->st, a->ev_phase, 0));
+            std::vector<Xfer> theirs = xfers(a, phase);
+            for (size_t k = 0; k < mine.size(); k++)
+                CU(cudaMemcpyPeerAsync(mine[k].dst_bottom, b->d.device, theirs[k].src_top, a->d.device, mine[k].bytes, b->st));
+        }
+        CU(cudaEventRecord(b->ev_copied, b->st));
+    }
+    // a rank may overwrite its boundary rows only after its neighbours copied them
+    for (hw_solver* a : grp->ranks) {
+        CU(cudaSetDevice(a->d.device));
+        const int pv = prev_rank(a), nx_ = next_rank(a);
+        if (pv >= 0) CU(cudaStreamWaitEvent(a->st, grp->ranks[pv]->ev_copied, 0));
+        if (nx_ >= 0) CU(cudaStreamWaitEvent(a->st, grp->ranks[nx_]->ev_copied, 0));
+    }
+    return HW_OK;
+}
+
+int exchange(hw_solver* h, int phase) {
+    if (h->world == 1) return HW_OK;
+    if (h->transport == 2) return exchange_nccl(h, phase);
+    return HW_OK;  // group ranks are exchanged by the group driver
 }
 
 }  // namespace
@@ -472,120 +769,86 @@ int hw_field_shape(const hw_desc* d, int32_t field, int64_t shape[3]) {
     return HW_OK;
 }
 
+int hw_nccl_unique_id(void* out128) {
+    int rc = nccl_load();
+    if (rc) return rc;
+    ncclUniqueId id;
+    NC(g_nccl.GetUniqueId(&id));
+    memcpy(out128, &id, sizeof(id));
+    return HW_OK;
+}
+
 int hw_create(const hw_desc* desc, hw_solver** out) {
     int rc = check_desc(desc);
     if (rc) return rc;
-    CU(cudaSetDevice(desc->device));
     hw_solver* h = new hw_solver();
     h->d = *desc;
-    h->LS = desc->lane_s;
-    h->LU = desc->lane_u;
-    h->W = (desc->nx % 2 == 0) ? 2 : 1;
-    h->d3 = desc->ndim == 3;
-    h->fs = desc->bc_slow == HW_BC_FREE_SURFACE;
-    h->ac = desc->equation == HW_EQ_ACOUSTIC;
-    h->ext = ext_order(desc->equation, desc->ndim, &h->nsol);
-    h->dt_u = round_lane(h->LU, desc->dt);
-    int64_t pitch = (desc->nx + 31) / 32 * 32;
-    h->g = Geom{desc->nx, desc->nm, pitch, desc->nm * pitch};
-    auto cleanup = [&](int code) { hw_destroy(h); return code; };
-    if (cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreate(&h->ev0) != cudaSuccess || cudaEventCreate(&h->ev1) != cudaSuccess)
-        return cleanup(fail(HW_ECUDA, "stream/event creation failed"));
-    int esz = lane_bytes(h->LU);
-    int64_t max_rows = 0;
-    for (int j = 0; j < 2 * h->nsol; j++) {
-        int f = h->ext[j % h->nsol];
-        bool resid = j >= h->nsol;
-        int64_t rows = field_rows(h, f);
-        max_rows = rows > max_rows ? rows : max_rows;
-        size_t bytes = (size_t)(rows + 2 * G) * h->g.slab * esz;
-        void* p = nullptr;
-        if (cudaMalloc(&p, bytes) != cudaSuccess) return cleanup(fail(HW_ECUDA, "out of device memory for fields"));
-        cudaMemset(p, 0, bytes);
-        h->mem[j] = p;
-        FieldView fv;
-        fv.base = (char*)p + (size_t)G * h->g.slab * esz;
-        fv.rows = rows;
-        fv.half_s = HALF_S[f];
-        fv.bit = j;
-        fv.odd = 0;
-        fv.gmode = GHOST_NONE;
-        if (!resid) {
-            if (!h->fs) {
-                fv.gmode = GHOST_PERIODIC;
-            } else if (f == F_VX || f == F_VS) {
-                fv.gmode = GHOST_IMAGE;  // even parity (dvx_y, dvy: elastic.py:210-213, 233-236)
-            } else if (f == F_SXS || f == F_SSS) {
-                fv.gmode = GHOST_IMAGE;  // odd parity (dsxy_y, dsyy_y: elastic.py:186-189)
-                fv.odd = 1;
-            }
-        }
-        (resid ? h->rv : h->fv)[f] = fv;
+    h->world = desc->world_size;
+    h->rank = desc->rank;
+    if (h->world > 1) {  // one process per GPU: NCCL transport
+        if (!desc->nccl_unique_id) { release_handle(h); return fail(HW_EINVAL, "world_size > 1 needs nccl_unique_id"); }
+        if ((rc = nccl_load())) { release_handle(h); return rc; }
+        h->transport = 2;
+        CU(cudaSetDevice(desc->device));
+        ncclUniqueId id;
+        memcpy(&id, desc->nccl_unique_id, sizeof(id));
+        ncclResult_t r = g_nccl.CommInitRank(&h->nccl, h->world, id, h->rank);
+        if (r != ncclSuccess) { release_handle(h); return fail(HW_ENCCL, std::string("ncclCommInitRank: ") + g_nccl.GetErrorString(r)); }
     }
-    for (int pl = 0; pl < HW_NPLANES; pl++)
-        if ((rc = upload_plane(h, pl))) return cleanup(rc);
-    {
-        const char* path = getenv("HALFWAVE_PATH");
-        bool want = !(path && strcmp(path, "generic") == 0);
-        int dev_smem = 0, nsm = 0;
-        cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, desc->device);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, desc->device);
-        if (want && h->ac && !h->d3 && h->LS == 16 && h->LU == 16 && desc->world_size == 1 &&
-            fused2d_eligible(desc->nx, dev_smem)) {
-            for (int j = 0; j < 2 * h->nsol; j++) {
-                int f = h->ext[j % h->nsol];
-                size_t bytes = (size_t)(field_rows(h, f) + 2 * G) * h->g.slab * esz;
-                if (cudaMalloc(&h->mem_b[j], bytes) != cudaSuccess) return cleanup(fail(HW_ECUDA, "out of memory (B)"));
-                cudaMemset(h->mem_b[j], 0, bytes);
-            }
-            if (fused2d_prepare(desc->nx) != cudaSuccess) return cleanup(fail(HW_ECUDA, "fused kernel setup failed"));
-            int64_t nbf = desc->ns / 4;
-            if (nbf < 1) nbf = 1;
-            h->fused_blocks = (int)(nbf < nsm ? nbf : nsm);
-            h->fused = true;
-        }
-    }
-    if (cudaMalloc(&h->ctrl, sizeof(Ctrl)) != cudaSuccess) return cleanup(fail(HW_ECUDA, "ctrl alloc"));
-    h->max_rows = max_rows;
-    h->nblocks = grid_blocks(h->g, h->W, max_rows);
-    if (cudaMalloc(&h->partials, h->nblocks * NCOMP * sizeof(double)) != cudaSuccess)
-        return cleanup(fail(HW_ECUDA, "partials alloc"));
-    if (desc->n_receivers > 0) {
-        int f = h->ac ? F_P : F_VS;
-        std::vector<int64_t> off(desc->n_receivers);
-        for (int j = 0; j < desc->n_receivers; j++) {
-            const int64_t* r = desc->receivers + 3 * j;
-            if (r[0] < 0 || r[0] >= desc->nx || r[1] < 0 || r[1] >= desc->nm || r[2] < 0 || r[2] >= field_rows(h, f))
-                return cleanup(fail(HW_EINVAL, "receiver outside the grid"));
-            off[j] = r[2] * h->g.slab + r[1] * h->g.pitch + r[0];
-        }
-        if (cudaMalloc(&h->rec_off, off.size() * 8) != cudaSuccess) return cleanup(fail(HW_ECUDA, "rec alloc"));
-        cudaMemcpy(h->rec_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice);
-        if (cudaMalloc(&h->rec_xyz, off.size() * 24) != cudaSuccess) return cleanup(fail(HW_ECUDA, "rec alloc"));
-        cudaMemcpy(h->rec_xyz, desc->receivers, off.size() * 24, cudaMemcpyHostToDevice);
-    }
-    if (cudaDeviceSynchronize() != cudaSuccess) return cleanup(fail(HW_ECUDA, "setup failed"));
+    if ((rc = setup_handle(h))) { release_handle(h); return rc; }
     *out = h;
+    return HW_OK;
+}
+
+int hw_create_group(const hw_desc* desc, int32_t nslabs, const int32_t* devices, hw_solver** out) {
+    hw_desc d = *desc;
+    d.world_size = nslabs;
+    d.rank = 0;
+    int rc = check_desc(&d);
+    if (rc) return rc;
+    hw_group* grp = new hw_group();
+    Ctrl* shared = nullptr;
+    for (int r = 0; r < nslabs; r++) {
+        hw_solver* h = new hw_solver();
+        h->d = d;
+        h->d.rank = r;
+        h->d.device = devices ? devices[r] : desc->device;
+        h->world = nslabs;
+        h->rank = r;
+        h->transport = 1;
+        h->group = grp;
+        if (r == 0) {
+            CU(cudaSetDevice(h->d.device));
+            CU(cudaMalloc(&shared, sizeof(Ctrl)));  // one run-control block: exact failure semantics
+        } else {
+            h->owns_ctrl = false;
+            if (h->d.device != grp->ranks[0]->d.device) {
+                cudaSetDevice(h->d.device);
+                cudaDeviceEnablePeerAccess(grp->ranks[0]->d.device, 0);
+                cudaGetLastError();
+            }
+        }
+        h->ctrl = shared;
+        grp->ranks.push_back(h);
+        if ((rc = setup_handle(h))) {
+            for (hw_solver* x : grp->ranks) release_handle(x);
+            delete grp;
+            return rc;
+        }
+        out[r] = h;
+    }
     return HW_OK;
 }
 
 int hw_destroy(hw_solver* h) {
     if (!h) return HW_OK;
-    cudaSetDevice(h->d.device);
-    for (void* p : h->mem) if (p) cudaFree(p);
-    for (void* p : h->mem_b) if (p) cudaFree(p);
-    for (void* p : h->plane_mem) cudaFree(p);
-    if (h->ctrl) cudaFree(h->ctrl);
-    if (h->partials) cudaFree(h->partials);
-    if (h->traces) cudaFree(h->traces);
-    if (h->evals) cudaFree(h->evals);
-    if (h->rec_off) cudaFree(h->rec_off);
-    if (h->rec_xyz) cudaFree(h->rec_xyz);
-    if (h->ev0) cudaEventDestroy(h->ev0);
-    if (h->ev1) cudaEventDestroy(h->ev1);
-    if (h->st) cudaStreamDestroy(h->st);
-    delete h;
+    hw_group* grp = h->group;
+    if (grp) {  // destroying any rank of a group releases the whole group
+        for (hw_solver* x : grp->ranks) release_handle(x);
+        delete grp;
+        return HW_OK;
+    }
+    release_handle(h);
     return HW_OK;
 }
 
@@ -593,35 +856,36 @@ int hw_set_state(hw_solver* h, const void* const* fields) {
     CU(cudaSetDevice(h->d.device));
     int esz = lane_bytes(h->LU);
     h->res_bad = 0;
+    const size_t off = (size_t)h->r0 * h->d.nm * h->d.nx * esz;  // this slab's rows of the global arrays
     for (int j = 0; j < 2 * h->nsol; j++) {
         int f = h->ext[j % h->nsol];
         const FieldView& fv = j < h->nsol ? h->fv[f] : h->rv[f];
-        CU(cudaMemcpy2DAsync(fv.base, h->g.pitch * esz, fields[j], h->d.nx * esz, h->d.nx * esz,
-                             fv.rows * h->d.nm, cudaMemcpyHostToDevice, h->st));
+        const char* src = (const char*)fields[j] + off;
+        CU(cudaMemcpy2DAsync(fv.base, h->g.pitch * esz, src, h->d.nx * esz, h->d.nx * esz, fv.rows * h->d.nm,
+                             cudaMemcpyHostToDevice, h->st));
         if (j >= h->nsol) {  // naive runs never rewrite residuals: remember non-finite ones
             int64_t n = fv.rows * h->d.nm * h->d.nx;
             bool bad = false;
             for (int64_t i = 0; i < n && !bad; i++) {
-                double v;
-                if (esz == 2) {
-                    uint16_t b = ((const uint16_t*)fields[j])[i];
-                    bad = (b & 0x7c00) == 0x7c00;
-                    continue;
-                } else if (esz == 4) v = ((const float*)fields[j])[i];
-                else v = ((const double*)fields[j])[i];
-                bad = !std::isfinite(v);
+                if (esz == 2) bad = (((const uint16_t*)src)[i] & 0x7c00) == 0x7c00;
+                else if (esz == 4) bad = !std::isfinite(((const float*)src)[i]);
+                else bad = !std::isfinite(((const double*)src)[i]);
             }
             if (bad) h->res_bad |= 1u << j;
         }
-        if (fv.gmode != GHOST_NONE) {
+        if ((fv.gtop | fv.gbot) != GHOST_NONE) {
             int64_t nthr = 2 * G * h->d.nm * h->d.nx;
             int64_t nb = (nthr + 255) / 256;
-            if (esz == 2) k_fill_ghosts<__half><<<nb, 256, 0, h->st>>>(fv, h->g, esz);
-            else if (esz == 4) k_fill_ghosts<float><<<nb, 256, 0, h->st>>>(fv, h->g, esz);
-            else k_fill_ghosts<double><<<nb, 256, 0, h->st>>>(fv, h->g, esz);
+            if (esz == 2) k_fill_ghosts<__half><<<nb, 256, 0, h->st>>>(fv, h->g);
+            else if (esz == 4) k_fill_ghosts<float><<<nb, 256, 0, h->st>>>(fv, h->g);
+            else k_fill_ghosts<double><<<nb, 256, 0, h->st>>>(fv, h->g);
         }
     }
     CU(cudaGetLastError());
+    if (h->transport == 2) {  // ghosts facing other ranks
+        int rc;
+        if ((rc = exchange_nccl(h, 0)) || (rc = exchange_nccl(h, 1))) return rc;
+    }
     CU(cudaStreamSynchronize(h->st));
     return HW_OK;
 }
@@ -629,10 +893,11 @@ int hw_set_state(hw_solver* h, const void* const* fields) {
 int hw_get_state(hw_solver* h, void* const* fields) {
     CU(cudaSetDevice(h->d.device));
     int esz = lane_bytes(h->LU);
+    const size_t off = (size_t)h->r0 * h->d.nm * h->d.nx * esz;
     for (int j = 0; j < 2 * h->nsol; j++) {
         int f = h->ext[j % h->nsol];
         const FieldView& fv = j < h->nsol ? h->fv[f] : h->rv[f];
-        CU(cudaMemcpy2DAsync(fields[j], h->d.nx * esz, fv.base, h->g.pitch * esz, h->d.nx * esz,
+        CU(cudaMemcpy2DAsync((char*)fields[j] + off, h->d.nx * esz, fv.base, h->g.pitch * esz, h->d.nx * esz,
                              fv.rows * h->d.nm, cudaMemcpyDeviceToHost, h->st));
     }
     CU(cudaStreamSynchronize(h->st));
@@ -649,53 +914,94 @@ static int ensure(double** p, int64_t* cap, int64_t need) {
     return HW_OK;
 }
 
-// The time loop (acoustic.py:210-226 / elastic.py:271-286) on the device.
-static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src, bool energy, bool timed) {
+// Per-run setup shared by every driver: buffers, control block, kernel params, E(0).
+struct RunCtx {
+    EpParams E;
+    AcParams A;
+    ElParams L;
+    int64_t nt = 0, every = 1;
+    bool energy = false;
+    int variant = 0;
+};
+
+static int run_begin(hw_solver* h, int32_t variant, int64_t nt, bool energy, bool reset_ctrl, RunCtx& C) {
     if (variant != HW_NAIVE && variant != HW_OP3 && variant != HW_OP6) return fail(HW_EINVAL, "bad variant");
     if (nt < 0) return fail(HW_EINVAL, "nt must be nonnegative");
     CU(cudaSetDevice(h->d.device));
     int rc;
-    int64_t nrec = h->d.n_receivers;
+    const int64_t nrec = h->d.n_receivers;
     if ((rc = ensure(&h->traces, &h->traces_cap, nrec * nt > 0 ? nrec * nt : 1))) return rc;
-    int64_t ecap = 1 + nt / h->d.energy_every;
-    if ((rc = ensure(&h->evals, &h->evals_cap, ecap))) return rc;
-    Ctrl c0;
-    c0.fail_step = INT64_MAX;
-    c0.fail_mask = 0;
-    c0.pad = 0;
-    if (variant == HW_NAIVE && h->res_bad && nt > 0) {  // untouched non-finite residuals fail step 0
-        c0.fail_step = 0;
-        c0.fail_mask = h->res_bad;
+    if ((rc = ensure(&h->evals, &h->evals_cap, 1 + nt / h->d.energy_every))) return rc;
+    if (nrec * nt > 0) CU(cudaMemsetAsync(h->traces, 0, nrec * nt * sizeof(double), h->st));
+    if (reset_ctrl) {
+        Ctrl c0;
+        c0.fail_step = INT64_MAX;
+        c0.fail_mask = 0;
+        c0.pad = 0;
+        if (variant == HW_NAIVE && h->res_bad && nt > 0) {  // untouched non-finite residuals fail step 0
+            c0.fail_step = 0;
+            c0.fail_mask = h->res_bad;
+        }
+        CU(cudaMemcpyAsync(h->ctrl, &c0, sizeof(Ctrl), cudaMemcpyHostToDevice, h->st));
     }
-    CU(cudaMemcpyAsync(h->ctrl, &c0, sizeof(Ctrl), cudaMemcpyHostToDevice, h->st));
-    EpParams E;
-    memset(&E, 0, sizeof(E));
-    E.trace_base = (h->ac ? h->fv[F_P] : h->fv[F_VS]).base;
-    E.rec_off = h->rec_off;
-    E.n_rec = (int32_t)nrec;
-    E.nblocks = (int32_t)h->nblocks;
-    E.traces = h->traces;
-    E.nt = nt;
-    E.e_vals = h->evals;
-    E.scale = 0.5 * h->d.dx * h->d.dx * (h->d3 ? h->d.dx : 1.0);
-    E.partials = h->partials;
-    E.ctrl = h->ctrl;
-    AcParams A;
-    ElParams L;
-    if (h->ac) fill_params(h, A);
-    else fill_params(h, L);
-    A.variant = L.variant = variant;
-    const int LS = h->LS, LU = h->LU, W = h->W;
-    const int64_t nb = h->max_rows;  // launchers take the slow extent of the grid
-    const int64_t every = h->d.energy_every;
-    const int sk = h->d.src_kind;
-    int64_t launches = 0;
+    memset(&C.E, 0, sizeof(C.E));
+    C.E.trace_base = (h->ac ? h->fv[F_P] : h->fv[F_VS]).base;
+    C.E.rec_off = h->rec_off;
+    C.E.n_rec = (int32_t)nrec;
+    C.E.nblocks = (int32_t)h->nblocks;
+    C.E.traces = h->traces;
+    C.E.nt = nt;
+    C.E.e_vals = h->evals;
+    C.E.scale = 0.5 * h->d.dx * h->d.dx * (h->d3 ? h->d.dx : 1.0);
+    C.E.partials = h->partials;
+    C.E.ctrl = h->ctrl;
+    if (h->ac) fill_params(h, C.A);
+    else fill_params(h, C.L);
+    C.A.variant = C.L.variant = variant;
+    C.variant = variant;
+    C.nt = nt;
+    C.every = h->d.energy_every;
+    C.energy = energy;
+    h->launches = 0;
     if (energy) {  // E(t=0) pairs the state with itself
-        if (h->ac) launch_ac_energy(LU, W, A, nb, h->st);
-        else launch_el_energy(LU, W, L, nb, h->st);
-        launch_epilogue(LU, E, -1, 1, 0, h->st);
-        launches += 2;
+        if (h->ac) launch_ac_energy(h->LU, h->W, C.A, h->max_rows, h->st);
+        else launch_el_energy(h->LU, h->W, C.L, h->max_rows, h->st);
+        launch_epilogue(h->LU, C.E, -1, 1, 0, h->st);
+        h->launches += 2;
     }
+    CU(cudaGetLastError());
+    return HW_OK;
+}
+
+// one leapfrog phase (0 = velocities, 1 = pressure / stresses) of step n
+static void run_phase(hw_solver* h, const RunCtx& C, int phase, int64_t n, const double* src) {
+    const int sk = h->d.src_kind;
+    const double s = src ? src[n] : 0.0;
+    const int sample = C.energy && ((n + 1) % C.every == 0);
+    if (phase == 0) {
+        if (h->ac) launch_ac_vel(h->LS, h->LU, h->W, C.A, n, h->max_rows, h->st);
+        else launch_el_vel(h->LS, h->LU, h->W, C.L, n, sk == HW_SRC_VSLOW ? s : 0.0, h->max_rows, h->st);
+    } else {
+        if (h->ac) launch_ac_pres(h->LS, h->LU, h->W, C.A, n, sk == HW_SRC_PRESSURE ? s : 0.0, sample, h->max_rows, h->st);
+        else launch_el_stress(h->LS, h->LU, h->W, C.L, n, sk == HW_SRC_EXPLOSIVE ? s : 0.0, sample, h->max_rows, h->st);
+    }
+    h->launches++;
+}
+
+static void run_epilogue(hw_solver* h, const RunCtx& C, int64_t n) {
+    const int sample = C.energy && ((n + 1) % C.every == 0);
+    if (sample || C.E.n_rec > 0) {
+        launch_epilogue(h->LU, C.E, n, sample, (n + 1) / C.every, h->st);
+        h->launches++;
+    }
+}
+
+// The time loop (acoustic.py:210-226 / elastic.py:271-286) of one handle on the device.
+static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src, bool energy, bool timed) {
+    if (h->transport == 1) return fail(HW_EINVAL, "slab-group handles run through hw_run_group");
+    RunCtx C;
+    int rc = run_begin(h, variant, nt, energy, true, C);
+    if (rc) return rc;
     if (timed) CU(cudaEventRecord(h->ev0, h->st));
     if (h->fused) {  // one fused kernel per step, ping-pong A <-> B
         AcFusedParams F;
@@ -705,59 +1011,45 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
         F.pitch = h->g.pitch;
         const int64_t ghost = (int64_t)G * h->g.slab * 2;  // bytes before row 0
         __half* bufs[2][FUSED_NSTREAM];
-        // external order p vx vy rp rvx rvy == fused stream order
-        for (int j = 0; j < FUSED_NSTREAM; j++) {
+        for (int j = 0; j < FUSED_NSTREAM; j++) {  // external order p vx vy rp rvx rvy == stream order
             bufs[0][j] = (__half*)((char*)h->mem[j] + ghost);
             bufs[1][j] = (__half*)((char*)h->mem_b[j] + ghost);
         }
         F.rho_x = h->lp[HW_PL_RHO_X]; F.rho_s = h->lp[HW_PL_RHO_S]; F.beta = h->lp[HW_PL_BETA];
         F.e_beta = h->ep64[HW_PL_BETA]; F.e_rho_x = h->ep64[HW_PL_RHO_X]; F.e_rho_s = h->ep64[HW_PL_RHO_S];
         F.k = make_consts(h->d.taps, h->dt_u);
-        F.has_src = sk == HW_SRC_PRESSURE;
+        F.has_src = h->d.src_kind == HW_SRC_PRESSURE && h->src_active;
         F.src_x = h->d.src_x;
-        F.src_s = h->d.src_s;
-        F.n_rec = (int32_t)nrec;
+        F.src_s = h->src_s_loc;
+        F.n_rec = C.E.n_rec;
         F.rec = h->rec_xyz;
         F.traces = h->traces;
         F.nt = nt;
         F.ctrl = h->ctrl;
         F.partials = h->partials;
         F.e_vals = h->evals;
-        F.scale = E.scale;
+        F.scale = C.E.scale;
         for (int64_t n = 0; n < nt; n++) {
-            const int sample = energy && ((n + 1) % every == 0);
+            const int sample = energy && ((n + 1) % C.every == 0);
             for (int j = 0; j < FUSED_NSTREAM; j++) {
                 F.in[j] = bufs[n & 1][j];
                 F.out[j] = bufs[(n + 1) & 1][j];
             }
             launch_ac2d_fused(variant, h->d.order, F, h->fused_blocks, n, src ? src[n] : 0.0, sample,
-                              (n + 1) / every, h->st);
-            launches++;
+                              (n + 1) / C.every, h->st);
+            h->launches++;
         }
-        if (timed) CU(cudaEventRecord(h->ev1, h->st));
-        CU(cudaGetLastError());
-        h->launches = launches;
-        return HW_OK;
-    }
-    for (int64_t n = 0; n < nt; n++) {
-        const int sample = energy && ((n + 1) % every == 0);
-        const double s = src ? src[n] : 0.0;
-        if (h->ac) {
-            launch_ac_vel(LS, LU, W, A, n, nb, h->st);
-            launch_ac_pres(LS, LU, W, A, n, sk == HW_SRC_PRESSURE ? s : 0.0, sample, nb, h->st);
-        } else {
-            launch_el_vel(LS, LU, W, L, n, sk == HW_SRC_VSLOW ? s : 0.0, nb, h->st);
-            launch_el_stress(LS, LU, W, L, n, sk == HW_SRC_EXPLOSIVE ? s : 0.0, sample, nb, h->st);
-        }
-        launches += 2;
-        if (sample || nrec > 0) {
-            launch_epilogue(LU, E, n, sample, (n + 1) / every, h->st);
-            launches++;
+    } else {
+        for (int64_t n = 0; n < nt; n++) {
+            run_phase(h, C, 0, n, src);
+            if ((rc = exchange(h, 0))) return rc;
+            run_phase(h, C, 1, n, src);
+            if ((rc = exchange(h, 1))) return rc;
+            run_epilogue(h, C, n);
         }
     }
     if (timed) CU(cudaEventRecord(h->ev1, h->st));
     CU(cudaGetLastError());
-    h->launches = launches;
     return HW_OK;
 }
 
@@ -775,6 +1067,15 @@ static int fused_copy_back(hw_solver* h, int64_t executed, int32_t variant) {
     return HW_OK;
 }
 
+static void fill_times(const hw_solver* h, double* e_times, int64_t ne) {
+    if (!e_times || ne <= 0) return;
+    e_times[0] = 0.0;
+    for (int64_t k = 1; k < ne; k++) {
+        int64_t n = k * h->d.energy_every - 1;
+        e_times[k] = ((double)n + 0.5) * h->d.dt;  // local step index, as acoustic.py:226
+    }
+}
+
 int hw_run(hw_solver* h, int32_t variant, int64_t step0, int64_t nt, const double* src_samples, double* traces,
            double* e_times, double* e_vals, int64_t* n_energy, int64_t* fail_step, int32_t* fail_field) {
     if (!h) return fail(HW_EINVAL, "null solver");
@@ -784,6 +1085,19 @@ int hw_run(hw_solver* h, int32_t variant, int64_t step0, int64_t nt, const doubl
     Ctrl c;
     CU(cudaMemcpyAsync(&c, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->st));
     CU(cudaStreamSynchronize(h->st));
+    if (h->transport == 2) {  // agree on the first failure across ranks; combine energy and traces
+        Ctrl* all = nullptr;
+        CU(cudaMalloc(&all, sizeof(Ctrl) * h->world));
+        NC(g_nccl.AllGather(h->ctrl, all, sizeof(Ctrl), ncclInt8, h->nccl, h->st));
+        std::vector<Ctrl> hc(h->world);
+        CU(cudaMemcpyAsync(hc.data(), all, sizeof(Ctrl) * h->world, cudaMemcpyDeviceToHost, h->st));
+        CU(cudaStreamSynchronize(h->st));
+        cudaFree(all);
+        c.fail_step = INT64_MAX;
+        c.fail_mask = 0;
+        for (const Ctrl& x : hc) c.fail_step = x.fail_step < c.fail_step ? x.fail_step : c.fail_step;
+        for (const Ctrl& x : hc) if (x.fail_step == c.fail_step) c.fail_mask |= x.fail_mask;
+    }
     int64_t done = nt;
     int status = HW_OK;
     if (c.fail_step != INT64_MAX) {
@@ -796,18 +1110,100 @@ int hw_run(hw_solver* h, int32_t variant, int64_t step0, int64_t nt, const doubl
         g_err = "non-finite value after step " + std::to_string(step0 + c.fail_step);
     }
     if ((rc = fused_copy_back(h, done, variant))) return rc;
-    int64_t nrec = h->d.n_receivers;
+    const int64_t nrec = h->d.n_receivers;
+    const int64_t ne = energy ? 1 + (status == HW_OK ? nt / h->d.energy_every : (done - 1) / h->d.energy_every) : 0;
+    if (h->transport == 2) {
+        if (ne > 0) NC(g_nccl.AllReduce(h->evals, h->evals, ne, ncclFloat64, ncclSum, h->nccl, h->st));
+        for (int64_t j = 0; j < nrec && nt > 0; j++) {  // receiver traces from their owning slab
+            int owner = 0;
+            for (int r = 0; r < h->world; r++) {
+                int64_t r0 = (int64_t)r * h->d.ns / h->world, r1 = (int64_t)(r + 1) * h->d.ns / h->world;
+                if (h->d.receivers[3 * j + 2] >= r0 && h->d.receivers[3 * j + 2] < r1) owner = r;
+            }
+            NC(g_nccl.Broadcast(h->traces + j * nt, h->traces + j * nt, nt, ncclFloat64, owner, h->nccl, h->st));
+        }
+        CU(cudaStreamSynchronize(h->st));
+    }
     if (traces && nrec > 0 && nt > 0) CU(cudaMemcpy(traces, h->traces, nrec * nt * sizeof(double), cudaMemcpyDeviceToHost));
-    // energy samples of completed steps only: E0 + one per sample step before the failure
-    int64_t ne = energy ? 1 + (status == HW_OK ? nt / h->d.energy_every : (done - 1) / h->d.energy_every) : 0;
     if (e_vals && ne > 0) CU(cudaMemcpy(e_vals, h->evals, ne * sizeof(double), cudaMemcpyDeviceToHost));
-    if (e_times && ne > 0) {
-        e_times[0] = 0.0;
-        for (int64_t k = 1; k < ne; k++) {
-            int64_t n = k * h->d.energy_every - 1;
-            e_times[k] = ((double)n + 0.5) * h->d.dt;  // local step index, as acoustic.py:226
+    fill_times(h, e_times, ne);
+    if (n_energy) *n_energy = ne;
+    return status;
+}
+
+int hw_run_group(hw_solver* const* hs, int32_t nslabs, int32_t variant, int64_t step0, int64_t nt,
+                 const double* src_samples, double* traces, double* e_times, double* e_vals, int64_t* n_energy,
+                 int64_t* fail_step, int32_t* fail_field) {
+    if (!hs || nslabs < 1 || !hs[0]->group || (int)hs[0]->group->ranks.size() != nslabs)
+        return fail(HW_EINVAL, "hw_run_group needs the handles of one slab group");
+    hw_group* grp = hs[0]->group;
+    bool energy = e_vals != nullptr || e_times != nullptr || n_energy != nullptr;
+    std::vector<RunCtx> C(nslabs);
+    int rc;
+    for (int r = 0; r < nslabs; r++)
+        if ((rc = run_begin(grp->ranks[r], variant, nt, energy, r == 0, C[r]))) return rc;
+    if (nslabs > 1) {  // E(0) and the control reset precede every slab's first step
+        CU(cudaSetDevice(grp->ranks[0]->d.device));
+        CU(cudaEventRecord(grp->ranks[0]->ev_phase, grp->ranks[0]->st));
+        for (int r = 1; r < nslabs; r++) {
+            CU(cudaSetDevice(grp->ranks[r]->d.device));
+            CU(cudaStreamWaitEvent(grp->ranks[r]->st, grp->ranks[0]->ev_phase, 0));
         }
     }
+    for (int64_t n = 0; n < nt; n++) {
+        for (int phase = 0; phase < 2; phase++) {
+            for (hw_solver* h : grp->ranks) {
+                cudaSetDevice(h->d.device);
+                run_phase(h, C[h->rank], phase, n, src_samples);
+            }
+            if (nslabs > 1 && (rc = exchange_group(grp, phase))) return rc;
+        }
+        for (hw_solver* h : grp->ranks) {
+            cudaSetDevice(h->d.device);
+            run_epilogue(h, C[h->rank], n);
+        }
+    }
+    for (hw_solver* h : grp->ranks) {
+        CU(cudaSetDevice(h->d.device));
+        CU(cudaGetLastError());
+        CU(cudaStreamSynchronize(h->st));
+    }
+    hw_solver* h0 = grp->ranks[0];
+    Ctrl c;
+    CU(cudaSetDevice(h0->d.device));
+    CU(cudaMemcpy(&c, h0->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+    int64_t done = nt;
+    int status = HW_OK;
+    if (c.fail_step != INT64_MAX) {
+        done = c.fail_step + 1;
+        status = HW_RANGE_FAILURE;
+        int bit = 0;
+        while (bit < 32 && !((c.fail_mask >> bit) & 1u)) bit++;
+        if (fail_step) *fail_step = step0 + c.fail_step;
+        if (fail_field) *fail_field = bit;
+        g_err = "non-finite value after step " + std::to_string(step0 + c.fail_step);
+    }
+    const int64_t nrec = h0->d.n_receivers;
+    const int64_t ne = energy ? 1 + (status == HW_OK ? nt / h0->d.energy_every : (done - 1) / h0->d.energy_every) : 0;
+    std::vector<double> tmp;
+    if (e_vals && ne > 0) {  // per-slab energies summed in slab order (fixed)
+        std::fill(e_vals, e_vals + ne, 0.0);
+        tmp.resize(ne);
+        for (hw_solver* h : grp->ranks) {
+            CU(cudaSetDevice(h->d.device));
+            CU(cudaMemcpy(tmp.data(), h->evals, ne * sizeof(double), cudaMemcpyDeviceToHost));
+            for (int64_t k = 0; k < ne; k++) e_vals[k] += tmp[k];
+        }
+    }
+    if (traces && nrec > 0 && nt > 0) {
+        for (hw_solver* h : grp->ranks) {
+            CU(cudaSetDevice(h->d.device));
+            for (int64_t j = 0; j < nrec; j++)
+                if (h->rec_owned[j])
+                    CU(cudaMemcpy(traces + j * nt, h->traces + j * nt, nt * sizeof(double), cudaMemcpyDeviceToHost));
+        }
+    }
+    fill_times(h0, e_times, ne);
     if (n_energy) *n_energy = ne;
     return status;
 }

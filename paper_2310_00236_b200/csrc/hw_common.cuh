@@ -24,12 +24,16 @@ constexpr int BLOCK = 256;    // threads per block for the phase kernels
 enum GhostMode { GHOST_NONE = 0, GHOST_PERIODIC = 1, GHOST_IMAGE = 2 };
 
 struct FieldView {
-    void* base;       // element (s=0, m=0, x=0)
-    int64_t rows;     // slow-axis extent (ns or ns+1)
-    int32_t gmode;    // GhostMode for write-through
+    void* base;       // element (s=0, m=0, x=0) of this rank's slab
+    int64_t rows;     // local slow-axis extent
+    int64_t row0;     // global slow index of local row 0 (slab decomposition)
+    int64_t nglob;    // global slow-axis extent of the field (ns or ns+1)
+    int32_t gtop;     // GhostMode of the top ghost slabs (NONE = filled by the halo exchange)
+    int32_t gbot;     // GhostMode of the bottom ghost slabs
     int32_t half_s;   // field sits on the half-offset slow sub-grid
     int32_t odd;      // free-surface parity: image rows are negated
     int32_t bit;      // external field index (check_finite order) for failure masks
+    int32_t pad;
 };
 
 struct Geom {
@@ -225,25 +229,31 @@ __device__ __forceinline__ void finish(vec<LS, W> rhs, const PlaneView* div, int
     u = sm_;
 }
 
-// Store W cells of field f at (s, m, x) and keep its ghost slabs current.
+// Store W cells of field f at local row s and keep its ghost slabs current
+// ("write-through ghosts"): periodic wrap copies within a single-rank domain, or
+// free-surface image rows (stencil.py:121-144) on the ranks owning a global boundary.
+// Ghosts facing another rank are filled by the halo exchange instead.
 template <int LU, int W>
 __device__ __forceinline__ void store_field(const FieldView& f, const Geom& g, int64_t s, int64_t m, int64_t x,
                                             vec<LU, W> v) {
     using T = typename lane<LU>::T;
     vstore<LU, W>(frow<T>(f, g, s, m) + x, v);
-    if (f.gmode == GHOST_NONE) return;
-    int64_t n = f.rows;
-    if (f.gmode == GHOST_PERIODIC) {
-        if (s < G) vstore<LU, W>(frow<T>(f, g, n + s, m) + x, v);
-        if (s >= n - G) vstore<LU, W>(frow<T>(f, g, s - n, m) + x, v);
-        return;
+    if ((f.gtop | f.gbot) == GHOST_NONE) return;
+    const int64_t n = f.rows;
+    if (f.gtop == GHOST_PERIODIC && s >= n - G) vstore<LU, W>(frow<T>(f, g, s - n, m) + x, v);
+    if (f.gbot == GHOST_PERIODIC && s < G) vstore<LU, W>(frow<T>(f, g, n + s, m) + x, v);
+    if ((f.gtop | f.gbot) & GHOST_IMAGE) {
+        const vec<LU, W> w = f.odd ? vneg<LU, W>(v) : v;
+        const int64_t sg = f.row0 + s, ng = f.nglob;
+        if (f.gtop == GHOST_IMAGE) {
+            const int64_t k1 = f.half_s ? -sg - 1 : -sg;
+            if (k1 < 0 && k1 >= -G) vstore<LU, W>(frow<T>(f, g, k1 - f.row0, m) + x, w);
+        }
+        if (f.gbot == GHOST_IMAGE) {
+            const int64_t k2 = f.half_s ? 2 * ng - 1 - sg : 2 * ng - 2 - sg;
+            if (k2 >= ng && k2 < ng + G) vstore<LU, W>(frow<T>(f, g, k2 - f.row0, m) + x, w);
+        }
     }
-    vec<LU, W> w = f.odd ? vneg<LU, W>(v) : v;
-    int64_t k1, k2;
-    if (f.half_s) { k1 = -s - 1; k2 = 2 * n - 1 - s; }
-    else { k1 = -s; k2 = 2 * n - 2 - s; }
-    if (k1 < 0 && k1 >= -G) vstore<LU, W>(frow<T>(f, g, k1, m) + x, w);
-    if (k2 >= n && k2 < n + G) vstore<LU, W>(frow<T>(f, g, k2, m) + x, w);
 }
 
 // Warp-aggregated failure record: first failing step + external field bits.

@@ -120,7 +120,8 @@ __global__ void __launch_bounds__(BLOCK) k_el_stress(ElParams P, int64_t n, doub
             xtaps<LU, W>(frow<TU>(P.vx, g, s, m), x, g.nx, true, vxt);
             vec<LS, W> dvx = fold<LS, LU, W>(c, vxt, P.order);
             vec<LS, W> dvs{}, dvm{};
-            const bool surf = P.fs && (s == 0 || s == P.sxx.rows - 1);
+            const int64_t sg = P.sxx.row0 + s;  // global row: free surfaces are global rows 0 and ns
+            const bool surf = P.fs && (sg == 0 || sg == P.sxx.nglob - 1);
             if (!surf || s < P.vs.rows) {
                 staps<LU, W>(P.vs, g, s, m, x, true, P.order, vst);
                 dvs = fold<LS, LU, W>(c, vst, P.order);
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(BLOCK) k_el_stress(ElParams P, int64_t n, doub
             // sxx: fl(fl(stiff dvx) + fl(lam dvs)) [+ fl(lam dvm)]; surface rows fl(ep dvx) (elastic.py:215-221)
             vec<LS, W> a;
             if (surf) {
-                a = OS::mul(pload<LS, W>(P.ep, s == 0 ? 0 : 1, 0, x), dvx);
+                a = OS::mul(pload<LS, W>(P.ep, sg == 0 ? 0 : 1, 0, x), dvx);
             } else {
                 a = OS::add(OS::mul(stiff, dvx), OS::mul(lam, dvs));
                 if (P.d3) a = OS::add(a, OS::mul(lam, dvm));
@@ -278,7 +279,8 @@ __global__ void __launch_bounds__(BLOCK) k_el_energy(ElParams P) {
     if (xv < nxv && s < rows) {
         const int64_t x = xv * W;
         if (s < P.sxx.rows) {
-            const bool surf = P.fs && (s == 0 || s == P.sxx.rows - 1);
+            const int64_t sg = P.sxx.row0 + s;
+            const bool surf = P.fs && (sg == 0 || sg == P.sxx.nglob - 1);
             const double w = surf ? 0.5 : 1.0;
             vec<LU, W> vx = ld<LU, W>(P.vx, g, s, m, x), sxx = ld<LU, W>(P.sxx, g, s, m, x),
                        sss = ld<LU, W>(P.sss, g, s, m, x);

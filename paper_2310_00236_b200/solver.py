@@ -54,8 +54,18 @@ class _DeviceSolver:
 
     def __init__(self, grid, medium, source=None, *, stencil_precision=Precision.FP64,
                  update_precision=None, receivers=(), energy_every=DEFAULT_ENERGY_EVERY,
-                 device: int = 0):
+                 device: int = 0, slabs: int = 1, devices=None, distributed: bool = False):
+        """Extra keywords (not in the reference): `device` (CUDA ordinal); `slabs=N`
+        decomposes the slow axis into N slabs driven by this process (on `devices`,
+        default all on `device`); `distributed=True` makes this process one rank of a
+        torch.distributed job (one process per GPU, NCCL halo exchange)."""
         self._handle = None
+        self._group = None
+        self.slabs = int(slabs)
+        self.devices = list(devices) if devices is not None else None
+        self.distributed = bool(distributed)
+        if self.slabs > 1 and self.distributed:
+            raise ValueError("use either slabs= (one process) or distributed=True (one process per GPU)")
         self._validate(grid, medium, source, receivers, energy_every)
         self.grid = grid
         self.medium = medium
@@ -139,6 +149,19 @@ class _DeviceSolver:
         d.rank = 0
         d.device = self.device
         d.nccl_unique_id = None
+        if self.distributed:
+            import torch.distributed as dist
+
+            d.world_size = dist.get_world_size()
+            d.rank = dist.get_rank()
+            box = [None]
+            if d.rank == 0:
+                uid = ctypes.create_string_buffer(128)
+                _abi.check(_abi.load().hw_nccl_unique_id(uid), "hw_nccl_unique_id")
+                box[0] = uid.raw
+            dist.broadcast_object_list(box, src=0)
+            self._uid = ctypes.create_string_buffer(box[0], 128)
+            d.nccl_unique_id = ctypes.cast(self._uid, ctypes.c_void_p)
         d.energy_every = self.energy_every
         self._desc = d
 
@@ -155,15 +178,31 @@ class _DeviceSolver:
     def _lib_handle(self):
         if self._handle is None:
             lib = _abi.load()
-            h = ctypes.c_void_p()
-            _abi.check(lib.hw_create(ctypes.byref(self._desc), ctypes.byref(h)), "hw_create")
-            self._handle = h
+            if self.slabs > 1:
+                hs = (ctypes.c_void_p * self.slabs)()
+                devs = None
+                if self.devices is not None:
+                    devs = (ctypes.c_int32 * self.slabs)(*[self.devices[r % len(self.devices)] for r in range(self.slabs)])
+                _abi.check(lib.hw_create_group(ctypes.byref(self._desc), self.slabs, devs, hs), "hw_create_group")
+                self._group = hs
+                self._handle = ctypes.c_void_p(hs[0])
+            else:
+                h = ctypes.c_void_p()
+                _abi.check(lib.hw_create(ctypes.byref(self._desc), ctypes.byref(h)), "hw_create")
+                self._handle = h
         return self._handle
+
+    def _handles(self):
+        self._lib_handle()
+        if self._group is not None:
+            return [ctypes.c_void_p(h) for h in self._group]
+        return [self._handle]
 
     def close(self):
         if self._handle is not None:
-            _abi.load().hw_destroy(self._handle)
+            _abi.load().hw_destroy(self._handle)  # releases every slab of a group
             self._handle = None
+            self._group = None
 
     def __del__(self):
         try:
@@ -197,15 +236,27 @@ class _DeviceSolver:
     def _upload(self, state):
         arrs = self._field_arrays(state)
         ptrs = (ctypes.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
-        _abi.check(_abi.load().hw_set_state(self._lib_handle(), ptrs), "hw_set_state")
+        for h in self._handles():  # every slab takes its rows of the global arrays
+            _abi.check(_abi.load().hw_set_state(h, ptrs), "hw_set_state")
+        self._uploaded = arrs
 
     def _download(self, state):
         dtype = DTYPES[self.update_precision]
-        arrs = [np.empty(self.grid.shape(self._stagger_of(n)), dtype=dtype) for n in self.FIELDS]
+        if self.distributed:  # rows of other ranks keep their uploaded values
+            arrs = [a.copy() for a in self._uploaded]
+        else:
+            arrs = [np.empty(self.grid.shape(self._stagger_of(n)), dtype=dtype) for n in self.FIELDS]
         ptrs = (ctypes.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
-        _abi.check(_abi.load().hw_get_state(self._lib_handle(), ptrs), "hw_get_state")
+        for h in self._handles():
+            _abi.check(_abi.load().hw_get_state(h, ptrs), "hw_get_state")
         for name, a in zip(self.FIELDS, arrs):
             getattr(state, name).values = a
+
+    def _hw_run(self, *args):
+        lib = _abi.load()
+        if self._group is not None:
+            return lib.hw_run_group(self._group, self.slabs, *args)
+        return lib.hw_run(self._lib_handle(), *args)
 
     def _fail_name(self, j: int) -> str:
         name = self.FIELDS[j]
@@ -235,9 +286,9 @@ class _DeviceSolver:
         src = self.source_samples(state.step, 1)
         fs, ff = ctypes.c_int64(-1), ctypes.c_int32(-1)
         P = ctypes.POINTER(ctypes.c_double)
-        rc = lib.hw_run(h, variant_code(variant), state.step, 1,
-                        src.ctypes.data_as(P) if src is not None else None,
-                        None, None, None, None, ctypes.byref(fs), ctypes.byref(ff))
+        rc = self._hw_run(variant_code(variant), state.step, 1,
+                          src.ctypes.data_as(P) if src is not None else None,
+                          None, None, None, None, ctypes.byref(fs), ctypes.byref(ff))
         if rc not in (_abi.OK, _abi.RANGE_FAILURE):
             _abi.check(rc, "hw_run")
         self._download(state)
@@ -263,10 +314,10 @@ class _DeviceSolver:
         ne = ctypes.c_int64(0)
         fs, ff = ctypes.c_int64(-1), ctypes.c_int32(-1)
         P = ctypes.POINTER(ctypes.c_double)
-        rc = lib.hw_run(h, variant_code(variant), step0, nt,
-                        src.ctypes.data_as(P) if src is not None else None,
-                        traces.ctypes.data_as(P), e_times.ctypes.data_as(P), e_vals.ctypes.data_as(P),
-                        ctypes.byref(ne), ctypes.byref(fs), ctypes.byref(ff))
+        rc = self._hw_run(variant_code(variant), step0, nt,
+                          src.ctypes.data_as(P) if src is not None else None,
+                          traces.ctypes.data_as(P), e_times.ctypes.data_as(P), e_vals.ctypes.data_as(P),
+                          ctypes.byref(ne), ctypes.byref(fs), ctypes.byref(ff))
         if rc not in (_abi.OK, _abi.RANGE_FAILURE):
             _abi.check(rc, "hw_run")
         self._download(state)
