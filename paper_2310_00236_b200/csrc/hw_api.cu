@@ -882,12 +882,8 @@ int hw_set_state(hw_solver* h, const void* const* fields) {
         }
     }
     CU(cudaGetLastError());
-    if (h->transport == 2) {  // ghosts facing other ranks
-        int rc;
-        if ((rc = exchange_nccl(h, 0)) || (rc = exchange_nccl(h, 1))) return rc;
-    }
     CU(cudaStreamSynchronize(h->st));
-    return HW_OK;
+    return HW_OK;  // ghosts facing other ranks are exchanged at the start of each run
 }
 
 int hw_get_state(hw_solver* h, void* const* fields) {
@@ -1002,6 +998,7 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
     RunCtx C;
     int rc = run_begin(h, variant, nt, energy, true, C);
     if (rc) return rc;
+    if ((rc = exchange(h, 0)) || (rc = exchange(h, 1))) return rc;  // halos of the uploaded state
     if (timed) CU(cudaEventRecord(h->ev0, h->st));
     if (h->fused) {  // one fused kernel per step, ping-pong A <-> B
         AcFusedParams F;
@@ -1149,6 +1146,7 @@ int hw_run_group(hw_solver* const* hs, int32_t nslabs, int32_t variant, int64_t 
             CU(cudaSetDevice(grp->ranks[r]->d.device));
             CU(cudaStreamWaitEvent(grp->ranks[r]->st, grp->ranks[0]->ev_phase, 0));
         }
+        if ((rc = exchange_group(grp, 0)) || (rc = exchange_group(grp, 1))) return rc;  // halos of the uploaded state
     }
     for (int64_t n = 0; n < nt; n++) {
         for (int phase = 0; phase < 2; phase++) {
