@@ -1,14 +1,26 @@
-// hw_acoustic.cu — acoustic p-v leapfrog phase kernels (sm_100a).
+// hw_acoustic.cu — acoustic p-v leapfrog phase kernels (sm_100a), any lanes, 2D/3D.
 //
 // Per step n (AcousticSolver._step_work, acoustic.py:162-181):
-//   velocity phase  vx, vy(, vz) from p^n         -> k_ac_vel
-//   pressure phase  p from div v^{n+1/2} + source -> k_ac_pres (+ fused fp64 energy
+//   velocity phase  vx, v_slow(, v_mid) from p^n    -> k_ac_vel
+//   pressure phase  p from div v^{n+1/2} + source    -> k_ac_pres (+ fused fp64 energy
 //                   partials on sample steps, diagnostics.py:76-87)
-// One thread owns W consecutive x cells of one (slow, mid) row; all loads and
-// stores are W-wide and coalesced along x.
+// One thread owns W consecutive x cells of one (slow, mid) row; every tap address
+// is the thread's precomputed cell offset plus a constant (Cell, hw_common.cuh).
+// (The binary16 2D case runs in the fused single-pass kernel, hw_fused2d.cu.)
 #include "hw_params.h"
 
 namespace hw {
+
+template <int LU, int W>
+__device__ __forceinline__ void upd_store(const FieldView& f, const FieldView& rf, const Cell& c, int64_t s,
+                                          vec<LU, W> u, vec<LU, W> rr, bool comp, unsigned int& mask) {
+    store_c<LU, W>(f, c, s, u);
+    if (!vfinite<LU, W>(u)) mask |= 1u << f.bit;
+    if (comp) {
+        store_c<LU, W>(rf, c, s, rr);
+        if (!vfinite<LU, W>(rr)) mask |= 1u << rf.bit;
+    }
+}
 
 template <int LS, int LU, int W>
 __global__ void __launch_bounds__(BLOCK) k_ac_vel(AcParams P, int64_t n) {
@@ -16,58 +28,40 @@ __global__ void __launch_bounds__(BLOCK) k_ac_vel(AcParams P, int64_t n) {
     using TU = typename lane<LU>::T;
     using TS = typename lane<LS>::T;
     const Geom& g = P.g;
-    const int64_t nxv = g.nx / W;
     const int64_t xv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t m = blockIdx.y, s = blockIdx.z;
     unsigned int mask = 0;
-    if (xv < nxv && s < P.p.rows) {
-        const int64_t x = xv * W;
-        TS c[4];
+    if (xv * W < g.nx && s < P.p.rows) {
+        const Cell c = make_cell(g, s, m, xv * W);
+        TS k[4];
 #pragma unroll
-        for (int j = 0; j < 4; j++) c[j] = lconst<LS>(P.k, j);
+        for (int j = 0; j < 4; j++) k[j] = lconst<LS>(P.k, j);
         const TU dt = lconst<LU>(P.k, 4);
         const bool comp = P.variant != 0;
+        const TU* pp = fptr<TU>(P.p, c);
         vec<LU, W> t[4];
         // vx = fl(fl(ddx p / rho_x) * dt), advance (acoustic.py:167-168)
-        xtaps<LU, W>(frow<TU>(P.p, g, s, m), x, g.nx, false, t);
+        xtaps_c<LU, W>(pp, c, false, t);
         {
-            vec<LS, W> d = fold<LS, LU, W>(c, t, P.order);
-            vec<LU, W> u = vload<LU, W>(frow<TU>(P.vx, g, s, m) + x);
-            vec<LU, W> rr = comp ? vload<LU, W>(frow<TU>(P.rvx, g, s, m) + x) : vec<LU, W>{};
-            finish<LS, LU, W>(d, &P.rho_x, s, m, x, dt, P.variant, -1, 0.0, u, rr);
-            store_field<LU, W>(P.vx, g, s, m, x, u);
-            if (!vfinite<LU, W>(u)) mask |= 1u << P.vx.bit;
-            if (comp) {
-                store_field<LU, W>(P.rvx, g, s, m, x, rr);
-                if (!vfinite<LU, W>(rr)) mask |= 1u << P.rvx.bit;
-            }
+            vec<LU, W> u = vload<LU, W>(fptr<TU>(P.vx, c));
+            vec<LU, W> rr = comp ? vload<LU, W>(fptr<TU>(P.rvx, c)) : vec<LU, W>{};
+            finish<LS, LU, W>(fold<LS, LU, W>(k, t, P.order), &P.rho_x, s, m, xv * W, dt, P.variant, -1, 0.0, u, rr);
+            upd_store<LU, W>(P.vx, P.rvx, c, s, u, rr, comp, mask);
         }
         // v_slow from dds p (acoustic.py:169-170)
-        staps<LU, W>(P.p, g, s, m, x, false, P.order, t);
+        staps_c<LU, W>(pp, c, false, P.order, t);
         {
-            vec<LS, W> d = fold<LS, LU, W>(c, t, P.order);
-            vec<LU, W> u = vload<LU, W>(frow<TU>(P.vs, g, s, m) + x);
-            vec<LU, W> rr = comp ? vload<LU, W>(frow<TU>(P.rvs, g, s, m) + x) : vec<LU, W>{};
-            finish<LS, LU, W>(d, &P.rho_s, s, m, x, dt, P.variant, -1, 0.0, u, rr);
-            store_field<LU, W>(P.vs, g, s, m, x, u);
-            if (!vfinite<LU, W>(u)) mask |= 1u << P.vs.bit;
-            if (comp) {
-                store_field<LU, W>(P.rvs, g, s, m, x, rr);
-                if (!vfinite<LU, W>(rr)) mask |= 1u << P.rvs.bit;
-            }
+            vec<LU, W> u = vload<LU, W>(fptr<TU>(P.vs, c));
+            vec<LU, W> rr = comp ? vload<LU, W>(fptr<TU>(P.rvs, c)) : vec<LU, W>{};
+            finish<LS, LU, W>(fold<LS, LU, W>(k, t, P.order), &P.rho_s, s, m, xv * W, dt, P.variant, -1, 0.0, u, rr);
+            upd_store<LU, W>(P.vs, P.rvs, c, s, u, rr, comp, mask);
         }
         if (P.d3) {  // v_mid from ddm p (3D extension)
-            mtaps<LU, W>(P.p, g, s, m, x, false, P.order, t);
-            vec<LS, W> d = fold<LS, LU, W>(c, t, P.order);
-            vec<LU, W> u = vload<LU, W>(frow<TU>(P.vm, g, s, m) + x);
-            vec<LU, W> rr = comp ? vload<LU, W>(frow<TU>(P.rvm, g, s, m) + x) : vec<LU, W>{};
-            finish<LS, LU, W>(d, &P.rho_m, s, m, x, dt, P.variant, -1, 0.0, u, rr);
-            store_field<LU, W>(P.vm, g, s, m, x, u);
-            if (!vfinite<LU, W>(u)) mask |= 1u << P.vm.bit;
-            if (comp) {
-                store_field<LU, W>(P.rvm, g, s, m, x, rr);
-                if (!vfinite<LU, W>(rr)) mask |= 1u << P.rvm.bit;
-            }
+            mtaps_c<LU, W>(pp, c, false, P.order, t);
+            vec<LU, W> u = vload<LU, W>(fptr<TU>(P.vm, c));
+            vec<LU, W> rr = comp ? vload<LU, W>(fptr<TU>(P.rvm, c)) : vec<LU, W>{};
+            finish<LS, LU, W>(fold<LS, LU, W>(k, t, P.order), &P.rho_m, s, m, xv * W, dt, P.variant, -1, 0.0, u, rr);
+            upd_store<LU, W>(P.vm, P.rvm, c, s, u, rr, comp, mask);
         }
     }
     record_failure(P.ctrl, n, mask);
@@ -79,41 +73,36 @@ __global__ void __launch_bounds__(BLOCK) k_ac_pres(AcParams P, int64_t n, double
     using TU = typename lane<LU>::T;
     using TS = typename lane<LS>::T;
     const Geom& g = P.g;
-    const int64_t nxv = g.nx / W;
     const int64_t xv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t m = blockIdx.y, s = blockIdx.z;
     unsigned int mask = 0;
     double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    if (xv < nxv && s < P.p.rows) {
+    if (xv * W < g.nx && s < P.p.rows) {
         const int64_t x = xv * W;
-        TS c[4];
+        const Cell c = make_cell(g, s, m, x);
+        TS k[4];
 #pragma unroll
-        for (int j = 0; j < 4; j++) c[j] = lconst<LS>(P.k, j);
+        for (int j = 0; j < 4; j++) k[j] = lconst<LS>(P.k, j);
         const TU dt = lconst<LU>(P.k, 4);
         const bool comp = P.variant != 0;
         using OS = vops<LS, W>;
         vec<LU, W> tx[4], ts[4], tm[4];
         // divergence fl(fl(ddx vx + dds vs) + ddm vm) (acoustic.py:172-175)
-        xtaps<LU, W>(frow<TU>(P.vx, g, s, m), x, g.nx, true, tx);
-        staps<LU, W>(P.vs, g, s, m, x, true, P.order, ts);
-        vec<LS, W> div = OS::add(fold<LS, LU, W>(c, tx, P.order), fold<LS, LU, W>(c, ts, P.order));
+        xtaps_c<LU, W>(fptr<TU>(P.vx, c), c, true, tx);
+        staps_c<LU, W>(fptr<TU>(P.vs, c), c, true, P.order, ts);
+        vec<LS, W> div = OS::add(fold<LS, LU, W>(k, tx, P.order), fold<LS, LU, W>(k, ts, P.order));
         if (P.d3) {
-            mtaps<LU, W>(P.vm, g, s, m, x, true, P.order, tm);
-            div = OS::add(div, fold<LS, LU, W>(c, tm, P.order));
+            mtaps_c<LU, W>(fptr<TU>(P.vm, c), c, true, P.order, tm);
+            div = OS::add(div, fold<LS, LU, W>(k, tm, P.order));
         }
         int src_lane = -1;
         if (P.has_src && s == P.src_s && m == P.src_m && P.src_x >= x && P.src_x < x + W)
             src_lane = (int)(P.src_x - x);
-        const vec<LU, W> p_old = vload<LU, W>(frow<TU>(P.p, g, s, m) + x);
+        const vec<LU, W> p_old = vload<LU, W>(fptr<TU>(P.p, c));
         vec<LU, W> u = p_old;
-        vec<LU, W> rr = comp ? vload<LU, W>(frow<TU>(P.rp, g, s, m) + x) : vec<LU, W>{};
+        vec<LU, W> rr = comp ? vload<LU, W>(fptr<TU>(P.rp, c)) : vec<LU, W>{};
         finish<LS, LU, W>(div, &P.beta, s, m, x, dt, P.variant, src_lane, src, u, rr);
-        store_field<LU, W>(P.p, g, s, m, x, u);
-        if (!vfinite<LU, W>(u)) mask |= 1u << P.p.bit;
-        if (comp) {
-            store_field<LU, W>(P.rp, g, s, m, x, rr);
-            if (!vfinite<LU, W>(rr)) mask |= 1u << P.rp.bit;
-        }
+        upd_store<LU, W>(P.p, P.rp, c, s, u, rr, comp, mask);
         if (sample) {  // E = dx^2/2 [sum beta p^n p^{n+1} + sum rho v^2] (diagnostics.py:76-87)
 #pragma unroll
             for (int i = 0; i < W; i++) {
@@ -139,15 +128,15 @@ template <int LU, int W>
 __global__ void __launch_bounds__(BLOCK) k_ac_energy(AcParams P) {
     using TU = typename lane<LU>::T;
     const Geom& g = P.g;
-    const int64_t nxv = g.nx / W;
     const int64_t xv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t m = blockIdx.y, s = blockIdx.z;
     double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    if (xv < nxv && s < P.p.rows) {
+    if (xv * W < g.nx && s < P.p.rows) {
         const int64_t x = xv * W;
-        vec<LU, W> p = vload<LU, W>(frow<TU>(P.p, g, s, m) + x);
-        vec<LU, W> vx = vload<LU, W>(frow<TU>(P.vx, g, s, m) + x);
-        vec<LU, W> vs = vload<LU, W>(frow<TU>(P.vs, g, s, m) + x);
+        const Cell c = make_cell(g, s, m, x);
+        vec<LU, W> p = vload<LU, W>(fptr<TU>(P.p, c));
+        vec<LU, W> vx = vload<LU, W>(fptr<TU>(P.vx, c));
+        vec<LU, W> vs = vload<LU, W>(fptr<TU>(P.vs, c));
 #pragma unroll
         for (int i = 0; i < W; i++) {
             const int64_t xi = x + i;
@@ -158,7 +147,7 @@ __global__ void __launch_bounds__(BLOCK) k_ac_energy(AcParams P) {
             e[2] += p64(P.e_rho_s, s, m, xi) * (b * b);
         }
         if (P.d3) {
-            vec<LU, W> vm = vload<LU, W>(frow<TU>(P.vm, g, s, m) + x);
+            vec<LU, W> vm = vload<LU, W>(fptr<TU>(P.vm, c));
 #pragma unroll
             for (int i = 0; i < W; i++) {
                 double a = lane<LU>::to_f64(vm.e[i]);

@@ -179,6 +179,74 @@ __device__ __forceinline__ void mtaps(const FieldView& f, const Geom& g, int64_t
     if (order == 2) { t[0] = t[1]; t[3] = t[2]; }
 }
 
+// ---------------------------------------------------------------- per-thread addressing
+// Offsets computed once per thread; every tap is then base + off + constant.
+struct Cell {
+    int64_t off;     // (s, m, x) element offset from a field's base
+    int64_t xo[5];   // x offsets of x-2 .. x+2 relative to x (periodic wrap folded in)
+    int64_t mo[5];   // mid-axis offsets of m-2 .. m+2 relative to m (periodic wrap folded in)
+    int64_t slab;    // slow-axis stride
+};
+
+__device__ __forceinline__ Cell make_cell(const Geom& g, int64_t s, int64_t m, int64_t x) {
+    Cell c;
+    c.off = s * g.slab + m * g.pitch + x;
+    c.slab = g.slab;
+#pragma unroll
+    for (int j = 0; j < 5; j++) c.xo[j] = wrap(x - 2 + j, g.nx) - x;
+#pragma unroll
+    for (int j = 0; j < 5; j++) c.mo[j] = (wrap(m - 2 + j, g.nm) - m) * g.pitch;
+    return c;
+}
+
+template <typename T>
+__device__ __forceinline__ const T* fptr(const FieldView& f, const Cell& c) {
+    return reinterpret_cast<const T*>(f.base) + c.off;
+}
+
+// x taps relative to p = &field[s][m][x]
+template <int LU, int W>
+__device__ __forceinline__ void xtaps_c(const typename lane<LU>::T* p, const Cell& c, bool to_int, vec<LU, W> t[4]) {
+    if constexpr (W == 2) {
+        vec<LU, W> a = vload<LU, W>(p + c.xo[0]);
+        vec<LU, W> b = vload<LU, W>(p);
+        vec<LU, W> d = vload<LU, W>(p + c.xo[4]);
+        if (to_int) {
+            t[0] = a; t[1] = vshift(a, b); t[2] = b; t[3] = vshift(b, d);
+        } else {
+            t[0] = vshift(a, b); t[1] = b; t[2] = vshift(b, d); t[3] = d;
+        }
+    } else {
+        const int b0 = to_int ? 0 : 1;
+#pragma unroll
+        for (int j = 0; j < 4; j++) t[j].e[0] = p[c.xo[b0 + j]];
+    }
+}
+
+template <int LU, int W>
+__device__ __forceinline__ void staps_c(const typename lane<LU>::T* p, const Cell& c, bool to_int, int order,
+                                        vec<LU, W> t[4]) {
+    const int64_t b0 = to_int ? -2 : -1;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        if (order == 2 && (j == 0 || j == 3)) continue;
+        t[j] = vload<LU, W>(p + (b0 + j) * c.slab);
+    }
+    if (order == 2) { t[0] = t[1]; t[3] = t[2]; }
+}
+
+template <int LU, int W>
+__device__ __forceinline__ void mtaps_c(const typename lane<LU>::T* p, const Cell& c, bool to_int, int order,
+                                        vec<LU, W> t[4]) {
+    const int b0 = to_int ? 0 : 1;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        if (order == 2 && (j == 0 || j == 3)) continue;
+        t[j] = vload<LU, W>(p + c.mo[b0 + j]);
+    }
+    if (order == 2) { t[0] = t[1]; t[3] = t[2]; }
+}
+
 // UpdatePipeline.increment (stepping.py:58-80) + .advance (stepping.py:82-98,
 // efsum.py:100-121) for W cells.  src_lane >= 0 marks the element holding the
 // point source, injected as round_U(src) before the division when src != 0.
@@ -252,6 +320,30 @@ __device__ __forceinline__ void store_field(const FieldView& f, const Geom& g, i
         if (f.gbot == GHOST_IMAGE) {
             const int64_t k2 = f.half_s ? 2 * ng - 1 - sg : 2 * ng - 2 - sg;
             if (k2 >= ng && k2 < ng + G) vstore<LU, W>(frow<T>(f, g, k2 - f.row0, m) + x, w);
+        }
+    }
+}
+
+// store_field with precomputed addressing (s = local slow row of the cell)
+template <int LU, int W>
+__device__ __forceinline__ void store_c(const FieldView& f, const Cell& c, int64_t s, vec<LU, W> v) {
+    using T = typename lane<LU>::T;
+    T* p = reinterpret_cast<T*>(f.base) + c.off;
+    vstore<LU, W>(p, v);
+    if ((f.gtop | f.gbot) == GHOST_NONE) return;
+    const int64_t n = f.rows;
+    if (f.gtop == GHOST_PERIODIC && s >= n - G) vstore<LU, W>(p - n * c.slab, v);
+    if (f.gbot == GHOST_PERIODIC && s < G) vstore<LU, W>(p + n * c.slab, v);
+    if ((f.gtop | f.gbot) & GHOST_IMAGE) {
+        const vec<LU, W> w = f.odd ? vneg<LU, W>(v) : v;
+        const int64_t sg = f.row0 + s, ng = f.nglob;
+        if (f.gtop == GHOST_IMAGE) {
+            const int64_t k1 = f.half_s ? -sg - 1 : -sg;
+            if (k1 < 0 && k1 >= -G) vstore<LU, W>(p + (k1 - sg) * c.slab, w);
+        }
+        if (f.gbot == GHOST_IMAGE) {
+            const int64_t k2 = f.half_s ? 2 * ng - 1 - sg : 2 * ng - 2 - sg;
+            if (k2 >= ng && k2 < ng + G) vstore<LU, W>(p + (k2 - sg) * c.slab, w);
         }
     }
 }

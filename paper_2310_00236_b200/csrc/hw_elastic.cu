@@ -12,20 +12,19 @@
 namespace hw {
 
 template <int LU, int W>
-__device__ __forceinline__ void upd_store(const FieldView& f, const FieldView& rf, const Geom& g, int64_t s,
-                                          int64_t m, int64_t x, vec<LU, W> u, vec<LU, W> rr, bool comp,
-                                          unsigned int& mask) {
-    store_field<LU, W>(f, g, s, m, x, u);
+__device__ __forceinline__ void upd_store(const FieldView& f, const FieldView& rf, const Cell& c, int64_t s,
+                                          vec<LU, W> u, vec<LU, W> rr, bool comp, unsigned int& mask) {
+    store_c<LU, W>(f, c, s, u);
     if (!vfinite<LU, W>(u)) mask |= 1u << f.bit;
     if (comp) {
-        store_field<LU, W>(rf, g, s, m, x, rr);
+        store_c<LU, W>(rf, c, s, rr);
         if (!vfinite<LU, W>(rr)) mask |= 1u << rf.bit;
     }
 }
 
 template <int LU, int W>
-__device__ __forceinline__ vec<LU, W> ld(const FieldView& f, const Geom& g, int64_t s, int64_t m, int64_t x) {
-    return vload<LU, W>(frow<typename lane<LU>::T>(f, g, s, m) + x);
+__device__ __forceinline__ vec<LU, W> ld(const FieldView& f, const Cell& c) {
+    return vload<LU, W>(fptr<typename lane<LU>::T>(f, c));
 }
 
 template <int LS, int LU, int W>
@@ -42,6 +41,7 @@ __global__ void __launch_bounds__(BLOCK) k_el_vel(ElParams P, int64_t n, double 
     unsigned int mask = 0;
     if (xv < nxv && s < rows) {
         const int64_t x = xv * W;
+        const Cell cl = make_cell(g, s, m, x);
         TS c[4];
 #pragma unroll
         for (int j = 0; j < 4; j++) c[j] = lconst<LS>(P.k, j);
@@ -49,46 +49,46 @@ __global__ void __launch_bounds__(BLOCK) k_el_vel(ElParams P, int64_t n, double 
         const bool comp = P.variant != 0;
         vec<LU, W> t[4];
         if (s < P.vx.rows) {  // vx: fl(fl(ddx sxx + dds sxy) + ddm sxm) / rho_x (elastic.py:191-194)
-            xtaps<LU, W>(frow<TU>(P.sxx, g, s, m), x, g.nx, false, t);
+            xtaps_c<LU, W>(fptr<TU>(P.sxx, cl), cl, false, t);
             vec<LS, W> a = fold<LS, LU, W>(c, t, P.order);
-            staps<LU, W>(P.sxs, g, s, m, x, true, P.order, t);
+            staps_c<LU, W>(fptr<TU>(P.sxs, cl), cl, true, P.order, t);
             a = OS::add(a, fold<LS, LU, W>(c, t, P.order));
             if (P.d3) {
-                mtaps<LU, W>(P.sxm, g, s, m, x, true, P.order, t);
+                mtaps_c<LU, W>(fptr<TU>(P.sxm, cl), cl, true, P.order, t);
                 a = OS::add(a, fold<LS, LU, W>(c, t, P.order));
             }
-            vec<LU, W> u = ld<LU, W>(P.vx, g, s, m, x);
-            vec<LU, W> rr = comp ? ld<LU, W>(P.rvx, g, s, m, x) : vec<LU, W>{};
+            vec<LU, W> u = ld<LU, W>(P.vx, cl);
+            vec<LU, W> rr = comp ? ld<LU, W>(P.rvx, cl) : vec<LU, W>{};
             finish<LS, LU, W>(a, &P.rho_x, s, m, x, dt, P.variant, -1, 0.0, u, rr);
-            upd_store<LU, W>(P.vx, P.rvx, g, s, m, x, u, rr, comp, mask);
+            upd_store<LU, W>(P.vx, P.rvx, cl, s, u, rr, comp, mask);
         }
         if (s < P.vs.rows) {  // vy: fl(fl(ddx sxy + dds syy) + ddm sms) (+ src) / rho_y (elastic.py:196-205)
-            xtaps<LU, W>(frow<TU>(P.sxs, g, s, m), x, g.nx, true, t);
+            xtaps_c<LU, W>(fptr<TU>(P.sxs, cl), cl, true, t);
             vec<LS, W> a = fold<LS, LU, W>(c, t, P.order);
-            staps<LU, W>(P.sss, g, s, m, x, false, P.order, t);
+            staps_c<LU, W>(fptr<TU>(P.sss, cl), cl, false, P.order, t);
             a = OS::add(a, fold<LS, LU, W>(c, t, P.order));
             if (P.d3) {
-                mtaps<LU, W>(P.sms, g, s, m, x, true, P.order, t);
+                mtaps_c<LU, W>(fptr<TU>(P.sms, cl), cl, true, P.order, t);
                 a = OS::add(a, fold<LS, LU, W>(c, t, P.order));
             }
             int src_lane = -1;
             if (P.src_kind == 2 && s == P.src_s && m == P.src_m && P.src_x >= x && P.src_x < x + W)
                 src_lane = (int)(P.src_x - x);
-            vec<LU, W> u = ld<LU, W>(P.vs, g, s, m, x);
-            vec<LU, W> rr = comp ? ld<LU, W>(P.rvs, g, s, m, x) : vec<LU, W>{};
+            vec<LU, W> u = ld<LU, W>(P.vs, cl);
+            vec<LU, W> rr = comp ? ld<LU, W>(P.rvs, cl) : vec<LU, W>{};
             finish<LS, LU, W>(a, &P.rho_s, s, m, x, dt, P.variant, src_lane, src, u, rr);
-            upd_store<LU, W>(P.vs, P.rvs, g, s, m, x, u, rr, comp, mask);
+            upd_store<LU, W>(P.vs, P.rvs, cl, s, u, rr, comp, mask);
             if (P.d3) {  // v_mid: fl(fl(ddx sxm + dds sms) + ddm smm) / rho_m
-                xtaps<LU, W>(frow<TU>(P.sxm, g, s, m), x, g.nx, true, t);
+                xtaps_c<LU, W>(fptr<TU>(P.sxm, cl), cl, true, t);
                 vec<LS, W> b = fold<LS, LU, W>(c, t, P.order);
-                staps<LU, W>(P.sms, g, s, m, x, true, P.order, t);
+                staps_c<LU, W>(fptr<TU>(P.sms, cl), cl, true, P.order, t);
                 b = OS::add(b, fold<LS, LU, W>(c, t, P.order));
-                mtaps<LU, W>(P.smm, g, s, m, x, false, P.order, t);
+                mtaps_c<LU, W>(fptr<TU>(P.smm, cl), cl, false, P.order, t);
                 b = OS::add(b, fold<LS, LU, W>(c, t, P.order));
-                vec<LU, W> um = ld<LU, W>(P.vm, g, s, m, x);
-                vec<LU, W> rm = comp ? ld<LU, W>(P.rvm, g, s, m, x) : vec<LU, W>{};
+                vec<LU, W> um = ld<LU, W>(P.vm, cl);
+                vec<LU, W> rm = comp ? ld<LU, W>(P.rvm, cl) : vec<LU, W>{};
                 finish<LS, LU, W>(b, &P.rho_m, s, m, x, dt, P.variant, -1, 0.0, um, rm);
-                upd_store<LU, W>(P.vm, P.rvm, g, s, m, x, um, rm, comp, mask);
+                upd_store<LU, W>(P.vm, P.rvm, cl, s, um, rm, comp, mask);
             }
         }
     }
@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(BLOCK) k_el_stress(ElParams P, int64_t n, doub
     double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
     if (xv < nxv && s < rows) {
         const int64_t x = xv * W;
+        const Cell cl = make_cell(g, s, m, x);
         TS c[4];
 #pragma unroll
         for (int j = 0; j < 4; j++) c[j] = lconst<LS>(P.k, j);
@@ -117,17 +118,17 @@ __global__ void __launch_bounds__(BLOCK) k_el_stress(ElParams P, int64_t n, doub
         const bool comp = P.variant != 0;
         vec<LU, W> t[4], vxt[4], vst[4], vmt[4];
         if (s < P.sxx.rows) {
-            xtaps<LU, W>(frow<TU>(P.vx, g, s, m), x, g.nx, true, vxt);
+            xtaps_c<LU, W>(fptr<TU>(P.vx, cl), cl, true, vxt);
             vec<LS, W> dvx = fold<LS, LU, W>(c, vxt, P.order);
             vec<LS, W> dvs{}, dvm{};
             const int64_t sg = P.sxx.row0 + s;  // global row: free surfaces are global rows 0 and ns
             const bool surf = P.fs && (sg == 0 || sg == P.sxx.nglob - 1);
             if (!surf || s < P.vs.rows) {
-                staps<LU, W>(P.vs, g, s, m, x, true, P.order, vst);
+                staps_c<LU, W>(fptr<TU>(P.vs, cl), cl, true, P.order, vst);
                 dvs = fold<LS, LU, W>(c, vst, P.order);
             }
             if (P.d3) {
-                mtaps<LU, W>(P.vm, g, s, m, x, true, P.order, vmt);
+                mtaps_c<LU, W>(fptr<TU>(P.vm, cl), cl, true, P.order, vmt);
                 dvm = fold<LS, LU, W>(c, vmt, P.order);
             }
             const vec<LS, W> stiff = pload<LS, W>(P.stiff, s, m, x);
@@ -143,11 +144,11 @@ __global__ void __launch_bounds__(BLOCK) k_el_stress(ElParams P, int64_t n, doub
                 a = OS::add(OS::mul(stiff, dvx), OS::mul(lam, dvs));
                 if (P.d3) a = OS::add(a, OS::mul(lam, dvm));
             }
-            const vec<LU, W> sxx_old = ld<LU, W>(P.sxx, g, s, m, x);
+            const vec<LU, W> sxx_old = ld<LU, W>(P.sxx, cl);
             vec<LU, W> u = sxx_old;
-            vec<LU, W> rr = comp ? ld<LU, W>(P.rsxx, g, s, m, x) : vec<LU, W>{};
+            vec<LU, W> rr = comp ? ld<LU, W>(P.rsxx, cl) : vec<LU, W>{};
             finish<LS, LU, W>(a, nullptr, s, m, x, dt, P.variant, src_lane, src, u, rr);
-            upd_store<LU, W>(P.sxx, P.rsxx, g, s, m, x, u, rr, comp, mask);
+            upd_store<LU, W>(P.sxx, P.rsxx, cl, s, u, rr, comp, mask);
             const vec<LU, W> sxx_new = u;
             // s_slow: fl(fl(lam dvx) + fl(stiff dvs)) [+ fl(lam dvm)]; surface rows: zero increment (elastic.py:223-230)
             if (surf) {
@@ -156,20 +157,20 @@ __global__ void __launch_bounds__(BLOCK) k_el_stress(ElParams P, int64_t n, doub
                 a = OS::add(OS::mul(lam, dvx), OS::mul(stiff, dvs));
                 if (P.d3) a = OS::add(a, OS::mul(lam, dvm));
             }
-            const vec<LU, W> sss_old = ld<LU, W>(P.sss, g, s, m, x);
+            const vec<LU, W> sss_old = ld<LU, W>(P.sss, cl);
             u = sss_old;
-            rr = comp ? ld<LU, W>(P.rsss, g, s, m, x) : vec<LU, W>{};
+            rr = comp ? ld<LU, W>(P.rsss, cl) : vec<LU, W>{};
             finish<LS, LU, W>(a, nullptr, s, m, x, dt, P.variant, src_lane, src, u, rr);
-            upd_store<LU, W>(P.sss, P.rsss, g, s, m, x, u, rr, comp, mask);
+            upd_store<LU, W>(P.sss, P.rsss, cl, s, u, rr, comp, mask);
             const vec<LU, W> sss_new = u;
             vec<LU, W> smm_old{}, smm_new{};
             if (P.d3) {  // s_mid: fl(fl(fl(lam dvx) + fl(lam dvs)) + fl(stiff dvm))
                 a = OS::add(OS::add(OS::mul(lam, dvx), OS::mul(lam, dvs)), OS::mul(stiff, dvm));
-                smm_old = ld<LU, W>(P.smm, g, s, m, x);
+                smm_old = ld<LU, W>(P.smm, cl);
                 u = smm_old;
-                rr = comp ? ld<LU, W>(P.rsmm, g, s, m, x) : vec<LU, W>{};
+                rr = comp ? ld<LU, W>(P.rsmm, cl) : vec<LU, W>{};
                 finish<LS, LU, W>(a, nullptr, s, m, x, dt, P.variant, src_lane, src, u, rr);
-                upd_store<LU, W>(P.smm, P.rsmm, g, s, m, x, u, rr, comp, mask);
+                upd_store<LU, W>(P.smm, P.rsmm, cl, s, u, rr, comp, mask);
                 smm_new = u;
             }
             if (sample) {  // kinetic x + strain energy at this integer-slow row (diagnostics.py:100-162)
@@ -211,43 +212,43 @@ __global__ void __launch_bounds__(BLOCK) k_el_stress(ElParams P, int64_t n, doub
         if (s < P.sxs.rows) {
             const vec<LS, W> mu = pload<LS, W>(P.mu_n, s, m, x);
             // sxy: fl(mu fl(dds vx + ddx vy)) (elastic.py:232-238)
-            staps<LU, W>(P.vx, g, s, m, x, false, P.order, t);
+            staps_c<LU, W>(fptr<TU>(P.vx, cl), cl, false, P.order, t);
             vec<LS, W> a = fold<LS, LU, W>(c, t, P.order);
-            xtaps<LU, W>(frow<TU>(P.vs, g, s, m), x, g.nx, false, vst);
+            xtaps_c<LU, W>(fptr<TU>(P.vs, cl), cl, false, vst);
             a = OS::mul(mu, OS::add(a, fold<LS, LU, W>(c, vst, P.order)));
             vec<LU, W> old[3], nw[3];
-            old[0] = ld<LU, W>(P.sxs, g, s, m, x);
+            old[0] = ld<LU, W>(P.sxs, cl);
             vec<LU, W> u = old[0];
-            vec<LU, W> rr = comp ? ld<LU, W>(P.rsxs, g, s, m, x) : vec<LU, W>{};
+            vec<LU, W> rr = comp ? ld<LU, W>(P.rsxs, cl) : vec<LU, W>{};
             finish<LS, LU, W>(a, nullptr, s, m, x, dt, P.variant, -1, 0.0, u, rr);
-            upd_store<LU, W>(P.sxs, P.rsxs, g, s, m, x, u, rr, comp, mask);
+            upd_store<LU, W>(P.sxs, P.rsxs, cl, s, u, rr, comp, mask);
             nw[0] = u;
             if (P.d3) {
                 // s_xm: fl(mu fl(ddm vx + ddx vm))
-                mtaps<LU, W>(P.vx, g, s, m, x, false, P.order, t);
+                mtaps_c<LU, W>(fptr<TU>(P.vx, cl), cl, false, P.order, t);
                 a = fold<LS, LU, W>(c, t, P.order);
-                xtaps<LU, W>(frow<TU>(P.vm, g, s, m), x, g.nx, false, t);
+                xtaps_c<LU, W>(fptr<TU>(P.vm, cl), cl, false, t);
                 a = OS::mul(mu, OS::add(a, fold<LS, LU, W>(c, t, P.order)));
-                old[1] = ld<LU, W>(P.sxm, g, s, m, x);
+                old[1] = ld<LU, W>(P.sxm, cl);
                 u = old[1];
-                rr = comp ? ld<LU, W>(P.rsxm, g, s, m, x) : vec<LU, W>{};
+                rr = comp ? ld<LU, W>(P.rsxm, cl) : vec<LU, W>{};
                 finish<LS, LU, W>(a, nullptr, s, m, x, dt, P.variant, -1, 0.0, u, rr);
-                upd_store<LU, W>(P.sxm, P.rsxm, g, s, m, x, u, rr, comp, mask);
+                upd_store<LU, W>(P.sxm, P.rsxm, cl, s, u, rr, comp, mask);
                 nw[1] = u;
                 // s_ms: fl(mu fl(dds vm + ddm vs))
-                staps<LU, W>(P.vm, g, s, m, x, false, P.order, t);
+                staps_c<LU, W>(fptr<TU>(P.vm, cl), cl, false, P.order, t);
                 a = fold<LS, LU, W>(c, t, P.order);
-                mtaps<LU, W>(P.vs, g, s, m, x, false, P.order, t);
+                mtaps_c<LU, W>(fptr<TU>(P.vs, cl), cl, false, P.order, t);
                 a = OS::mul(mu, OS::add(a, fold<LS, LU, W>(c, t, P.order)));
-                old[2] = ld<LU, W>(P.sms, g, s, m, x);
+                old[2] = ld<LU, W>(P.sms, cl);
                 u = old[2];
-                rr = comp ? ld<LU, W>(P.rsms, g, s, m, x) : vec<LU, W>{};
+                rr = comp ? ld<LU, W>(P.rsms, cl) : vec<LU, W>{};
                 finish<LS, LU, W>(a, nullptr, s, m, x, dt, P.variant, -1, 0.0, u, rr);
-                upd_store<LU, W>(P.sms, P.rsms, g, s, m, x, u, rr, comp, mask);
+                upd_store<LU, W>(P.sms, P.rsms, cl, s, u, rr, comp, mask);
                 nw[2] = u;
             }
             if (sample) {  // kinetic slow + shear energy at this half-slow row
-                vec<LU, W> vsv = ld<LU, W>(P.vs, g, s, m, x);
+                vec<LU, W> vsv = ld<LU, W>(P.vs, cl);
                 const int nsh = P.d3 ? 3 : 1;
 #pragma unroll
                 for (int i = 0; i < W; i++) {
@@ -278,14 +279,15 @@ __global__ void __launch_bounds__(BLOCK) k_el_energy(ElParams P) {
     double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
     if (xv < nxv && s < rows) {
         const int64_t x = xv * W;
+        const Cell cl = make_cell(g, s, m, x);
         if (s < P.sxx.rows) {
             const int64_t sg = P.sxx.row0 + s;
             const bool surf = P.fs && (sg == 0 || sg == P.sxx.nglob - 1);
             const double w = surf ? 0.5 : 1.0;
-            vec<LU, W> vx = ld<LU, W>(P.vx, g, s, m, x), sxx = ld<LU, W>(P.sxx, g, s, m, x),
-                       sss = ld<LU, W>(P.sss, g, s, m, x);
-            vec<LU, W> smm = P.d3 ? ld<LU, W>(P.smm, g, s, m, x) : vec<LU, W>{};
-            vec<LU, W> vm = P.d3 ? ld<LU, W>(P.vm, g, s, m, x) : vec<LU, W>{};
+            vec<LU, W> vx = ld<LU, W>(P.vx, cl), sxx = ld<LU, W>(P.sxx, cl),
+                       sss = ld<LU, W>(P.sss, cl);
+            vec<LU, W> smm = P.d3 ? ld<LU, W>(P.smm, cl) : vec<LU, W>{};
+            vec<LU, W> vm = P.d3 ? ld<LU, W>(P.vm, cl) : vec<LU, W>{};
 #pragma unroll
             for (int i = 0; i < W; i++) {
                 const int64_t xi = x + i;
@@ -317,12 +319,12 @@ __global__ void __launch_bounds__(BLOCK) k_el_energy(ElParams P) {
             }
         }
         if (s < P.sxs.rows) {
-            vec<LU, W> vs = ld<LU, W>(P.vs, g, s, m, x);
+            vec<LU, W> vs = ld<LU, W>(P.vs, cl);
             vec<LU, W> sh[3];
-            sh[0] = ld<LU, W>(P.sxs, g, s, m, x);
+            sh[0] = ld<LU, W>(P.sxs, cl);
             if (P.d3) {
-                sh[1] = ld<LU, W>(P.sxm, g, s, m, x);
-                sh[2] = ld<LU, W>(P.sms, g, s, m, x);
+                sh[1] = ld<LU, W>(P.sxm, cl);
+                sh[2] = ld<LU, W>(P.sms, cl);
             }
             const int nsh = P.d3 ? 3 : 1;
 #pragma unroll
