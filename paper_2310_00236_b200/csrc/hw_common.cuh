@@ -385,7 +385,7 @@ __device__ __forceinline__ void block_partials(double v[NCOMP], double* out) {
 // Launch shape of the phase kernels: a block covers BX x-vectors of BY consecutive
 // slow rows (so the slow-axis taps of neighbouring rows hit in L1), mid index on
 // blockIdx.y; no integer division anywhere.
-constexpr int BY = 4;
+constexpr int BY = 1;
 inline int block_threads(int64_t nxv) {
     int64_t b = (nxv + 31) / 32 * 32;
     const int64_t cap = BLOCK / BY;
