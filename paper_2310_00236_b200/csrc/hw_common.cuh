@@ -382,52 +382,24 @@ __device__ __forceinline__ void block_partials(double v[NCOMP], double* out) {
     }
 }
 
-// Launch shape of the phase kernels: a thread owns W x cells of one mid index and
-// streams RS consecutive slow rows, carrying every slow-axis tap in a register
-// queue (each row is loaded once per thread, not once per tap).  Blocks span x.
-constexpr int RS = 8;
+// Launch shape of the phase kernels: a block covers BX x-vectors of BY consecutive
+// slow rows (so the slow-axis taps of neighbouring rows hit in L1), mid index on
+// blockIdx.y; no integer division anywhere.
+constexpr int BY = 1;
 inline int block_threads(int64_t nxv) {
     int64_t b = (nxv + 31) / 32 * 32;
-    return (int)(b > BLOCK ? BLOCK : (b < 32 ? 32 : b));
+    const int64_t cap = BLOCK / BY;
+    return (int)(b > cap ? cap : (b < 32 ? 32 : b));
 }
-inline dim3 block3(const Geom& g, int W) { return dim3(block_threads(g.nx / W)); }
+inline dim3 block3(const Geom& g, int W) { return dim3(block_threads(g.nx / W), BY); }
 inline dim3 grid3(const Geom& g, int W, int64_t rows) {
     int64_t nxv = g.nx / W;
     int bt = block_threads(nxv);
-    return dim3((unsigned)((nxv + bt - 1) / bt), (unsigned)g.nm, (unsigned)((rows + RS - 1) / RS));
+    return dim3((unsigned)((nxv + bt - 1) / bt), (unsigned)g.nm, (unsigned)((rows + BY - 1) / BY));
 }
 inline int64_t grid_blocks(const Geom& g, int W, int64_t rows) {
     dim3 gr = grid3(g, W, rows);
     return (int64_t)gr.x * gr.y * gr.z;
-}
-
-// 4-deep register queue of slow rows (q[0] oldest)
-template <int L, int W>
-struct Q4 {
-    vec<L, W> q[4];
-    __device__ __forceinline__ void push(vec<L, W> v) {
-        q[0] = q[1];
-        q[1] = q[2];
-        q[2] = q[3];
-        q[3] = v;
-    }
-};
-
-// x taps of the W cells at p when the own cells are already in registers
-template <int LU, int W>
-__device__ __forceinline__ void xtaps_own(const typename lane<LU>::T* p, const Cell& c, vec<LU, W> own, bool to_int,
-                                          vec<LU, W> t[4]) {
-    if constexpr (W == 2) {
-        vec<LU, W> a = vload<LU, W>(p + c.xo[0]);
-        vec<LU, W> d = vload<LU, W>(p + c.xo[4]);
-        if (to_int) {
-            t[0] = a; t[1] = vshift(a, own); t[2] = own; t[3] = vshift(own, d);
-        } else {
-            t[0] = vshift(a, own); t[1] = own; t[2] = vshift(own, d); t[3] = d;
-        }
-    } else {
-        xtaps_c<LU, W>(p, c, to_int, t);
-    }
 }
 
 }  // namespace hw
