@@ -204,13 +204,16 @@ __device__ __forceinline__ const T* fptr(const FieldView& f, const Cell& c) {
     return reinterpret_cast<const T*>(f.base) + c.off;
 }
 
+// Tap loaders.  Every field they read is read-only within the kernel that calls
+// them (velocity kernels read p / stresses, pressure-stress kernels read v), so
+// they use the non-coherent path.
 // x taps relative to p = &field[s][m][x]
 template <int LU, int W>
 __device__ __forceinline__ void xtaps_c(const typename lane<LU>::T* p, const Cell& c, bool to_int, vec<LU, W> t[4]) {
     if constexpr (W == 2) {
-        vec<LU, W> a = vload<LU, W>(p + c.xo[0]);
-        vec<LU, W> b = vload<LU, W>(p);
-        vec<LU, W> d = vload<LU, W>(p + c.xo[4]);
+        vec<LU, W> a = vload_nc<LU, W>(p + c.xo[0]);
+        vec<LU, W> b = vload_nc<LU, W>(p);
+        vec<LU, W> d = vload_nc<LU, W>(p + c.xo[4]);
         if (to_int) {
             t[0] = a; t[1] = vshift(a, b); t[2] = b; t[3] = vshift(b, d);
         } else {
@@ -219,7 +222,7 @@ __device__ __forceinline__ void xtaps_c(const typename lane<LU>::T* p, const Cel
     } else {
         const int b0 = to_int ? 0 : 1;
 #pragma unroll
-        for (int j = 0; j < 4; j++) t[j].e[0] = p[c.xo[b0 + j]];
+        for (int j = 0; j < 4; j++) t[j].e[0] = __ldg(p + c.xo[b0 + j]);
     }
 }
 
@@ -230,7 +233,7 @@ __device__ __forceinline__ void staps_c(const typename lane<LU>::T* p, const Cel
 #pragma unroll
     for (int j = 0; j < 4; j++) {
         if (order == 2 && (j == 0 || j == 3)) continue;
-        t[j] = vload<LU, W>(p + (b0 + j) * c.slab);
+        t[j] = vload_nc<LU, W>(p + (b0 + j) * c.slab);
     }
     if (order == 2) { t[0] = t[1]; t[3] = t[2]; }
 }
@@ -242,7 +245,7 @@ __device__ __forceinline__ void mtaps_c(const typename lane<LU>::T* p, const Cel
 #pragma unroll
     for (int j = 0; j < 4; j++) {
         if (order == 2 && (j == 0 || j == 3)) continue;
-        t[j] = vload<LU, W>(p + c.mo[b0 + j]);
+        t[j] = vload_nc<LU, W>(p + c.mo[b0 + j]);
     }
     if (order == 2) { t[0] = t[1]; t[3] = t[2]; }
 }

@@ -252,6 +252,27 @@ __device__ __forceinline__ vec<L, W> vload(const typename lane<L>::T* p) {
     return r;
 }
 
+// Read-only (non-coherent) load: for fields no thread writes during the kernel,
+// so the compiler may batch them ahead of the stores to other fields.
+template <int L, int W>
+__device__ __forceinline__ vec<L, W> vload_nc(const typename lane<L>::T* p) {
+    vec<L, W> r;
+    if constexpr (W == 1) {
+        r.e[0] = __ldg(p);
+    } else if constexpr (L == 16) {
+        r.h2 = __ldg(reinterpret_cast<const __half2*>(p));
+    } else if constexpr (L == 32) {
+        float2 x = __ldg(reinterpret_cast<const float2*>(p));
+        r.e[0] = x.x;
+        r.e[1] = x.y;
+    } else {
+        double2 x = __ldg(reinterpret_cast<const double2*>(p));
+        r.e[0] = x.x;
+        r.e[1] = x.y;
+    }
+    return r;
+}
+
 template <int L, int W>
 __device__ __forceinline__ void vstore(typename lane<L>::T* p, vec<L, W> v) {
     if constexpr (W == 1) {
