@@ -11,7 +11,10 @@ from __future__ import annotations
 import ctypes
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libhalfwave_b200.so"
+import os
+
+# HALFWAVE_LIB overrides the library path (A/B measurements of alternative builds)
+LIB_PATH = Path(os.environ.get("HALFWAVE_LIB", Path(__file__).resolve().parent / "lib" / "libhalfwave_b200.so"))
 
 ABI_VERSION = 1
 
