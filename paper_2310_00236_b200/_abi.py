@@ -111,12 +111,13 @@ def load() -> ctypes.CDLL:
     lib.hw_cheap_div_table.restype = ctypes.c_int
     lib.hw_plane_div_mode.argtypes = [vp, i32]
     lib.hw_plane_div_mode.restype = ctypes.c_int
-    lib.hw_nccl_unique_id.argtypes = [vp]
-    lib.hw_nccl_unique_id.restype = ctypes.c_int
-    lib.hw_create_group.argtypes = [P(Desc), i32, P(i32), P(vp)]
-    lib.hw_create_group.restype = ctypes.c_int
-    lib.hw_run_group.argtypes = [P(vp), i32, i32, i64, i64, P(dbl), P(dbl), P(dbl), P(dbl), P(i64), P(i64), P(i32)]
-    lib.hw_run_group.restype = ctypes.c_int
+    if hasattr(lib, "hw_create_group"):  # absent only in older A/B builds
+        lib.hw_nccl_unique_id.argtypes = [vp]
+        lib.hw_nccl_unique_id.restype = ctypes.c_int
+        lib.hw_create_group.argtypes = [P(Desc), i32, P(i32), P(vp)]
+        lib.hw_create_group.restype = ctypes.c_int
+        lib.hw_run_group.argtypes = [P(vp), i32, i32, i64, i64, P(dbl), P(dbl), P(dbl), P(dbl), P(i64), P(i64), P(i32)]
+        lib.hw_run_group.restype = ctypes.c_int
     lib.hw_version.argtypes = []
     lib.hw_version.restype = ctypes.c_char_p
     for name in ("hw_create", "hw_destroy", "hw_set_state", "hw_get_state", "hw_run", "hw_run_device"):

@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(BLOCK) k_ac_vel(AcParams P, int64_t n) {
     using TS = typename lane<LS>::T;
     const Geom& g = P.g;
     const int64_t xv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t m = blockIdx.y, s = (int64_t)blockIdx.z * BY + threadIdx.y;
+    const int64_t m = blockIdx.y, s = blockIdx.z;
     unsigned int mask = 0;
     if (xv * W < g.nx && s < P.p.rows) {
         const Cell c = make_cell(g, s, m, xv * W);
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(BLOCK) k_ac_pres(AcParams P, int64_t n, double
     using TS = typename lane<LS>::T;
     const Geom& g = P.g;
     const int64_t xv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t m = blockIdx.y, s = (int64_t)blockIdx.z * BY + threadIdx.y;
+    const int64_t m = blockIdx.y, s = blockIdx.z;
     unsigned int mask = 0;
     double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
     if (xv * W < g.nx && s < P.p.rows) {
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(BLOCK) k_ac_energy(AcParams P) {
     using TU = typename lane<LU>::T;
     const Geom& g = P.g;
     const int64_t xv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t m = blockIdx.y, s = (int64_t)blockIdx.z * BY + threadIdx.y;
+    const int64_t m = blockIdx.y, s = blockIdx.z;
     double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
     if (xv * W < g.nx && s < P.p.rows) {
         const int64_t x = xv * W;

@@ -354,7 +354,7 @@ __device__ __forceinline__ void store_c(const FieldView& f, const Cell& c, int64
 // Warp-aggregated failure record: first failing step + external field bits.
 __device__ __forceinline__ void record_failure(Ctrl* ctrl, int64_t n, unsigned int mask) {
     unsigned int any = __reduce_or_sync(0xffffffffu, mask);
-    if (any && ((threadIdx.y * blockDim.x + threadIdx.x) & 31) == 0) {
+    if (any && (threadIdx.x & 31) == 0) {
         atomicMin(reinterpret_cast<unsigned long long*>(&ctrl->fail_step), (unsigned long long)n);
         atomicOr(&ctrl->fail_mask, any);
     }
@@ -367,7 +367,7 @@ __device__ __forceinline__ bool halted(const Ctrl* ctrl, int64_t n) {
 // Block-wide fp64 sum of NCOMP components; thread 0 writes the block partial.
 __device__ __forceinline__ void block_partials(double v[NCOMP], double* out) {
     __shared__ double red[BLOCK / 32][NCOMP];
-    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+    const int tid = threadIdx.x;
     int lane_id = tid & 31, warp = tid >> 5;
 #pragma unroll
     for (int c = 0; c < NCOMP; c++) {
@@ -379,26 +379,24 @@ __device__ __forceinline__ void block_partials(double v[NCOMP], double* out) {
     __syncthreads();
     if (tid < NCOMP) {
         double a = 0.0;
-        for (int w = 0; w < (int)((blockDim.x * blockDim.y) >> 5); w++) a += red[w][tid];
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) a += red[w][tid];
         const int64_t bid = ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
         out[bid * NCOMP + tid] = a;
     }
 }
 
-// Launch shape of the phase kernels: a block covers BX x-vectors of BY consecutive
-// slow rows (so the slow-axis taps of neighbouring rows hit in L1), mid index on
-// blockIdx.y; no integer division anywhere.
-constexpr int BY = 1;
+// Launch shape of the phase kernels: x vectors across blockIdx.x (one row segment
+// per block), mid index on blockIdx.y, slow index on blockIdx.z, so (s, m) stay
+// warp-uniform (uniform datapath for row addressing); no integer division.
 inline int block_threads(int64_t nxv) {
     int64_t b = (nxv + 31) / 32 * 32;
-    const int64_t cap = BLOCK / BY;
-    return (int)(b > cap ? cap : (b < 32 ? 32 : b));
+    return (int)(b > BLOCK ? BLOCK : (b < 32 ? 32 : b));
 }
-inline dim3 block3(const Geom& g, int W) { return dim3(block_threads(g.nx / W), BY); }
+inline dim3 block3(const Geom& g, int W) { return dim3(block_threads(g.nx / W)); }
 inline dim3 grid3(const Geom& g, int W, int64_t rows) {
     int64_t nxv = g.nx / W;
     int bt = block_threads(nxv);
-    return dim3((unsigned)((nxv + bt - 1) / bt), (unsigned)g.nm, (unsigned)((rows + BY - 1) / BY));
+    return dim3((unsigned)((nxv + bt - 1) / bt), (unsigned)g.nm, (unsigned)rows);
 }
 inline int64_t grid_blocks(const Geom& g, int W, int64_t rows) {
     dim3 gr = grid3(g, W, rows);

@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(BLOCK) k_el_vel(ElParams P, int64_t n, double 
     const int64_t nxv = g.nx / W;
     const int64_t rows = P.vx.rows > P.vs.rows ? P.vx.rows : P.vs.rows;
     const int64_t xv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t m = blockIdx.y, s = (int64_t)blockIdx.z * BY + threadIdx.y;
+    const int64_t m = blockIdx.y, s = blockIdx.z;
     unsigned int mask = 0;
     if (xv < nxv && s < rows) {
         const int64_t x = xv * W;
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(BLOCK) k_el_stress(ElParams P, int64_t n, doub
     const int64_t nxv = g.nx / W;
     const int64_t rows = P.sxx.rows > P.sxs.rows ? P.sxx.rows : P.sxs.rows;
     const int64_t xv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t m = blockIdx.y, s = (int64_t)blockIdx.z * BY + threadIdx.y;
+    const int64_t m = blockIdx.y, s = blockIdx.z;
     unsigned int mask = 0;
     double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
     if (xv < nxv && s < rows) {
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(BLOCK) k_el_energy(ElParams P) {
     const int64_t nxv = g.nx / W;
     const int64_t rows = P.sxx.rows > P.sxs.rows ? P.sxx.rows : P.sxs.rows;
     const int64_t xv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t m = blockIdx.y, s = (int64_t)blockIdx.z * BY + threadIdx.y;
+    const int64_t m = blockIdx.y, s = blockIdx.z;
     double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
     if (xv < nxv && s < rows) {
         const int64_t x = xv * W;
