@@ -25,7 +25,10 @@ from .grids import (
     build_layered_elastic,
     cfl_limit,
     extend_rows,
+    load_medium,
+    save_medium,
 )
+from .config import DT16, PRESETS, ConfigError, SimConfig, parse_config
 from .precision import FORMATS, Precision, round_fraction, round_to
 from .sources import RickerSpec, SourceKind, SourceSpec, ricker, sample_source
 from .stencil import StencilSpec
@@ -37,7 +40,8 @@ __all__ = [
     "StencilSpec", "TraceSeries", "Variant", "build_acoustic_from_velocity",
     "build_homogeneous_acoustic", "build_layered_acoustic", "build_layered_elastic", "cfl_limit",
     "compare_traces", "energy_drift", "extend_rows", "ricker", "round_fraction", "round_to",
-    "sample_source",
+    "sample_source", "load_medium", "save_medium", "DT16", "PRESETS", "ConfigError", "SimConfig",
+    "parse_config",
 ]
 
 __version__ = "0.1.0"

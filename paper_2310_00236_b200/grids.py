@@ -347,3 +347,48 @@ def extend_rows(plane: np.ndarray, grid, stagger: Stagger) -> np.ndarray:
     if rows == plane.shape[0]:
         return plane
     return np.concatenate([plane, plane[-1:, :]], axis=0)
+
+
+# --- WMED medium files (reference grids.py:272-318): little-endian header
+# b"WMED", u32 version 1, u32 kind, u32 nx, u32 ny; then the canonical planes of
+# the kind, each ny*nx binary64 row-major.  2D media only (the reference format).
+
+import struct as _struct
+
+_WMED = _struct.Struct("<4s4I")
+
+
+def save_medium(path, medium: Medium) -> None:
+    if medium.ndim != 2:
+        raise ValueError("the WMED format stores 2D media only")
+    with open(path, "wb") as f:
+        f.write(_WMED.pack(b"WMED", 1, medium.kind.value, medium.nx, medium.ny))
+        for name in plane_order(medium.kind, 2):
+            f.write(np.ascontiguousarray(medium.planes[name], dtype="<f8").tobytes())
+
+
+def load_medium(path) -> Medium:
+    raw = open(path, "rb").read()
+    if len(raw) < _WMED.size:
+        raise ValueError(f"{path}: truncated header")
+    magic, version, kind_code, nx, ny = _WMED.unpack_from(raw)
+    if magic != b"WMED":
+        raise ValueError(f"{path}: bad magic {magic!r}, expected b'WMED'")
+    if version != 1:
+        raise ValueError(f"{path}: unsupported version {version}")
+    try:
+        kind = MediumKind(kind_code)
+    except ValueError:
+        raise ValueError(f"{path}: unknown medium kind {kind_code}") from None
+    names = plane_order(kind, 2)
+    need = _WMED.size + len(names) * nx * ny * 8
+    if len(raw) != need:
+        raise ValueError(f"{path}: size mismatch, got {len(raw)} bytes, need {need} "
+                         f"for {len(names)} planes of {nx}x{ny}")
+    planes = {}
+    for k, name in enumerate(names):
+        off = _WMED.size + k * nx * ny * 8
+        planes[name] = np.frombuffer(raw, dtype="<f8", count=nx * ny, offset=off).reshape(ny, nx).astype(np.float64)
+    m = Medium(kind, nx, ny, planes)
+    m.validate()
+    return m
