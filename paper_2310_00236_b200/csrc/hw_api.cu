@@ -146,6 +146,25 @@ __global__ void k_fill_ghosts(FieldView f, Geom g) {
     base[k * g.slab + m * g.pitch + x] = v;
 }
 
+// Naive runs never rewrite the residual fields, so a non-finite value uploaded in
+// one of them fails step 0 (check_finite after the first step, stepping.py:101-105):
+// flag it on the device as part of the run's control block.
+template <typename T>
+__global__ void k_flag_nonfinite(const T* base, Geom g, int64_t rows, unsigned int bit, Ctrl* ctrl) {
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t m = blockIdx.y, s = blockIdx.z;
+    if (x >= g.nx || s >= rows) return;
+    const T v = base[s * g.slab + m * g.pitch + x];
+    bool bad;
+    if constexpr (sizeof(T) == 2) bad = !lane<16>::finite(v);
+    else if constexpr (sizeof(T) == 4) bad = !lane<32>::finite(v);
+    else bad = !lane<64>::finite(v);
+    if (bad) {
+        atomicMin(reinterpret_cast<unsigned long long*>(&ctrl->fail_step), 0ull);
+        atomicOr(&ctrl->fail_mask, 1u << bit);
+    }
+}
+
 // Per-step epilogue: receiver traces (acoustic.py:217-218) and the fixed-order
 // reduction of the block energy partials into one fp64 sample.
 template <int LU>
@@ -322,7 +341,6 @@ struct hw_solver {
     int64_t evals_cap = 0;
     int64_t* rec_off = nullptr;
     int64_t* rec_xyz = nullptr;
-    unsigned int res_bad = 0;   // residual fields holding non-finite values at upload
     cudaStream_t st = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t ev_phase = nullptr, ev_copied = nullptr;
@@ -855,7 +873,6 @@ int hw_destroy(hw_solver* h) {
 int hw_set_state(hw_solver* h, const void* const* fields) {
     CU(cudaSetDevice(h->d.device));
     int esz = lane_bytes(h->LU);
-    h->res_bad = 0;
     const size_t off = (size_t)h->r0 * h->d.nm * h->d.nx * esz;  // this slab's rows of the global arrays
     for (int j = 0; j < 2 * h->nsol; j++) {
         int f = h->ext[j % h->nsol];
@@ -863,16 +880,6 @@ int hw_set_state(hw_solver* h, const void* const* fields) {
         const char* src = (const char*)fields[j] + off;
         CU(cudaMemcpy2DAsync(fv.base, h->g.pitch * esz, src, h->d.nx * esz, h->d.nx * esz, fv.rows * h->d.nm,
                              cudaMemcpyHostToDevice, h->st));
-        if (j >= h->nsol) {  // naive runs never rewrite residuals: remember non-finite ones
-            int64_t n = fv.rows * h->d.nm * h->d.nx;
-            bool bad = false;
-            for (int64_t i = 0; i < n && !bad; i++) {
-                if (esz == 2) bad = (((const uint16_t*)src)[i] & 0x7c00) == 0x7c00;
-                else if (esz == 4) bad = !std::isfinite(((const float*)src)[i]);
-                else bad = !std::isfinite(((const double*)src)[i]);
-            }
-            if (bad) h->res_bad |= 1u << j;
-        }
         if ((fv.gtop | fv.gbot) != GHOST_NONE) {
             int64_t nthr = 2 * G * h->d.nm * h->d.nx;
             int64_t nb = (nthr + 255) / 256;
@@ -934,11 +941,17 @@ static int run_begin(hw_solver* h, int32_t variant, int64_t nt, bool energy, boo
         c0.fail_step = INT64_MAX;
         c0.fail_mask = 0;
         c0.pad = 0;
-        if (variant == HW_NAIVE && h->res_bad && nt > 0) {  // untouched non-finite residuals fail step 0
-            c0.fail_step = 0;
-            c0.fail_mask = h->res_bad;
-        }
         CU(cudaMemcpyAsync(h->ctrl, &c0, sizeof(Ctrl), cudaMemcpyHostToDevice, h->st));
+    }
+    if (variant == HW_NAIVE && nt > 0) {  // untouched non-finite residuals fail step 0
+        const int esz = lane_bytes(h->LU);
+        for (int j = h->nsol; j < 2 * h->nsol; j++) {
+            const FieldView& fv = h->rv[h->ext[j - h->nsol]];
+            dim3 gr((unsigned)((h->d.nx + 255) / 256), (unsigned)h->d.nm, (unsigned)fv.rows);
+            if (esz == 2) k_flag_nonfinite<__half><<<gr, 256, 0, h->st>>>((const __half*)fv.base, h->g, fv.rows, j, h->ctrl);
+            else if (esz == 4) k_flag_nonfinite<float><<<gr, 256, 0, h->st>>>((const float*)fv.base, h->g, fv.rows, j, h->ctrl);
+            else k_flag_nonfinite<double><<<gr, 256, 0, h->st>>>((const double*)fv.base, h->g, fv.rows, j, h->ctrl);
+        }
     }
     memset(&C.E, 0, sizeof(C.E));
     C.E.trace_base = (h->ac ? h->fv[F_P] : h->fv[F_VS]).base;
@@ -1137,15 +1150,16 @@ int hw_run_group(hw_solver* const* hs, int32_t nslabs, int32_t variant, int64_t 
     bool energy = e_vals != nullptr || e_times != nullptr || n_energy != nullptr;
     std::vector<RunCtx> C(nslabs);
     int rc;
-    for (int r = 0; r < nslabs; r++)
-        if ((rc = run_begin(grp->ranks[r], variant, nt, energy, r == 0, C[r]))) return rc;
-    if (nslabs > 1) {  // E(0) and the control reset precede every slab's first step
-        CU(cudaSetDevice(grp->ranks[0]->d.device));
-        CU(cudaEventRecord(grp->ranks[0]->ev_phase, grp->ranks[0]->st));
-        for (int r = 1; r < nslabs; r++) {
-            CU(cudaSetDevice(grp->ranks[r]->d.device));
-            CU(cudaStreamWaitEvent(grp->ranks[r]->st, grp->ranks[0]->ev_phase, 0));
-        }
+    // slab 0 resets the shared control block; every other slab orders its work
+    // (naive-residual flags, E(0), first step) after that reset
+    if ((rc = run_begin(grp->ranks[0], variant, nt, energy, true, C[0]))) return rc;
+    CU(cudaEventRecord(grp->ranks[0]->ev_phase, grp->ranks[0]->st));
+    for (int r = 1; r < nslabs; r++) {
+        CU(cudaSetDevice(grp->ranks[r]->d.device));
+        CU(cudaStreamWaitEvent(grp->ranks[r]->st, grp->ranks[0]->ev_phase, 0));
+        if ((rc = run_begin(grp->ranks[r], variant, nt, energy, false, C[r]))) return rc;
+    }
+    if (nslabs > 1) {
         if ((rc = exchange_group(grp, 0)) || (rc = exchange_group(grp, 1))) return rc;  // halos of the uploaded state
     }
     for (int64_t n = 0; n < nt; n++) {

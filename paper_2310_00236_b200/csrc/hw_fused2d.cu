@@ -138,6 +138,11 @@ __device__ __forceinline__ void finish_row(H2 rhs, float rcp, __half2 dt2, int s
 template <int V, int ORDER, bool ROWMED>
 __global__ void __launch_bounds__(512, 1)
     k_ac2d_fused(AcFusedParams P, int64_t n, double src, int sample, int64_t eidx) {
+    // Programmatic dependent launch: the next step's grid may launch as soon as this
+    // one is running (its CTAs take SMs as ours retire); it waits here until every
+    // write of the previous step is visible.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (halted(P.ctrl, n)) return;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
@@ -424,7 +429,17 @@ void launch_ac2d_fused(int variant, int order, const AcFusedParams& P, int nbloc
     const size_t bytes = fused2d_smem_bytes(P.nx);
     void* fn = fused2d_rowmed(P) ? fused_fn<true>(variant, order) : fused_fn<false>(variant, order);
     void* args[] = {(void*)&P, (void*)&n, (void*)&src, (void*)&sample, (void*)&eidx};
-    cudaLaunchKernel(fn, dim3(nblocks), dim3(threads), args, bytes, st);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nblocks);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 }  // namespace hw
