@@ -23,7 +23,7 @@ __device__ __forceinline__ void upd_store(const FieldView& f, const FieldView& r
 }
 
 template <int LS, int LU, int W>
-__global__ void __launch_bounds__(BLOCK) k_ac_vel(AcParams P, int64_t n) {
+__global__ void __launch_bounds__(BLOCK, 8) k_ac_vel(AcParams P, int64_t n) {
     if (halted(P.ctrl, n)) return;
     using TU = typename lane<LU>::T;
     using TS = typename lane<LS>::T;
@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(BLOCK) k_ac_vel(AcParams P, int64_t n) {
 }
 
 template <int LS, int LU, int W>
-__global__ void __launch_bounds__(BLOCK) k_ac_pres(AcParams P, int64_t n, double src, int sample) {
+__global__ void __launch_bounds__(BLOCK, 8) k_ac_pres(AcParams P, int64_t n, double src, int sample) {
     if (halted(P.ctrl, n)) return;
     using TU = typename lane<LU>::T;
     using TS = typename lane<LS>::T;
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(BLOCK) k_ac_pres(AcParams P, int64_t n, double
 
 // E(t=0): the state paired with itself (acoustic.py:205-208).
 template <int LU, int W>
-__global__ void __launch_bounds__(BLOCK) k_ac_energy(AcParams P) {
+__global__ void __launch_bounds__(BLOCK, 8) k_ac_energy(AcParams P) {
     using TU = typename lane<LU>::T;
     const Geom& g = P.g;
     const int64_t xv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -28,7 +28,7 @@ __device__ __forceinline__ vec<LU, W> ld(const FieldView& f, const Cell& c) {
 }
 
 template <int LS, int LU, int W>
-__global__ void __launch_bounds__(BLOCK) k_el_vel(ElParams P, int64_t n, double src) {
+__global__ void __launch_bounds__(BLOCK, 8) k_el_vel(ElParams P, int64_t n, double src) {
     if (halted(P.ctrl, n)) return;
     using TU = typename lane<LU>::T;
     using TS = typename lane<LS>::T;
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(BLOCK) k_el_vel(ElParams P, int64_t n, double 
 }
 
 template <int LS, int LU, int W>
-__global__ void __launch_bounds__(BLOCK) k_el_stress(ElParams P, int64_t n, double src, int sample) {
+__global__ void __launch_bounds__(BLOCK, 8) k_el_stress(ElParams P, int64_t n, double src, int sample) {
     if (halted(P.ctrl, n)) return;
     using TU = typename lane<LU>::T;
     using TS = typename lane<LS>::T;
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(BLOCK) k_el_stress(ElParams P, int64_t n, doub
 
 // E(t=0): stresses paired with themselves (elastic.py:265-267).
 template <int LU, int W>
-__global__ void __launch_bounds__(BLOCK) k_el_energy(ElParams P) {
+__global__ void __launch_bounds__(BLOCK, 8) k_el_energy(ElParams P) {
     const Geom& g = P.g;
     const int64_t nxv = g.nx / W;
     const int64_t rows = P.sxx.rows > P.sxs.rows ? P.sxx.rows : P.sxs.rows;
