@@ -164,6 +164,11 @@ int hw_run_device(hw_solver* h, int32_t variant, int64_t step0, int64_t nt,
 /* Kernel launches issued by the last hw_run / hw_run_device (evidence for bench.py). */
 int64_t hw_last_launch_count(const hw_solver* h);
 
+/* Which kernel family this handle's steps use (chosen at hw_create from the lanes,
+ * dimension and nx): "fused2d" (single-pass 2D acoustic), "stream2d" (streaming 2D
+ * elastic phases) or "generic" (phase kernels).  Static string; "" for NULL. */
+const char* hw_kernel_path(const hw_solver* h);
+
 /* Average duration (ms) of the dominant (fused step) kernel in the last
  * hw_run_device, measured with CUDA events on the launching stream; 0 if unknown. */
 double hw_last_kernel_ms(const hw_solver* h);

@@ -351,6 +351,9 @@ struct hw_solver {
     bool fused = false;
     int fused_blocks = 0;
     void* mem_b[2 * F_N] = {};
+    // streaming phase kernels (2D elastic, binary16): in place on the standard layout
+    bool el_stream = false;
+    int stream_blocks = 0;
     // slab decomposition over the slow axis
     int world = 1, rank = 0;
     int64_t r0 = 0, ns_loc = 0;
@@ -624,11 +627,18 @@ int setup_handle(hw_solver* h) {
             h->fused_blocks = (int)(nbf < nsm ? nbf : nsm);
             h->fused = true;
         }
+        if (want && !h->ac && !h->d3 && h->LS == 16 && h->LU == 16 && el2d_stream_eligible(desc->nx, dev_smem)) {
+            if (el2d_stream_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "streaming kernel setup failed");
+            int64_t nbs = max_rows / 4;
+            if (nbs < 1) nbs = 1;
+            h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
+            h->el_stream = true;
+        }
     }
     if (!h->ctrl) CU(cudaMalloc(&h->ctrl, sizeof(Ctrl)));
     h->max_rows = max_rows;
     h->nblocks = grid_blocks(h->g, h->W, max_rows);
-    CU(cudaMalloc(&h->partials, h->nblocks * NCOMP * sizeof(double)));
+    CU(cudaMalloc(&h->partials, (h->nblocks > h->stream_blocks ? h->nblocks : h->stream_blocks) * NCOMP * sizeof(double)));
     // the point source belongs to the slab holding its row
     int srcf = desc->src_kind == HW_SRC_PRESSURE ? F_P : (desc->src_kind == HW_SRC_VSLOW ? F_VS : F_SXX);
     if (desc->src_kind != HW_SRC_NONE && desc->src_s >= h->r0 && desc->src_s < h->r0 + field_rows(h, srcf)) {
@@ -989,9 +999,12 @@ static void run_phase(hw_solver* h, const RunCtx& C, int phase, int64_t n, const
     const int sample = C.energy && ((n + 1) % C.every == 0);
     if (phase == 0) {
         if (h->ac) launch_ac_vel(h->LS, h->LU, h->W, C.A, n, h->max_rows, h->st);
+        else if (h->el_stream) launch_el2d_vel_stream(C.variant, h->d.order, C.L, h->stream_blocks, n, sk == HW_SRC_VSLOW ? s : 0.0, h->st);
         else launch_el_vel(h->LS, h->LU, h->W, C.L, n, sk == HW_SRC_VSLOW ? s : 0.0, h->max_rows, h->st);
     } else {
         if (h->ac) launch_ac_pres(h->LS, h->LU, h->W, C.A, n, sk == HW_SRC_PRESSURE ? s : 0.0, sample, h->max_rows, h->st);
+        else if (h->el_stream)
+            launch_el2d_stress_stream(C.variant, h->d.order, C.L, h->stream_blocks, n, sk == HW_SRC_EXPLOSIVE ? s : 0.0, sample, h->st);
         else launch_el_stress(h->LS, h->LU, h->W, C.L, n, sk == HW_SRC_EXPLOSIVE ? s : 0.0, sample, h->max_rows, h->st);
     }
     h->launches++;
@@ -1000,7 +1013,9 @@ static void run_phase(hw_solver* h, const RunCtx& C, int phase, int64_t n, const
 static void run_epilogue(hw_solver* h, const RunCtx& C, int64_t n) {
     const int sample = C.energy && ((n + 1) % C.every == 0);
     if (sample || C.E.n_rec > 0) {
-        launch_epilogue(h->LU, C.E, n, sample, (n + 1) / C.every, h->st);
+        EpParams E = C.E;
+        if (h->el_stream) E.nblocks = h->stream_blocks;  // partials of the streaming stress kernel
+        launch_epilogue(h->LU, E, n, sample, (n + 1) / C.every, h->st);
         h->launches++;
     }
 }
@@ -1237,6 +1252,11 @@ int hw_run_device(hw_solver* h, int32_t variant, int64_t step0, int64_t nt, cons
 }
 
 int64_t hw_last_launch_count(const hw_solver* h) { return h ? h->launches : 0; }
+
+const char* hw_kernel_path(const hw_solver* h) {
+    if (!h) return "";
+    return h->fused ? "fused2d" : (h->el_stream ? "stream2d" : "generic");
+}
 
 double hw_last_kernel_ms(const hw_solver* h) { return h ? h->kernel_ms : 0.0; }
 

@@ -366,7 +366,7 @@ __device__ __forceinline__ bool halted(const Ctrl* ctrl, int64_t n) {
 
 // Block-wide fp64 sum of NCOMP components; thread 0 writes the block partial.
 __device__ __forceinline__ void block_partials(double v[NCOMP], double* out) {
-    __shared__ double red[BLOCK / 32][NCOMP];
+    __shared__ double red[32][NCOMP];  // any block size up to 1024 threads
     const int tid = threadIdx.x;
     int lane_id = tid & 31, warp = tid >> 5;
 #pragma unroll

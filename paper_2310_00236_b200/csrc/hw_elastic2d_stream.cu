@@ -1,0 +1,481 @@
+// hw_elastic2d_stream.cu — streaming phase kernels for the 2D elastic solver,
+// binary16 state (BASELINE config 4: 4096^2, free surface, op6), sm_100a.
+//
+// Same two phases as ElasticSolver._step_work (elastic.py:176-238) and the generic
+// kernels (identical bits: same device helpers), restructured like the fused
+// acoustic kernel: CTA b owns rows [y0, y1) and the full row width (x periodic inside
+// the CTA); rows stream through a 4-slot TMA ring filled 2 rows ahead
+// (cp.async.bulk + mbarrier complete_tx).  Per slot three row streams: two feed
+// per-thread register queues for the slow-axis taps, one is the row whose x taps
+// are needed now.  Own-cell fields (old values, residuals) come with coalesced
+// 16-byte loads.  Ghost slabs (free-surface images, periodic wrap) are read in place
+// and kept current by write-through on every store, as in the generic kernels.
+#include <cuda_runtime.h>
+
+#include "hw_params.h"
+#include "hw_tma.cuh"
+#include "../../include/halfwave_b200.h"
+
+namespace hw {
+
+constexpr int ECPT = 8;   // cells per thread
+constexpr int ER = 4;     // ring slots (unroll factor)
+constexpr int ED = 2;     // prefetch distance: slot of iteration i-1 stays valid during i
+constexpr int ENS = 3;    // TMA row streams per slot
+
+using EH2 = vec<16, 2>;
+using EO2 = vops<16, 2>;
+
+struct E8 {
+    EH2 q[4];
+};
+
+__device__ __forceinline__ E8 e_ld8(const __half* p) {
+    E8 r;
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    *reinterpret_cast<unsigned int*>(&r.q[0].h2) = u.x;
+    *reinterpret_cast<unsigned int*>(&r.q[1].h2) = u.y;
+    *reinterpret_cast<unsigned int*>(&r.q[2].h2) = u.z;
+    *reinterpret_cast<unsigned int*>(&r.q[3].h2) = u.w;
+    return r;
+}
+
+__device__ __forceinline__ void e_st8(__half* p, const E8& v) {
+    uint4 u;
+    u.x = *reinterpret_cast<const unsigned int*>(&v.q[0].h2);
+    u.y = *reinterpret_cast<const unsigned int*>(&v.q[1].h2);
+    u.z = *reinterpret_cast<const unsigned int*>(&v.q[2].h2);
+    u.w = *reinterpret_cast<const unsigned int*>(&v.q[3].h2);
+    *reinterpret_cast<uint4*>(p) = u;
+}
+
+__device__ __forceinline__ EH2 e_ld2(const __half* p) {
+    EH2 r;
+    r.h2 = *reinterpret_cast<const __half2*>(p);
+    return r;
+}
+
+__device__ __forceinline__ E8 e_neg8(const E8& v) {
+    E8 r;
+#pragma unroll
+    for (int j = 0; j < 4; j++) r.q[j] = vneg<16, 2>(v.q[j]);
+    return r;
+}
+
+template <int ORDER>
+__device__ __forceinline__ EH2 e_fold(const __half c[4], EH2 t0, EH2 t1, EH2 t2, EH2 t3) {
+    EH2 inner = EO2::add(EO2::mul(vsplat<16, 2>(c[1]), t1), EO2::mul(vsplat<16, 2>(c[2]), t2));
+    if (ORDER == 2) return inner;
+    EH2 outer = EO2::add(EO2::mul(vsplat<16, 2>(c[0]), t0), EO2::mul(vsplat<16, 2>(c[3]), t3));
+    return EO2::add(inner, outer);
+}
+
+// x derivative of 8 cells (periodic) from a shared row; to_int: shifts (-2..1) else (-1..2)
+template <int ORDER>
+__device__ __forceinline__ E8 e_xfold(const __half c[4], const __half* row, int x, int xl, int xr, bool to_int) {
+    EH2 Q[6];
+    Q[0] = e_ld2(row + xl);
+    const E8 own = e_ld8(row + x);
+#pragma unroll
+    for (int j = 0; j < 4; j++) Q[j + 1] = own.q[j];
+    Q[5] = e_ld2(row + xr);
+    EH2 S[5];
+#pragma unroll
+    for (int j = 0; j < 5; j++) S[j] = vshift<16, 2>(Q[j], Q[j + 1]);
+    E8 r;
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+        r.q[j] = to_int ? e_fold<ORDER>(c, Q[j], S[j], Q[j + 1], S[j + 1]) : e_fold<ORDER>(c, S[j], Q[j + 1], S[j + 1], Q[j + 2]);
+    return r;
+}
+
+// slow taps from a 4-deep register queue (q[k] = row base + k) for each of the 4 pairs
+template <int ORDER>
+__device__ __forceinline__ E8 e_sfold(const __half c[4], const E8& a, const E8& b, const E8& d, const E8& e) {
+    E8 r;
+#pragma unroll
+    for (int j = 0; j < 4; j++) r.q[j] = e_fold<ORDER>(c, a.q[j], b.q[j], d.q[j], e.q[j]);
+    return r;
+}
+
+__device__ __forceinline__ unsigned int e_nonfinite(__half2 acc) {  // |max| is inf or NaN
+    const unsigned int b = *reinterpret_cast<const unsigned int*>(&acc);
+    return (((b & 0x7c00u) == 0x7c00u) || ((b & 0x7c000000u) == 0x7c000000u)) ? 1u : 0u;
+}
+
+// ring rows below the first ghost slab are never consumed (r < y0); keep the copy in bounds
+__device__ __forceinline__ int64_t e_row(int r) { return (int64_t)(r < -G ? -G : r); }
+
+__device__ __forceinline__ void e_track(__half2& acc, const E8& v) {
+#pragma unroll
+    for (int j = 0; j < 4; j++) acc = __hmax2_nan(acc, __habs2(v.q[j].h2));
+}
+
+// store one row (8 cells per thread) of field f and its write-through ghost rows
+__device__ __forceinline__ void e_store_row(const FieldView& f, int64_t pitch, int s, int x, const E8& v) {
+    __half* base = reinterpret_cast<__half*>(f.base);
+    e_st8(base + (int64_t)s * pitch + x, v);
+    if ((f.gtop | f.gbot) == GHOST_NONE) return;
+    const int n = (int)f.rows;
+    if (f.gtop == GHOST_PERIODIC && s >= n - G) e_st8(base + (int64_t)(s - n) * pitch + x, v);
+    if (f.gbot == GHOST_PERIODIC && s < G) e_st8(base + (int64_t)(n + s) * pitch + x, v);
+    if ((f.gtop | f.gbot) & GHOST_IMAGE) {
+        const E8 w = f.odd ? e_neg8(v) : v;
+        const int sg = (int)f.row0 + s, ng = (int)f.nglob;
+        if (f.gtop == GHOST_IMAGE) {
+            const int k1 = f.half_s ? -sg - 1 : -sg;
+            if (k1 < 0 && k1 >= -G) e_st8(base + (int64_t)(k1 - (int)f.row0) * pitch + x, w);
+        }
+        if (f.gbot == GHOST_IMAGE) {
+            const int k2 = f.half_s ? 2 * ng - 1 - sg : 2 * ng - 2 - sg;
+            if (k2 >= ng && k2 < ng + G) e_st8(base + (int64_t)(k2 - (int)f.row0) * pitch + x, w);
+        }
+    }
+}
+
+struct ERing {
+    uint64_t* bar;
+    __half* ring;
+    int64_t nx;
+    __device__ __forceinline__ __half* row(int slot, int st) const { return ring + (slot * ENS + st) * nx; }
+};
+
+__device__ __forceinline__ void e_init_ring(const ERing& R) {
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ER; s++) mbar_init(&R.bar[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------- velocity phase
+// front F at iteration i = y0 - 2 + i; output row r = F - 2 (once r >= y0).
+//   stream 0: syy[F]      -> queue ssq (rows r-1..r+2)
+//   stream 1: sxy[F-1]    -> queue xsq (rows r-2..r+1); its x taps for vy[r] (= row F-2)
+//                            come from the previous slot's stream 1
+//   stream 2: sxx[F-2]    -> x taps for vx[r]
+template <int V, int ORDER>
+__global__ void __launch_bounds__(512, 1) k_el2d_vel_stream(ElParams P, int64_t n, double src) {
+    if (halted(P.ctrl, n)) return;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const ERing R{reinterpret_cast<uint64_t*>(smem), reinterpret_cast<__half*>(smem + 128), P.g.nx};
+    const int64_t pitch = P.g.slab;  // row stride (2D: nm = 1)
+    const int nx = (int)P.g.nx;
+    const int rows = (int)(P.vx.rows > P.vs.rows ? P.vx.rows : P.vs.rows);
+    const int nb = gridDim.x, b = blockIdx.x;
+    const int y0 = (int)((int64_t)b * rows / nb), y1 = (int)((int64_t)(b + 1) * rows / nb);
+    const int F0 = y0 - 2, NI = y1 - y0 + 4;
+    const int tid = threadIdx.x, x = tid * ECPT;
+    constexpr bool comp = V != 0;
+    const uint32_t rb = (uint32_t)(nx * sizeof(__half));
+    const __half* SSS = reinterpret_cast<const __half*>(P.sss.base);
+    const __half* SXS = reinterpret_cast<const __half*>(P.sxs.base);
+    const __half* SXX = reinterpret_cast<const __half*>(P.sxx.base);
+    auto issue = [&](int i) {
+        const int F = F0 + i, slot = i % ER;
+        mbar_arrive_expect_tx(&R.bar[slot], 3 * rb);
+        tma_load_1d(R.row(slot, 0), SSS + e_row(F) * pitch, rb, &R.bar[slot]);
+        tma_load_1d(R.row(slot, 1), SXS + e_row(F - 1) * pitch, rb, &R.bar[slot]);
+        tma_load_1d(R.row(slot, 2), SXX + e_row(F - 2) * pitch, rb, &R.bar[slot]);
+    };
+    e_init_ring(R);
+    if (tid == 0)
+        for (int i = 0; i < ED && i < NI; i++) issue(i);
+    __half c[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) c[j] = lconst<16>(P.k, j);
+    const __half dt = lconst<16>(P.k, 4);
+    const int xl = x == 0 ? nx - 2 : x - 2, xr = x + ECPT >= nx ? 0 : x + ECPT;
+    const bool src_here = P.src_kind == HW_SRC_VSLOW && src != 0.0 && P.src_x >= x && P.src_x < x + ECPT;
+    E8 ssq[4], xsq[4];  // slow-tap queues indexed by iteration mod 4
+    __half2 acc[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) acc[q] = __float2half2_rn(0.f);
+    for (int i0 = 0; i0 < NI; i0 += ER) {
+        const uint32_t par = (uint32_t)((i0 / ER) & 1);
+#pragma unroll
+        for (int u = 0; u < ER; u++) {
+            const int i = i0 + u;
+            if (i < NI) {
+                if (tid == 0 && i + ED < NI) {
+                    fence_proxy_async_smem();
+                    issue(i + ED);
+                }
+                mbar_wait(&R.bar[u], par);
+                const int r = F0 + i - 2;
+                ssq[u] = e_ld8(R.row(u, 0) + x);
+                xsq[u] = e_ld8(R.row(u, 1) + x);
+                if (r >= y0 && r < y1) {
+                    if (r < P.vx.rows) {  // vx = fl(fl(ddx sxx + dds sxy) / rho_x * dt) (elastic.py:191-194)
+                        E8 a = e_xfold<ORDER>(c, R.row(u, 2), x, xl, xr, false);
+                        // sxy rows r-2..r+1 were queued at iterations i-3..i
+                        const E8 d = e_sfold<ORDER>(c, xsq[(u + 1) % ER], xsq[(u + 2) % ER], xsq[(u + 3) % ER], xsq[u]);
+                        __half* vxp = reinterpret_cast<__half*>(P.vx.base) + (int64_t)r * pitch + x;
+                        E8 v = e_ld8(vxp);
+                        E8 rr = comp ? e_ld8(reinterpret_cast<__half*>(P.rvx.base) + (int64_t)r * pitch + x) : E8{};
+#pragma unroll
+                        for (int j = 0; j < 4; j++)
+                            finish<16, 16, 2>(EO2::add(a.q[j], d.q[j]), &P.rho_x, r, 0, x + 2 * j, dt, V, -1, 0.0, v.q[j], rr.q[j]);
+                        e_store_row(P.vx, pitch, r, x, v);
+                        e_track(acc[0], v);
+                        if (comp) {
+                            e_store_row(P.rvx, pitch, r, x, rr);
+                            e_track(acc[2], rr);
+                        }
+                    }
+                    if (r < P.vs.rows) {  // vy = fl(fl(ddx sxy + dds syy) (+src) / rho_y * dt) (elastic.py:196-205)
+                        E8 a = e_xfold<ORDER>(c, R.row((u + ER - 1) % ER, 1), x, xl, xr, true);
+                        // syy rows r-1..r+2 were queued at iterations i-3..i
+                        const E8 d = e_sfold<ORDER>(c, ssq[(u + 1) % ER], ssq[(u + 2) % ER], ssq[(u + 3) % ER], ssq[u]);
+                        const bool sk = src_here && r == P.src_s;
+                        const int sj = (int)((P.src_x - x) >> 1), sl = (int)((P.src_x - x) & 1);
+                        __half* vyp = reinterpret_cast<__half*>(P.vs.base) + (int64_t)r * pitch + x;
+                        E8 v = e_ld8(vyp);
+                        E8 rr = comp ? e_ld8(reinterpret_cast<__half*>(P.rvs.base) + (int64_t)r * pitch + x) : E8{};
+#pragma unroll
+                        for (int j = 0; j < 4; j++)
+                            finish<16, 16, 2>(EO2::add(a.q[j], d.q[j]), &P.rho_s, r, 0, x + 2 * j, dt, V,
+                                              (sk && j == sj) ? sl : -1, src, v.q[j], rr.q[j]);
+                        e_store_row(P.vs, pitch, r, x, v);
+                        e_track(acc[1], v);
+                        if (comp) {
+                            e_store_row(P.rvs, pitch, r, x, rr);
+                            e_track(acc[3], rr);
+                        }
+                    }
+                }
+                __syncthreads();  // slot (i-1) % ER is reused at iteration i + 1
+            }
+        }
+    }
+    unsigned int mask = 0;
+    mask |= e_nonfinite(acc[0]) << P.vx.bit;
+    mask |= e_nonfinite(acc[1]) << P.vs.bit;
+    if (comp) {
+        mask |= e_nonfinite(acc[2]) << P.rvx.bit;
+        mask |= e_nonfinite(acc[3]) << P.rvs.bit;
+    }
+    record_failure(P.ctrl, n, mask);
+}
+
+// ---------------------------------------------------------------- stress phase
+// front F at iteration i = y0 - 2 + i; output row r = F - 2.
+//   stream 0: vx[F]    -> queue vxq (rows r-1..r+2, to-half taps of sxy)
+//   stream 1: vy[F-1]  -> queue vyq (rows r-2..r+1, to-int taps of dvy); its x taps for
+//                         sxy[r] (= row F-2) come from the previous slot's stream 1
+//   stream 2: vx[F-2]  -> x taps of dvx at row r
+template <int V, int ORDER>
+__global__ void __launch_bounds__(512, 1) k_el2d_stress_stream(ElParams P, int64_t n, double src, int sample) {
+    if (halted(P.ctrl, n)) return;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const ERing R{reinterpret_cast<uint64_t*>(smem), reinterpret_cast<__half*>(smem + 128), P.g.nx};
+    const int64_t pitch = P.g.slab;  // row stride (2D: nm = 1)
+    const int nx = (int)P.g.nx;
+    const int rows = (int)(P.sxx.rows > P.sxs.rows ? P.sxx.rows : P.sxs.rows);
+    const int nb = gridDim.x, b = blockIdx.x;
+    const int y0 = (int)((int64_t)b * rows / nb), y1 = (int)((int64_t)(b + 1) * rows / nb);
+    const int F0 = y0 - 2, NI = y1 - y0 + 4;
+    const int tid = threadIdx.x, x = tid * ECPT;
+    constexpr bool comp = V != 0;
+    const uint32_t rb = (uint32_t)(nx * sizeof(__half));
+    const __half* VX = reinterpret_cast<const __half*>(P.vx.base);
+    const __half* VY = reinterpret_cast<const __half*>(P.vs.base);
+    auto issue = [&](int i) {
+        const int F = F0 + i, slot = i % ER;
+        mbar_arrive_expect_tx(&R.bar[slot], 3 * rb);
+        tma_load_1d(R.row(slot, 0), VX + e_row(F) * pitch, rb, &R.bar[slot]);
+        tma_load_1d(R.row(slot, 1), VY + e_row(F - 1) * pitch, rb, &R.bar[slot]);
+        tma_load_1d(R.row(slot, 2), VX + e_row(F - 2) * pitch, rb, &R.bar[slot]);
+    };
+    e_init_ring(R);
+    if (tid == 0)
+        for (int i = 0; i < ED && i < NI; i++) issue(i);
+    __half c[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) c[j] = lconst<16>(P.k, j);
+    const __half dt = lconst<16>(P.k, 4);
+    const int xl = x == 0 ? nx - 2 : x - 2, xr = x + ECPT >= nx ? 0 : x + ECPT;
+    const bool src_here = P.src_kind == HW_SRC_EXPLOSIVE && src != 0.0 && P.src_x >= x && P.src_x < x + ECPT;
+    E8 vxq[4], vyq[4];
+    __half2 acc[6];
+#pragma unroll
+    for (int q = 0; q < 6; q++) acc[q] = __float2half2_rn(0.f);
+    double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int i0 = 0; i0 < NI; i0 += ER) {
+        const uint32_t par = (uint32_t)((i0 / ER) & 1);
+#pragma unroll
+        for (int u = 0; u < ER; u++) {
+            const int i = i0 + u;
+            if (i < NI) {
+                if (tid == 0 && i + ED < NI) {
+                    fence_proxy_async_smem();
+                    issue(i + ED);
+                }
+                mbar_wait(&R.bar[u], par);
+                const int r = F0 + i - 2;
+                vxq[u] = e_ld8(R.row(u, 0) + x);
+                vyq[u] = e_ld8(R.row(u, 1) + x);
+                if (r >= y0 && r < y1) {
+                    if (r < P.sxx.rows) {
+                        const E8 vxr = e_ld8(R.row(u, 2) + x);  // vx[r], own cells
+                        const E8 dvx = e_xfold<ORDER>(c, R.row(u, 2), x, xl, xr, true);
+                        // vy rows r-2..r+1 were queued at iterations i-3..i
+                        const E8 dvs = e_sfold<ORDER>(c, vyq[(u + 1) % ER], vyq[(u + 2) % ER], vyq[(u + 3) % ER], vyq[u]);
+                        const int sg = (int)P.sxx.row0 + r;
+                        const bool surf = P.fs && (sg == 0 || sg == (int)P.sxx.nglob - 1);
+                        const bool sk = src_here && r == P.src_s;
+                        const int sj = (int)((P.src_x - x) >> 1), sl = (int)((P.src_x - x) & 1);
+                        const int64_t off = (int64_t)r * pitch + x;
+                        const E8 sxx_old = e_ld8(reinterpret_cast<__half*>(P.sxx.base) + off);
+                        const E8 sss_old = e_ld8(reinterpret_cast<__half*>(P.sss.base) + off);
+                        E8 sxx = sxx_old, sss = sss_old;
+                        E8 rsxx = comp ? e_ld8(reinterpret_cast<__half*>(P.rsxx.base) + off) : E8{};
+                        E8 rsss = comp ? e_ld8(reinterpret_cast<__half*>(P.rsss.base) + off) : E8{};
+#pragma unroll
+                        for (int j = 0; j < 4; j++) {
+                            const EH2 stiff = pload<16, 2>(P.stiff, r, 0, x + 2 * j);
+                            const EH2 lam = pload<16, 2>(P.lam, r, 0, x + 2 * j);
+                            EH2 a1, a2;
+                            if (surf) {  // plane-stress surface row; syy takes a zero increment (elastic.py:215-230)
+                                a1 = EO2::mul(pload<16, 2>(P.ep, sg == 0 ? 0 : 1, 0, x + 2 * j), dvx.q[j]);
+                                a2 = vsplat<16, 2>(lane<16>::zero());
+                            } else {
+                                a1 = EO2::add(EO2::mul(stiff, dvx.q[j]), EO2::mul(lam, dvs.q[j]));
+                                a2 = EO2::add(EO2::mul(lam, dvx.q[j]), EO2::mul(stiff, dvs.q[j]));
+                            }
+                            const int lsrc = (sk && j == sj) ? sl : -1;
+                            finish<16, 16, 2>(a1, nullptr, r, 0, x, dt, V, lsrc, src, sxx.q[j], rsxx.q[j]);
+                            finish<16, 16, 2>(a2, nullptr, r, 0, x, dt, V, lsrc, src, sss.q[j], rsss.q[j]);
+                        }
+                        e_store_row(P.sxx, pitch, r, x, sxx);
+                        e_store_row(P.sss, pitch, r, x, sss);
+                        e_track(acc[0], sxx);
+                        e_track(acc[1], sss);
+                        if (comp) {
+                            e_store_row(P.rsxx, pitch, r, x, rsxx);
+                            e_store_row(P.rsss, pitch, r, x, rsss);
+                            e_track(acc[3], rsxx);
+                            e_track(acc[4], rsss);
+                        }
+                        if (sample) {  // kinetic x + strain energy at this integer row (diagnostics.py:100-162)
+                            const double w = surf ? 0.5 : 1.0;
+#pragma unroll
+                            for (int k = 0; k < ECPT; k++) {
+                                const int xi = x + k;
+                                const double v = (double)__half2float(vxr.q[k >> 1].e[k & 1]);
+                                e[0] += (w * p64(P.e_rho_x, r, 0, xi)) * (v * v);
+                                const double lamd = p64(P.e_lam, r, 0, xi), mu = p64(P.e_mu, r, 0, xi);
+                                const double xn = (double)__half2float(sxx_old.q[k >> 1].e[k & 1]);
+                                const double x1 = (double)__half2float(sxx.q[k >> 1].e[k & 1]);
+                                const double sn = (double)__half2float(sss_old.q[k >> 1].e[k & 1]);
+                                const double s1 = (double)__half2float(sss.q[k >> 1].e[k & 1]);
+                                const double stiffd = lamd + 2.0 * mu;
+                                const double dd = 4.0 * mu * (lamd + mu);
+                                double val;
+                                if (mu == 0.0) val = surf ? 0.0 : (xn * x1) / (lamd + mu);
+                                else if (surf) val = xn * x1 * stiffd / dd;
+                                else val = (stiffd * (xn * x1 + sn * s1) - lamd * (xn * s1 + sn * x1)) / dd;
+                                if (surf) val = 0.5 * val;
+                                e[3] += val;
+                            }
+                        }
+                    }
+                    if (r < P.sxs.rows) {  // sxy = fl(mu fl(dds vx + ddx vy)) (elastic.py:232-238)
+                        // vx rows r-1..r+2 were queued at iterations i-2..i (row r+2 is this slot)
+                        const E8 dvxy = e_sfold<ORDER>(c, vxq[(u + 1) % ER], vxq[(u + 2) % ER], vxq[(u + 3) % ER], vxq[u]);
+                        const E8 dvyx = e_xfold<ORDER>(c, R.row((u + ER - 1) % ER, 1), x, xl, xr, false);
+                        const int64_t off = (int64_t)r * pitch + x;
+                        const E8 old = e_ld8(reinterpret_cast<__half*>(P.sxs.base) + off);
+                        E8 s = old;
+                        E8 rs = comp ? e_ld8(reinterpret_cast<__half*>(P.rsxs.base) + off) : E8{};
+#pragma unroll
+                        for (int j = 0; j < 4; j++) {
+                            const EH2 mu = pload<16, 2>(P.mu_n, r, 0, x + 2 * j);
+                            finish<16, 16, 2>(EO2::mul(mu, EO2::add(dvxy.q[j], dvyx.q[j])), nullptr, r, 0, x, dt, V, -1,
+                                              0.0, s.q[j], rs.q[j]);
+                        }
+                        e_store_row(P.sxs, pitch, r, x, s);
+                        e_track(acc[2], s);
+                        if (comp) {
+                            e_store_row(P.rsxs, pitch, r, x, rs);
+                            e_track(acc[5], rs);
+                        }
+                        if (sample) {  // kinetic y + shear energy at this half row
+                            const E8 vyr = vyq[(u + 3) % ER];  // vy[r] was queued one iteration ago
+#pragma unroll
+                            for (int k = 0; k < ECPT; k++) {
+                                const int xi = x + k;
+                                const double v = (double)__half2float(vyr.q[k >> 1].e[k & 1]);
+                                e[1] += p64(P.e_rho_s, r, 0, xi) * (v * v);
+                                const double mun = p64(P.e_mu_n, r, 0, xi);
+                                const double a0 = (double)__half2float(old.q[k >> 1].e[k & 1]);
+                                const double a1 = (double)__half2float(s.q[k >> 1].e[k & 1]);
+                                e[4] += mun > 0.0 ? (a0 * a1) / mun : 0.0;
+                            }
+                        }
+                    }
+                }
+                __syncthreads();  // slot (i-1) % ER is reused at iteration i + 1
+            }
+        }
+    }
+    unsigned int mask = 0;
+    mask |= e_nonfinite(acc[0]) << P.sxx.bit;
+    mask |= e_nonfinite(acc[1]) << P.sss.bit;
+    mask |= e_nonfinite(acc[2]) << P.sxs.bit;
+    if (comp) {
+        mask |= e_nonfinite(acc[3]) << P.rsxx.bit;
+        mask |= e_nonfinite(acc[4]) << P.rsss.bit;
+        mask |= e_nonfinite(acc[5]) << P.rsxs.bit;
+    }
+    record_failure(P.ctrl, n, mask);
+    if (sample) block_partials(e, P.partials);
+}
+
+// ---------------------------------------------------------------- host side
+
+size_t el2d_stream_smem_bytes(int64_t nx) { return 128 + (size_t)ER * ENS * nx * sizeof(__half); }
+
+bool el2d_stream_eligible(int64_t nx, int max_smem) {
+    return nx % 256 == 0 && nx / ECPT <= 512 && el2d_stream_smem_bytes(nx) <= (size_t)max_smem;
+}
+
+template <int V, int O>
+static void el2d_attrs(int bytes) {
+    cudaFuncSetAttribute((void*)k_el2d_vel_stream<V, O>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute((void*)k_el2d_stress_stream<V, O>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+cudaError_t el2d_stream_prepare(int64_t nx) {
+    const int bytes = (int)el2d_stream_smem_bytes(nx);
+    el2d_attrs<0, 2>(bytes); el2d_attrs<3, 2>(bytes); el2d_attrs<6, 2>(bytes);
+    el2d_attrs<0, 4>(bytes); el2d_attrs<3, 4>(bytes); el2d_attrs<6, 4>(bytes);
+    return cudaGetLastError();
+}
+
+#define EL2D_DISPATCH(variant, order, CALL)                                          \
+    if (order == 2) {                                                                \
+        if (variant == 0) { constexpr int V_ = 0, O_ = 2; CALL; }                    \
+        else if (variant == 3) { constexpr int V_ = 3, O_ = 2; CALL; }               \
+        else { constexpr int V_ = 6, O_ = 2; CALL; }                                 \
+    } else {                                                                         \
+        if (variant == 0) { constexpr int V_ = 0, O_ = 4; CALL; }                    \
+        else if (variant == 3) { constexpr int V_ = 3, O_ = 4; CALL; }               \
+        else { constexpr int V_ = 6, O_ = 4; CALL; }                                 \
+    }
+
+void launch_el2d_vel_stream(int variant, int order, const ElParams& P, int nblocks, int64_t n, double src,
+                            cudaStream_t st) {
+    const size_t bytes = el2d_stream_smem_bytes(P.g.nx);
+    const int threads = (int)(P.g.nx / ECPT);
+    EL2D_DISPATCH(variant, order, (k_el2d_vel_stream<V_, O_><<<nblocks, threads, bytes, st>>>(P, n, src)))
+}
+
+void launch_el2d_stress_stream(int variant, int order, const ElParams& P, int nblocks, int64_t n, double src,
+                               int sample, cudaStream_t st) {
+    const size_t bytes = el2d_stream_smem_bytes(P.g.nx);
+    const int threads = (int)(P.g.nx / ECPT);
+    EL2D_DISPATCH(variant, order, (k_el2d_stress_stream<V_, O_><<<nblocks, threads, bytes, st>>>(P, n, src, sample)))
+}
+
+}  // namespace hw

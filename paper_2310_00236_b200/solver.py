@@ -354,5 +354,9 @@ class _DeviceSolver:
     def download(self, state):
         self._download(state)
 
+    def kernel_path(self) -> str:
+        """Kernel family of the device steps: "fused2d", "stream2d" or "generic"."""
+        return _abi.load().hw_kernel_path(self._lib_handle()).decode()
+
     def last_launch_count(self) -> int:
         return int(_abi.load().hw_last_launch_count(self._lib_handle()))

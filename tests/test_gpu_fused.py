@@ -102,4 +102,5 @@ def test_fused_single_steps_and_resume():
 def test_fused_path_is_selected():
     s, st = _case(4096, 64, 2)
     s.run(hw.Variant.OP3, st)
+    assert s.kernel_path() == "fused2d"
     assert s.last_launch_count() == 2 + 2  # E0 kernel + finalize, then one fused launch per step
