@@ -22,6 +22,7 @@ constexpr int ECPT = 8;   // cells per thread
 constexpr int ER = 4;     // ring slots (unroll factor)
 constexpr int ED = 2;     // prefetch distance: slot of iteration i-1 stays valid during i
 constexpr int ENS = 3;    // TMA row streams per slot
+constexpr int EOWN = 6;   // own-cell row streams per slot of the 2-slot own ring (max over phases)
 
 using EH2 = vec<16, 2>;
 using EO2 = vops<16, 2>;
@@ -133,16 +134,26 @@ __device__ __forceinline__ void e_store_row(const FieldView& f, int64_t pitch, i
     }
 }
 
+// Two TMA rings: the tap ring (ER slots x ENS rows, filled ED rows ahead) and the own
+// ring (2 slots x EOWN rows: the old values / residuals of the output row, filled one
+// output row ahead).  smem: [tap barriers | own barriers | tap ring | own ring].
 struct ERing {
     uint64_t* bar;
+    uint64_t* obar;
     __half* ring;
+    __half* own;
     int64_t nx;
+    __device__ __forceinline__ ERing(unsigned char* smem, int64_t n)
+        : bar(reinterpret_cast<uint64_t*>(smem)), obar(reinterpret_cast<uint64_t*>(smem + 64)),
+          ring(reinterpret_cast<__half*>(smem + 128)), own(ring + (int64_t)ER * ENS * n), nx(n) {}
     __device__ __forceinline__ __half* row(int slot, int st) const { return ring + (slot * ENS + st) * nx; }
+    __device__ __forceinline__ __half* orow(int slot, int st) const { return own + (slot * EOWN + st) * nx; }
 };
 
 __device__ __forceinline__ void e_init_ring(const ERing& R) {
     if (threadIdx.x == 0) {
         for (int s = 0; s < ER; s++) mbar_init(&R.bar[s], 1);
+        for (int s = 0; s < 2; s++) mbar_init(&R.obar[s], 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -158,7 +169,7 @@ template <int V, int ORDER>
 __global__ void __launch_bounds__(512, 1) k_el2d_vel_stream(ElParams P, int64_t n, double src) {
     if (halted(P.ctrl, n)) return;
     extern __shared__ __align__(128) unsigned char smem[];
-    const ERing R{reinterpret_cast<uint64_t*>(smem), reinterpret_cast<__half*>(smem + 128), P.g.nx};
+    const ERing R(smem, P.g.nx);
     const int64_t pitch = P.g.slab;  // row stride (2D: nm = 1)
     const int nx = (int)P.g.nx;
     const int rows = (int)(P.vx.rows > P.vs.rows ? P.vx.rows : P.vs.rows);
@@ -178,41 +189,59 @@ __global__ void __launch_bounds__(512, 1) k_el2d_vel_stream(ElParams P, int64_t 
         tma_load_1d(R.row(slot, 1), SXS + e_row(F - 1) * pitch, rb, &R.bar[slot]);
         tma_load_1d(R.row(slot, 2), SXX + e_row(F - 2) * pitch, rb, &R.bar[slot]);
     };
+    constexpr int NOWN = comp ? 4 : 2;  // vx vy [rvx rvy] of output row y0 + k
+    const __half* OWN[4] = {reinterpret_cast<const __half*>(P.vx.base), reinterpret_cast<const __half*>(P.vs.base),
+                            reinterpret_cast<const __half*>(P.rvx.base), reinterpret_cast<const __half*>(P.rvs.base)};
+    auto issue_own = [&](int k) {
+        const int slot = k & 1;
+        mbar_arrive_expect_tx(&R.obar[slot], NOWN * rb);
+#pragma unroll
+        for (int q = 0; q < NOWN; q++) tma_load_1d(R.orow(slot, q), OWN[q] + (int64_t)(y0 + k) * pitch, rb, &R.obar[slot]);
+    };
     e_init_ring(R);
-    if (tid == 0)
+    if (tid == 0) {
         for (int i = 0; i < ED && i < NI; i++) issue(i);
+        if (y1 > y0) issue_own(0);
+    }
     __half c[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) c[j] = lconst<16>(P.k, j);
     const __half dt = lconst<16>(P.k, 4);
     const int xl = x == 0 ? nx - 2 : x - 2, xr = x + ECPT >= nx ? 0 : x + ECPT;
     const bool src_here = P.src_kind == HW_SRC_VSLOW && src != 0.0 && P.src_x >= x && P.src_x < x + ECPT;
-    E8 ssq[4], xsq[4];  // slow-tap queues indexed by iteration mod 4
+    E8 ssq[4], xsq[4];  // slow-tap queues, [3] = newest row
     __half2 acc[4];
 #pragma unroll
     for (int q = 0; q < 4; q++) acc[q] = __float2half2_rn(0.f);
-    for (int i0 = 0; i0 < NI; i0 += ER) {
-        const uint32_t par = (uint32_t)((i0 / ER) & 1);
-#pragma unroll
-        for (int u = 0; u < ER; u++) {
-            const int i = i0 + u;
-            if (i < NI) {
+    #pragma unroll 1
+    for (int i = 0; i < NI; i++) {
+        const int u = i % ER;
+        const uint32_t par = (uint32_t)((i / ER) & 1);
+        {
+            {
                 if (tid == 0 && i + ED < NI) {
                     fence_proxy_async_smem();
                     issue(i + ED);
                 }
                 mbar_wait(&R.bar[u], par);
                 const int r = F0 + i - 2;
-                ssq[u] = e_ld8(R.row(u, 0) + x);
-                xsq[u] = e_ld8(R.row(u, 1) + x);
+                ssq[0] = ssq[1]; ssq[1] = ssq[2]; ssq[2] = ssq[3];  // queue rows F-3..F
+                ssq[3] = e_ld8(R.row(u, 0) + x);
+                xsq[0] = xsq[1]; xsq[1] = xsq[2]; xsq[2] = xsq[3];  // queue rows F-4..F-1
+                xsq[3] = e_ld8(R.row(u, 1) + x);
                 if (r >= y0 && r < y1) {
+                    const int kr = r - y0;
+                    if (tid == 0 && r + 1 < y1) {  // own slot (kr+1)&1 was last read before the previous barrier
+                        fence_proxy_async_smem();
+                        issue_own(kr + 1);
+                    }
+                    mbar_wait(&R.obar[kr & 1], (uint32_t)((kr >> 1) & 1));
                     if (r < P.vx.rows) {  // vx = fl(fl(ddx sxx + dds sxy) / rho_x * dt) (elastic.py:191-194)
                         E8 a = e_xfold<ORDER>(c, R.row(u, 2), x, xl, xr, false);
                         // sxy rows r-2..r+1 were queued at iterations i-3..i
-                        const E8 d = e_sfold<ORDER>(c, xsq[(u + 1) % ER], xsq[(u + 2) % ER], xsq[(u + 3) % ER], xsq[u]);
-                        __half* vxp = reinterpret_cast<__half*>(P.vx.base) + (int64_t)r * pitch + x;
-                        E8 v = e_ld8(vxp);
-                        E8 rr = comp ? e_ld8(reinterpret_cast<__half*>(P.rvx.base) + (int64_t)r * pitch + x) : E8{};
+                        const E8 d = e_sfold<ORDER>(c, xsq[0], xsq[1], xsq[2], xsq[3]);
+                        E8 v = e_ld8(R.orow(kr & 1, 0) + x);
+                        E8 rr = comp ? e_ld8(R.orow(kr & 1, 2) + x) : E8{};
 #pragma unroll
                         for (int j = 0; j < 4; j++)
                             finish<16, 16, 2>(EO2::add(a.q[j], d.q[j]), &P.rho_x, r, 0, x + 2 * j, dt, V, -1, 0.0, v.q[j], rr.q[j]);
@@ -226,12 +255,11 @@ __global__ void __launch_bounds__(512, 1) k_el2d_vel_stream(ElParams P, int64_t 
                     if (r < P.vs.rows) {  // vy = fl(fl(ddx sxy + dds syy) (+src) / rho_y * dt) (elastic.py:196-205)
                         E8 a = e_xfold<ORDER>(c, R.row((u + ER - 1) % ER, 1), x, xl, xr, true);
                         // syy rows r-1..r+2 were queued at iterations i-3..i
-                        const E8 d = e_sfold<ORDER>(c, ssq[(u + 1) % ER], ssq[(u + 2) % ER], ssq[(u + 3) % ER], ssq[u]);
+                        const E8 d = e_sfold<ORDER>(c, ssq[0], ssq[1], ssq[2], ssq[3]);
                         const bool sk = src_here && r == P.src_s;
                         const int sj = (int)((P.src_x - x) >> 1), sl = (int)((P.src_x - x) & 1);
-                        __half* vyp = reinterpret_cast<__half*>(P.vs.base) + (int64_t)r * pitch + x;
-                        E8 v = e_ld8(vyp);
-                        E8 rr = comp ? e_ld8(reinterpret_cast<__half*>(P.rvs.base) + (int64_t)r * pitch + x) : E8{};
+                        E8 v = e_ld8(R.orow(kr & 1, 1) + x);
+                        E8 rr = comp ? e_ld8(R.orow(kr & 1, 3) + x) : E8{};
 #pragma unroll
                         for (int j = 0; j < 4; j++)
                             finish<16, 16, 2>(EO2::add(a.q[j], d.q[j]), &P.rho_s, r, 0, x + 2 * j, dt, V,
@@ -268,7 +296,7 @@ template <int V, int ORDER>
 __global__ void __launch_bounds__(512, 1) k_el2d_stress_stream(ElParams P, int64_t n, double src, int sample) {
     if (halted(P.ctrl, n)) return;
     extern __shared__ __align__(128) unsigned char smem[];
-    const ERing R{reinterpret_cast<uint64_t*>(smem), reinterpret_cast<__half*>(smem + 128), P.g.nx};
+    const ERing R(smem, P.g.nx);
     const int64_t pitch = P.g.slab;  // row stride (2D: nm = 1)
     const int nx = (int)P.g.nx;
     const int rows = (int)(P.sxx.rows > P.sxs.rows ? P.sxx.rows : P.sxs.rows);
@@ -287,9 +315,21 @@ __global__ void __launch_bounds__(512, 1) k_el2d_stress_stream(ElParams P, int64
         tma_load_1d(R.row(slot, 1), VY + e_row(F - 1) * pitch, rb, &R.bar[slot]);
         tma_load_1d(R.row(slot, 2), VX + e_row(F - 2) * pitch, rb, &R.bar[slot]);
     };
+    constexpr int NOWN = comp ? 6 : 3;  // sxx syy sxy [rsxx rsyy rsxy] of output row y0 + k
+    const __half* OWN[6] = {reinterpret_cast<const __half*>(P.sxx.base), reinterpret_cast<const __half*>(P.sss.base),
+                            reinterpret_cast<const __half*>(P.sxs.base), reinterpret_cast<const __half*>(P.rsxx.base),
+                            reinterpret_cast<const __half*>(P.rsss.base), reinterpret_cast<const __half*>(P.rsxs.base)};
+    auto issue_own = [&](int k) {
+        const int slot = k & 1;
+        mbar_arrive_expect_tx(&R.obar[slot], NOWN * rb);
+#pragma unroll
+        for (int q = 0; q < NOWN; q++) tma_load_1d(R.orow(slot, q), OWN[q] + (int64_t)(y0 + k) * pitch, rb, &R.obar[slot]);
+    };
     e_init_ring(R);
-    if (tid == 0)
+    if (tid == 0) {
         for (int i = 0; i < ED && i < NI; i++) issue(i);
+        if (y1 > y0) issue_own(0);
+    }
     __half c[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) c[j] = lconst<16>(P.k, j);
@@ -301,36 +341,43 @@ __global__ void __launch_bounds__(512, 1) k_el2d_stress_stream(ElParams P, int64
 #pragma unroll
     for (int q = 0; q < 6; q++) acc[q] = __float2half2_rn(0.f);
     double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    for (int i0 = 0; i0 < NI; i0 += ER) {
-        const uint32_t par = (uint32_t)((i0 / ER) & 1);
-#pragma unroll
-        for (int u = 0; u < ER; u++) {
-            const int i = i0 + u;
-            if (i < NI) {
+    #pragma unroll 1
+    for (int i = 0; i < NI; i++) {
+        const int u = i % ER;
+        const uint32_t par = (uint32_t)((i / ER) & 1);
+        {
+            {
                 if (tid == 0 && i + ED < NI) {
                     fence_proxy_async_smem();
                     issue(i + ED);
                 }
                 mbar_wait(&R.bar[u], par);
                 const int r = F0 + i - 2;
-                vxq[u] = e_ld8(R.row(u, 0) + x);
-                vyq[u] = e_ld8(R.row(u, 1) + x);
+                vxq[0] = vxq[1]; vxq[1] = vxq[2]; vxq[2] = vxq[3];  // queue rows F-3..F
+                vxq[3] = e_ld8(R.row(u, 0) + x);
+                vyq[0] = vyq[1]; vyq[1] = vyq[2]; vyq[2] = vyq[3];  // queue rows F-4..F-1
+                vyq[3] = e_ld8(R.row(u, 1) + x);
                 if (r >= y0 && r < y1) {
+                    const int kr = r - y0;
+                    if (tid == 0 && r + 1 < y1) {  // own slot (kr+1)&1 was last read before the previous barrier
+                        fence_proxy_async_smem();
+                        issue_own(kr + 1);
+                    }
+                    mbar_wait(&R.obar[kr & 1], (uint32_t)((kr >> 1) & 1));
                     if (r < P.sxx.rows) {
                         const E8 vxr = e_ld8(R.row(u, 2) + x);  // vx[r], own cells
                         const E8 dvx = e_xfold<ORDER>(c, R.row(u, 2), x, xl, xr, true);
                         // vy rows r-2..r+1 were queued at iterations i-3..i
-                        const E8 dvs = e_sfold<ORDER>(c, vyq[(u + 1) % ER], vyq[(u + 2) % ER], vyq[(u + 3) % ER], vyq[u]);
+                        const E8 dvs = e_sfold<ORDER>(c, vyq[0], vyq[1], vyq[2], vyq[3]);
                         const int sg = (int)P.sxx.row0 + r;
                         const bool surf = P.fs && (sg == 0 || sg == (int)P.sxx.nglob - 1);
                         const bool sk = src_here && r == P.src_s;
                         const int sj = (int)((P.src_x - x) >> 1), sl = (int)((P.src_x - x) & 1);
-                        const int64_t off = (int64_t)r * pitch + x;
-                        const E8 sxx_old = e_ld8(reinterpret_cast<__half*>(P.sxx.base) + off);
-                        const E8 sss_old = e_ld8(reinterpret_cast<__half*>(P.sss.base) + off);
+                        const E8 sxx_old = e_ld8(R.orow(kr & 1, 0) + x);
+                        const E8 sss_old = e_ld8(R.orow(kr & 1, 1) + x);
                         E8 sxx = sxx_old, sss = sss_old;
-                        E8 rsxx = comp ? e_ld8(reinterpret_cast<__half*>(P.rsxx.base) + off) : E8{};
-                        E8 rsss = comp ? e_ld8(reinterpret_cast<__half*>(P.rsss.base) + off) : E8{};
+                        E8 rsxx = comp ? e_ld8(R.orow(kr & 1, 3) + x) : E8{};
+                        E8 rsss = comp ? e_ld8(R.orow(kr & 1, 4) + x) : E8{};
 #pragma unroll
                         for (int j = 0; j < 4; j++) {
                             const EH2 stiff = pload<16, 2>(P.stiff, r, 0, x + 2 * j);
@@ -382,12 +429,11 @@ __global__ void __launch_bounds__(512, 1) k_el2d_stress_stream(ElParams P, int64
                     }
                     if (r < P.sxs.rows) {  // sxy = fl(mu fl(dds vx + ddx vy)) (elastic.py:232-238)
                         // vx rows r-1..r+2 were queued at iterations i-2..i (row r+2 is this slot)
-                        const E8 dvxy = e_sfold<ORDER>(c, vxq[(u + 1) % ER], vxq[(u + 2) % ER], vxq[(u + 3) % ER], vxq[u]);
+                        const E8 dvxy = e_sfold<ORDER>(c, vxq[0], vxq[1], vxq[2], vxq[3]);
                         const E8 dvyx = e_xfold<ORDER>(c, R.row((u + ER - 1) % ER, 1), x, xl, xr, false);
-                        const int64_t off = (int64_t)r * pitch + x;
-                        const E8 old = e_ld8(reinterpret_cast<__half*>(P.sxs.base) + off);
+                        const E8 old = e_ld8(R.orow(kr & 1, 2) + x);
                         E8 s = old;
-                        E8 rs = comp ? e_ld8(reinterpret_cast<__half*>(P.rsxs.base) + off) : E8{};
+                        E8 rs = comp ? e_ld8(R.orow(kr & 1, 5) + x) : E8{};
 #pragma unroll
                         for (int j = 0; j < 4; j++) {
                             const EH2 mu = pload<16, 2>(P.mu_n, r, 0, x + 2 * j);
@@ -401,7 +447,7 @@ __global__ void __launch_bounds__(512, 1) k_el2d_stress_stream(ElParams P, int64
                             e_track(acc[5], rs);
                         }
                         if (sample) {  // kinetic y + shear energy at this half row
-                            const E8 vyr = vyq[(u + 3) % ER];  // vy[r] was queued one iteration ago
+                            const E8 vyr = vyq[2];  // vy[r] was queued one iteration ago
 #pragma unroll
                             for (int k = 0; k < ECPT; k++) {
                                 const int xi = x + k;
@@ -434,7 +480,7 @@ __global__ void __launch_bounds__(512, 1) k_el2d_stress_stream(ElParams P, int64
 
 // ---------------------------------------------------------------- host side
 
-size_t el2d_stream_smem_bytes(int64_t nx) { return 128 + (size_t)ER * ENS * nx * sizeof(__half); }
+size_t el2d_stream_smem_bytes(int64_t nx) { return 128 + (size_t)(ER * ENS + 2 * EOWN) * nx * sizeof(__half); }
 
 bool el2d_stream_eligible(int64_t nx, int max_smem) {
     return nx % 256 == 0 && nx / ECPT <= 512 && el2d_stream_smem_bytes(nx) <= (size_t)max_smem;
