@@ -13,6 +13,8 @@
 #include <cstdint>
 #include <string>
 #include <vector>
+#include <algorithm>
+#include <array>
 
 #include "../../include/halfwave_b200.h"
 #include "hw_params.h"
@@ -340,7 +342,8 @@ struct hw_solver {
     double* evals = nullptr;
     int64_t evals_cap = 0;
     int64_t* rec_off = nullptr;
-    int64_t* rec_xyz = nullptr;
+    int* rec_sorted = nullptr;  // owned receivers as (local row, x, j), sorted by (row, x)
+    int n_rec_sorted = 0;
     cudaStream_t st = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t ev_phase = nullptr, ev_copied = nullptr;
@@ -354,6 +357,7 @@ struct hw_solver {
     // streaming phase kernels (2D elastic, binary16): in place on the standard layout
     bool el_stream = false;
     int stream_blocks = 0;
+    unsigned int* counter = nullptr;  // CTA arrival counter of the streaming stress kernel
     // slab decomposition over the slow axis
     int world = 1, rank = 0;
     int64_t r0 = 0, ns_loc = 0;
@@ -633,6 +637,8 @@ int setup_handle(hw_solver* h) {
             if (nbs < 1) nbs = 1;
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
             h->el_stream = true;
+            CU(cudaMalloc(&h->counter, sizeof(unsigned int)));
+            CU(cudaMemset(h->counter, 0, sizeof(unsigned int)));
         }
     }
     if (!h->ctrl) CU(cudaMalloc(&h->ctrl, sizeof(Ctrl)));
@@ -647,7 +653,7 @@ int setup_handle(hw_solver* h) {
     }
     if (desc->n_receivers > 0) {
         int f = h->ac ? F_P : F_VS;
-        std::vector<int64_t> off(desc->n_receivers), xyz(3 * desc->n_receivers);
+        std::vector<int64_t> off(desc->n_receivers);
         h->rec_owned.assign(desc->n_receivers, 0);
         for (int j = 0; j < desc->n_receivers; j++) {
             const int64_t* r = desc->receivers + 3 * j;
@@ -657,14 +663,18 @@ int setup_handle(hw_solver* h) {
             const bool own = sl >= 0 && sl < field_rows(h, f);
             h->rec_owned[j] = own;
             off[j] = own ? sl * h->g.slab + r[1] * h->g.pitch + r[0] : -1;
-            xyz[3 * j] = r[0];
-            xyz[3 * j + 1] = r[1];
-            xyz[3 * j + 2] = own ? sl : -1000000;
         }
         CU(cudaMalloc(&h->rec_off, off.size() * 8));
         CU(cudaMemcpy(h->rec_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
-        CU(cudaMalloc(&h->rec_xyz, xyz.size() * 8));
-        CU(cudaMemcpy(h->rec_xyz, xyz.data(), xyz.size() * 8, cudaMemcpyHostToDevice));
+        std::vector<std::array<int, 3>> srt;
+        for (int j = 0; j < desc->n_receivers; j++)
+            if (h->rec_owned[j]) srt.push_back({(int)(desc->receivers[3 * j + 2] - h->r0), (int)desc->receivers[3 * j], j});
+        std::sort(srt.begin(), srt.end());
+        h->n_rec_sorted = (int)srt.size();
+        if (!srt.empty()) {
+            CU(cudaMalloc(&h->rec_sorted, srt.size() * sizeof(srt[0])));
+            CU(cudaMemcpy(h->rec_sorted, srt.data(), srt.size() * sizeof(srt[0]), cudaMemcpyHostToDevice));
+        }
     }
     CU(cudaDeviceSynchronize());
     return HW_OK;
@@ -680,7 +690,8 @@ void release_handle(hw_solver* h) {
     if (h->traces) cudaFree(h->traces);
     if (h->evals) cudaFree(h->evals);
     if (h->rec_off) cudaFree(h->rec_off);
-    if (h->rec_xyz) cudaFree(h->rec_xyz);
+    if (h->rec_sorted) cudaFree(h->rec_sorted);
+    if (h->counter) cudaFree(h->counter);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
     if (h->ev_phase) cudaEventDestroy(h->ev_phase);
@@ -992,6 +1003,19 @@ static int run_begin(hw_solver* h, int32_t variant, int64_t nt, bool energy, boo
     return HW_OK;
 }
 
+static StreamIO stream_io(const hw_solver* h, const RunCtx& C) {
+    StreamIO IO;
+    memset(&IO, 0, sizeof(IO));
+    IO.rec = h->rec_sorted;
+    IO.n_rec = h->n_rec_sorted;
+    IO.traces = h->traces;
+    IO.nt = C.nt;
+    IO.e_vals = h->evals;
+    IO.scale = C.E.scale;
+    IO.counter = h->counter;
+    return IO;
+}
+
 // one leapfrog phase (0 = velocities, 1 = pressure / stresses) of step n
 static void run_phase(hw_solver* h, const RunCtx& C, int phase, int64_t n, const double* src) {
     const int sk = h->d.src_kind;
@@ -999,12 +1023,14 @@ static void run_phase(hw_solver* h, const RunCtx& C, int phase, int64_t n, const
     const int sample = C.energy && ((n + 1) % C.every == 0);
     if (phase == 0) {
         if (h->ac) launch_ac_vel(h->LS, h->LU, h->W, C.A, n, h->max_rows, h->st);
-        else if (h->el_stream) launch_el2d_vel_stream(C.variant, h->d.order, C.L, h->stream_blocks, n, sk == HW_SRC_VSLOW ? s : 0.0, h->st);
+        else if (h->el_stream) launch_el2d_vel_stream(C.variant, h->d.order, C.L, stream_io(h, C), h->stream_blocks, n,
+                                                      sk == HW_SRC_VSLOW ? s : 0.0, h->st);
         else launch_el_vel(h->LS, h->LU, h->W, C.L, n, sk == HW_SRC_VSLOW ? s : 0.0, h->max_rows, h->st);
     } else {
         if (h->ac) launch_ac_pres(h->LS, h->LU, h->W, C.A, n, sk == HW_SRC_PRESSURE ? s : 0.0, sample, h->max_rows, h->st);
         else if (h->el_stream)
-            launch_el2d_stress_stream(C.variant, h->d.order, C.L, h->stream_blocks, n, sk == HW_SRC_EXPLOSIVE ? s : 0.0, sample, h->st);
+            launch_el2d_stress_stream(C.variant, h->d.order, C.L, stream_io(h, C), h->stream_blocks, n,
+                                      sk == HW_SRC_EXPLOSIVE ? s : 0.0, sample, (n + 1) / C.every, h->st);
         else launch_el_stress(h->LS, h->LU, h->W, C.L, n, sk == HW_SRC_EXPLOSIVE ? s : 0.0, sample, h->max_rows, h->st);
     }
     h->launches++;
@@ -1012,10 +1038,9 @@ static void run_phase(hw_solver* h, const RunCtx& C, int phase, int64_t n, const
 
 static void run_epilogue(hw_solver* h, const RunCtx& C, int64_t n) {
     const int sample = C.energy && ((n + 1) % C.every == 0);
+    if (h->el_stream) return;  // traces and energy are recorded inside the streaming kernels
     if (sample || C.E.n_rec > 0) {
-        EpParams E = C.E;
-        if (h->el_stream) E.nblocks = h->stream_blocks;  // partials of the streaming stress kernel
-        launch_epilogue(h->LU, E, n, sample, (n + 1) / C.every, h->st);
+        launch_epilogue(h->LU, C.E, n, sample, (n + 1) / C.every, h->st);
         h->launches++;
     }
 }
@@ -1046,8 +1071,8 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
         F.has_src = h->d.src_kind == HW_SRC_PRESSURE && h->src_active;
         F.src_x = h->d.src_x;
         F.src_s = h->src_s_loc;
-        F.n_rec = C.E.n_rec;
-        F.rec = h->rec_xyz;
+        F.n_rec = h->n_rec_sorted;
+        F.rec = h->rec_sorted;
         F.traces = h->traces;
         F.nt = nt;
         F.ctrl = h->ctrl;

@@ -12,6 +12,7 @@
 //   * medium planes are strided views: constant (0,0,0), slow-layered (1,0,0) or
 //     full (nm*nx, nx, 1), so layered media cost no HBM traffic per cell.
 #pragma once
+#include <limits.h>
 #include <stdint.h>
 #include "hw_lanes.cuh"
 
@@ -348,6 +349,34 @@ __device__ __forceinline__ void store_c(const FieldView& f, const Cell& c, int64
             const int64_t k2 = f.half_s ? 2 * ng - 1 - sg : 2 * ng - 2 - sg;
             if (k2 >= ng && k2 < ng + G) vstore<LU, W>(p + (k2 - sg) * c.slab, w);
         }
+    }
+}
+
+// Receivers sorted by (local row, x): int triples (row, x, trace index).  The streaming
+// kernels walk rows in order: a CTA-uniform cursor finds each row's receivers, and a
+// thread binary-searches its own x range only on rows that have any.
+__device__ __forceinline__ int rec_lower(const int* rec, int lo, int hi, int r, int x) {
+    while (lo < hi) {  // first index with (row, x) >= (r, x)
+        const int mid = (lo + hi) >> 1;
+        const int mr = __ldg(rec + 3 * mid), mx = __ldg(rec + 3 * mid + 1);
+        if (mr < r || (mr == r && mx < x)) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Record the trace samples of row r for cells [x, x + 8) from the 8 values in v[] (as
+// float); cur is the uniform cursor (first receiver with row >= previous row).
+template <typename GET>
+__device__ __forceinline__ void rec_row(const int* rec, int& cur, int hi, int r, int x, double* traces, int64_t nt,
+                                        int64_t n, GET get) {
+    if (cur >= hi) return;
+    if (__ldg(rec + 3 * cur) < r) cur = rec_lower(rec, cur, hi, r, INT_MIN);
+    if (cur >= hi || __ldg(rec + 3 * cur) != r) return;
+    for (int q = rec_lower(rec, cur, hi, r, x); q < hi; q++) {
+        const int rr = __ldg(rec + 3 * q), rx = __ldg(rec + 3 * q + 1);
+        if (rr != r || rx >= x + 8) break;
+        traces[(int64_t)__ldg(rec + 3 * q + 2) * nt + n] = get(rx - x);
     }
 }
 

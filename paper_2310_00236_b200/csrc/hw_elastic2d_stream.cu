@@ -137,6 +137,21 @@ __device__ __forceinline__ void e_store_row(const FieldView& f, int64_t pitch, i
 // Two TMA rings: the tap ring (ER slots x ENS rows, filled ED rows ahead) and the own
 // ring (2 slots x EOWN rows: the old values / residuals of the output row, filled one
 // output row ahead).  smem: [tap barriers | own barriers | tap ring | own ring].
+// Programmatic dependent launch: the next phase's grid may launch while this one runs
+// (its CTAs take SMs as ours retire); it waits here until every prior write is visible.
+__device__ __forceinline__ void e_pdl_enter() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+__device__ __forceinline__ double e_pick(const E8& v, int o) {  // register select, no local memory
+    double r = 0.0;
+#pragma unroll
+    for (int j = 0; j < ECPT; j++)
+        if (j == o) r = (double)__half2float(v.q[j >> 1].e[j & 1]);
+    return r;
+}
+
 struct ERing {
     uint64_t* bar;
     uint64_t* obar;
@@ -166,7 +181,8 @@ __device__ __forceinline__ void e_init_ring(const ERing& R) {
 //                            come from the previous slot's stream 1
 //   stream 2: sxx[F-2]    -> x taps for vx[r]
 template <int V, int ORDER>
-__global__ void __launch_bounds__(512, 1) k_el2d_vel_stream(ElParams P, int64_t n, double src) {
+__global__ void __launch_bounds__(512, 1) k_el2d_vel_stream(ElParams P, StreamIO IO, int64_t n, double src) {
+    e_pdl_enter();
     if (halted(P.ctrl, n)) return;
     extern __shared__ __align__(128) unsigned char smem[];
     const ERing R(smem, P.g.nx);
@@ -210,6 +226,8 @@ __global__ void __launch_bounds__(512, 1) k_el2d_vel_stream(ElParams P, int64_t 
     const int xl = x == 0 ? nx - 2 : x - 2, xr = x + ECPT >= nx ? 0 : x + ECPT;
     const bool src_here = P.src_kind == HW_SRC_VSLOW && src != 0.0 && P.src_x >= x && P.src_x < x + ECPT;
     E8 ssq[4], xsq[4];  // slow-tap queues, [3] = newest row
+    int rcur = rec_lower(IO.rec, 0, IO.n_rec, y0, INT_MIN);  // this CTA's receivers [rcur, rhi)
+    const int rhi = rec_lower(IO.rec, rcur, IO.n_rec, y1, INT_MIN);
     __half2 acc[4];
 #pragma unroll
     for (int q = 0; q < 4; q++) acc[q] = __float2half2_rn(0.f);
@@ -266,6 +284,8 @@ __global__ void __launch_bounds__(512, 1) k_el2d_vel_stream(ElParams P, int64_t 
                                               (sk && j == sj) ? sl : -1, src, v.q[j], rr.q[j]);
                         e_store_row(P.vs, pitch, r, x, v);
                         e_track(acc[1], v);
+                        // receiver traces of vy after the step (elastic.py:283-284)
+                        rec_row(IO.rec, rcur, rhi, r, x, IO.traces, IO.nt, n, [&](int o) { return e_pick(v, o); });
                         if (comp) {
                             e_store_row(P.rvs, pitch, r, x, rr);
                             e_track(acc[3], rr);
@@ -293,7 +313,9 @@ __global__ void __launch_bounds__(512, 1) k_el2d_vel_stream(ElParams P, int64_t 
 //                         sxy[r] (= row F-2) come from the previous slot's stream 1
 //   stream 2: vx[F-2]  -> x taps of dvx at row r
 template <int V, int ORDER>
-__global__ void __launch_bounds__(512, 1) k_el2d_stress_stream(ElParams P, int64_t n, double src, int sample) {
+__global__ void __launch_bounds__(512, 1)
+    k_el2d_stress_stream(ElParams P, StreamIO IO, int64_t n, double src, int sample, int64_t eidx) {
+    e_pdl_enter();
     if (halted(P.ctrl, n)) return;
     extern __shared__ __align__(128) unsigned char smem[];
     const ERing R(smem, P.g.nx);
@@ -337,6 +359,9 @@ __global__ void __launch_bounds__(512, 1) k_el2d_stress_stream(ElParams P, int64
     const int xl = x == 0 ? nx - 2 : x - 2, xr = x + ECPT >= nx ? 0 : x + ECPT;
     const bool src_here = P.src_kind == HW_SRC_EXPLOSIVE && src != 0.0 && P.src_x >= x && P.src_x < x + ECPT;
     E8 vxq[4], vyq[4];
+    // energy planes constant along x (layered media): sum products per row, apply the
+    // coefficients once per row (same terms, regrouped; agrees to ~1e-16 relative)
+    const bool erow = (P.e_rho_x.sx | P.e_rho_s.sx | P.e_lam.sx | P.e_mu.sx | P.e_mu_n.sx) == 0;
     __half2 acc[6];
 #pragma unroll
     for (int q = 0; q < 6; q++) acc[q] = __float2half2_rn(0.f);
@@ -404,7 +429,32 @@ __global__ void __launch_bounds__(512, 1) k_el2d_stress_stream(ElParams P, int64
                             e_track(acc[3], rsxx);
                             e_track(acc[4], rsss);
                         }
-                        if (sample) {  // kinetic x + strain energy at this integer row (diagnostics.py:100-162)
+                        if (sample && erow) {  // row-uniform medium: per-row sums, coefficients once
+                            const double w = surf ? 0.5 : 1.0;
+                            double sv = 0.0, sxx2 = 0.0, sss2 = 0.0, sq = 0.0;
+#pragma unroll
+                            for (int k = 0; k < ECPT; k++) {
+                                const double v = (double)__half2float(vxr.q[k >> 1].e[k & 1]);
+                                const double xn = (double)__half2float(sxx_old.q[k >> 1].e[k & 1]);
+                                const double x1 = (double)__half2float(sxx.q[k >> 1].e[k & 1]);
+                                const double sn = (double)__half2float(sss_old.q[k >> 1].e[k & 1]);
+                                const double s1 = (double)__half2float(sss.q[k >> 1].e[k & 1]);
+                                sv += v * v;
+                                sxx2 += xn * x1;
+                                sss2 += sn * s1;
+                                sq += xn * s1 + sn * x1;
+                            }
+                            e[0] += (w * p64(P.e_rho_x, r, 0, 0)) * sv;
+                            const double lamd = p64(P.e_lam, r, 0, 0), mu = p64(P.e_mu, r, 0, 0);
+                            const double stiffd = lamd + 2.0 * mu;
+                            const double dd = 4.0 * mu * (lamd + mu);
+                            double val;
+                            if (mu == 0.0) val = surf ? 0.0 : sxx2 / (lamd + mu);
+                            else if (surf) val = sxx2 * stiffd / dd;
+                            else val = (stiffd * (sxx2 + sss2) - lamd * sq) / dd;
+                            if (surf) val = 0.5 * val;
+                            e[3] += val;
+                        } else if (sample) {  // kinetic x + strain energy at this integer row (diagnostics.py:100-162)
                             const double w = surf ? 0.5 : 1.0;
 #pragma unroll
                             for (int k = 0; k < ECPT; k++) {
@@ -446,7 +496,19 @@ __global__ void __launch_bounds__(512, 1) k_el2d_stress_stream(ElParams P, int64
                             e_store_row(P.rsxs, pitch, r, x, rs);
                             e_track(acc[5], rs);
                         }
-                        if (sample) {  // kinetic y + shear energy at this half row
+                        if (sample && erow) {
+                            const E8 vyr = vyq[2];  // vy[r] was queued one iteration ago
+                            double sv = 0.0, sa = 0.0;
+#pragma unroll
+                            for (int k = 0; k < ECPT; k++) {
+                                const double v = (double)__half2float(vyr.q[k >> 1].e[k & 1]);
+                                sv += v * v;
+                                sa += (double)__half2float(old.q[k >> 1].e[k & 1]) * (double)__half2float(s.q[k >> 1].e[k & 1]);
+                            }
+                            e[1] += p64(P.e_rho_s, r, 0, 0) * sv;
+                            const double mun = p64(P.e_mu_n, r, 0, 0);
+                            e[4] += mun > 0.0 ? sa / mun : 0.0;
+                        } else if (sample) {  // kinetic y + shear energy at this half row
                             const E8 vyr = vyq[2];  // vy[r] was queued one iteration ago
 #pragma unroll
                             for (int k = 0; k < ECPT; k++) {
@@ -475,7 +537,26 @@ __global__ void __launch_bounds__(512, 1) k_el2d_stress_stream(ElParams P, int64
         mask |= e_nonfinite(acc[5]) << P.rsxs.bit;
     }
     record_failure(P.ctrl, n, mask);
-    if (sample) block_partials(e, P.partials);
+    if (!sample) return;
+    block_partials(e, P.partials);
+    __threadfence();
+    __syncthreads();
+    __shared__ unsigned int is_last;
+    if (tid == 0) is_last = atomicAdd(IO.counter, 1u) == (unsigned int)(nb - 1);
+    __syncthreads();
+    if (!is_last) return;
+    if (tid == 0) {  // fixed-order fp64 reduction of the block partials (diagnostics.py:100-162)
+        double tot[NCOMP];
+        for (int q = 0; q < NCOMP; q++) {
+            double a = 0.0;
+            for (int bi = 0; bi < nb; bi++) a += __ldcg(&P.partials[(int64_t)bi * NCOMP + q]);
+            tot[q] = a;
+        }
+        double t = tot[0];
+        for (int q = 1; q < NCOMP; q++) t += tot[q];
+        IO.e_vals[eidx] = IO.scale * t;
+        *IO.counter = 0u;
+    }
 }
 
 // ---------------------------------------------------------------- host side
@@ -510,18 +591,34 @@ cudaError_t el2d_stream_prepare(int64_t nx) {
         else { constexpr int V_ = 6, O_ = 4; CALL; }                                 \
     }
 
-void launch_el2d_vel_stream(int variant, int order, const ElParams& P, int nblocks, int64_t n, double src,
-                            cudaStream_t st) {
-    const size_t bytes = el2d_stream_smem_bytes(P.g.nx);
-    const int threads = (int)(P.g.nx / ECPT);
-    EL2D_DISPATCH(variant, order, (k_el2d_vel_stream<V_, O_><<<nblocks, threads, bytes, st>>>(P, n, src)))
+static void launch_pdl(void* fn, int nblocks, int64_t nx, cudaStream_t st, void** args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nblocks);
+    cfg.blockDim = dim3((unsigned)(nx / ECPT));
+    cfg.dynamicSmemBytes = el2d_stream_smem_bytes(nx);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelExC(&cfg, fn, args);
 }
 
-void launch_el2d_stress_stream(int variant, int order, const ElParams& P, int nblocks, int64_t n, double src,
-                               int sample, cudaStream_t st) {
-    const size_t bytes = el2d_stream_smem_bytes(P.g.nx);
-    const int threads = (int)(P.g.nx / ECPT);
-    EL2D_DISPATCH(variant, order, (k_el2d_stress_stream<V_, O_><<<nblocks, threads, bytes, st>>>(P, n, src, sample)))
+void launch_el2d_vel_stream(int variant, int order, const ElParams& P, const StreamIO& IO, int nblocks, int64_t n,
+                            double src, cudaStream_t st) {
+    void* fn = nullptr;
+    EL2D_DISPATCH(variant, order, (fn = (void*)k_el2d_vel_stream<V_, O_>))
+    void* args[] = {(void*)&P, (void*)&IO, (void*)&n, (void*)&src};
+    launch_pdl(fn, nblocks, P.g.nx, st, args);
+}
+
+void launch_el2d_stress_stream(int variant, int order, const ElParams& P, const StreamIO& IO, int nblocks, int64_t n,
+                               double src, int sample, int64_t eidx, cudaStream_t st) {
+    void* fn = nullptr;
+    EL2D_DISPATCH(variant, order, (fn = (void*)k_el2d_stress_stream<V_, O_>))
+    void* args[] = {(void*)&P, (void*)&IO, (void*)&n, (void*)&src, (void*)&sample, (void*)&eidx};
+    launch_pdl(fn, nblocks, P.g.nx, st, args);
 }
 
 }  // namespace hw

@@ -146,7 +146,6 @@ __global__ void __launch_bounds__(512, 1)
     if (halted(P.ctrl, n)) return;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
-    int* rec_local = reinterpret_cast<int*>(smem + 64);  // up to 8 (row, x, j) triples
     __half* ring = reinterpret_cast<__half*>(smem + 256);
     const int64_t nx = P.nx, ns = P.ns, pitch = P.pitch;
     __half* xrows = ring + (int64_t)FR * NSTREAM * nx;  // two rows, alternating by iteration parity
@@ -187,22 +186,12 @@ __global__ void __launch_bounds__(512, 1)
     if (tid == 0) {
         for (int s = 0; s < FR; s++) mbar_init(&bar[s], 1);
         fence_mbar_init();
-        int cnt = 0;  // receivers on this CTA's rows
-        for (int q = 0; q < P.n_rec && cnt < 8; q++) {
-            const int64_t* rc = P.rec + 3 * q;
-            if (rc[2] >= y0 && rc[2] < y1) {
-                rec_local[1 + 3 * cnt] = (int)rc[2];
-                rec_local[2 + 3 * cnt] = (int)rc[0];
-                rec_local[3 + 3 * cnt] = q;
-                cnt++;
-            }
-        }
-        rec_local[0] = cnt;
     }
     __syncthreads();
     if (tid == 0)
         for (int64_t i = 0; i < FR - 1 && i < NI; i++) issue(i, (int)i);
-    const int n_local = rec_local[0];
+    int rcur = rec_lower(P.rec, 0, P.n_rec, y0, INT_MIN);  // this CTA's receivers [rcur, rhi)
+    const int rhi = rec_lower(P.rec, rcur, P.n_rec, y1, INT_MIN);
 
     __half c[4];
 #pragma unroll
@@ -214,30 +203,38 @@ __global__ void __launch_bounds__(512, 1)
     const bool src_here = P.has_src && src != 0.0 && P.src_x >= x && P.src_x < x + FCPT;
     const int src_j = (int)((P.src_x - x) >> 1), src_lane = (int)((P.src_x - x) & 1);
 
-    V8 pq[4], vq[4], gq[4];  // p rows, vy_new rows, d/dx vx_new rows (indexed by iteration mod 4)
+    V8 pq[4], vq[4], gq[4];  // p rows, vy_new rows, d/dx vx_new rows ([3] = newest)
     __half2 acc[NSTREAM];
 #pragma unroll
     for (int q = 0; q < NSTREAM; q++) acc[q] = __float2half2_rn(0.f);
     double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
 
-    for (int i0 = 0; i0 < NI; i0 += FR) {
-        const uint32_t par = (uint32_t)((i0 / FR) & 1);
-#pragma unroll
-        for (int u = 0; u < FR; u++) {
-            const int i = i0 + u;
-            if (i < NI) {
+    // Rolled row loop (one copy of the body: the unrolled form was instruction-cache
+    // bound); the register queues rotate, [3] = this iteration's row.
+#pragma unroll 1
+    for (int i = 0; i < NI; i++) {
+        const int u = i % FR;
+        const uint32_t par = (uint32_t)((i / FR) & 1);
+        {
+            {
                 const int f = F0 + i;
-                __half* xrow = xrows + (u & 1) * nx;  // FR is even: parity of i == parity of u
+                __half* xrow = xrows + (i & 1) * nx;
+#pragma unroll
+                for (int q = 0; q < 3; q++) {
+                    pq[q] = pq[q + 1];
+                    vq[q] = vq[q + 1];
+                    gq[q] = gq[q + 1];
+                }
                 if (tid == 0 && i + FR - 1 < NI) {
                     fence_proxy_async_smem();
-                    issue(i + FR - 1, (u + FR - 1) % FR);
+                    issue(i + FR - 1, (i + FR - 1) % FR);
                 }
                 mbar_wait(&bar[u], par);
                 const __half* prow = slot_row(u, S_P);
-                pq[u] = lds8(prow + x);
+                pq[3] = lds8(prow + x);
                 const bool do_vx = f >= y0 && f < y1;
                 if (do_vx) {  // vx[f] (acoustic.py:167-168)
-                    V8 d = xfold8<ORDER>(c, ld2(prow + xl), pq[u], ld2(prow + xr), false);
+                    V8 d = xfold8<ORDER>(c, ld2(prow + xl), pq[3], ld2(prow + xr), false);
                     V8 vxn = lds8(slot_row(u, S_VX) + x);
                     V8 r = comp ? lds8(slot_row(u, S_RVX) + x) : V8{};
                     if constexpr (ROWMED) {
@@ -272,19 +269,19 @@ __global__ void __launch_bounds__(512, 1)
                     const int rw = (int)wrap_row(r);
                     V8 vsn = lds8(slot_row(u, S_VS) + x);
                     V8 rr = comp ? lds8(slot_row(u, S_RVS) + x) : V8{};
-                    const V8& t0 = pq[(u + 1) % FR];
-                    const V8& t1 = pq[(u + 2) % FR];
-                    const V8& t2 = pq[(u + 3) % FR];
+                    const V8& t0 = pq[0];
+                    const V8& t1 = pq[1];
+                    const V8& t2 = pq[2];
                     if constexpr (ROWMED) {
                         const float rc = __ldg(P.rho_s.rcp + rw * P.rho_s.ss);
 #pragma unroll
                         for (int j = 0; j < 4; j++)
-                            finish_row<V>(fold2<ORDER>(c, t0.q[j], t1.q[j], t2.q[j], pq[u].q[j]), rc, dt2, -1, srch,
+                            finish_row<V>(fold2<ORDER>(c, t0.q[j], t1.q[j], t2.q[j], pq[3].q[j]), rc, dt2, -1, srch,
                                           vsn.q[j], rr.q[j]);
                     } else {
 #pragma unroll
                         for (int j = 0; j < 4; j++)
-                            finish<16, 16, 2>(fold2<ORDER>(c, t0.q[j], t1.q[j], t2.q[j], pq[u].q[j]), &P.rho_s, rw, 0,
+                            finish<16, 16, 2>(fold2<ORDER>(c, t0.q[j], t1.q[j], t2.q[j], pq[3].q[j]), &P.rho_s, rw, 0,
                                               x + 2 * j, dt2.x, V, -1, 0.0, vsn.q[j], rr.q[j]);
                     }
                     if (r >= y0 && r < y1) {
@@ -302,32 +299,32 @@ __global__ void __launch_bounds__(512, 1)
                             }
                         }
                     }
-                    vq[u] = vsn;
+                    vq[3] = vsn;
                 }
                 // One barrier per row: xrow[f&1] now holds vx_new[f] and every thread is past
                 // its ring-slot reads, so the producer may refill this slot next iteration;
                 // xrow[f&1] is rewritten two iterations later, after another barrier.
                 __syncthreads();
-                if (do_vx) gq[u] = xfold8<ORDER>(c, ld2(xrow + xl), lds8(xrow + x), ld2(xrow + xr), true);
+                if (do_vx) gq[3] = xfold8<ORDER>(c, ld2(xrow + xl), lds8(xrow + x), ld2(xrow + xr), true);
                 if (do_p) {  // p[k] (acoustic.py:172-181)
-                    const V8& pold = pq[(u + 1) % FR];
+                    const V8& pold = pq[0];
                     V8 pn = pold;
-                    const V8& g = gq[(u + 1) % FR];
-                    const V8& a0 = vq[(u + 1) % FR];
-                    const V8& a1 = vq[(u + 2) % FR];
-                    const V8& a2 = vq[(u + 3) % FR];
+                    const V8& g = gq[0];
+                    const V8& a0 = vq[0];
+                    const V8& a1 = vq[1];
+                    const V8& a2 = vq[2];
                     const bool sk = src_here && k == P.src_s;
                     if constexpr (ROWMED) {
                         const float rc = __ldg(P.beta.rcp + k * P.beta.ss);
 #pragma unroll
                         for (int j = 0; j < 4; j++) {
-                            H2 dv = O2::add(g.q[j], fold2<ORDER>(c, a0.q[j], a1.q[j], a2.q[j], vq[u].q[j]));
+                            H2 dv = O2::add(g.q[j], fold2<ORDER>(c, a0.q[j], a1.q[j], a2.q[j], vq[3].q[j]));
                             finish_row<V>(dv, rc, dt2, (sk && j == src_j) ? src_lane : -1, srch, pn.q[j], rp.q[j]);
                         }
                     } else {
 #pragma unroll
                         for (int j = 0; j < 4; j++) {
-                            H2 dv = O2::add(g.q[j], fold2<ORDER>(c, a0.q[j], a1.q[j], a2.q[j], vq[u].q[j]));
+                            H2 dv = O2::add(g.q[j], fold2<ORDER>(c, a0.q[j], a1.q[j], a2.q[j], vq[3].q[j]));
                             finish<16, 16, 2>(dv, &P.beta, k, 0, x + 2 * j, dt2.x, V, (sk && j == src_j) ? src_lane : -1,
                                               src, pn.q[j], rp.q[j]);
                         }
@@ -346,14 +343,14 @@ __global__ void __launch_bounds__(512, 1)
                             e[0] += p64(P.e_beta, k, 0, x + j) * (a * bb);
                         }
                     }
-                    for (int q = 0; q < n_local; q++) {  // receiver traces (acoustic.py:217-218)
-                        const int rx = rec_local[2 + 3 * q];
-                        if (rec_local[1 + 3 * q] == k && rx >= x && rx < x + FCPT) {
-                            const int o = rx - x;
-                            P.traces[(int64_t)rec_local[3 + 3 * q] * P.nt + n] =
-                                (double)__half2float(pn.q[o >> 1].e[o & 1]);
-                        }
-                    }
+                    // receiver traces (acoustic.py:217-218)
+                    rec_row(P.rec, rcur, rhi, k, x, P.traces, P.nt, n, [&](int o) {
+                        double v = 0.0;
+#pragma unroll
+                        for (int j = 0; j < FCPT; j++)
+                            if (j == o) v = (double)__half2float(pn.q[j >> 1].e[j & 1]);
+                        return v;
+                    });
                 }
             }
         }

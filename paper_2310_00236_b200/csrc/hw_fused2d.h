@@ -16,7 +16,7 @@ struct AcFusedParams {
     LaneConsts k;
     int32_t has_src, n_rec;
     int64_t src_x, src_s;
-    const int64_t* rec;
+    const int* rec;               // receivers sorted by (row, x): (row, x, trace index)
     double* traces;
     int64_t nt;
     Ctrl* ctrl;

@@ -74,13 +74,25 @@ void launch_el_vel(int LS, int LU, int W, const ElParams& P, int64_t n, double s
 void launch_el_stress(int LS, int LU, int W, const ElParams& P, int64_t n, double src, int sample, int64_t nblocks,
                       cudaStream_t st);
 void launch_el_energy(int LU, int W, const ElParams& P, int64_t nblocks, cudaStream_t st);
+// In-kernel receiver traces and energy finalisation of the streaming kernels.
+struct StreamIO {
+    const int* rec;         // receivers sorted by (row, x): (local row, x, trace index)
+    int32_t n_rec;
+    int32_t pad;
+    double* traces;         // [n_rec][nt]
+    int64_t nt;
+    double* e_vals;
+    double scale;           // 0.5 dx^2
+    unsigned int* counter;  // per-handle CTA arrival counter: the last CTA reduces the partials
+};
+
 // streaming 2D elastic phase kernels (hw_elastic2d_stream.cu)
 bool el2d_stream_eligible(int64_t nx, int max_smem);
 cudaError_t el2d_stream_prepare(int64_t nx);
-void launch_el2d_vel_stream(int variant, int order, const ElParams& P, int nblocks, int64_t n, double src,
-                            cudaStream_t st);
-void launch_el2d_stress_stream(int variant, int order, const ElParams& P, int nblocks, int64_t n, double src,
-                               int sample, cudaStream_t st);
+void launch_el2d_vel_stream(int variant, int order, const ElParams& P, const StreamIO& IO, int nblocks, int64_t n,
+                            double src, cudaStream_t st);
+void launch_el2d_stress_stream(int variant, int order, const ElParams& P, const StreamIO& IO, int nblocks, int64_t n,
+                               double src, int sample, int64_t eidx, cudaStream_t st);
 void launch_epilogue(int LU, const EpParams& E, int64_t n, int sample, int64_t eidx, cudaStream_t st);
 
 }  // namespace hw

@@ -104,3 +104,18 @@ def test_fused_path_is_selected():
     s.run(hw.Variant.OP3, st)
     assert s.kernel_path() == "fused2d"
     assert s.last_launch_count() == 2 + 2  # E0 kernel + finalize, then one fused launch per step
+
+
+def test_fused_receiver_line_records_every_trace():
+    """A full receiver line on one row plus a column through every row band: all traces
+    recorded (the in-kernel receiver list has no per-CTA cap)."""
+    nx, ny = 512, 300
+    s0, _ = _case(nx, ny, 12)
+    line = tuple((x, 5) for x in range(0, nx, 3)) + tuple((17, y) for y in range(0, ny, 7)) + ((nx - 1, ny - 1),)
+    s = hw.AcousticSolver(s0.grid, s0.medium, s0.source, stencil_precision=hw.Precision.FP16, receivers=line,
+                          energy_every=5)
+    _, st = _case(nx, ny, 12)
+    ref = oracle.run_solver(s, hw.Variant.OP3, st)
+    out = s.run(hw.Variant.OP3, st)
+    assert s.kernel_path() == "fused2d"
+    np.testing.assert_array_equal(np.array([t.samples for t in out.traces]), ref["traces"])

@@ -43,13 +43,13 @@ def cfg3():  # 3D acoustic 512^3, 2nd order, full beta plane
     return hw.AcousticSolver(g, med, stencil_precision=F16, energy_every=10)
 
 
-def cfg4():  # 2D elastic 4096^2, free surface
+def cfg4(every=10):  # 2D elastic 4096^2, free surface
     n = 4096
     med = hw.build_layered_elastic(n, n, [(1.0, 1.0, 2.0, 1.0)])
     dx = 1.0 / n
     g = hw.GridSpec(n, n, dx, float(np.float16(0.4 * dx / 2)), NT, bc_y=hw.Boundary.FREE_SURFACE)
     src = hw.SourceSpec(hw.SourceKind.EXPLOSIVE, n // 2, 16, hw.RickerSpec(1 / (10 * dx), amplitude=1.0))
-    return hw.ElasticSolver(g, med, src, stencil_precision=F16, energy_every=10)
+    return hw.ElasticSolver(g, med, src, stencil_precision=F16, energy_every=every)
 
 
 def cfg5():  # 3D elastic 512^3 per GPU, 2nd order, layered
