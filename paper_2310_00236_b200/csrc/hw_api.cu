@@ -355,7 +355,8 @@ struct hw_solver {
     int fused_blocks = 0;
     void* mem_b[2 * F_N] = {};
     // streaming phase kernels (2D elastic, binary16): in place on the standard layout
-    bool el_stream = false;
+    bool el_stream = false;   // streaming 2D elastic phases
+    bool ac3_stream = false;  // streaming 3D acoustic phases
     int stream_blocks = 0;
     unsigned int* counter = nullptr;  // CTA arrival counter of the streaming stress kernel
     // slab decomposition over the slow axis
@@ -637,6 +638,17 @@ int setup_handle(hw_solver* h) {
             if (nbs < 1) nbs = 1;
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
             h->el_stream = true;
+        }
+        if (want && h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
+            ac3d_stream_eligible(desc->nx, desc->nm, h->g.pitch, dev_smem)) {
+            if (ac3d_stream_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "streaming kernel setup failed");
+            const int64_t units = (desc->nm / (4096 / desc->nx)) * max_rows;
+            int64_t nbs = units / 4;
+            if (nbs < 1) nbs = 1;
+            h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
+            h->ac3_stream = true;
+        }
+        if (h->el_stream || h->ac3_stream) {
             CU(cudaMalloc(&h->counter, sizeof(unsigned int)));
             CU(cudaMemset(h->counter, 0, sizeof(unsigned int)));
         }
@@ -668,7 +680,9 @@ int setup_handle(hw_solver* h) {
         CU(cudaMemcpy(h->rec_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
         std::vector<std::array<int, 3>> srt;
         for (int j = 0; j < desc->n_receivers; j++)
-            if (h->rec_owned[j]) srt.push_back({(int)(desc->receivers[3 * j + 2] - h->r0), (int)desc->receivers[3 * j], j});
+            if (h->rec_owned[j])  // key (local slow row * nm + mid row, x)
+                srt.push_back({(int)((desc->receivers[3 * j + 2] - h->r0) * desc->nm + desc->receivers[3 * j + 1]),
+                               (int)desc->receivers[3 * j], j});
         std::sort(srt.begin(), srt.end());
         h->n_rec_sorted = (int)srt.size();
         if (!srt.empty()) {
@@ -1022,12 +1036,16 @@ static void run_phase(hw_solver* h, const RunCtx& C, int phase, int64_t n, const
     const double s = src ? src[n] : 0.0;
     const int sample = C.energy && ((n + 1) % C.every == 0);
     if (phase == 0) {
-        if (h->ac) launch_ac_vel(h->LS, h->LU, h->W, C.A, n, h->max_rows, h->st);
+        if (h->ac3_stream) launch_ac3d_vel_stream(C.variant, h->d.order, C.A, h->stream_blocks, n, h->st);
+        else if (h->ac) launch_ac_vel(h->LS, h->LU, h->W, C.A, n, h->max_rows, h->st);
         else if (h->el_stream) launch_el2d_vel_stream(C.variant, h->d.order, C.L, stream_io(h, C), h->stream_blocks, n,
                                                       sk == HW_SRC_VSLOW ? s : 0.0, h->st);
         else launch_el_vel(h->LS, h->LU, h->W, C.L, n, sk == HW_SRC_VSLOW ? s : 0.0, h->max_rows, h->st);
     } else {
-        if (h->ac) launch_ac_pres(h->LS, h->LU, h->W, C.A, n, sk == HW_SRC_PRESSURE ? s : 0.0, sample, h->max_rows, h->st);
+        if (h->ac3_stream)
+            launch_ac3d_pres_stream(C.variant, h->d.order, C.A, stream_io(h, C), h->stream_blocks, n,
+                                    sk == HW_SRC_PRESSURE ? s : 0.0, sample, (n + 1) / C.every, h->st);
+        else if (h->ac) launch_ac_pres(h->LS, h->LU, h->W, C.A, n, sk == HW_SRC_PRESSURE ? s : 0.0, sample, h->max_rows, h->st);
         else if (h->el_stream)
             launch_el2d_stress_stream(C.variant, h->d.order, C.L, stream_io(h, C), h->stream_blocks, n,
                                       sk == HW_SRC_EXPLOSIVE ? s : 0.0, sample, (n + 1) / C.every, h->st);
@@ -1038,7 +1056,7 @@ static void run_phase(hw_solver* h, const RunCtx& C, int phase, int64_t n, const
 
 static void run_epilogue(hw_solver* h, const RunCtx& C, int64_t n) {
     const int sample = C.energy && ((n + 1) % C.every == 0);
-    if (h->el_stream) return;  // traces and energy are recorded inside the streaming kernels
+    if (h->el_stream || h->ac3_stream) return;  // traces and energy are recorded inside the streaming kernels
     if (sample || C.E.n_rec > 0) {
         launch_epilogue(h->LU, C.E, n, sample, (n + 1) / C.every, h->st);
         h->launches++;
@@ -1280,7 +1298,7 @@ int64_t hw_last_launch_count(const hw_solver* h) { return h ? h->launches : 0; }
 
 const char* hw_kernel_path(const hw_solver* h) {
     if (!h) return "";
-    return h->fused ? "fused2d" : (h->el_stream ? "stream2d" : "generic");
+    return h->fused ? "fused2d" : (h->el_stream ? "stream2d" : (h->ac3_stream ? "stream3d" : "generic"));
 }
 
 double hw_last_kernel_ms(const hw_solver* h) { return h ? h->kernel_ms : 0.0; }

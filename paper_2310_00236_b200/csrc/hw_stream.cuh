@@ -1,0 +1,138 @@
+// hw_stream.cuh — helpers shared by the full-row streaming kernels (binary16 state):
+// 8 cells per thread as four half2, shared-memory row taps, register slow-axis queues,
+// write-through ghost stores, failure tracking and PDL entry.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "hw_common.cuh"
+
+namespace hw {
+
+constexpr int ECPT = 8;   // cells per thread
+
+using EH2 = vec<16, 2>;
+using EO2 = vops<16, 2>;
+
+struct E8 {
+    EH2 q[4];
+};
+
+__device__ __forceinline__ E8 e_ld8(const __half* p) {
+    E8 r;
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    *reinterpret_cast<unsigned int*>(&r.q[0].h2) = u.x;
+    *reinterpret_cast<unsigned int*>(&r.q[1].h2) = u.y;
+    *reinterpret_cast<unsigned int*>(&r.q[2].h2) = u.z;
+    *reinterpret_cast<unsigned int*>(&r.q[3].h2) = u.w;
+    return r;
+}
+
+__device__ __forceinline__ void e_st8(__half* p, const E8& v) {
+    uint4 u;
+    u.x = *reinterpret_cast<const unsigned int*>(&v.q[0].h2);
+    u.y = *reinterpret_cast<const unsigned int*>(&v.q[1].h2);
+    u.z = *reinterpret_cast<const unsigned int*>(&v.q[2].h2);
+    u.w = *reinterpret_cast<const unsigned int*>(&v.q[3].h2);
+    *reinterpret_cast<uint4*>(p) = u;
+}
+
+__device__ __forceinline__ EH2 e_ld2(const __half* p) {
+    EH2 r;
+    r.h2 = *reinterpret_cast<const __half2*>(p);
+    return r;
+}
+
+__device__ __forceinline__ E8 e_neg8(const E8& v) {
+    E8 r;
+#pragma unroll
+    for (int j = 0; j < 4; j++) r.q[j] = vneg<16, 2>(v.q[j]);
+    return r;
+}
+
+template <int ORDER>
+__device__ __forceinline__ EH2 e_fold(const __half c[4], EH2 t0, EH2 t1, EH2 t2, EH2 t3) {
+    EH2 inner = EO2::add(EO2::mul(vsplat<16, 2>(c[1]), t1), EO2::mul(vsplat<16, 2>(c[2]), t2));
+    if (ORDER == 2) return inner;
+    EH2 outer = EO2::add(EO2::mul(vsplat<16, 2>(c[0]), t0), EO2::mul(vsplat<16, 2>(c[3]), t3));
+    return EO2::add(inner, outer);
+}
+
+// x derivative of 8 cells (periodic) from a shared row; to_int: shifts (-2..1) else (-1..2)
+template <int ORDER>
+__device__ __forceinline__ E8 e_xfold(const __half c[4], const __half* row, int x, int xl, int xr, bool to_int) {
+    EH2 Q[6];
+    Q[0] = e_ld2(row + xl);
+    const E8 own = e_ld8(row + x);
+#pragma unroll
+    for (int j = 0; j < 4; j++) Q[j + 1] = own.q[j];
+    Q[5] = e_ld2(row + xr);
+    EH2 S[5];
+#pragma unroll
+    for (int j = 0; j < 5; j++) S[j] = vshift<16, 2>(Q[j], Q[j + 1]);
+    E8 r;
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+        r.q[j] = to_int ? e_fold<ORDER>(c, Q[j], S[j], Q[j + 1], S[j + 1]) : e_fold<ORDER>(c, S[j], Q[j + 1], S[j + 1], Q[j + 2]);
+    return r;
+}
+
+// slow taps from a 4-deep register queue (q[k] = row base + k) for each of the 4 pairs
+template <int ORDER>
+__device__ __forceinline__ E8 e_sfold(const __half c[4], const E8& a, const E8& b, const E8& d, const E8& e) {
+    E8 r;
+#pragma unroll
+    for (int j = 0; j < 4; j++) r.q[j] = e_fold<ORDER>(c, a.q[j], b.q[j], d.q[j], e.q[j]);
+    return r;
+}
+
+__device__ __forceinline__ unsigned int e_nonfinite(__half2 acc) {  // |max| is inf or NaN
+    const unsigned int b = *reinterpret_cast<const unsigned int*>(&acc);
+    return (((b & 0x7c00u) == 0x7c00u) || ((b & 0x7c000000u) == 0x7c000000u)) ? 1u : 0u;
+}
+
+// ring rows below the first ghost slab are never consumed (r < y0); keep the copy in bounds
+__device__ __forceinline__ int64_t e_row(int r) { return (int64_t)(r < -G ? -G : r); }
+
+__device__ __forceinline__ void e_track(__half2& acc, const E8& v) {
+#pragma unroll
+    for (int j = 0; j < 4; j++) acc = __hmax2_nan(acc, __habs2(v.q[j].h2));
+}
+
+// store one row (8 cells per thread) of field f and its write-through ghost rows
+__device__ __forceinline__ void e_store_row(const FieldView& f, int64_t pitch, int s, int x, const E8& v) {
+    __half* base = reinterpret_cast<__half*>(f.base);
+    e_st8(base + (int64_t)s * pitch + x, v);
+    if ((f.gtop | f.gbot) == GHOST_NONE) return;
+    const int n = (int)f.rows;
+    if (f.gtop == GHOST_PERIODIC && s >= n - G) e_st8(base + (int64_t)(s - n) * pitch + x, v);
+    if (f.gbot == GHOST_PERIODIC && s < G) e_st8(base + (int64_t)(n + s) * pitch + x, v);
+    if ((f.gtop | f.gbot) & GHOST_IMAGE) {
+        const E8 w = f.odd ? e_neg8(v) : v;
+        const int sg = (int)f.row0 + s, ng = (int)f.nglob;
+        if (f.gtop == GHOST_IMAGE) {
+            const int k1 = f.half_s ? -sg - 1 : -sg;
+            if (k1 < 0 && k1 >= -G) e_st8(base + (int64_t)(k1 - (int)f.row0) * pitch + x, w);
+        }
+        if (f.gbot == GHOST_IMAGE) {
+            const int k2 = f.half_s ? 2 * ng - 1 - sg : 2 * ng - 2 - sg;
+            if (k2 >= ng && k2 < ng + G) e_st8(base + (int64_t)(k2 - (int)f.row0) * pitch + x, w);
+        }
+    }
+}
+
+// Programmatic dependent launch: the next phase's grid may launch while this one runs
+// (its CTAs take SMs as ours retire); it waits here until every prior write is visible.
+__device__ __forceinline__ void e_pdl_enter() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+__device__ __forceinline__ double e_pick(const E8& v, int o) {  // register select, no local memory
+    double r = 0.0;
+#pragma unroll
+    for (int j = 0; j < ECPT; j++)
+        if (j == o) r = (double)__half2float(v.q[j >> 1].e[j & 1]);
+    return r;
+}
+
+}  // namespace hw
