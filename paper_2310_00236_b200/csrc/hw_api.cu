@@ -353,6 +353,9 @@ struct hw_solver {
     // fused single-pass path (2D acoustic, binary16): ping-pong partner buffers
     bool fused = false;
     int fused_blocks = 0;
+    bool tb2 = false;  // two steps per launch (temporal blocking, hw_tb2d.cu)
+    int tb2_tiles = 0, tb2_bands = 0;
+    double* partials_b = nullptr;  // stage-B energy partials of the two-step kernel
     void* mem_b[2 * F_N] = {};
     // streaming phase kernels (2D elastic, binary16): in place on the standard layout
     bool el_stream = false;   // streaming 2D elastic phases
@@ -631,6 +634,14 @@ int setup_handle(hw_solver* h) {
             if (nbf < 1) nbf = 1;
             h->fused_blocks = (int)(nbf < nsm ? nbf : nsm);
             h->fused = true;
+            // two steps per launch: opt-in (HALFWAVE_TB=1); measured slower than the
+            // single-step kernel on B200 (compute/latency-bound)
+            const char* tbe = getenv("HALFWAVE_TB");
+            if (tbe && strcmp(tbe, "1") == 0 && tb2_eligible(desc->nx, desc->ns, dev_smem)) {
+                if (tb2_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "two-step kernel setup failed");
+                tb2_grid(desc->nx, desc->ns, nsm, &h->tb2_tiles, &h->tb2_bands);
+                h->tb2 = true;
+            }
         }
         if (want && !h->ac && !h->d3 && h->LS == 16 && h->LU == 16 && el2d_stream_eligible(desc->nx, dev_smem)) {
             if (el2d_stream_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "streaming kernel setup failed");
@@ -656,7 +667,13 @@ int setup_handle(hw_solver* h) {
     if (!h->ctrl) CU(cudaMalloc(&h->ctrl, sizeof(Ctrl)));
     h->max_rows = max_rows;
     h->nblocks = grid_blocks(h->g, h->W, max_rows);
-    CU(cudaMalloc(&h->partials, (h->nblocks > h->stream_blocks ? h->nblocks : h->stream_blocks) * NCOMP * sizeof(double)));
+    {
+        int64_t np = h->nblocks > h->stream_blocks ? h->nblocks : h->stream_blocks;
+        const int64_t ntb = (int64_t)h->tb2_tiles * h->tb2_bands;
+        np = np > ntb ? np : ntb;
+        CU(cudaMalloc(&h->partials, 2 * np * NCOMP * sizeof(double)));
+        h->partials_b = h->partials + np * NCOMP;
+    }
     // the point source belongs to the slab holding its row
     int srcf = desc->src_kind == HW_SRC_PRESSURE ? F_P : (desc->src_kind == HW_SRC_VSLOW ? F_VS : F_SXX);
     if (desc->src_kind != HW_SRC_NONE && desc->src_s >= h->r0 && desc->src_s < h->r0 + field_rows(h, srcf)) {
@@ -1063,6 +1080,38 @@ static void run_epilogue(hw_solver* h, const RunCtx& C, int64_t n) {
     }
 }
 
+// Parameters of the fused 2D kernels (in / out buffers are set per launch).
+static AcFusedParams fused_params(const hw_solver* h, int64_t nt) {
+    AcFusedParams F;
+    memset(&F, 0, sizeof(F));
+    F.nx = h->d.nx;
+    F.ns = h->d.ns;
+    F.pitch = h->g.pitch;
+    F.rho_x = h->lp[HW_PL_RHO_X]; F.rho_s = h->lp[HW_PL_RHO_S]; F.beta = h->lp[HW_PL_BETA];
+    F.e_beta = h->ep64[HW_PL_BETA]; F.e_rho_x = h->ep64[HW_PL_RHO_X]; F.e_rho_s = h->ep64[HW_PL_RHO_S];
+    F.k = make_consts(h->d.taps, h->dt_u);
+    F.has_src = h->d.src_kind == HW_SRC_PRESSURE && h->src_active;
+    F.src_x = h->d.src_x;
+    F.src_s = h->src_s_loc;
+    F.n_rec = h->n_rec_sorted;
+    F.rec = h->rec_sorted;
+    F.traces = h->traces;
+    F.nt = nt;
+    F.ctrl = h->ctrl;
+    F.partials = h->partials;
+    F.e_vals = h->evals;
+    F.scale = 0.5 * h->d.dx * h->d.dx;
+    return F;
+}
+
+static void fused_bufs(const hw_solver* h, __half* bufs[2][FUSED_NSTREAM]) {
+    const int64_t ghost = (int64_t)G * h->g.slab * 2;  // bytes before row 0
+    for (int j = 0; j < FUSED_NSTREAM; j++) {  // external order p vx vy rp rvx rvy == stream order
+        bufs[0][j] = (__half*)((char*)h->mem[j] + ghost);
+        bufs[1][j] = (__half*)((char*)h->mem_b[j] + ghost);
+    }
+}
+
 // The time loop (acoustic.py:210-226 / elastic.py:271-286) of one handle on the device.
 static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src, bool energy, bool timed) {
     if (h->transport == 1) return fail(HW_EINVAL, "slab-group handles run through hw_run_group");
@@ -1071,40 +1120,28 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
     if (rc) return rc;
     if ((rc = exchange(h, 0)) || (rc = exchange(h, 1))) return rc;  // halos of the uploaded state
     if (timed) CU(cudaEventRecord(h->ev0, h->st));
-    if (h->fused) {  // one fused kernel per step, ping-pong A <-> B
-        AcFusedParams F;
-        memset(&F, 0, sizeof(F));
-        F.nx = h->d.nx;
-        F.ns = h->d.ns;
-        F.pitch = h->g.pitch;
-        const int64_t ghost = (int64_t)G * h->g.slab * 2;  // bytes before row 0
+    if (h->fused) {  // fused kernels, ping-pong A <-> B: launch L reads buffer L % 2
+        AcFusedParams F = fused_params(h, nt);
         __half* bufs[2][FUSED_NSTREAM];
-        for (int j = 0; j < FUSED_NSTREAM; j++) {  // external order p vx vy rp rvx rvy == stream order
-            bufs[0][j] = (__half*)((char*)h->mem[j] + ghost);
-            bufs[1][j] = (__half*)((char*)h->mem_b[j] + ghost);
-        }
-        F.rho_x = h->lp[HW_PL_RHO_X]; F.rho_s = h->lp[HW_PL_RHO_S]; F.beta = h->lp[HW_PL_BETA];
-        F.e_beta = h->ep64[HW_PL_BETA]; F.e_rho_x = h->ep64[HW_PL_RHO_X]; F.e_rho_s = h->ep64[HW_PL_RHO_S];
-        F.k = make_consts(h->d.taps, h->dt_u);
-        F.has_src = h->d.src_kind == HW_SRC_PRESSURE && h->src_active;
-        F.src_x = h->d.src_x;
-        F.src_s = h->src_s_loc;
-        F.n_rec = h->n_rec_sorted;
-        F.rec = h->rec_sorted;
-        F.traces = h->traces;
-        F.nt = nt;
-        F.ctrl = h->ctrl;
-        F.partials = h->partials;
-        F.e_vals = h->evals;
-        F.scale = C.E.scale;
-        for (int64_t n = 0; n < nt; n++) {
-            const int sample = energy && ((n + 1) % C.every == 0);
+        fused_bufs(h, bufs);
+        const int64_t every = C.every;
+        int cur = 0;
+        for (int64_t n = 0; n < nt;) {
             for (int j = 0; j < FUSED_NSTREAM; j++) {
-                F.in[j] = bufs[n & 1][j];
-                F.out[j] = bufs[(n + 1) & 1][j];
+                F.in[j] = bufs[cur][j];
+                F.out[j] = bufs[cur ^ 1][j];
             }
-            launch_ac2d_fused(variant, h->d.order, F, h->fused_blocks, n, src ? src[n] : 0.0, sample,
-                              (n + 1) / C.every, h->st);
+            if (h->tb2 && n + 1 < nt) {  // steps n and n+1 in one launch
+                launch_ac2d_tb2(variant, h->d.order, F, h->tb2_tiles, h->tb2_bands, h->partials_b, n,
+                                src ? src[n] : 0.0, src ? src[n + 1] : 0.0, energy && ((n + 1) % every == 0),
+                                energy && ((n + 2) % every == 0), (n + 1) / every, (n + 2) / every, h->st);
+                n += 2;
+            } else {
+                launch_ac2d_fused(variant, h->d.order, F, h->fused_blocks, n, src ? src[n] : 0.0,
+                                  energy && ((n + 1) % every == 0), (n + 1) / every, h->st);
+                n += 1;
+            }
+            cur ^= 1;
             h->launches++;
         }
     } else {
@@ -1121,10 +1158,12 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
     return HW_OK;
 }
 
-// After `executed` fused steps the newest state sits in buffer B when the count is
-// odd: copy it home so buffer A is always current between calls.
+// After `executed` fused steps (L launches: one per step, or one per pair of steps
+// with the two-step kernel) the newest state sits in buffer B when L is odd: copy it
+// home so buffer A is always current between calls.
 static int fused_copy_back(hw_solver* h, int64_t executed, int32_t variant) {
-    if (!h->fused || (executed & 1) == 0) return HW_OK;
+    const int64_t launches = h->tb2 ? (executed + 1) / 2 : executed;
+    if (!h->fused || (launches & 1) == 0) return HW_OK;
     const int nf = variant == HW_NAIVE ? h->nsol : 2 * h->nsol;  // naive runs never touch residuals
     for (int j = 0; j < nf; j++) {
         int f = h->ext[j % h->nsol];
@@ -1144,6 +1183,36 @@ static void fill_times(const hw_solver* h, double* e_times, int64_t ne) {
     }
 }
 
+// A two-step launch whose FIRST step went non-finite has also written step n+1: replay
+// step n alone with the single-step kernel from the launch's untouched input buffer,
+// so the state, failure record and traces are exactly "after the failing step".
+static int tb2_replay(hw_solver* h, int32_t variant, int64_t nt, const double* src, bool energy, Ctrl& c) {
+    if (!h->tb2 || c.fail_step == INT64_MAX || (c.fail_step & 1) || c.fail_step + 1 >= nt) return HW_OK;
+    const int64_t n = c.fail_step, every = h->d.energy_every;
+    const int cur = (int)((n / 2) & 1);
+    AcFusedParams F = fused_params(h, nt);
+    __half* bufs[2][FUSED_NSTREAM];
+    fused_bufs(h, bufs);
+    for (int j = 0; j < FUSED_NSTREAM; j++) {
+        F.in[j] = bufs[cur][j];
+        F.out[j] = bufs[cur ^ 1][j];
+    }
+    Ctrl c0;
+    c0.fail_step = INT64_MAX;
+    c0.fail_mask = 0;
+    c0.pad = 0;
+    CU(cudaMemcpyAsync(h->ctrl, &c0, sizeof(Ctrl), cudaMemcpyHostToDevice, h->st));
+    for (int64_t j = 0; j < h->n_rec_sorted; j++)  // the pair's second step recorded samples at n+1
+        CU(cudaMemsetAsync(h->traces + j * nt + n + 1, 0, (nt - n - 1) * sizeof(double), h->st));
+    launch_ac2d_fused(variant, h->d.order, F, h->fused_blocks, n, src ? src[n] : 0.0,
+                      energy && ((n + 1) % every == 0), (n + 1) / every, h->st);
+    h->launches++;
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(&c, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    return HW_OK;
+}
+
 int hw_run(hw_solver* h, int32_t variant, int64_t step0, int64_t nt, const double* src_samples, double* traces,
            double* e_times, double* e_vals, int64_t* n_energy, int64_t* fail_step, int32_t* fail_field) {
     if (!h) return fail(HW_EINVAL, "null solver");
@@ -1153,6 +1222,7 @@ int hw_run(hw_solver* h, int32_t variant, int64_t step0, int64_t nt, const doubl
     Ctrl c;
     CU(cudaMemcpyAsync(&c, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, h->st));
     CU(cudaStreamSynchronize(h->st));
+    if ((rc = tb2_replay(h, variant, nt, src_samples, energy, c))) return rc;
     if (h->transport == 2) {  // agree on the first failure across ranks; combine energy and traces
         Ctrl* all = nullptr;
         CU(cudaMalloc(&all, sizeof(Ctrl) * h->world));
@@ -1288,6 +1358,7 @@ int hw_run_device(hw_solver* h, int32_t variant, int64_t step0, int64_t nt, cons
     CU(cudaEventElapsedTime(&t, h->ev0, h->ev1));
     Ctrl c;
     CU(cudaMemcpy(&c, h->ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+    if ((rc = tb2_replay(h, variant, nt, src_samples, true, c))) return rc;
     if ((rc = fused_copy_back(h, c.fail_step != INT64_MAX ? c.fail_step + 1 : nt, variant))) return rc;
     if (ms) *ms = t;
     h->kernel_ms = nt > 0 ? t / nt : 0.0;
@@ -1298,7 +1369,7 @@ int64_t hw_last_launch_count(const hw_solver* h) { return h ? h->launches : 0; }
 
 const char* hw_kernel_path(const hw_solver* h) {
     if (!h) return "";
-    return h->fused ? "fused2d" : (h->el_stream ? "stream2d" : (h->ac3_stream ? "stream3d" : "generic"));
+    return h->tb2 ? "fused2d-tb2" : h->fused ? "fused2d" : (h->el_stream ? "stream2d" : (h->ac3_stream ? "stream3d" : "generic"));
 }
 
 double hw_last_kernel_ms(const hw_solver* h) { return h ? h->kernel_ms : 0.0; }

@@ -365,17 +365,17 @@ __device__ __forceinline__ int rec_lower(const int* rec, int lo, int hi, int r, 
     return lo;
 }
 
-// Record the trace samples of row r for cells [x, x + 8) from the 8 values in v[] (as
-// float); cur is the uniform cursor (first receiver with row >= previous row).
+// Record the trace samples of row r for cells [x, x + width) (values from get(offset));
+// cur is the uniform cursor (first receiver with row >= previous row).
 template <typename GET>
 __device__ __forceinline__ void rec_row(const int* rec, int& cur, int hi, int r, int x, double* traces, int64_t nt,
-                                        int64_t n, GET get) {
+                                        int64_t n, GET get, int width = 8) {
     if (cur >= hi) return;
     if (__ldg(rec + 3 * cur) < r) cur = rec_lower(rec, cur, hi, r, INT_MIN);
     if (cur >= hi || __ldg(rec + 3 * cur) != r) return;
     for (int q = rec_lower(rec, cur, hi, r, x); q < hi; q++) {
         const int rr = __ldg(rec + 3 * q), rx = __ldg(rec + 3 * q + 1);
-        if (rr != r || rx >= x + 8) break;
+        if (rr != r || rx >= x + width) break;
         traces[(int64_t)__ldg(rec + 3 * q + 2) * nt + n] = get(rx - x);
     }
 }

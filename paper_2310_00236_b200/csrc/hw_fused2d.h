@@ -27,6 +27,14 @@ struct AcFusedParams {
 size_t fused2d_smem_bytes(int64_t nx);
 bool fused2d_eligible(int64_t nx, int max_smem);
 cudaError_t fused2d_prepare(int64_t nx);
+// two steps per launch (hw_tb2d.cu)
+size_t tb2_smem_bytes(int64_t nx);
+bool tb2_eligible(int64_t nx, int64_t ns, int max_smem);
+void tb2_grid(int64_t nx, int64_t ns, int nsm, int* ntiles, int* nbands);
+cudaError_t tb2_prepare(int64_t nx);
+void launch_ac2d_tb2(int variant, int order, const AcFusedParams& F, int ntiles, int nbands, double* partials_b,
+                     int64_t n, double srcA, double srcB, int sampleA, int sampleB, int64_t eidxA, int64_t eidxB,
+                     cudaStream_t st);
 void launch_ac2d_fused(int variant, int order, const AcFusedParams& P, int nblocks, int64_t n, double src, int sample,
                        int64_t eidx, cudaStream_t st);
 }  // namespace hw

@@ -1,15 +1,20 @@
-"""Short run of one BASELINE config for ncu: python tools/profile_config.py <1|3|4|5> [nt]."""
+"""Short run of one BASELINE config for ncu: python tools/profile_config.py <1|2|3|4|5> [nt]."""
 import sys
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-sys.argv += [] 
 import tools.measure_configs as mc  # noqa: E402
 import paper_2310_00236_b200 as hw  # noqa: E402
 
 which = sys.argv[1]
 nt = int(sys.argv[2]) if len(sys.argv) > 2 else 6
-s = {"1": lambda: mc.cfg1(4), "3": mc.cfg3, "4": mc.cfg4, "5": mc.cfg5}[which]()
+
+def cfg2():
+    import bench
+    return bench.make_solver(hw, nt=nt)
+
+
+s = {"1": lambda: mc.cfg1(4), "2": cfg2, "3": mc.cfg3, "4": mc.cfg4, "5": mc.cfg5}[which]()
 st = s.new_state()
 s.upload(st)
 v = hw.Variant.OP6 if which in ("4", "5") else hw.Variant.OP3
