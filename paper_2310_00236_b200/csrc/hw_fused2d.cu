@@ -210,11 +210,29 @@ __global__ void __launch_bounds__(512, 1)
     double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
 
     // Rolled row loop (one copy of the body: the unrolled form was instruction-cache
-    // bound); the register queues rotate, [3] = this iteration's row.
+    // bound); the register queues rotate, [3] = this iteration's row.  fw is the
+    // wrapped front row, advanced without integer division; the row-uniform divisor
+    // reciprocals of the next iteration are prefetched into registers.
+    const int ns32 = (int)ns;
+    auto back = [&](int r, int k) { r -= k; return r < 0 ? r + ns32 : r; };  // wrapped r - k (k < ns)
+    int fw = (int)wrap_row(F0);
+    float rcx = 0.f, rcs = 0.f, rcb = 0.f;
+    if constexpr (ROWMED) {
+        rcx = __ldg(P.rho_x.rcp + fw * P.rho_x.ss);
+        rcs = __ldg(P.rho_s.rcp + back(fw, 2) * P.rho_s.ss);
+        rcb = __ldg(P.beta.rcp + back(fw, 3) * P.beta.ss);
+    }
 #pragma unroll 1
     for (int i = 0; i < NI; i++) {
         const int u = i % FR;
         const uint32_t par = (uint32_t)((i / FR) & 1);
+        const int fwn = fw + 1 == ns32 ? 0 : fw + 1;
+        float rcx_n = 0.f, rcs_n = 0.f, rcb_n = 0.f;
+        if constexpr (ROWMED) {
+            rcx_n = __ldg(P.rho_x.rcp + fwn * P.rho_x.ss);
+            rcs_n = __ldg(P.rho_s.rcp + back(fwn, 2) * P.rho_s.ss);
+            rcb_n = __ldg(P.beta.rcp + back(fwn, 3) * P.beta.ss);
+        }
         {
             {
                 const int f = F0 + i;
@@ -238,7 +256,7 @@ __global__ void __launch_bounds__(512, 1)
                     V8 vxn = lds8(slot_row(u, S_VX) + x);
                     V8 r = comp ? lds8(slot_row(u, S_RVX) + x) : V8{};
                     if constexpr (ROWMED) {
-                        const float rc = __ldg(P.rho_x.rcp + f * P.rho_x.ss);
+                        const float rc = rcx;
 #pragma unroll
                         for (int j = 0; j < 4; j++) finish_row<V>(d.q[j], rc, dt2, -1, srch, vxn.q[j], r.q[j]);
                     } else {
@@ -266,14 +284,14 @@ __global__ void __launch_bounds__(512, 1)
                 V8 rp = (comp && do_p) ? lds8(slot_row(u, S_RP) + x) : V8{};  // all ring reads before the barrier
                 if (f >= y0 && f < y1 + 3) {  // vy[f-2] from p rows f-3..f (acoustic.py:169-170)
                     const int r = f - 2;
-                    const int rw = (int)wrap_row(r);
+                    const int rw = back(fw, 2);
                     V8 vsn = lds8(slot_row(u, S_VS) + x);
                     V8 rr = comp ? lds8(slot_row(u, S_RVS) + x) : V8{};
                     const V8& t0 = pq[0];
                     const V8& t1 = pq[1];
                     const V8& t2 = pq[2];
                     if constexpr (ROWMED) {
-                        const float rc = __ldg(P.rho_s.rcp + rw * P.rho_s.ss);
+                        const float rc = rcs;
 #pragma unroll
                         for (int j = 0; j < 4; j++)
                             finish_row<V>(fold2<ORDER>(c, t0.q[j], t1.q[j], t2.q[j], pq[3].q[j]), rc, dt2, -1, srch,
@@ -315,7 +333,7 @@ __global__ void __launch_bounds__(512, 1)
                     const V8& a2 = vq[2];
                     const bool sk = src_here && k == P.src_s;
                     if constexpr (ROWMED) {
-                        const float rc = __ldg(P.beta.rcp + k * P.beta.ss);
+                        const float rc = rcb;
 #pragma unroll
                         for (int j = 0; j < 4; j++) {
                             H2 dv = O2::add(g.q[j], fold2<ORDER>(c, a0.q[j], a1.q[j], a2.q[j], vq[3].q[j]));
@@ -354,6 +372,10 @@ __global__ void __launch_bounds__(512, 1)
                 }
             }
         }
+        fw = fwn;
+        rcx = rcx_n;
+        rcs = rcs_n;
+        rcb = rcb_n;
     }
     unsigned int mask = 0;
     // bit order = external field order p vx vy rp rvx rvy == stream order
