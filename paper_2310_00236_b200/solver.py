@@ -26,6 +26,28 @@ from .precision import DTYPES, LANE_BITS, Precision, as_precision
 from .sources import sample_source
 from .stencil import StencilSpec
 
+_PINNED = None  # torch's caching pinned-host allocator (None: not probed yet, False: unavailable)
+
+
+def _host_empty(shape, dtype) -> np.ndarray:
+    """A new host array for downloaded state.  Page-locked when torch + CUDA are present:
+    the arrays come from torch's caching pinned allocator (returned to its pool when the
+    numpy array is freed), so device<->host copies of the state run at pinned bandwidth
+    without a cudaHostAlloc per call; plain numpy memory otherwise."""
+    global _PINNED
+    if _PINNED is None:
+        try:
+            import torch
+            _PINNED = torch if torch.cuda.is_available() else False
+        except Exception:  # noqa: BLE001 - torch is optional plumbing here
+            _PINNED = False
+    if _PINNED is not False:
+        tdt = {np.dtype(np.float16): _PINNED.float16, np.dtype(np.float32): _PINNED.float32,
+               np.dtype(np.float64): _PINNED.float64}.get(np.dtype(dtype))
+        if tdt is not None:
+            return _PINNED.empty(tuple(shape), dtype=tdt, pin_memory=True).numpy()
+    return np.empty(shape, dtype=dtype)
+
 DEFAULT_ENERGY_EVERY = 10
 
 
@@ -244,8 +266,8 @@ class _DeviceSolver:
         dtype = DTYPES[self.update_precision]
         if self.distributed:  # rows of other ranks keep their uploaded values
             arrs = [a.copy() for a in self._uploaded]
-        else:
-            arrs = [np.empty(self.grid.shape(self._stagger_of(n)), dtype=dtype) for n in self.FIELDS]
+        else:  # fresh arrays, as the reference returns (acoustic.py:147-152), in pinned memory
+            arrs = [_host_empty(self.grid.shape(self._stagger_of(n)), dtype) for n in self.FIELDS]
         ptrs = (ctypes.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
         for h in self._handles():
             _abi.check(_abi.load().hw_get_state(h, ptrs), "hw_get_state")
