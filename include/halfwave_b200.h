@@ -169,6 +169,10 @@ int64_t hw_last_launch_count(const hw_solver* h);
  * elastic phases) or "generic" (phase kernels).  Static string; "" for NULL. */
 const char* hw_kernel_path(const hw_solver* h);
 
+/* Halo transport of the handle: 0 single domain, 1 in-process slab group (peer copies),
+ * 2 NCCL (one process per GPU).  -1 for NULL. */
+int32_t hw_transport(const hw_solver* h);
+
 /* Average duration (ms) of the dominant (fused step) kernel in the last
  * hw_run_device, measured with CUDA events on the launching stream; 0 if unknown. */
 double hw_last_kernel_ms(const hw_solver* h);

@@ -34,7 +34,7 @@ NPLANES = 9
 
 EXPORTED = (
     "hw_num_fields", "hw_field_shape", "hw_create", "hw_destroy", "hw_set_state",
-    "hw_get_state", "hw_run", "hw_run_device", "hw_last_launch_count", "hw_kernel_path",
+    "hw_get_state", "hw_run", "hw_run_device", "hw_last_launch_count", "hw_kernel_path", "hw_transport",
     "hw_last_kernel_ms", "hw_last_error", "hw_version", "hw_selftest_div16",
     "hw_cheap_div_table", "hw_plane_div_mode", "hw_nccl_unique_id", "hw_create_group", "hw_run_group",
 )
@@ -102,6 +102,8 @@ def load() -> ctypes.CDLL:
     lib.hw_last_launch_count.argtypes = [vp]
     lib.hw_last_launch_count.restype = i64
     lib.hw_kernel_path.argtypes = [vp]
+    lib.hw_transport.argtypes = [vp]
+    lib.hw_transport.restype = i32
     lib.hw_kernel_path.restype = ctypes.c_char_p
     lib.hw_last_kernel_ms.argtypes = [vp]
     lib.hw_last_kernel_ms.restype = dbl

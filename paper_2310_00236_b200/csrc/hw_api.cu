@@ -607,7 +607,7 @@ int setup_handle(hw_solver* h) {
         if (!resid && needs_ghosts(h, f)) {
             // parity of the image: odd for sxy/syy (elastic.py:186-189), even for vx/vy (:210-236)
             fv.odd = (f == F_SXS || f == F_SSS) ? 1 : 0;
-            if (h->world == 1 && !h->fs) fv.gtop = fv.gbot = GHOST_PERIODIC;
+            if (h->world == 1 && !h->fs && h->transport != 2) fv.gtop = fv.gbot = GHOST_PERIODIC;
             if (top_image) fv.gtop = GHOST_IMAGE;
             if (bot_image) fv.gbot = GHOST_IMAGE;
         }
@@ -621,7 +621,7 @@ int setup_handle(hw_solver* h) {
         int dev_smem = 0, nsm = 0;
         cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, desc->device);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, desc->device);
-        if (want && h->ac && !h->d3 && h->LS == 16 && h->LU == 16 && h->world == 1 &&
+        if (want && h->ac && !h->d3 && h->LS == 16 && h->LU == 16 && h->world == 1 && h->transport != 2 &&
             fused2d_eligible(desc->nx, dev_smem)) {
             for (int j = 0; j < 2 * h->nsol; j++) {
                 int f = h->ext[j % h->nsol];
@@ -813,8 +813,8 @@ int exchange_group(hw_group* grp, int phase) {
 }
 
 int exchange(hw_solver* h, int phase) {
-    if (h->world == 1) return HW_OK;
     if (h->transport == 2) return exchange_nccl(h, phase);
+    if (h->world == 1) return HW_OK;
     return HW_OK;  // group ranks are exchanged by the group driver
 }
 
@@ -855,7 +855,11 @@ int hw_create(const hw_desc* desc, hw_solver** out) {
     h->d = *desc;
     h->world = desc->world_size;
     h->rank = desc->rank;
-    if (h->world > 1) {  // one process per GPU: NCCL transport
+    // HALFWAVE_NCCL_SELF=1 (test hook): a one-rank job still takes the NCCL transport,
+    // its periodic ghosts filled by send/recv to itself, so the whole NCCL path runs on one GPU
+    const char* self_env = getenv("HALFWAVE_NCCL_SELF");
+    const bool nccl_self = h->world == 1 && self_env && strcmp(self_env, "1") == 0 && desc->nccl_unique_id;
+    if (h->world > 1 || nccl_self) {  // one process per GPU: NCCL transport
         if (!desc->nccl_unique_id) { release_handle(h); return fail(HW_EINVAL, "world_size > 1 needs nccl_unique_id"); }
         if ((rc = nccl_load())) { release_handle(h); return rc; }
         h->transport = 2;
@@ -1371,6 +1375,8 @@ const char* hw_kernel_path(const hw_solver* h) {
     if (!h) return "";
     return h->tb2 ? "fused2d-tb2" : h->fused ? "fused2d" : (h->el_stream ? "stream2d" : (h->ac3_stream ? "stream3d" : "generic"));
 }
+
+int32_t hw_transport(const hw_solver* h) { return h ? h->transport : -1; }
 
 double hw_last_kernel_ms(const hw_solver* h) { return h ? h->kernel_ms : 0.0; }
 

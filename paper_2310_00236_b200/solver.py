@@ -380,5 +380,9 @@ class _DeviceSolver:
         """Kernel family of the device steps: "fused2d", "stream2d" or "generic"."""
         return _abi.load().hw_kernel_path(self._lib_handle()).decode()
 
+    def transport(self) -> int:
+        """Halo transport: 0 single domain, 1 in-process slab group, 2 NCCL."""
+        return int(_abi.load().hw_transport(self._lib_handle()))
+
     def last_launch_count(self) -> int:
         return int(_abi.load().hw_last_launch_count(self._lib_handle()))

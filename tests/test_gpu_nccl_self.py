@@ -1,0 +1,92 @@
+"""The NCCL transport (one process per GPU) on real hardware: with HALFWAVE_NCCL_SELF=1 a
+one-rank torch.distributed job takes the NCCL path — libnccl dlopen'ed, communicator
+from hw_nccl_unique_id, periodic ghosts exchanged by grouped ncclSend/ncclRecv to itself
+after every phase, control blocks all-gathered, energy all-reduced, traces broadcast —
+and must reproduce the single-process run bit for bit (energy within 1e-12)."""
+
+import socket
+
+import numpy as np
+import pytest
+
+import paper_2310_00236_b200 as hw
+from golden_cases import assert_same_bits
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def one_rank_job(monkeypatch):
+    import torch.distributed as dist
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    monkeypatch.setenv("HALFWAVE_NCCL_SELF", "1")
+    yield
+    dist.destroy_process_group()
+
+
+def _acoustic(**kw):
+    nx, ny = 256, 96
+    dx = 1.0 / nx
+    g = hw.GridSpec(nx, ny, dx, float(np.float16(0.3 * dx)), 30)
+    src = hw.SourceSpec(hw.SourceKind.PRESSURE_POINT, 100, 47, hw.RickerSpec(1 / (10 * dx), amplitude=2.0))
+    s = hw.AcousticSolver(g, hw.build_layered_acoustic(nx, ny, [(0.4, 1.0, 1.0), (1.0, 1.5, 2.25)]), src,
+                          stencil_precision=hw.Precision.FP16, energy_every=5, receivers=((100, 47), (3, 0), (250, 95)),
+                          **kw)
+    st = s.new_state()
+    yy, xx = np.mgrid[0:ny, 0:nx] / nx
+    st.p.values = np.exp(-((xx - 0.5) ** 2 + (yy - 0.2) ** 2) / 0.005).astype(np.float16)
+    return s, st
+
+
+def _elastic(**kw):
+    nx, ny = 256, 64
+    g = hw.GridSpec(nx, ny, 0.05, 0.004, 30, bc_y=hw.Boundary.PERIODIC)
+    src = hw.SourceSpec(hw.SourceKind.VY_POINT, 40, 33, hw.RickerSpec(5.0, amplitude=20.0))
+    s = hw.ElasticSolver(g, hw.build_layered_elastic(nx, ny, [(0.5, 2.0, 2.0, 1.0), (1.0, 2.3, 2.8, 1.4)]), src,
+                         stencil_precision=hw.Precision.FP16, energy_every=4, receivers=((40, 33), (10, 0)), **kw)
+    st = s.new_state()
+    st.sxx.values = np.random.default_rng(3).uniform(-0.1, 0.1, st.sxx.values.shape).astype(np.float16)
+    return s, st
+
+
+def _acoustic3d(**kw):
+    nz, ny, nx = 24, 16, 256
+    g = hw.GridSpec(nx, ny, 1.0 / nx, float(np.float16(0.2 / nx)), 12, nz=nz, order=2)
+    s = hw.AcousticSolver(g, hw.build_homogeneous_acoustic(nx, ny, 1.0, 1.0, nz=nz), stencil_precision=hw.Precision.FP16,
+                          receivers=((5, 5, 20), (12, 8, 2)), energy_every=3, **kw)
+    st = s.new_state()
+    z, y, x = np.mgrid[0:nz, 0:ny, 0:nx]
+    st.p.values = np.exp(-((x - 120) ** 2 / 200.0 + (y - 8) ** 2 / 10.0 + (z - 3) ** 2 / 10.0)).astype(np.float16)
+    return s, st
+
+
+@pytest.mark.parametrize("make,variant", [(_acoustic, hw.Variant.OP3), (_elastic, hw.Variant.OP6),
+                                          (_acoustic3d, hw.Variant.OP3)])
+def test_nccl_transport_equals_single_process(one_rank_job, make, variant):
+    a, sa = make()
+    oa = a.run(variant, sa)
+    b, sb = make(distributed=True)
+    ob = b.run(variant, sb)
+    assert a.transport() == 0 and b.transport() == 2
+    for n in a.FIELDS:
+        assert_same_bits(getattr(sb, n).values, getattr(sa, n).values, n)
+    np.testing.assert_array_equal(np.array([t.samples for t in ob.traces]), np.array([t.samples for t in oa.traces]))
+    np.testing.assert_allclose(ob.energy.values, oa.energy.values, rtol=1e-12)
+
+
+def test_nccl_transport_range_failure(one_rank_job):
+    a, sa = _acoustic()
+    sa.p.values = (sa.p.values.astype(np.float32) * 3e4).astype(np.float16)
+    with pytest.raises(hw.RangeFailureError) as ea:
+        a.run(None, sa)
+    b, sb = _acoustic(distributed=True)
+    sb.p.values = (sb.p.values.astype(np.float32) * 3e4).astype(np.float16)
+    with pytest.raises(hw.RangeFailureError) as eb:
+        b.run(None, sb)
+    assert (eb.value.step, eb.value.field_name) == (ea.value.step, ea.value.field_name)
+    for n in a.FIELDS:
+        assert_same_bits(getattr(sb, n).values, getattr(sa, n).values, n)
