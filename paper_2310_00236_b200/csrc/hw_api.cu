@@ -125,7 +125,7 @@ __global__ void k_fill_ghosts(FieldView f, Geom g) {
     int64_t q = i / per, rem = i % per;
     int64_t m = rem / g.nx, x = rem % g.nx;
     const int64_t n = f.rows;
-    const int64_t k = q < G ? q - G : n + (q - G);  // -2,-1, n, n+1
+    const int64_t k = q < G ? q - G : n + (q - G);  // -G .. -1, n .. n+G-1
     const int mode = k < 0 ? f.gtop : f.gbot;
     if (mode == GHOST_NONE) return;
     int64_t src;
@@ -426,9 +426,28 @@ int upload_plane(hw_solver* h, int pl) {
     h->ep64[pl] = Plane64{nullptr, 0, 0, 0};
     if (!rows) return HW_OK;
     int64_t nm = pl == HW_PL_EP ? 1 : h->d.nm, nx = h->d.nx;
-    int64_t per = nm * nx, n = rows * per;
+    int64_t per = nm * nx;
     if (!h->d.plane[pl]) return fail(HW_EINVAL, "medium plane " + std::to_string(pl) + " missing");
     const double* src = h->d.plane[pl] + (pl == HW_PL_EP ? 0 : h->r0 * per);
+    // Slab mode: G halo rows each side (global rows wrapped, or clamped at a free
+    // surface), views pointing at local row 0, so kernels that recompute halo rows
+    // (the fused 2D kernel's vy) find their coefficients.
+    const int64_t pad = ((h->world > 1 || h->transport == 2) && pl != HW_PL_EP) ? G : 0;
+    std::vector<double> ext;
+    if (pad) {
+        static const int PLANE_FIELD[HW_NPLANES] = {F_VX, F_VS, F_VM, F_P, F_SXX, F_SXX, F_SXX, F_SXS, F_SXX};
+        const int64_t ng = nglob_rows(h, PLANE_FIELD[pl]);
+        ext.resize((rows + 2 * pad) * per);
+        for (int64_t r = -pad; r < rows + pad; r++) {
+            int64_t gr = h->r0 + r;
+            if (h->fs) gr = gr < 0 ? 0 : (gr >= ng ? ng - 1 : gr);
+            else gr = ((gr % ng) + ng) % ng;
+            memcpy(&ext[(r + pad) * per], h->d.plane[pl] + gr * per, per * sizeof(double));
+        }
+        src = ext.data();
+        rows += 2 * pad;
+    }
+    const int64_t n = rows * per;
     bool cst = true, layered = true;
     for (int64_t i = 1; i < n && cst; i++) cst = memcmp(&src[i], &src[0], 8) == 0;
     if (!cst)
@@ -448,11 +467,12 @@ int upload_plane(hw_solver* h, int pl) {
         ss = per; sm = nx; sx = 1;
     }
     int64_t cnt = (int64_t)packed.size();
+    const int64_t off = pad * ss;  // elements before local row 0
     double* d64 = nullptr;
     CU(cudaMalloc(&d64, cnt * 8));
     h->plane_mem.push_back(d64);
     CU(cudaMemcpy(d64, packed.data(), cnt * 8, cudaMemcpyHostToDevice));
-    h->ep64[pl] = Plane64{d64, ss, sm, sx};
+    h->ep64[pl] = Plane64{d64 + off, ss, sm, sx};
     int L = plane_lane(h, pl);
     if (L) {
         void* dl = nullptr;
@@ -493,7 +513,7 @@ int upload_plane(hw_solver* h, int pl) {
                 }
             }
         }
-        h->lp[pl] = PlaneView{dl, rcp, ss, sm, sx, mode, 0};
+        h->lp[pl] = PlaneView{(const char*)dl + off * lane_bytes(L), rcp ? rcp + off : nullptr, ss, sm, sx, mode, 0};
     }
     return HW_OK;
 }
@@ -621,7 +641,9 @@ int setup_handle(hw_solver* h) {
         int dev_smem = 0, nsm = 0;
         cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, desc->device);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, desc->device);
-        if (want && h->ac && !h->d3 && h->LS == 16 && h->LU == 16 && h->world == 1 && h->transport != 2 &&
+        // fused 2D kernel: single domain, or one slab of a decomposed domain (ghost rows
+        // exchanged once per step; periodic slow axis only, as the acoustic solver)
+        if (want && h->ac && !h->d3 && h->LS == 16 && h->LU == 16 && !h->fs && field_rows(h, F_P) >= 8 &&
             fused2d_eligible(desc->nx, dev_smem)) {
             for (int j = 0; j < 2 * h->nsol; j++) {
                 int f = h->ext[j % h->nsol];
@@ -630,14 +652,15 @@ int setup_handle(hw_solver* h) {
                 CU(cudaMemset(h->mem_b[j], 0, bytes));
             }
             if (fused2d_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "fused kernel setup failed");
-            int64_t nbf = desc->ns / 4;
+            int64_t nbf = field_rows(h, F_P) / 4;
             if (nbf < 1) nbf = 1;
             h->fused_blocks = (int)(nbf < nsm ? nbf : nsm);
             h->fused = true;
             // two steps per launch: opt-in (HALFWAVE_TB=1); measured slower than the
             // single-step kernel on B200 (compute/latency-bound)
             const char* tbe = getenv("HALFWAVE_TB");
-            if (tbe && strcmp(tbe, "1") == 0 && tb2_eligible(desc->nx, desc->ns, dev_smem)) {
+            if (tbe && strcmp(tbe, "1") == 0 && h->world == 1 && h->transport != 2 &&
+                tb2_eligible(desc->nx, desc->ns, dev_smem)) {
                 if (tb2_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "two-step kernel setup failed");
                 tb2_grid(desc->nx, desc->ns, nsm, &h->tb2_tiles, &h->tb2_bands);
                 h->tb2 = true;
@@ -659,7 +682,7 @@ int setup_handle(hw_solver* h) {
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
             h->ac3_stream = true;
         }
-        if (h->el_stream || h->ac3_stream) {
+        if (h->el_stream || h->ac3_stream || h->fused) {
             CU(cudaMalloc(&h->counter, sizeof(unsigned int)));
             CU(cudaMemset(h->counter, 0, sizeof(unsigned int)));
         }
@@ -759,9 +782,22 @@ std::vector<Xfer> xfers(const hw_solver* h, int phase) {
     return out;
 }
 
-int exchange_nccl(hw_solver* h, int phase) {
+// Ghost plan of the fused 2D kernel's buffer `buf` (0 = A, 1 = B): p (3 rows each way:
+// its redundant vy halo reads p rows -3 .. L+2), vy and rvy (the old values of those vy
+// halo rows); one exchange per step.
+std::vector<Xfer> xfers_fused(const hw_solver* h, int buf) {
+    std::vector<Xfer> out;
+    const size_t row = (size_t)h->g.slab * 2;
+    for (int j : {0, 2, 5}) {  // p, vy, rvy in the external order p vx vy rp rvx rvy
+        char* b = (char*)(buf ? h->mem_b[j] : h->mem[j]) + G * row;
+        const int64_t n = h->ns_loc;
+        out.push_back(Xfer{b + (n - G) * row, b, b - G * row, b + n * row, G * row});
+    }
+    return out;
+}
+
+int exchange_nccl_list(hw_solver* h, const std::vector<Xfer>& xs) {
     const int pv = prev_rank(h), nx_ = next_rank(h);
-    std::vector<Xfer> xs = xfers(h, phase);
     NC(g_nccl.GroupStart());
     for (const Xfer& x : xs) {  // canonical order: bottom->next / top ghost<-prev, then the reverse
         if (nx_ >= 0) NC(g_nccl.Send(x.src_bottom, x.bytes, ncclInt8, nx_, h->nccl, h->st));
@@ -775,9 +811,13 @@ int exchange_nccl(hw_solver* h, int phase) {
     return HW_OK;
 }
 
+int exchange_nccl(hw_solver* h, int phase) { return exchange_nccl_list(h, xfers(h, phase)); }
+
 // In-process slab group: every rank pulls its ghosts from its neighbours' slabs with
 // peer copies ordered by events (works on one GPU or across NVLink peers).
-int exchange_group(hw_group* grp, int phase) {
+// plan(h) lists the transfers of rank h (the same fields in the same order on every rank).
+template <typename PLAN>
+int exchange_group_plan(hw_group* grp, PLAN plan) {
     for (hw_solver* h : grp->ranks) {
         CU(cudaSetDevice(h->d.device));
         CU(cudaEventRecord(h->ev_phase, h->st));
@@ -785,18 +825,18 @@ int exchange_group(hw_group* grp, int phase) {
     for (hw_solver* b : grp->ranks) {
         CU(cudaSetDevice(b->d.device));
         const int pv = prev_rank(b), nx_ = next_rank(b);
-        std::vector<Xfer> mine = xfers(b, phase);
+        std::vector<Xfer> mine = plan(b);
         if (pv >= 0) {
             hw_solver* a = grp->ranks[pv];
             CU(cudaStreamWaitEvent(b->st, a->ev_phase, 0));
-            std::vector<Xfer> theirs = xfers(a, phase);
+            std::vector<Xfer> theirs = plan(a);
             for (size_t k = 0; k < mine.size(); k++)
                 CU(cudaMemcpyPeerAsync(mine[k].dst_top, b->d.device, theirs[k].src_bottom, a->d.device, mine[k].bytes, b->st));
         }
         if (nx_ >= 0) {
             hw_solver* a = grp->ranks[nx_];
             CU(cudaStreamWaitEvent(b->st, a->ev_phase, 0));
-            std::vector<Xfer> theirs = xfers(a, phase);
+            std::vector<Xfer> theirs = plan(a);
             for (size_t k = 0; k < mine.size(); k++)
                 CU(cudaMemcpyPeerAsync(mine[k].dst_bottom, b->d.device, theirs[k].src_top, a->d.device, mine[k].bytes, b->st));
         }
@@ -810,6 +850,10 @@ int exchange_group(hw_group* grp, int phase) {
         if (nx_ >= 0) CU(cudaStreamWaitEvent(a->st, grp->ranks[nx_]->ev_copied, 0));
     }
     return HW_OK;
+}
+
+int exchange_group(hw_group* grp, int phase) {
+    return exchange_group_plan(grp, [phase](const hw_solver* h) { return xfers(h, phase); });
 }
 
 int exchange(hw_solver* h, int phase) {
@@ -1089,8 +1133,10 @@ static AcFusedParams fused_params(const hw_solver* h, int64_t nt) {
     AcFusedParams F;
     memset(&F, 0, sizeof(F));
     F.nx = h->d.nx;
-    F.ns = h->d.ns;
+    F.ns = field_rows(h, F_P);  // local rows (= ns in a single domain)
     F.pitch = h->g.pitch;
+    F.slab = (h->world > 1 || h->transport == 2) ? 1 : 0;
+    F.counter = h->counter;
     F.rho_x = h->lp[HW_PL_RHO_X]; F.rho_s = h->lp[HW_PL_RHO_S]; F.beta = h->lp[HW_PL_BETA];
     F.e_beta = h->ep64[HW_PL_BETA]; F.e_rho_x = h->ep64[HW_PL_RHO_X]; F.e_rho_s = h->ep64[HW_PL_RHO_S];
     F.k = make_consts(h->d.taps, h->dt_u);
@@ -1122,7 +1168,12 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
     RunCtx C;
     int rc = run_begin(h, variant, nt, energy, true, C);
     if (rc) return rc;
-    if ((rc = exchange(h, 0)) || (rc = exchange(h, 1))) return rc;  // halos of the uploaded state
+    const bool fused_slab = h->fused && h->transport == 2;
+    if (fused_slab) {  // halos of the uploaded state
+        if ((rc = exchange_nccl_list(h, xfers_fused(h, 0)))) return rc;
+    } else if ((rc = exchange(h, 0)) || (rc = exchange(h, 1))) {
+        return rc;
+    }
     if (timed) CU(cudaEventRecord(h->ev0, h->st));
     if (h->fused) {  // fused kernels, ping-pong A <-> B: launch L reads buffer L % 2
         AcFusedParams F = fused_params(h, nt);
@@ -1147,6 +1198,7 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
             }
             cur ^= 1;
             h->launches++;
+            if (fused_slab && (rc = exchange_nccl_list(h, xfers_fused(h, cur)))) return rc;
         }
     } else {
         for (int64_t n = 0; n < nt; n++) {
@@ -1291,6 +1343,36 @@ int hw_run_group(hw_solver* const* hs, int32_t nslabs, int32_t variant, int64_t 
         CU(cudaStreamWaitEvent(grp->ranks[r]->st, grp->ranks[0]->ev_phase, 0));
         if ((rc = run_begin(grp->ranks[r], variant, nt, energy, false, C[r]))) return rc;
     }
+    if (grp->ranks[0]->fused) {  // fused 2D slabs: one kernel per step per slab, one exchange per step
+        std::vector<AcFusedParams> F(nslabs);
+        std::vector<std::array<std::array<__half*, FUSED_NSTREAM>, 2>> bufs(nslabs);
+        for (hw_solver* h : grp->ranks) {
+            F[h->rank] = fused_params(h, nt);
+            __half* b[2][FUSED_NSTREAM];
+            fused_bufs(h, b);
+            for (int k = 0; k < 2; k++)
+                for (int j = 0; j < FUSED_NSTREAM; j++) bufs[h->rank][k][j] = b[k][j];
+        }
+        auto plan = [](int buf) { return [buf](const hw_solver* h) { return xfers_fused(h, buf); }; };
+        if ((rc = exchange_group_plan(grp, plan(0)))) return rc;  // halos of the uploaded state
+        int cur = 0;
+        for (int64_t n = 0; n < nt; n++) {
+            for (hw_solver* h : grp->ranks) {
+                cudaSetDevice(h->d.device);
+                AcFusedParams& P = F[h->rank];
+                for (int j = 0; j < FUSED_NSTREAM; j++) {
+                    P.in[j] = bufs[h->rank][cur][j];
+                    P.out[j] = bufs[h->rank][cur ^ 1][j];
+                }
+                const int64_t every = h->d.energy_every;
+                launch_ac2d_fused(variant, h->d.order, P, h->fused_blocks, n, src_samples ? src_samples[n] : 0.0,
+                                  energy && ((n + 1) % every == 0), (n + 1) / every, h->st);
+                h->launches++;
+            }
+            cur ^= 1;
+            if ((rc = exchange_group_plan(grp, plan(cur)))) return rc;
+        }
+    } else {
     if (nslabs > 1) {
         if ((rc = exchange_group(grp, 0)) || (rc = exchange_group(grp, 1))) return rc;  // halos of the uploaded state
     }
@@ -1306,6 +1388,7 @@ int hw_run_group(hw_solver* const* hs, int32_t nslabs, int32_t variant, int64_t 
             cudaSetDevice(h->d.device);
             run_epilogue(h, C[h->rank], n);
         }
+    }
     }
     for (hw_solver* h : grp->ranks) {
         CU(cudaSetDevice(h->d.device));
@@ -1326,6 +1409,10 @@ int hw_run_group(hw_solver* const* hs, int32_t nslabs, int32_t variant, int64_t 
         if (fail_step) *fail_step = step0 + c.fail_step;
         if (fail_field) *fail_field = bit;
         g_err = "non-finite value after step " + std::to_string(step0 + c.fail_step);
+    }
+    for (hw_solver* h : grp->ranks) {  // fused slabs: newest state home to buffer A
+        CU(cudaSetDevice(h->d.device));
+        if ((rc = fused_copy_back(h, done, variant))) return rc;
     }
     const int64_t nrec = h0->d.n_receivers;
     const int64_t ne = energy ? 1 + (status == HW_OK ? nt / h0->d.energy_every : (done - 1) / h0->d.energy_every) : 0;

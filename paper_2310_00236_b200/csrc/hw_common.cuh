@@ -2,7 +2,7 @@
 //
 // HBM layout:
 //   * every field is [rows + 2G][nm][pitch] in its update-lane storage type, with
-//     G = 2 ghost slabs on each end of the slow axis and pitch a multiple of 32
+//     G = 3 ghost slabs on each end of the slow axis and pitch a multiple of 32
 //     elements (64 B rows for fp16); `base` points at (s=0, m=0, x=0).
 //   * x and mid are periodic through index arithmetic; the slow axis reads its
 //     ghost slabs, which encode the boundary condition and are kept current by the
@@ -18,7 +18,8 @@
 
 namespace hw {
 
-constexpr int G = 2;          // ghost slabs per side (4th-order staggered reach)
+constexpr int G = 3;          // ghost slabs per side: 4th-order staggered reach (2) + the fused
+                              // kernel's redundant vy halo rows, which read p rows -3 .. L+2 (slab mode)
 constexpr int NCOMP = 5;      // energy partial components per block
 constexpr int BLOCK = 256;    // threads per block for the phase kernels
 

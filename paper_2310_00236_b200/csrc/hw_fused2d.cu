@@ -159,7 +159,10 @@ __global__ void __launch_bounds__(512, 1)
     const uint32_t rb = (uint32_t)(nx * sizeof(__half));
 
     auto slot_row = [&](int slot, int st) { return ring + (slot * NSTREAM + st) * nx; };
+    // rows outside [0, ns): periodic wrap in a single domain, ghost rows (filled by the
+    // halo exchange, G >= 3 deep) in a slab
     auto wrap_row = [&](int64_t r) {
+        if (P.slab) return r;
         r %= ns;
         return r < 0 ? r + ns : r;
     };
@@ -214,7 +217,8 @@ __global__ void __launch_bounds__(512, 1)
     // wrapped front row, advanced without integer division; the row-uniform divisor
     // reciprocals of the next iteration are prefetched into registers.
     const int ns32 = (int)ns;
-    auto back = [&](int r, int k) { r -= k; return r < 0 ? r + ns32 : r; };  // wrapped r - k (k < ns)
+    const bool slab = P.slab != 0;
+    auto back = [&](int r, int k) { r -= k; return (!slab && r < 0) ? r + ns32 : r; };  // wrapped r - k (k < ns)
     int fw = (int)wrap_row(F0);
     float rcx = 0.f, rcs = 0.f, rcb = 0.f;
     if constexpr (ROWMED) {
@@ -226,7 +230,7 @@ __global__ void __launch_bounds__(512, 1)
     for (int i = 0; i < NI; i++) {
         const int u = i % FR;
         const uint32_t par = (uint32_t)((i / FR) & 1);
-        const int fwn = fw + 1 == ns32 ? 0 : fw + 1;
+        const int fwn = (!slab && fw + 1 == ns32) ? 0 : fw + 1;
         float rcx_n = 0.f, rcs_n = 0.f, rcb_n = 0.f;
         if constexpr (ROWMED) {
             rcx_n = __ldg(P.rho_x.rcp + fwn * P.rho_x.ss);
@@ -387,7 +391,7 @@ __global__ void __launch_bounds__(512, 1)
     __threadfence();
     __syncthreads();
     __shared__ unsigned int is_last;
-    if (tid == 0) is_last = atomicAdd(&P.ctrl->pad, 1u) == (unsigned int)(nb - 1);
+    if (tid == 0) is_last = atomicAdd(P.counter, 1u) == (unsigned int)(nb - 1);
     __syncthreads();
     if (!is_last) return;
     __shared__ double tot[NCOMP];
@@ -401,7 +405,7 @@ __global__ void __launch_bounds__(512, 1)
         double t = tot[0];
         for (int q = 1; q < NCOMP; q++) t += tot[q];
         P.e_vals[eidx] = P.scale * t;
-        P.ctrl->pad = 0u;
+        *P.counter = 0u;
     }
 }
 

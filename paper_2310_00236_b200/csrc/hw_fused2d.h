@@ -23,6 +23,9 @@ struct AcFusedParams {
     double* partials;
     double* e_vals;
     double scale;
+    unsigned int* counter;        // per-handle CTA arrival counter (last CTA reduces the energy)
+    int32_t slab;                 // slab of a decomposed domain: rows outside [0, ns) are ghost rows
+    int32_t pad;
 };
 size_t fused2d_smem_bytes(int64_t nx);
 bool fused2d_eligible(int64_t nx, int max_smem);

@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(288, 1)
     __threadfence();
     __syncthreads();
     __shared__ unsigned int is_last;
-    if (tid == 0) is_last = atomicAdd(&P.ctrl->pad, 1u) == (unsigned int)(gridDim.x - 1);
+    if (tid == 0) is_last = atomicAdd(P.counter, 1u) == (unsigned int)(gridDim.x - 1);
     __syncthreads();
     if (!is_last) return;
     if (tid == 0) {  // fixed-order fp64 reduction of the block partials
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(288, 1)
             for (int k = 1; k < NCOMP; k++) t += tot[k];
             P.e_vals[st == 0 ? eidxA : eidxB] = P.scale * t;
         }
-        P.ctrl->pad = 0u;
+        *P.counter = 0u;
     }
 }
 

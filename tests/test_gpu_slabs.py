@@ -134,3 +134,30 @@ def test_slab_group_single_steps():
         b.step_compensated(sb)
     for n in a.FIELDS:
         assert_same_bits(getattr(sb, n).values, getattr(sa, n).values, n)
+
+
+@pytest.mark.parametrize("slabs", [2, 5])
+def test_fused_2d_slabs_receivers_on_slab_edges(slabs):
+    """The fused single-pass kernel on slabs (ghost rows exchanged once per step; its
+    redundant vy halo rows read the padded medium planes) equals the single domain."""
+    nx, ny = 512, 200
+
+    def make(k):
+        dx = 1.0 / nx
+        med = hw.build_layered_acoustic(nx, ny, [(0.3, 1.0, 1.0), (0.55, 1.3, 2.0), (1.0, 1.5, 2.25)])
+        g = hw.GridSpec(nx, ny, dx, float(np.float16(0.3 * dx)), 33)
+        src = hw.SourceSpec(hw.SourceKind.PRESSURE_POINT, 200, 80, hw.RickerSpec(1 / (10 * dx), amplitude=2.0))
+        edges = sorted({r * ny // slabs + d for r in range(slabs) for d in (-1, 0)} - {-1})
+        s = hw.AcousticSolver(g, med, src, stencil_precision=hw.Precision.FP16, energy_every=1, slabs=k,
+                              receivers=tuple((7 * j % nx, e) for j, e in enumerate(edges)) + ((0, ny - 1),))
+        st = s.new_state()
+        yy, xx = np.mgrid[0:ny, 0:nx] / nx
+        st.p.values = np.exp(-((xx - 0.5) ** 2 + (yy - 0.2) ** 2) / 0.005).astype(np.float16)
+        st.vy.values = np.random.default_rng(5).uniform(-0.01, 0.01, (ny, nx)).astype(np.float16)
+        return s, st
+
+    a, sa, b, sb = _pair(make, slabs)
+    oa = a.run(hw.Variant.OP6, sa)
+    ob = b.run(hw.Variant.OP6, sb)
+    assert a.kernel_path() == "fused2d" and b.kernel_path() == "fused2d" and b.transport() == 1
+    _compare(a, sa, oa, b, sb, ob)
