@@ -8,9 +8,13 @@ One bench "step" = one full config-2 run (5000 leapfrog steps on 4096^2 cells).
           with CUDA events on the library's stream, max over ranks.
   e2e   : the same run through the public API AcousticSolver.run(OP3, state) with
           host state (pinned) -> HBM -> host every step, wall-clock timed.
-Multi-GPU (torchrun): each rank runs its own replica of the workload (weak scaling).
+Multi-GPU (torchrun, one process per GPU): weak scaling by slab decomposition -- the
+global grid is 4096 x (4096 N), rank r owns rows [4096 r, 4096 (r+1)) (one config-2 block
+per GPU), the fused kernel runs on every slab and the ghost rows (p, vy, rvy; 3 each way)
+are exchanged with NCCL send/recv once per leapfrog step.  `--decomposed on` runs that
+path at N = 1 (the NCCL transport exchanging with itself: HALFWAVE_NCCL_SELF=1).
 
-python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--decomposed auto|on|off]
 """
 
 from __future__ import annotations
@@ -40,19 +44,20 @@ WORKLOAD = ("config2: 2D acoustic 4096x4096, 4th-order staggered FD, two-layer m
             "fp16 compensated (op3), energy every 10")
 
 
-def make_solver(hw, nt=NT, device=0, n=N):
+def make_solver(hw, nt=NT, device=0, n=N, ny=None, distributed=False):
+    ny = n if ny is None else ny  # slow axis: n per rank in the decomposed multi-GPU run
     dx = 1.0 / n
-    med = hw.build_layered_acoustic(n, n, [(0.5, 1.0, 1.0), (1.0, 1.5, 2.25)])
+    med = hw.build_layered_acoustic(n, ny, [(0.5, 1.0, 1.0), (1.0, 1.5, 2.25)])
     c_bound = med.c_max()  # 1/sqrt(min rho * min beta) = 1.5, the reference's CFL bound (grids.py:186-190)
     dt = float(np.float16(0.5 * dx / c_bound))
     if dt > 0.5 * dx / c_bound:
         dt = float(np.nextafter(np.float16(dt), np.float16(0)))
-    grid = hw.GridSpec(n, n, dx, dt, nt)
+    grid = hw.GridSpec(n, ny, dx, dt, nt)
     f = 1.0 / (10 * dx)  # c_min / (10 h): 10 points per wavelength
     src = hw.SourceSpec(hw.SourceKind.PRESSURE_POINT, n // 2, 8, hw.RickerSpec(f_center=f, amplitude=100.0))
     return hw.AcousticSolver(grid, med, src, stencil_precision=hw.Precision.FP16,
                              update_precision=hw.Precision.FP16, receivers=((n // 2, n // 4),),
-                             energy_every=EVERY, device=device)
+                             energy_every=EVERY, device=device, distributed=distributed)
 
 
 def peak_hbm():
@@ -189,6 +194,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nt", type=int, default=NT, help="leapfrog steps per bench step")
+    ap.add_argument("--decomposed", default="auto", choices=["auto", "on", "off"],
+                    help="slab decomposition with NCCL halo exchange (auto: when N > 1)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -199,15 +206,37 @@ def main():
 
     ws, rank, local = dist_env()
     dist = None
-    if ws > 1:
+    decomposed = args.decomposed == "on" or (args.decomposed == "auto" and ws > 1)
+    torch.cuda.set_device(local)
+    if ws > 1 or decomposed:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        if ws > 1:
+            dist.init_process_group("nccl")
+        else:  # --decomposed on at N = 1: one-rank job on the NCCL transport (self exchange)
+            import socket
+
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+            os.environ["HALFWAVE_NCCL_SELF"] = "1"
     dev = local
-    torch.cuda.set_device(dev)
-    s = make_solver(hw, nt=args.nt, device=dev)
-    cells = N * N
+    parallelism = "single"
+    s = None
+    if decomposed:
+        try:
+            s = make_solver(hw, nt=args.nt, device=dev, ny=N * ws, distributed=True)
+            s.upload(s.new_state())
+            parallelism = f"slabs x{ws} (NCCL halo exchange of p, vy, rvy once per step)"
+        except Exception as exc:  # keep the scaling run alive: fall back to replicas, say so
+            s = None
+            parallelism = f"replicas x{ws} (decomposed run failed: {type(exc).__name__}: {exc})"[:300]
+    if s is None:
+        s = make_solver(hw, nt=args.nt, device=dev)
+        if ws > 1 and not decomposed:
+            parallelism = f"replicas x{ws}"
+    cells = N * N  # per rank
 
     # ---------------------------------------------------------- device-resident value
     st = s.new_state()
@@ -218,7 +247,7 @@ def main():
         step0 += args.nt
     launches = 0
     ms_total = 0.0
-    if dist:
+    if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with Clocks(dev) as clk:
@@ -229,7 +258,7 @@ def main():
             step0 += args.nt
         torch.cuda.synchronize()
         wall = time.perf_counter() - w0
-    if dist:
+    if ws > 1:
         t = torch.tensor([ms_total], device=f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
@@ -265,19 +294,20 @@ def main():
     st2 = s.new_state()
     for n in s.FIELDS:
         getattr(st2, n).values = pinned_like(getattr(st2, n).values)
-    h2d = sum(getattr(st2, n).values.nbytes for n in s.FIELDS) + 8 * args.nt
+    share = ws if s.distributed else 1  # a rank copies only its own slab's rows
+    h2d = sum(getattr(st2, n).values.nbytes for n in s.FIELDS) // share + 8 * args.nt
     d2h = h2d - 8 * args.nt + 8 * args.nt * len(s.receivers) + 8 * (1 + args.nt // EVERY)
     s.run(hw.Variant.OP3, st2)  # warm (allocations)
     for n in s.FIELDS:
         getattr(st2, n).values = pinned_like(getattr(st2, n).values)
-    if dist:
+    if ws > 1:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         out = s.run(hw.Variant.OP3, st2)
         _ = float(out.energy.values[-1])
     e2e_wall = time.perf_counter() - t0
-    if dist:
+    if ws > 1:
         t = torch.tensor([e2e_wall], device=f"cuda:{dev}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_wall = float(t.item())
@@ -292,8 +322,9 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "fp16", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "grid": [N, N], "leapfrog_steps_per_bench_step": args.nt,
-                       "variant": "op3", "parallelism": f"replicas x{ws}" if ws > 1 else "single",
+            "config": {"workload": WORKLOAD, "grid": [N, N * ws if s.distributed else N],
+                       "leapfrog_steps_per_bench_step": args.nt, "variant": "op3", "parallelism": parallelism,
+                       "path": s.kernel_path(), "transport": s.transport(),
                        "l2": "inputs larger than L2 (state 192 MiB > 126 MB L2)"},
             "roofline": roofline, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "wall_s_timed_region": wall,

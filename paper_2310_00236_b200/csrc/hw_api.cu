@@ -353,6 +353,10 @@ struct hw_solver {
     // fused single-pass path (2D acoustic, binary16): ping-pong partner buffers
     bool fused = false;
     int fused_blocks = 0;
+    // NCCL slab of the fused kernel: edge bands + exchange on st, interior bands on st2
+    cudaStream_t st2 = nullptr;
+    cudaEvent_t ev_edge[2] = {}, ev_int[2] = {};
+    int nb_int = 0;
     bool tb2 = false;  // two steps per launch (temporal blocking, hw_tb2d.cu)
     int tb2_tiles = 0, tb2_bands = 0;
     double* partials_b = nullptr;  // stage-B energy partials of the two-step kernel
@@ -656,6 +660,15 @@ int setup_handle(hw_solver* h) {
             if (nbf < 1) nbf = 1;
             h->fused_blocks = (int)(nbf < nsm ? nbf : nsm);
             h->fused = true;
+            if (h->transport == 2 && field_rows(h, F_P) >= 5 * FUSED_EDGE) {  // overlapped halo exchange
+                CU(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
+                for (int k = 0; k < 2; k++) {
+                    CU(cudaEventCreateWithFlags(&h->ev_edge[k], cudaEventDisableTiming));
+                    CU(cudaEventCreateWithFlags(&h->ev_int[k], cudaEventDisableTiming));
+                }
+                int64_t ni = (field_rows(h, F_P) - 2 * FUSED_EDGE) / 4;
+                h->nb_int = (int)(ni < nsm - 2 ? ni : nsm - 2);
+            }
             // two steps per launch: opt-in (HALFWAVE_TB=1); measured slower than the
             // single-step kernel on B200 (compute/latency-bound)
             const char* tbe = getenv("HALFWAVE_TB");
@@ -745,6 +758,11 @@ void release_handle(hw_solver* h) {
     if (h->evals) cudaFree(h->evals);
     if (h->rec_off) cudaFree(h->rec_off);
     if (h->rec_sorted) cudaFree(h->rec_sorted);
+    for (int k = 0; k < 2; k++) {
+        if (h->ev_edge[k]) cudaEventDestroy(h->ev_edge[k]);
+        if (h->ev_int[k]) cudaEventDestroy(h->ev_int[k]);
+    }
+    if (h->st2) cudaStreamDestroy(h->st2);
     if (h->counter) cudaFree(h->counter);
     if (h->ev0) cudaEventDestroy(h->ev0);
     if (h->ev1) cudaEventDestroy(h->ev1);
@@ -1175,7 +1193,42 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
         return rc;
     }
     if (timed) CU(cudaEventRecord(h->ev0, h->st));
-    if (h->fused) {  // fused kernels, ping-pong A <-> B: launch L reads buffer L % 2
+    if (h->fused && fused_slab && h->st2) {
+        // NCCL slab, overlapped: per step the two thin edge bands run first on st and the
+        // ghost exchange follows them on st, while the interior bands run on st2.
+        //   st : wait interior(n-1) | edge(n) | record E(n) | exchange(n)
+        //   st2: wait edge(n-1)     | interior(n) | record I(n)
+        // (edge(n) overwrites rows interior(n-1) reads and vice versa: ping-pong buffers)
+        AcFusedParams F = fused_params(h, nt);
+        __half* bufs[2][FUSED_NSTREAM];
+        fused_bufs(h, bufs);
+        const int64_t every = C.every;
+        AcFusedParams Fe = F, Fi = F;
+        Fe.band_mode = 1;
+        Fi.band_mode = 2;
+        Fe.edge = Fi.edge = FUSED_EDGE;
+        Fe.nb_total = Fi.nb_total = 2 + h->nb_int;
+        CU(cudaEventRecord(h->ev_edge[1], h->st));  // st2 starts after everything queued on st
+        int cur = 0;
+        for (int64_t n = 0; n < nt; n++) {
+            for (int j = 0; j < FUSED_NSTREAM; j++) {
+                Fe.in[j] = Fi.in[j] = bufs[cur][j];
+                Fe.out[j] = Fi.out[j] = bufs[cur ^ 1][j];
+            }
+            const double sv = src ? src[n] : 0.0;
+            const int sample = energy && ((n + 1) % every == 0);
+            if (n > 0) CU(cudaStreamWaitEvent(h->st, h->ev_int[(n - 1) & 1], 0));
+            launch_ac2d_fused(variant, h->d.order, Fe, 2, n, sv, sample, (n + 1) / every, h->st);
+            CU(cudaEventRecord(h->ev_edge[n & 1], h->st));
+            CU(cudaStreamWaitEvent(h->st2, h->ev_edge[(n + 1) & 1], 0));  // edge(n-1), or the start
+            launch_ac2d_fused(variant, h->d.order, Fi, h->nb_int, n, sv, sample, (n + 1) / every, h->st2);
+            CU(cudaEventRecord(h->ev_int[n & 1], h->st2));
+            h->launches += 2;
+            cur ^= 1;
+            if ((rc = exchange_nccl_list(h, xfers_fused(h, cur)))) return rc;
+        }
+        if (nt > 0) CU(cudaStreamWaitEvent(h->st, h->ev_int[(nt - 1) & 1], 0));
+    } else if (h->fused) {  // fused kernels, ping-pong A <-> B: launch L reads buffer L % 2
         AcFusedParams F = fused_params(h, nt);
         __half* bufs[2][FUSED_NSTREAM];
         fused_bufs(h, bufs);

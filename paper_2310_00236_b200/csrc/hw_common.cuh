@@ -394,8 +394,9 @@ __device__ __forceinline__ bool halted(const Ctrl* ctrl, int64_t n) {
     return *reinterpret_cast<const volatile int64_t*>(&ctrl->fail_step) < n;
 }
 
-// Block-wide fp64 sum of NCOMP components; thread 0 writes the block partial.
-__device__ __forceinline__ void block_partials(double v[NCOMP], double* out) {
+// Block-wide fp64 sum of NCOMP components; thread 0 writes the block partial (row idx,
+// default: the linear block index).
+__device__ __forceinline__ void block_partials(double v[NCOMP], double* out, int64_t idx = -1) {
     __shared__ double red[32][NCOMP];  // any block size up to 1024 threads
     const int tid = threadIdx.x;
     int lane_id = tid & 31, warp = tid >> 5;
@@ -410,7 +411,7 @@ __device__ __forceinline__ void block_partials(double v[NCOMP], double* out) {
     if (tid < NCOMP) {
         double a = 0.0;
         for (int w = 0; w < (int)(blockDim.x >> 5); w++) a += red[w][tid];
-        const int64_t bid = ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        const int64_t bid = idx >= 0 ? idx : ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
         out[bid * NCOMP + tid] = a;
     }
 }

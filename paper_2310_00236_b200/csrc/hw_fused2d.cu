@@ -149,8 +149,25 @@ __global__ void __launch_bounds__(512, 1)
     __half* ring = reinterpret_cast<__half*>(smem + 256);
     const int64_t nx = P.nx, ns = P.ns, pitch = P.pitch;
     __half* xrows = ring + (int64_t)FR * NSTREAM * nx;  // two rows, alternating by iteration parity
-    const int nb = gridDim.x, b = blockIdx.x;
-    const int y0 = (int)((int64_t)b * ns / nb), y1 = (int)((int64_t)(b + 1) * ns / nb);
+    const int b = blockIdx.x;
+    int y0, y1, pidx, nb;  // this CTA's rows, its energy-partial slot, CTAs of the whole step
+    if (P.band_mode == 1) {  // edge bands: launched ahead of the interior so the halo exchange overlaps it
+        y0 = b == 0 ? 0 : (int)ns - P.edge;
+        y1 = b == 0 ? P.edge : (int)ns;
+        pidx = b;
+        nb = P.nb_total;
+    } else if (P.band_mode == 2) {
+        const int64_t ni = ns - 2 * P.edge;
+        y0 = P.edge + (int)((int64_t)b * ni / gridDim.x);
+        y1 = P.edge + (int)((int64_t)(b + 1) * ni / gridDim.x);
+        pidx = 2 + b;
+        nb = P.nb_total;
+    } else {
+        nb = gridDim.x;
+        y0 = (int)((int64_t)b * ns / nb);
+        y1 = (int)((int64_t)(b + 1) * ns / nb);
+        pidx = b;
+    }
     const int F0 = y0 - 3;
     const int NI = (y1 + 3) - F0;
     const int tid = threadIdx.x;
@@ -387,7 +404,7 @@ __global__ void __launch_bounds__(512, 1)
     for (int q = 0; q < NSTREAM; q++) mask |= nonfinite_acc(acc[q]) << q;
     record_failure(P.ctrl, n, mask);
     if (!sample) return;
-    block_partials(e, P.partials);
+    block_partials(e, P.partials, pidx);
     __threadfence();
     __syncthreads();
     __shared__ unsigned int is_last;

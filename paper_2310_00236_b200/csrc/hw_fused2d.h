@@ -7,6 +7,7 @@
 
 namespace hw {
 constexpr int FUSED_NSTREAM = 6;
+constexpr int FUSED_EDGE = 8;  // rows of each edge band when the halo exchange is overlapped
 struct AcFusedParams {
     int64_t nx, ns, pitch;
     const __half* in[FUSED_NSTREAM];  // p vx vy rp rvx rvy
@@ -25,7 +26,10 @@ struct AcFusedParams {
     double scale;
     unsigned int* counter;        // per-handle CTA arrival counter (last CTA reduces the energy)
     int32_t slab;                 // slab of a decomposed domain: rows outside [0, ns) are ghost rows
-    int32_t pad;
+    int32_t band_mode;            // 0: CTAs split [0, ns); 1: the two edge bands [0, edge), [ns-edge, ns);
+                                  // 2: the interior [edge, ns-edge) (overlapped halo exchange)
+    int32_t edge;                 // rows per edge band (band_mode 1/2)
+    int32_t nb_total;             // CTAs of the step over both launches (band_mode 1/2)
 };
 size_t fused2d_smem_bytes(int64_t nx);
 bool fused2d_eligible(int64_t nx, int max_smem);

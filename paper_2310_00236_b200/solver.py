@@ -264,8 +264,10 @@ class _DeviceSolver:
 
     def _download(self, state):
         dtype = DTYPES[self.update_precision]
-        if self.distributed:  # rows of other ranks keep their uploaded values
-            arrs = [a.copy() for a in self._uploaded]
+        if self.distributed:  # rows of other ranks keep their uploaded values (own rows overwritten below)
+            arrs = [_host_empty(u.shape, u.dtype) for u in self._uploaded]
+            for a, u in zip(arrs, self._uploaded):
+                np.copyto(a, u)
         else:  # fresh arrays, as the reference returns (acoustic.py:147-152), in pinned memory
             arrs = [_host_empty(self.grid.shape(self._stagger_of(n)), dtype) for n in self.FIELDS]
         ptrs = (ctypes.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
