@@ -70,6 +70,7 @@ class Stagger(enum.Enum):
 class Boundary(enum.Enum):
     PERIODIC = "periodic"
     FREE_SURFACE = "free-surface"
+    RIGID = "rigid"  # extension (BASELINE config 1): p = 0 walls, 2D acoustic only
 
     def __str__(self):
         return self.value
@@ -97,8 +98,10 @@ class GridSpec:
             raise ValueError("dx and dt must be positive")
         if self.nt < 0:
             raise ValueError("nt must be nonnegative")
-        if self.bc_x is not Boundary.PERIODIC:
-            raise ValueError("x boundary must be periodic; free surfaces are y-only")
+        if self.bc_x is Boundary.FREE_SURFACE:
+            raise ValueError("x boundary must be periodic (or rigid); free surfaces are y-only")
+        if Boundary.RIGID in (self.bc_x, self.bc_y) and self.nz is not None:
+            raise ValueError("rigid walls are a 2D acoustic extension")
         if self.order not in (2, 4):
             raise ValueError(f"order must be 2 or 4, got {self.order}")
         if self.nz is not None and self.bc_y is not Boundary.PERIODIC:
@@ -112,18 +115,33 @@ class GridSpec:
     def free_surface_y(self) -> bool:
         return self.bc_y is Boundary.FREE_SURFACE
 
+    @property
+    def rigid_x(self) -> bool:
+        return self.bc_x is Boundary.RIGID
+
+    @property
+    def rigid_y(self) -> bool:
+        return self.bc_y is Boundary.RIGID
+
     def rows(self, stagger: Stagger) -> int:
-        """Extent along the slow axis (y in 2D, z in 3D)."""
+        """Extent along the slow axis (y in 2D, z in 3D): integer-y sub-grids carry
+        the wall / surface row too (ny + 1) with free surfaces and rigid walls."""
         if self.nz is not None:
             return self.nz
-        if self.free_surface_y and not stagger.half_y:
+        if (self.free_surface_y or self.rigid_y) and not stagger.half_y:
             return self.ny + 1
         return self.ny
+
+    def cols(self, stagger: Stagger) -> int:
+        """Extent along x: integer-x sub-grids carry both rigid walls (nx + 1)."""
+        if self.nz is None and self.rigid_x and not stagger.half_x:
+            return self.nx + 1
+        return self.nx
 
     def shape(self, stagger: Stagger) -> tuple:
         if self.nz is not None:
             return (self.nz, self.ny, self.nx)
-        return (self.rows(stagger), self.nx)
+        return (self.rows(stagger), self.cols(stagger))
 
     def cfl(self, c_max: float) -> float:
         return c_max * self.dt / self.dx
@@ -347,6 +365,14 @@ def extend_rows(plane: np.ndarray, grid, stagger: Stagger) -> np.ndarray:
     if rows == plane.shape[0]:
         return plane
     return np.concatenate([plane, plane[-1:, :]], axis=0)
+
+
+def extend_cols(plane: np.ndarray, grid, stagger: Stagger) -> np.ndarray:
+    """Canonical plane onto a rigid-x sub-grid's nx+1 columns by repeating the last
+    column (the column analogue of extend_rows)."""
+    if grid.cols(stagger) == plane.shape[1]:
+        return plane
+    return np.concatenate([plane, plane[:, -1:]], axis=1)
 
 
 # --- WMED medium files (reference grids.py:272-318): little-endian header

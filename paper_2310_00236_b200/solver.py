@@ -102,14 +102,16 @@ class _DeviceSolver:
         self.ndim = 2 if _grid_nz(grid) is None else 3
         self.order = getattr(grid, "order", 4)
         self.stencil = StencilSpec.make(sp, grid.dx, self.order)
+        self._dgrid = self._device_grid()
         self._build_desc()
 
     # ------------------------------------------------------------ validation
     @staticmethod
-    def _check_index(what, idx, grid):
+    def _check_index(what, idx, grid, ext=None):
         ix, iy = idx[0], idx[1]
         nz = _grid_nz(grid)
-        ok = 0 <= ix < grid.nx and 0 <= iy < grid.ny
+        nx_, ny_ = ext if ext is not None else (grid.nx, grid.ny)
+        ok = 0 <= ix < nx_ and 0 <= iy < ny_
         if nz is not None:
             iz = idx[2] if len(idx) > 2 and idx[2] is not None else -1
             ok = ok and 0 <= iz < nz
@@ -124,8 +126,12 @@ class _DeviceSolver:
         grid.check_cfl(medium.c_max())
         if source is not None:
             self._check_index("source", (source.ix, source.iy, getattr(source, "iz", None)), grid)
+        ext = None
+        if hasattr(grid, "cols") and _grid_nz(grid) is None and self.TRACE_FIELD in self.STAGGERS:
+            st = self.STAGGERS[self.TRACE_FIELD]  # receivers index the trace field's own sub-grid
+            ext = (grid.cols(st), grid.ny if _is_free_surface(grid) else grid.rows(st))
         for r in receivers:
-            self._check_index("receiver", tuple(r), grid)
+            self._check_index("receiver", tuple(r), grid, ext)
         if energy_every < 1:
             raise ValueError("energy_every must be at least 1")
 
@@ -136,8 +142,23 @@ class _DeviceSolver:
     def _source_code(self) -> int:
         raise NotImplementedError
 
+    # ------------------------------------------------------------ device domain hooks
+    def _device_grid(self):
+        """The grid the device runs (the mirrored periodic grid for rigid walls)."""
+        return self.grid
+
+    def _to_device(self, name, arr):
+        """User state array -> device-domain array (identity unless mirrored)."""
+        return arr
+
+    def _to_user(self, name, arr):
+        return arr
+
+    def _energy_scale(self) -> float:
+        return 1.0
+
     def _build_desc(self):
-        g = self.grid
+        g = self._dgrid
         nz = _grid_nz(g)
         d = _abi.Desc()
         d.abi_version = _abi.ABI_VERSION
@@ -249,7 +270,7 @@ class _DeviceSolver:
             want = self.grid.shape(self._stagger_of(name))
             if arr.shape != tuple(want):
                 raise ValueError(f"state field {name} has shape {arr.shape}, expected {tuple(want)}")
-            out.append(arr)
+            out.append(self._to_device(name, arr))
         return out
 
     def _stagger_of(self, name):
@@ -269,12 +290,12 @@ class _DeviceSolver:
             for a, u in zip(arrs, self._uploaded):
                 np.copyto(a, u)
         else:  # fresh arrays, as the reference returns (acoustic.py:147-152), in pinned memory
-            arrs = [_host_empty(self.grid.shape(self._stagger_of(n)), dtype) for n in self.FIELDS]
+            arrs = [_host_empty(self._dgrid.shape(self._stagger_of(n)), dtype) for n in self.FIELDS]
         ptrs = (ctypes.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
         for h in self._handles():
             _abi.check(_abi.load().hw_get_state(h, ptrs), "hw_get_state")
         for name, a in zip(self.FIELDS, arrs):
-            getattr(state, name).values = a
+            getattr(state, name).values = self._to_user(name, a)
 
     def _hw_run(self, *args):
         lib = _abi.load()
@@ -356,7 +377,7 @@ class _DeviceSolver:
                 ts.iz = int(r[2])
             out_traces.append(ts)
         k = ne.value
-        energy = EnergySeries(e_times[:k].copy(), e_vals[:k].copy())
+        energy = EnergySeries(e_times[:k].copy(), e_vals[:k] * self._energy_scale())
         return RunOutput(out_traces, energy, {"range_failure": None})
 
     # ------------------------------------------------------------ bench hooks
