@@ -121,3 +121,14 @@ def test_cli_desk_run_matches_reference_outputs(tmp_path, preset):
     want = np.loadtxt(GOLD / preset / "energy.csv", delimiter=",", skiprows=1)
     np.testing.assert_array_equal(got[:, 0], want[:, 0])
     np.testing.assert_allclose(got[:, 1], want[:, 1], rtol=1e-12)
+
+
+def test_ini_rigid_walls(tmp_path):
+    """grid.bc_x / grid.bc_y = rigid (p = 0 walls, extension) parse into a rigid GridSpec."""
+    ini = tmp_path / "box.ini"
+    ini.write_text("[grid]\nnx = 32\nny = 24\ndx = 0.03125\ndt = 0.005\nnt = 4\norder = 2\nbc_x = rigid\nbc_y = rigid\n"
+                   "[medium]\nkind = acoustic\nrho = 1.0\nc = 1.0\n[precision]\nstencil = fp16\nmode = op3\n")
+    c = config.parse_config(ini)
+    assert c.grid.rigid_x and c.grid.rigid_y and c.grid.shape(hw.Stagger.CELL) == (25, 33)
+    with pytest.raises(ValueError, match="periodic"):
+        config.parse_config(ini, sets=["grid.bc_x=free-surface"])

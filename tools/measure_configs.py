@@ -26,11 +26,13 @@ def timed(name, s, variant, bytes_per_cell, cells, nt=NT):
                       "frac_of_6551": rate * bytes_per_cell / 6551.7e9, "launches": s.last_launch_count()}), flush=True)
 
 
-def cfg1(order):  # 2D acoustic 256^2, CFL 0.5 (4th order twin: reference-native periodic)
+def cfg1(order=2, prec=F16):
+    """BASELINE config 1: 256^2 cells, h = 1/256, 2nd order, dt = 0.5 h, rigid p = 0 walls
+    (mirrored periodic 512^2 on the device), constant rho = kappa = 1, energy every step."""
     n = 256
     dx = 1.0 / n
-    g = hw.GridSpec(n, n, dx, 0.5 * dx if order == 2 else 0.5 * dx, NT, order=order)
-    return hw.AcousticSolver(g, hw.build_homogeneous_acoustic(n, n, 1.0, 1.0), stencil_precision=F16, energy_every=1)
+    g = hw.GridSpec(n, n, dx, 0.5 * dx, NT, order=order, bc_x=hw.Boundary.RIGID, bc_y=hw.Boundary.RIGID)
+    return hw.AcousticSolver(g, hw.build_homogeneous_acoustic(n, n, 1.0, 1.0), stencil_precision=prec, energy_every=1)
 
 
 def cfg3():  # 3D acoustic 512^3, 2nd order, full beta plane
@@ -63,7 +65,10 @@ def cfg5():  # 3D elastic 512^3 per GPU, 2nd order, layered
 if __name__ == "__main__":
     which = sys.argv[2].split(",") if len(sys.argv) > 2 else ["1", "3", "4", "5"]
     if "1" in which:
-        timed("1: 2D acoustic 256^2 4th-order periodic fp16 op3", cfg1(4), hw.Variant.OP3, 24, 256 * 256)
+        for name, prec, var in (("fp16 naive", F16, None), ("fp16 op3", F16, hw.Variant.OP3),
+                                ("fp64", hw.Precision.FP64, None)):
+            timed(f"1: 2D acoustic 256^2 2nd order rigid walls {name}, energy every step", cfg1(2, prec), var, 24,
+                  256 * 256)
     if "3" in which:
         timed("3: 3D acoustic 512^3 2nd order fp16 op3 (beta plane)", cfg3(), hw.Variant.OP3, 34, 512 ** 3)
     if "4" in which:

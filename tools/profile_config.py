@@ -14,7 +14,7 @@ def cfg2():
     return bench.make_solver(hw, nt=nt)
 
 
-s = {"1": lambda: mc.cfg1(4), "2": cfg2, "3": mc.cfg3, "4": mc.cfg4, "5": mc.cfg5}[which]()
+s = {"1": lambda: mc.cfg1(2), "2": cfg2, "3": mc.cfg3, "4": mc.cfg4, "5": mc.cfg5}[which]()
 st = s.new_state()
 s.upload(st)
 v = hw.Variant.OP6 if which in ("4", "5") else hw.Variant.OP3
