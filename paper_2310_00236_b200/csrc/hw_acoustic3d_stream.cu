@@ -23,21 +23,6 @@ constexpr int AD = 3;      // prefetch distance (every datum of iteration i sits
 constexpr int A3T = 512;   // threads per CTA; TM = A3T * ECPT / nx rows of the mid axis
 constexpr int AOWN = 6;    // own-ring rows (in units of TM rows) per slot
 
-__device__ __forceinline__ int a3_wrap(int r, int n) { return r < 0 ? r + n : (r >= n ? r - n : r); }
-
-// TMA copy of mid rows [a, b) (periodic) of slab s into dst (row stride = pitch)
-__device__ __forceinline__ void a3_rows(__half* dst, const __half* fbase, int64_t slab, int64_t s, int a, int b,
-                                        int nm, int64_t pitch, uint64_t* bar) {
-    const __half* sb = fbase + s * slab;
-    for (int r = a; r < b;) {
-        const int rr = a3_wrap(r, nm);
-        const int seg = min(b - r, nm - rr);
-        tma_load_1d(dst, sb + (int64_t)rr * pitch, (uint32_t)(seg * pitch * sizeof(__half)), bar);
-        dst += (int64_t)seg * pitch;
-        r += seg;
-    }
-}
-
 struct A3Layout {
     uint64_t* bar;   // AR tap barriers
     uint64_t* obar;  // 2 own barriers
@@ -59,39 +44,6 @@ __device__ __forceinline__ void a3_init(const A3Layout& L) {
         fence_mbar_init();
     }
     __syncthreads();
-}
-
-// division by a binary16 divisor pair staged in shared memory (same three modes as finish())
-__device__ __forceinline__ EH2 a3_div(EH2 x, EH2 b, int mode) {
-    if (mode == DIV_CHEAP) {
-        const float r[2] = {__frcp_rn(__half2float(b.e[0])), __frcp_rn(__half2float(b.e[1]))};
-        return vdiv_cheap<2>(x, r);
-    }
-    if (mode == DIV_FAST) return EO2::div(x, b);
-    return EO2::div_ieee(x, b);
-}
-
-// finish() with the divisor values given (staged per-cell plane)
-template <int V>
-__device__ __forceinline__ void a3_finish(EH2 rhs, EH2 b, int mode, __half dt, int src_lane, double src, EH2& u,
-                                          EH2& t) {
-    EH2 xv = rhs;
-    if (src_lane >= 0 && src != 0.0) xv.e[src_lane] = lane<16>::add(xv.e[src_lane], lane<16>::from_f64(src));
-    xv = EO2::mul(a3_div(xv, b, mode), vsplat<16, 2>(dt));
-    if (V == 0) {
-        u = EO2::add(u, xv);
-        return;
-    }
-    const EH2 r = EO2::add(t, xv);
-    const EH2 sm = EO2::add(u, r);
-    if (V == 3) {
-        t = EO2::sub(r, EO2::sub(sm, u));
-    } else {
-        const EH2 pa = EO2::sub(sm, r);
-        const EH2 pb = EO2::sub(sm, pa);
-        t = EO2::add(EO2::sub(u, pa), EO2::sub(r, pb));
-    }
-    u = sm;
 }
 
 __device__ __forceinline__ bool a3_full(const PlaneView& v) { return v.sx != 0; }

@@ -364,6 +364,7 @@ struct hw_solver {
     // streaming phase kernels (2D elastic, binary16): in place on the standard layout
     bool el_stream = false;   // streaming 2D elastic phases
     bool ac3_stream = false;  // streaming 3D acoustic phases
+    bool el3_stream = false;  // streaming 3D elastic phases
     int stream_blocks = 0;
     unsigned int* counter = nullptr;  // CTA arrival counter of the streaming stress kernel
     // slab decomposition over the slow axis
@@ -695,7 +696,16 @@ int setup_handle(hw_solver* h) {
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
             h->ac3_stream = true;
         }
-        if (h->el_stream || h->ac3_stream || h->fused) {
+        if (want && !h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
+            el3d_stream_eligible(desc->nx, desc->nm, h->g.pitch, dev_smem)) {
+            if (el3d_stream_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "streaming kernel setup failed");
+            const int64_t units = (desc->nm / (2048 / desc->nx)) * max_rows;
+            int64_t nbs = units / 4;
+            if (nbs < 1) nbs = 1;
+            h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
+            h->el3_stream = true;
+        }
+        if (h->el_stream || h->ac3_stream || h->el3_stream || h->fused) {
             CU(cudaMalloc(&h->counter, sizeof(unsigned int)));
             CU(cudaMemset(h->counter, 0, sizeof(unsigned int)));
         }
@@ -1121,6 +1131,8 @@ static void run_phase(hw_solver* h, const RunCtx& C, int phase, int64_t n, const
     if (phase == 0) {
         if (h->ac3_stream) launch_ac3d_vel_stream(C.variant, h->d.order, C.A, h->stream_blocks, n, h->st);
         else if (h->ac) launch_ac_vel(h->LS, h->LU, h->W, C.A, n, h->max_rows, h->st);
+        else if (h->el3_stream)
+            launch_el3d_vel_stream(C.variant, h->d.order, C.L, h->stream_blocks, n, sk == HW_SRC_VSLOW ? s : 0.0, h->st);
         else if (h->el_stream) launch_el2d_vel_stream(C.variant, h->d.order, C.L, stream_io(h, C), h->stream_blocks, n,
                                                       sk == HW_SRC_VSLOW ? s : 0.0, h->st);
         else launch_el_vel(h->LS, h->LU, h->W, C.L, n, sk == HW_SRC_VSLOW ? s : 0.0, h->max_rows, h->st);
@@ -1129,6 +1141,9 @@ static void run_phase(hw_solver* h, const RunCtx& C, int phase, int64_t n, const
             launch_ac3d_pres_stream(C.variant, h->d.order, C.A, stream_io(h, C), h->stream_blocks, n,
                                     sk == HW_SRC_PRESSURE ? s : 0.0, sample, (n + 1) / C.every, h->st);
         else if (h->ac) launch_ac_pres(h->LS, h->LU, h->W, C.A, n, sk == HW_SRC_PRESSURE ? s : 0.0, sample, h->max_rows, h->st);
+        else if (h->el3_stream)
+            launch_el3d_stress_stream(C.variant, h->d.order, C.L, stream_io(h, C), h->stream_blocks, n,
+                                      sk == HW_SRC_EXPLOSIVE ? s : 0.0, sample, (n + 1) / C.every, h->st);
         else if (h->el_stream)
             launch_el2d_stress_stream(C.variant, h->d.order, C.L, stream_io(h, C), h->stream_blocks, n,
                                       sk == HW_SRC_EXPLOSIVE ? s : 0.0, sample, (n + 1) / C.every, h->st);
@@ -1140,6 +1155,13 @@ static void run_phase(hw_solver* h, const RunCtx& C, int phase, int64_t n, const
 static void run_epilogue(hw_solver* h, const RunCtx& C, int64_t n) {
     const int sample = C.energy && ((n + 1) % C.every == 0);
     if (h->el_stream || h->ac3_stream) return;  // traces and energy are recorded inside the streaming kernels
+    if (h->el3_stream) {  // energy is finalised inside; receiver traces from the epilogue
+        if (C.E.n_rec > 0) {
+            launch_epilogue(h->LU, C.E, n, 0, 0, h->st);
+            h->launches++;
+        }
+        return;
+    }
     if (sample || C.E.n_rec > 0) {
         launch_epilogue(h->LU, C.E, n, sample, (n + 1) / C.every, h->st);
         h->launches++;
@@ -1513,7 +1535,7 @@ int64_t hw_last_launch_count(const hw_solver* h) { return h ? h->launches : 0; }
 
 const char* hw_kernel_path(const hw_solver* h) {
     if (!h) return "";
-    return h->tb2 ? "fused2d-tb2" : h->fused ? "fused2d" : (h->el_stream ? "stream2d" : (h->ac3_stream ? "stream3d" : "generic"));
+    return h->tb2 ? "fused2d-tb2" : h->fused ? "fused2d" : (h->el_stream ? "stream2d" : ((h->ac3_stream || h->el3_stream) ? "stream3d" : "generic"));
 }
 
 int32_t hw_transport(const hw_solver* h) { return h ? h->transport : -1; }

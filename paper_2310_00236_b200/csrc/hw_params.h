@@ -99,6 +99,13 @@ cudaError_t ac3d_stream_prepare(int64_t nx);
 void launch_ac3d_vel_stream(int variant, int order, const AcParams& P, int nblocks, int64_t n, cudaStream_t st);
 void launch_ac3d_pres_stream(int variant, int order, const AcParams& P, const StreamIO& IO, int nblocks, int64_t n,
                              double src, int sample, int64_t eidx, cudaStream_t st);
+// streaming 3D elastic phase kernels (hw_elastic3d_stream.cu)
+bool el3d_stream_eligible(int64_t nx, int64_t nm, int64_t pitch, int max_smem);
+cudaError_t el3d_stream_prepare(int64_t nx);
+void launch_el3d_vel_stream(int variant, int order, const ElParams& P, int nblocks, int64_t n, double src,
+                            cudaStream_t st);
+void launch_el3d_stress_stream(int variant, int order, const ElParams& P, const StreamIO& IO, int nblocks, int64_t n,
+                               double src, int sample, int64_t eidx, cudaStream_t st);
 void launch_epilogue(int LU, const EpParams& E, int64_t n, int sample, int64_t eidx, cudaStream_t st);
 
 }  // namespace hw
