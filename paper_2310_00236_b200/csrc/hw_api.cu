@@ -796,16 +796,19 @@ struct Xfer {
     size_t bytes;
 };
 
+// Ghost rows the phase kernels read across a slab edge: the slow-axis stencil reach
+// (1 row at 2nd order, 2 at 4th), not the full G-deep ghost slabs.
 std::vector<Xfer> xfers(const hw_solver* h, int phase) {
     std::vector<Xfer> out;
     const size_t esz = lane_bytes(h->LU);
+    const int64_t depth = h->d.order == 2 ? 1 : 2;
     for (int j = 0; j < h->nsol; j++) {
         const int f = h->ext[j];
         if (!needs_ghosts(h, f) || is_velocity(f) != (phase == 0)) continue;
         const FieldView& fv = h->fv[f];
         const size_t row = (size_t)h->g.slab * esz;
         char* b = (char*)fv.base;
-        out.push_back(Xfer{b + (fv.rows - G) * row, b, b - G * row, b + fv.rows * row, G * row});
+        out.push_back(Xfer{b + (fv.rows - depth) * row, b, b - depth * row, b + fv.rows * row, depth * row});
     }
     return out;
 }
