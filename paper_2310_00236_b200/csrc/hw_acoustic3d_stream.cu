@@ -352,15 +352,8 @@ __global__ void __launch_bounds__(A3T, 1)
     if (tid == 0) is_last = atomicAdd(IO.counter, 1u) == (unsigned int)(gridDim.x - 1);
     __syncthreads();
     if (!is_last) return;
-    if (tid == 0) {  // fixed-order fp64 reduction of the block partials
-        double tot[NCOMP];
-        for (int k = 0; k < NCOMP; k++) {
-            double a = 0.0;
-            for (int bi = 0; bi < (int)gridDim.x; bi++) a += __ldcg(&P.partials[(int64_t)bi * NCOMP + k]);
-            tot[k] = a;
-        }
-        double t = tot[0];
-        for (int k = 1; k < NCOMP; k++) t += tot[k];
+    const double t = finalize_partials(P.partials, (int)gridDim.x);  // fixed-order fp64 reduction
+    if (tid == 0) {
         IO.e_vals[eidx] = IO.scale * t;
         *IO.counter = 0u;
     }

@@ -416,6 +416,25 @@ __device__ __forceinline__ void block_partials(double v[NCOMP], double* out, int
     }
 }
 
+// Last-CTA energy finalisation: warp w sums components w, w + nwarps, ... of the nb
+// block partials (fixed lane-strided order + fixed shuffle tree: deterministic), thread 0
+// combines the components left to right.  Any block size >= 32; total on thread 0.
+__device__ __forceinline__ double finalize_partials(const double* part, int nb) {
+    __shared__ double tot[NCOMP];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (int)(blockDim.x >> 5);
+    for (int c = w; c < NCOMP; c += nw) {
+        double a = 0.0;
+        for (int bi = lane; bi < nb; bi += 32) a += __ldcg(&part[(int64_t)bi * NCOMP + c]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+        if (lane == 0) tot[c] = a;
+    }
+    __syncthreads();
+    double t = tot[0];
+    for (int c = 1; c < NCOMP; c++) t += tot[c];
+    return t;
+}
+
 // Launch shape of the phase kernels: x vectors across blockIdx.x (one row segment
 // per block), mid index on blockIdx.y, slow index on blockIdx.z, so (s, m) stay
 // warp-uniform (uniform datapath for row addressing); no integer division.

@@ -420,15 +420,8 @@ __global__ void __launch_bounds__(512, 1)
     if (tid == 0) is_last = atomicAdd(IO.counter, 1u) == (unsigned int)(nb - 1);
     __syncthreads();
     if (!is_last) return;
-    if (tid == 0) {  // fixed-order fp64 reduction of the block partials (diagnostics.py:100-162)
-        double tot[NCOMP];
-        for (int q = 0; q < NCOMP; q++) {
-            double a = 0.0;
-            for (int bi = 0; bi < nb; bi++) a += __ldcg(&P.partials[(int64_t)bi * NCOMP + q]);
-            tot[q] = a;
-        }
-        double t = tot[0];
-        for (int q = 1; q < NCOMP; q++) t += tot[q];
+    const double t = finalize_partials(P.partials, nb);  // fixed-order fp64 reduction
+    if (tid == 0) {
         IO.e_vals[eidx] = IO.scale * t;
         *IO.counter = 0u;
     }

@@ -455,22 +455,13 @@ __global__ void __launch_bounds__(288, 1)
     if (tid == 0) is_last = atomicAdd(P.counter, 1u) == (unsigned int)(gridDim.x - 1);
     __syncthreads();
     if (!is_last) return;
-    if (tid == 0) {  // fixed-order fp64 reduction of the block partials
-        for (int st = 0; st < 2; st++) {
-            if (!(st == 0 ? sampleA : sampleB)) continue;
-            const double* part = st == 0 ? P.partials : T.partials_b;
-            double tot[NCOMP];
-            for (int k = 0; k < NCOMP; k++) {
-                double a = 0.0;
-                for (int bi = 0; bi < (int)gridDim.x; bi++) a += __ldcg(&part[(int64_t)bi * NCOMP + k]);
-                tot[k] = a;
-            }
-            double t = tot[0];
-            for (int k = 1; k < NCOMP; k++) t += tot[k];
-            P.e_vals[st == 0 ? eidxA : eidxB] = P.scale * t;
-        }
-        *P.counter = 0u;
+    for (int st = 0; st < 2; st++) {  // fixed-order fp64 reduction of each stage's block partials
+        if (!(st == 0 ? sampleA : sampleB)) continue;
+        const double t = finalize_partials(st == 0 ? P.partials : T.partials_b, (int)gridDim.x);
+        if (tid == 0) P.e_vals[st == 0 ? eidxA : eidxB] = P.scale * t;
+        __syncthreads();
     }
+    if (tid == 0) *P.counter = 0u;
 }
 
 // ---------------------------------------------------------------- host side
