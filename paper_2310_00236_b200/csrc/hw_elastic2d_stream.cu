@@ -55,7 +55,9 @@ __device__ __forceinline__ void e_init_ring(const ERing& R) {
 //   stream 1: sxy[F-1]    -> queue xsq (rows r-2..r+1); its x taps for vy[r] (= row F-2)
 //                            come from the previous slot's stream 1
 //   stream 2: sxx[F-2]    -> x taps for vx[r]
-template <int V, int ORDER>
+// RM: row-uniform media (rho divisors DIV_CHEAP with per-row reciprocals; stiff / lam /
+// mu row-uniform): coefficients loaded once per row instead of per pair.
+template <int V, int ORDER, bool RM>
 __global__ void __launch_bounds__(512, 1) k_el2d_vel_stream(ElParams P, StreamIO IO, int64_t n, double src) {
     e_pdl_enter();
     if (halted(P.ctrl, n)) return;
@@ -100,6 +102,8 @@ __global__ void __launch_bounds__(512, 1) k_el2d_vel_stream(ElParams P, StreamIO
     const __half dt = lconst<16>(P.k, 4);
     const int xl = x == 0 ? nx - 2 : x - 2, xr = x + ECPT >= nx ? 0 : x + ECPT;
     const bool src_here = P.src_kind == HW_SRC_VSLOW && src != 0.0 && P.src_x >= x && P.src_x < x + ECPT;
+    const __half2 dt2 = __half2half2(dt);
+    const __half srch = __double2half(src);
     E8 ssq[4], xsq[4];  // slow-tap queues, [3] = newest row
     int rcur = rec_lower(IO.rec, 0, IO.n_rec, y0, INT_MIN);  // this CTA's receivers [rcur, rhi)
     const int rhi = rec_lower(IO.rec, rcur, IO.n_rec, y1, INT_MIN);
@@ -135,9 +139,17 @@ __global__ void __launch_bounds__(512, 1) k_el2d_vel_stream(ElParams P, StreamIO
                         const E8 d = e_sfold<ORDER>(c, xsq[0], xsq[1], xsq[2], xsq[3]);
                         E8 v = e_ld8(R.orow(kr & 1, 0) + x);
                         E8 rr = comp ? e_ld8(R.orow(kr & 1, 2) + x) : E8{};
+                        if constexpr (RM) {
+                            const float rc = __ldg(P.rho_x.rcp + r * P.rho_x.ss);
 #pragma unroll
-                        for (int j = 0; j < 4; j++)
-                            finish<16, 16, 2>(EO2::add(a.q[j], d.q[j]), &P.rho_x, r, 0, x + 2 * j, dt, V, -1, 0.0, v.q[j], rr.q[j]);
+                            for (int j = 0; j < 4; j++)
+                                e_finish_rc<V>(EO2::add(a.q[j], d.q[j]), rc, dt2, -1, srch, v.q[j], rr.q[j]);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 4; j++)
+                                finish<16, 16, 2>(EO2::add(a.q[j], d.q[j]), &P.rho_x, r, 0, x + 2 * j, dt, V, -1, 0.0,
+                                                  v.q[j], rr.q[j]);
+                        }
                         e_store_row(P.vx, pitch, r, x, v);
                         e_track(acc[0], v);
                         if (comp) {
@@ -153,10 +165,18 @@ __global__ void __launch_bounds__(512, 1) k_el2d_vel_stream(ElParams P, StreamIO
                         const int sj = (int)((P.src_x - x) >> 1), sl = (int)((P.src_x - x) & 1);
                         E8 v = e_ld8(R.orow(kr & 1, 1) + x);
                         E8 rr = comp ? e_ld8(R.orow(kr & 1, 3) + x) : E8{};
+                        if constexpr (RM) {
+                            const float rc = __ldg(P.rho_s.rcp + r * P.rho_s.ss);
 #pragma unroll
-                        for (int j = 0; j < 4; j++)
-                            finish<16, 16, 2>(EO2::add(a.q[j], d.q[j]), &P.rho_s, r, 0, x + 2 * j, dt, V,
-                                              (sk && j == sj) ? sl : -1, src, v.q[j], rr.q[j]);
+                            for (int j = 0; j < 4; j++)
+                                e_finish_rc<V>(EO2::add(a.q[j], d.q[j]), rc, dt2, (sk && j == sj) ? sl : -1, srch,
+                                               v.q[j], rr.q[j]);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 4; j++)
+                                finish<16, 16, 2>(EO2::add(a.q[j], d.q[j]), &P.rho_s, r, 0, x + 2 * j, dt, V,
+                                                  (sk && j == sj) ? sl : -1, src, v.q[j], rr.q[j]);
+                        }
                         e_store_row(P.vs, pitch, r, x, v);
                         e_track(acc[1], v);
                         // receiver traces of vy after the step (elastic.py:283-284)
@@ -187,7 +207,7 @@ __global__ void __launch_bounds__(512, 1) k_el2d_vel_stream(ElParams P, StreamIO
 //   stream 1: vy[F-1]  -> queue vyq (rows r-2..r+1, to-int taps of dvy); its x taps for
 //                         sxy[r] (= row F-2) come from the previous slot's stream 1
 //   stream 2: vx[F-2]  -> x taps of dvx at row r
-template <int V, int ORDER>
+template <int V, int ORDER, bool RM>
 __global__ void __launch_bounds__(512, 1)
     k_el2d_stress_stream(ElParams P, StreamIO IO, int64_t n, double src, int sample, int64_t eidx) {
     e_pdl_enter();
@@ -278,10 +298,15 @@ __global__ void __launch_bounds__(512, 1)
                         E8 sxx = sxx_old, sss = sss_old;
                         E8 rsxx = comp ? e_ld8(R.orow(kr & 1, 3) + x) : E8{};
                         E8 rsss = comp ? e_ld8(R.orow(kr & 1, 4) + x) : E8{};
+                        EH2 stiff_r, lam_r;
+                        if constexpr (RM) {
+                            stiff_r = e_rowval(P.stiff, r);
+                            lam_r = e_rowval(P.lam, r);
+                        }
 #pragma unroll
                         for (int j = 0; j < 4; j++) {
-                            const EH2 stiff = pload<16, 2>(P.stiff, r, 0, x + 2 * j);
-                            const EH2 lam = pload<16, 2>(P.lam, r, 0, x + 2 * j);
+                            const EH2 stiff = RM ? stiff_r : pload<16, 2>(P.stiff, r, 0, x + 2 * j);
+                            const EH2 lam = RM ? lam_r : pload<16, 2>(P.lam, r, 0, x + 2 * j);
                             EH2 a1, a2;
                             if (surf) {  // plane-stress surface row; syy takes a zero increment (elastic.py:215-230)
                                 a1 = EO2::mul(pload<16, 2>(P.ep, sg == 0 ? 0 : 1, 0, x + 2 * j), dvx.q[j]);
@@ -359,9 +384,11 @@ __global__ void __launch_bounds__(512, 1)
                         const E8 old = e_ld8(R.orow(kr & 1, 2) + x);
                         E8 s = old;
                         E8 rs = comp ? e_ld8(R.orow(kr & 1, 5) + x) : E8{};
+                        EH2 mu_r;
+                        if constexpr (RM) mu_r = e_rowval(P.mu_n, r);
 #pragma unroll
                         for (int j = 0; j < 4; j++) {
-                            const EH2 mu = pload<16, 2>(P.mu_n, r, 0, x + 2 * j);
+                            const EH2 mu = RM ? mu_r : pload<16, 2>(P.mu_n, r, 0, x + 2 * j);
                             finish<16, 16, 2>(EO2::mul(mu, EO2::add(dvxy.q[j], dvyx.q[j])), nullptr, r, 0, x, dt, V, -1,
                                               0.0, s.q[j], rs.q[j]);
                         }
@@ -437,8 +464,16 @@ bool el2d_stream_eligible(int64_t nx, int max_smem) {
 
 template <int V, int O>
 static void el2d_attrs(int bytes) {
-    cudaFuncSetAttribute((void*)k_el2d_vel_stream<V, O>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    cudaFuncSetAttribute((void*)k_el2d_stress_stream<V, O>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute((void*)k_el2d_vel_stream<V, O, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute((void*)k_el2d_stress_stream<V, O, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute((void*)k_el2d_vel_stream<V, O, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute((void*)k_el2d_stress_stream<V, O, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+static bool el2d_rowmed(const ElParams& P) {
+    auto div = [](const PlaneView& v) { return v.div_mode == DIV_CHEAP && v.sx == 0 && v.sm == 0; };
+    auto row = [](const PlaneView& v) { return v.sx == 0 && v.sm == 0; };
+    return div(P.rho_x) && div(P.rho_s) && row(P.stiff) && row(P.lam) && row(P.mu_n);
 }
 
 cudaError_t el2d_stream_prepare(int64_t nx) {
@@ -476,7 +511,11 @@ static void launch_pdl(void* fn, int nblocks, int64_t nx, cudaStream_t st, void*
 void launch_el2d_vel_stream(int variant, int order, const ElParams& P, const StreamIO& IO, int nblocks, int64_t n,
                             double src, cudaStream_t st) {
     void* fn = nullptr;
-    EL2D_DISPATCH(variant, order, (fn = (void*)k_el2d_vel_stream<V_, O_>))
+    if (el2d_rowmed(P)) {
+        EL2D_DISPATCH(variant, order, (fn = (void*)k_el2d_vel_stream<V_, O_, true>))
+    } else {
+        EL2D_DISPATCH(variant, order, (fn = (void*)k_el2d_vel_stream<V_, O_, false>))
+    }
     void* args[] = {(void*)&P, (void*)&IO, (void*)&n, (void*)&src};
     launch_pdl(fn, nblocks, P.g.nx, st, args);
 }
@@ -484,7 +523,11 @@ void launch_el2d_vel_stream(int variant, int order, const ElParams& P, const Str
 void launch_el2d_stress_stream(int variant, int order, const ElParams& P, const StreamIO& IO, int nblocks, int64_t n,
                                double src, int sample, int64_t eidx, cudaStream_t st) {
     void* fn = nullptr;
-    EL2D_DISPATCH(variant, order, (fn = (void*)k_el2d_stress_stream<V_, O_>))
+    if (el2d_rowmed(P)) {
+        EL2D_DISPATCH(variant, order, (fn = (void*)k_el2d_stress_stream<V_, O_, true>))
+    } else {
+        EL2D_DISPATCH(variant, order, (fn = (void*)k_el2d_stress_stream<V_, O_, false>))
+    }
     void* args[] = {(void*)&P, (void*)&IO, (void*)&n, (void*)&src, (void*)&sample, (void*)&eidx};
     launch_pdl(fn, nblocks, P.g.nx, st, args);
 }

@@ -136,6 +136,38 @@ __device__ __forceinline__ double e_pick(const E8& v, int o) {  // register sele
     return r;
 }
 
+// increment + advance for one pair, division by a row-uniform divisor through its
+// verified reciprocal (DIV_CHEAP): the same ops as finish() (stepping.py:58-98,
+// efsum.py:100-121), without the per-pair plane load and mode dispatch
+template <int V>
+__device__ __forceinline__ void e_finish_rc(EH2 rhs, float rc, __half2 dt2, int src_lane, __half srch, EH2& u,
+                                            EH2& t) {
+    if (src_lane == 0) rhs.e[0] = __hadd_rn(rhs.e[0], srch);
+    else if (src_lane == 1) rhs.e[1] = __hadd_rn(rhs.e[1], srch);
+    const float2 fx = __half22float2(rhs.h2);
+    EH2 x;
+    x.h2 = __hmul2_rn(__floats2half2_rn(__fmul_rn(fx.x, rc), __fmul_rn(fx.y, rc)), dt2);
+    if (V == 0) {
+        u.h2 = __hadd2_rn(u.h2, x.h2);
+        return;
+    }
+    const __half2 r = __hadd2_rn(t.h2, x.h2);
+    const __half2 s = __hadd2_rn(u.h2, r);
+    if (V == 3) {
+        t.h2 = __hsub2_rn(r, __hsub2_rn(s, u.h2));
+    } else {
+        const __half2 pa = __hsub2_rn(s, r);
+        const __half2 pb = __hsub2_rn(s, pa);
+        t.h2 = __hadd2_rn(__hsub2_rn(u.h2, pa), __hsub2_rn(r, pb));
+    }
+    u.h2 = s;
+}
+
+// row-uniform binary16 plane value at slow row r (plane strides (ss, 0, 0))
+__device__ __forceinline__ EH2 e_rowval(const PlaneView& pv, int64_t r) {
+    return vsplat<16, 2>(__ldg(reinterpret_cast<const __half*>(pv.p) + r * pv.ss));
+}
+
 // ---- mid-axis tiles (3D streaming kernels)
 __device__ __forceinline__ int a3_wrap(int r, int n) { return r < 0 ? r + n : (r >= n ? r - n : r); }
 
