@@ -74,6 +74,10 @@ __global__ void __launch_bounds__(A3T, 1) k_ac3d_vel_stream(AcParams P, int64_t 
     for (int q = 0; q < 4; q++) c[q] = lconst<16>(P.k, q);
     const __half dt = lconst<16>(P.k, 4);
     const int xl = x == 0 ? nx - 2 : x - 2, xr = x + ECPT >= nx ? 0 : x + ECPT;
+    // divisors constant along x: one reciprocal per (slab, row) instead of a plane load per pair
+    const bool rm = e_rowdiv(P.rho_x) && e_rowdiv(P.rho_s) && e_rowdiv(P.rho_m);
+    const __half2 dt2 = __half2half2(dt);
+    const __half zero_h = __float2half(0.f);
     __half2 acc[6];
 #pragma unroll
     for (int q = 0; q < 6; q++) acc[q] = __float2half2_rn(0.f);
@@ -135,9 +139,15 @@ __global__ void __launch_bounds__(A3T, 1) k_ac3d_vel_stream(AcParams P, int64_t 
                     const E8 a = e_xfold<ORDER>(c, tile_row, x, xl, xr, false);
                     E8 v = e_ld8(L.orow(os, 0) + ro);
                     E8 rr = comp ? e_ld8(L.orow(os, 3) + ro) : E8{};
+                    if (rm) {
+                        const float rc = e_rcp_at(P.rho_x, s, m);
 #pragma unroll
-                    for (int h = 0; h < 4; h++)
-                        finish<16, 16, 2>(a.q[h], &P.rho_x, s, m, x + 2 * h, dt, V, -1, 0.0, v.q[h], rr.q[h]);
+                        for (int h = 0; h < 4; h++) e_finish_rc<V>(a.q[h], rc, dt2, -1, zero_h, v.q[h], rr.q[h]);
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < 4; h++)
+                            finish<16, 16, 2>(a.q[h], &P.rho_x, s, m, x + 2 * h, dt, V, -1, 0.0, v.q[h], rr.q[h]);
+                    }
                     e_store_row(P.vx, slab, s, (int)off, v);
                     e_track(acc[0], v);
                     if (comp) {
@@ -150,9 +160,15 @@ __global__ void __launch_bounds__(A3T, 1) k_ac3d_vel_stream(AcParams P, int64_t 
                     const E8 a = e_sfold<ORDER>(c, q[0], q[1], q[2], q[3]);
                     E8 v = e_ld8(L.orow(os, 1) + ro);
                     E8 rr = comp ? e_ld8(L.orow(os, 4) + ro) : E8{};
+                    if (rm) {
+                        const float rc = e_rcp_at(P.rho_s, s, m);
 #pragma unroll
-                    for (int h = 0; h < 4; h++)
-                        finish<16, 16, 2>(a.q[h], &P.rho_s, s, m, x + 2 * h, dt, V, -1, 0.0, v.q[h], rr.q[h]);
+                        for (int h = 0; h < 4; h++) e_finish_rc<V>(a.q[h], rc, dt2, -1, zero_h, v.q[h], rr.q[h]);
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < 4; h++)
+                            finish<16, 16, 2>(a.q[h], &P.rho_s, s, m, x + 2 * h, dt, V, -1, 0.0, v.q[h], rr.q[h]);
+                    }
                     e_store_row(P.vs, slab, s, (int)off, v);
                     e_track(acc[1], v);
                     if (comp) {
@@ -167,9 +183,15 @@ __global__ void __launch_bounds__(A3T, 1) k_ac3d_vel_stream(AcParams P, int64_t 
                                                 e_ld8(t0 + 3 * pitch));
                     E8 v = e_ld8(L.orow(os, 2) + ro);
                     E8 rr = comp ? e_ld8(L.orow(os, 5) + ro) : E8{};
+                    if (rm) {
+                        const float rc = e_rcp_at(P.rho_m, s, m);
 #pragma unroll
-                    for (int h = 0; h < 4; h++)
-                        finish<16, 16, 2>(a.q[h], &P.rho_m, s, m, x + 2 * h, dt, V, -1, 0.0, v.q[h], rr.q[h]);
+                        for (int h = 0; h < 4; h++) e_finish_rc<V>(a.q[h], rc, dt2, -1, zero_h, v.q[h], rr.q[h]);
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < 4; h++)
+                            finish<16, 16, 2>(a.q[h], &P.rho_m, s, m, x + 2 * h, dt, V, -1, 0.0, v.q[h], rr.q[h]);
+                    }
                     e_store_row(P.vm, slab, s, (int)off, v);
                     e_track(acc[2], v);
                     if (comp) {
@@ -212,6 +234,9 @@ __global__ void __launch_bounds__(A3T, 1)
     const int tid = threadIdx.x, j = tid / TPR, x = (tid % TPR) * ECPT;
     constexpr bool comp = V != 0;
     const bool bfull = a3_full(P.beta);
+    const bool brow = !bfull && e_rowdiv(P.beta);
+    const __half2 dt2 = __half2half2(lconst<16>(P.k, 4));
+    const __half srch = __double2half(src);
     const int NOWN = 1 + (comp ? 1 : 0) + (bfull ? 1 : 0);  // p [rp] [beta]
     const __half* VS = reinterpret_cast<const __half*>(P.vs.base);
     const __half* VX = reinterpret_cast<const __half*>(P.vx.base);
@@ -303,6 +328,12 @@ __global__ void __launch_bounds__(A3T, 1)
                     for (int h = 0; h < 4; h++)
                         a3_finish<V>(EO2::add(EO2::add(tx.q[h], ts.q[h]), tm.q[h]), bv.q[h], P.beta.div_mode, dt,
                                      (sk && h == sj) ? sln : -1, src, pn.q[h], rr.q[h]);
+                } else if (brow) {
+                    const float rc = e_rcp_at(P.beta, s, m);
+#pragma unroll
+                    for (int h = 0; h < 4; h++)
+                        e_finish_rc<V>(EO2::add(EO2::add(tx.q[h], ts.q[h]), tm.q[h]), rc, dt2, (sk && h == sj) ? sln : -1,
+                                       srch, pn.q[h], rr.q[h]);
                 } else {
 #pragma unroll
                     for (int h = 0; h < 4; h++)

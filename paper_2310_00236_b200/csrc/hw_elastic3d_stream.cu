@@ -102,6 +102,9 @@ __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t 
     const __half dt = lconst<16>(P.k, 4);
     const int xl = x == 0 ? nx - 2 : x - 2, xr = x + ECPT >= nx ? 0 : x + ECPT;
     const bool src_col = P.src_kind == HW_SRC_VSLOW && src != 0.0 && P.src_x >= x && P.src_x < x + ECPT;
+    const bool rm = e_rowdiv(P.rho_x) && e_rowdiv(P.rho_s) && e_rowdiv(P.rho_m);  // one reciprocal per row
+    const __half2 dt2 = __half2half2(dt);
+    const __half srch = __double2half(src);
     const int sj = (int)((P.src_x - x) >> 1), sln = (int)((P.src_x - x) & 1);
     __half2 acc[6];
 #pragma unroll
@@ -176,25 +179,44 @@ __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t 
                 E8 a = e_xfold<ORDER>(c, d + o_sxx * pitch + jr, x, xl, xr, false);
                 a = e3_add(a, e_sfold<ORDER>(c, qxs[0], qxs[1], qxs[2], qxs[3]));
                 a = e3_add(a, e3_mfold<ORDER>(c, d + o_sxm * pitch + jr + x, pitch));
+                if (rm) {
+                    const float rc = e_rcp_at(P.rho_x, s, m);
 #pragma unroll
-                for (int h = 0; h < 4; h++)
-                    finish<16, 16, 2>(a.q[h], &P.rho_x, s, m, x + 2 * h, dt, V, -1, 0.0, v[0].q[h], rr[0].q[h]);
+                    for (int h = 0; h < 4; h++) e_finish_rc<V>(a.q[h], rc, dt2, -1, srch, v[0].q[h], rr[0].q[h]);
+                } else {
+#pragma unroll
+                    for (int h = 0; h < 4; h++)
+                        finish<16, 16, 2>(a.q[h], &P.rho_x, s, m, x + 2 * h, dt, V, -1, 0.0, v[0].q[h], rr[0].q[h]);
+                }
                 // v_slow: fl(fl(ddx sxs + dds sss) + ddm sms) (+ src) (elastic.py:196-205)
                 a = e_xfold<ORDER>(c, pd + o_sxs * pitch + jr, x, xl, xr, true);
                 a = e3_add(a, e_sfold<ORDER>(c, qss[0], qss[1], qss[2], qss[3]));
                 a = e3_add(a, e3_mfold<ORDER>(c, pd + o_sms * pitch + jr + x, pitch));
                 const bool sk = src_col && s == P.src_s && m == P.src_m;
+                if (rm) {
+                    const float rc = e_rcp_at(P.rho_s, s, m);
 #pragma unroll
-                for (int h = 0; h < 4; h++)
-                    finish<16, 16, 2>(a.q[h], &P.rho_s, s, m, x + 2 * h, dt, V, (sk && h == sj) ? sln : -1, src,
-                                      v[1].q[h], rr[1].q[h]);
+                    for (int h = 0; h < 4; h++)
+                        e_finish_rc<V>(a.q[h], rc, dt2, (sk && h == sj) ? sln : -1, srch, v[1].q[h], rr[1].q[h]);
+                } else {
+#pragma unroll
+                    for (int h = 0; h < 4; h++)
+                        finish<16, 16, 2>(a.q[h], &P.rho_s, s, m, x + 2 * h, dt, V, (sk && h == sj) ? sln : -1, src,
+                                          v[1].q[h], rr[1].q[h]);
+                }
                 // v_mid: fl(fl(ddx sxm + dds sms) + ddm smm)
                 a = e_xfold<ORDER>(c, d + o_sxm * pitch + jr + 2 * pitch, x, xl, xr, true);
                 a = e3_add(a, e_sfold<ORDER>(c, qms[0], qms[1], qms[2], qms[3]));
                 a = e3_add(a, e3_mfold<ORDER>(c, d + o_smm * pitch + jr + pitch + x, pitch));
+                if (rm) {
+                    const float rc = e_rcp_at(P.rho_m, s, m);
 #pragma unroll
-                for (int h = 0; h < 4; h++)
-                    finish<16, 16, 2>(a.q[h], &P.rho_m, s, m, x + 2 * h, dt, V, -1, 0.0, v[2].q[h], rr[2].q[h]);
+                    for (int h = 0; h < 4; h++) e_finish_rc<V>(a.q[h], rc, dt2, -1, srch, v[2].q[h], rr[2].q[h]);
+                } else {
+#pragma unroll
+                    for (int h = 0; h < 4; h++)
+                        finish<16, 16, 2>(a.q[h], &P.rho_m, s, m, x + 2 * h, dt, V, -1, 0.0, v[2].q[h], rr[2].q[h]);
+                }
 #pragma unroll
                 for (int q = 0; q < 3; q++) {
                     e_store_row(*OF[q], slab, s, (int)off, v[q]);
@@ -248,6 +270,7 @@ __global__ void __launch_bounds__(E3T, 1)
     const __half dt = lconst<16>(P.k, 4);
     const int xl = x == 0 ? nx - 2 : x - 2, xr = x + ECPT >= nx ? 0 : x + ECPT;
     const bool src_col = P.src_kind == HW_SRC_EXPLOSIVE && src != 0.0 && P.src_x >= x && P.src_x < x + ECPT;
+    const bool mrow = P.stiff.sx == 0 && P.lam.sx == 0 && P.mu_n.sx == 0;
     const int sj = (int)((P.src_x - x) >> 1), sln = (int)((P.src_x - x) & 1);
     // energy planes constant within a slab (layered along the slow axis): per-slab sums
     const bool erow = ((P.e_rho_x.sx | P.e_rho_s.sx | P.e_rho_m.sx | P.e_lam.sx | P.e_mu.sx | P.e_mu_n.sx) |
@@ -330,10 +353,16 @@ __global__ void __launch_bounds__(E3T, 1)
                     rr[q] = comp ? e_ld8(L.orow(os, 6 + q) + ro) : E8{};
                 }
                 const bool sk = src_col && s == P.src_s && m == P.src_m;
+                EH2 stiff_r, lam_r, mu_r;  // moduli constant along x: one load per row
+                if (mrow) {
+                    stiff_r = e_val_at(P.stiff, s, m);
+                    lam_r = e_val_at(P.lam, s, m);
+                    mu_r = e_val_at(P.mu_n, s, m);
+                }
 #pragma unroll
                 for (int h = 0; h < 4; h++) {
-                    const EH2 stiff = pload<16, 2>(P.stiff, s, m, x + 2 * h);
-                    const EH2 lam = pload<16, 2>(P.lam, s, m, x + 2 * h);
+                    const EH2 stiff = mrow ? stiff_r : pload<16, 2>(P.stiff, s, m, x + 2 * h);
+                    const EH2 lam = mrow ? lam_r : pload<16, 2>(P.lam, s, m, x + 2 * h);
                     const int lsrc = (sk && h == sj) ? sln : -1;
                     // sxx: fl(fl(fl(stiff dvx) + fl(lam dvs)) + fl(lam dvm)); s_slow / s_mid likewise
                     const EH2 a0 = EO2::add(EO2::add(EO2::mul(stiff, dvx.q[h]), EO2::mul(lam, dvs.q[h])),
@@ -355,7 +384,7 @@ __global__ void __launch_bounds__(E3T, 1)
                 const E8 sms_b = e3_mfold<ORDER>(c, vst + pitch + x, pitch);
 #pragma unroll
                 for (int h = 0; h < 4; h++) {
-                    const EH2 mu = pload<16, 2>(P.mu_n, s, m, x + 2 * h);
+                    const EH2 mu = mrow ? mu_r : pload<16, 2>(P.mu_n, s, m, x + 2 * h);
                     finish<16, 16, 2>(EO2::mul(mu, EO2::add(sxs_a.q[h], sxs_b.q[h])), nullptr, s, m, x, dt, V, -1, 0.0,
                                       nw[3].q[h], rr[3].q[h]);
                     finish<16, 16, 2>(EO2::mul(mu, EO2::add(sxm_a.q[h], sxm_b.q[h])), nullptr, s, m, x, dt, V, -1, 0.0,

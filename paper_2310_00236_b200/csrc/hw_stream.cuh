@@ -163,6 +163,15 @@ __device__ __forceinline__ void e_finish_rc(EH2 rhs, float rc, __half2 dt2, int 
     u.h2 = s;
 }
 
+// planes constant along x (constant, slow-layered, or per (slow, mid) row in 3D)
+__device__ __forceinline__ bool e_rowdiv(const PlaneView& v) { return v.div_mode == DIV_CHEAP && v.sx == 0; }
+__device__ __forceinline__ float e_rcp_at(const PlaneView& v, int64_t s, int64_t m) {
+    return __ldg(v.rcp + s * v.ss + m * v.sm);
+}
+__device__ __forceinline__ EH2 e_val_at(const PlaneView& v, int64_t s, int64_t m) {
+    return vsplat<16, 2>(__ldg(reinterpret_cast<const __half*>(v.p) + s * v.ss + m * v.sm));
+}
+
 // row-uniform binary16 plane value at slow row r (plane strides (ss, 0, 0))
 __device__ __forceinline__ EH2 e_rowval(const PlaneView& pv, int64_t r) {
     return vsplat<16, 2>(__ldg(reinterpret_cast<const __half*>(pv.p) + r * pv.ss));
