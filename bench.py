@@ -270,14 +270,14 @@ def main():
     peak, peak_src = peak_hbm()
     per_leap_ms = ms_total / (args.steps * args.nt)
     achieved = B_ALG * cells / (per_leap_ms / 1e3) / 1e9
-    traffic = None
+    traffic, traffic_src = None, None
     tf = ROOT / "profiles" / "traffic.json"  # dram bytes per launch from the committed ncu --set full capture
     if tf.exists():
         tj = json.loads(tf.read_text())
-        traffic = {"bytes_per_launch": tj["dram_bytes_per_launch"], "source": tj["source"],
-                   "bytes_per_cell_step": tj["dram_bytes_per_launch"] / cells}
+        traffic, traffic_src = float(tj["dram_bytes_per_launch"]), tj["source"]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_source": peak_src,
+                "traffic": traffic, "traffic_source": traffic_src,
+                "traffic_bytes_per_cell_step": traffic / cells if traffic else None, "peak_source": peak_src,
                 "algorithmic_bytes_per_cell_step": B_ALG,
                 "kernel": "k_ac2d_fused (one launch per leapfrog step of 4096^2 cells); achieved uses the "
                           "CUDA-event time of the whole step loop (launch gaps included)"}
