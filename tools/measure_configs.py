@@ -1,5 +1,7 @@
 """Device-resident throughput of the BASELINE configs on one GPU (short runs):
-python tools/measure_configs.py [nt] -> one JSON line per config."""
+python tools/measure_configs.py [nt] [configs] [--cpu] -> one JSON line per config.
+--cpu adds the CPU oracle port (oracle/halfwave_oracle.c, all host threads) on a bounded
+sample of the same config (steady state: setup timed with nt = 0 and subtracted)."""
 import json
 import sys
 from pathlib import Path
@@ -11,19 +13,44 @@ sys.path.insert(0, str(ROOT))
 
 import paper_2310_00236_b200 as hw  # noqa: E402
 
-NT = int(sys.argv[1]) if len(sys.argv) > 1 else 50
+CPU = "--cpu" in sys.argv
+ARGS = [a for a in sys.argv[1:] if a != "--cpu"]
+NT = int(ARGS[0]) if len(ARGS) > 0 else 50
 F16 = hw.Precision.FP16
 
 
-def timed(name, s, variant, bytes_per_cell, cells, nt=NT):
+def cpu_rate(s, variant, cells, steps):
+    """The oracle port on `steps` steps of the same solver description (the mirrored
+    domain for rigid walls: the cells it advances are what the device advances)."""
+    import os
+
+    import oracle
+    from paper_2310_00236_b200.efsum import variant_code
+
+    st = s.new_state()
+    arrays = [np.ascontiguousarray(s._to_device(n, getattr(st, n).values), dtype=np.float64) for n in s.FIELDS]
+    v = variant_code(variant)
+    cores = os.cpu_count() or 1
+    t0 = oracle.timed_steps(s.desc, arrays, v, 0, 0, None, cores, energy=True)
+    t1 = oracle.timed_steps(s.desc, arrays, v, 0, steps, s.source_samples(0, steps), cores, energy=True)
+    return cells * steps / max(t1 - t0, 1e-9), cores, steps
+
+
+def timed(name, s, variant, bytes_per_cell, cells, nt=NT, cpu_steps=2):
     st = s.new_state()
     s.upload(st)
     s.run_device(variant, 0, 3)
     ms = s.run_device(variant, 3, nt)
     rate = cells * nt / (ms / 1e3)
-    print(json.dumps({"config": name, "cell_steps_per_s": rate, "us_per_step": 1e3 * ms / nt,
-                      "B_alg": bytes_per_cell, "GBps": rate * bytes_per_cell / 1e9,
-                      "frac_of_6551": rate * bytes_per_cell / 6551.7e9, "launches": s.last_launch_count()}), flush=True)
+    line = {"config": name, "cell_steps_per_s": rate, "us_per_step": 1e3 * ms / nt,
+            "B_alg": bytes_per_cell, "GBps": rate * bytes_per_cell / 1e9,
+            "frac_of_6551": rate * bytes_per_cell / 6551.7e9, "launches": s.last_launch_count()}
+    if CPU:
+        cr, cores, steps = cpu_rate(s, variant, cells, cpu_steps)
+        line["cpu_port_cell_steps_per_s"] = cr
+        line["cpu_port"] = f"oracle port, {cores} threads, {steps} steps"
+        line["gpu_over_cpu"] = rate / cr
+    print(json.dumps(line), flush=True)
 
 
 def cfg1(order=2, prec=F16):
@@ -63,15 +90,15 @@ def cfg5():  # 3D elastic 512^3 per GPU, 2nd order, layered
 
 
 if __name__ == "__main__":
-    which = sys.argv[2].split(",") if len(sys.argv) > 2 else ["1", "3", "4", "5"]
+    which = ARGS[1].split(",") if len(ARGS) > 1 else ["1", "3", "4", "5"]
     if "1" in which:
         for name, prec, var in (("fp16 naive", F16, None), ("fp16 op3", F16, hw.Variant.OP3),
                                 ("fp64", hw.Precision.FP64, None)):
             timed(f"1: 2D acoustic 256^2 2nd order rigid walls {name}, energy every step", cfg1(2, prec), var, 24,
-                  256 * 256)
+                  256 * 256, cpu_steps=200)
     if "3" in which:
-        timed("3: 3D acoustic 512^3 2nd order fp16 op3 (beta plane)", cfg3(), hw.Variant.OP3, 34, 512 ** 3)
+        timed("3: 3D acoustic 512^3 2nd order fp16 op3 (beta plane)", cfg3(), hw.Variant.OP3, 34, 512 ** 3, cpu_steps=1)
     if "4" in which:
-        timed("4: 2D elastic 4096^2 free surface fp16 op6", cfg4(), hw.Variant.OP6, 40, 4096 * 4097)
+        timed("4: 2D elastic 4096^2 free surface fp16 op6", cfg4(), hw.Variant.OP6, 40, 4096 * 4097, cpu_steps=5)
     if "5" in which:
-        timed("5: 3D elastic 512^3 2nd order fp16 op6", cfg5(), hw.Variant.OP6, 72, 512 ** 3)
+        timed("5: 3D elastic 512^3 2nd order fp16 op6", cfg5(), hw.Variant.OP6, 72, 512 ** 3, cpu_steps=1)
