@@ -246,6 +246,14 @@ __global__ void __launch_bounds__(512, 1)
         rcs = __ldg(P.rho_s.rcp + back(fw, 2) * P.rho_s.ss);
         rcb = __ldg(P.beta.rcp + back(fw, 3) * P.beta.ss);
     }
+    // energy coefficients of the rows of the next iteration (sample steps, row-uniform planes)
+    const bool epre = sample && erow;
+    double ex = 0.0, es = 0.0, eb = 0.0;
+    if (epre) {
+        ex = p64(P.e_rho_x, fw, 0, 0);
+        es = p64(P.e_rho_s, back(fw, 2), 0, 0);
+        eb = p64(P.e_beta, back(fw, 3), 0, 0);
+    }
 #pragma unroll 1
     for (int i = 0; i < NI; i++) {
         const int u = i % FR;
@@ -256,6 +264,12 @@ __global__ void __launch_bounds__(512, 1)
             rcx_n = __ldg(P.rho_x.rcp + fwn * P.rho_x.ss);
             rcs_n = __ldg(P.rho_s.rcp + back(fwn, 2) * P.rho_s.ss);
             rcb_n = __ldg(P.beta.rcp + back(fwn, 3) * P.beta.ss);
+        }
+        double ex_n = 0.0, es_n = 0.0, eb_n = 0.0;
+        if (epre) {
+            ex_n = p64(P.e_rho_x, fwn, 0, 0);
+            es_n = p64(P.e_rho_s, back(fwn, 2), 0, 0);
+            eb_n = p64(P.e_beta, back(fwn, 3), 0, 0);
         }
         {
             {
@@ -295,15 +309,22 @@ __global__ void __launch_bounds__(512, 1)
                         track(acc[S_RVX], r);
                     }
                     st8(xrow + x, vxn);
-                    if (sample) {  // per-row sum when the plane is row-uniform (one multiply per row)
+                    if (sample) {  // per-row sum when the plane is row-uniform (one multiply per row);
+                        // a product of two binary16 values is exact in binary32 (<= 22 bits)
                         double sv = 0.0;
 #pragma unroll
-                        for (int j = 0; j < FCPT; j++) {
-                            const double v = (double)__half2float(vxn.q[j >> 1].e[j & 1]);
-                            if (erow) sv += v * v;
-                            else e[1] += p64(P.e_rho_x, f, 0, x + j) * (v * v);
+                        for (int j = 0; j < 4; j++) {
+                            const float2 v = __half22float2(vxn.q[j].h2);
+                            const double a = (double)__fmul_rn(v.x, v.x), b = (double)__fmul_rn(v.y, v.y);
+                            if (erow) {
+                                sv += a;
+                                sv += b;
+                            } else {
+                                e[1] += p64(P.e_rho_x, f, 0, x + 2 * j) * a;
+                                e[1] += p64(P.e_rho_x, f, 0, x + 2 * j + 1) * b;
+                            }
                         }
-                        if (erow) e[1] += p64(P.e_rho_x, f, 0, 0) * sv;
+                        if (erow) e[1] += ex * sv;
                     }
                 }
                 const int k = f - 3;
@@ -339,12 +360,18 @@ __global__ void __launch_bounds__(512, 1)
                         if (sample) {
                             double sv = 0.0;
 #pragma unroll
-                            for (int j = 0; j < FCPT; j++) {
-                                const double v = (double)__half2float(vsn.q[j >> 1].e[j & 1]);
-                                if (erow) sv += v * v;
-                                else e[2] += p64(P.e_rho_s, r, 0, x + j) * (v * v);
+                            for (int j = 0; j < 4; j++) {
+                                const float2 v = __half22float2(vsn.q[j].h2);
+                                const double a = (double)__fmul_rn(v.x, v.x), b = (double)__fmul_rn(v.y, v.y);
+                                if (erow) {
+                                    sv += a;
+                                    sv += b;
+                                } else {
+                                    e[2] += p64(P.e_rho_s, r, 0, x + 2 * j) * a;
+                                    e[2] += p64(P.e_rho_s, r, 0, x + 2 * j + 1) * b;
+                                }
                             }
-                            if (erow) e[2] += p64(P.e_rho_s, r, 0, 0) * sv;
+                            if (erow) e[2] += es * sv;
                         }
                     }
                     vq[3] = vsn;
@@ -386,13 +413,18 @@ __global__ void __launch_bounds__(512, 1)
                     if (sample) {
                         double sp = 0.0;
 #pragma unroll
-                        for (int j = 0; j < FCPT; j++) {
-                            const double a = (double)__half2float(pold.q[j >> 1].e[j & 1]);
-                            const double bb = (double)__half2float(pn.q[j >> 1].e[j & 1]);
-                            if (erow) sp += a * bb;
-                            else e[0] += p64(P.e_beta, k, 0, x + j) * (a * bb);
+                        for (int j = 0; j < 4; j++) {
+                            const float2 a = __half22float2(pold.q[j].h2), bb = __half22float2(pn.q[j].h2);
+                            const double u0 = (double)__fmul_rn(a.x, bb.x), u1 = (double)__fmul_rn(a.y, bb.y);
+                            if (erow) {
+                                sp += u0;
+                                sp += u1;
+                            } else {
+                                e[0] += p64(P.e_beta, k, 0, x + 2 * j) * u0;
+                                e[0] += p64(P.e_beta, k, 0, x + 2 * j + 1) * u1;
+                            }
                         }
-                        if (erow) e[0] += p64(P.e_beta, k, 0, 0) * sp;
+                        if (erow) e[0] += eb * sp;
                     }
                     // receiver traces (acoustic.py:217-218)
                     rec_row(P.rec, rcur, rhi, k, x, P.traces, P.nt, n, [&](int o) {
@@ -406,6 +438,9 @@ __global__ void __launch_bounds__(512, 1)
             }
         }
         fw = fwn;
+        ex = ex_n;
+        es = es_n;
+        eb = eb_n;
         rcx = rcx_n;
         rcs = rcs_n;
         rcb = rcb_n;
