@@ -90,3 +90,17 @@ def test_nccl_transport_range_failure(one_rank_job):
     assert (eb.value.step, eb.value.field_name) == (ea.value.step, ea.value.field_name)
     for n in a.FIELDS:
         assert_same_bits(getattr(sb, n).values, getattr(sa, n).values, n)
+
+
+def test_nccl_transport_device_resident_run(one_rank_job):
+    """The bench's decomposed path: upload -> run_device (overlapped edge/interior bands,
+    NCCL exchange every step) -> download equals the single-process run."""
+    a, sa = _acoustic()
+    a.run(hw.Variant.OP3, sa)
+    b, sb = _acoustic(distributed=True)
+    b.upload(sb)
+    ms = b.run_device(hw.Variant.OP3, 0, b.grid.nt)
+    b.download(sb)
+    assert ms > 0 and b.transport() == 2 and b.kernel_path() == "fused2d"
+    for n in a.FIELDS:
+        assert_same_bits(getattr(sb, n).values, getattr(sa, n).values, n)
