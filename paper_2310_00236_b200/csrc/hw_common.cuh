@@ -381,9 +381,29 @@ __device__ __forceinline__ void rec_row(const int* rec, int& cur, int hi, int r,
     }
 }
 
+// Blocks need not be a multiple of 32 threads (the fused 2D kernel runs nx/8 threads):
+// the collectives below use only the lanes that exist.
+__device__ __forceinline__ int warp_lanes() {
+    const int rem = (int)blockDim.x - (int)(threadIdx.x & ~31u);
+    return rem < 32 ? rem : 32;
+}
+
+// fixed-tree warp sum (lane 0 holds the result); identical bits to the full-warp tree
+__device__ __forceinline__ double warp_sum(double a) {
+    const int lane = threadIdx.x & 31, nl = warp_lanes();
+    const unsigned m = nl == 32 ? 0xffffffffu : ((1u << nl) - 1u);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double b = __shfl_down_sync(m, a, o);
+        if (lane + o < nl) a += b;
+    }
+    return a;
+}
+
 // Warp-aggregated failure record: first failing step + external field bits.
 __device__ __forceinline__ void record_failure(Ctrl* ctrl, int64_t n, unsigned int mask) {
-    unsigned int any = __reduce_or_sync(0xffffffffu, mask);
+    const int nl = warp_lanes();
+    unsigned int any = __reduce_or_sync(nl == 32 ? 0xffffffffu : ((1u << nl) - 1u), mask);
     if (any && (threadIdx.x & 31) == 0) {
         atomicMin(reinterpret_cast<unsigned long long*>(&ctrl->fail_step), (unsigned long long)n);
         atomicOr(&ctrl->fail_mask, any);
@@ -402,15 +422,13 @@ __device__ __forceinline__ void block_partials(double v[NCOMP], double* out, int
     int lane_id = tid & 31, warp = tid >> 5;
 #pragma unroll
     for (int c = 0; c < NCOMP; c++) {
-        double a = v[c];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+        const double a = warp_sum(v[c]);
         if (lane_id == 0) red[warp][c] = a;
     }
     __syncthreads();
     if (tid < NCOMP) {
         double a = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); w++) a += red[w][tid];
+        for (int w = 0; w < (int)((blockDim.x + 31) >> 5); w++) a += red[w][tid];
         const int64_t bid = idx >= 0 ? idx : ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
         out[bid * NCOMP + tid] = a;
     }
@@ -421,12 +439,12 @@ __device__ __forceinline__ void block_partials(double v[NCOMP], double* out, int
 // combines the components left to right.  Any block size >= 32; total on thread 0.
 __device__ __forceinline__ double finalize_partials(const double* part, int nb) {
     __shared__ double tot[NCOMP];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (int)(blockDim.x >> 5);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = (int)((blockDim.x + 31) >> 5);
+    const int nl = warp_lanes();
     for (int c = w; c < NCOMP; c += nw) {
         double a = 0.0;
-        for (int bi = lane; bi < nb; bi += 32) a += __ldcg(&part[(int64_t)bi * NCOMP + c]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+        for (int bi = lane; bi < nb; bi += nl) a += __ldcg(&part[(int64_t)bi * NCOMP + c]);
+        a = warp_sum(a);
         if (lane == 0) tot[c] = a;
     }
     __syncthreads();

@@ -470,7 +470,9 @@ size_t fused2d_smem_bytes(int64_t nx) { return 256 + ((size_t)FR * NSTREAM + 2) 
 int fused2d_threads(int64_t nx) { return (int)(nx / FCPT); }
 
 bool fused2d_eligible(int64_t nx, int max_smem) {
-    if (nx % 256 != 0 || nx / FCPT > 512) return false;
+    // 8 cells per thread, 16-byte TMA rows: nx % 8 == 0 (nx / 8 threads; the last warp may
+    // be partial -- the collectives use the existing lanes only)
+    if (nx % 8 != 0 || nx < 64 || nx / FCPT > 512) return false;
     return fused2d_smem_bytes(nx) <= (size_t)max_smem;
 }
 

@@ -119,3 +119,23 @@ def test_fused_receiver_line_records_every_trace():
     out = s.run(hw.Variant.OP3, st)
     assert s.kernel_path() == "fused2d"
     np.testing.assert_array_equal(np.array([t.samples for t in out.traces]), ref["traces"])
+
+
+@pytest.mark.parametrize("nx,ny", [(600, 64), (104, 40), (264, 30), (1000, 24)])
+def test_fused_any_width_multiple_of_8(nx, ny):
+    """The single-pass kernel takes any nx % 8 == 0 (the reference presets' 600 x 600):
+    nx / 8 threads, the last warp possibly partial (collectives over existing lanes)."""
+    s, st = _case(nx, ny, 18, every=1)
+    ref = oracle.run_solver(s, hw.Variant.OP6, st)
+    out = s.run(hw.Variant.OP6, st)
+    assert s.kernel_path() == "fused2d"
+    _check(s, st, out, ref)
+
+
+def test_fused_range_failure_partial_warp():
+    s, st = _case(600, 32, 300, amp=1e9, layered=False)
+    ref = oracle.run_solver(s, None, st)
+    with pytest.raises(hw.RangeFailureError) as err:
+        s.run(None, st)
+    assert err.value.step == ref["fail"][0]
+    assert err.value.field_name == s._fail_name(ref["fail"][1])
