@@ -357,6 +357,14 @@ struct hw_solver {
     cudaStream_t st2 = nullptr;
     cudaEvent_t ev_edge[2] = {}, ev_int[2] = {};
     int nb_int = 0;
+    // persistent small-grid kernel: one cooperative launch per run, state in shared memory
+    bool small = false;
+    int small_nb = 0;
+    __half* xch = nullptr;
+    unsigned int* gbar = nullptr;
+    double* src_dev = nullptr;
+    int64_t src_cap = 0;
+    double* partials2 = nullptr;
     bool tb2 = false;  // two steps per launch (temporal blocking, hw_tb2d.cu)
     int tb2_tiles = 0, tb2_bands = 0;
     double* partials_b = nullptr;  // stage-B energy partials of the two-step kernel
@@ -680,6 +688,20 @@ int setup_handle(hw_solver* h) {
                 h->tb2 = true;
             }
         }
+        // small grids: the persistent kernel (latency, not bandwidth, bounds them)
+        const char* sme = getenv("HALFWAVE_SMALL");
+        if (want && !(sme && strcmp(sme, "0") == 0) && h->ac && !h->d3 && h->LS == 16 && h->LU == 16 &&
+            h->world == 1 && h->transport == 0 && desc->nx * desc->ns <= (int64_t)1 << 20 &&
+            small2d_eligible(desc->nx, desc->ns, nsm, dev_smem)) {
+            h->small_nb = small2d_blocks(desc->ns, nsm);
+            if (small2d_prepare(desc->nx, desc->ns, h->small_nb) != cudaSuccess)
+                return fail(HW_ECUDA, "small-grid kernel setup failed");
+            CU(cudaMalloc(&h->xch, small2d_xch_bytes(desc->nx, h->small_nb)));
+            CU(cudaMemset(h->xch, 0, small2d_xch_bytes(desc->nx, h->small_nb)));
+            CU(cudaMalloc(&h->gbar, 2 * sizeof(unsigned int)));
+            CU(cudaMalloc(&h->partials2, (size_t)h->small_nb * NCOMP * sizeof(double)));
+            h->small = true;
+        }
         if (want && !h->ac && !h->d3 && h->LS == 16 && h->LU == 16 && el2d_stream_eligible(desc->nx, dev_smem)) {
             if (el2d_stream_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "streaming kernel setup failed");
             int64_t nbs = max_rows / 4;
@@ -768,6 +790,10 @@ void release_handle(hw_solver* h) {
     if (h->evals) cudaFree(h->evals);
     if (h->rec_off) cudaFree(h->rec_off);
     if (h->rec_sorted) cudaFree(h->rec_sorted);
+    if (h->xch) cudaFree(h->xch);
+    if (h->gbar) cudaFree(h->gbar);
+    if (h->src_dev) cudaFree(h->src_dev);
+    if (h->partials2) cudaFree(h->partials2);
     for (int k = 0; k < 2; k++) {
         if (h->ev_edge[k]) cudaEventDestroy(h->ev_edge[k]);
         if (h->ev_int[k]) cudaEventDestroy(h->ev_int[k]);
@@ -1218,7 +1244,27 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
         return rc;
     }
     if (timed) CU(cudaEventRecord(h->ev0, h->st));
-    if (h->fused && fused_slab && h->st2) {
+    if (h->small) {  // every step in one cooperative launch (hw_small2d.cu)
+        if (src && nt > h->src_cap) {
+            if (h->src_dev) cudaFree(h->src_dev);
+            h->src_dev = nullptr;
+            h->src_cap = 0;
+            CU(cudaMalloc(&h->src_dev, nt * sizeof(double)));
+            h->src_cap = nt;
+        }
+        if (src && nt > 0) CU(cudaMemcpyAsync(h->src_dev, src, nt * sizeof(double), cudaMemcpyHostToDevice, h->st));
+        CU(cudaMemsetAsync(h->gbar, 0, 2 * sizeof(unsigned int), h->st));
+        AcFusedParams F = fused_params(h, nt);
+        __half* bufs[2][FUSED_NSTREAM];
+        for (int j = 0; j < FUSED_NSTREAM; j++)
+            F.in[j] = F.out[j] = (__half*)((char*)h->mem[j] + (int64_t)G * h->g.slab * 2);
+        (void)bufs;
+        if (nt > 0) {
+            CU(launch_ac2d_small(variant, h->d.order, F, h->xch, h->gbar, src ? h->src_dev : nullptr, h->partials2,
+                                 (int)C.every, energy ? 1 : 0, h->small_nb, nt, h->st));
+            h->launches++;
+        }
+    } else if (h->fused && fused_slab && h->st2) {
         // NCCL slab, overlapped: per step the two thin edge bands run first on st and the
         // ghost exchange follows them on st, while the interior bands run on st2.
         //   st : wait interior(n-1) | edge(n) | record E(n) | exchange(n)
@@ -1297,7 +1343,7 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
 // home so buffer A is always current between calls.
 static int fused_copy_back(hw_solver* h, int64_t executed, int32_t variant) {
     const int64_t launches = h->tb2 ? (executed + 1) / 2 : executed;
-    if (!h->fused || (launches & 1) == 0) return HW_OK;
+    if (!h->fused || h->small || (launches & 1) == 0) return HW_OK;  // the small-grid kernel writes A itself
     const int nf = variant == HW_NAIVE ? h->nsol : 2 * h->nsol;  // naive runs never touch residuals
     for (int j = 0; j < nf; j++) {
         int f = h->ext[j % h->nsol];
@@ -1538,7 +1584,7 @@ int64_t hw_last_launch_count(const hw_solver* h) { return h ? h->launches : 0; }
 
 const char* hw_kernel_path(const hw_solver* h) {
     if (!h) return "";
-    return h->tb2 ? "fused2d-tb2" : h->fused ? "fused2d" : (h->el_stream ? "stream2d" : ((h->ac3_stream || h->el3_stream) ? "stream3d" : "generic"));
+    return h->small ? "small2d" : h->tb2 ? "fused2d-tb2" : h->fused ? "fused2d" : (h->el_stream ? "stream2d" : ((h->ac3_stream || h->el3_stream) ? "stream3d" : "generic"));
 }
 
 int32_t hw_transport(const hw_solver* h) { return h ? h->transport : -1; }

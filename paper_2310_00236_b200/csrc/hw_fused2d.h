@@ -42,6 +42,14 @@ cudaError_t tb2_prepare(int64_t nx);
 void launch_ac2d_tb2(int variant, int order, const AcFusedParams& F, int ntiles, int nbands, double* partials_b,
                      int64_t n, double srcA, double srcB, int sampleA, int sampleB, int64_t eidxA, int64_t eidxB,
                      cudaStream_t st);
+// persistent small-grid kernel (hw_small2d.cu)
+bool small2d_eligible(int64_t nx, int64_t ns, int nsm, int max_smem);
+int small2d_blocks(int64_t ns, int nsm);
+size_t small2d_xch_bytes(int64_t nx, int nb);
+cudaError_t small2d_prepare(int64_t nx, int64_t ns, int nb);
+cudaError_t launch_ac2d_small(int variant, int order, const AcFusedParams& F, __half* xch, unsigned int* gbar,
+                              const double* src_dev, double* partials2, int every, int energy, int nb, int64_t nt,
+                              cudaStream_t st);
 void launch_ac2d_fused(int variant, int order, const AcFusedParams& P, int nblocks, int64_t n, double src, int sample,
                        int64_t eidx, cudaStream_t st);
 }  // namespace hw

@@ -14,6 +14,11 @@ from golden_cases import assert_same_bits
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _streaming_kernel(monkeypatch):  # these grids would otherwise take the persistent small-grid kernel
+    monkeypatch.setenv("HALFWAVE_SMALL", "0")
+
+
 def _case(nx, ny, nt, *, order=4, amp=2.0, every=5, seed=0, src_row=3, layered=True):
     rng = np.random.default_rng(seed)
     dx = 1.0 / nx

@@ -54,7 +54,7 @@ def test_gpu_rigid_config1_box_vs_direct_oracle(variant, vname):
     st.p.values = p.astype(np.float16)
     init = {k: getattr(st, k).values.copy() for k in FIELDS}
     out = s.run(variant, st)
-    assert s.kernel_path() == "fused2d"  # the 512^2 mirrored domain runs the single-pass kernel
+    assert s.kernel_path() == "small2d"  # the 512^2 mirrored domain runs the persistent small-grid kernel
     bp = {"rho_x": np.ones((n + 1, n)), "rho_y": np.ones((n, n + 1)), "beta": np.ones((n + 1, n + 1))}
     taps = hw.StencilSpec.make(hw.Precision.FP16, h, 2).coefficients
     ref, e, tr = orig.run(init, {k: v.astype(np.float16) for k, v in bp.items()}, bp, taps, h, 0.5 * h, nt,

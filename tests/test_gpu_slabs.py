@@ -159,5 +159,5 @@ def test_fused_2d_slabs_receivers_on_slab_edges(slabs):
     a, sa, b, sb = _pair(make, slabs)
     oa = a.run(hw.Variant.OP6, sa)
     ob = b.run(hw.Variant.OP6, sb)
-    assert a.kernel_path() == "fused2d" and b.kernel_path() == "fused2d" and b.transport() == 1
+    assert a.kernel_path() == "small2d" and b.kernel_path() == "fused2d" and b.transport() == 1
     _compare(a, sa, oa, b, sb, ob)

@@ -17,6 +17,7 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(autouse=True)
 def _two_step(monkeypatch):  # the two-step kernel is opt-in
     monkeypatch.setenv("HALFWAVE_TB", "1")
+    monkeypatch.setenv("HALFWAVE_SMALL", "0")
 
 
 def _case(nx, ny, nt, *, order=4, amp=2.0, every=5, seed=0, src_row=3, layered=True, recs=None):
