@@ -702,7 +702,7 @@ int setup_handle(hw_solver* h) {
             CU(cudaMalloc(&h->partials2, (size_t)h->small_nb * NCOMP * sizeof(double)));
             h->small = true;
         }
-        if (want && !h->ac && !h->d3 && h->LS == 16 && h->LU == 16 && el2d_stream_eligible(desc->nx, dev_smem)) {
+        if (want && !h->ac && !h->d3 && h->LS == 16 && h->LU == 16 && el2d_stream_eligible(desc->nx, desc->ns, dev_smem)) {
             if (el2d_stream_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "streaming kernel setup failed");
             int64_t nbs = max_rows / 4;
             if (nbs < 1) nbs = 1;

@@ -458,8 +458,13 @@ __global__ void __launch_bounds__(512, 1)
 
 size_t el2d_stream_smem_bytes(int64_t nx) { return 128 + (size_t)(ER * ENS + 2 * EOWN) * nx * sizeof(__half); }
 
-bool el2d_stream_eligible(int64_t nx, int max_smem) {
-    return nx % 256 == 0 && nx / ECPT <= 512 && el2d_stream_smem_bytes(nx) <= (size_t)max_smem;
+bool el2d_stream_eligible(int64_t nx, int64_t ns, int max_smem) {
+    // nx / 8 threads (the last warp may be partial: the collectives use the existing lanes).  Widths that
+    // are not a multiple of 256 give under-filled CTAs: worth it only on large grids (the 600^2 presets
+    // run faster on the phase kernels).
+    if (nx % 8 != 0 || nx < 64 || nx / ECPT > 512) return false;
+    if (nx % 256 != 0 && nx * ns < ((int64_t)1 << 21)) return false;
+    return el2d_stream_smem_bytes(nx) <= (size_t)max_smem;
 }
 
 template <int V, int O>

@@ -87,7 +87,7 @@ struct StreamIO {
 };
 
 // streaming 2D elastic phase kernels (hw_elastic2d_stream.cu)
-bool el2d_stream_eligible(int64_t nx, int max_smem);
+bool el2d_stream_eligible(int64_t nx, int64_t ns, int max_smem);
 cudaError_t el2d_stream_prepare(int64_t nx);
 void launch_el2d_vel_stream(int variant, int order, const ElParams& P, const StreamIO& IO, int nblocks, int64_t n,
                             double src, cudaStream_t st);

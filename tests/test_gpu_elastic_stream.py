@@ -134,7 +134,7 @@ def test_stream_free_surface_syy_rows_bit_zero():
     assert np.any(st.syy.values[1:-1] != 0.0)
 
 
-@pytest.mark.parametrize("nx,lanes,path", [(4096, hw.Precision.FP16, "stream2d"), (200, hw.Precision.FP16, "generic"),
+@pytest.mark.parametrize("nx,lanes,path", [(4096, hw.Precision.FP16, "stream2d"), (100, hw.Precision.FP16, "generic"),
                                            (256, hw.Precision.FP32, "generic")])
 def test_stream_path_selection(nx, lanes, path):
     med = hw.build_layered_elastic(nx, 16, LAYERS)
@@ -142,3 +142,13 @@ def test_stream_path_selection(nx, lanes, path):
     s = hw.ElasticSolver(g, med, None, stencil_precision=lanes, update_precision=lanes)
     s.run(hw.Variant.OP3, s.new_state())
     assert s.kernel_path() == path
+
+
+@pytest.mark.parametrize("nx,ny,fs", [(600, 3500, True), (264, 8000, False)])
+def test_stream_any_width_multiple_of_8(nx, ny, fs):
+    """Large grids of any nx % 8 == 0: nx / 8 threads, partial last warp."""
+    s, st = _case(nx, ny, 6, fs=fs, src_row=min(6, ny - 1))
+    ref = oracle.run_solver(s, hw.Variant.OP6, st)
+    out = s.run(hw.Variant.OP6, st)
+    assert s.kernel_path() == "stream2d"
+    _check(s, st, out, ref)
