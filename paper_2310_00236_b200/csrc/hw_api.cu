@@ -358,7 +358,7 @@ struct hw_solver {
     cudaEvent_t ev_edge[2] = {}, ev_int[2] = {};
     int nb_int = 0;
     // persistent small-grid kernel: one cooperative launch per run, state in shared memory
-    bool small = false;
+    bool small = false, small_el = false;
     int small_nb = 0;
     __half* xch = nullptr;
     unsigned int* gbar = nullptr;
@@ -702,7 +702,20 @@ int setup_handle(hw_solver* h) {
             CU(cudaMalloc(&h->partials2, (size_t)h->small_nb * NCOMP * sizeof(double)));
             h->small = true;
         }
-        if (want && !h->ac && !h->d3 && h->LS == 16 && h->LU == 16 && el2d_stream_eligible(desc->nx, desc->ns, dev_smem)) {
+        if (want && !(sme && strcmp(sme, "0") == 0) && !h->ac && !h->d3 && h->LS == 16 && h->LU == 16 &&
+            h->world == 1 && h->transport == 0 && desc->nx * desc->ns <= (int64_t)1 << 20 &&
+            small_el2d_eligible(desc->nx, desc->ns, nsm, dev_smem)) {
+            h->small_nb = small2d_blocks(desc->ns, nsm);
+            if (small_el2d_prepare(desc->nx, desc->ns, h->small_nb) != cudaSuccess)
+                return fail(HW_ECUDA, "small-grid kernel setup failed");
+            CU(cudaMalloc(&h->xch, small_el2d_xch_bytes(desc->nx, h->small_nb)));
+            CU(cudaMemset(h->xch, 0, small_el2d_xch_bytes(desc->nx, h->small_nb)));
+            CU(cudaMalloc(&h->gbar, 2 * sizeof(unsigned int)));
+            CU(cudaMalloc(&h->partials2, (size_t)h->small_nb * NCOMP * sizeof(double)));
+            h->small_el = true;
+        }
+        if (want && !h->small_el && !h->ac && !h->d3 && h->LS == 16 && h->LU == 16 &&
+            el2d_stream_eligible(desc->nx, desc->ns, dev_smem)) {
             if (el2d_stream_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "streaming kernel setup failed");
             int64_t nbs = max_rows / 4;
             if (nbs < 1) nbs = 1;
@@ -1244,7 +1257,7 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
         return rc;
     }
     if (timed) CU(cudaEventRecord(h->ev0, h->st));
-    if (h->small) {  // every step in one cooperative launch (hw_small2d.cu)
+    if (h->small || h->small_el) {  // every step in one cooperative launch (hw_small2d.cu)
         if (src && nt > h->src_cap) {
             if (h->src_dev) cudaFree(h->src_dev);
             h->src_dev = nullptr;
@@ -1254,15 +1267,22 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
         }
         if (src && nt > 0) CU(cudaMemcpyAsync(h->src_dev, src, nt * sizeof(double), cudaMemcpyHostToDevice, h->st));
         CU(cudaMemsetAsync(h->gbar, 0, 2 * sizeof(unsigned int), h->st));
-        AcFusedParams F = fused_params(h, nt);
-        __half* bufs[2][FUSED_NSTREAM];
-        for (int j = 0; j < FUSED_NSTREAM; j++)
-            F.in[j] = F.out[j] = (__half*)((char*)h->mem[j] + (int64_t)G * h->g.slab * 2);
-        (void)bufs;
-        if (nt > 0) {
-            CU(launch_ac2d_small(variant, h->d.order, F, h->xch, h->gbar, src ? h->src_dev : nullptr, h->partials2,
-                                 (int)C.every, energy ? 1 : 0, h->small_nb, nt, h->st));
-            h->launches++;
+        if (h->small_el) {
+            if (nt > 0) {
+                CU(launch_el2d_small(variant, h->d.order, C.L, stream_io(h, C), h->xch, h->gbar,
+                                     src ? h->src_dev : nullptr, h->partials2, (int)C.every, energy ? 1 : 0,
+                                     h->small_nb, nt, h->st));
+                h->launches++;
+            }
+        } else {
+            AcFusedParams F = fused_params(h, nt);
+            for (int j = 0; j < FUSED_NSTREAM; j++)
+                F.in[j] = F.out[j] = (__half*)((char*)h->mem[j] + (int64_t)G * h->g.slab * 2);
+            if (nt > 0) {
+                CU(launch_ac2d_small(variant, h->d.order, F, h->xch, h->gbar, src ? h->src_dev : nullptr, h->partials2,
+                                     (int)C.every, energy ? 1 : 0, h->small_nb, nt, h->st));
+                h->launches++;
+            }
         }
     } else if (h->fused && fused_slab && h->st2) {
         // NCCL slab, overlapped: per step the two thin edge bands run first on st and the
@@ -1584,7 +1604,7 @@ int64_t hw_last_launch_count(const hw_solver* h) { return h ? h->launches : 0; }
 
 const char* hw_kernel_path(const hw_solver* h) {
     if (!h) return "";
-    return h->small ? "small2d" : h->tb2 ? "fused2d-tb2" : h->fused ? "fused2d" : (h->el_stream ? "stream2d" : ((h->ac3_stream || h->el3_stream) ? "stream3d" : "generic"));
+    return (h->small || h->small_el) ? "small2d" : h->tb2 ? "fused2d-tb2" : h->fused ? "fused2d" : (h->el_stream ? "stream2d" : ((h->ac3_stream || h->el3_stream) ? "stream3d" : "generic"));
 }
 
 int32_t hw_transport(const hw_solver* h) { return h ? h->transport : -1; }

@@ -106,6 +106,14 @@ void launch_el3d_vel_stream(int variant, int order, const ElParams& P, int nbloc
                             cudaStream_t st);
 void launch_el3d_stress_stream(int variant, int order, const ElParams& P, const StreamIO& IO, int nblocks, int64_t n,
                                double src, int sample, int64_t eidx, cudaStream_t st);
+// persistent small-grid 2D elastic kernel (hw_small2d.cu)
+bool small_el2d_eligible(int64_t nx, int64_t nh, int nsm, int max_smem);
+size_t small_el2d_xch_bytes(int64_t nx, int nb);
+cudaError_t small_el2d_prepare(int64_t nx, int64_t nh, int nb);
+cudaError_t launch_el2d_small(int variant, int order, const ElParams& P, const StreamIO& IO, __half* xch,
+                              unsigned int* gbar, const double* src_dev, double* partials2, int every, int energy,
+                              int nb, int64_t nt, cudaStream_t st);
+int small2d_blocks(int64_t ns, int nsm);
 void launch_epilogue(int LU, const EpParams& E, int64_t n, int sample, int64_t eidx, cudaStream_t st);
 
 }  // namespace hw

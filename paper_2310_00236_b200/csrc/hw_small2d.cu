@@ -18,6 +18,8 @@
 #include "hw_fused2d.h"
 #include "hw_params.h"
 #include "hw_stream.cuh"
+#include "../../include/halfwave_b200.h"
+#include <string.h>
 
 namespace hw {
 
@@ -274,6 +276,313 @@ __global__ void __launch_bounds__(1024, 1) k_ac2d_small(SmallParams S, int64_t n
     }
 }
 
+// ---------------------------------------------------------------- elastic (2D, velocity-stress)
+// Same design for ElasticSolver._step_work (elastic.py:176-238): per step two neighbour
+// exchanges and two grid barriers (stress halos before the velocity phase, velocity halos
+// before the stress phase; each CTA updates only its own rows, so single-buffered exchange
+// rows suffice).  Free surfaces: the edge CTAs fill their outer halos with the reference's
+// images (stencil.py:121-144: odd sxy / syy, even vx / vy), the surface rows use the
+// plane-stress modulus for sxx and a zero increment for syy (elastic.py:215-230).
+constexpr int SE_ROWS = 12;  // published rows: sxy 1 + 2, syy 2 + 1, vx 2 + 1, vy 1 + 2
+
+struct SmallElParams {
+    ElParams P;
+    double* traces;           // [n_rec][nt]
+    const int* rec;           // receivers sorted by (row, x)
+    int32_t n_rec, every, energy, pad;
+    int64_t nt;
+    double* e_vals;
+    double scale;
+    __half* xch;              // [nb][SE_ROWS][nx]
+    unsigned int* gbar;
+    const double* src;        // [nt]
+    double* partials2;
+};
+
+template <int V, int ORDER>
+__global__ void __launch_bounds__(1024, 1) k_el2d_small(SmallElParams S, int64_t nt) {
+    const ElParams& P = S.P;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int nx = (int)P.g.nx, nh = (int)P.vs.rows, nb = gridDim.x, b = blockIdx.x;  // nh: half rows (= ns)
+    const int64_t pitch = P.g.pitch;
+    const bool fs = P.fs != 0, top = b == 0, bot = b == nb - 1;
+    const int g0 = (int)((int64_t)b * nh / nb), Rh = (int)((int64_t)(b + 1) * nh / nb) - g0;
+    const int Ri = Rh + ((fs && bot) ? 1 : 0);  // the last band also owns the bottom surface row
+    const int above = (b + nb - 1) % nb, below = (b + 1) % nb;
+    const int tid = threadIdx.x, x = 2 * tid;
+    constexpr bool comp = V != 0;
+    // shared rows: syy [-1, Rh+2), sxy [-2, Ri+1), vx [-1, Rh+2), vy [-2, Ri+1), sxx / residuals own rows
+    __half* base = reinterpret_cast<__half*>(smem);
+    int off = 0;
+    auto alloc = [&](int lo, int hi) { __half* p = base + (off - lo) * nx; off += hi - lo; return p; };
+    __half* syy = alloc(-1, Rh + 2);
+    __half* sxy = alloc(-2, Ri + 1);
+    __half* vx = alloc(-1, Rh + 2);
+    __half* vy = alloc(-2, Ri + 1);
+    __half* sxx = alloc(0, Ri);
+    __half* rvx = alloc(0, Ri);
+    __half* rvy = alloc(0, Rh);
+    __half* rsxx = alloc(0, Ri);
+    __half* rsyy = alloc(0, Ri);
+    __half* rsxy = alloc(0, Rh);
+    auto gl = [&](const FieldView& f, int r) { return reinterpret_cast<__half*>(f.base) + (int64_t)(g0 + r) * pitch + x; };
+    for (int r = 0; r < Ri; r++) {  // load the band from the A buffers
+        s_st(vx + r * nx + x, s_ld(gl(P.vx, r)));
+        s_st(sxx + r * nx + x, s_ld(gl(P.sxx, r)));
+        s_st(syy + r * nx + x, s_ld(gl(P.sss, r)));
+        if (comp) {
+            s_st(rvx + r * nx + x, s_ld(gl(P.rvx, r)));
+            s_st(rsxx + r * nx + x, s_ld(gl(P.rsxx, r)));
+            s_st(rsyy + r * nx + x, s_ld(gl(P.rsss, r)));
+        }
+    }
+    for (int r = 0; r < Rh; r++) {
+        s_st(vy + r * nx + x, s_ld(gl(P.vs, r)));
+        s_st(sxy + r * nx + x, s_ld(gl(P.sxs, r)));
+        if (comp) {
+            s_st(rvy + r * nx + x, s_ld(gl(P.rvs, r)));
+            s_st(rsxy + r * nx + x, s_ld(gl(P.rsxs, r)));
+        }
+    }
+    auto xr = [&](int blk, int k) { return S.xch + ((int64_t)blk * SE_ROWS + k) * nx + x; };
+    auto neg = [](EH2 v) { return vneg<16, 2>(v); };
+    // stress rows for the neighbours: sxy row 0 | sxy rows Rh-2, Rh-1 | syy rows 0, 1 | syy row Ri-1
+    auto publish_s = [&]() {
+        s_st(xr(b, 0), s_ld(sxy + x));
+        s_st(xr(b, 1), s_ld(sxy + (Rh - 2) * nx + x));
+        s_st(xr(b, 2), s_ld(sxy + (Rh - 1) * nx + x));
+        s_st(xr(b, 3), s_ld(syy + x));
+        s_st(xr(b, 4), s_ld(syy + nx + x));
+        s_st(xr(b, 5), s_ld(syy + (Ri - 1) * nx + x));
+    };
+    // velocity rows: vx rows 0, 1 | vx row Ri-1 | vy row 0 | vy rows Rh-2, Rh-1
+    auto publish_v = [&]() {
+        s_st(xr(b, 6), s_ld(vx + x));
+        s_st(xr(b, 7), s_ld(vx + nx + x));
+        s_st(xr(b, 8), s_ld(vx + (Ri - 1) * nx + x));
+        s_st(xr(b, 9), s_ld(vy + x));
+        s_st(xr(b, 10), s_ld(vy + (Rh - 2) * nx + x));
+        s_st(xr(b, 11), s_ld(vy + (Rh - 1) * nx + x));
+    };
+    auto ingest_s = [&]() {  // sxy rows -2, -1 and [Rh, Ri+1); syy row -1 and [Ri, Rh+2)
+        if (fs && top) {
+            s_st(sxy - nx + x, neg(s_ld(sxy + x)));
+            s_st(sxy - 2 * nx + x, neg(s_ld(sxy + nx + x)));
+            s_st(syy - nx + x, neg(s_ld(syy + nx + x)));
+        } else {
+            s_st(sxy - 2 * nx + x, s_ldx(xr(above, 1)));
+            s_st(sxy - nx + x, s_ldx(xr(above, 2)));
+            s_st(syy - nx + x, s_ldx(xr(above, 5)));
+        }
+        if (fs && bot) {  // sxy rows ns, ns+1; syy row ns+1 (images about the bottom surface)
+            s_st(sxy + Rh * nx + x, neg(s_ld(sxy + (Rh - 1) * nx + x)));
+            s_st(sxy + (Rh + 1) * nx + x, neg(s_ld(sxy + (Rh - 2) * nx + x)));
+            s_st(syy + (Rh + 1) * nx + x, neg(s_ld(syy + (Ri - 2) * nx + x)));
+        } else {
+            s_st(sxy + Rh * nx + x, s_ldx(xr(below, 0)));
+            s_st(syy + Ri * nx + x, s_ldx(xr(below, 3)));
+            s_st(syy + (Ri + 1) * nx + x, s_ldx(xr(below, 4)));
+        }
+    };
+    auto ingest_v = [&]() {  // vx row -1 and [Ri, Rh+2); vy rows -2, -1 and [Rh, Ri+1)
+        if (fs && top) {
+            s_st(vx - nx + x, s_ld(vx + nx + x));
+            s_st(vy - nx + x, s_ld(vy + x));
+            s_st(vy - 2 * nx + x, s_ld(vy + nx + x));
+        } else {
+            s_st(vx - nx + x, s_ldx(xr(above, 8)));
+            s_st(vy - 2 * nx + x, s_ldx(xr(above, 10)));
+            s_st(vy - nx + x, s_ldx(xr(above, 11)));
+        }
+        if (fs && bot) {
+            s_st(vx + (Rh + 1) * nx + x, s_ld(vx + (Ri - 2) * nx + x));
+            s_st(vy + Rh * nx + x, s_ld(vy + (Rh - 1) * nx + x));
+            s_st(vy + (Rh + 1) * nx + x, s_ld(vy + (Rh - 2) * nx + x));
+        } else {
+            s_st(vx + Ri * nx + x, s_ldx(xr(below, 6)));
+            s_st(vx + (Ri + 1) * nx + x, s_ldx(xr(below, 7)));
+            s_st(vy + Rh * nx + x, s_ldx(xr(below, 9)));
+        }
+    };
+    __syncthreads();
+    publish_s();
+    grid_barrier(S.gbar, nb);
+
+    __half c[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) c[j] = lconst<16>(P.k, j);
+    const __half2 dt2 = __half2half2(lconst<16>(P.k, 4));
+    const int xl = x == 0 ? nx - 2 : x - 2, xrr = x + 2 >= nx ? 0 : x + 2;
+    const bool src_col = P.src_x >= x && P.src_x < x + 2;
+    const int src_lane = (int)(P.src_x - x) & 1, src_row = (int)P.src_s - g0;
+    const int ni = (int)P.sxx.nglob;  // integer rows globally (ns + 1 with free surfaces)
+    __half2 acc[10];
+#pragma unroll
+    for (int q = 0; q < 10; q++) acc[q] = __float2half2_rn(0.f);
+    auto track = [&](int q, EH2 v) { acc[q] = __hmax2_nan(acc[q], __habs2(v.h2)); };
+
+    for (int64_t n = 0; n < nt; n++) {
+        const double srcv = S.src ? S.src[n] : 0.0;
+        const __half srch = __double2half(srcv);
+        const int sample = S.energy && ((n + 1) % S.every == 0);
+        double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        // ---- velocity phase (stress halos of step n)
+        ingest_s();
+        __syncthreads();
+        for (int r = 0; r < Ri; r++) {  // vx = fl(fl(ddx sxx + dds sxy) / rho_x dt)
+            const EH2 a = EO2::add(s_xfold<ORDER>(c, sxx + r * nx, x, xl, xrr, false),
+                                   e_fold<ORDER>(c, s_ld(sxy + (r - 2) * nx + x), s_ld(sxy + (r - 1) * nx + x),
+                                                 s_ld(sxy + r * nx + x), s_ld(sxy + (r + 1) * nx + x)));
+            EH2 v = s_ld(vx + r * nx + x), t = comp ? s_ld(rvx + r * nx + x) : EH2{};
+            finish<16, 16, 2>(a, &P.rho_x, g0 + r, 0, x, dt2.x, V, -1, 0.0, v, t);
+            s_st(vx + r * nx + x, v);
+            track(0, v);
+            if (comp) {
+                s_st(rvx + r * nx + x, t);
+                track(5, t);
+            }
+        }
+        for (int r = 0; r < Rh; r++) {  // vy = fl(fl(ddx sxy + dds syy) (+ src) / rho_y dt)
+            const EH2 a = EO2::add(s_xfold<ORDER>(c, sxy + r * nx, x, xl, xrr, true),
+                                   e_fold<ORDER>(c, s_ld(syy + (r - 1) * nx + x), s_ld(syy + r * nx + x),
+                                                 s_ld(syy + (r + 1) * nx + x), s_ld(syy + (r + 2) * nx + x)));
+            EH2 v = s_ld(vy + r * nx + x), t = comp ? s_ld(rvy + r * nx + x) : EH2{};
+            const int sl = (P.src_kind == HW_SRC_VSLOW && src_col && r == src_row && srcv != 0.0) ? src_lane : -1;
+            finish<16, 16, 2>(a, &P.rho_s, g0 + r, 0, x, dt2.x, V, sl, srcv, v, t);
+            s_st(vy + r * nx + x, v);
+            track(1, v);
+            if (comp) {
+                s_st(rvy + r * nx + x, t);
+                track(6, t);
+            }
+            // receiver traces of vy after the step (elastic.py:283-284)
+            for (int q = rec_lower(S.rec, 0, S.n_rec, g0 + r, x);
+                 q < S.n_rec && __ldg(S.rec + 3 * q) == g0 + r && __ldg(S.rec + 3 * q + 1) < x + 2; q++)
+                S.traces[(int64_t)__ldg(S.rec + 3 * q + 2) * S.nt + n] = (double)__half2float(v.e[__ldg(S.rec + 3 * q + 1) - x]);
+        }
+        __syncthreads();
+        publish_v();
+        grid_barrier(S.gbar, nb);
+        // ---- stress phase (velocity halos of step n+1/2)
+        ingest_v();
+        __syncthreads();
+        for (int r = 0; r < Ri; r++) {  // sxx, syy at integer rows
+            const int sg = g0 + r;
+            const bool surf = fs && (sg == 0 || sg == ni - 1);
+            const EH2 dvx = s_xfold<ORDER>(c, vx + r * nx, x, xl, xrr, true);
+            const EH2 dvs = e_fold<ORDER>(c, s_ld(vy + (r - 2) * nx + x), s_ld(vy + (r - 1) * nx + x),
+                                          s_ld(vy + r * nx + x), s_ld(vy + (r + 1) * nx + x));
+            const EH2 stiff = pload<16, 2>(P.stiff, sg, 0, x), lam = pload<16, 2>(P.lam, sg, 0, x);
+            EH2 a1, a2;
+            if (surf) {
+                a1 = EO2::mul(pload<16, 2>(P.ep, sg == 0 ? 0 : 1, 0, x), dvx);
+                a2 = vsplat<16, 2>(lane<16>::zero());
+            } else {
+                a1 = EO2::add(EO2::mul(stiff, dvx), EO2::mul(lam, dvs));
+                a2 = EO2::add(EO2::mul(lam, dvx), EO2::mul(stiff, dvs));
+            }
+            const int sl = (P.src_kind == HW_SRC_EXPLOSIVE && src_col && r == src_row && srcv != 0.0) ? src_lane : -1;
+            const EH2 xo = s_ld(sxx + r * nx + x), so = s_ld(syy + r * nx + x);
+            EH2 xn = xo, sn = so;
+            EH2 t1 = comp ? s_ld(rsxx + r * nx + x) : EH2{}, t2 = comp ? s_ld(rsyy + r * nx + x) : EH2{};
+            finish<16, 16, 2>(a1, nullptr, sg, 0, x, dt2.x, V, sl, srcv, xn, t1);
+            finish<16, 16, 2>(a2, nullptr, sg, 0, x, dt2.x, V, sl, srcv, sn, t2);
+            s_st(sxx + r * nx + x, xn);
+            s_st(syy + r * nx + x, sn);
+            track(2, xn);
+            track(3, sn);
+            if (comp) {
+                s_st(rsxx + r * nx + x, t1);
+                s_st(rsyy + r * nx + x, t2);
+                track(7, t1);
+                track(8, t2);
+            }
+            if (sample) {  // kinetic x + strain energy at this integer row (diagnostics.py:100-162)
+                const EH2 vxo = s_ld(vx + r * nx + x);
+#pragma unroll
+                for (int k = 0; k < 2; k++) {
+                    const int xi = x + k;
+                    const double w = surf ? 0.5 : 1.0;
+                    const double v = (double)__half2float(vxo.e[k]);
+                    e[0] += (w * p64(P.e_rho_x, sg, 0, xi)) * (v * v);
+                    const double lamd = p64(P.e_lam, sg, 0, xi), mu = p64(P.e_mu, sg, 0, xi);
+                    const double xa = (double)__half2float(xo.e[k]), x1 = (double)__half2float(xn.e[k]);
+                    const double sa = (double)__half2float(so.e[k]), s1 = (double)__half2float(sn.e[k]);
+                    const double stiffd = lamd + 2.0 * mu, dd = 4.0 * mu * (lamd + mu);
+                    double val;
+                    if (mu == 0.0) val = surf ? 0.0 : (xa * x1) / (lamd + mu);
+                    else if (surf) val = xa * x1 * stiffd / dd;
+                    else val = (stiffd * (xa * x1 + sa * s1) - lamd * (xa * s1 + sa * x1)) / dd;
+                    if (surf) val = 0.5 * val;
+                    e[3] += val;
+                }
+            }
+        }
+        for (int r = 0; r < Rh; r++) {  // sxy = fl(mu fl(dds vx + ddx vy)) at half rows
+            const int sg = g0 + r;
+            const EH2 a = EO2::mul(pload<16, 2>(P.mu_n, sg, 0, x),
+                                   EO2::add(e_fold<ORDER>(c, s_ld(vx + (r - 1) * nx + x), s_ld(vx + r * nx + x),
+                                                          s_ld(vx + (r + 1) * nx + x), s_ld(vx + (r + 2) * nx + x)),
+                                            s_xfold<ORDER>(c, vy + r * nx, x, xl, xrr, false)));
+            const EH2 old = s_ld(sxy + r * nx + x);
+            EH2 sv = old, t = comp ? s_ld(rsxy + r * nx + x) : EH2{};
+            finish<16, 16, 2>(a, nullptr, sg, 0, x, dt2.x, V, -1, 0.0, sv, t);
+            s_st(sxy + r * nx + x, sv);
+            track(4, sv);
+            if (comp) {
+                s_st(rsxy + r * nx + x, t);
+                track(9, t);
+            }
+            if (sample) {  // kinetic y + shear energy at this half row
+                const EH2 vyo = s_ld(vy + r * nx + x);
+#pragma unroll
+                for (int k = 0; k < 2; k++) {
+                    const double v = (double)__half2float(vyo.e[k]);
+                    e[1] += p64(P.e_rho_s, sg, 0, x + k) * (v * v);
+                    const double mun = p64(P.e_mu_n, sg, 0, x + k);
+                    const double a0 = (double)__half2float(old.e[k]), a1 = (double)__half2float(sv.e[k]);
+                    e[4] += mun > 0.0 ? (a0 * a1) / mun : 0.0;
+                }
+            }
+        }
+        __syncthreads();
+        publish_s();
+        unsigned int mask = 0;  // external order vx vy sxx syy sxy, then residuals
+#pragma unroll
+        for (int q = 0; q < 10; q++) {
+            const unsigned int bits = *reinterpret_cast<const unsigned int*>(&acc[q]);
+            if (((bits & 0x7c00u) == 0x7c00u) || ((bits & 0x7c000000u) == 0x7c000000u)) mask |= 1u << q;
+        }
+        record_failure(P.ctrl, n, mask);
+        double* part = (n / S.every) & 1 ? S.partials2 : P.partials;
+        if (sample) block_partials(e, part);
+        grid_barrier(S.gbar, nb);
+        if (sample && b == 0) {
+            const double tsum = finalize_partials(part, nb);
+            if (tid == 0) S.e_vals[(n + 1) / S.every] = S.scale * tsum;
+        }
+        if (*reinterpret_cast<const volatile int64_t*>(&P.ctrl->fail_step) <= n) break;
+    }
+    for (int r = 0; r < Ri; r++) {  // write the band back (A buffers)
+        s_st(gl(P.vx, r), s_ld(vx + r * nx + x));
+        s_st(gl(P.sxx, r), s_ld(sxx + r * nx + x));
+        s_st(gl(P.sss, r), s_ld(syy + r * nx + x));
+        if (comp) {
+            s_st(gl(P.rvx, r), s_ld(rvx + r * nx + x));
+            s_st(gl(P.rsxx, r), s_ld(rsxx + r * nx + x));
+            s_st(gl(P.rsss, r), s_ld(rsyy + r * nx + x));
+        }
+    }
+    for (int r = 0; r < Rh; r++) {
+        s_st(gl(P.vs, r), s_ld(vy + r * nx + x));
+        s_st(gl(P.sxs, r), s_ld(sxy + r * nx + x));
+        if (comp) {
+            s_st(gl(P.rvs, r), s_ld(rvy + r * nx + x));
+            s_st(gl(P.rsxs, r), s_ld(rsxy + r * nx + x));
+        }
+    }
+}
+
 // ---------------------------------------------------------------- host side
 
 static int small_blocks(int64_t ns, int nsm) {
@@ -336,6 +645,65 @@ cudaError_t launch_ac2d_small(int variant, int order, const AcFusedParams& F, __
     void* fn = fused2d_rowmed(F) ? small_fn<true>(variant, order) : small_fn<false>(variant, order);
     void* args[] = {(void*)&S, (void*)&nt};
     return cudaLaunchCooperativeKernel(fn, dim3(nb), dim3((unsigned)(F.nx / 2)), args, small_smem(F.nx, F.ns, nb), st);
+}
+
+// elastic: bands of >= 3 half rows; shared rows 10 R + 17 (R = max half rows + 1)
+static size_t small_el_smem(int64_t nx, int64_t nh, int nb) {
+    const int64_t R = (nh + nb - 1) / nb + 1;
+    return (size_t)(10 * R + 17) * nx * sizeof(__half);
+}
+
+bool small_el2d_eligible(int64_t nx, int64_t nh, int nsm, int max_smem) {
+    if (nx % 2 != 0 || nx < 16 || nx / 2 > 1024 || nh < 6) return false;
+    const int nb = small_blocks(nh, nsm);
+    if (nb < 2) return false;
+    return small_el_smem(nx, nh, nb) <= (size_t)max_smem && small_el_smem(nx, nh, nb) <= 160 * 1024;
+}
+
+size_t small_el2d_xch_bytes(int64_t nx, int nb) { return (size_t)nb * SE_ROWS * nx * sizeof(__half); }
+
+static void* small_el_fn(int variant, int order) {
+    if (order == 2) {
+        if (variant == 0) return (void*)k_el2d_small<0, 2>;
+        if (variant == 3) return (void*)k_el2d_small<3, 2>;
+        return (void*)k_el2d_small<6, 2>;
+    }
+    if (variant == 0) return (void*)k_el2d_small<0, 4>;
+    if (variant == 3) return (void*)k_el2d_small<3, 4>;
+    return (void*)k_el2d_small<6, 4>;
+}
+
+cudaError_t small_el2d_prepare(int64_t nx, int64_t nh, int nb) {
+    const int bytes = (int)small_el_smem(nx, nh, nb);
+    for (int v : {0, 3, 6})
+        for (int o : {2, 4}) {
+            cudaError_t e = cudaFuncSetAttribute(small_el_fn(v, o), cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+            if (e != cudaSuccess) return e;
+        }
+    return cudaSuccess;
+}
+
+cudaError_t launch_el2d_small(int variant, int order, const ElParams& P, const StreamIO& IO, __half* xch,
+                              unsigned int* gbar, const double* src_dev, double* partials2, int every, int energy,
+                              int nb, int64_t nt, cudaStream_t st) {
+    SmallElParams S;
+    memset(&S, 0, sizeof(S));
+    S.P = P;
+    S.traces = IO.traces;
+    S.rec = IO.rec;
+    S.n_rec = IO.n_rec;
+    S.every = every;
+    S.energy = energy;
+    S.nt = IO.nt;
+    S.e_vals = IO.e_vals;
+    S.scale = IO.scale;
+    S.xch = xch;
+    S.gbar = gbar;
+    S.src = src_dev;
+    S.partials2 = partials2;
+    void* args[] = {(void*)&S, (void*)&nt};
+    return cudaLaunchCooperativeKernel(small_el_fn(variant, order), dim3(nb), dim3((unsigned)(P.g.nx / 2)), args,
+                                       small_el_smem(P.g.nx, P.vs.rows, nb), st);
 }
 
 }  // namespace hw

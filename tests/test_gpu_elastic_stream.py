@@ -12,6 +12,11 @@ from golden_cases import assert_same_bits
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(autouse=True)
+def _streaming_kernels(monkeypatch):  # these grids would otherwise take the persistent small-grid kernel
+    monkeypatch.setenv("HALFWAVE_SMALL", "0")
+
 LAYERS = [(0.3, 2.0, 2.0, 1.0), (0.7, 2.3, 2.8, 1.4), (1.0, 2.6, 3.2, 0.0)]
 
 
