@@ -19,7 +19,7 @@
 
 namespace hw {
 
-constexpr int ER = 4;     // ring slots (unroll factor)
+constexpr int ER = 4;     // tap ring slots
 constexpr int ED = 2;     // prefetch distance: slot of iteration i-1 stays valid during i
 constexpr int ENS = 3;    // TMA row streams per slot
 constexpr int EOWN = 6;   // own-cell row streams per slot of the 2-slot own ring (max over phases)

@@ -31,7 +31,7 @@
 namespace hw {
 
 constexpr int FCPT = 8;  // cells per thread
-constexpr int FR = 4;    // TMA ring slots (prefetch distance FR-1); also the unroll factor
+constexpr int FR = 4;    // TMA ring slots (prefetch distance FR-1)
 constexpr int NSTREAM = FUSED_NSTREAM;
 enum { S_P = 0, S_VX = 1, S_VS = 2, S_RP = 3, S_RVX = 4, S_RVS = 5 };
 
