@@ -372,6 +372,7 @@ struct hw_solver {
     // streaming phase kernels (2D elastic, binary16): in place on the standard layout
     bool el_stream = false;   // streaming 2D elastic phases
     bool ac3_stream = false;  // streaming 3D acoustic phases
+    bool fused3 = false;      // one-pass 3D acoustic step (2nd order), ping-pong A <-> B
     bool el3_stream = false;  // streaming 3D elastic phases
     int stream_blocks = 0;
     unsigned int* counter = nullptr;  // CTA arrival counter of the streaming stress kernel
@@ -722,7 +723,25 @@ int setup_handle(hw_solver* h) {
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
             h->el_stream = true;
         }
-        if (want && h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
+        // one-pass 3D acoustic step (2nd order, single domain): ping-pong partner buffers
+        const char* f3e = getenv("HALFWAVE_FUSED3");
+        if (want && !(f3e && strcmp(f3e, "0") == 0) && h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
+            h->world == 1 && h->transport == 0 &&
+            ac3d_fused_eligible(desc->nx, desc->nm, desc->ns, h->g.pitch, desc->order, dev_smem)) {
+            for (int j = 0; j < 2 * h->nsol; j++) {
+                int f = h->ext[j % h->nsol];
+                size_t bytes = (size_t)(field_rows(h, f) + 2 * G) * h->g.slab * esz;
+                if (cudaMalloc(&h->mem_b[j], bytes) != cudaSuccess) return fail(HW_ECUDA, "out of memory (B)");
+                CU(cudaMemset(h->mem_b[j], 0, bytes));
+            }
+            if (ac3d_fused_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "fused 3D kernel setup failed");
+            const int64_t units = (desc->nm / (4096 / desc->nx)) * max_rows;
+            int64_t nbs = units / 4;
+            if (nbs < 1) nbs = 1;
+            h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
+            h->fused3 = true;
+        }
+        if (want && !h->fused3 && h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
             ac3d_stream_eligible(desc->nx, desc->nm, h->g.pitch, dev_smem)) {
             if (ac3d_stream_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "streaming kernel setup failed");
             const int64_t units = (desc->nm / (4096 / desc->nx)) * max_rows;
@@ -740,7 +759,7 @@ int setup_handle(hw_solver* h) {
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
             h->el3_stream = true;
         }
-        if (h->el_stream || h->ac3_stream || h->el3_stream || h->fused) {
+        if (h->el_stream || h->ac3_stream || h->el3_stream || h->fused || h->fused3) {
             CU(cudaMalloc(&h->counter, sizeof(unsigned int)));
             CU(cudaMemset(h->counter, 0, sizeof(unsigned int)));
         }
@@ -1236,6 +1255,24 @@ static AcFusedParams fused_params(const hw_solver* h, int64_t nt) {
     return F;
 }
 
+// Field views / input pointers of the one-pass 3D kernel reading buffer `cur` (0 = A,
+// 1 = B) and writing the other one (same ghost policies: write-through periodic slabs).
+static void fused3_bufs(const hw_solver* h, int cur, AcParams& P, Ac3In& in) {
+    const int64_t ghost = (int64_t)G * h->g.slab * 2;  // bytes before row 0
+    const __half* src[2 * F_N] = {};
+    for (int j = 0; j < 2 * h->nsol; j++) {
+        const int f = h->ext[j % h->nsol];
+        void* const* rd = cur ? h->mem_b : h->mem;
+        void* const* wr = cur ? h->mem : h->mem_b;
+        FieldView& v = j < h->nsol ? (f == F_P ? P.p : f == F_VX ? P.vx : f == F_VS ? P.vs : P.vm)
+                                   : (f == F_P ? P.rp : f == F_VX ? P.rvx : f == F_VS ? P.rvs : P.rvm);
+        v.base = (char*)wr[j] + ghost;
+        src[(j < h->nsol ? 0 : F_N) + f] = (const __half*)((const char*)rd[j] + ghost);
+    }
+    in.p = src[F_P]; in.vx = src[F_VX]; in.vs = src[F_VS]; in.vm = src[F_VM];
+    in.rp = src[F_N + F_P]; in.rvx = src[F_N + F_VX]; in.rvs = src[F_N + F_VS]; in.rvm = src[F_N + F_VM];
+}
+
 static void fused_bufs(const hw_solver* h, __half* bufs[2][FUSED_NSTREAM]) {
     const int64_t ghost = (int64_t)G * h->g.slab * 2;  // bytes before row 0
     for (int j = 0; j < FUSED_NSTREAM; j++) {  // external order p vx vy rp rvx rvy == stream order
@@ -1319,6 +1356,20 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
             if ((rc = exchange_nccl_list(h, xfers_fused(h, cur)))) return rc;
         }
         if (nt > 0) CU(cudaStreamWaitEvent(h->st, h->ev_int[(nt - 1) & 1], 0));
+    } else if (h->fused3) {  // one-pass 3D kernel, ping-pong A <-> B: step n reads buffer n % 2
+        const StreamIO IO = stream_io(h, C);
+        const int sk = h->d.src_kind;
+        int cur = 0;
+        for (int64_t n = 0; n < nt; n++) {
+            AcParams P = C.A;
+            Ac3In in;
+            fused3_bufs(h, cur, P, in);
+            const int sample = energy && ((n + 1) % C.every == 0);
+            launch_ac3d_fused(variant, P, in, IO, h->stream_blocks, n, (src && sk == HW_SRC_PRESSURE) ? src[n] : 0.0,
+                              sample, (n + 1) / C.every, h->st);
+            h->launches++;
+            cur ^= 1;
+        }
     } else if (h->fused) {  // fused kernels, ping-pong A <-> B: launch L reads buffer L % 2
         AcFusedParams F = fused_params(h, nt);
         __half* bufs[2][FUSED_NSTREAM];
@@ -1363,7 +1414,7 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
 // home so buffer A is always current between calls.
 static int fused_copy_back(hw_solver* h, int64_t executed, int32_t variant) {
     const int64_t launches = h->tb2 ? (executed + 1) / 2 : executed;
-    if (!h->fused || h->small || (launches & 1) == 0) return HW_OK;  // the small-grid kernel writes A itself
+    if (!(h->fused || h->fused3) || h->small || (launches & 1) == 0) return HW_OK;  // the small-grid kernel writes A itself
     const int nf = variant == HW_NAIVE ? h->nsol : 2 * h->nsol;  // naive runs never touch residuals
     for (int j = 0; j < nf; j++) {
         int f = h->ext[j % h->nsol];
@@ -1604,7 +1655,7 @@ int64_t hw_last_launch_count(const hw_solver* h) { return h ? h->launches : 0; }
 
 const char* hw_kernel_path(const hw_solver* h) {
     if (!h) return "";
-    return (h->small || h->small_el) ? "small2d" : h->tb2 ? "fused2d-tb2" : h->fused ? "fused2d" : (h->el_stream ? "stream2d" : ((h->ac3_stream || h->el3_stream) ? "stream3d" : "generic"));
+    return (h->small || h->small_el) ? "small2d" : h->tb2 ? "fused2d-tb2" : h->fused ? "fused2d" : h->fused3 ? "fused3d" : (h->el_stream ? "stream2d" : ((h->ac3_stream || h->el3_stream) ? "stream3d" : "generic"));
 }
 
 int32_t hw_transport(const hw_solver* h) { return h ? h->transport : -1; }

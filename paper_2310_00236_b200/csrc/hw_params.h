@@ -99,6 +99,15 @@ cudaError_t ac3d_stream_prepare(int64_t nx);
 void launch_ac3d_vel_stream(int variant, int order, const AcParams& P, int nblocks, int64_t n, cudaStream_t st);
 void launch_ac3d_pres_stream(int variant, int order, const AcParams& P, const StreamIO& IO, int nblocks, int64_t n,
                              double src, int sample, int64_t eidx, cudaStream_t st);
+// one-pass 3D acoustic step, 2nd order (hw_acoustic3d_fused.cu): state n read from these
+// buffers (A), state n+1 written through the AcParams field views (B)
+struct Ac3In {
+    const __half *p, *vx, *vs, *vm, *rp, *rvx, *rvs, *rvm;
+};
+bool ac3d_fused_eligible(int64_t nx, int64_t nm, int64_t ns, int64_t pitch, int order, int max_smem);
+cudaError_t ac3d_fused_prepare(int64_t nx);
+void launch_ac3d_fused(int variant, const AcParams& P, const Ac3In& in, const StreamIO& IO, int nblocks, int64_t n,
+                       double src, int sample, int64_t eidx, cudaStream_t st);
 // streaming 3D elastic phase kernels (hw_elastic3d_stream.cu)
 bool el3d_stream_eligible(int64_t nx, int64_t nm, int64_t pitch, int max_smem);
 cudaError_t el3d_stream_prepare(int64_t nx);

@@ -13,6 +13,12 @@ from golden_cases import assert_same_bits
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _two_phase(monkeypatch):
+    """2nd-order single-domain cases would take the one-pass kernel (test_gpu_acoustic3d_fused.py)."""
+    monkeypatch.setenv("HALFWAVE_FUSED3", "0")
+
+
 def _case(nx, ny, nz, nt, *, order=2, full=True, slabs=1, amp=5.0, seed=0, recs=None):
     rng = np.random.default_rng(seed)
     if full:

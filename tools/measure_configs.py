@@ -17,6 +17,8 @@ CPU = "--cpu" in sys.argv
 ARGS = [a for a in sys.argv[1:] if a != "--cpu"]
 NT = int(ARGS[0]) if len(ARGS) > 0 else 50
 F16 = hw.Precision.FP16
+_PEAKS = ROOT / "MEASURED_PEAKS.json"
+PEAK_GBS = json.loads(_PEAKS.read_text())["hbm_gbs"] if _PEAKS.exists() else 6551.7  # measured copy GB/s
 
 
 def cpu_rate(s, variant, cells, steps):
@@ -44,7 +46,8 @@ def timed(name, s, variant, bytes_per_cell, cells, nt=NT, cpu_steps=2):
     rate = cells * nt / (ms / 1e3)
     line = {"config": name, "cell_steps_per_s": rate, "us_per_step": 1e3 * ms / nt,
             "B_alg": bytes_per_cell, "GBps": rate * bytes_per_cell / 1e9,
-            "frac_of_6551": rate * bytes_per_cell / 6551.7e9, "launches": s.last_launch_count()}
+            "frac_of_peak": rate * bytes_per_cell / (PEAK_GBS * 1e9), "peak_GBps": PEAK_GBS,
+            "path": s.kernel_path(), "launches": s.last_launch_count()}
     if CPU:
         cr, cores, steps = cpu_rate(s, variant, cells, cpu_steps)
         line["cpu_port_cell_steps_per_s"] = cr
