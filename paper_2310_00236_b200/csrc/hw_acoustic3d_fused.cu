@@ -69,12 +69,11 @@ static size_t f3_bytes(int64_t nx) {
     return 128 + (size_t)rows * nx * sizeof(__half);
 }
 
-// one finished velocity pair: row-uniform reciprocal or the generic plane path
+// one finished velocity row: row-uniform reciprocal rc (prefetched) or the generic plane path
 template <int V>
-__device__ __forceinline__ void f3_finish_v(const E8& a, bool rm, const PlaneView& rho, int64_t s, int64_t m, int x,
-                                            __half dt, __half2 dt2, __half zero_h, E8& v, E8& rr) {
+__device__ __forceinline__ void f3_finish_v(const E8& a, bool rm, float rc, const PlaneView& rho, int64_t s, int64_t m,
+                                            int x, __half dt, __half2 dt2, __half zero_h, E8& v, E8& rr) {
     if (rm) {
-        const float rc = e_rcp_at(rho, s, m);
 #pragma unroll
         for (int h = 0; h < 4; h++) e_finish_rc<V>(a.q[h], rc, dt2, -1, zero_h, v.q[h], rr.q[h]);
     } else {
@@ -171,12 +170,20 @@ __global__ void __launch_bounds__(F3T, 1)
                 fence_proxy_async_smem();
                 issue(i + FD);
             }
+            // row-uniform reciprocals of slab s = F - 1, loaded before the waits (latency off the chain)
+            const int sw = F0 + i - 1 < 0 ? ns - 1 : F0 + i - 1;  // periodic: v_slow(-1) is row ns - 1's medium
+            float rcx = 0.f, rcs = 0.f, rcm = 0.f, rch = 0.f;
+            if (rm && i > 0) {
+                rcs = e_rcp_at(P.rho_s, sw, m);
+                rcx = e_rcp_at(P.rho_x, sw, m);
+                rcm = e_rcp_at(P.rho_m, sw, m);
+                rch = e_rcp_at(P.rho_m, sw, mh);
+            }
             mbar_wait(&L.bar[k], (uint32_t)(((gi0 + i) / FR) & 1));
             qp0 = qp1;
             qp1 = e_ld8(L.sl(k) + (int64_t)(j + 1) * pitch + x);
             if (i > 0) {
                 const int s = F0 + i - 1, kr = i - 1, os = (gk0 + kr) & 1;
-                const int sw = s < 0 ? ns - 1 : s;  // medium row of v_slow(sb - 1) in the warm-up iteration
                 if (tid == 0 && s + 1 < se) {  // that own slot was last read before the previous barrier
                     fence_proxy_async_smem();
                     issue_own(kr + 1);
@@ -186,13 +193,13 @@ __global__ void __launch_bounds__(F3T, 1)
                 // v_slow(s) from p rows s, s+1 (acoustic.py:169-170, to-half shifts (0, 1))
                 E8 vsn = e_ld8(L.ob(os, O_VS) + ro);
                 E8 rvs = comp ? e_ld8(L.ob(os, O_RVS) + ro) : E8{};
-                f3_finish_v<V>(e_sfold<2>(c, qp0, qp0, qp1, qp1), rm, P.rho_s, sw, m, x, dt, dt2, zero_h, vsn, rvs);
+                f3_finish_v<V>(e_sfold<2>(c, qp0, qp0, qp1, qp1), rm, rcs, P.rho_s, sw, m, x, dt, dt2, zero_h, vsn, rvs);
                 if (i > 1) {
                     const __half* pt = L.sl(kp);  // p tile of slab s: row m at index j + 1
                     // vx(s) = fl(fl(ddx p / rho_x) dt) (acoustic.py:167-168)
                     E8 vxn = e_ld8(L.ob(os, O_VX) + ro);
                     E8 rvx = comp ? e_ld8(L.ob(os, O_RVX) + ro) : E8{};
-                    f3_finish_v<V>(e_xfold<2>(c, pt + (int64_t)(j + 1) * pitch, x, xl, xr, false), rm, P.rho_x, s, m,
+                    f3_finish_v<V>(e_xfold<2>(c, pt + (int64_t)(j + 1) * pitch, x, xl, xr, false), rm, rcx, P.rho_x, s, m,
                                    x, dt, dt2, zero_h, vxn, rvx);
                     e_st8(L.xv + ro, vxn);
                     // vm(s) rows m (and m0-1 for j == 0) from p mid rows r, r+1
@@ -201,7 +208,7 @@ __global__ void __launch_bounds__(F3T, 1)
                         const E8 a = e_ld8(t), b = e_ld8(t + pitch);
                         E8 vmn = e_ld8(L.ovm(os) + ro + pitch);
                         E8 rvm = comp ? e_ld8(L.orvm(os) + ro + pitch) : E8{};
-                        f3_finish_v<V>(e_sfold<2>(c, a, a, b, b), rm, P.rho_m, s, m, x, dt, dt2, zero_h, vmn, rvm);
+                        f3_finish_v<V>(e_sfold<2>(c, a, a, b, b), rm, rcm, P.rho_m, s, m, x, dt, dt2, zero_h, vmn, rvm);
                         e_st8(L.vmn + ro + pitch, vmn);
                         e_store_row(P.vm, slab, s, (int)off, vmn);
                         e_track(acc[3], vmn);
@@ -215,7 +222,7 @@ __global__ void __launch_bounds__(F3T, 1)
                         const E8 a = e_ld8(t), b = e_ld8(t + pitch);
                         E8 vmh = e_ld8(L.ovm(os) + x);
                         E8 rvh = comp ? e_ld8(L.orvm(os) + x) : E8{};
-                        f3_finish_v<V>(e_sfold<2>(c, a, a, b, b), rm, P.rho_m, s, mh, x, dt, dt2, zero_h, vmh, rvh);
+                        f3_finish_v<V>(e_sfold<2>(c, a, a, b, b), rm, rch, P.rho_m, s, mh, x, dt, dt2, zero_h, vmh, rvh);
                         e_st8(L.vmn + x, vmh);
                     }
                     e_store_row(P.vx, slab, s, (int)off, vxn);
