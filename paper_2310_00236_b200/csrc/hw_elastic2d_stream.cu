@@ -120,8 +120,13 @@ __global__ void __launch_bounds__(512, 1) k_el2d_vel_stream(ElParams P, StreamIO
                     fence_proxy_async_smem();
                     issue(i + ED);
                 }
-                mbar_wait(&R.bar[u], par);
                 const int r = F0 + i - 2;
+                float rcx = 0.f, rcs = 0.f;  // row reciprocals, loaded before the waits (latency off the chain)
+                if (RM && r >= y0 && r < y1) {
+                    if (r < P.vx.rows) rcx = __ldg(P.rho_x.rcp + r * P.rho_x.ss);
+                    if (r < P.vs.rows) rcs = __ldg(P.rho_s.rcp + r * P.rho_s.ss);
+                }
+                mbar_wait(&R.bar[u], par);
                 ssq[0] = ssq[1]; ssq[1] = ssq[2]; ssq[2] = ssq[3];  // queue rows F-3..F
                 ssq[3] = e_ld8(R.row(u, 0) + x);
                 xsq[0] = xsq[1]; xsq[1] = xsq[2]; xsq[2] = xsq[3];  // queue rows F-4..F-1
@@ -140,10 +145,9 @@ __global__ void __launch_bounds__(512, 1) k_el2d_vel_stream(ElParams P, StreamIO
                         E8 v = e_ld8(R.orow(kr & 1, 0) + x);
                         E8 rr = comp ? e_ld8(R.orow(kr & 1, 2) + x) : E8{};
                         if constexpr (RM) {
-                            const float rc = __ldg(P.rho_x.rcp + r * P.rho_x.ss);
 #pragma unroll
                             for (int j = 0; j < 4; j++)
-                                e_finish_rc<V>(EO2::add(a.q[j], d.q[j]), rc, dt2, -1, srch, v.q[j], rr.q[j]);
+                                e_finish_rc<V>(EO2::add(a.q[j], d.q[j]), rcx, dt2, -1, srch, v.q[j], rr.q[j]);
                         } else {
 #pragma unroll
                             for (int j = 0; j < 4; j++)
@@ -166,10 +170,9 @@ __global__ void __launch_bounds__(512, 1) k_el2d_vel_stream(ElParams P, StreamIO
                         E8 v = e_ld8(R.orow(kr & 1, 1) + x);
                         E8 rr = comp ? e_ld8(R.orow(kr & 1, 3) + x) : E8{};
                         if constexpr (RM) {
-                            const float rc = __ldg(P.rho_s.rcp + r * P.rho_s.ss);
 #pragma unroll
                             for (int j = 0; j < 4; j++)
-                                e_finish_rc<V>(EO2::add(a.q[j], d.q[j]), rc, dt2, (sk && j == sj) ? sl : -1, srch,
+                                e_finish_rc<V>(EO2::add(a.q[j], d.q[j]), rcs, dt2, (sk && j == sj) ? sl : -1, srch,
                                                v.q[j], rr.q[j]);
                         } else {
 #pragma unroll

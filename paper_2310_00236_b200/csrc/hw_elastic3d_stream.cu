@@ -49,10 +49,13 @@ __device__ __forceinline__ void e3_init(const E3Layout& L) {
     __syncthreads();
 }
 
-// fold of 4 consecutive rows of a tile (mid taps) at the thread's cells
+// fold of 4 consecutive rows t0 .. t0+3 of a tile (mid taps) at the thread's cells; 2nd
+// order reads only the inner pair (t0 may then lie one row before the tile)
 template <int ORDER>
 __device__ __forceinline__ E8 e3_mfold(const __half c[4], const __half* t0, int64_t pitch) {
-    return e_sfold<ORDER>(c, e_ld8(t0), e_ld8(t0 + pitch), e_ld8(t0 + 2 * pitch), e_ld8(t0 + 3 * pitch));
+    const E8 b = e_ld8(t0 + pitch), d = e_ld8(t0 + 2 * pitch);
+    if (ORDER == 2) return e_sfold<2>(c, b, b, d, d);
+    return e_sfold<ORDER>(c, e_ld8(t0), b, d, e_ld8(t0 + 3 * pitch));
 }
 
 __device__ __forceinline__ E8 e3_add(const E8& a, const E8& b) {
@@ -70,7 +73,8 @@ __device__ __forceinline__ void e3_shift(E8 q[4], const E8& v) {
 }
 
 // ---------------------------------------------------------------- velocity phase
-// slot rows: [sss(F) TM | sxs(F-1) TM | sms tile(F-1) TM+4 | sxx(s) TM | sxm tile(s) TM+4 | smm tile(s) TM+4]
+// slot rows: [sss(F) TM | sxs(F-1) TM | sms tile(F-1) TM+2H | sxx(s) TM | sxm tile(s) TM+2H | smm tile(s) TM+2H]
+// (tiles: mid rows m0-H .. m0+TM+H-1, H = ORDER/2 halo rows each side; row m at index j + H)
 template <int V, int ORDER>
 __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t n, double src) {
     e_pdl_enter();
@@ -79,8 +83,9 @@ __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t 
     const int nx = (int)P.g.nx, nm = (int)P.g.nm, ns = (int)P.vx.rows;
     const int64_t pitch = P.g.pitch, slab = P.g.slab;
     const int TM = E3T * ECPT / nx, TPR = nx / ECPT;
-    const E3Layout L(smem, 6 * TM + 12, TM, pitch, 6);
-    const int o_sxs = TM, o_sms = 2 * TM, o_sxx = 3 * TM + 4, o_sxm = 4 * TM + 4, o_smm = 5 * TM + 8;
+    constexpr int H = ORDER / 2;
+    const E3Layout L(smem, 6 * TM + 6 * H, TM, pitch, 6);
+    const int o_sxs = TM, o_sms = 2 * TM, o_sxx = 3 * TM + 2 * H, o_sxm = 4 * TM + 2 * H, o_smm = 5 * TM + 4 * H;
     const int tid = threadIdx.x, j = tid / TPR, x = (tid % TPR) * ECPT;
     constexpr bool comp = V != 0;
     constexpr int NOWN = comp ? 6 : 3;  // vx vs vm [rvx rvs rvm]
@@ -126,13 +131,13 @@ __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t 
             const int F = F0 + i, k = (gi0 + i) % QR;
             __half* d = L.sl(k);
             const int64_t mo = (int64_t)m0 * pitch;
-            mbar_arrive_expect_tx(&L.bar[k], (uint32_t)((6 * TM + 12) * pitch * sizeof(__half)));
+            mbar_arrive_expect_tx(&L.bar[k], (uint32_t)((6 * TM + 6 * H) * pitch * sizeof(__half)));
             tma_load_1d(d, SSS + e_row(F) * slab + mo, tmb, &L.bar[k]);
             tma_load_1d(d + o_sxs * pitch, SXS + e_row(F - 1) * slab + mo, tmb, &L.bar[k]);
-            a3_rows(d + o_sms * pitch, SMS, slab, e_row(F - 1), m0 - 2, m0 + TM + 2, nm, pitch, &L.bar[k]);
+            a3_rows(d + o_sms * pitch, SMS, slab, e_row(F - 1), m0 - H, m0 + TM + H, nm, pitch, &L.bar[k]);
             tma_load_1d(d + o_sxx * pitch, SXX + e_row(F - 2) * slab + mo, tmb, &L.bar[k]);
-            a3_rows(d + o_sxm * pitch, SXM, slab, e_row(F - 2), m0 - 2, m0 + TM + 2, nm, pitch, &L.bar[k]);
-            a3_rows(d + o_smm * pitch, SMM, slab, e_row(F - 2), m0 - 2, m0 + TM + 2, nm, pitch, &L.bar[k]);
+            a3_rows(d + o_sxm * pitch, SXM, slab, e_row(F - 2), m0 - H, m0 + TM + H, nm, pitch, &L.bar[k]);
+            a3_rows(d + o_smm * pitch, SMM, slab, e_row(F - 2), m0 - H, m0 + TM + H, nm, pitch, &L.bar[k]);
         };
         auto issue_own = [&](int kk) {
             const int os = (gk0 + kk) & 1;
@@ -153,14 +158,20 @@ __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t 
                 fence_proxy_async_smem();
                 issue(i + QD);
             }
+            const int s = F0 + i - 2;
+            float rcx = 0.f, rcs = 0.f, rcm = 0.f;  // row reciprocals, loaded before the waits
+            if (rm && s >= sb) {
+                rcx = e_rcp_at(P.rho_x, s, m);
+                rcs = e_rcp_at(P.rho_s, s, m);
+                rcm = e_rcp_at(P.rho_m, s, m);
+            }
             mbar_wait(&L.bar[k], (uint32_t)(((gi0 + i) / QR) & 1));
             const __half* d = L.sl(k);
             const __half* pd = L.sl(kp);  // slab F-2 = s rows / tiles of the delayed streams
             const int64_t jr = (int64_t)j * pitch;
             e3_shift(qss, e_ld8(d + jr + x));
             e3_shift(qxs, e_ld8(d + o_sxs * pitch + jr + x));
-            e3_shift(qms, e_ld8(d + o_sms * pitch + jr + 2 * pitch + x));
-            const int s = F0 + i - 2;
+            e3_shift(qms, e_ld8(d + o_sms * pitch + jr + H * pitch + x));
             if (s >= sb) {
                 const int kr = s - sb, os = (gk0 + kr) & 1;
                 if (tid == 0 && s + 1 < se) {
@@ -178,11 +189,10 @@ __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t 
                 // vx: fl(fl(ddx sxx + dds sxs) + ddm sxm) (elastic.py:191-194 + mid term)
                 E8 a = e_xfold<ORDER>(c, d + o_sxx * pitch + jr, x, xl, xr, false);
                 a = e3_add(a, e_sfold<ORDER>(c, qxs[0], qxs[1], qxs[2], qxs[3]));
-                a = e3_add(a, e3_mfold<ORDER>(c, d + o_sxm * pitch + jr + x, pitch));
+                a = e3_add(a, e3_mfold<ORDER>(c, d + o_sxm * pitch + jr + (H - 2) * pitch + x, pitch));
                 if (rm) {
-                    const float rc = e_rcp_at(P.rho_x, s, m);
 #pragma unroll
-                    for (int h = 0; h < 4; h++) e_finish_rc<V>(a.q[h], rc, dt2, -1, srch, v[0].q[h], rr[0].q[h]);
+                    for (int h = 0; h < 4; h++) e_finish_rc<V>(a.q[h], rcx, dt2, -1, srch, v[0].q[h], rr[0].q[h]);
                 } else {
 #pragma unroll
                     for (int h = 0; h < 4; h++)
@@ -191,13 +201,12 @@ __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t 
                 // v_slow: fl(fl(ddx sxs + dds sss) + ddm sms) (+ src) (elastic.py:196-205)
                 a = e_xfold<ORDER>(c, pd + o_sxs * pitch + jr, x, xl, xr, true);
                 a = e3_add(a, e_sfold<ORDER>(c, qss[0], qss[1], qss[2], qss[3]));
-                a = e3_add(a, e3_mfold<ORDER>(c, pd + o_sms * pitch + jr + x, pitch));
+                a = e3_add(a, e3_mfold<ORDER>(c, pd + o_sms * pitch + jr + (H - 2) * pitch + x, pitch));
                 const bool sk = src_col && s == P.src_s && m == P.src_m;
                 if (rm) {
-                    const float rc = e_rcp_at(P.rho_s, s, m);
 #pragma unroll
                     for (int h = 0; h < 4; h++)
-                        e_finish_rc<V>(a.q[h], rc, dt2, (sk && h == sj) ? sln : -1, srch, v[1].q[h], rr[1].q[h]);
+                        e_finish_rc<V>(a.q[h], rcs, dt2, (sk && h == sj) ? sln : -1, srch, v[1].q[h], rr[1].q[h]);
                 } else {
 #pragma unroll
                     for (int h = 0; h < 4; h++)
@@ -205,13 +214,12 @@ __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t 
                                           v[1].q[h], rr[1].q[h]);
                 }
                 // v_mid: fl(fl(ddx sxm + dds sms) + ddm smm)
-                a = e_xfold<ORDER>(c, d + o_sxm * pitch + jr + 2 * pitch, x, xl, xr, true);
+                a = e_xfold<ORDER>(c, d + o_sxm * pitch + jr + H * pitch, x, xl, xr, true);
                 a = e3_add(a, e_sfold<ORDER>(c, qms[0], qms[1], qms[2], qms[3]));
-                a = e3_add(a, e3_mfold<ORDER>(c, d + o_smm * pitch + jr + pitch + x, pitch));
+                a = e3_add(a, e3_mfold<ORDER>(c, d + o_smm * pitch + jr + (H - 1) * pitch + x, pitch));
                 if (rm) {
-                    const float rc = e_rcp_at(P.rho_m, s, m);
 #pragma unroll
-                    for (int h = 0; h < 4; h++) e_finish_rc<V>(a.q[h], rc, dt2, -1, srch, v[2].q[h], rr[2].q[h]);
+                    for (int h = 0; h < 4; h++) e_finish_rc<V>(a.q[h], rcm, dt2, -1, srch, v[2].q[h], rr[2].q[h]);
                 } else {
 #pragma unroll
                     for (int h = 0; h < 4; h++)
@@ -242,7 +250,7 @@ __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t 
 }
 
 // ---------------------------------------------------------------- stress phase
-// slot rows: [vx(F) TM | vm(F) TM | vs tile(F-1) TM+4 | vx tile(s) TM+4 | vm tile(s) TM+4]
+// slot rows: [vx(F) TM | vm(F) TM | vs tile(F-1) TM+2H | vx tile(s) TM+2H | vm tile(s) TM+2H]
 template <int V, int ORDER>
 __global__ void __launch_bounds__(E3T, 1)
     k_el3d_stress_stream(ElParams P, StreamIO IO, int64_t n, double src, int sample, int64_t eidx) {
@@ -252,8 +260,9 @@ __global__ void __launch_bounds__(E3T, 1)
     const int nx = (int)P.g.nx, nm = (int)P.g.nm, ns = (int)P.sxx.rows;
     const int64_t pitch = P.g.pitch, slab = P.g.slab;
     const int TM = E3T * ECPT / nx, TPR = nx / ECPT;
-    const E3Layout L(smem, 5 * TM + 12, TM, pitch, 12);
-    const int o_vm = TM, o_vs = 2 * TM, o_vxt = 3 * TM + 4, o_vmt = 4 * TM + 8;
+    constexpr int H = ORDER / 2;
+    const E3Layout L(smem, 5 * TM + 6 * H, TM, pitch, 12);
+    const int o_vm = TM, o_vs = 2 * TM, o_vxt = 3 * TM + 2 * H, o_vmt = 4 * TM + 4 * H;
     const int tid = threadIdx.x, j = tid / TPR, x = (tid % TPR) * ECPT;
     constexpr bool comp = V != 0;
     constexpr int NOWN = comp ? 12 : 6;  // sxx sss smm sxs sxm sms [residuals]
@@ -296,12 +305,12 @@ __global__ void __launch_bounds__(E3T, 1)
             const int F = F0 + i, k = (gi0 + i) % QR;
             __half* d = L.sl(k);
             const int64_t mo = (int64_t)m0 * pitch;
-            mbar_arrive_expect_tx(&L.bar[k], (uint32_t)((5 * TM + 12) * pitch * sizeof(__half)));
+            mbar_arrive_expect_tx(&L.bar[k], (uint32_t)((5 * TM + 6 * H) * pitch * sizeof(__half)));
             tma_load_1d(d, VX + e_row(F) * slab + mo, tmb, &L.bar[k]);
             tma_load_1d(d + o_vm * pitch, VM + e_row(F) * slab + mo, tmb, &L.bar[k]);
-            a3_rows(d + o_vs * pitch, VS, slab, e_row(F - 1), m0 - 2, m0 + TM + 2, nm, pitch, &L.bar[k]);
-            a3_rows(d + o_vxt * pitch, VX, slab, e_row(F - 2), m0 - 2, m0 + TM + 2, nm, pitch, &L.bar[k]);
-            a3_rows(d + o_vmt * pitch, VM, slab, e_row(F - 2), m0 - 2, m0 + TM + 2, nm, pitch, &L.bar[k]);
+            a3_rows(d + o_vs * pitch, VS, slab, e_row(F - 1), m0 - H, m0 + TM + H, nm, pitch, &L.bar[k]);
+            a3_rows(d + o_vxt * pitch, VX, slab, e_row(F - 2), m0 - H, m0 + TM + H, nm, pitch, &L.bar[k]);
+            a3_rows(d + o_vmt * pitch, VM, slab, e_row(F - 2), m0 - H, m0 + TM + H, nm, pitch, &L.bar[k]);
         };
         auto issue_own = [&](int kk) {
             const int os = (gk0 + kk) & 1;
@@ -328,7 +337,7 @@ __global__ void __launch_bounds__(E3T, 1)
             const int64_t jr = (int64_t)j * pitch;
             e3_shift(qvx, e_ld8(d + jr + x));
             e3_shift(qvm, e_ld8(d + o_vm * pitch + jr + x));
-            e3_shift(qvs, e_ld8(d + o_vs * pitch + jr + 2 * pitch + x));
+            e3_shift(qvs, e_ld8(d + o_vs * pitch + jr + H * pitch + x));
             const int s = F0 + i - 2;
             if (s >= sb) {
                 const int kr = s - sb, os = (gk0 + kr) & 1;
@@ -338,9 +347,10 @@ __global__ void __launch_bounds__(E3T, 1)
                 }
                 mbar_wait(&L.obar[os], (uint32_t)(((gk0 + kr) >> 1) & 1));
                 const int64_t ro = jr + x, off = (int64_t)m * pitch + x;
-                const __half* vxt = d + o_vxt * pitch + jr;  // vx tile rows m-2 .. (row j+2 = m)
-                const __half* vmt = d + o_vmt * pitch + jr;
-                const __half* vst = pd + o_vs * pitch + jr;
+                // tile row pointers at row m - 2 (row m at index j + H; 2nd order never reads m - 2)
+                const __half* vxt = d + o_vxt * pitch + jr + (H - 2) * pitch;
+                const __half* vmt = d + o_vmt * pitch + jr + (H - 2) * pitch;
+                const __half* vst = pd + o_vs * pitch + jr + (H - 2) * pitch;
                 // normal stresses from dvx, dvs, dvm (to-int taps)
                 const E8 dvx = e_xfold<ORDER>(c, vxt + 2 * pitch, x, xl, xr, true);
                 const E8 dvs = e_sfold<ORDER>(c, qvs[0], qvs[1], qvs[2], qvs[3]);
@@ -482,27 +492,28 @@ __global__ void __launch_bounds__(E3T, 1)
 
 // ---------------------------------------------------------------- host side
 
-static size_t e3_vel_bytes(int64_t nx) {
-    const int64_t TM = E3T * ECPT / nx;
-    return 128 + ((size_t)QR * (6 * TM + 12) + 2 * 6 * TM) * nx * sizeof(__half);
+static size_t e3_vel_bytes(int64_t nx, int order) {
+    const int64_t TM = E3T * ECPT / nx, H = order / 2;
+    return 128 + ((size_t)QR * (6 * TM + 6 * H) + 2 * 6 * TM) * nx * sizeof(__half);
 }
-static size_t e3_stress_bytes(int64_t nx) {
-    const int64_t TM = E3T * ECPT / nx;
-    return 128 + ((size_t)QR * (5 * TM + 12) + 2 * 12 * TM) * nx * sizeof(__half);
+static size_t e3_stress_bytes(int64_t nx, int order) {
+    const int64_t TM = E3T * ECPT / nx, H = order / 2;
+    return 128 + ((size_t)QR * (5 * TM + 6 * H) + 2 * 12 * TM) * nx * sizeof(__half);
 }
 
 bool el3d_stream_eligible(int64_t nx, int64_t nm, int64_t pitch, int max_smem) {
     if (nx % 256 != 0 || nx > E3T * ECPT || pitch != nx) return false;
     const int64_t TM = E3T * ECPT / nx;
     if (nm % TM != 0) return false;
-    return e3_vel_bytes(nx) <= (size_t)max_smem && e3_stress_bytes(nx) <= (size_t)max_smem;
+    return e3_vel_bytes(nx, 4) <= (size_t)max_smem && e3_stress_bytes(nx, 4) <= (size_t)max_smem;
 }
 
 template <int V, int O>
 static void e3_attrs(int64_t nx) {
-    cudaFuncSetAttribute((void*)k_el3d_vel_stream<V, O>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e3_vel_bytes(nx));
+    cudaFuncSetAttribute((void*)k_el3d_vel_stream<V, O>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)e3_vel_bytes(nx, O));
     cudaFuncSetAttribute((void*)k_el3d_stress_stream<V, O>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)e3_stress_bytes(nx));
+                         (int)e3_stress_bytes(nx, O));
 }
 
 cudaError_t el3d_stream_prepare(int64_t nx) {
@@ -541,7 +552,7 @@ void launch_el3d_vel_stream(int variant, int order, const ElParams& P, int nbloc
     void* fn = nullptr;
     E3_DISPATCH(variant, order, (fn = (void*)k_el3d_vel_stream<V_, O_>))
     void* args[] = {(void*)&P, (void*)&n, (void*)&src};
-    e3_launch(fn, nblocks, e3_vel_bytes(P.g.nx), st, args);
+    e3_launch(fn, nblocks, e3_vel_bytes(P.g.nx, order), st, args);
 }
 
 void launch_el3d_stress_stream(int variant, int order, const ElParams& P, const StreamIO& IO, int nblocks, int64_t n,
@@ -549,7 +560,7 @@ void launch_el3d_stress_stream(int variant, int order, const ElParams& P, const 
     void* fn = nullptr;
     E3_DISPATCH(variant, order, (fn = (void*)k_el3d_stress_stream<V_, O_>))
     void* args[] = {(void*)&P, (void*)&IO, (void*)&n, (void*)&src, (void*)&sample, (void*)&eidx};
-    e3_launch(fn, nblocks, e3_stress_bytes(P.g.nx), st, args);
+    e3_launch(fn, nblocks, e3_stress_bytes(P.g.nx, order), st, args);
 }
 
 }  // namespace hw
