@@ -373,6 +373,7 @@ struct hw_solver {
     bool el_stream = false;   // streaming 2D elastic phases
     bool ac3_stream = false;  // streaming 3D acoustic phases
     bool fused3 = false;      // one-pass 3D acoustic step (2nd order), ping-pong A <-> B
+    bool fused_el = false;    // one-pass 2D elastic step, ping-pong A <-> B
     bool el3_stream = false;  // streaming 3D elastic phases
     int stream_blocks = 0;
     unsigned int* counter = nullptr;  // CTA arrival counter of the streaming stress kernel
@@ -715,7 +716,23 @@ int setup_handle(hw_solver* h) {
             CU(cudaMalloc(&h->partials2, (size_t)h->small_nb * NCOMP * sizeof(double)));
             h->small_el = true;
         }
-        if (want && !h->small_el && !h->ac && !h->d3 && h->LS == 16 && h->LU == 16 &&
+        // one-pass 2D elastic step (single domain): ping-pong partner buffers
+        const char* fee = getenv("HALFWAVE_FUSED_EL");
+        if (want && !h->small_el && !(fee && strcmp(fee, "0") == 0) && !h->ac && !h->d3 && h->LS == 16 &&
+            h->LU == 16 && h->world == 1 && h->transport == 0 && el2d_fused_eligible(desc->nx, desc->ns, dev_smem)) {
+            for (int j = 0; j < 2 * h->nsol; j++) {
+                int f = h->ext[j % h->nsol];
+                size_t bytes = (size_t)(field_rows(h, f) + 2 * G) * h->g.slab * esz;
+                if (cudaMalloc(&h->mem_b[j], bytes) != cudaSuccess) return fail(HW_ECUDA, "out of memory (B)");
+                CU(cudaMemset(h->mem_b[j], 0, bytes));
+            }
+            if (el2d_fused_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "fused elastic kernel setup failed");
+            int64_t nbs = max_rows / 4;
+            if (nbs < 1) nbs = 1;
+            h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
+            h->fused_el = true;
+        }
+        if (want && !h->small_el && !h->fused_el && !h->ac && !h->d3 && h->LS == 16 && h->LU == 16 &&
             el2d_stream_eligible(desc->nx, desc->ns, dev_smem)) {
             if (el2d_stream_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "streaming kernel setup failed");
             int64_t nbs = max_rows / 4;
@@ -759,7 +776,7 @@ int setup_handle(hw_solver* h) {
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
             h->el3_stream = true;
         }
-        if (h->el_stream || h->ac3_stream || h->el3_stream || h->fused || h->fused3) {
+        if (h->el_stream || h->ac3_stream || h->el3_stream || h->fused || h->fused3 || h->fused_el) {
             CU(cudaMalloc(&h->counter, sizeof(unsigned int)));
             CU(cudaMemset(h->counter, 0, sizeof(unsigned int)));
         }
@@ -1273,6 +1290,19 @@ static void fused3_bufs(const hw_solver* h, int cur, AcParams& P, Ac3In& in) {
     in.rp = src[F_N + F_P]; in.rvx = src[F_N + F_VX]; in.rvs = src[F_N + F_VS]; in.rvm = src[F_N + F_VM];
 }
 
+// The same for the one-pass 2D elastic kernel (external order vx vy sxx syy sxy + residuals).
+static void fused_el_bufs(const hw_solver* h, int cur, ElParams& P, El2In& in) {
+    const int64_t ghost = (int64_t)G * h->g.slab * 2;  // bytes before row 0
+    void* const* rd = cur ? h->mem_b : h->mem;
+    void* const* wr = cur ? h->mem : h->mem_b;
+    FieldView* out[10] = {&P.vx, &P.vs, &P.sxx, &P.sss, &P.sxs, &P.rvx, &P.rvs, &P.rsxx, &P.rsss, &P.rsxs};
+    const __half** src[10] = {&in.vx, &in.vs, &in.sxx, &in.sss, &in.sxs, &in.rvx, &in.rvs, &in.rsxx, &in.rsss, &in.rsxs};
+    for (int j = 0; j < 10; j++) {  // EXT_EL2 = vx vs sxx sss sxs: slot j holds field j (j % 5)
+        out[j]->base = (char*)wr[j] + ghost;
+        *src[j] = (const __half*)((const char*)rd[j] + ghost);
+    }
+}
+
 static void fused_bufs(const hw_solver* h, __half* bufs[2][FUSED_NSTREAM]) {
     const int64_t ghost = (int64_t)G * h->g.slab * 2;  // bytes before row 0
     for (int j = 0; j < FUSED_NSTREAM; j++) {  // external order p vx vy rp rvx rvy == stream order
@@ -1370,6 +1400,19 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
             h->launches++;
             cur ^= 1;
         }
+    } else if (h->fused_el) {  // one-pass 2D elastic kernel, ping-pong A <-> B: step n reads buffer n % 2
+        const StreamIO IO = stream_io(h, C);
+        int cur = 0;
+        for (int64_t n = 0; n < nt; n++) {
+            ElParams P = C.L;
+            El2In in;
+            fused_el_bufs(h, cur, P, in);
+            const int sample = energy && ((n + 1) % C.every == 0);
+            launch_el2d_fused(variant, h->d.order, P, in, IO, h->stream_blocks, n, src ? src[n] : 0.0, sample,
+                              (n + 1) / C.every, h->st);
+            h->launches++;
+            cur ^= 1;
+        }
     } else if (h->fused) {  // fused kernels, ping-pong A <-> B: launch L reads buffer L % 2
         AcFusedParams F = fused_params(h, nt);
         __half* bufs[2][FUSED_NSTREAM];
@@ -1414,7 +1457,7 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
 // home so buffer A is always current between calls.
 static int fused_copy_back(hw_solver* h, int64_t executed, int32_t variant) {
     const int64_t launches = h->tb2 ? (executed + 1) / 2 : executed;
-    if (!(h->fused || h->fused3) || h->small || (launches & 1) == 0) return HW_OK;  // the small-grid kernel writes A itself
+    if (!(h->fused || h->fused3 || h->fused_el) || h->small || (launches & 1) == 0) return HW_OK;  // the small-grid kernel writes A itself
     const int nf = variant == HW_NAIVE ? h->nsol : 2 * h->nsol;  // naive runs never touch residuals
     for (int j = 0; j < nf; j++) {
         int f = h->ext[j % h->nsol];
@@ -1655,7 +1698,7 @@ int64_t hw_last_launch_count(const hw_solver* h) { return h ? h->launches : 0; }
 
 const char* hw_kernel_path(const hw_solver* h) {
     if (!h) return "";
-    return (h->small || h->small_el) ? "small2d" : h->tb2 ? "fused2d-tb2" : h->fused ? "fused2d" : h->fused3 ? "fused3d" : (h->el_stream ? "stream2d" : ((h->ac3_stream || h->el3_stream) ? "stream3d" : "generic"));
+    return (h->small || h->small_el) ? "small2d" : h->tb2 ? "fused2d-tb2" : h->fused ? "fused2d" : h->fused3 ? "fused3d" : h->fused_el ? "fused2d-el" : (h->el_stream ? "stream2d" : ((h->ac3_stream || h->el3_stream) ? "stream3d" : "generic"));
 }
 
 int32_t hw_transport(const hw_solver* h) { return h ? h->transport : -1; }

@@ -108,6 +108,15 @@ bool ac3d_fused_eligible(int64_t nx, int64_t nm, int64_t ns, int64_t pitch, int 
 cudaError_t ac3d_fused_prepare(int64_t nx);
 void launch_ac3d_fused(int variant, const AcParams& P, const Ac3In& in, const StreamIO& IO, int nblocks, int64_t n,
                        double src, int sample, int64_t eidx, cudaStream_t st);
+// one-pass 2D elastic step (hw_elastic2d_fused.cu): state n read from these buffers (A),
+// state n+1 written through the ElParams field views (B)
+struct El2In {
+    const __half *vx, *vs, *sxx, *sss, *sxs, *rvx, *rvs, *rsxx, *rsss, *rsxs;
+};
+bool el2d_fused_eligible(int64_t nx, int64_t ns, int max_smem);
+cudaError_t el2d_fused_prepare(int64_t nx);
+void launch_el2d_fused(int variant, int order, const ElParams& P, const El2In& in, const StreamIO& IO, int nblocks,
+                       int64_t n, double src, int sample, int64_t eidx, cudaStream_t st);
 // streaming 3D elastic phase kernels (hw_elastic3d_stream.cu)
 bool el3d_stream_eligible(int64_t nx, int64_t nm, int64_t pitch, int max_smem);
 cudaError_t el3d_stream_prepare(int64_t nx);

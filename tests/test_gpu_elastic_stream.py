@@ -15,7 +15,8 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(autouse=True)
 def _streaming_kernels(monkeypatch):  # these grids would otherwise take the persistent small-grid kernel
-    monkeypatch.setenv("HALFWAVE_SMALL", "0")
+    monkeypatch.setenv("HALFWAVE_SMALL", "0")  # (or, single domain, the one-pass kernel: test_gpu_elastic_fused.py)
+    monkeypatch.setenv("HALFWAVE_FUSED_EL", "0")
 
 LAYERS = [(0.3, 2.0, 2.0, 1.0), (0.7, 2.3, 2.8, 1.4), (1.0, 2.6, 3.2, 0.0)]
 

@@ -149,7 +149,7 @@ def test_small_elastic_equals_phase_kernels(monkeypatch):
     monkeypatch.setenv("HALFWAVE_SMALL", "0")
     s2, st2 = _el(512, 200, 40)
     out2 = s2.run(hw.Variant.OP6, st2)
-    assert s2.kernel_path() == "stream2d"
+    assert s2.kernel_path() == "fused2d-el"
     for n in s1.FIELDS:
         assert_same_bits(getattr(st1, n).values, getattr(st2, n).values, n)
     np.testing.assert_array_equal(np.array([t.samples for t in out1.traces]),
