@@ -100,6 +100,17 @@ __device__ __forceinline__ void e2_finish_nd(EH2 rhs, __half2 dt2, int src_lane,
     u.h2 = s;
 }
 
+// point source: add round_U(s) to the right-hand side of the source cell (the first op of
+// finish(), stepping.py:71-80); called only on the source row (warp-uniform branch)
+__device__ __forceinline__ void e2_add_src(EH2 r[4], bool here, int sj, int sln, __half srch) {
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+        if (here && j == sj) {
+            if (sln == 0) r[j].e[0] = __hadd_rn(r[j].e[0], srch);
+            else r[j].e[1] = __hadd_rn(r[j].e[1], srch);
+        }
+}
+
 // 4-row register queue (named members, not an array: no local-memory indexing)
 struct Q4 {
     E8 q0, q1, q2, q3;  // q3 = newest
@@ -111,9 +122,12 @@ struct Q4 {
     }
 };
 
-template <int V, int ORDER, bool RM>
+// SAMPLE: energy sample step (a separate instantiation: the fp64 accumulators and energy code
+// stay out of the register budget of the other steps)
+template <int V, int ORDER, bool RM, bool SAMPLE>
 __global__ void __launch_bounds__(512, 1)
-    k_el2d_fused(ElParams P, El2In in, StreamIO IO, int64_t n, double src, int sample, int64_t eidx) {
+    k_el2d_fused(ElParams P, El2In in, StreamIO IO, int64_t n, double src, int64_t eidx) {
+    constexpr bool sample = SAMPLE;
     e_pdl_enter();
     if (halted(P.ctrl, n)) return;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -177,8 +191,10 @@ __global__ void __launch_bounds__(512, 1)
     const __half2 dt2 = __half2half2(dt);
     const __half srch = __double2half(src);
     const int xl = x == 0 ? nx - 2 : x - 2, xr = x + ECPT >= nx ? 0 : x + ECPT;
-    const bool src_v = P.src_kind == HW_SRC_VSLOW && src != 0.0 && P.src_x >= x && P.src_x < x + ECPT;
-    const bool src_s = P.src_kind == HW_SRC_EXPLOSIVE && src != 0.0 && P.src_x >= x && P.src_x < x + ECPT;
+    const bool vsrc = P.src_kind == HW_SRC_VSLOW && src != 0.0;      // warp-uniform
+    const bool ssrc = P.src_kind == HW_SRC_EXPLOSIVE && src != 0.0;  // warp-uniform
+    const bool src_v = vsrc && P.src_x >= x && P.src_x < x + ECPT;
+    const bool src_s = ssrc && P.src_x >= x && P.src_x < x + ECPT;
     const int sj = (int)((P.src_x - x) >> 1), sln = (int)((P.src_x - x) & 1);
     int rcur = rec_lower(IO.rec, 0, IO.n_rec, y0, INT_MIN);  // this CTA's receivers [rcur, rhi)
     const int rhi = rec_lower(IO.rec, rcur, IO.n_rec, y1, INT_MIN);
@@ -222,76 +238,70 @@ __global__ void __launch_bounds__(512, 1)
         mbar_wait(S.abar(), (uint32_t)(i & 1));
         const bool vel = i >= 3;
         if (vel) {
-            // ---- vx_new[rx] = fl(fl(ddx sxx + dds sxy) / rho_x * dt) (elastic.py:191-194)
-            E8 v = e_ld8(S.a(A_VX) + x);
+            // vx_new[rx] = fl(fl(ddx sxx + dds sxy) / rho_x * dt) (elastic.py:191-194) and
+            // vy_new[ry] = fl(fl(ddx sxy + dds syy) (+src) / rho_y * dt) (elastic.py:196-205),
+            // computed side by side (one basic block: the two dependency chains interleave)
+            E8 v = e_ld8(S.a(A_VX) + x), w = e_ld8(S.a(A_VS) + x);
             E8 rr = comp ? e_ld8(S.a(A_RVX) + x) : E8{};
+            E8 rw = comp ? e_ld8(S.a(A_RVS) + x) : E8{};
             {
-                const E8 a = e_xfold<ORDER>(c, S.l(ls, L_SXX), x, xl, xr, false);
-                const E8 d = e_sfold<ORDER>(c, e_ld8(S.l(l3, L_SXS) + x), e_ld8(S.l(l2, L_SXS) + x),
-                                            e_ld8(S.l(l1, L_SXS) + x), e_ld8(S.l(ls, L_SXS) + x));  // sxy F-3..F
+                const E8 ax = e_xfold<ORDER>(c, S.l(ls, L_SXX), x, xl, xr, false);
+                const E8 dx = e_sfold<ORDER>(c, e_ld8(S.l(l3, L_SXS) + x), e_ld8(S.l(l2, L_SXS) + x),
+                                             e_ld8(S.l(l1, L_SXS) + x), e_ld8(S.l(ls, L_SXS) + x));  // sxy F-3..F
+                const E8 ay = e_xfold<ORDER>(c, S.l(l2, L_SXS), x, xl, xr, true);
+                const E8 dy = e_sfold<ORDER>(c, e_ld8(S.l(l3, L_SSS) + x), e_ld8(S.l(l2, L_SSS) + x),
+                                             e_ld8(S.l(l1, L_SSS) + x), e_ld8(S.l(ls, L_SSS) + x));  // syy F-3..F
+                const bool sk = src_v && ryw == P.src_s;  // (periodic halo rows: the wrapped row)
                 if constexpr (RM) {
+                    EH2 hx[4], hy[4];
 #pragma unroll
-                    for (int j = 0; j < 4; j++) e_finish_rc<V>(EO2::add(a.q[j], d.q[j]), rcx, dt2, -1, srch, v.q[j], rr.q[j]);
+                    for (int j = 0; j < 4; j++) {
+                        hx[j] = EO2::add(ax.q[j], dx.q[j]);
+                        hy[j] = EO2::add(ay.q[j], dy.q[j]);
+                    }
+                    if (vsrc && ryw == P.src_s) e2_add_src(hy, sk, sj, sln, srch);
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
+                        e_finish_rc<V>(hx[j], rcx, dt2, -1, srch, v.q[j], rr.q[j]);
+                        e_finish_rc<V>(hy[j], rcs, dt2, -1, srch, w.q[j], rw.q[j]);
+                    }
                 } else {
 #pragma unroll
-                    for (int j = 0; j < 4; j++)
-                        finish<16, 16, 2>(EO2::add(a.q[j], d.q[j]), &P.rho_x, rxw, 0, x + 2 * j, dt, V, -1, 0.0,
+                    for (int j = 0; j < 4; j++) {
+                        finish<16, 16, 2>(EO2::add(ax.q[j], dx.q[j]), &P.rho_x, rxw, 0, x + 2 * j, dt, V, -1, 0.0,
                                           v.q[j], rr.q[j]);
+                        finish<16, 16, 2>(EO2::add(ay.q[j], dy.q[j]), &P.rho_s, ryw, 0, x + 2 * j, dt, V,
+                                          (sk && j == sj) ? sln : -1, src, w.q[j], rw.q[j]);
+                    }
                 }
             }
             if (fs && rx >= ri) {  // bottom images: rows ri-2, ri-3 (pre-push)
                 if (rx == ri) v = vxq.q2;
                 else v = vxq.q0;
             }
-            if (rx >= y0 && rx < y1 && rx < ri) {
-                e2_store(inner_v, P.vx, ox, pitch, rx, x, v);
-                e_track(acc[0], v);
-                if (comp) {
-                    e2_store(inner_v, P.rvx, ox, pitch, rx, x, rr);
-                    
-                }
-            }
-            vxq.push(v);
-            if (fs && rx == 1) vxq.q1 = vxq.q3;  // top image: row -1 = row 1
-            e_st8(S.vx((rx + 3) % 3) + x, v);  // rx >= -4
-            // ---- vy_new[ry] = fl(fl(ddx sxy + dds syy) (+src) / rho_y * dt) (elastic.py:196-205)
-            E8 w = e_ld8(S.a(A_VS) + x);
-            E8 rw = comp ? e_ld8(S.a(A_RVS) + x) : E8{};
-            {
-                const E8 a = e_xfold<ORDER>(c, S.l(l2, L_SXS), x, xl, xr, true);
-                const E8 d = e_sfold<ORDER>(c, e_ld8(S.l(l3, L_SSS) + x), e_ld8(S.l(l2, L_SSS) + x),
-                                            e_ld8(S.l(l1, L_SSS) + x), e_ld8(S.l(ls, L_SSS) + x));  // syy F-3..F
-                const bool sk = src_v && ryw == P.src_s;  // (periodic halo rows: the wrapped row)
-                if constexpr (RM) {
-#pragma unroll
-                    for (int j = 0; j < 4; j++)
-                        e_finish_rc<V>(EO2::add(a.q[j], d.q[j]), rcs, dt2, (sk && j == sj) ? sln : -1, srch, w.q[j],
-                                       rw.q[j]);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 4; j++)
-                        finish<16, 16, 2>(EO2::add(a.q[j], d.q[j]), &P.rho_s, ryw, 0, x + 2 * j, dt, V,
-                                          (sk && j == sj) ? sln : -1, src, w.q[j], rw.q[j]);
-                }
-            }
             if (fs && ry >= rh) {  // bottom images: rows rh-1, rh-2 (pre-push)
                 if (ry == rh) w = vyq.q3;
                 else w = vyq.q1;
             }
+            e_st8(S.vx((rx + 3) % 3) + x, v);  // rx >= -1
+            e_st8(S.vy(par) + x, w);
+            if (rx >= y0 && rx < y1 && rx < ri) {
+                e2_store(inner_v, P.vx, ox, pitch, rx, x, v);
+                e_track(acc[0], v);
+                if (comp) e2_store(inner_v, P.rvx, ox, pitch, rx, x, rr);
+            }
             if (ry >= y0 && ry < y1 && ry < rh) {
                 e2_store(inner_v, P.vs, oy, pitch, ry, x, w);
                 e_track(acc[1], w);
-                if (comp) {
-                    e2_store(inner_v, P.rvs, oy, pitch, ry, x, rw);
-                    
-                }
+                if (comp) e2_store(inner_v, P.rvs, oy, pitch, ry, x, rw);
                 // receiver traces of vy after the step (elastic.py:283-284)
                 rec_row(IO.rec, rcur, rhi, ry, x, IO.traces, IO.nt, n, [&](int o) { return e_pick(w, o); });
             }
+            vxq.push(v);
             vyq.push(w);
-            if (fs && ry == 0) vyq.q2 = vyq.q3;  // top images: row -1 = row 0
-            if (fs && ry == 1) vyq.q0 = vyq.q3;  //             row -2 = row 1
-            e_st8(S.vy(par) + x, w);
+            if (fs && rx == 1) vxq.q1 = vxq.q3;  // top images: vx row -1 = row 1
+            if (fs && ry == 0) vyq.q2 = vyq.q3;  //             vy row -1 = row 0
+            if (fs && ry == 1) vyq.q0 = vyq.q3;  //             vy row -2 = row 1
         }
         __syncthreads();  // vx / vy rows visible; every read of tap slot (i+1) % LR and of the A rows is done
         if (tid == 0 && i + 1 < NI) {
@@ -302,44 +312,62 @@ __global__ void __launch_bounds__(512, 1)
         const E8 gy = vel ? e_xfold<ORDER>(c, S.vy(par), x, xl, xr, false) : E8{};  // d/dx vy_new[ry] (to-half)
         const bool own_k = k >= y0 && k < y1;
         if (comp && own_k) mbar_wait(S.bbar(), (uint32_t)(i & 1));
-        if (own_k) {
+        if (own_k) {  // stresses of row k (k < ri always; sxy only for k < rh)
             const int sg = (int)P.sxx.row0 + k;
-            if (k < ri) {  // ---- sxx, syy (elastic.py:210-230)
-                const E8 dvs = e_sfold<ORDER>(c, vyq.q0, vyq.q1, vyq.q2, vyq.q3);  // vy rows k-2..k+1
-                const E8 dvx = e_xfold<ORDER>(c, S.vx((k + 3) % 3), x, xl, xr, true);  // d/dx vx_new[k] (to-int)
-                const bool surf = fs && (sg == 0 || sg == (int)P.sxx.nglob - 1);
-                const bool sk = src_s && k == P.src_s;
-                const E8 sxx_old = e_ld8(S.l(l2, L_SXX) + x);  // sxx[F-3], loaded at i-2
-                const E8 sss_old = e_ld8(S.l(l3, L_SSS) + x);  // syy[F-3]
-                E8 sxx = sxx_old, sss = sss_old;
-                E8 rsxx = comp ? e_ld8(S.b(B_RSXX) + x) : E8{};
-                E8 rsss = comp ? e_ld8(S.b(B_RSSS) + x) : E8{};
+            const bool surf = fs && (sg == 0 || sg == (int)P.sxx.nglob - 1);
+            const bool sk = src_s && k == P.src_s;
+            const E8 dvs = e_sfold<ORDER>(c, vyq.q0, vyq.q1, vyq.q2, vyq.q3);      // vy rows k-2..k+1 (to-int)
+            const E8 dvx = e_xfold<ORDER>(c, S.vx((k + 3) % 3), x, xl, xr, true);  // d/dx vx_new[k] (to-int)
+            const E8 dvxy = e_sfold<ORDER>(c, vxq.q0, vxq.q1, vxq.q2, vxq.q3);     // vx rows k-1..k+2 (to-half)
+            const E8 sxx_old = e_ld8(S.l(l2, L_SXX) + x);  // sxx[F-3], loaded at i-2
+            const E8 sss_old = e_ld8(S.l(l3, L_SSS) + x);  // syy[F-3]
+            const E8 old = e_ld8(S.l(l3, L_SXS) + x);      // sxy[F-3]
+            E8 sxx = sxx_old, sss = sss_old, s = old;
+            E8 rsxx = comp ? e_ld8(S.b(B_RSXX) + x) : E8{};
+            E8 rsss = comp ? e_ld8(S.b(B_RSSS) + x) : E8{};
+            E8 rs = comp ? e_ld8(S.b(B_RSXS) + x) : E8{};
+            EH2 a1[4], a2[4];
+            if (!surf) {  // sxx, syy (elastic.py:210-214)
 #pragma unroll
                 for (int j = 0; j < 4; j++) {
                     const EH2 stiff = RM ? stiff_r : pload<16, 2>(P.stiff, k, 0, x + 2 * j);
                     const EH2 lam = RM ? lam_r : pload<16, 2>(P.lam, k, 0, x + 2 * j);
-                    EH2 a1, a2;
-                    if (surf) {  // plane-stress surface row; syy takes a zero increment (elastic.py:215-230)
-                        a1 = EO2::mul(pload<16, 2>(P.ep, sg == 0 ? 0 : 1, 0, x + 2 * j), dvx.q[j]);
-                        a2 = vsplat<16, 2>(lane<16>::zero());
-                    } else {
-                        a1 = EO2::add(EO2::mul(stiff, dvx.q[j]), EO2::mul(lam, dvs.q[j]));
-                        a2 = EO2::add(EO2::mul(lam, dvx.q[j]), EO2::mul(stiff, dvs.q[j]));
-                    }
-                    const int lsrc = (sk && j == sj) ? sln : -1;
-                    e2_finish_nd<V>(a1, dt2, lsrc, srch, sxx.q[j], rsxx.q[j]);
-                    e2_finish_nd<V>(a2, dt2, lsrc, srch, sss.q[j], rsss.q[j]);
+                    a1[j] = EO2::add(EO2::mul(stiff, dvx.q[j]), EO2::mul(lam, dvs.q[j]));
+                    a2[j] = EO2::add(EO2::mul(lam, dvx.q[j]), EO2::mul(stiff, dvs.q[j]));
                 }
-                e2_store(inner_k, P.sxx, ok, pitch, k, x, sxx);
-                e2_store(inner_k, P.sss, ok, pitch, k, x, sss);
-                e_track(acc[2], sxx);
-                e_track(acc[3], sss);
-                if (comp) {
-                    e2_store(inner_k, P.rsxx, ok, pitch, k, x, rsxx);
-                    e2_store(inner_k, P.rsss, ok, pitch, k, x, rsss);
-                    
-                    
+            } else {  // plane-stress surface row; syy takes a zero increment (elastic.py:215-230)
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    a1[j] = EO2::mul(pload<16, 2>(P.ep, sg == 0 ? 0 : 1, 0, x + 2 * j), dvx.q[j]);
+                    a2[j] = vsplat<16, 2>(lane<16>::zero());
                 }
+            }
+            if (ssrc && k == P.src_s) {  // explosive source into both normal stresses
+                e2_add_src(a1, sk, sj, sln, srch);
+                e2_add_src(a2, sk, sj, sln, srch);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                e2_finish_nd<V>(a1[j], dt2, -1, srch, sxx.q[j], rsxx.q[j]);
+                e2_finish_nd<V>(a2[j], dt2, -1, srch, sss.q[j], rsss.q[j]);
+                // sxy = fl(mu fl(dds vx + ddx vy)) (elastic.py:232-238)
+                const EH2 mu = RM ? mu_r : pload<16, 2>(P.mu_n, kwh, 0, x + 2 * j);
+                e2_finish_nd<V>(EO2::mul(mu, EO2::add(dvxy.q[j], gyp.q[j])), dt2, -1, srch, s.q[j], rs.q[j]);
+            }
+            e2_store(inner_k, P.sxx, ok, pitch, k, x, sxx);
+            e2_store(inner_k, P.sss, ok, pitch, k, x, sss);
+            e_track(acc[2], sxx);
+            e_track(acc[3], sss);
+            if (comp) {
+                e2_store(inner_k, P.rsxx, ok, pitch, k, x, rsxx);
+                e2_store(inner_k, P.rsss, ok, pitch, k, x, rsss);
+            }
+            if (k < rh) {
+                e2_store(inner_k, P.sxs, ok, pitch, k, x, s);
+                e_track(acc[4], s);
+                if (comp) e2_store(inner_k, P.rsxs, ok, pitch, k, x, rs);
+            }
+            {
                 if (sample) {  // kinetic x + strain energy at this integer row (diagnostics.py:100-162)
                     const E8& vxr = vxq.q1;  // vx_new[k]
                     const double w = surf ? 0.5 : 1.0;
@@ -390,22 +418,7 @@ __global__ void __launch_bounds__(512, 1)
                     }
                 }
             }
-            if (k < rh) {  // ---- sxy = fl(mu fl(dds vx + ddx vy)) (elastic.py:232-238)
-                const E8 dvxy = e_sfold<ORDER>(c, vxq.q0, vxq.q1, vxq.q2, vxq.q3);  // vx rows k-1..k+2
-                const E8 old = e_ld8(S.l(l3, L_SXS) + x);  // sxy[F-3]
-                E8 s = old;
-                E8 rs = comp ? e_ld8(S.b(B_RSXS) + x) : E8{};
-#pragma unroll
-                for (int j = 0; j < 4; j++) {
-                    const EH2 mu = RM ? mu_r : pload<16, 2>(P.mu_n, k, 0, x + 2 * j);
-                    e2_finish_nd<V>(EO2::mul(mu, EO2::add(dvxy.q[j], gyp.q[j])), dt2, -1, srch, s.q[j], rs.q[j]);
-                }
-                e2_store(inner_k, P.sxs, ok, pitch, k, x, s);
-                e_track(acc[4], s);
-                if (comp) {
-                    e2_store(inner_k, P.rsxs, ok, pitch, k, x, rs);
-                    
-                }
+            if (k < rh) {
                 if (sample) {  // kinetic y + shear energy at this half row
                     const E8& vyr = vyq.q2;  // vy_new[k]
                     if (erow) {
@@ -426,9 +439,9 @@ __global__ void __launch_bounds__(512, 1)
                             const double v = (double)__half2float(vyr.q[q >> 1].e[q & 1]);
                             e[1] += p64(P.e_rho_s, k, 0, xi) * (v * v);
                             const double mun = p64(P.e_mu_n, k, 0, xi);
-                            const double a0 = (double)__half2float(old.q[q >> 1].e[q & 1]);
-                            const double a1 = (double)__half2float(s.q[q >> 1].e[q & 1]);
-                            e[4] += mun > 0.0 ? (a0 * a1) / mun : 0.0;
+                            const double o0 = (double)__half2float(old.q[q >> 1].e[q & 1]);
+                            const double o1 = (double)__half2float(s.q[q >> 1].e[q & 1]);
+                            e[4] += mun > 0.0 ? (o0 * o1) / mun : 0.0;
                         }
                     }
                 }
@@ -454,7 +467,7 @@ __global__ void __launch_bounds__(512, 1)
     mask |= e_nonfinite(acc[3]) << P.sss.bit;
     mask |= e_nonfinite(acc[4]) << P.sxs.bit;
     record_failure(P.ctrl, n, mask);
-    if (!sample) return;
+    if constexpr (!SAMPLE) return;
     block_partials(e, P.partials);
     __threadfence();
     __syncthreads();
@@ -481,8 +494,10 @@ bool el2d_fused_eligible(int64_t nx, int64_t ns, int max_smem) {
 
 template <int V, int O>
 static void el2f_attrs(int bytes) {
-    cudaFuncSetAttribute((void*)k_el2d_fused<V, O, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    cudaFuncSetAttribute((void*)k_el2d_fused<V, O, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute((void*)k_el2d_fused<V, O, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute((void*)k_el2d_fused<V, O, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute((void*)k_el2d_fused<V, O, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute((void*)k_el2d_fused<V, O, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 cudaError_t el2d_fused_prepare(int64_t nx) {
@@ -512,12 +527,17 @@ static bool el2f_rowmed(const ElParams& P) {
 void launch_el2d_fused(int variant, int order, const ElParams& P, const El2In& in, const StreamIO& IO, int nblocks,
                        int64_t n, double src, int sample, int64_t eidx, cudaStream_t st) {
     void* fn = nullptr;
-    if (el2f_rowmed(P)) {
-        EL2F_DISPATCH(variant, order, (fn = (void*)k_el2d_fused<V_, O_, true>))
+    const bool rm = el2f_rowmed(P);
+    if (rm && sample) {
+        EL2F_DISPATCH(variant, order, (fn = (void*)k_el2d_fused<V_, O_, true, true>))
+    } else if (rm) {
+        EL2F_DISPATCH(variant, order, (fn = (void*)k_el2d_fused<V_, O_, true, false>))
+    } else if (sample) {
+        EL2F_DISPATCH(variant, order, (fn = (void*)k_el2d_fused<V_, O_, false, true>))
     } else {
-        EL2F_DISPATCH(variant, order, (fn = (void*)k_el2d_fused<V_, O_, false>))
+        EL2F_DISPATCH(variant, order, (fn = (void*)k_el2d_fused<V_, O_, false, false>))
     }
-    void* args[] = {(void*)&P, (void*)&in, (void*)&IO, (void*)&n, (void*)&src, (void*)&sample, (void*)&eidx};
+    void* args[] = {(void*)&P, (void*)&in, (void*)&IO, (void*)&n, (void*)&src, (void*)&eidx};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nblocks);
     cfg.blockDim = dim3((unsigned)(P.g.nx / ECPT));
