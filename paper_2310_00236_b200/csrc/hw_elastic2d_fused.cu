@@ -68,49 +68,6 @@ struct E2F {
 
 size_t el2d_fused_smem_bytes(int64_t nx) { return 128 + (size_t)(LR * L_N + A_N + B_N + 5) * nx * sizeof(__half); }
 
-// row store at element offset off = s * pitch + x; rows away from the slow-axis ends skip
-// the write-through ghost logic
-__device__ __forceinline__ void e2_store(bool inner, const FieldView& f, int64_t off, int64_t pitch, int s, int x,
-                                         const E8& v) {
-    if (inner) e_st8(reinterpret_cast<__half*>(f.base) + off, v);
-    else e_store_row(f, pitch, s, x, v);
-}
-
-// finish() without a divisor (stresses, elastic.py:210-238): source (round_U(s), lane
-// src_lane) before x dt, then the advance -- the same ops as finish<16, 16, 2>
-template <int V>
-__device__ __forceinline__ void e2_finish_nd(EH2 rhs, __half2 dt2, int src_lane, __half srch, EH2& u, EH2& t) {
-    if (src_lane == 0) rhs.e[0] = __hadd_rn(rhs.e[0], srch);
-    else if (src_lane == 1) rhs.e[1] = __hadd_rn(rhs.e[1], srch);
-    EH2 x;
-    x.h2 = __hmul2_rn(rhs.h2, dt2);
-    if (V == 0) {
-        u.h2 = __hadd2_rn(u.h2, x.h2);
-        return;
-    }
-    const __half2 r = __hadd2_rn(t.h2, x.h2);
-    const __half2 s = __hadd2_rn(u.h2, r);
-    if (V == 3) {
-        t.h2 = __hsub2_rn(r, __hsub2_rn(s, u.h2));
-    } else {
-        const __half2 pa = __hsub2_rn(s, r);
-        const __half2 pb = __hsub2_rn(s, pa);
-        t.h2 = __hadd2_rn(__hsub2_rn(u.h2, pa), __hsub2_rn(r, pb));
-    }
-    u.h2 = s;
-}
-
-// point source: add round_U(s) to the right-hand side of the source cell (the first op of
-// finish(), stepping.py:71-80); called only on the source row (warp-uniform branch)
-__device__ __forceinline__ void e2_add_src(EH2 r[4], bool here, int sj, int sln, __half srch) {
-#pragma unroll
-    for (int j = 0; j < 4; j++)
-        if (here && j == sj) {
-            if (sln == 0) r[j].e[0] = __hadd_rn(r[j].e[0], srch);
-            else r[j].e[1] = __hadd_rn(r[j].e[1], srch);
-        }
-}
-
 // 4-row register queue (named members, not an array: no local-memory indexing)
 struct Q4 {
     E8 q0, q1, q2, q3;  // q3 = newest

@@ -106,7 +106,8 @@ __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t 
     for (int q = 0; q < 4; q++) c[q] = lconst<16>(P.k, q);
     const __half dt = lconst<16>(P.k, 4);
     const int xl = x == 0 ? nx - 2 : x - 2, xr = x + ECPT >= nx ? 0 : x + ECPT;
-    const bool src_col = P.src_kind == HW_SRC_VSLOW && src != 0.0 && P.src_x >= x && P.src_x < x + ECPT;
+    const bool vsrc = P.src_kind == HW_SRC_VSLOW && src != 0.0;  // warp-uniform
+    const bool src_col = vsrc && P.src_x >= x && P.src_x < x + ECPT;
     const bool rm = e_rowdiv(P.rho_x) && e_rowdiv(P.rho_s) && e_rowdiv(P.rho_m);  // one reciprocal per row
     const __half2 dt2 = __half2half2(dt);
     const __half srch = __double2half(src);
@@ -180,6 +181,8 @@ __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t 
                 }
                 mbar_wait(&L.obar[os], (uint32_t)(((gk0 + kr) >> 1) & 1));
                 const int64_t ro = jr + x, off = (int64_t)m * pitch + x;
+                const int64_t goff = (int64_t)s * slab + off;
+                const bool inner = s >= G && s < ns - G;  // stores that never touch a ghost slab
                 E8 v[3], rr[3];
 #pragma unroll
                 for (int q = 0; q < 3; q++) {
@@ -204,9 +207,9 @@ __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t 
                 a = e3_add(a, e3_mfold<ORDER>(c, pd + o_sms * pitch + jr + (H - 2) * pitch + x, pitch));
                 const bool sk = src_col && s == P.src_s && m == P.src_m;
                 if (rm) {
+                    if (vsrc && s == P.src_s && m == P.src_m) e2_add_src(a.q, sk, sj, sln, srch);  // (m: warp-uniform)
 #pragma unroll
-                    for (int h = 0; h < 4; h++)
-                        e_finish_rc<V>(a.q[h], rcs, dt2, (sk && h == sj) ? sln : -1, srch, v[1].q[h], rr[1].q[h]);
+                    for (int h = 0; h < 4; h++) e_finish_rc<V>(a.q[h], rcs, dt2, -1, srch, v[1].q[h], rr[1].q[h]);
                 } else {
 #pragma unroll
                     for (int h = 0; h < 4; h++)
@@ -227,12 +230,9 @@ __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t 
                 }
 #pragma unroll
                 for (int q = 0; q < 3; q++) {
-                    e_store_row(*OF[q], slab, s, (int)off, v[q]);
+                    e2_store(inner, *OF[q], goff, slab, s, (int)off, v[q]);
                     e_track(acc[q], v[q]);
-                    if (comp) {
-                        e_store_row(*OF[3 + q], slab, s, (int)off, rr[q]);
-                        e_track(acc[3 + q], rr[q]);
-                    }
+                    if (comp) e2_store(inner, *OF[3 + q], goff, slab, s, (int)off, rr[q]);
                 }
             }
             __syncthreads();
@@ -243,8 +243,7 @@ __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t 
     unsigned int mask = 0;
 #pragma unroll
     for (int q = 0; q < 3; q++) {
-        mask |= e_nonfinite(acc[q]) << OF[q]->bit;
-        if (comp) mask |= e_nonfinite(acc[3 + q]) << OF[3 + q]->bit;
+        mask |= e_nonfinite(acc[q]) << OF[q]->bit;  // (residuals: see k_el2d_fused)
     }
     record_failure(P.ctrl, n, mask);
 }
@@ -278,7 +277,10 @@ __global__ void __launch_bounds__(E3T, 1)
     for (int q = 0; q < 4; q++) c[q] = lconst<16>(P.k, q);
     const __half dt = lconst<16>(P.k, 4);
     const int xl = x == 0 ? nx - 2 : x - 2, xr = x + ECPT >= nx ? 0 : x + ECPT;
-    const bool src_col = P.src_kind == HW_SRC_EXPLOSIVE && src != 0.0 && P.src_x >= x && P.src_x < x + ECPT;
+    const bool ssrc = P.src_kind == HW_SRC_EXPLOSIVE && src != 0.0;  // warp-uniform
+    const bool src_col = ssrc && P.src_x >= x && P.src_x < x + ECPT;
+    const __half2 dt2 = __half2half2(dt);
+    const __half srch = __double2half(src);
     const bool mrow = P.stiff.sx == 0 && P.lam.sx == 0 && P.mu_n.sx == 0;
     const int sj = (int)((P.src_x - x) >> 1), sln = (int)((P.src_x - x) & 1);
     // energy planes constant within a slab (layered along the slow axis): per-slab sums
@@ -347,6 +349,8 @@ __global__ void __launch_bounds__(E3T, 1)
                 }
                 mbar_wait(&L.obar[os], (uint32_t)(((gk0 + kr) >> 1) & 1));
                 const int64_t ro = jr + x, off = (int64_t)m * pitch + x;
+                const int64_t goff = (int64_t)s * slab + off;
+                const bool inner = s >= G && s < ns - G;  // stores that never touch a ghost slab
                 // tile row pointers at row m - 2 (row m at index j + H; 2nd order never reads m - 2)
                 const __half* vxt = d + o_vxt * pitch + jr + (H - 2) * pitch;
                 const __half* vmt = d + o_vmt * pitch + jr + (H - 2) * pitch;
@@ -369,21 +373,26 @@ __global__ void __launch_bounds__(E3T, 1)
                     lam_r = e_val_at(P.lam, s, m);
                     mu_r = e_val_at(P.mu_n, s, m);
                 }
+                EH2 a0[4], a1[4], a2[4];
 #pragma unroll
                 for (int h = 0; h < 4; h++) {
                     const EH2 stiff = mrow ? stiff_r : pload<16, 2>(P.stiff, s, m, x + 2 * h);
                     const EH2 lam = mrow ? lam_r : pload<16, 2>(P.lam, s, m, x + 2 * h);
-                    const int lsrc = (sk && h == sj) ? sln : -1;
                     // sxx: fl(fl(fl(stiff dvx) + fl(lam dvs)) + fl(lam dvm)); s_slow / s_mid likewise
-                    const EH2 a0 = EO2::add(EO2::add(EO2::mul(stiff, dvx.q[h]), EO2::mul(lam, dvs.q[h])),
-                                            EO2::mul(lam, dvm.q[h]));
-                    const EH2 a1 = EO2::add(EO2::add(EO2::mul(lam, dvx.q[h]), EO2::mul(stiff, dvs.q[h])),
-                                            EO2::mul(lam, dvm.q[h]));
-                    const EH2 a2 = EO2::add(EO2::add(EO2::mul(lam, dvx.q[h]), EO2::mul(lam, dvs.q[h])),
-                                            EO2::mul(stiff, dvm.q[h]));
-                    finish<16, 16, 2>(a0, nullptr, s, m, x, dt, V, lsrc, src, nw[0].q[h], rr[0].q[h]);
-                    finish<16, 16, 2>(a1, nullptr, s, m, x, dt, V, lsrc, src, nw[1].q[h], rr[1].q[h]);
-                    finish<16, 16, 2>(a2, nullptr, s, m, x, dt, V, lsrc, src, nw[2].q[h], rr[2].q[h]);
+                    a0[h] = EO2::add(EO2::add(EO2::mul(stiff, dvx.q[h]), EO2::mul(lam, dvs.q[h])), EO2::mul(lam, dvm.q[h]));
+                    a1[h] = EO2::add(EO2::add(EO2::mul(lam, dvx.q[h]), EO2::mul(stiff, dvs.q[h])), EO2::mul(lam, dvm.q[h]));
+                    a2[h] = EO2::add(EO2::add(EO2::mul(lam, dvx.q[h]), EO2::mul(lam, dvs.q[h])), EO2::mul(stiff, dvm.q[h]));
+                }
+                if (ssrc && s == P.src_s && m == P.src_m) {  // explosive source into the normal stresses
+                    e2_add_src(a0, sk, sj, sln, srch);
+                    e2_add_src(a1, sk, sj, sln, srch);
+                    e2_add_src(a2, sk, sj, sln, srch);
+                }
+#pragma unroll
+                for (int h = 0; h < 4; h++) {
+                    e2_finish_nd<V>(a0[h], dt2, -1, srch, nw[0].q[h], rr[0].q[h]);
+                    e2_finish_nd<V>(a1[h], dt2, -1, srch, nw[1].q[h], rr[1].q[h]);
+                    e2_finish_nd<V>(a2[h], dt2, -1, srch, nw[2].q[h], rr[2].q[h]);
                 }
                 // shear: fl(mu fl(dd_a v_b + dd_b v_a)) (elastic.py:232-238 per plane), to-half taps
                 const E8 sxs_a = e_sfold<ORDER>(c, qvx[0], qvx[1], qvx[2], qvx[3]);
@@ -395,21 +404,15 @@ __global__ void __launch_bounds__(E3T, 1)
 #pragma unroll
                 for (int h = 0; h < 4; h++) {
                     const EH2 mu = mrow ? mu_r : pload<16, 2>(P.mu_n, s, m, x + 2 * h);
-                    finish<16, 16, 2>(EO2::mul(mu, EO2::add(sxs_a.q[h], sxs_b.q[h])), nullptr, s, m, x, dt, V, -1, 0.0,
-                                      nw[3].q[h], rr[3].q[h]);
-                    finish<16, 16, 2>(EO2::mul(mu, EO2::add(sxm_a.q[h], sxm_b.q[h])), nullptr, s, m, x, dt, V, -1, 0.0,
-                                      nw[4].q[h], rr[4].q[h]);
-                    finish<16, 16, 2>(EO2::mul(mu, EO2::add(sms_a.q[h], sms_b.q[h])), nullptr, s, m, x, dt, V, -1, 0.0,
-                                      nw[5].q[h], rr[5].q[h]);
+                    e2_finish_nd<V>(EO2::mul(mu, EO2::add(sxs_a.q[h], sxs_b.q[h])), dt2, -1, srch, nw[3].q[h], rr[3].q[h]);
+                    e2_finish_nd<V>(EO2::mul(mu, EO2::add(sxm_a.q[h], sxm_b.q[h])), dt2, -1, srch, nw[4].q[h], rr[4].q[h]);
+                    e2_finish_nd<V>(EO2::mul(mu, EO2::add(sms_a.q[h], sms_b.q[h])), dt2, -1, srch, nw[5].q[h], rr[5].q[h]);
                 }
 #pragma unroll
                 for (int q = 0; q < 6; q++) {
-                    e_store_row(*OF[q], slab, s, (int)off, nw[q]);
+                    e2_store(inner, *OF[q], goff, slab, s, (int)off, nw[q]);
                     e_track(acc[q], nw[q]);
-                    if (comp) {
-                        e_store_row(*OF[6 + q], slab, s, (int)off, rr[q]);
-                        e_track(acc[6 + q], rr[q]);
-                    }
+                    if (comp) e2_store(inner, *OF[6 + q], goff, slab, s, (int)off, rr[q]);
                 }
                 if (sample) {  // diagnostics.py:100-162, 3D compliance form (k_el_stress)
                     const E8 vxo = e_ld8(vxt + 2 * pitch + x), vmo = e_ld8(vmt + 2 * pitch + x);
@@ -471,8 +474,7 @@ __global__ void __launch_bounds__(E3T, 1)
     unsigned int mask = 0;
 #pragma unroll
     for (int q = 0; q < 6; q++) {
-        mask |= e_nonfinite(acc[q]) << OF[q]->bit;
-        if (comp) mask |= e_nonfinite(acc[6 + q]) << OF[6 + q]->bit;
+        mask |= e_nonfinite(acc[q]) << OF[q]->bit;  // (residuals: see k_el2d_fused)
     }
     record_failure(P.ctrl, n, mask);
     if (!sample) return;
