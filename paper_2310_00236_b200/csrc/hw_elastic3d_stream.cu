@@ -250,9 +250,12 @@ __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t 
 
 // ---------------------------------------------------------------- stress phase
 // slot rows: [vx(F) TM | vm(F) TM | vs tile(F-1) TM+2H | vx tile(s) TM+2H | vm tile(s) TM+2H]
-template <int V, int ORDER>
+// SAMPLE: energy sample step (separate instantiation: the energy code stays out of the loop
+// body -- instruction cache -- and the register budget of the other steps)
+template <int V, int ORDER, bool SAMPLE>
 __global__ void __launch_bounds__(E3T, 1)
-    k_el3d_stress_stream(ElParams P, StreamIO IO, int64_t n, double src, int sample, int64_t eidx) {
+    k_el3d_stress_stream(ElParams P, StreamIO IO, int64_t n, double src, int64_t eidx) {
+    constexpr bool sample = SAMPLE;
     e_pdl_enter();
     if (halted(P.ctrl, n)) return;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -477,7 +480,7 @@ __global__ void __launch_bounds__(E3T, 1)
         mask |= e_nonfinite(acc[q]) << OF[q]->bit;  // (residuals: see k_el2d_fused)
     }
     record_failure(P.ctrl, n, mask);
-    if (!sample) return;
+    if constexpr (!SAMPLE) return;
     block_partials(e, P.partials);
     __threadfence();
     __syncthreads();
@@ -514,7 +517,9 @@ template <int V, int O>
 static void e3_attrs(int64_t nx) {
     cudaFuncSetAttribute((void*)k_el3d_vel_stream<V, O>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)e3_vel_bytes(nx, O));
-    cudaFuncSetAttribute((void*)k_el3d_stress_stream<V, O>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute((void*)k_el3d_stress_stream<V, O, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)e3_stress_bytes(nx, O));
+    cudaFuncSetAttribute((void*)k_el3d_stress_stream<V, O, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)e3_stress_bytes(nx, O));
 }
 
@@ -560,8 +565,12 @@ void launch_el3d_vel_stream(int variant, int order, const ElParams& P, int nbloc
 void launch_el3d_stress_stream(int variant, int order, const ElParams& P, const StreamIO& IO, int nblocks, int64_t n,
                                double src, int sample, int64_t eidx, cudaStream_t st) {
     void* fn = nullptr;
-    E3_DISPATCH(variant, order, (fn = (void*)k_el3d_stress_stream<V_, O_>))
-    void* args[] = {(void*)&P, (void*)&IO, (void*)&n, (void*)&src, (void*)&sample, (void*)&eidx};
+    if (sample) {
+        E3_DISPATCH(variant, order, (fn = (void*)k_el3d_stress_stream<V_, O_, true>))
+    } else {
+        E3_DISPATCH(variant, order, (fn = (void*)k_el3d_stress_stream<V_, O_, false>))
+    }
+    void* args[] = {(void*)&P, (void*)&IO, (void*)&n, (void*)&src, (void*)&eidx};
     e3_launch(fn, nblocks, e3_stress_bytes(P.g.nx, order), st, args);
 }
 
