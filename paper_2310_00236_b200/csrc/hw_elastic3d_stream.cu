@@ -73,8 +73,9 @@ __device__ __forceinline__ void e3_shift(E8 q[4], const E8& v) {
 }
 
 // ---------------------------------------------------------------- velocity phase
-// slot rows: [sss(F) TM | sxs(F-1) TM | sms tile(F-1) TM+2H | sxx(s) TM | sxm tile(s) TM+2H | smm tile(s) TM+2H]
-// (tiles: mid rows m0-H .. m0+TM+H-1, H = ORDER/2 halo rows each side; row m at index j + H)
+// slot rows: [sss(F) TM | sxs(F-1) TM | sms tile(F-1) | sxx(s) TM | sxm tile(s) | smm tile(s)], tiles of
+// TM + 2H - 1 rows (H = ORDER/2): a tile read by to-int mid taps holds rows m0-H .. m0+TM+H-2 (row m
+// at index j + H), one read by to-half mid taps rows m0-H+1 .. m0+TM+H-1 (row m at index j + H - 1)
 template <int V, int ORDER>
 __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t n, double src) {
     e_pdl_enter();
@@ -84,8 +85,9 @@ __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t 
     const int64_t pitch = P.g.pitch, slab = P.g.slab;
     const int TM = E3T * ECPT / nx, TPR = nx / ECPT;
     constexpr int H = ORDER / 2;
-    const E3Layout L(smem, 6 * TM + 6 * H, TM, pitch, 6);
-    const int o_sxs = TM, o_sms = 2 * TM, o_sxx = 3 * TM + 2 * H, o_sxm = 4 * TM + 2 * H, o_smm = 5 * TM + 4 * H;
+    constexpr int TH = 2 * H - 1;  // halo rows of a one-sided tile
+    const E3Layout L(smem, 6 * TM + 3 * TH, TM, pitch, 6);
+    const int o_sxs = TM, o_sms = 2 * TM, o_sxx = 3 * TM + TH, o_sxm = 4 * TM + TH, o_smm = 5 * TM + 2 * TH;
     const int tid = threadIdx.x, j = tid / TPR, x = (tid % TPR) * ECPT;
     constexpr bool comp = V != 0;
     constexpr int NOWN = comp ? 6 : 3;  // vx vs vm [rvx rvs rvm]
@@ -132,13 +134,13 @@ __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t 
             const int F = F0 + i, k = (gi0 + i) % QR;
             __half* d = L.sl(k);
             const int64_t mo = (int64_t)m0 * pitch;
-            mbar_arrive_expect_tx(&L.bar[k], (uint32_t)((6 * TM + 6 * H) * pitch * sizeof(__half)));
+            mbar_arrive_expect_tx(&L.bar[k], (uint32_t)((6 * TM + 3 * TH) * pitch * sizeof(__half)));
             tma_load_1d(d, SSS + e_row(F) * slab + mo, tmb, &L.bar[k]);
             tma_load_1d(d + o_sxs * pitch, SXS + e_row(F - 1) * slab + mo, tmb, &L.bar[k]);
-            a3_rows(d + o_sms * pitch, SMS, slab, e_row(F - 1), m0 - H, m0 + TM + H, nm, pitch, &L.bar[k]);
+            a3_rows(d + o_sms * pitch, SMS, slab, e_row(F - 1), m0 - H, m0 + TM + H - 1, nm, pitch, &L.bar[k]);
             tma_load_1d(d + o_sxx * pitch, SXX + e_row(F - 2) * slab + mo, tmb, &L.bar[k]);
-            a3_rows(d + o_sxm * pitch, SXM, slab, e_row(F - 2), m0 - H, m0 + TM + H, nm, pitch, &L.bar[k]);
-            a3_rows(d + o_smm * pitch, SMM, slab, e_row(F - 2), m0 - H, m0 + TM + H, nm, pitch, &L.bar[k]);
+            a3_rows(d + o_sxm * pitch, SXM, slab, e_row(F - 2), m0 - H, m0 + TM + H - 1, nm, pitch, &L.bar[k]);
+            a3_rows(d + o_smm * pitch, SMM, slab, e_row(F - 2), m0 - H + 1, m0 + TM + H, nm, pitch, &L.bar[k]);
         };
         auto issue_own = [&](int kk) {
             const int os = (gk0 + kk) & 1;
@@ -219,7 +221,7 @@ __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t 
                 // v_mid: fl(fl(ddx sxm + dds sms) + ddm smm)
                 a = e_xfold<ORDER>(c, d + o_sxm * pitch + jr + H * pitch, x, xl, xr, true);
                 a = e3_add(a, e_sfold<ORDER>(c, qms[0], qms[1], qms[2], qms[3]));
-                a = e3_add(a, e3_mfold<ORDER>(c, d + o_smm * pitch + jr + (H - 1) * pitch + x, pitch));
+                a = e3_add(a, e3_mfold<ORDER>(c, d + o_smm * pitch + jr + (H - 2) * pitch + x, pitch));  // to-half tile
                 if (rm) {
 #pragma unroll
                     for (int h = 0; h < 4; h++) e_finish_rc<V>(a.q[h], rcm, dt2, -1, srch, v[2].q[h], rr[2].q[h]);
@@ -249,7 +251,7 @@ __global__ void __launch_bounds__(E3T, 1) k_el3d_vel_stream(ElParams P, int64_t 
 }
 
 // ---------------------------------------------------------------- stress phase
-// slot rows: [vx(F) TM | vm(F) TM | vs tile(F-1) TM+2H | vx tile(s) TM+2H | vm tile(s) TM+2H]
+// slot rows: [vx(F) TM | vm(F) TM | vs tile(F-1) | vx tile(s) | vm tile(s)] (vs, vx: to-half tiles; vm: to-int)
 // SAMPLE: energy sample step (separate instantiation: the energy code stays out of the loop
 // body -- instruction cache -- and the register budget of the other steps)
 template <int V, int ORDER, bool SAMPLE>
@@ -263,8 +265,9 @@ __global__ void __launch_bounds__(E3T, 1)
     const int64_t pitch = P.g.pitch, slab = P.g.slab;
     const int TM = E3T * ECPT / nx, TPR = nx / ECPT;
     constexpr int H = ORDER / 2;
-    const E3Layout L(smem, 5 * TM + 6 * H, TM, pitch, 12);
-    const int o_vm = TM, o_vs = 2 * TM, o_vxt = 3 * TM + 2 * H, o_vmt = 4 * TM + 4 * H;
+    constexpr int TH = 2 * H - 1;  // halo rows of a one-sided tile
+    const E3Layout L(smem, 5 * TM + 3 * TH, TM, pitch, 12);
+    const int o_vm = TM, o_vs = 2 * TM, o_vxt = 3 * TM + TH, o_vmt = 4 * TM + 2 * TH;
     const int tid = threadIdx.x, j = tid / TPR, x = (tid % TPR) * ECPT;
     constexpr bool comp = V != 0;
     constexpr int NOWN = comp ? 12 : 6;  // sxx sss smm sxs sxm sms [residuals]
@@ -310,12 +313,12 @@ __global__ void __launch_bounds__(E3T, 1)
             const int F = F0 + i, k = (gi0 + i) % QR;
             __half* d = L.sl(k);
             const int64_t mo = (int64_t)m0 * pitch;
-            mbar_arrive_expect_tx(&L.bar[k], (uint32_t)((5 * TM + 6 * H) * pitch * sizeof(__half)));
+            mbar_arrive_expect_tx(&L.bar[k], (uint32_t)((5 * TM + 3 * TH) * pitch * sizeof(__half)));
             tma_load_1d(d, VX + e_row(F) * slab + mo, tmb, &L.bar[k]);
             tma_load_1d(d + o_vm * pitch, VM + e_row(F) * slab + mo, tmb, &L.bar[k]);
-            a3_rows(d + o_vs * pitch, VS, slab, e_row(F - 1), m0 - H, m0 + TM + H, nm, pitch, &L.bar[k]);
-            a3_rows(d + o_vxt * pitch, VX, slab, e_row(F - 2), m0 - H, m0 + TM + H, nm, pitch, &L.bar[k]);
-            a3_rows(d + o_vmt * pitch, VM, slab, e_row(F - 2), m0 - H, m0 + TM + H, nm, pitch, &L.bar[k]);
+            a3_rows(d + o_vs * pitch, VS, slab, e_row(F - 1), m0 - H + 1, m0 + TM + H, nm, pitch, &L.bar[k]);
+            a3_rows(d + o_vxt * pitch, VX, slab, e_row(F - 2), m0 - H + 1, m0 + TM + H, nm, pitch, &L.bar[k]);
+            a3_rows(d + o_vmt * pitch, VM, slab, e_row(F - 2), m0 - H, m0 + TM + H - 1, nm, pitch, &L.bar[k]);
         };
         auto issue_own = [&](int kk) {
             const int os = (gk0 + kk) & 1;
@@ -342,7 +345,7 @@ __global__ void __launch_bounds__(E3T, 1)
             const int64_t jr = (int64_t)j * pitch;
             e3_shift(qvx, e_ld8(d + jr + x));
             e3_shift(qvm, e_ld8(d + o_vm * pitch + jr + x));
-            e3_shift(qvs, e_ld8(d + o_vs * pitch + jr + H * pitch + x));
+            e3_shift(qvs, e_ld8(d + o_vs * pitch + jr + (H - 1) * pitch + x));  // to-half tile: row m at j + H - 1
             const int s = F0 + i - 2;
             if (s >= sb) {
                 const int kr = s - sb, os = (gk0 + kr) & 1;
@@ -355,9 +358,9 @@ __global__ void __launch_bounds__(E3T, 1)
                 const int64_t goff = (int64_t)s * slab + off;
                 const bool inner = s >= G && s < ns - G;  // stores that never touch a ghost slab
                 // tile row pointers at row m - 2 (row m at index j + H; 2nd order never reads m - 2)
-                const __half* vxt = d + o_vxt * pitch + jr + (H - 2) * pitch;
-                const __half* vmt = d + o_vmt * pitch + jr + (H - 2) * pitch;
-                const __half* vst = pd + o_vs * pitch + jr + (H - 2) * pitch;
+                const __half* vxt = d + o_vxt * pitch + jr + (H - 3) * pitch;  // (to-half tile)
+                const __half* vmt = d + o_vmt * pitch + jr + (H - 2) * pitch;  // (to-int tile)
+                const __half* vst = pd + o_vs * pitch + jr + (H - 3) * pitch;  // (to-half tile)
                 // normal stresses from dvx, dvs, dvm (to-int taps)
                 const E8 dvx = e_xfold<ORDER>(c, vxt + 2 * pitch, x, xl, xr, true);
                 const E8 dvs = e_sfold<ORDER>(c, qvs[0], qvs[1], qvs[2], qvs[3]);
@@ -499,11 +502,11 @@ __global__ void __launch_bounds__(E3T, 1)
 
 static size_t e3_vel_bytes(int64_t nx, int order) {
     const int64_t TM = E3T * ECPT / nx, H = order / 2;
-    return 128 + ((size_t)QR * (6 * TM + 6 * H) + 2 * 6 * TM) * nx * sizeof(__half);
+    return 128 + ((size_t)QR * (6 * TM + 3 * (2 * H - 1)) + 2 * 6 * TM) * nx * sizeof(__half);
 }
 static size_t e3_stress_bytes(int64_t nx, int order) {
     const int64_t TM = E3T * ECPT / nx, H = order / 2;
-    return 128 + ((size_t)QR * (5 * TM + 6 * H) + 2 * 12 * TM) * nx * sizeof(__half);
+    return 128 + ((size_t)QR * (5 * TM + 3 * (2 * H - 1)) + 2 * 12 * TM) * nx * sizeof(__half);
 }
 
 bool el3d_stream_eligible(int64_t nx, int64_t nm, int64_t pitch, int max_smem) {
