@@ -81,7 +81,7 @@ struct Q4 {
 
 // SAMPLE: energy sample step (a separate instantiation: the fp64 accumulators and energy code
 // stay out of the register budget of the other steps)
-template <int V, int ORDER, bool RM, bool SAMPLE>
+template <int V, int ORDER, bool RM, bool SAMPLE, bool FS>
 __global__ void __launch_bounds__(512, 1)
     k_el2d_fused(ElParams P, El2In in, StreamIO IO, int64_t n, double src, int64_t eidx) {
     constexpr bool sample = SAMPLE;
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(512, 1)
     const int F0 = y0 - 3, NI = y1 - y0 + 6;
     const int tid = threadIdx.x, x = tid * ECPT;
     constexpr bool comp = V != 0;
-    const bool fs = P.fs != 0;
+    constexpr bool fs = FS;  // free surfaces (else periodic): a template parameter, the row logic folds away
     const uint32_t rb = (uint32_t)(nx * sizeof(__half));
     // rows outside the domain: periodic -> wrapped; free surface -> clamped (those values
     // are never used: image rows replace them); tap rows with images use the ghost slabs
@@ -449,12 +449,17 @@ bool el2d_fused_eligible(int64_t nx, int64_t ns, int max_smem) {
     return el2d_fused_smem_bytes(nx) <= (size_t)max_smem;
 }
 
+template <int V, int O, bool F>
+static void el2f_attrs1(int bytes) {
+    cudaFuncSetAttribute((void*)k_el2d_fused<V, O, false, false, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute((void*)k_el2d_fused<V, O, true, false, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute((void*)k_el2d_fused<V, O, false, true, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute((void*)k_el2d_fused<V, O, true, true, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
 template <int V, int O>
 static void el2f_attrs(int bytes) {
-    cudaFuncSetAttribute((void*)k_el2d_fused<V, O, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    cudaFuncSetAttribute((void*)k_el2d_fused<V, O, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    cudaFuncSetAttribute((void*)k_el2d_fused<V, O, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    cudaFuncSetAttribute((void*)k_el2d_fused<V, O, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    el2f_attrs1<V, O, false>(bytes);
+    el2f_attrs1<V, O, true>(bytes);
 }
 
 cudaError_t el2d_fused_prepare(int64_t nx) {
@@ -485,15 +490,22 @@ void launch_el2d_fused(int variant, int order, const ElParams& P, const El2In& i
                        int64_t n, double src, int sample, int64_t eidx, cudaStream_t st) {
     void* fn = nullptr;
     const bool rm = el2f_rowmed(P);
-    if (rm && sample) {
-        EL2F_DISPATCH(variant, order, (fn = (void*)k_el2d_fused<V_, O_, true, true>))
-    } else if (rm) {
-        EL2F_DISPATCH(variant, order, (fn = (void*)k_el2d_fused<V_, O_, true, false>))
-    } else if (sample) {
-        EL2F_DISPATCH(variant, order, (fn = (void*)k_el2d_fused<V_, O_, false, true>))
-    } else {
-        EL2F_DISPATCH(variant, order, (fn = (void*)k_el2d_fused<V_, O_, false, false>))
+#define EL2F_PICK(FS_)                                                                    \
+    if (rm && sample) {                                                                   \
+        EL2F_DISPATCH(variant, order, (fn = (void*)k_el2d_fused<V_, O_, true, true, FS_>))   \
+    } else if (rm) {                                                                      \
+        EL2F_DISPATCH(variant, order, (fn = (void*)k_el2d_fused<V_, O_, true, false, FS_>))  \
+    } else if (sample) {                                                                  \
+        EL2F_DISPATCH(variant, order, (fn = (void*)k_el2d_fused<V_, O_, false, true, FS_>))  \
+    } else {                                                                              \
+        EL2F_DISPATCH(variant, order, (fn = (void*)k_el2d_fused<V_, O_, false, false, FS_>)) \
     }
+    if (P.fs) {
+        EL2F_PICK(true)
+    } else {
+        EL2F_PICK(false)
+    }
+#undef EL2F_PICK
     void* args[] = {(void*)&P, (void*)&in, (void*)&IO, (void*)&n, (void*)&src, (void*)&eidx};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nblocks);
