@@ -114,3 +114,18 @@ def test_fused3d_zero_steps_and_zero_state():
     z.run(hw.Variant.OP3, sz)
     for n in z.FIELDS:
         assert not np.any(getattr(sz, n).values.view(np.uint16)), n
+
+
+def test_fused3d_source_on_tile_and_slab_edges():
+    """Pressure source on a mid-tile edge row and a slab-segment boundary (the halo rows and the
+    warm-up slab recompute neighbours' values: the source must be injected exactly once)."""
+    for iz, iy in ((0, 7), (5, 8), (11, 15)):
+        s, st = _case(256, 16, 12, 9)
+        src = hw.SourceSpec(hw.SourceKind.PRESSURE_POINT, 17, iy, hw.RickerSpec(1 / (10 * s.grid.dx), amplitude=5.0),
+                            iz=iz)
+        s = hw.AcousticSolver(s.grid, s.medium, src, stencil_precision=hw.Precision.FP16,
+                              receivers=((17, iy, iz), (3, 0, 0)), energy_every=4)
+        ref = oracle.run_solver(s, hw.Variant.OP3, st)
+        out = s.run(hw.Variant.OP3, st)
+        assert s.kernel_path() == "fused3d"
+        _check(s, st, out, ref)

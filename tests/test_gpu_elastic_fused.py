@@ -125,3 +125,13 @@ def test_fused_el_free_surface_syy_rows_bit_zero():
         assert np.all(rows[0].view(np.uint16) == 0)
         assert np.all(rows[-1].view(np.uint16) == 0)
     assert np.any(st.syy.values[1:-1] != 0.0)
+
+
+@pytest.mark.parametrize("fs", [True, False])
+def test_fused_el_width_not_multiple_of_256(fs):
+    """nx = 1000: 125 threads per CTA (a partial last warp) on a grid large enough for the one-pass path."""
+    s, st = _case(1000, 2100, 6, fs=fs, src_row=700, every=3)
+    assert s.kernel_path() == "fused2d-el"
+    ref = oracle.run_solver(s, hw.Variant.OP6, st)
+    out = s.run(hw.Variant.OP6, st)
+    _check(s, st, out, ref)
