@@ -374,6 +374,7 @@ struct hw_solver {
     bool ac3_stream = false;  // streaming 3D acoustic phases
     bool fused3 = false;      // one-pass 3D acoustic step (2nd order), ping-pong A <-> B
     bool fused_el = false;    // one-pass 2D elastic step, ping-pong A <-> B
+    bool fused_el3 = false;   // one-pass 3D elastic step (2nd order), ping-pong A <-> B
     bool el3_stream = false;  // streaming 3D elastic phases
     int stream_blocks = 0;
     unsigned int* counter = nullptr;  // CTA arrival counter of the streaming stress kernel
@@ -767,7 +768,25 @@ int setup_handle(hw_solver* h) {
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
             h->ac3_stream = true;
         }
-        if (want && !h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
+        // one-pass 3D elastic step (2nd order, single domain; opt-in: HALFWAVE_FUSED_EL3=1)
+        const char* fe3 = getenv("HALFWAVE_FUSED_EL3");
+        if (want && fe3 && strcmp(fe3, "1") == 0 && !h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
+            h->world == 1 && h->transport == 0 &&
+            el3d_fused_eligible(desc->nx, desc->nm, desc->ns, h->g.pitch, desc->order, dev_smem)) {
+            for (int j = 0; j < 2 * h->nsol; j++) {
+                int f = h->ext[j % h->nsol];
+                size_t bytes = (size_t)(field_rows(h, f) + 2 * G) * h->g.slab * esz;
+                if (cudaMalloc(&h->mem_b[j], bytes) != cudaSuccess) return fail(HW_ECUDA, "out of memory (B)");
+                CU(cudaMemset(h->mem_b[j], 0, bytes));
+            }
+            if (el3d_fused_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "fused 3D elastic setup failed");
+            const int64_t units = (desc->nm / (2048 / desc->nx)) * max_rows;
+            int64_t nbs = units / 4;
+            if (nbs < 1) nbs = 1;
+            h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
+            h->fused_el3 = true;
+        }
+        if (want && !h->fused_el3 && !h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
             el3d_stream_eligible(desc->nx, desc->nm, h->g.pitch, dev_smem)) {
             if (el3d_stream_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "streaming kernel setup failed");
             const int64_t units = (desc->nm / (2048 / desc->nx)) * max_rows;
@@ -776,7 +795,7 @@ int setup_handle(hw_solver* h) {
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
             h->el3_stream = true;
         }
-        if (h->el_stream || h->ac3_stream || h->el3_stream || h->fused || h->fused3 || h->fused_el) {
+        if (h->el_stream || h->ac3_stream || h->el3_stream || h->fused || h->fused3 || h->fused_el || h->fused_el3) {
             CU(cudaMalloc(&h->counter, sizeof(unsigned int)));
             CU(cudaMemset(h->counter, 0, sizeof(unsigned int)));
         }
@@ -1303,6 +1322,32 @@ static void fused_el_bufs(const hw_solver* h, int cur, ElParams& P, El2In& in) {
     }
 }
 
+// The same for the one-pass 3D elastic kernel.
+static void fused_el3_bufs(const hw_solver* h, int cur, ElParams& P, El3In& in) {
+    const int64_t ghost = (int64_t)G * h->g.slab * 2;  // bytes before row 0
+    void* const* rd = cur ? h->mem_b : h->mem;
+    void* const* wr = cur ? h->mem : h->mem_b;
+    for (int j = 0; j < 2 * h->nsol; j++) {
+        const int f = h->ext[j % h->nsol];
+        const bool r = j >= h->nsol;
+        FieldView* o = nullptr;
+        const __half** q = nullptr;
+        switch (f) {
+            case F_VX: o = r ? &P.rvx : &P.vx; q = r ? &in.rvx : &in.vx; break;
+            case F_VS: o = r ? &P.rvs : &P.vs; q = r ? &in.rvs : &in.vs; break;
+            case F_VM: o = r ? &P.rvm : &P.vm; q = r ? &in.rvm : &in.vm; break;
+            case F_SXX: o = r ? &P.rsxx : &P.sxx; q = r ? &in.rsxx : &in.sxx; break;
+            case F_SSS: o = r ? &P.rsss : &P.sss; q = r ? &in.rsss : &in.sss; break;
+            case F_SMM: o = r ? &P.rsmm : &P.smm; q = r ? &in.rsmm : &in.smm; break;
+            case F_SXS: o = r ? &P.rsxs : &P.sxs; q = r ? &in.rsxs : &in.sxs; break;
+            case F_SXM: o = r ? &P.rsxm : &P.sxm; q = r ? &in.rsxm : &in.sxm; break;
+            default: o = r ? &P.rsms : &P.sms; q = r ? &in.rsms : &in.sms; break;
+        }
+        o->base = (char*)wr[j] + ghost;
+        *q = (const __half*)((const char*)rd[j] + ghost);
+    }
+}
+
 static void fused_bufs(const hw_solver* h, __half* bufs[2][FUSED_NSTREAM]) {
     const int64_t ghost = (int64_t)G * h->g.slab * 2;  // bytes before row 0
     for (int j = 0; j < FUSED_NSTREAM; j++) {  // external order p vx vy rp rvx rvy == stream order
@@ -1400,6 +1445,25 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
             h->launches++;
             cur ^= 1;
         }
+    } else if (h->fused_el3) {  // one-pass 3D elastic kernel, ping-pong A <-> B; traces from the epilogue
+        const StreamIO IO = stream_io(h, C);
+        int cur = 0;
+        for (int64_t n = 0; n < nt; n++) {
+            ElParams P = C.L;
+            El3In in;
+            fused_el3_bufs(h, cur, P, in);
+            const int sample = energy && ((n + 1) % C.every == 0);
+            launch_el3d_fused(variant, P, in, IO, h->stream_blocks, n, src ? src[n] : 0.0, sample, (n + 1) / C.every,
+                              h->st);
+            h->launches++;
+            if (C.E.n_rec > 0) {  // receiver traces of v_slow after the step, from the buffer just written
+                EpParams E = C.E;
+                E.trace_base = P.vs.base;
+                launch_epilogue(h->LU, E, n, 0, 0, h->st);
+                h->launches++;
+            }
+            cur ^= 1;
+        }
     } else if (h->fused_el) {  // one-pass 2D elastic kernel, ping-pong A <-> B: step n reads buffer n % 2
         const StreamIO IO = stream_io(h, C);
         int cur = 0;
@@ -1457,7 +1521,7 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
 // home so buffer A is always current between calls.
 static int fused_copy_back(hw_solver* h, int64_t executed, int32_t variant) {
     const int64_t launches = h->tb2 ? (executed + 1) / 2 : executed;
-    if (!(h->fused || h->fused3 || h->fused_el) || h->small || (launches & 1) == 0) return HW_OK;  // the small-grid kernel writes A itself
+    if (!(h->fused || h->fused3 || h->fused_el || h->fused_el3) || h->small || (launches & 1) == 0) return HW_OK;  // the small-grid kernel writes A itself
     const int nf = variant == HW_NAIVE ? h->nsol : 2 * h->nsol;  // naive runs never touch residuals
     for (int j = 0; j < nf; j++) {
         int f = h->ext[j % h->nsol];
@@ -1698,7 +1762,7 @@ int64_t hw_last_launch_count(const hw_solver* h) { return h ? h->launches : 0; }
 
 const char* hw_kernel_path(const hw_solver* h) {
     if (!h) return "";
-    return (h->small || h->small_el) ? "small2d" : h->tb2 ? "fused2d-tb2" : h->fused ? "fused2d" : h->fused3 ? "fused3d" : h->fused_el ? "fused2d-el" : (h->el_stream ? "stream2d" : ((h->ac3_stream || h->el3_stream) ? "stream3d" : "generic"));
+    return (h->small || h->small_el) ? "small2d" : h->tb2 ? "fused2d-tb2" : h->fused ? "fused2d" : h->fused3 ? "fused3d" : h->fused_el ? "fused2d-el" : h->fused_el3 ? "fused3d-el" : (h->el_stream ? "stream2d" : ((h->ac3_stream || h->el3_stream) ? "stream3d" : "generic"));
 }
 
 int32_t hw_transport(const hw_solver* h) { return h ? h->transport : -1; }

@@ -117,6 +117,15 @@ bool el2d_fused_eligible(int64_t nx, int64_t ns, int max_smem);
 cudaError_t el2d_fused_prepare(int64_t nx);
 void launch_el2d_fused(int variant, int order, const ElParams& P, const El2In& in, const StreamIO& IO, int nblocks,
                        int64_t n, double src, int sample, int64_t eidx, cudaStream_t st);
+// one-pass 3D elastic step, 2nd order (hw_elastic3d_fused.cu)
+struct El3In {
+    const __half *vx, *vs, *vm, *sxx, *sss, *smm, *sxs, *sxm, *sms;
+    const __half *rvx, *rvs, *rvm, *rsxx, *rsss, *rsmm, *rsxs, *rsxm, *rsms;
+};
+bool el3d_fused_eligible(int64_t nx, int64_t nm, int64_t ns, int64_t pitch, int order, int max_smem);
+cudaError_t el3d_fused_prepare(int64_t nx);
+void launch_el3d_fused(int variant, const ElParams& P, const El3In& in, const StreamIO& IO, int nblocks, int64_t n,
+                       double src, int sample, int64_t eidx, cudaStream_t st);
 // streaming 3D elastic phase kernels (hw_elastic3d_stream.cu)
 bool el3d_stream_eligible(int64_t nx, int64_t nm, int64_t pitch, int max_smem);
 cudaError_t el3d_stream_prepare(int64_t nx);
