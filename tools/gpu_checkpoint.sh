@@ -7,6 +7,7 @@ set -u
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/ck_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/ck_pytest.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/ck_smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/ck_smoke.log
 timeout 900 python bench.py > gpurun_out/ck_bench.jsonl 2> gpurun_out/ck_bench.err; echo "bench rc=$?"
 timeout 900 python bench.py --impl reference > gpurun_out/ck_bench_ref.jsonl 2> gpurun_out/ck_bench_ref.err; echo "ref rc=$?"
 if python tools/profile_step.py 20 > gpurun_out/ck_step.log 2>&1; then
@@ -15,4 +16,4 @@ if python tools/profile_step.py 20 > gpurun_out/ck_step.log 2>&1; then
   ncu --set full --clock-control none --import-source on -k regex:k_ac2d_fused -s 5 -c 1 \
       -o gpurun_out/ck_fused_full python tools/profile_step.py 20 > gpurun_out/ck_ncu.log 2>&1
 fi
-tail -3 gpurun_out/ck_pytest.log; cat gpurun_out/ck_bench.jsonl | cut -c1-300
+tail -3 gpurun_out/ck_pytest.log; tail -2 gpurun_out/ck_smoke.log; cat gpurun_out/ck_bench.jsonl | cut -c1-300
