@@ -373,6 +373,7 @@ struct hw_solver {
     bool el_stream = false;   // streaming 2D elastic phases
     bool ac3_stream = false;  // streaming 3D acoustic phases
     bool fused3 = false;      // one-pass 3D acoustic step (2nd order), ping-pong A <-> B
+    bool fused3_32 = false;   // the same in binary32 lanes (config 3's fp32 arm), ping-pong A <-> B
     bool fused_el = false;    // one-pass 2D elastic step, ping-pong A <-> B
     bool fused_el3 = false;   // one-pass 3D elastic step (2nd order), ping-pong A <-> B
     bool el3_stream = false;  // streaming 3D elastic phases
@@ -759,6 +760,23 @@ int setup_handle(hw_solver* h) {
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
             h->fused3 = true;
         }
+        // the one-pass 3D acoustic step in binary32 lanes (BASELINE config 3's fp32 arm)
+        if (want && !(f3e && strcmp(f3e, "0") == 0) && h->ac && h->d3 && h->LS == 32 && h->LU == 32 &&
+            h->world == 1 && h->transport == 0 &&
+            ac3d_fused32_eligible(desc->nx, desc->nm, desc->ns, h->g.pitch, desc->order, dev_smem)) {
+            for (int j = 0; j < 2 * h->nsol; j++) {
+                int f = h->ext[j % h->nsol];
+                size_t bytes = (size_t)(field_rows(h, f) + 2 * G) * h->g.slab * esz;
+                if (cudaMalloc(&h->mem_b[j], bytes) != cudaSuccess) return fail(HW_ECUDA, "out of memory (B)");
+                CU(cudaMemset(h->mem_b[j], 0, bytes));
+            }
+            if (ac3d_fused32_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "fused 3D fp32 kernel setup failed");
+            const int64_t units = (desc->nm / (2048 / desc->nx)) * max_rows;
+            int64_t nbs = units / 4;
+            if (nbs < 1) nbs = 1;
+            h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
+            h->fused3_32 = true;
+        }
         if (want && !h->fused3 && h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
             ac3d_stream_eligible(desc->nx, desc->nm, h->g.pitch, dev_smem)) {
             if (ac3d_stream_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "streaming kernel setup failed");
@@ -795,7 +813,8 @@ int setup_handle(hw_solver* h) {
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
             h->el3_stream = true;
         }
-        if (h->el_stream || h->ac3_stream || h->el3_stream || h->fused || h->fused3 || h->fused_el || h->fused_el3) {
+        if (h->el_stream || h->ac3_stream || h->el3_stream || h->fused || h->fused3 || h->fused3_32 || h->fused_el ||
+            h->fused_el3) {
             CU(cudaMalloc(&h->counter, sizeof(unsigned int)));
             CU(cudaMemset(h->counter, 0, sizeof(unsigned int)));
         }
@@ -1294,7 +1313,7 @@ static AcFusedParams fused_params(const hw_solver* h, int64_t nt) {
 // Field views / input pointers of the one-pass 3D kernel reading buffer `cur` (0 = A,
 // 1 = B) and writing the other one (same ghost policies: write-through periodic slabs).
 static void fused3_bufs(const hw_solver* h, int cur, AcParams& P, Ac3In& in) {
-    const int64_t ghost = (int64_t)G * h->g.slab * 2;  // bytes before row 0
+    const int64_t ghost = (int64_t)G * h->g.slab * lane_bytes(h->LU);  // bytes before row 0
     const __half* src[2 * F_N] = {};
     for (int j = 0; j < 2 * h->nsol; j++) {
         const int f = h->ext[j % h->nsol];
@@ -1431,7 +1450,7 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
             if ((rc = exchange_nccl_list(h, xfers_fused(h, cur)))) return rc;
         }
         if (nt > 0) CU(cudaStreamWaitEvent(h->st, h->ev_int[(nt - 1) & 1], 0));
-    } else if (h->fused3) {  // one-pass 3D kernel, ping-pong A <-> B: step n reads buffer n % 2
+    } else if (h->fused3 || h->fused3_32) {  // one-pass 3D kernel, ping-pong A <-> B: step n reads buffer n % 2
         const StreamIO IO = stream_io(h, C);
         const int sk = h->d.src_kind;
         int cur = 0;
@@ -1440,8 +1459,9 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
             Ac3In in;
             fused3_bufs(h, cur, P, in);
             const int sample = energy && ((n + 1) % C.every == 0);
-            launch_ac3d_fused(variant, P, in, IO, h->stream_blocks, n, (src && sk == HW_SRC_PRESSURE) ? src[n] : 0.0,
-                              sample, (n + 1) / C.every, h->st);
+            const double sv = (src && sk == HW_SRC_PRESSURE) ? src[n] : 0.0;
+            if (h->fused3_32) launch_ac3d_fused32(variant, P, in, IO, h->stream_blocks, n, sv, sample, (n + 1) / C.every, h->st);
+            else launch_ac3d_fused(variant, P, in, IO, h->stream_blocks, n, sv, sample, (n + 1) / C.every, h->st);
             h->launches++;
             cur ^= 1;
         }
@@ -1521,7 +1541,7 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
 // home so buffer A is always current between calls.
 static int fused_copy_back(hw_solver* h, int64_t executed, int32_t variant) {
     const int64_t launches = h->tb2 ? (executed + 1) / 2 : executed;
-    if (!(h->fused || h->fused3 || h->fused_el || h->fused_el3) || h->small || (launches & 1) == 0) return HW_OK;  // the small-grid kernel writes A itself
+    if (!(h->fused || h->fused3 || h->fused3_32 || h->fused_el || h->fused_el3) || h->small || (launches & 1) == 0) return HW_OK;  // the small-grid kernel writes A itself
     const int nf = variant == HW_NAIVE ? h->nsol : 2 * h->nsol;  // naive runs never touch residuals
     for (int j = 0; j < nf; j++) {
         int f = h->ext[j % h->nsol];
@@ -1762,7 +1782,7 @@ int64_t hw_last_launch_count(const hw_solver* h) { return h ? h->launches : 0; }
 
 const char* hw_kernel_path(const hw_solver* h) {
     if (!h) return "";
-    return (h->small || h->small_el) ? "small2d" : h->tb2 ? "fused2d-tb2" : h->fused ? "fused2d" : h->fused3 ? "fused3d" : h->fused_el ? "fused2d-el" : h->fused_el3 ? "fused3d-el" : (h->el_stream ? "stream2d" : ((h->ac3_stream || h->el3_stream) ? "stream3d" : "generic"));
+    return (h->small || h->small_el) ? "small2d" : h->tb2 ? "fused2d-tb2" : h->fused ? "fused2d" : h->fused3 ? "fused3d" : h->fused3_32 ? "fused3d-f32" : h->fused_el ? "fused2d-el" : h->fused_el3 ? "fused3d-el" : (h->el_stream ? "stream2d" : ((h->ac3_stream || h->el3_stream) ? "stream3d" : "generic"));
 }
 
 int32_t hw_transport(const hw_solver* h) { return h ? h->transport : -1; }

@@ -31,43 +31,64 @@
 
 namespace hw {
 
-constexpr int X3T = 512;  // threads per CTA
-constexpr int X3C = 4;    // cells per thread (two half2)
+#ifndef HW_X3C
+#define HW_X3C 4
+#endif
+constexpr int X3C = HW_X3C;        // cells per thread (X3C / 2 half2): 4 or 8
+constexpr int X3T = 2048 / X3C;    // threads per CTA (TM = 2048 / nx either way)
+constexpr int X3P = X3C / 2;       // half2 pairs per thread
 constexpr int XR = 4;     // tap ring slots
 
 struct E4 {
-    EH2 q[2];
+    EH2 q[X3P];
 };
 
 __device__ __forceinline__ E4 ld4(const __half* p) {
     E4 r;
-    const uint2 u = *reinterpret_cast<const uint2*>(p);
-    *reinterpret_cast<unsigned int*>(&r.q[0].h2) = u.x;
-    *reinterpret_cast<unsigned int*>(&r.q[1].h2) = u.y;
+    if constexpr (X3P == 2) {
+        const uint2 u = *reinterpret_cast<const uint2*>(p);
+        *reinterpret_cast<unsigned int*>(&r.q[0].h2) = u.x;
+        *reinterpret_cast<unsigned int*>(&r.q[1].h2) = u.y;
+    } else {
+        const uint4 u = *reinterpret_cast<const uint4*>(p);
+        *reinterpret_cast<unsigned int*>(&r.q[0].h2) = u.x;
+        *reinterpret_cast<unsigned int*>(&r.q[1].h2) = u.y;
+        *reinterpret_cast<unsigned int*>(&r.q[2].h2) = u.z;
+        *reinterpret_cast<unsigned int*>(&r.q[3].h2) = u.w;
+    }
     return r;
 }
 
 __device__ __forceinline__ void st4(__half* p, const E4& v) {
-    uint2 u;
-    u.x = *reinterpret_cast<const unsigned int*>(&v.q[0].h2);
-    u.y = *reinterpret_cast<const unsigned int*>(&v.q[1].h2);
-    *reinterpret_cast<uint2*>(p) = u;
+    if constexpr (X3P == 2) {
+        uint2 u;
+        u.x = *reinterpret_cast<const unsigned int*>(&v.q[0].h2);
+        u.y = *reinterpret_cast<const unsigned int*>(&v.q[1].h2);
+        *reinterpret_cast<uint2*>(p) = u;
+    } else {
+        uint4 u;
+        u.x = *reinterpret_cast<const unsigned int*>(&v.q[0].h2);
+        u.y = *reinterpret_cast<const unsigned int*>(&v.q[1].h2);
+        u.z = *reinterpret_cast<const unsigned int*>(&v.q[2].h2);
+        u.w = *reinterpret_cast<const unsigned int*>(&v.q[3].h2);
+        *reinterpret_cast<uint4*>(p) = u;
+    }
 }
 
 // x derivative of 4 cells (periodic) from a shared row; to_int: shifts (-1, 0) else (0, 1) (2nd order)
 __device__ __forceinline__ E4 xf4(const __half c[4], const __half* row, int x, int xl, int xr, bool to_int) {
-    EH2 Q[4];
+    EH2 Q[X3P + 2];
     Q[0] = e_ld2(row + xl);
     const E4 own = ld4(row + x);
-    Q[1] = own.q[0];
-    Q[2] = own.q[1];
-    Q[3] = e_ld2(row + xr);
-    EH2 S[3];
 #pragma unroll
-    for (int j = 0; j < 3; j++) S[j] = vshift<16, 2>(Q[j], Q[j + 1]);
+    for (int j = 0; j < X3P; j++) Q[1 + j] = own.q[j];
+    Q[X3P + 1] = e_ld2(row + xr);
+    EH2 S[X3P + 1];
+#pragma unroll
+    for (int j = 0; j < X3P + 1; j++) S[j] = vshift<16, 2>(Q[j], Q[j + 1]);
     E4 r;
 #pragma unroll
-    for (int j = 0; j < 2; j++)
+    for (int j = 0; j < X3P; j++)
         r.q[j] = to_int ? e_fold<2>(c, Q[j], S[j], Q[j + 1], S[j + 1]) : e_fold<2>(c, S[j], Q[j + 1], S[j + 1], Q[j + 2]);
     return r;
 }
@@ -76,20 +97,20 @@ __device__ __forceinline__ E4 xf4(const __half c[4], const __half* row, int x, i
 __device__ __forceinline__ E4 f4(const __half c[4], const E4& a, const E4& b) {
     E4 r;
 #pragma unroll
-    for (int j = 0; j < 2; j++) r.q[j] = e_fold<2>(c, a.q[j], a.q[j], b.q[j], b.q[j]);
+    for (int j = 0; j < X3P; j++) r.q[j] = e_fold<2>(c, a.q[j], a.q[j], b.q[j], b.q[j]);
     return r;
 }
 
 __device__ __forceinline__ E4 add4(const E4& a, const E4& b) {
     E4 r;
 #pragma unroll
-    for (int j = 0; j < 2; j++) r.q[j] = EO2::add(a.q[j], b.q[j]);
+    for (int j = 0; j < X3P; j++) r.q[j] = EO2::add(a.q[j], b.q[j]);
     return r;
 }
 
 __device__ __forceinline__ void track4(__half2& acc, const E4& v) {
 #pragma unroll
-    for (int j = 0; j < 2; j++) acc = __hmax2_nan(acc, __habs2(v.q[j].h2));
+    for (int j = 0; j < X3P; j++) acc = __hmax2_nan(acc, __habs2(v.q[j].h2));
 }
 
 // store of a row of 4 cells at element offset goff = s * slab + off; periodic ghost slabs written through
@@ -115,9 +136,9 @@ __device__ __forceinline__ void x3_finish_v(EH2 a, bool rm, float rc, const Plan
 
 // point source into the right-hand side of the source cell (the first op of finish()); a
 // register select per pair (no dynamic indexing)
-__device__ __forceinline__ void add_src2(EH2 r[2], int sj, int sln, __half srch) {
+__device__ __forceinline__ void add_src2(EH2 r[X3P], int sj, int sln, __half srch) {
 #pragma unroll
-    for (int h = 0; h < 2; h++)
+    for (int h = 0; h < X3P; h++)
         if (h == sj) {
             if (sln == 0) r[h].e[0] = __hadd_rn(r[h].e[0], srch);
             else r[h].e[1] = __hadd_rn(r[h].e[1], srch);
@@ -272,7 +293,7 @@ __global__ void __launch_bounds__(X3T, 1)
                     add_src2(as.q, sj, sln, srch);
                 }
 #pragma unroll
-                for (int h = 0; h < 2; h++) {
+                for (int h = 0; h < X3P; h++) {
                     x3_finish_v<V>(ax.q[h], rm, rcx, P.rho_x, k, m, x + 2 * h, dt, dt2, -1, srch, 0.0, vx.q[h], rvx.q[h]);
                     x3_finish_v<V>(as.q[h], rm, rcs, P.rho_s, k, m, x + 2 * h, dt, dt2, -1, srch, 0.0, vsv.q[h], rvs.q[h]);
                     x3_finish_v<V>(am.q[h], rm, rcm, P.rho_m, k, m, x + 2 * h, dt, dt2, -1, srch, 0.0, vm.q[h], rvm.q[h]);
@@ -306,7 +327,7 @@ __global__ void __launch_bounds__(X3T, 1)
                                       f4(c, ld4(tap(s1, T_SMM) + x), ld4(tap(s1, T_SMM) + pitch + x)));
                     const float rc = rm ? e_rcp_at(P.rho_m, k, mlo) : 0.f;
 #pragma unroll
-                    for (int q = 0; q < 2; q++)
+                    for (int q = 0; q < X3P; q++)
                         x3_finish_v<V>(a.q[q], rm, rc, P.rho_m, k, mlo, x + 2 * q, dt, dt2, -1, srch, 0.0, h.q[q], rh.q[q]);
                     st4(vt(gen, 2) + x, h);
                 } else if (j == 1) {
@@ -318,7 +339,7 @@ __global__ void __launch_bounds__(X3T, 1)
                                       f4(c, ld4(tap(s1, T_SXM) + hr + x), ld4(tap(s1, T_SXM) + hr + pitch + x)));
                     const float rc = rm ? e_rcp_at(P.rho_x, k, mhi) : 0.f;
 #pragma unroll
-                    for (int q = 0; q < 2; q++)
+                    for (int q = 0; q < X3P; q++)
                         x3_finish_v<V>(a.q[q], rm, rc, P.rho_x, k, mhi, x + 2 * q, dt, dt2, -1, srch, 0.0, h.q[q], rh.q[q]);
                     st4(vt(gen, 0) + hr + x, h);
                 } else if (j == 2) {
@@ -333,7 +354,7 @@ __global__ void __launch_bounds__(X3T, 1)
                     }
                     const float rc = rm ? e_rcp_at(P.rho_s, k, mhi) : 0.f;
 #pragma unroll
-                    for (int q = 0; q < 2; q++)
+                    for (int q = 0; q < X3P; q++)
                         x3_finish_v<V>(a.q[q], rm, rc, P.rho_s, k, mhi, x + 2 * q, dt, dt2, -1, srch, 0.0, h.q[q], rh.q[q]);
                     st4(vt(gen, 1) + hr + x, h);
                 }
@@ -373,9 +394,9 @@ __global__ void __launch_bounds__(X3T, 1)
                     lam_r = e_val_at(P.lam, sw, m);
                     mu_r = e_val_at(P.mu_n, sw, m);
                 }
-                EH2 a0[2], a1[2], a2[2];
+                EH2 a0[X3P], a1[X3P], a2[X3P];
 #pragma unroll
-                for (int h = 0; h < 2; h++) {
+                for (int h = 0; h < X3P; h++) {
                     const EH2 stiff = mrow ? stiff_r : pload<16, 2>(P.stiff, sw, m, x + 2 * h);
                     const EH2 lam = mrow ? lam_r : pload<16, 2>(P.lam, sw, m, x + 2 * h);
                     a0[h] = EO2::add(EO2::add(EO2::mul(stiff, dvx.q[h]), EO2::mul(lam, dvs.q[h])), EO2::mul(lam, dvm.q[h]));
@@ -395,7 +416,7 @@ __global__ void __launch_bounds__(X3T, 1)
                 const E4 sms_a = f4(c, ld4(vmt + jr + pitch + x), ld4(vt(gen, 2) + jr + pitch + x));  // vm(s), vm(s+1)
                 const E4 sms_b = f4(c, ld4(vst + jr + x), ld4(vst + jr + pitch + x));     // vs rows m, m+1
 #pragma unroll
-                for (int h = 0; h < 2; h++) {
+                for (int h = 0; h < X3P; h++) {
                     e2_finish_nd<V>(a0[h], dt2, -1, srch, nw[0].q[h], rr[0].q[h]);
                     e2_finish_nd<V>(a1[h], dt2, -1, srch, nw[1].q[h], rr[1].q[h]);
                     e2_finish_nd<V>(a2[h], dt2, -1, srch, nw[2].q[h], rr[2].q[h]);

@@ -108,6 +108,11 @@ bool ac3d_fused_eligible(int64_t nx, int64_t nm, int64_t ns, int64_t pitch, int 
 cudaError_t ac3d_fused_prepare(int64_t nx);
 void launch_ac3d_fused(int variant, const AcParams& P, const Ac3In& in, const StreamIO& IO, int nblocks, int64_t n,
                        double src, int sample, int64_t eidx, cudaStream_t st);
+// the same step in binary32 lanes (hw_acoustic3d_fused32.cu; Ac3In pointers hold float data)
+bool ac3d_fused32_eligible(int64_t nx, int64_t nm, int64_t ns, int64_t pitch, int order, int max_smem);
+cudaError_t ac3d_fused32_prepare(int64_t nx);
+void launch_ac3d_fused32(int variant, const AcParams& P, const Ac3In& in, const StreamIO& IO, int nblocks, int64_t n,
+                         double src, int sample, int64_t eidx, cudaStream_t st);
 // one-pass 2D elastic step (hw_elastic2d_fused.cu): state n read from these buffers (A),
 // state n+1 written through the ElParams field views (B)
 struct El2In {

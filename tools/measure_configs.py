@@ -15,7 +15,7 @@ import paper_2310_00236_b200 as hw  # noqa: E402
 
 CPU = "--cpu" in sys.argv
 ARGS = [a for a in sys.argv[1:] if a != "--cpu"]
-NT = int(ARGS[0]) if len(ARGS) > 0 else 50
+NT = int(ARGS[0]) if ARGS and ARGS[0].isdigit() else 50
 F16 = hw.Precision.FP16
 _PEAKS = ROOT / "MEASURED_PEAKS.json"
 PEAK_GBS = json.loads(_PEAKS.read_text())["hbm_gbs"] if _PEAKS.exists() else 6551.7  # measured copy GB/s
@@ -38,8 +38,10 @@ def cpu_rate(s, variant, cells, steps):
     return cells * steps / max(t1 - t0, 1e-9), cores, steps
 
 
-def timed(name, s, variant, bytes_per_cell, cells, nt=NT, cpu_steps=2):
+def timed(name, s, variant, bytes_per_cell, cells, nt=NT, cpu_steps=2, init=None):
     st = s.new_state()
+    if init is not None:
+        init(st)
     s.upload(st)
     s.run_device(variant, 0, 3)
     ms = s.run_device(variant, 3, nt)
@@ -65,14 +67,24 @@ def cfg1(order=2, prec=F16):
     return hw.AcousticSolver(g, hw.build_homogeneous_acoustic(n, n, 1.0, 1.0), stencil_precision=prec, energy_every=1)
 
 
-def cfg3():  # 3D acoustic 512^3, 2nd order, full beta plane
+def cfg3(prec=F16):  # 3D acoustic 512^3, 2nd order, full beta plane (fp16 op3 vs the fp32 naive arm)
     n = 512
     rng = np.random.default_rng(0)
     c = 1.5 + 3.0 * rng.random((n, n, n))
     med = hw.build_acoustic_from_velocity(c)
     dx = 1.0 / n
     g = hw.GridSpec(n, n, dx, float(np.float16(0.5 * dx / (med.c_max() * np.sqrt(3)))), NT, nz=n, order=2)
-    return hw.AcousticSolver(g, med, stencil_precision=F16, energy_every=10)
+    return hw.AcousticSolver(g, med, stencil_precision=prec, energy_every=10)
+
+
+def gauss3(st):
+    """Config 3's initial state: Gaussian pressure exp(-|x - c|^2 / 0.01) at cell coordinates, v = 0
+    (fp64, one cast to the state's type)."""
+    v = st.p.values
+    n = v.shape[0]
+    a = np.arange(n) / n - 0.5
+    g = np.exp(-(a[:, None, None] ** 2 + a[None, :, None] ** 2 + a[None, None, :] ** 2) / 0.01)
+    st.p.values = g.astype(v.dtype)
 
 
 def cfg4(every=10):  # 2D elastic 4096^2, free surface
@@ -100,7 +112,11 @@ if __name__ == "__main__":
             timed(f"1: 2D acoustic 256^2 2nd order rigid walls {name}, energy every step", cfg1(2, prec), var, 24,
                   256 * 256, cpu_steps=200)
     if "3" in which:
-        timed("3: 3D acoustic 512^3 2nd order fp16 op3 (beta plane)", cfg3(), hw.Variant.OP3, 34, 512 ** 3, cpu_steps=1)
+        timed("3: 3D acoustic 512^3 2nd order fp16 op3 (beta plane, Gaussian p0)", cfg3(), hw.Variant.OP3, 34,
+              512 ** 3, cpu_steps=1, init=gauss3)
+    if "3f32" in which:  # p, vx, vy, vz binary32 read + written, beta binary32 read
+        timed("3: 3D acoustic 512^3 2nd order fp32 naive (beta plane, Gaussian p0)", cfg3(hw.Precision.FP32), None, 36,
+              512 ** 3, cpu_steps=1, init=gauss3)
     if "4" in which:
         timed("4: 2D elastic 4096^2 free surface fp16 op6", cfg4(), hw.Variant.OP6, 40, 4096 * 4097, cpu_steps=5)
     if "5" in which:

@@ -1,4 +1,4 @@
-"""Short run of one BASELINE config for ncu: python tools/profile_config.py <1|2|3|4|5> [nt]."""
+"""Short run of one BASELINE config for ncu: python tools/profile_config.py <1|2|3|3f32|4|5> [nt]."""
 import sys
 from pathlib import Path
 
@@ -14,9 +14,10 @@ def cfg2():
     return bench.make_solver(hw, nt=nt)
 
 
-s = {"1": lambda: mc.cfg1(2), "2": cfg2, "3": mc.cfg3, "4": mc.cfg4, "5": mc.cfg5}[which]()
+s = {"1": lambda: mc.cfg1(2), "2": cfg2, "3": mc.cfg3, "3f32": lambda: mc.cfg3(hw.Precision.FP32), "4": mc.cfg4,
+     "5": mc.cfg5}[which]()
 st = s.new_state()
 s.upload(st)
-v = hw.Variant.OP6 if which in ("4", "5") else hw.Variant.OP3
+v = hw.Variant.OP6 if which in ("4", "5") else (None if which == "3f32" else hw.Variant.OP3)
 ms = s.run_device(v, 0, nt)
 print(f"config {which}: {nt} steps {ms:.3f} ms")
