@@ -101,7 +101,7 @@ struct QDiv {
 __device__ __forceinline__ QDiv q_rowdiv(const PlaneView& v, int64_t s, int64_t m) {
     QDiv q{0.f, 0.f, v.sx == 0, false};
     if (q.row) {
-        q.d = __ldg(reinterpret_cast<const float*>(v.p) + s * v.ss + m * v.sm);
+        q.d = __ldg(reinterpret_cast<const float*>(v.p) + (int)(s * v.ss + m * v.sm));  // (planes < 2^31 elements)
         const unsigned int b = __float_as_uint(q.d), e = (b >> 23) & 0xffu;
         q.pow2 = (b & 0x7fffffu) == 0u && e >= 1u && e <= 253u;  // 2^k with a normal reciprocal
         q.r = __uint_as_float((b & 0x80000000u) | ((254u - e) << 23));  // 2^-k exactly (used when pow2)
@@ -120,8 +120,8 @@ __device__ __forceinline__ float q_divz(float a, float b) {
 // UpdatePipeline.increment + advance (stepping.py:58-98, efsum.py:100-121) for 4 cells:
 // rhs [+ round_U(src) on lane src_lane] -> / divisor -> x dt -> naive / op3 / op6 advance.
 // The source and the division mode are warp-uniform branches around all four cells.
-template <int V>
-__device__ __forceinline__ void q_finish(const F4& rhs, const QDiv& q, const F4& dcell, float dt, int src_lane,
+template <int V, bool ROWONLY>
+__device__ __forceinline__ void q_finish(const F4& rhs, const QDiv& q, const float* dcell, float dt, int src_lane,
                                          float srcf, F4& u, F4& t) {
     F4 xq = rhs;
     if (src_lane >= 0) {
@@ -135,9 +135,10 @@ __device__ __forceinline__ void q_finish(const F4& rhs, const QDiv& q, const F4&
     } else if (q.row) {
 #pragma unroll
         for (int i = 0; i < 4; i++) xq.e[i] = q_divz(xq.e[i], q.d);
-    } else {
+    } else if constexpr (!ROWONLY) {  // per-cell divisors (staged in shared memory, or the plane row in global memory)
+        const F4 dv = q_ld(dcell);
 #pragma unroll
-        for (int i = 0; i < 4; i++) xq.e[i] = q_divz(xq.e[i], dcell.e[i]);
+        for (int i = 0; i < 4; i++) xq.e[i] = q_divz(xq.e[i], dv.e[i]);
     }
 #pragma unroll
     for (int i = 0; i < 4; i++) {
@@ -159,10 +160,10 @@ __device__ __forceinline__ void q_finish(const F4& rhs, const QDiv& q, const F4&
     }
 }
 
-// per-cell divisors of a plane that varies along x (sx == 1), else unused
-__device__ __forceinline__ F4 q_dcell(const PlaneView& v, int64_t s, int64_t m, int x) {
-    if (v.sx == 0) return F4{};
-    return q_ld(reinterpret_cast<const float*>(v.p) + s * v.ss + m * v.sm + x);
+// per-cell divisors of a plane that varies along x (sx == 1): its cells at (s, m, x); read
+// only by q_finish's per-cell branch
+__device__ __forceinline__ const float* q_dcell(const PlaneView& v, int64_t s, int64_t m, int x) {
+    return reinterpret_cast<const float*>(v.p) + s * v.ss + m * v.sm + x;
 }
 
 // store one row segment (4 cells) and its periodic / image ghost copies (as e_store_row)
@@ -212,7 +213,9 @@ static size_t q3_bytes(int64_t nx) {
     return 128 + (size_t)rows * nx * sizeof(float);
 }
 
-template <int V>
+// RR: the three density planes are constant along x (constant / layered media): no per-cell
+// density code is compiled in
+template <int V, bool RR>
 __global__ void __launch_bounds__(Q3T, 1)
     k_ac3d_fused32(AcParams P, Ac3In in_, StreamIO IO, int64_t n, double src, int sample, int64_t eidx) {
     e_pdl_enter();
@@ -341,22 +344,22 @@ __global__ void __launch_bounds__(Q3T, 1)
                 // v_slow(s) from p rows s, s+1 (acoustic.py:169-170, to-half shifts (0, 1))
                 F4 vsn = q_ld(ob(os, Q_VS) + ro);
                 F4 rvs = comp ? q_ld(ob(os, Q_RVS) + ro) : F4{};
-                q_finish<V>(q_sfold(c1, c2, qp0, qp1), d_s, q_dcell(P.rho_s, sw, m, x), dt, -1,
+                q_finish<V, RR>(q_sfold(c1, c2, qp0, qp1), d_s, RR ? nullptr : q_dcell(P.rho_s, sw, m, x), dt, -1,
                             srcf, vsn, rvs);
                 if (i > 1) {
                     const float* pt = sl(kp);  // p tile of slab s: row m at index j + 1
                     // vx(s) = fl(fl(ddx p / rho_x) dt) (acoustic.py:167-168)
                     F4 vxn = q_ld(ob(os, Q_VX) + ro);
                     F4 rvx = comp ? q_ld(ob(os, Q_RVX) + ro) : F4{};
-                    q_finish<V>(q_xfold(c1, c2, pt + (int64_t)(j + 1) * pitch, x, xl, xr, false),
-                                d_x, q_dcell(P.rho_x, s, m, x), dt, -1, srcf, vxn, rvx);
+                    q_finish<V, RR>(q_xfold(c1, c2, pt + (int64_t)(j + 1) * pitch, x, xl, xr, false),
+                                d_x, RR ? nullptr : q_dcell(P.rho_x, s, m, x), dt, -1, srcf, vxn, rvx);
                     q_st(xv + ro, vxn);
                     {  // vm(s) row m from p mid rows m, m+1
                         const float* t = pt + (int64_t)(j + 1) * pitch + x;
                         F4 vmv = q_ld(ovm(os) + ro + pitch);
                         F4 rvm = comp ? q_ld(orvm(os) + ro + pitch) : F4{};
-                        q_finish<V>(q_sfold(c1, c2, q_ld(t), q_ld(t + pitch)), d_m,
-                                    q_dcell(P.rho_m, s, m, x), dt, -1, srcf, vmv, rvm);
+                        q_finish<V, RR>(q_sfold(c1, c2, q_ld(t), q_ld(t + pitch)), d_m,
+                                    RR ? nullptr : q_dcell(P.rho_m, s, m, x), dt, -1, srcf, vmv, rvm);
                         q_st(vmn + ro + pitch, vmv);
                         q_store(P.vm, slab, s, off, vmv, sin);
                         q_track(acc[3], vmv);
@@ -369,8 +372,8 @@ __global__ void __launch_bounds__(Q3T, 1)
                         const float* t = pt + x;
                         F4 vmh = q_ld(ovm(os) + x);
                         F4 rvh = comp ? q_ld(orvm(os) + x) : F4{};
-                        q_finish<V>(q_sfold(c1, c2, q_ld(t), q_ld(t + pitch)), d_h,
-                                    q_dcell(P.rho_m, s, mh, x), dt, -1, srcf, vmh, rvh);
+                        q_finish<V, RR>(q_sfold(c1, c2, q_ld(t), q_ld(t + pitch)), d_h,
+                                    RR ? nullptr : q_dcell(P.rho_m, s, mh, x), dt, -1, srcf, vmh, rvh);
                         q_st(vmn + x, vmh);
                     }
                     q_store(P.vx, slab, s, off, vxn, sin);
@@ -393,8 +396,7 @@ __global__ void __launch_bounds__(Q3T, 1)
                     const F4 pold = q_ld(pt + (int64_t)(j + 1) * pitch + x);
                     F4 pn = pold;
                     F4 rr = comp ? q_ld(ob(os, Q_RP) + ro) : F4{};
-                    const F4 bcell = bfull ? q_ld(ob(os, Q_BETA) + ro) : F4{};
-                    q_finish<V>(q_add(q_add(tx, ts), tmv), d_b, bcell, dt, sk ? sln : -1, srcf,
+                    q_finish<V, false>(q_add(q_add(tx, ts), tmv), d_b, ob(os, Q_BETA) + ro, dt, sk ? sln : -1, srcf,
                                 pn, rr);
                     q_store(P.p, slab, s, off, pn, sin);
                     q_track(acc[0], pn);
@@ -470,16 +472,19 @@ bool ac3d_fused32_eligible(int64_t nx, int64_t nm, int64_t ns, int64_t pitch, in
 
 cudaError_t ac3d_fused32_prepare(int64_t nx) {
     const int b = (int)q3_bytes(nx);
-    cudaFuncSetAttribute((void*)k_ac3d_fused32<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    cudaFuncSetAttribute((void*)k_ac3d_fused32<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    cudaFuncSetAttribute((void*)k_ac3d_fused32<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    void* fns[] = {(void*)k_ac3d_fused32<0, false>, (void*)k_ac3d_fused32<3, false>, (void*)k_ac3d_fused32<6, false>,
+                   (void*)k_ac3d_fused32<0, true>, (void*)k_ac3d_fused32<3, true>, (void*)k_ac3d_fused32<6, true>};
+    for (void* fn : fns) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
     return cudaGetLastError();
 }
 
 void launch_ac3d_fused32(int variant, const AcParams& P, const Ac3In& in, const StreamIO& IO, int nblocks, int64_t n,
                          double src, int sample, int64_t eidx, cudaStream_t st) {
-    void* fn = variant == 0 ? (void*)k_ac3d_fused32<0>
-                            : (variant == 3 ? (void*)k_ac3d_fused32<3> : (void*)k_ac3d_fused32<6>);
+    const bool rr = P.rho_x.sx == 0 && P.rho_s.sx == 0 && P.rho_m.sx == 0;
+    void* fn = rr ? (variant == 0 ? (void*)k_ac3d_fused32<0, true>
+                                  : (variant == 3 ? (void*)k_ac3d_fused32<3, true> : (void*)k_ac3d_fused32<6, true>))
+                  : (variant == 0 ? (void*)k_ac3d_fused32<0, false>
+                                  : (variant == 3 ? (void*)k_ac3d_fused32<3, false> : (void*)k_ac3d_fused32<6, false>));
     void* args[] = {(void*)&P, (void*)&in, (void*)&IO, (void*)&n, (void*)&src, (void*)&sample, (void*)&eidx};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nblocks);

@@ -146,3 +146,21 @@ def test_fused3d_f32_source_on_tile_and_slab_edges():
         out = s.run(None, st)
         assert s.kernel_path() == "fused3d-f32"
         _check(s, st, out, ref)
+
+
+@pytest.mark.parametrize("variant", [None, hw.Variant.OP3])
+def test_fused3d_f32_per_cell_density(variant):
+    """Density planes that vary along x take the per-cell division path (the other kernel
+    instantiation); beta per cell as well."""
+    nx, ny, nz = 256, 16, 12
+    rng = np.random.default_rng(3)
+    planes = {n: 1.0 + rng.random((nz, ny, nx)) for n in ("rho_x", "rho_y", "rho_z")}
+    planes["beta"] = 0.2 + 0.3 * rng.random((nz, ny, nx))
+    med = hw.Medium(hw.MediumKind.ACOUSTIC, nx, ny, planes, nz)
+    s0, st = _case(nx, ny, nz, 7)
+    s = hw.AcousticSolver(hw.GridSpec(nx, ny, 1.0 / nx, s0.grid.dt, 7, nz=nz, order=2), med, s0.source,
+                          stencil_precision=F32, receivers=((5, 3, 2),), energy_every=3)
+    ref = oracle.run_solver(s, variant, st)
+    out = s.run(variant, st)
+    assert s.kernel_path() == "fused3d-f32"
+    _check(s, st, out, ref)

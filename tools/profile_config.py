@@ -17,6 +17,8 @@ def cfg2():
 s = {"1": lambda: mc.cfg1(2), "2": cfg2, "3": mc.cfg3, "3f32": lambda: mc.cfg3(hw.Precision.FP32), "4": mc.cfg4,
      "5": mc.cfg5}[which]()
 st = s.new_state()
+if which in ("3", "3f32"):
+    mc.gauss3(st)
 s.upload(st)
 v = hw.Variant.OP6 if which in ("4", "5") else (None if which == "3f32" else hw.Variant.OP3)
 ms = s.run_device(v, 0, nt)
