@@ -11,7 +11,11 @@
 using namespace hw;
 constexpr int NX = 4096, NS = 6, FR = 4;
 
-__global__ void __launch_bounds__(512, 1) k_tma(const __half* in, __half* out, int ny, int per) {
+__device__ __forceinline__ size_t rowoff(int q, int y, int per, int il) {
+    return il ? ((size_t)y * NS + q) * NX : (size_t)q * per + (size_t)y * NX;
+}
+
+__global__ void __launch_bounds__(512, 1) k_tma(const __half* in, __half* out, int ny, int per, int il) {
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = (uint64_t*)smem;
     unsigned* rel = (unsigned*)(full + FR);
@@ -24,7 +28,7 @@ __global__ void __launch_bounds__(512, 1) k_tma(const __half* in, __half* out, i
         fence_proxy_async_smem();
         mbar_arrive_expect_tx(&full[s], NS * NX * 2);
         for (int q = 0; q < NS; q++)
-            tma_load_1d(ring + (s * NS + q) * NX, in + (size_t)q * per + (size_t)(y0 + i) * NX, NX * 2, &full[s]);
+            tma_load_1d(ring + (s * NS + q) * NX, in + rowoff(q, y0 + i, per, il), NX * 2, &full[s]);
     };
     if (tid == 0) {
         for (int s = 0; s < FR; s++) { mbar_init(&full[s], 1); rel[s] = 0; }
@@ -39,7 +43,7 @@ __global__ void __launch_bounds__(512, 1) k_tma(const __half* in, __half* out, i
         for (int q = 0; q < NS; q++) {
             uint4 v = *(const uint4*)(ring + (s * NS + q) * NX + tid * 8);
             acc.x ^= v.x;
-            *(uint4*)(out + (size_t)q * per + (size_t)(y0 + i) * NX + tid * 8) = v;
+            *(uint4*)(out + rowoff(q, y0 + i, per, il) + tid * 8) = v;
         }
         __syncwarp();
         if (lane == 0) {
@@ -82,16 +86,16 @@ int main() {
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     double bytes = 2.0 * NS * per * 2;
-    for (int mode = 0; mode < 3; mode++) {
+    for (int mode = 0; mode < 4; mode++) {
         for (int w = 0; w < 3; w++) {
-            if (mode == 0) k_tma<<<148, 512, smem>>>(in, out, ny, (int)per);
+            if (mode == 0 || mode == 3) k_tma<<<148, 512, smem>>>(in, out, ny, (int)per, mode == 3);
             else if (mode == 1) k_ldg<<<148, 512>>>(in, out, ny, (int)per);
             else k_copy<<<148 * 8, 256>>>((const uint4*)in, (uint4*)out, NS * per * 2 / 16);
         }
         cudaEventRecord(a);
         const int reps = 20;
         for (int r = 0; r < reps; r++) {
-            if (mode == 0) k_tma<<<148, 512, smem>>>(in, out, ny, (int)per);
+            if (mode == 0 || mode == 3) k_tma<<<148, 512, smem>>>(in, out, ny, (int)per, mode == 3);
             else if (mode == 1) k_ldg<<<148, 512>>>(in, out, ny, (int)per);
             else k_copy<<<148 * 8, 256>>>((const uint4*)in, (uint4*)out, NS * per * 2 / 16);
         }
@@ -99,7 +103,7 @@ int main() {
         cudaEventSynchronize(b);
         float ms;
         cudaEventElapsedTime(&ms, a, b);
-        const char* nm[] = {"tma-ring rows", "ldg rows", "grid-stride copy"};
+        const char* nm[] = {"tma-ring rows", "ldg rows", "grid-stride copy", "tma-ring interleaved"};
         printf("%-18s %8.1f us/iter  %7.0f GB/s  (%s)\n", nm[mode], ms * 1e3 / reps, bytes * reps / (ms * 1e-3) / 1e9,
                cudaGetErrorString(cudaGetLastError()));
     }
