@@ -96,24 +96,32 @@ __device__ __forceinline__ unsigned int q_nonfinite(float acc) {
 // divisor of one (slow, mid) row: a plane constant along x (sx == 0) gives one value per row
 struct QDiv {
     float d, r;
-    bool row, pow2;
+    bool row, pow2, ok;  // ok: d finite and nonzero (the inline zero-dividend answer applies)
 };
 __device__ __forceinline__ QDiv q_rowdiv(const PlaneView& v, int64_t s, int64_t m) {
-    QDiv q{0.f, 0.f, v.sx == 0, false};
+    QDiv q{0.f, 0.f, v.sx == 0, false, false};
     if (q.row) {
         q.d = __ldg(reinterpret_cast<const float*>(v.p) + (int)(s * v.ss + m * v.sm));  // (planes < 2^31 elements)
         const unsigned int b = __float_as_uint(q.d), e = (b >> 23) & 0xffu;
         q.pow2 = (b & 0x7fffffu) == 0u && e >= 1u && e <= 253u;  // 2^k with a normal reciprocal
         q.r = __uint_as_float((b & 0x80000000u) | ((254u - e) << 23));  // 2^-k exactly (used when pow2)
+        q.ok = fabsf(q.d) < INFINITY && q.d != 0.0f;
     }
     return q;
+}
+// QDiv through shared memory: (d, r, flags) -- one uniform 16-byte load per use
+__device__ __forceinline__ float4 q_pack(const QDiv& q) {
+    return make_float4(q.d, q.r, __int_as_float((q.row ? 1 : 0) | (q.pow2 ? 2 : 0) | (q.ok ? 4 : 0)), 0.f);
+}
+__device__ __forceinline__ QDiv q_unpack(const float4& t) {
+    const int f = __float_as_int(t.z);
+    return QDiv{t.x, t.y, (f & 1) != 0, (f & 2) != 0, (f & 4) != 0};
 }
 // IEEE quotient a / b (__fdiv_rn) with zero dividends answered inline: __fdiv_rn sends a
 // zero dividend down its slow path (a subroutine call per element), and the state is zero
 // wherever the wave has not arrived yet.  ±0 / b for finite nonzero b is the signed zero.
-__device__ __forceinline__ float q_divz(float a, float b) {
-    if (a == 0.0f && fabsf(b) < INFINITY && b != 0.0f)
-        return __uint_as_float((__float_as_uint(a) ^ __float_as_uint(b)) & 0x80000000u);
+__device__ __forceinline__ float q_divz(float a, float b, bool bok) {
+    if (a == 0.0f && bok) return __uint_as_float((__float_as_uint(a) ^ __float_as_uint(b)) & 0x80000000u);
     return __fdiv_rn(a, b);
 }
 
@@ -134,11 +142,11 @@ __device__ __forceinline__ void q_finish(const F4& rhs, const QDiv& q, const flo
         for (int i = 0; i < 4; i++) xq.e[i] = __fmul_rn(xq.e[i], q.r);
     } else if (q.row) {
 #pragma unroll
-        for (int i = 0; i < 4; i++) xq.e[i] = q_divz(xq.e[i], q.d);
+        for (int i = 0; i < 4; i++) xq.e[i] = q_divz(xq.e[i], q.d, q.ok);
     } else if constexpr (!ROWONLY) {  // per-cell divisors (staged in shared memory, or the plane row in global memory)
         const F4 dv = q_ld(dcell);
 #pragma unroll
-        for (int i = 0; i < 4; i++) xq.e[i] = q_divz(xq.e[i], dv.e[i]);
+        for (int i = 0; i < 4; i++) xq.e[i] = q_divz(xq.e[i], dv.e[i], fabsf(dv.e[i]) < INFINITY && dv.e[i] != 0.0f);
     }
 #pragma unroll
     for (int i = 0; i < 4; i++) {
@@ -210,7 +218,7 @@ __device__ __forceinline__ void q_rows(float* dst, const float* fbase, int64_t s
 static size_t q3_bytes(int64_t nx) {
     const int64_t TM = Q3T * Q3C / nx;
     const int64_t rows = QR * (TM + 2) + 2 * (Q_NTM * TM + 2 * (TM + 1)) + TM + (TM + 1);
-    return 128 + (size_t)rows * nx * sizeof(float);
+    return 256 + (size_t)rows * nx * sizeof(float);
 }
 
 // RR: the three density planes are constant along x (constant / layered media): no per-cell
@@ -238,7 +246,8 @@ __global__ void __launch_bounds__(Q3T, 1)
     // shared layout (rows of pitch floats)
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
     uint64_t* obar = reinterpret_cast<uint64_t*>(smem + 64);
-    float* ring = reinterpret_cast<float*>(smem + 128);
+    float4* qdiv = reinterpret_cast<float4*>(smem + 128);  // [2][4]: row divisors of the next / this slab
+    float* ring = reinterpret_cast<float*>(smem + 256);
     const int64_t tm = (int64_t)TM * pitch, slot = (int64_t)(TM + 2) * pitch;
     const int64_t oslot = ((int64_t)Q_NTM * TM + 2 * (TM + 1)) * pitch;
     float* own = ring + QR * slot;
@@ -320,14 +329,20 @@ __global__ void __launch_bounds__(Q3T, 1)
                 issue(i + QD);
             }
             const int sw = F0 + i - 1 < 0 ? ns - 1 : F0 + i - 1;  // periodic: v_slow(-1) is row ns - 1's medium
-            // row divisors of slab s = F - 1, loaded before the waits (latency off the chain)
-            QDiv d_s{}, d_x{}, d_m{}, d_h{}, d_b{};
+            // row divisors: threads 0-3 stage those of the next iteration's slab (F0 + i) in shared memory
+            // (constant / slow-layered planes depend on the slab only; the barriers below order the use)
+            if (tid < 4 && i + 1 < NI) {
+                const int sn = F0 + i < 0 ? ns - 1 : F0 + i;
+                const PlaneView& pv = tid == 0 ? P.rho_s : (tid == 1 ? P.rho_x : (tid == 2 ? P.rho_m : P.beta));
+                qdiv[((i + 1) & 1) * 4 + tid] = q_pack(q_rowdiv(pv, sn, 0));
+            }
+            QDiv d_s{}, d_x{}, d_m{}, d_b{};
             if (i > 0) {
-                d_s = q_rowdiv(P.rho_s, sw, m);
-                d_x = q_rowdiv(P.rho_x, sw, m);
-                d_m = q_rowdiv(P.rho_m, sw, m);
-                d_h = q_rowdiv(P.rho_m, sw, mh);
-                d_b = q_rowdiv(P.beta, sw, m);
+                const float4* qd = qdiv + (i & 1) * 4;
+                d_s = q_unpack(qd[0]);
+                d_x = q_unpack(qd[1]);
+                d_m = q_unpack(qd[2]);
+                d_b = q_unpack(qd[3]);
             }
             mbar_wait(&bar[k], kph);
             qp0 = qp1;
@@ -372,7 +387,7 @@ __global__ void __launch_bounds__(Q3T, 1)
                         const float* t = pt + x;
                         F4 vmh = q_ld(ovm(os) + x);
                         F4 rvh = comp ? q_ld(orvm(os) + x) : F4{};
-                        q_finish<V, RR>(q_sfold(c1, c2, q_ld(t), q_ld(t + pitch)), d_h,
+                        q_finish<V, RR>(q_sfold(c1, c2, q_ld(t), q_ld(t + pitch)), d_m,
                                     RR ? nullptr : q_dcell(P.rho_m, s, mh, x), dt, -1, srcf, vmh, rvh);
                         q_st(vmn + x, vmh);
                     }
