@@ -443,7 +443,20 @@ __device__ __forceinline__ double finalize_partials(const double* part, int nb) 
     const int nl = warp_lanes();
     for (int c = w; c < NCOMP; c += nw) {
         double a = 0.0;
-        for (int bi = lane; bi < nb; bi += nl) a += __ldcg(&part[(int64_t)bi * NCOMP + c]);
+        // UN loads in flight per lane ahead of the sum (the L2 latencies overlap instead of chaining);
+        // the adds stay in the fixed order bi = lane, lane + nl, ... (identical bits)
+        constexpr int UN = 8;
+        for (int b0 = lane; b0 < nb; b0 += UN * nl) {
+            double v[UN];
+#pragma unroll
+            for (int q = 0; q < UN; q++) {
+                const int bi = b0 + q * nl;
+                v[q] = bi < nb ? __ldcg(&part[(int64_t)bi * NCOMP + c]) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < UN; q++)
+                if (b0 + q * nl < nb) a += v[q];
+        }
         a = warp_sum(a);
         if (lane == 0) tot[c] = a;
     }
