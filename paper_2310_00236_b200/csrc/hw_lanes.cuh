@@ -50,13 +50,20 @@ template <> struct lane<16> {
     static __device__ __forceinline__ T zero() { return __ushort_as_half(0); }
 };
 
+// IEEE quotients with zero dividends answered inline: __fdiv_rn / __ddiv_rn send a zero dividend
+// down their slow path (a subroutine call), and wavefields are zero wherever the wave has not
+// arrived.  +-0 / b for finite nonzero b is the signed zero (identical bits).
 template <> struct lane<32> {
     using T = float;
     static __device__ __forceinline__ T add(T a, T b) { return __fadd_rn(a, b); }
     static __device__ __forceinline__ T sub(T a, T b) { return __fsub_rn(a, b); }
     static __device__ __forceinline__ T mul(T a, T b) { return __fmul_rn(a, b); }
-    static __device__ __forceinline__ T div(T a, T b) { return __fdiv_rn(a, b); }
-    static __device__ __forceinline__ T div_ieee(T a, T b) { return __fdiv_rn(a, b); }
+    static __device__ __forceinline__ T div(T a, T b) { return div_ieee(a, b); }
+    static __device__ __forceinline__ T div_ieee(T a, T b) {
+        if (a == 0.0f && fabsf(b) < INFINITY && b != 0.0f)
+            return __uint_as_float((__float_as_uint(a) ^ __float_as_uint(b)) & 0x80000000u);
+        return __fdiv_rn(a, b);
+    }
     static __device__ __forceinline__ bool finite(T a) {
         return (__float_as_uint(a) & 0x7f800000u) != 0x7f800000u;
     }
@@ -71,8 +78,13 @@ template <> struct lane<64> {
     static __device__ __forceinline__ T add(T a, T b) { return __dadd_rn(a, b); }
     static __device__ __forceinline__ T sub(T a, T b) { return __dsub_rn(a, b); }
     static __device__ __forceinline__ T mul(T a, T b) { return __dmul_rn(a, b); }
-    static __device__ __forceinline__ T div(T a, T b) { return __ddiv_rn(a, b); }
-    static __device__ __forceinline__ T div_ieee(T a, T b) { return __ddiv_rn(a, b); }
+    static __device__ __forceinline__ T div(T a, T b) { return div_ieee(a, b); }
+    static __device__ __forceinline__ T div_ieee(T a, T b) {
+        if (a == 0.0 && fabs(b) < INFINITY && b != 0.0)
+            return __longlong_as_double((__double_as_longlong(a) ^ __double_as_longlong(b)) &
+                                        (long long)0x8000000000000000ull);
+        return __ddiv_rn(a, b);
+    }
     static __device__ __forceinline__ bool finite(T a) {
         return (__double_as_longlong(a) & 0x7ff0000000000000ll) != 0x7ff0000000000000ll;
     }
