@@ -286,9 +286,16 @@ class _DeviceSolver:
     def _download(self, state):
         dtype = DTYPES[self.update_precision]
         if self.distributed:  # rows of other ranks keep their uploaded values (own rows overwritten below)
-            arrs = [_host_empty(u.shape, u.dtype) for u in self._uploaded]
-            for a, u in zip(arrs, self._uploaded):
-                np.copyto(a, u)
+            # a caller array that went up unconverted is updated in place (its own rows only): no full
+            # global-size copy per run on every rank; converted / mirrored inputs get a fresh array
+            arrs = []
+            for name, u in zip(self.FIELDS, self._uploaded):
+                if getattr(state, name).values is u and u.flags.writeable:
+                    arrs.append(u)
+                else:
+                    a = _host_empty(u.shape, u.dtype)
+                    np.copyto(a, u)
+                    arrs.append(a)
         else:  # fresh arrays, as the reference returns (acoustic.py:147-152), in pinned memory
             arrs = [_host_empty(self._dgrid.shape(self._stagger_of(n)), dtype) for n in self.FIELDS]
         ptrs = (ctypes.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
