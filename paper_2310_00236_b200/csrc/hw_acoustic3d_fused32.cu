@@ -32,23 +32,36 @@
 
 namespace hw {
 
-constexpr int Q3T = 512;  // threads per CTA
-constexpr int Q3C = 4;    // cells per thread (one float4)
+#ifndef HW_Q3C
+#define HW_Q3C 4
+#endif
+constexpr int Q3C = HW_Q3C;      // cells per thread (one or two float4)
+constexpr int Q3T = 2048 / Q3C;  // threads per CTA (TM = 2048 / nx either way)
 constexpr int QR = 5;     // tap ring slots
 constexpr int QD = 3;     // prefetch distance
 
 enum { Q_VX = 0, Q_VS, Q_RP, Q_BETA, Q_RVX, Q_RVS, Q_NTM };
 
 struct F4 {
-    float e[4];
+    float e[Q3C];
 };
 
 __device__ __forceinline__ F4 q_ld(const float* p) {
-    const float4 v = *reinterpret_cast<const float4*>(p);
-    return F4{{v.x, v.y, v.z, v.w}};
+    F4 r;
+#pragma unroll
+    for (int h = 0; h < Q3C / 4; h++) {
+        const float4 v = *reinterpret_cast<const float4*>(p + 4 * h);
+        r.e[4 * h] = v.x;
+        r.e[4 * h + 1] = v.y;
+        r.e[4 * h + 2] = v.z;
+        r.e[4 * h + 3] = v.w;
+    }
+    return r;
 }
 __device__ __forceinline__ void q_st(float* p, const F4& v) {
-    *reinterpret_cast<float4*>(p) = make_float4(v.e[0], v.e[1], v.e[2], v.e[3]);
+#pragma unroll
+    for (int h = 0; h < Q3C / 4; h++)
+        *reinterpret_cast<float4*>(p + 4 * h) = make_float4(v.e[4 * h], v.e[4 * h + 1], v.e[4 * h + 2], v.e[4 * h + 3]);
 }
 // 2nd-order fold of the inner tap pair: fl(fl(c1 a) + fl(c2 b)) (stencil.py:72-79, outer pair dropped)
 __device__ __forceinline__ float q_fold(float c1, float c2, float a, float b) {
@@ -57,7 +70,7 @@ __device__ __forceinline__ float q_fold(float c1, float c2, float a, float b) {
 __device__ __forceinline__ F4 q_sfold(float c1, float c2, const F4& a, const F4& b) {
     F4 r;
 #pragma unroll
-    for (int i = 0; i < 4; i++) r.e[i] = q_fold(c1, c2, a.e[i], b.e[i]);
+    for (int i = 0; i < Q3C; i++) r.e[i] = q_fold(c1, c2, a.e[i], b.e[i]);
     return r;
 }
 // x derivative of 4 cells (periodic) from a shared row: to-int shifts (-1, 0), to-half (0, 1)
@@ -68,26 +81,26 @@ __device__ __forceinline__ F4 q_xfold(float c1, float c2, const float* row, int 
         const float l = row[xl];
         r.e[0] = q_fold(c1, c2, l, o.e[0]);
 #pragma unroll
-        for (int i = 1; i < 4; i++) r.e[i] = q_fold(c1, c2, o.e[i - 1], o.e[i]);
+        for (int i = 1; i < Q3C; i++) r.e[i] = q_fold(c1, c2, o.e[i - 1], o.e[i]);
     } else {
         const float rr = row[xr];
 #pragma unroll
-        for (int i = 0; i < 3; i++) r.e[i] = q_fold(c1, c2, o.e[i], o.e[i + 1]);
-        r.e[3] = q_fold(c1, c2, o.e[3], rr);
+        for (int i = 0; i < Q3C - 1; i++) r.e[i] = q_fold(c1, c2, o.e[i], o.e[i + 1]);
+        r.e[Q3C - 1] = q_fold(c1, c2, o.e[Q3C - 1], rr);
     }
     return r;
 }
 __device__ __forceinline__ F4 q_add(const F4& a, const F4& b) {
     F4 r;
 #pragma unroll
-    for (int i = 0; i < 4; i++) r.e[i] = __fadd_rn(a.e[i], b.e[i]);
+    for (int i = 0; i < Q3C; i++) r.e[i] = __fadd_rn(a.e[i], b.e[i]);
     return r;
 }
 
 // running max of |x| that propagates NaN: non-finite iff the result is inf or NaN
 __device__ __forceinline__ void q_track(float& acc, const F4& v) {
 #pragma unroll
-    for (int i = 0; i < 4; i++) asm("max.NaN.f32 %0, %0, %1;" : "+f"(acc) : "f"(fabsf(v.e[i])));
+    for (int i = 0; i < Q3C; i++) asm("max.NaN.f32 %0, %0, %1;" : "+f"(acc) : "f"(fabsf(v.e[i])));
 }
 __device__ __forceinline__ unsigned int q_nonfinite(float acc) {
     return (__float_as_uint(acc) & 0x7f800000u) == 0x7f800000u ? 1u : 0u;
@@ -134,22 +147,22 @@ __device__ __forceinline__ void q_finish(const F4& rhs, const QDiv& q, const flo
     F4 xq = rhs;
     if (src_lane >= 0) {
 #pragma unroll
-        for (int i = 0; i < 4; i++)
+        for (int i = 0; i < Q3C; i++)
             if (i == src_lane) xq.e[i] = __fadd_rn(xq.e[i], srcf);
     }
     if (q.row && q.pow2) {
 #pragma unroll
-        for (int i = 0; i < 4; i++) xq.e[i] = __fmul_rn(xq.e[i], q.r);
+        for (int i = 0; i < Q3C; i++) xq.e[i] = __fmul_rn(xq.e[i], q.r);
     } else if (q.row) {
 #pragma unroll
-        for (int i = 0; i < 4; i++) xq.e[i] = q_divz(xq.e[i], q.d, q.ok);
+        for (int i = 0; i < Q3C; i++) xq.e[i] = q_divz(xq.e[i], q.d, q.ok);
     } else if constexpr (!ROWONLY) {  // per-cell divisors (staged in shared memory, or the plane row in global memory)
         const F4 dv = q_ld(dcell);
 #pragma unroll
-        for (int i = 0; i < 4; i++) xq.e[i] = q_divz(xq.e[i], dv.e[i], fabsf(dv.e[i]) < INFINITY && dv.e[i] != 0.0f);
+        for (int i = 0; i < Q3C; i++) xq.e[i] = q_divz(xq.e[i], dv.e[i], fabsf(dv.e[i]) < INFINITY && dv.e[i] != 0.0f);
     }
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
+    for (int i = 0; i < Q3C; i++) {
         const float x = __fmul_rn(xq.e[i], dt);
         if (V == 0) {
             u.e[i] = __fadd_rn(u.e[i], x);
@@ -188,7 +201,7 @@ __device__ __forceinline__ void q_store(const FieldView& f, int64_t slab, int s,
         F4 w = v;
         if (f.odd) {
 #pragma unroll
-            for (int i = 0; i < 4; i++) w.e[i] = lane<32>::neg(v.e[i]);
+            for (int i = 0; i < Q3C; i++) w.e[i] = lane<32>::neg(v.e[i]);
         }
         const int sg = (int)f.row0 + s, ng = (int)f.nglob;
         if (f.gtop == GHOST_IMAGE) {
@@ -424,7 +437,7 @@ __global__ void __launch_bounds__(Q3T, 1)
                             [&](int o) {
                                 double r = 0.0;
 #pragma unroll
-                                for (int q = 0; q < 4; q++)
+                                for (int q = 0; q < Q3C; q++)
                                     if (q == o) r = (double)pn.e[q];
                                 return r;
                             },
