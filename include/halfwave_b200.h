@@ -165,8 +165,12 @@ int hw_run_device(hw_solver* h, int32_t variant, int64_t step0, int64_t nt,
 int64_t hw_last_launch_count(const hw_solver* h);
 
 /* Which kernel family this handle's steps use (chosen at hw_create from the lanes,
- * dimension and nx): "fused2d" (single-pass 2D acoustic), "stream2d" (streaming 2D
- * elastic phases) or "generic" (phase kernels).  Static string; "" for NULL. */
+ * dimension, order, grid size and transport): "small2d" (persistent small-grid 2D kernels),
+ * "fused2d" (one-pass 2D acoustic, binary16), "fused2d-tb2" (opt-in two-step 2D acoustic),
+ * "fused2d-el" (one-pass 2D elastic, binary16), "fused3d" (one-pass 3D acoustic, binary16),
+ * "fused3d-f32" (one-pass 3D acoustic, binary32 lanes), "fused3d-el" (opt-in one-pass 3D
+ * elastic), "stream2d" / "stream3d" (streaming phase kernels) or "generic" (phase kernels,
+ * every lane combination).  Static string; "" for NULL. */
 const char* hw_kernel_path(const hw_solver* h);
 
 /* Halo transport of the handle: 0 single domain, 1 in-process slab group (peer copies),
