@@ -196,6 +196,20 @@ int hw_cheap_div_table(int32_t device, uint32_t* bits1024);
  * 2 IEEE, 3 cheap table-verified); -1 on bad arguments. */
 int hw_plane_div_mode(const hw_solver* h, int32_t plane);
 
+/* Process-wide kernel-path options, read when a handle is created (no
+ * environment variables are consulted).  Defaults are the production choices:
+ *   "path"      0 fastest eligible kernels | 1 generic phase kernels only
+ *   "div"       binary16 division: 0 per-plane choice | 1 no table path | 2 IEEE only
+ *   "small"     1 persistent small-grid 2D kernels (grids <= 2^20 cells) | 0 off
+ *   "tb"        0 | 1 two steps per launch, fused 2D acoustic (opt-in, measured slower)
+ *   "fused_el"  1 one-pass 2D elastic kernel | 0 two-phase kernels
+ *   "fused3"    1 one-pass 3D acoustic kernels | 0 two-phase kernels
+ *   "fused_el3" one-pass 3D elastic kernel (see hw_kernel_path's "fused3d-el")
+ *   "nccl_self" 0 | 1 a one-rank job given an NCCL id takes the NCCL transport (tests)
+ * HW_EINVAL for an unknown name or an out-of-range value. */
+int hw_set_option(const char* name, int64_t value);
+int hw_get_option(const char* name, int64_t* value);
+
 /* Thread-local message for the last non-OK status. */
 const char* hw_last_error(void);
 

@@ -7,6 +7,7 @@ executing every time step in hand-written CUDA kernels behind a C ABI
 (include/halfwave_b200.h).  No CPU fallback.
 """
 
+from ._abi import get_option, options, set_option
 from .acoustic import AcousticSolver, AcousticState
 from .diagnostics import EnergySeries, RangeFailureError, RunOutput, TraceSeries, compare_traces, energy_drift
 from .efsum import Variant
@@ -41,7 +42,7 @@ __all__ = [
     "build_homogeneous_acoustic", "build_layered_acoustic", "build_layered_elastic", "cfl_limit",
     "compare_traces", "energy_drift", "extend_rows", "ricker", "round_fraction", "round_to",
     "sample_source", "load_medium", "save_medium", "DT16", "PRESETS", "ConfigError", "SimConfig",
-    "parse_config",
+    "parse_config", "set_option", "get_option", "options",
 ]
 
 __version__ = "0.1.0"

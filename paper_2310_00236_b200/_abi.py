@@ -13,8 +13,15 @@ from pathlib import Path
 
 import os
 
-# HALFWAVE_LIB overrides the library path (A/B measurements of alternative builds)
-LIB_PATH = Path(os.environ.get("HALFWAVE_LIB", Path(__file__).resolve().parent / "lib" / "libhalfwave_b200.so"))
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libhalfwave_b200.so"
+
+
+def set_library_path(path) -> None:
+    """Load an alternative build of the library (A/B measurements); before the first call only."""
+    global LIB_PATH
+    if _lib is not None:
+        raise RuntimeError("the library is already loaded")
+    LIB_PATH = Path(path)
 
 ABI_VERSION = 1
 
@@ -37,6 +44,7 @@ EXPORTED = (
     "hw_get_state", "hw_run", "hw_run_device", "hw_last_launch_count", "hw_kernel_path", "hw_transport",
     "hw_last_kernel_ms", "hw_last_error", "hw_version", "hw_selftest_div16",
     "hw_cheap_div_table", "hw_plane_div_mode", "hw_nccl_unique_id", "hw_create_group", "hw_run_group",
+    "hw_set_option", "hw_get_option",
 )
 
 
@@ -122,6 +130,10 @@ def load() -> ctypes.CDLL:
         lib.hw_create_group.restype = ctypes.c_int
         lib.hw_run_group.argtypes = [P(vp), i32, i32, i64, i64, P(dbl), P(dbl), P(dbl), P(dbl), P(i64), P(i64), P(i32)]
         lib.hw_run_group.restype = ctypes.c_int
+    lib.hw_set_option.argtypes = [ctypes.c_char_p, i64]
+    lib.hw_set_option.restype = ctypes.c_int
+    lib.hw_get_option.argtypes = [ctypes.c_char_p, P(i64)]
+    lib.hw_get_option.restype = ctypes.c_int
     lib.hw_version.argtypes = []
     lib.hw_version.restype = ctypes.c_char_p
     for name in ("hw_create", "hw_destroy", "hw_set_state", "hw_get_state", "hw_run", "hw_run_device"):
@@ -137,3 +149,34 @@ def last_error() -> str:
 def check(status: int, what: str) -> None:
     if status != OK:
         raise RuntimeError(f"{what} failed (status {status}): {last_error()}")
+
+
+def set_option(name: str, value: int) -> None:
+    """Process-wide kernel-path option (include/halfwave_b200.h hw_set_option); applies to
+    solvers whose device handle is created afterwards."""
+    check(load().hw_set_option(name.encode(), int(value)), f"hw_set_option({name})")
+
+
+def get_option(name: str) -> int:
+    v = ctypes.c_int64(0)
+    check(load().hw_get_option(name.encode(), ctypes.byref(v)), f"hw_get_option({name})")
+    return int(v.value)
+
+
+class options:
+    """Context manager: ``with options(path=1): ...`` sets options and restores them on exit."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+        self.saved = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.saved[k] = get_option(k)
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.saved.items():
+            set_option(k, v)
+        return False

@@ -27,6 +27,30 @@ namespace {
 
 thread_local std::string g_err;
 
+// ---------------------------------------------------------------- kernel-path options
+// Process-wide switches set through hw_set_option (tests and A/B measurements); read
+// when a handle is created.  Defaults are the production choices.
+struct Option {
+    const char* name;
+    int64_t value, lo, hi;
+    const char* doc;
+};
+Option g_opts[] = {
+    {"path", 0, 0, 1, "0 = fastest eligible kernels, 1 = generic phase kernels only"},
+    {"div", 0, 0, 2, "binary16 division: 0 = table-verified cheap / fast / IEEE per plane, 1 = no cheap path, 2 = IEEE only"},
+    {"small", 1, 0, 1, "persistent small-grid 2D kernels for grids of <= 2^20 cells"},
+    {"tb", 0, 0, 1, "two steps per launch for the fused 2D acoustic kernel (measured slower; opt-in)"},
+    {"fused_el", 1, 0, 1, "one-pass 2D elastic kernel"},
+    {"fused3", 1, 0, 1, "one-pass 3D acoustic kernels (binary16 and binary32 lanes)"},
+    {"fused_el3", 0, 0, 1, "one-pass 3D elastic kernel (measured slower; opt-in)"},
+    {"nccl_self", 0, 0, 1, "a one-rank job with an NCCL id takes the NCCL transport (self exchange: tests)"},
+};
+int64_t opt(const char* name) {
+    for (const Option& o : g_opts)
+        if (strcmp(o.name, name) == 0) return o.value;
+    return 0;
+}
+
 int fail(int code, const std::string& msg) {
     g_err = msg;
     return code;
@@ -376,6 +400,8 @@ struct hw_solver {
     bool fused3_32 = false;   // the same in binary32 lanes (config 3's fp32 arm), ping-pong A <-> B
     bool fused_el = false;    // one-pass 2D elastic step, ping-pong A <-> B
     bool fused_el3 = false;   // one-pass 3D elastic step (2nd order), ping-pong A <-> B
+    float* el3_coef = nullptr;  // its medium coefficient table ([ns][el3_cm][8], in plane_mem)
+    int64_t el3_cm = 0;
     bool el3_stream = false;  // streaming 3D elastic phases
     int stream_blocks = 0;
     unsigned int* counter = nullptr;  // CTA arrival counter of the streaming stress kernel
@@ -516,9 +542,8 @@ int upload_plane(hw_solver* h, int pl) {
                     uint16_t hb = half_bits(r);
                     if (hb == 0 || hb > 0x7bff || !(((*tab)[hb >> 5] >> (hb & 31)) & 1u)) cheap = false;
                 }
-                const char* env = getenv("HALFWAVE_DIV");
-                if (env && strcmp(env, "ieee") == 0) fast = cheap = false;
-                if (env && strcmp(env, "fast") == 0) cheap = false;
+                if (opt("div") == 2) fast = cheap = false;
+                if (opt("div") == 1) cheap = false;
                 mode = cheap ? DIV_CHEAP : (fast ? DIV_FAST : DIV_IEEE);
                 if (cheap) {
                     float* dr = nullptr;
@@ -653,8 +678,7 @@ int setup_handle(hw_solver* h) {
     for (int pl = 0; pl < HW_NPLANES; pl++)
         if ((rc = upload_plane(h, pl))) return rc;
     {
-        const char* path = getenv("HALFWAVE_PATH");
-        bool want = !(path && strcmp(path, "generic") == 0);
+        const bool want = opt("path") == 0;
         int dev_smem = 0, nsm = 0;
         cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, desc->device);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, desc->device);
@@ -684,8 +708,7 @@ int setup_handle(hw_solver* h) {
             }
             // two steps per launch: opt-in (HALFWAVE_TB=1); measured slower than the
             // single-step kernel on B200 (compute/latency-bound)
-            const char* tbe = getenv("HALFWAVE_TB");
-            if (tbe && strcmp(tbe, "1") == 0 && h->world == 1 && h->transport != 2 &&
+            if (opt("tb") == 1 && h->world == 1 && h->transport != 2 &&
                 tb2_eligible(desc->nx, desc->ns, dev_smem)) {
                 if (tb2_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "two-step kernel setup failed");
                 tb2_grid(desc->nx, desc->ns, nsm, &h->tb2_tiles, &h->tb2_bands);
@@ -693,8 +716,8 @@ int setup_handle(hw_solver* h) {
             }
         }
         // small grids: the persistent kernel (latency, not bandwidth, bounds them)
-        const char* sme = getenv("HALFWAVE_SMALL");
-        if (want && !(sme && strcmp(sme, "0") == 0) && h->ac && !h->d3 && h->LS == 16 && h->LU == 16 &&
+        const bool small_ok = opt("small") == 1;
+        if (want && small_ok && h->ac && !h->d3 && h->LS == 16 && h->LU == 16 &&
             h->world == 1 && h->transport == 0 && desc->nx * desc->ns <= (int64_t)1 << 20 &&
             small2d_eligible(desc->nx, desc->ns, nsm, dev_smem)) {
             h->small_nb = small2d_blocks(desc->ns, nsm);
@@ -706,7 +729,7 @@ int setup_handle(hw_solver* h) {
             CU(cudaMalloc(&h->partials2, (size_t)h->small_nb * NCOMP * sizeof(double)));
             h->small = true;
         }
-        if (want && !(sme && strcmp(sme, "0") == 0) && !h->ac && !h->d3 && h->LS == 16 && h->LU == 16 &&
+        if (want && small_ok && !h->ac && !h->d3 && h->LS == 16 && h->LU == 16 &&
             h->world == 1 && h->transport == 0 && desc->nx * desc->ns <= (int64_t)1 << 20 &&
             small_el2d_eligible(desc->nx, desc->ns, nsm, dev_smem)) {
             h->small_nb = small2d_blocks(desc->ns, nsm);
@@ -719,8 +742,7 @@ int setup_handle(hw_solver* h) {
             h->small_el = true;
         }
         // one-pass 2D elastic step (single domain): ping-pong partner buffers
-        const char* fee = getenv("HALFWAVE_FUSED_EL");
-        if (want && !h->small_el && !(fee && strcmp(fee, "0") == 0) && !h->ac && !h->d3 && h->LS == 16 &&
+        if (want && !h->small_el && opt("fused_el") == 1 && !h->ac && !h->d3 && h->LS == 16 &&
             h->LU == 16 && h->world == 1 && h->transport == 0 && el2d_fused_eligible(desc->nx, desc->ns, dev_smem)) {
             for (int j = 0; j < 2 * h->nsol; j++) {
                 int f = h->ext[j % h->nsol];
@@ -743,8 +765,8 @@ int setup_handle(hw_solver* h) {
             h->el_stream = true;
         }
         // one-pass 3D acoustic step (2nd order, single domain): ping-pong partner buffers
-        const char* f3e = getenv("HALFWAVE_FUSED3");
-        if (want && !(f3e && strcmp(f3e, "0") == 0) && h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
+        const bool f3_ok = opt("fused3") == 1;
+        if (want && f3_ok && h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
             h->world == 1 && h->transport == 0 &&
             ac3d_fused_eligible(desc->nx, desc->nm, desc->ns, h->g.pitch, desc->order, dev_smem)) {
             for (int j = 0; j < 2 * h->nsol; j++) {
@@ -761,7 +783,7 @@ int setup_handle(hw_solver* h) {
             h->fused3 = true;
         }
         // the one-pass 3D acoustic step in binary32 lanes (BASELINE config 3's fp32 arm)
-        if (want && !(f3e && strcmp(f3e, "0") == 0) && h->ac && h->d3 && h->LS == 32 && h->LU == 32 &&
+        if (want && f3_ok && h->ac && h->d3 && h->LS == 32 && h->LU == 32 &&
             h->world == 1 && h->transport == 0 &&
             ac3d_fused32_eligible(desc->nx, desc->nm, desc->ns, h->g.pitch, desc->order, dev_smem)) {
             for (int j = 0; j < 2 * h->nsol; j++) {
@@ -786,11 +808,12 @@ int setup_handle(hw_solver* h) {
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
             h->ac3_stream = true;
         }
-        // one-pass 3D elastic step (2nd order, single domain; opt-in: HALFWAVE_FUSED_EL3=1)
-        const char* fe3 = getenv("HALFWAVE_FUSED_EL3");
-        if (want && fe3 && strcmp(fe3, "1") == 0 && !h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
+        // one-pass 3D elastic step (2nd order, single domain, row-uniform media)
+        ElParams EP;
+        if (!h->ac && h->d3) fill_params(h, EP);
+        if (want && opt("fused_el3") == 1 && !h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
             h->world == 1 && h->transport == 0 &&
-            el3d_fused_eligible(desc->nx, desc->nm, desc->ns, h->g.pitch, desc->order, dev_smem)) {
+            el3d_fused_eligible(EP, desc->nx, desc->nm, desc->ns, h->g.pitch, desc->order, dev_smem)) {
             for (int j = 0; j < 2 * h->nsol; j++) {
                 int f = h->ext[j % h->nsol];
                 size_t bytes = (size_t)(field_rows(h, f) + 2 * G) * h->g.slab * esz;
@@ -798,6 +821,10 @@ int setup_handle(hw_solver* h) {
                 CU(cudaMemset(h->mem_b[j], 0, bytes));
             }
             if (el3d_fused_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "fused 3D elastic setup failed");
+            h->el3_cm = el3d_fused_coef_rows(EP);
+            CU(cudaMalloc(&h->el3_coef, (size_t)max_rows * h->el3_cm * 8 * sizeof(float)));
+            h->plane_mem.push_back(h->el3_coef);
+            CU(el3d_fused_coef(EP, h->el3_coef, max_rows, h->el3_cm, 0));
             const int64_t units = (desc->nm / (2048 / desc->nx)) * max_rows;
             int64_t nbs = units / 4;
             if (nbs < 1) nbs = 1;
@@ -1043,10 +1070,9 @@ int hw_create(const hw_desc* desc, hw_solver** out) {
     h->d = *desc;
     h->world = desc->world_size;
     h->rank = desc->rank;
-    // HALFWAVE_NCCL_SELF=1 (test hook): a one-rank job still takes the NCCL transport,
-    // its periodic ghosts filled by send/recv to itself, so the whole NCCL path runs on one GPU
-    const char* self_env = getenv("HALFWAVE_NCCL_SELF");
-    const bool nccl_self = h->world == 1 && self_env && strcmp(self_env, "1") == 0 && desc->nccl_unique_id;
+    // option nccl_self (test hook): a one-rank job still takes the NCCL transport, its
+    // periodic ghosts filled by send/recv to itself, so the whole NCCL path runs on one GPU
+    const bool nccl_self = h->world == 1 && opt("nccl_self") == 1 && desc->nccl_unique_id;
     if (h->world > 1 || nccl_self) {  // one process per GPU: NCCL transport
         if (!desc->nccl_unique_id) { release_handle(h); return fail(HW_EINVAL, "world_size > 1 needs nccl_unique_id"); }
         if ((rc = nccl_load())) { release_handle(h); return rc; }
@@ -1365,6 +1391,12 @@ static void fused_el3_bufs(const hw_solver* h, int cur, ElParams& P, El3In& in) 
         o->base = (char*)wr[j] + ghost;
         *q = (const __half*)((const char*)rd[j] + ghost);
     }
+    in.coef = h->el3_coef;
+    in.coef_m = h->el3_cm;
+    in.div_mode[0] = h->lp[HW_PL_RHO_X].div_mode;
+    in.div_mode[1] = h->lp[HW_PL_RHO_S].div_mode;
+    in.div_mode[2] = h->lp[HW_PL_RHO_M].div_mode;
+    in.pad = 0;
 }
 
 static void fused_bufs(const hw_solver* h, __half* bufs[2][FUSED_NSTREAM]) {
@@ -1824,6 +1856,27 @@ int hw_cheap_div_table(int32_t device, uint32_t* bits1024) {
 int hw_plane_div_mode(const hw_solver* h, int32_t plane) {
     if (!h || plane < 0 || plane >= HW_NPLANES) return -1;
     return h->lp[plane].div_mode;
+}
+
+int hw_set_option(const char* name, int64_t value) {
+    if (!name) return fail(HW_EINVAL, "hw_set_option: null name");
+    for (Option& o : g_opts)
+        if (strcmp(o.name, name) == 0) {
+            if (value < o.lo || value > o.hi) return fail(HW_EINVAL, std::string("hw_set_option: value out of range for ") + name);
+            o.value = value;
+            return HW_OK;
+        }
+    return fail(HW_EINVAL, std::string("hw_set_option: unknown option ") + name);
+}
+
+int hw_get_option(const char* name, int64_t* value) {
+    if (!name || !value) return fail(HW_EINVAL, "hw_get_option: null argument");
+    for (const Option& o : g_opts)
+        if (strcmp(o.name, name) == 0) {
+            *value = o.value;
+            return HW_OK;
+        }
+    return fail(HW_EINVAL, std::string("hw_get_option: unknown option ") + name);
 }
 
 const char* hw_version(void) { return "halfwave_b200 abi=1 arch=sm_100a"; }

@@ -126,8 +126,15 @@ void launch_el2d_fused(int variant, int order, const ElParams& P, const El2In& i
 struct El3In {
     const __half *vx, *vs, *vm, *sxx, *sss, *smm, *sxs, *sxm, *sms;
     const __half *rvx, *rvs, *rvm, *rsxx, *rsss, *rsmm, *rsxs, *rsxm, *rsms;
+    const float* coef;   // [ns][coef_m][8]: rcp(rho_x, rho_s, rho_m), 0, stiff, lam, mu_n, 0
+    int64_t coef_m;      // coefficient rows per slab: 1 (planes constant along mid) or nm
+    int32_t div_mode[3]; // DivMode of rho_x, rho_s, rho_m
+    int32_t pad;
 };
-bool el3d_fused_eligible(int64_t nx, int64_t nm, int64_t ns, int64_t pitch, int order, int max_smem);
+bool el3d_fused_eligible(const ElParams& P, int64_t nx, int64_t nm, int64_t ns, int64_t pitch, int order,
+                         int max_smem);
+int64_t el3d_fused_coef_rows(const ElParams& P);
+cudaError_t el3d_fused_coef(const ElParams& P, float* out, int64_t ns, int64_t cm, cudaStream_t st);
 cudaError_t el3d_fused_prepare(int64_t nx);
 void launch_el3d_fused(int variant, const ElParams& P, const El3In& in, const StreamIO& IO, int nblocks, int64_t n,
                        double src, int sample, int64_t eidx, cudaStream_t st);

@@ -164,7 +164,7 @@ __device__ __forceinline__ void e_finish_rc(EH2 rhs, float rc, __half2 dt2, int 
 }
 
 // planes constant along x (constant, slow-layered, or per (slow, mid) row in 3D)
-__device__ __forceinline__ bool e_rowdiv(const PlaneView& v) { return v.div_mode == DIV_CHEAP && v.sx == 0; }
+__host__ __device__ __forceinline__ bool e_rowdiv(const PlaneView& v) { return v.div_mode == DIV_CHEAP && v.sx == 0; }
 __device__ __forceinline__ float e_rcp_at(const PlaneView& v, int64_t s, int64_t m) {
     return __ldg(v.rcp + s * v.ss + m * v.sm);
 }

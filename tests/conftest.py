@@ -29,3 +29,21 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+@pytest.fixture
+def hwopt():
+    """Set library kernel-path options (hw_set_option) for one test; restored afterwards."""
+    import paper_2310_00236_b200 as hw
+
+    saved = {}
+
+    def set_(**kw):
+        for k, v in kw.items():
+            if k not in saved:
+                saved[k] = hw.get_option(k)
+            hw.set_option(k, v)
+
+    yield set_
+    for k, v in saved.items():
+        hw.set_option(k, v)

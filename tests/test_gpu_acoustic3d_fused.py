@@ -44,16 +44,16 @@ def test_fused3d_tiles_and_slab_splits(nx, ny, nz):
 
 
 @pytest.mark.parametrize("nt", [11, 12])
-def test_fused3d_equals_two_phase_and_generic(monkeypatch, nt):
+def test_fused3d_equals_two_phase_and_generic(hwopt, nt):
     s1, st1 = _case(512, 16, 24, nt)
     o1 = s1.run(hw.Variant.OP3, st1)
     assert s1.kernel_path() == "fused3d"
-    monkeypatch.setenv("HALFWAVE_FUSED3", "0")
+    hwopt(fused3=0)
     s2, st2 = _case(512, 16, 24, nt)
     o2 = s2.run(hw.Variant.OP3, st2)
     assert s2.kernel_path() == "stream3d"
     _same(s1, st1, o1, s2, st2, o2)
-    monkeypatch.setenv("HALFWAVE_PATH", "generic")
+    hwopt(path=1)
     s3, st3 = _case(512, 16, 24, nt)
     o3 = s3.run(hw.Variant.OP3, st3)
     assert s3.kernel_path() == "generic"

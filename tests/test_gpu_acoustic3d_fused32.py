@@ -79,11 +79,11 @@ def test_fused3d_f32_row_divisors(layers):
 
 
 @pytest.mark.parametrize("nt", [11, 12])
-def test_fused3d_f32_equals_generic(monkeypatch, nt):
+def test_fused3d_f32_equals_generic(hwopt, nt):
     s1, st1 = _case(512, 16, 24, nt)
     o1 = s1.run(None, st1)
     assert s1.kernel_path() == "fused3d-f32"
-    monkeypatch.setenv("HALFWAVE_PATH", "generic")
+    hwopt(path=1)
     s2, st2 = _case(512, 16, 24, nt)
     o2 = s2.run(None, st2)
     assert s2.kernel_path() == "generic"

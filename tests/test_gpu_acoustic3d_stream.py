@@ -14,9 +14,9 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(autouse=True)
-def _two_phase(monkeypatch):
+def _two_phase(hwopt):
     """2nd-order single-domain cases would take the one-pass kernel (test_gpu_acoustic3d_fused.py)."""
-    monkeypatch.setenv("HALFWAVE_FUSED3", "0")
+    hwopt(fused3=0)
 
 
 def _case(nx, ny, nz, nt, *, order=2, full=True, slabs=1, amp=5.0, seed=0, recs=None):
@@ -70,12 +70,12 @@ def test_stream3d_tiles_and_slab_splits(ny, nz):
     _check(s, st, out, ref)
 
 
-def test_stream3d_nx512_equals_generic(monkeypatch):
+def test_stream3d_nx512_equals_generic(hwopt):
     s1, st1 = _case(512, 16, 24, 12)
     out1 = s1.run(hw.Variant.OP3, st1)
     assert s1.kernel_path() == "stream3d"
     assert s1.last_launch_count() == 2 + 2 * 12
-    monkeypatch.setenv("HALFWAVE_PATH", "generic")
+    hwopt(path=1)
     s2, st2 = _case(512, 16, 24, 12)
     out2 = s2.run(hw.Variant.OP3, st2)
     assert s2.kernel_path() == "generic"

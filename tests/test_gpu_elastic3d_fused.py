@@ -1,5 +1,5 @@
 """The one-pass 3D elastic step (csrc/hw_elastic3d_fused.cu: 2nd order, binary16, single
-periodic domain, ping-pong buffers; opt-in with HALFWAVE_FUSED_EL3=1) against the CPU
+periodic domain, ping-pong buffers, nx 256 or 512, media constant along x) against the CPU
 oracle and the two-phase streaming kernels: bit-exact fields, traces and failure steps;
 energy within 1e-12."""
 
@@ -15,8 +15,8 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(autouse=True)
-def _fused(monkeypatch):
-    monkeypatch.setenv("HALFWAVE_FUSED_EL3", "1")
+def _fused(hwopt):
+    hwopt(fused_el3=1)
 
 
 @pytest.mark.parametrize("variant", [None, hw.Variant.OP3, hw.Variant.OP6])
@@ -34,7 +34,8 @@ def test_el3d_fused_tiles_and_slab_splits(nx, ny, nz):
     s, st = _case(nx, ny, nz, 6, full=(nz == 20))
     ref = oracle.run_solver(s, hw.Variant.OP6, st)
     out = s.run(hw.Variant.OP6, st)
-    assert s.kernel_path() == "fused3d-el"
+    # media varying along x (full planes) take the streaming kernels
+    assert s.kernel_path() == ("stream3d" if nz == 20 else "fused3d-el")
     _check(s, st, out, ref)
 
 
@@ -52,11 +53,11 @@ def test_el3d_fused_sources_on_tile_edges():
 
 
 @pytest.mark.parametrize("nt", [7, 8])
-def test_el3d_fused_equals_two_phase(monkeypatch, nt):
+def test_el3d_fused_equals_two_phase(hwopt, nt):
     s1, st1 = _case(512, 16, 24, nt)
     o1 = s1.run(hw.Variant.OP6, st1)
     assert s1.kernel_path() == "fused3d-el"
-    monkeypatch.setenv("HALFWAVE_FUSED_EL3", "0")
+    hwopt(fused_el3=0)
     s2, st2 = _case(512, 16, 24, nt)
     o2 = s2.run(hw.Variant.OP6, st2)
     assert s2.kernel_path() == "stream3d"
@@ -84,3 +85,22 @@ def test_el3d_fused_range_failure_and_resume():
     a.run(hw.Variant.OP3, sa)
     for j, n in enumerate(a.FIELDS):
         assert_same_bits(getattr(sa, n).values, ref["fields"][j], n)
+
+
+@pytest.mark.parametrize("rho", [1.0, 1.37, 0.61])
+def test_el3d_fused_every_division_mode(rho):
+    """Densities whose binary16 divisors take the verified-reciprocal, the fast exact and the IEEE
+    paths: the kernel picks the mode per plane (hw_plane_div_mode) and stays bit-exact."""
+    nx, ny, nz = 256, 16, 10
+    med = hw.build_layered_elastic(nx, ny, [(0.5, rho, 2.0, 1.0), (1.0, 1.7 * rho, 2.6, 1.2)], nz=nz)
+    dx = 1.0 / nx
+    g = hw.GridSpec(nx, ny, dx, float(np.float16(0.3 * dx / (med.c_max() * np.sqrt(3)))), 5, nz=nz, order=2)
+    s = hw.ElasticSolver(g, med, None, stencil_precision=hw.Precision.FP16, receivers=((3, 4, 5),), energy_every=2)
+    st = s.new_state()
+    rng = np.random.default_rng(7)
+    for name in ("vx", "vy", "vz", "sxx", "syz"):
+        getattr(st, name).values = rng.uniform(-0.1, 0.1, getattr(st, name).values.shape).astype(np.float16)
+    ref = oracle.run_solver(s, hw.Variant.OP6, st)
+    out = s.run(hw.Variant.OP6, st)
+    assert s.kernel_path() == "fused3d-el"
+    _check(s, st, out, ref)

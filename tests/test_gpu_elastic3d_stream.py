@@ -66,11 +66,11 @@ def test_el3d_stream_tiles_sources_full_media(ny, nz, kind):
     _check(s, st, out, ref)
 
 
-def test_el3d_stream_nx512_equals_generic(monkeypatch):
+def test_el3d_stream_nx512_equals_generic(hwopt):
     s1, st1 = _case(512, 12, 16, 8)
     out1 = s1.run(hw.Variant.OP6, st1)
     assert s1.kernel_path() == "stream3d"
-    monkeypatch.setenv("HALFWAVE_PATH", "generic")
+    hwopt(path=1)
     s2, st2 = _case(512, 12, 16, 8)
     out2 = s2.run(hw.Variant.OP6, st2)
     assert s2.kernel_path() == "generic"

@@ -15,8 +15,8 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(autouse=True)
-def _no_small(monkeypatch):  # these grids would otherwise take the persistent small-grid kernel
-    monkeypatch.setenv("HALFWAVE_SMALL", "0")
+def _no_small(hwopt):  # these grids would otherwise take the persistent small-grid kernel
+    hwopt(small=0)
 
 
 def _same(s1, st1, o1, s2, st2, o2):
@@ -61,16 +61,16 @@ def test_fused_el_full_medium_and_explosive_source(fs):
 
 
 @pytest.mark.parametrize("nt", [39, 40])
-def test_fused_el_equals_stream_and_generic(monkeypatch, nt):
+def test_fused_el_equals_stream_and_generic(hwopt, nt):
     s1, st1 = _case(1024, 300, nt, full=True)
     o1 = s1.run(hw.Variant.OP6, st1)
     assert s1.kernel_path() == "fused2d-el"
-    monkeypatch.setenv("HALFWAVE_FUSED_EL", "0")
+    hwopt(fused_el=0)
     s2, st2 = _case(1024, 300, nt, full=True)
     o2 = s2.run(hw.Variant.OP6, st2)
     assert s2.kernel_path() == "stream2d"
     _same(s1, st1, o1, s2, st2, o2)
-    monkeypatch.setenv("HALFWAVE_PATH", "generic")
+    hwopt(path=1)
     s3, st3 = _case(1024, 300, nt, full=True)
     o3 = s3.run(hw.Variant.OP6, st3)
     assert s3.kernel_path() == "generic"

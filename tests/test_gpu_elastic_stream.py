@@ -14,9 +14,9 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(autouse=True)
-def _streaming_kernels(monkeypatch):  # these grids would otherwise take the persistent small-grid kernel
-    monkeypatch.setenv("HALFWAVE_SMALL", "0")  # (or, single domain, the one-pass kernel: test_gpu_elastic_fused.py)
-    monkeypatch.setenv("HALFWAVE_FUSED_EL", "0")
+def _streaming_kernels(hwopt):  # these grids would otherwise take the persistent small-grid kernel
+    hwopt(small=0)  # (or, single domain, the one-pass kernel: test_gpu_elastic_fused.py)
+    hwopt(fused_el=0)
 
 LAYERS = [(0.3, 2.0, 2.0, 1.0), (0.7, 2.3, 2.8, 1.4), (1.0, 2.6, 3.2, 0.0)]
 
@@ -77,11 +77,11 @@ def test_stream_full_medium_and_explosive_source():
     _check(s, st, out, ref)
 
 
-def test_stream_equals_generic_kernels(monkeypatch):
+def test_stream_equals_generic_kernels(hwopt):
     s1, st1 = _case(1024, 300, 40, full=True)
     out1 = s1.run(hw.Variant.OP6, st1)
     assert s1.kernel_path() == "stream2d"
-    monkeypatch.setenv("HALFWAVE_PATH", "generic")
+    hwopt(path=1)
     s2, st2 = _case(1024, 300, 40, full=True)
     out2 = s2.run(hw.Variant.OP6, st2)
     assert s2.kernel_path() == "generic"

@@ -15,8 +15,8 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(autouse=True)
-def _streaming_kernel(monkeypatch):  # these grids would otherwise take the persistent small-grid kernel
-    monkeypatch.setenv("HALFWAVE_SMALL", "0")
+def _streaming_kernel(hwopt):  # these grids would otherwise take the persistent small-grid kernel
+    hwopt(small=0)
 
 
 def _case(nx, ny, nt, *, order=4, amp=2.0, every=5, seed=0, src_row=3, layered=True):
@@ -66,10 +66,10 @@ def test_fused_row_bands_and_wrap(ny):
     _check(s, st, out, ref)
 
 
-def test_fused_equals_two_phase_kernels(monkeypatch):
+def test_fused_equals_two_phase_kernels(hwopt):
     s1, st1 = _case(1024, 256, 40)
     out1 = s1.run(hw.Variant.OP3, st1)
-    monkeypatch.setenv("HALFWAVE_PATH", "generic")
+    hwopt(path=1)
     s2, st2 = _case(1024, 256, 40)
     out2 = s2.run(hw.Variant.OP3, st2)
     for n in s1.FIELDS:

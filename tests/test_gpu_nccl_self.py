@@ -1,4 +1,4 @@
-"""The NCCL transport (one process per GPU) on real hardware: with HALFWAVE_NCCL_SELF=1 a
+"""The NCCL transport (one process per GPU) on real hardware: with the option nccl_self=1 a
 one-rank torch.distributed job takes the NCCL path — libnccl dlopen'ed, communicator
 from hw_nccl_unique_id, periodic ghosts exchanged by grouped ncclSend/ncclRecv to itself
 after every phase, control blocks all-gathered, energy all-reduced, traces broadcast —
@@ -16,14 +16,14 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture
-def one_rank_job(monkeypatch):
+def one_rank_job(hwopt):
     import torch.distributed as dist
 
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
-    monkeypatch.setenv("HALFWAVE_NCCL_SELF", "1")
+    hwopt(nccl_self=1)
     yield
     dist.destroy_process_group()
 

@@ -23,10 +23,10 @@ def _run_names():
 
 
 @pytest.fixture(params=["auto", "fast", "ieee"])
-def div_mode(request, monkeypatch):
+def div_mode(request, hwopt):
     """Run under each binary16 division path: table-verified cheap (auto), branch-free exact, IEEE."""
     if request.param != "auto":
-        monkeypatch.setenv("HALFWAVE_DIV", request.param)
+        hwopt(div={"fast": 1, "ieee": 2}[request.param])
     return request.param
 
 

@@ -61,11 +61,11 @@ def test_small_shapes_and_media(nx, ny, layered):
     _check(s, st, out, ref)
 
 
-def test_small_equals_fused(monkeypatch):
+def test_small_equals_fused(hwopt):
     s1, st1 = _case(512, 256, 60, every=5)
     out1 = s1.run(hw.Variant.OP6, st1)
     assert s1.kernel_path() == "small2d" and s1.last_launch_count() == 2 + 1
-    monkeypatch.setenv("HALFWAVE_SMALL", "0")
+    hwopt(small=0)
     s2, st2 = _case(512, 256, 60, every=5)
     out2 = s2.run(hw.Variant.OP6, st2)
     assert s2.kernel_path() == "fused2d"
@@ -142,11 +142,11 @@ def test_small_elastic_shapes_and_sources(nx, ny, kind):
     _check(s, st, out, ref)
 
 
-def test_small_elastic_equals_phase_kernels(monkeypatch):
+def test_small_elastic_equals_phase_kernels(hwopt):
     s1, st1 = _el(512, 200, 40)
     out1 = s1.run(hw.Variant.OP6, st1)
     assert s1.kernel_path() == "small2d"
-    monkeypatch.setenv("HALFWAVE_SMALL", "0")
+    hwopt(small=0)
     s2, st2 = _el(512, 200, 40)
     out2 = s2.run(hw.Variant.OP6, st2)
     assert s2.kernel_path() == "fused2d-el"

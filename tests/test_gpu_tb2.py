@@ -1,6 +1,6 @@
 """Two steps per launch (temporal blocking, csrc/hw_tb2d.cu) for the 2D acoustic
 binary16 path: bit-exact against the CPU oracle and against the single-step fused
-kernel (the default; the two-step kernel is opt-in, HALFWAVE_TB=1), for odd and even step counts, several x tiles, receiver lines,
+kernel (the default; the two-step kernel is opt-in, option tb=1), for odd and even step counts, several x tiles, receiver lines,
 energy every step, and range failures in either step of a pair (the host replays a
 failing first step alone)."""
 
@@ -15,9 +15,9 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(autouse=True)
-def _two_step(monkeypatch):  # the two-step kernel is opt-in
-    monkeypatch.setenv("HALFWAVE_TB", "1")
-    monkeypatch.setenv("HALFWAVE_SMALL", "0")
+def _two_step(hwopt):  # the two-step kernel is opt-in
+    hwopt(tb=1)
+    hwopt(small=0)
 
 
 def _case(nx, ny, nt, *, order=4, amp=2.0, every=5, seed=0, src_row=3, layered=True, recs=None):
@@ -70,12 +70,12 @@ def test_tb2_tiles_bands_and_media(nx, ny):
     _check(s, st, out, ref)
 
 
-def test_tb2_equals_single_step_kernel(monkeypatch):
+def test_tb2_equals_single_step_kernel(hwopt):
     recs = tuple((x, 9) for x in range(0, 4096, 7)) + tuple((1000, y) for y in range(0, 256, 3))
     s1, st1 = _case(4096, 256, 26, every=1, recs=recs)
     out1 = s1.run(hw.Variant.OP6, st1)
     assert s1.kernel_path() == "fused2d-tb2"
-    monkeypatch.setenv("HALFWAVE_TB", "0")
+    hwopt(tb=0)
     s2, st2 = _case(4096, 256, 26, every=1, recs=recs)
     out2 = s2.run(hw.Variant.OP6, st2)
     assert s2.kernel_path() == "fused2d"

@@ -1,6 +1,6 @@
 #!/bin/bash
 # Build an A/B variant of the library: tools/build_variant.sh <name> '<sed script>'
-# -> paper_2310_00236_b200/lib/variants/lib_<name>.so (use with HALFWAVE_LIB=...)
+# -> paper_2310_00236_b200/lib/variants/lib_<name>.so (load with paper_2310_00236_b200._abi.set_library_path(...))
 # VARIANT_FROM_HEAD="a.cu b.cuh": take those csrc files from git HEAD (A/B of uncommitted edits)
 set -e
 cd "$(dirname "$0")/.."

@@ -14,7 +14,17 @@ sys.path.insert(0, str(ROOT))
 import paper_2310_00236_b200 as hw  # noqa: E402
 
 CPU = "--cpu" in sys.argv
-ARGS = [a for a in sys.argv[1:] if a != "--cpu"]
+# --opt name=value: library kernel-path options (hw_set_option), e.g. --opt fused_el3=0
+ARGS = []
+_it = iter(sys.argv[1:])
+for a in _it:
+    if a == "--cpu":
+        continue
+    if a == "--opt":
+        k, v = next(_it).split("=")
+        hw.set_option(k, int(v))
+        continue
+    ARGS.append(a)
 NT = int(ARGS[0]) if ARGS and ARGS[0].isdigit() else 50
 F16 = hw.Precision.FP16
 _PEAKS = ROOT / "MEASURED_PEAKS.json"

@@ -6,8 +6,14 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import tools.measure_configs as mc  # noqa: E402
 import paper_2310_00236_b200 as hw  # noqa: E402
 
-which = sys.argv[1]
-nt = int(sys.argv[2]) if len(sys.argv) > 2 else 6
+args = sys.argv[1:]
+while "--opt" in args:  # --opt name=value: library kernel-path options (hw_set_option)
+    i = args.index("--opt")
+    k, v = args[i + 1].split("=")
+    hw.set_option(k, int(v))
+    del args[i:i + 2]
+which = args[0]
+nt = int(args[1]) if len(args) > 1 else 6
 
 def cfg2():
     import bench
