@@ -204,7 +204,8 @@ int hw_plane_div_mode(const hw_solver* h, int32_t plane);
  *   "tb"        0 | 1 two steps per launch, fused 2D acoustic (opt-in, measured slower)
  *   "fused_el"  1 one-pass 2D elastic kernel | 0 two-phase kernels
  *   "fused3"    1 one-pass 3D acoustic kernels | 0 two-phase kernels
- *   "fused_el3" one-pass 3D elastic kernel (see hw_kernel_path's "fused3d-el")
+ *   "fused_el3" 1 one-pass 3D elastic kernel (2nd order, media constant along x) | 0 two-phase
+ *   "el3_group" 4 at most this many CTAs of the one-pass 3D elastic kernel stream adjacent tiles
  *   "nccl_self" 0 | 1 a one-rank job given an NCCL id takes the NCCL transport (tests)
  * HW_EINVAL for an unknown name or an out-of-range value. */
 int hw_set_option(const char* name, int64_t value);

@@ -42,7 +42,8 @@ Option g_opts[] = {
     {"tb", 0, 0, 1, "two steps per launch for the fused 2D acoustic kernel (measured slower; opt-in)"},
     {"fused_el", 1, 0, 1, "one-pass 2D elastic kernel"},
     {"fused3", 1, 0, 1, "one-pass 3D acoustic kernels (binary16 and binary32 lanes)"},
-    {"fused_el3", 0, 0, 1, "one-pass 3D elastic kernel (measured slower; opt-in)"},
+    {"fused_el3", 1, 0, 1, "one-pass 3D elastic kernel (2nd order, media constant along x) | 0 two-phase kernels"},
+    {"el3_group", 4, 1, 4, "one-pass 3D elastic kernel: at most this many CTAs stream adjacent tiles side by side"},
     {"nccl_self", 0, 0, 1, "a one-rank job with an NCCL id takes the NCCL transport (self exchange: tests)"},
 };
 int64_t opt(const char* name) {
@@ -402,6 +403,7 @@ struct hw_solver {
     bool fused_el3 = false;   // one-pass 3D elastic step (2nd order), ping-pong A <-> B
     float* el3_coef = nullptr;  // its medium coefficient table ([ns][el3_cm][8], in plane_mem)
     int64_t el3_cm = 0;
+    int el3_group = 1;          // its CTA groups of adjacent tiles (hw_elastic3d_fused.cu)
     bool el3_stream = false;  // streaming 3D elastic phases
     int stream_blocks = 0;
     unsigned int* counter = nullptr;  // CTA arrival counter of the streaming stress kernel
@@ -808,7 +810,7 @@ int setup_handle(hw_solver* h) {
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
             h->ac3_stream = true;
         }
-        // one-pass 3D elastic step (2nd order, single domain, row-uniform media)
+        // one-pass 3D elastic step (2nd order, single domain, media constant along x)
         ElParams EP;
         if (!h->ac && h->d3) fill_params(h, EP);
         if (want && opt("fused_el3") == 1 && !h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
@@ -829,6 +831,13 @@ int setup_handle(hw_solver* h) {
             int64_t nbs = units / 4;
             if (nbs < 1) nbs = 1;
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
+            const int64_t tiles = desc->nm / (2048 / desc->nx);
+            for (int g : {4, 2, 1})
+                if (g <= opt("el3_group") && h->stream_blocks % g == 0 && tiles % g == 0 &&
+                    (tiles / g) * max_rows >= h->stream_blocks / g) {
+                    h->el3_group = g;
+                    break;
+                }
             h->fused_el3 = true;
         }
         if (want && !h->fused_el3 && !h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
@@ -1396,7 +1405,7 @@ static void fused_el3_bufs(const hw_solver* h, int cur, ElParams& P, El3In& in) 
     in.div_mode[0] = h->lp[HW_PL_RHO_X].div_mode;
     in.div_mode[1] = h->lp[HW_PL_RHO_S].div_mode;
     in.div_mode[2] = h->lp[HW_PL_RHO_M].div_mode;
-    in.pad = 0;
+    in.group = h->el3_group;
 }
 
 static void fused_bufs(const hw_solver* h, __half* bufs[2][FUSED_NSTREAM]) {

@@ -156,23 +156,100 @@ __device__ __forceinline__ void add_srcv(EH2 r[P], int sj, int sln, __half srch)
 // store of the thread's cells of slab s at element offset so = s * slab + goff; the periodic
 // ghost slabs are written through on the first / last G slabs only (CTA-uniform branch)
 template <int P>
+__device__ __forceinline__ void ghost_st(__half* b, int64_t up, int64_t dn, EV<P> v) {
+    if (up) stv<P>(b + up, v);
+    if (dn) stv<P>(b + dn, v);
+}
+template <int P>
 __device__ __forceinline__ void gst(const FieldView& f, int64_t so, bool edge, int s, int64_t slab, const EV<P>& v) {
     __half* b = reinterpret_cast<__half*>(f.base) + so;
     stv<P>(b, v);
     if (edge && f.gtop == GHOST_PERIODIC) {
         const int nr = (int)f.rows;
-        if (s >= nr - G) stv<P>(b - (int64_t)nr * slab, v);
-        if (s < G) stv<P>(b + (int64_t)nr * slab, v);
+        ghost_st<P>(b, s >= nr - G ? -(int64_t)nr * slab : 0, s < G ? (int64_t)nr * slab : 0, v);
     }
 }
 
-// velocity increment + advance for one pair: division by the row-uniform density through its
-// verified reciprocal (DIV_CHEAP) or by the value itself (fast exact / IEEE binary16 division)
+// velocity increment + advance for one pair, divided by the row-uniform density b:
+//   DIV_CHEAP: fl16(fl32(a * rcp_rn(b))) with the table-verified reciprocal cf (inline);
+//   DIV_FAST : the branch-free exact division of lane<16>::div (hw_lanes.cuh) with b = cf and its
+//              rcp.approx rf computed once per row -- the same ops, so the same bits (inline);
+//   DIV_IEEE : zero / non-finite divisors.
+__device__ __forceinline__ __half x3_div1(__half a, float fb, float r) {
+    const float fa = __half2float(a);
+    const float q0 = __fmul_rn(fa, r);
+    const float e = __fmaf_rn(-fb, q0, fa);
+    const float q1 = __fmaf_rn(e, r, q0);
+    const bool keep = (e == 0.0f) || !(fabsf(q0) < INFINITY);
+    return __float2half_rn(keep ? q0 : q1);
+}
+__device__ __forceinline__ EH2 x3_div_ieee(EH2 a, float fb) {
+    return EO2::div_ieee(a, vsplat<16, 2>(__float2half_rn(fb)));
+}
 template <int V>
-__device__ __forceinline__ void x3_finish(EH2 a, float cf, int mode, __half dt, __half2 dt2, __half srch, EH2& u,
+__device__ __forceinline__ void x3_finish(EH2 a, float cf, float rf, int mode, __half2 dt2, __half srch, EH2& u,
                                           EH2& t) {
-    if (mode == DIV_CHEAP) e_finish_rc<V>(a, cf, dt2, -1, srch, u, t);
-    else a3_finish<V>(a, vsplat<16, 2>(__float2half_rn(cf)), mode, dt, -1, 0.0, u, t);
+    if (mode == DIV_CHEAP) {
+        e_finish_rc<V>(a, cf, dt2, -1, srch, u, t);
+    } else {
+        EH2 q;
+        if (mode == DIV_FAST) {
+            q.e[0] = x3_div1(a.e[0], cf, rf);
+            q.e[1] = x3_div1(a.e[1], cf, rf);
+        } else {
+            q = x3_div_ieee(a, cf);
+        }
+        e2_finish_nd<V>(q, dt2, -1, srch, u, t);  // x dt, then the advance (same ops as finish())
+    }
+}
+__device__ __forceinline__ float x3_rcp(float b) {  // lane<16>::div's reciprocal
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(b));
+    return r;
+}
+
+// TMA requests of one slot (thread 0)
+template <int NX, int TM>
+__device__ __forceinline__ void x3_issue_tap(__half* d, uint64_t* b, const __half* sxx, const __half* sxs,
+                                          const __half* sss, const __half* sxm, const __half* sms, const __half* smm,
+                                          int64_t slab, int s, int m0, int nm) {
+    constexpr int R1 = TM + 1, R2 = TM + 2;
+    constexpr uint32_t rb = NX * sizeof(__half);
+    mbar_arrive_expect_tx(b, (uint32_t)(3 * R1 + 3 * R2) * rb);
+    a3_rows(d, sxx, slab, s, m0, m0 + TM + 1, nm, NX, b);
+    a3_rows(d + R1 * NX, sxs, slab, s, m0, m0 + TM + 1, nm, NX, b);
+    a3_rows(d + 2 * R1 * NX, sss, slab, s, m0, m0 + TM + 1, nm, NX, b);
+    a3_rows(d + 3 * R1 * NX, sxm, slab, s, m0 - 1, m0 + TM + 1, nm, NX, b);
+    a3_rows(d + (3 * R1 + R2) * NX, sms, slab, s, m0 - 1, m0 + TM + 1, nm, NX, b);
+    a3_rows(d + (3 * R1 + 2 * R2) * NX, smm, slab, s, m0 - 1, m0 + TM + 1, nm, NX, b);
+}
+template <int NX, int TM>
+__device__ __forceinline__ void x3_issue_a(__half* d, uint64_t* b, const __half* vx, const __half* vs, const __half* vm,
+                                        const __half* rvx, const __half* rvs, const __half* rvm, int comp,
+                                        int64_t slab, int s, int m0, int nm) {
+    constexpr int R1 = TM + 1;
+    constexpr uint32_t rb = NX * sizeof(__half);
+    mbar_arrive_expect_tx(b, (uint32_t)((comp ? 6 : 3) * R1) * rb);
+    a3_rows(d, vx, slab, s, m0, m0 + TM + 1, nm, NX, b);
+    a3_rows(d + R1 * NX, vs, slab, s, m0, m0 + TM + 1, nm, NX, b);
+    a3_rows(d + 2 * R1 * NX, vm, slab, s, m0 - 1, m0 + TM, nm, NX, b);
+    if (comp) {
+        a3_rows(d + 3 * R1 * NX, rvx, slab, s, m0, m0 + TM + 1, nm, NX, b);
+        a3_rows(d + 4 * R1 * NX, rvs, slab, s, m0, m0 + TM + 1, nm, NX, b);
+        a3_rows(d + 5 * R1 * NX, rvm, slab, s, m0 - 1, m0 + TM, nm, NX, b);
+    }
+}
+template <int NX, int TM>
+__device__ __forceinline__ void x3_issue_b(__half* d, uint64_t* b, const __half* r0, const __half* r1, const __half* r2,
+                                        const __half* r3, const __half* r4, const __half* r5, int64_t off) {
+    constexpr uint32_t tb = (uint32_t)(TM * NX * sizeof(__half));
+    mbar_arrive_expect_tx(b, 6 * tb);
+    tma_load_1d(d, r0 + off, tb, b);
+    tma_load_1d(d + TM * NX, r1 + off, tb, b);
+    tma_load_1d(d + 2 * TM * NX, r2 + off, tb, b);
+    tma_load_1d(d + 3 * TM * NX, r3 + off, tb, b);
+    tma_load_1d(d + 4 * TM * NX, r4 + off, tb, b);
+    tma_load_1d(d + 5 * TM * NX, r5 + off, tb, b);
 }
 
 template <int V, int NX, int CPT, bool SAMPLE>
@@ -222,13 +299,18 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
     const int cm = (int)in.coef_m;  // coefficient rows per slab: 1 (slow-layered) or nm
 
     auto wrap = [&](int s) { return s < 0 ? s + ns : (s >= ns ? s - ns : s); };
-    const int tiles = nm / TM;
+    // Work split: groups of `grp` CTAs own `grp` adjacent mid tiles and stream the same slab
+    // range side by side, so the halo rows one CTA reads are the rows its neighbour in the
+    // group reads (or wrote) at about the same time: L2 hits instead of DRAM re-reads.  The
+    // group's (tile group, slab) units are split evenly over the groups.
+    const int grp = in.group, ngrp = (int)gridDim.x / grp, gid = (int)blockIdx.x / grp, gr = (int)blockIdx.x % grp;
+    const int tiles = nm / TM / grp;  // tile groups
     const int64_t U = (int64_t)tiles * ns;
-    int64_t u = (int64_t)blockIdx.x * U / gridDim.x;
-    const int64_t u1 = (int64_t)(blockIdx.x + 1) * U / gridDim.x;
+    int64_t u = (int64_t)gid * U / ngrp;
+    const int64_t u1 = (int64_t)(gid + 1) * U / ngrp;
     int gi = 0, ga = 0, gb = 0;  // running use counters of the tap slots, the A and the B slot
     while (u < u1) {
-        const int tile = (int)(u / ns), sb = (int)(u % ns);
+        const int tile = (int)(u / ns) * grp + gr, sb = (int)(u % ns);
         const int se = (int)min((int64_t)ns, sb + (u1 - u));
         u += se - sb;
         const int m0 = tile * TM, m = m0 + j;
@@ -239,38 +321,17 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
         const int F0 = sb - 2, NI = se - sb + 4;
         const int gi0 = gi, ga0 = ga, gb0 = gb;
         auto issue_tap = [&](int i) {  // the six stress tiles of slab F0 + i
-            const int sl = (gi0 + i) & 3, s = wrap(F0 + i);
-            uint64_t* b = &bar[sl];
-            __half* d = S + sl * SLOT * NX;
-            mbar_arrive_expect_tx(b, (uint32_t)SLOT * rb);
-            a3_rows(d + X::O_SXX * NX, in.sxx, slab, s, m0, m0 + TM + 1, nm, NX, b);
-            a3_rows(d + X::O_SXS * NX, in.sxs, slab, s, m0, m0 + TM + 1, nm, NX, b);
-            a3_rows(d + X::O_SSS * NX, in.sss, slab, s, m0, m0 + TM + 1, nm, NX, b);
-            a3_rows(d + X::O_SXM * NX, in.sxm, slab, s, m0 - 1, m0 + TM + 1, nm, NX, b);
-            a3_rows(d + X::O_SMS * NX, in.sms, slab, s, m0 - 1, m0 + TM + 1, nm, NX, b);
-            a3_rows(d + X::O_SMM * NX, in.smm, slab, s, m0 - 1, m0 + TM + 1, nm, NX, b);
+            const int sl = (gi0 + i) & 3;
+            x3_issue_tap<NX, TM>(S + sl * SLOT * NX, &bar[sl], in.sxx, in.sxs, in.sss, in.sxm, in.sms, in.smm, slab,
+                                 wrap(F0 + i), m0, nm);
         };
         auto issue_a = [&](int i) {  // old velocities (+ residuals) of slab F0 + i - 1
-            const int s = wrap(F0 + i - 1);
-            __half* d = S + X::A0;
-            mbar_arrive_expect_tx(abar, (uint32_t)((comp ? 6 : 3) * R1) * rb);
-            a3_rows(d, in.vx, slab, s, m0, m0 + TM + 1, nm, NX, abar);
-            a3_rows(d + R1 * NX, in.vs, slab, s, m0, m0 + TM + 1, nm, NX, abar);
-            a3_rows(d + 2 * R1 * NX, in.vm, slab, s, m0 - 1, m0 + TM, nm, NX, abar);
-            if (comp) {
-                a3_rows(d + 3 * R1 * NX, in.rvx, slab, s, m0, m0 + TM + 1, nm, NX, abar);
-                a3_rows(d + 4 * R1 * NX, in.rvs, slab, s, m0, m0 + TM + 1, nm, NX, abar);
-                a3_rows(d + 5 * R1 * NX, in.rvm, slab, s, m0 - 1, m0 + TM, nm, NX, abar);
-            }
+            x3_issue_a<NX, TM>(S + X::A0, abar, in.vx, in.vs, in.vm, in.rvx, in.rvs, in.rvm, comp ? 1 : 0, slab,
+                               wrap(F0 + i - 1), m0, nm);
         };
         auto issue_b = [&](int i) {  // stress residuals of slab F0 + i - 2 (own rows)
-            const int s = wrap(F0 + i - 2);
-            const int64_t off = (int64_t)s * slab + (int64_t)m0 * NX;
-            constexpr uint32_t tb = (uint32_t)TM * rb;
-            mbar_arrive_expect_tx(bbar, 6 * tb);
-            const __half* R[6] = {in.rsxx, in.rsss, in.rsmm, in.rsxs, in.rsxm, in.rsms};
-#pragma unroll
-            for (int q = 0; q < 6; q++) tma_load_1d(S + X::B0 + q * TM * NX, R[q] + off, tb, bbar);
+            x3_issue_b<NX, TM>(S + X::B0, bbar, in.rsxx, in.rsss, in.rsmm, in.rsxs, in.rsxm, in.rsms,
+                               (int64_t)wrap(F0 + i - 2) * slab + (int64_t)m0 * NX);
         };
         if (tid == 0) {
             issue_tap(0);
@@ -302,19 +363,11 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                 if (j < 3) rch = __ldg(in.coef + 8 * ((int64_t)k * cm + (cm > 1 ? mh : 0)) + hq);
             }
             mbar_wait(&bar[s0], (uint32_t)(((gi0 + i) >> 2) & 1));
-            mbar_wait(abar, (uint32_t)((ga0 + i) & 1));
+            if (!vel) mbar_wait(abar, (uint32_t)((ga0 + i) & 1));
             EV<PP> vs_new;
             if (vel) {  // ---- velocities of slab k = F-1 (elastic.py:191-205, 3D)
                 const __half* A = S + X::A0;
                 __half* VT = S + X::V0 + gen * 3 * R1 * NX;
-                // own rows: vx, vs at tile index j (row m), vm at index j + 1 of its tile
-                EV<PP> vx = ldv<PP>(A + to), vsv = ldv<PP>(A + R1 * NX + to), vm = ldv<PP>(A + (2 * R1 + 1) * NX + to);
-                EV<PP> rvx, rvs, rvm;
-                if (comp) {
-                    rvx = ldv<PP>(A + 3 * R1 * NX + to);
-                    rvs = ldv<PP>(A + 4 * R1 * NX + to);
-                    rvm = ldv<PP>(A + (5 * R1 + 1) * NX + to);
-                }
                 // vx: fl(fl(ddx sxx + dds sxs) + ddm sxm)
                 const EV<PP> ax =
                     addv<PP>(addv<PP>(xfv<PP>(c, T1 + X::O_SXX * NX, to, tl, tr, false),
@@ -331,11 +384,23 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                              fv<PP>(c, ldv<PP>(T2 + (X::O_SMS + 1) * NX + to), ldv<PP>(T1 + (X::O_SMS + 1) * NX + to))),
                     fv<PP>(c, ldv<PP>(T1 + (X::O_SMM + 1) * NX + to), ldv<PP>(T1 + (X::O_SMM + 2) * NX + to)));
                 if (vsrc && k == P.src_s && m == P.src_m && src_col) add_srcv<PP>(as.q, sj, sln, srch);
+                // the old values are waited for only now: the A slot was refilled during the previous
+                // iteration's stress phase, the stencil sums above overlap the rest of its latency
+                mbar_wait(abar, (uint32_t)((ga0 + i) & 1));
+                const float rx = x3_rcp(cv.x), ry = x3_rcp(cv.y), rz = x3_rcp(cv.z);  // (DIV_FAST rows)
+                // own rows: vx, vs at tile index j (row m), vm at index j + 1 of its tile
+                EV<PP> vx = ldv<PP>(A + to), vsv = ldv<PP>(A + R1 * NX + to), vm = ldv<PP>(A + (2 * R1 + 1) * NX + to);
+                EV<PP> rvx, rvs, rvm;
+                if (comp) {
+                    rvx = ldv<PP>(A + 3 * R1 * NX + to);
+                    rvs = ldv<PP>(A + 4 * R1 * NX + to);
+                    rvm = ldv<PP>(A + (5 * R1 + 1) * NX + to);
+                }
 #pragma unroll
                 for (int h = 0; h < PP; h++) {
-                    x3_finish<V>(ax.q[h], cv.x, in.div_mode[0], dt, dt2, srch, vx.q[h], rvx.q[h]);
-                    x3_finish<V>(as.q[h], cv.y, in.div_mode[1], dt, dt2, srch, vsv.q[h], rvs.q[h]);
-                    x3_finish<V>(am.q[h], cv.z, in.div_mode[2], dt, dt2, srch, vm.q[h], rvm.q[h]);
+                    x3_finish<V>(ax.q[h], cv.x, rx, in.div_mode[0], dt2, srch, vx.q[h], rvx.q[h]);
+                    x3_finish<V>(as.q[h], cv.y, ry, in.div_mode[1], dt2, srch, vsv.q[h], rvs.q[h]);
+                    x3_finish<V>(am.q[h], cv.z, rz, in.div_mode[2], dt2, srch, vm.q[h], rvm.q[h]);
                 }
                 stv<PP>(VT + to, vx);
                 stv<PP>(VT + R1 * NX + to, vsv);
@@ -368,7 +433,7 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                                           fv<PP>(c, ldv<PP>(T2 + X::O_SMS * NX + a0), ldv<PP>(T1 + X::O_SMS * NX + a0))),
                                  fv<PP>(c, ldv<PP>(T1 + X::O_SMM * NX + a0), ldv<PP>(T1 + (X::O_SMM + 1) * NX + a0)));
 #pragma unroll
-                    for (int q = 0; q < PP; q++) x3_finish<V>(a.q[q], rch, in.div_mode[2], dt, dt2, srch, h.q[q], rh.q[q]);
+                    for (int q = 0; q < PP; q++) x3_finish<V>(a.q[q], rch, x3_rcp(rch), in.div_mode[2], dt2, srch, h.q[q], rh.q[q]);
                     stv<PP>(VT + 2 * R1 * NX + a0, h);
                 } else if (j == 1 || j == 2) {
                     const int a0 = TM * NX + x;  // row TM of the tiles
@@ -390,7 +455,7 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
 #pragma unroll
                     const int hm = in.div_mode[j == 1 ? 0 : 1];
 #pragma unroll
-                    for (int q = 0; q < PP; q++) x3_finish<V>(a.q[q], rch, hm, dt, dt2, srch, h.q[q], rh.q[q]);
+                    for (int q = 0; q < PP; q++) x3_finish<V>(a.q[q], rch, x3_rcp(rch), hm, dt2, srch, h.q[q], rh.q[q]);
                     stv<PP>(VT + fo + a0, h);
                 }
             }
@@ -401,7 +466,6 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
             }
             const int s = F - 2;  // stress slab (unwrapped; in [0, ns) when computed)
             if (s >= sb && s < se) {  // ---- stresses of slab s (elastic.py:210-238, 3D)
-                mbar_wait(bbar, (uint32_t)((gb0 + (i - 4)) & 1));
                 const int pg = gen ^ 1;  // generation of slab s
                 const __half* vxt = S + X::V0 + pg * 3 * R1 * NX;  // rows m0 .. m0+TM
                 const __half* vst = vxt + R1 * NX;                 // rows m0 .. m0+TM
@@ -419,10 +483,7 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                 old[4] = ldv<PP>(T2 + (X::O_SXM + 1) * NX + to);
                 old[5] = ldv<PP>(T2 + (X::O_SMS + 1) * NX + to);
 #pragma unroll
-                for (int q = 0; q < 6; q++) {
-                    nw[q] = old[q];
-                    if (comp) rr[q] = ldv<PP>(S + X::B0 + q * TM * NX + to);
-                }
+                for (int q = 0; q < 6; q++) nw[q] = old[q];
                 const EH2 stiff = vsplat<16, 2>(__float2half_rn(cs.x)), lam = vsplat<16, 2>(__float2half_rn(cs.y));
                 const EH2 mu = vsplat<16, 2>(__float2half_rn(cs.z));  // (binary16 values: exact round trips)
                 EH2 a0[PP], a1[PP], a2[PP];
@@ -444,6 +505,12 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                 const EV<PP> sxm_b = xfv<PP>(c, vmt + NX, to, tl, tr, false);
                 const EV<PP> sms_a = fv<PP>(c, ldv<PP>(vmt + NX + to), ldv<PP>(vmn + NX + to));        // vm(s), vm(s+1)
                 const EV<PP> sms_b = fv<PP>(c, ldv<PP>(vst + to), ldv<PP>(vst + NX + to));             // vs rows m, m+1
+                // stress residuals (B slot, refilled during this iteration's velocity phase): waited for last
+                mbar_wait(bbar, (uint32_t)((gb0 + (i - 4)) & 1));
+                if (comp) {
+#pragma unroll
+                    for (int q = 0; q < 6; q++) rr[q] = ldv<PP>(S + X::B0 + q * TM * NX + to);
+                }
 #pragma unroll
                 for (int h = 0; h < PP; h++) {
                     e2_finish_nd<V>(a0[h], dt2, -1, srch, nw[0].q[h], rr[0].q[h]);
@@ -574,7 +641,7 @@ __global__ void k_el3_coef(PlaneView rx, PlaneView rs, PlaneView rm, PlaneView s
 // ---------------------------------------------------------------- host side
 
 #ifndef HW_X3C
-#define HW_X3C 8
+#define HW_X3C 4
 #endif
 constexpr int X3C = HW_X3C;  // cells per thread (4 or 8)
 

@@ -129,7 +129,7 @@ struct El3In {
     const float* coef;   // [ns][coef_m][8]: rcp(rho_x, rho_s, rho_m), 0, stiff, lam, mu_n, 0
     int64_t coef_m;      // coefficient rows per slab: 1 (planes constant along mid) or nm
     int32_t div_mode[3]; // DivMode of rho_x, rho_s, rho_m
-    int32_t pad;
+    int32_t group;       // CTAs per group of adjacent mid tiles streamed side by side (divides the grid)
 };
 bool el3d_fused_eligible(const ElParams& P, int64_t nx, int64_t nm, int64_t ns, int64_t pitch, int order,
                          int max_smem);

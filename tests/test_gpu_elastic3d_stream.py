@@ -12,6 +12,11 @@ from golden_cases import assert_same_bits
 
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(autouse=True)
+def _two_phase(hwopt):  # 2nd-order layered grids would otherwise take the one-pass kernel
+    hwopt(fused_el3=0)
+
 LAYERS = [(0.3, 1.0, 2.0, 1.0), (0.7, 1.4, 2.6, 1.3), (1.0, 1.8, 3.0, 0.0)]
 
 

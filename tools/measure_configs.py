@@ -16,9 +16,14 @@ import paper_2310_00236_b200 as hw  # noqa: E402
 CPU = "--cpu" in sys.argv
 # --opt name=value: library kernel-path options (hw_set_option), e.g. --opt fused_el3=0
 ARGS = []
+if "--lib" in sys.argv:  # an A/B build of the library (tools/build_variant.sh); before any library call
+    hw._abi.set_library_path(sys.argv[sys.argv.index("--lib") + 1])
 _it = iter(sys.argv[1:])
 for a in _it:
     if a == "--cpu":
+        continue
+    if a == "--lib":
+        next(_it)
         continue
     if a == "--opt":
         k, v = next(_it).split("=")
