@@ -404,6 +404,7 @@ struct hw_solver {
     float* el3_coef = nullptr;  // its medium coefficient table ([ns][el3_cm][8], in plane_mem)
     int64_t el3_cm = 0;
     int el3_group = 1;          // its CTA groups of adjacent tiles (hw_elastic3d_fused.cu)
+    double* el3_ecoef = nullptr;  // its per-slab energy coefficients (slow-layered media; in plane_mem)
     bool el3_stream = false;  // streaming 3D elastic phases
     int stream_blocks = 0;
     unsigned int* counter = nullptr;  // CTA arrival counter of the streaming stress kernel
@@ -827,6 +828,11 @@ int setup_handle(hw_solver* h) {
             CU(cudaMalloc(&h->el3_coef, (size_t)max_rows * h->el3_cm * 8 * sizeof(float)));
             h->plane_mem.push_back(h->el3_coef);
             CU(el3d_fused_coef(EP, h->el3_coef, max_rows, h->el3_cm, 0));
+            if (el3d_fused_erow(EP)) {
+                CU(cudaMalloc(&h->el3_ecoef, (size_t)max_rows * 8 * sizeof(double)));
+                h->plane_mem.push_back(h->el3_ecoef);
+                CU(el3d_fused_ecoef(EP, h->el3_ecoef, max_rows, 0));
+            }
             const int64_t units = (desc->nm / (2048 / desc->nx)) * max_rows;
             int64_t nbs = units / 4;
             if (nbs < 1) nbs = 1;
@@ -1406,6 +1412,7 @@ static void fused_el3_bufs(const hw_solver* h, int cur, ElParams& P, El3In& in) 
     in.div_mode[1] = h->lp[HW_PL_RHO_S].div_mode;
     in.div_mode[2] = h->lp[HW_PL_RHO_M].div_mode;
     in.group = h->el3_group;
+    in.ecoef = h->el3_ecoef;
 }
 
 static void fused_bufs(const hw_solver* h, __half* bufs[2][FUSED_NSTREAM]) {

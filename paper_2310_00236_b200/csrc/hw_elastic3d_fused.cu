@@ -170,6 +170,13 @@ __device__ __forceinline__ void gst(const FieldView& f, int64_t so, bool edge, i
     }
 }
 
+// binary16 -> binary64, one conversion (exact)
+__device__ __forceinline__ double h2d(__half h) {
+    double r;
+    asm("cvt.f64.f16 %0, %1;" : "=d"(r) : "h"(__half_as_ushort(h)));
+    return r;
+}
+
 // velocity increment + advance for one pair, divided by the row-uniform density b:
 //   DIV_CHEAP: fl16(fl32(a * rcp_rn(b))) with the table-verified reciprocal cf (inline);
 //   DIV_FAST : the branch-free exact division of lane<16>::div (hw_lanes.cuh) with b = cf and its
@@ -288,8 +295,7 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
     const bool ssrc = P.src_kind == HW_SRC_EXPLOSIVE && src != 0.0;  // CTA-uniform
     const bool src_col = (vsrc || ssrc) && P.src_x >= x && P.src_x < x + CPT;
     const int sj = (int)((P.src_x - x) >> 1), sln = (int)((P.src_x - x) & 1);
-    const bool erow = ((P.e_rho_x.sx | P.e_rho_s.sx | P.e_rho_m.sx | P.e_lam.sx | P.e_mu.sx | P.e_mu_n.sx) |
-                       (P.e_rho_x.sm | P.e_rho_s.sm | P.e_rho_m.sm | P.e_lam.sm | P.e_mu.sm | P.e_mu_n.sm)) == 0;
+    const bool erow = in.ecoef != nullptr;  // energy planes constant within a slab (per-slab table)
     const FieldView* OS[6] = {&P.sxx, &P.sss, &P.smm, &P.sxs, &P.sxm, &P.sms};
     const FieldView* ORS[6] = {&P.rsxx, &P.rsss, &P.rsmm, &P.rsxs, &P.rsxm, &P.rsms};
     __half2 acc[9];
@@ -531,29 +537,29 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                 if (sample) {  // diagnostics.py:100-162, 3D compliance form (k_el_stress)
                     const EV<PP> vxo = ldv<PP>(vxt + to), vmo = ldv<PP>(vmt + NX + to), vso = ldv<PP>(vst + to);
                     auto f = [&](const EV<PP>& a, int q) { return (double)__half2float(a.q[q >> 1].e[q & 1]); };
-                    if (erow) {
+                    if (erow) {  // per-slab medium: raw sums per iteration, one coefficient row per slab
                         double skx = 0.0, skm = 0.0, sks = 0.0, sx1 = 0.0, sdot = 0.0, str = 0.0, ssh = 0.0;
 #pragma unroll
                         for (int q = 0; q < CPT; q++) {
-                            const double a = f(vxo, q), b = f(vmo, q), g = f(vso, q);
+                            auto g = [&](const EV<PP>& a) { return h2d(a.q[q >> 1].e[q & 1]); };
+                            const double a = g(vxo), b = g(vmo), w = g(vso);
                             skx += a * a;
                             skm += b * b;
-                            sks += g * g;
-                            const double xn = f(old[0], q), x1 = f(nw[0], q), sn = f(old[1], q), s1 = f(nw[1], q);
-                            const double mn = f(old[2], q), m1 = f(nw[2], q);
+                            sks += w * w;
+                            const double xn = g(old[0]), x1 = g(nw[0]), sn = g(old[1]), s1 = g(nw[1]);
+                            const double mn = g(old[2]), m1 = g(nw[2]);
                             sx1 += xn * x1;
                             sdot += xn * x1 + sn * s1 + mn * m1;
                             str += (xn + sn + mn) * (x1 + s1 + m1);
-                            ssh += f(old[3], q) * f(nw[3], q) + f(old[4], q) * f(nw[4], q) + f(old[5], q) * f(nw[5], q);
+                            ssh += g(old[3]) * g(nw[3]) + g(old[4]) * g(nw[4]) + g(old[5]) * g(nw[5]);
                         }
-                        e[0] += p64(P.e_rho_x, s, 0, 0) * skx;
-                        e[2] += p64(P.e_rho_m, s, 0, 0) * skm;
-                        e[1] += p64(P.e_rho_s, s, 0, 0) * sks;
-                        const double lamd = p64(P.e_lam, s, 0, 0), mud = p64(P.e_mu, s, 0, 0);
-                        if (mud == 0.0) e[3] += sx1 / (lamd + mud);
-                        else e[3] += sdot / (2.0 * mud) - lamd * str / (2.0 * mud * (3.0 * lamd + 2.0 * mud));
-                        const double mun = p64(P.e_mu_n, s, 0, 0);
-                        e[4] += mun > 0.0 ? ssh / mun : 0.0;
+                        // rho_x, rho_s, rho_m, 1/(lam+mu) [mu = 0], 1/(2 mu), lam/(2 mu (3 lam + 2 mu)), 1/mu_n
+                        const double* ec = in.ecoef + 8 * (int64_t)s;
+                        e[0] += __ldg(ec + 0) * skx;
+                        e[1] += __ldg(ec + 1) * sks;
+                        e[2] += __ldg(ec + 2) * skm;
+                        e[3] += (__ldg(ec + 3) * sx1 + __ldg(ec + 4) * sdot) - __ldg(ec + 5) * str;
+                        e[4] += __ldg(ec + 6) * ssh;
                     } else {
 #pragma unroll
                         for (int q = 0; q < CPT; q++) {
@@ -638,6 +644,26 @@ __global__ void k_el3_coef(PlaneView rx, PlaneView rs, PlaneView rm, PlaneView s
     o[7] = 0.f;
 }
 
+// Energy coefficients of slow-layered media (every fp64 energy plane constant within a slab), per
+// slab: rho_x, rho_s, rho_m, then the compliance factors of diagnostics.py:100-162 (3D form)
+// 1/(lam+mu) when mu = 0 (else 0), 1/(2 mu) and lam/(2 mu (3 lam + 2 mu)) when mu > 0 (else 0),
+// 1/mu_n when mu_n > 0 (else 0): the sample steps multiply instead of dividing per iteration.
+__global__ void k_el3_ecoef(Plane64 rx, Plane64 rs, Plane64 rm, Plane64 la, Plane64 mu, Plane64 mn, double* out,
+                            int64_t ns) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= ns) return;
+    double* o = out + 8 * s;
+    o[0] = p64(rx, s, 0, 0);
+    o[1] = p64(rs, s, 0, 0);
+    o[2] = p64(rm, s, 0, 0);
+    const double l = p64(la, s, 0, 0), m = p64(mu, s, 0, 0), n = p64(mn, s, 0, 0);
+    o[3] = m == 0.0 ? 1.0 / (l + m) : 0.0;
+    o[4] = m == 0.0 ? 0.0 : 1.0 / (2.0 * m);
+    o[5] = m == 0.0 ? 0.0 : l / (2.0 * m * (3.0 * l + 2.0 * m));
+    o[6] = n > 0.0 ? 1.0 / n : 0.0;
+    o[7] = 0.0;
+}
+
 // ---------------------------------------------------------------- host side
 
 #ifndef HW_X3C
@@ -661,6 +687,17 @@ bool el3d_fused_eligible(const ElParams& P, int64_t nx, int64_t nm, int64_t ns, 
 
 int64_t el3d_fused_coef_rows(const ElParams& P) {
     return (P.rho_x.sm | P.rho_s.sm | P.rho_m.sm | P.stiff.sm | P.lam.sm | P.mu_n.sm) == 0 ? 1 : P.g.nm;
+}
+
+bool el3d_fused_erow(const ElParams& P) {
+    return ((P.e_rho_x.sx | P.e_rho_s.sx | P.e_rho_m.sx | P.e_lam.sx | P.e_mu.sx | P.e_mu_n.sx) |
+            (P.e_rho_x.sm | P.e_rho_s.sm | P.e_rho_m.sm | P.e_lam.sm | P.e_mu.sm | P.e_mu_n.sm)) == 0;
+}
+
+cudaError_t el3d_fused_ecoef(const ElParams& P, double* out, int64_t ns, cudaStream_t st) {
+    k_el3_ecoef<<<(unsigned)((ns + 127) / 128), 128, 0, st>>>(P.e_rho_x, P.e_rho_s, P.e_rho_m, P.e_lam, P.e_mu,
+                                                             P.e_mu_n, out, ns);
+    return cudaGetLastError();
 }
 
 cudaError_t el3d_fused_coef(const ElParams& P, float* out, int64_t ns, int64_t cm, cudaStream_t st) {

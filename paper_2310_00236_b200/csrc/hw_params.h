@@ -130,10 +130,13 @@ struct El3In {
     int64_t coef_m;      // coefficient rows per slab: 1 (planes constant along mid) or nm
     int32_t div_mode[3]; // DivMode of rho_x, rho_s, rho_m
     int32_t group;       // CTAs per group of adjacent mid tiles streamed side by side (divides the grid)
+    const double* ecoef; // [ns][8] energy coefficients of slow-layered media (k_el3_ecoef), or null
 };
 bool el3d_fused_eligible(const ElParams& P, int64_t nx, int64_t nm, int64_t ns, int64_t pitch, int order,
                          int max_smem);
 int64_t el3d_fused_coef_rows(const ElParams& P);
+bool el3d_fused_erow(const ElParams& P);
+cudaError_t el3d_fused_ecoef(const ElParams& P, double* out, int64_t ns, cudaStream_t st);
 cudaError_t el3d_fused_coef(const ElParams& P, float* out, int64_t ns, int64_t cm, cudaStream_t st);
 cudaError_t el3d_fused_prepare(int64_t nx);
 void launch_el3d_fused(int variant, const ElParams& P, const El3In& in, const StreamIO& IO, int nblocks, int64_t n,
