@@ -129,6 +129,24 @@ int hw_destroy(hw_solver* h);
  * Slab r owns global slow rows [r*ns/N, (r+1)*ns/N) (+ the extra free-surface row
  * on the last slab); hw_set_state / hw_get_state take the global host arrays. */
 int hw_nccl_unique_id(void* out128);
+
+/* The halo plan both transports execute (host only, no CUDA): for slab `rank` of `world`,
+ * the point-to-point transfers of one exchange in issue order.  row0 / nrows are local slow
+ * rows of external field `field` (row0 < 0: top ghost rows, row0 >= local rows: bottom ghost
+ * rows); peer is the rank sent to (send = 1) or received from (send = 0).  The k-th receive
+ * of rank b from rank a pairs with the k-th send of a to b.  Kinds: */
+enum hw_plan_kind {
+    HW_PLAN_VEL = 0,    /* after the velocity phase: velocities with slow-axis derivatives */
+    HW_PLAN_STRESS = 1, /* after the pressure / stress phase: the other ghosted fields */
+    HW_PLAN_FUSED = 2   /* once per step of the fused 2D acoustic kernel: p, vy, rvy (3 rows) */
+};
+typedef struct hw_xfer {
+    int32_t field, peer, send, pad;
+    int64_t row0, nrows;
+} hw_xfer;
+/* *n receives the number of transfers; at most cap are written to out (out may be NULL). */
+int hw_exchange_plan(const hw_desc* desc, int32_t world, int32_t rank, int32_t kind, hw_xfer* out, int32_t cap,
+                     int32_t* n);
 int hw_create_group(const hw_desc* desc, int32_t nslabs, const int32_t* devices, hw_solver** out);
 int hw_run_group(hw_solver* const* handles, int32_t nslabs, int32_t variant, int64_t step0, int64_t nt,
                  const double* src_samples, double* traces, double* e_times, double* e_vals,

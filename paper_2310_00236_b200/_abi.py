@@ -44,8 +44,18 @@ EXPORTED = (
     "hw_get_state", "hw_run", "hw_run_device", "hw_last_launch_count", "hw_kernel_path", "hw_transport",
     "hw_last_kernel_ms", "hw_last_error", "hw_version", "hw_selftest_div16",
     "hw_cheap_div_table", "hw_plane_div_mode", "hw_nccl_unique_id", "hw_create_group", "hw_run_group",
-    "hw_set_option", "hw_get_option",
+    "hw_set_option", "hw_get_option", "hw_exchange_plan",
 )
+
+# hw_plan_kind
+PLAN_VEL, PLAN_STRESS, PLAN_FUSED = 0, 1, 2
+
+
+class Xfer(ctypes.Structure):
+    """Mirror of ``hw_xfer``."""
+
+    _fields_ = [("field", ctypes.c_int32), ("peer", ctypes.c_int32), ("send", ctypes.c_int32), ("pad", ctypes.c_int32),
+                ("row0", ctypes.c_int64), ("nrows", ctypes.c_int64)]
 
 
 class Desc(ctypes.Structure):
@@ -130,6 +140,8 @@ def load() -> ctypes.CDLL:
         lib.hw_create_group.restype = ctypes.c_int
         lib.hw_run_group.argtypes = [P(vp), i32, i32, i64, i64, P(dbl), P(dbl), P(dbl), P(dbl), P(i64), P(i64), P(i32)]
         lib.hw_run_group.restype = ctypes.c_int
+    lib.hw_exchange_plan.argtypes = [P(Desc), i32, i32, i32, P(Xfer), i32, P(i32)]
+    lib.hw_exchange_plan.restype = ctypes.c_int
     lib.hw_set_option.argtypes = [ctypes.c_char_p, i64]
     lib.hw_set_option.restype = ctypes.c_int
     lib.hw_get_option.argtypes = [ctypes.c_char_p, P(i64)]
@@ -180,3 +192,14 @@ class options:
         for k, v in self.saved.items():
             set_option(k, v)
         return False
+
+
+def exchange_plan(desc, world: int, rank: int, kind: int) -> list:
+    """The library's halo plan for one slab (hw_exchange_plan): a list of dicts
+    (field, peer, send, row0, nrows) in issue order.  No CUDA device needed."""
+    lib = load()
+    n = ctypes.c_int32(0)
+    check(lib.hw_exchange_plan(ctypes.byref(desc), world, rank, kind, None, 0, ctypes.byref(n)), "hw_exchange_plan")
+    buf = (Xfer * max(n.value, 1))()
+    check(lib.hw_exchange_plan(ctypes.byref(desc), world, rank, kind, buf, n.value, ctypes.byref(n)), "hw_exchange_plan")
+    return [dict(field=x.field, peer=x.peer, send=bool(x.send), row0=x.row0, nrows=x.nrows) for x in buf[:n.value]]

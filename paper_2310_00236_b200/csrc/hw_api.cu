@@ -438,8 +438,6 @@ bool needs_ghosts(const hw_solver* h, int f) {
 }
 bool is_velocity(int f) { return f == F_VX || f == F_VS || f == F_VM; }
 
-int prev_rank(const hw_solver* h) { return h->rank > 0 ? h->rank - 1 : (h->fs ? -1 : h->world - 1); }
-int next_rank(const hw_solver* h) { return h->rank < h->world - 1 ? h->rank + 1 : (h->fs ? -1 : 0); }
 
 int plane_lane(const hw_solver* h, int pl) {
     switch (pl) {
@@ -475,10 +473,12 @@ int upload_plane(hw_solver* h, int pl) {
     int64_t per = nm * nx;
     if (!h->d.plane[pl]) return fail(HW_EINVAL, "medium plane " + std::to_string(pl) + " missing");
     const double* src = h->d.plane[pl] + (pl == HW_PL_EP ? 0 : h->r0 * per);
-    // Slab mode: G halo rows each side (global rows wrapped, or clamped at a free
-    // surface), views pointing at local row 0, so kernels that recompute halo rows
-    // (the fused 2D kernel's vy) find their coefficients.
-    const int64_t pad = ((h->world > 1 || h->transport == 2) && pl != HW_PL_EP) ? G : 0;
+    // Slab mode: 2G halo rows each side (global rows wrapped, or clamped at a free
+    // surface), views pointing at local row 0, so kernels that recompute halo rows (the
+    // fused 2D kernel's vy, rows -2 .. L) find their coefficients, and its row-uniform
+    // coefficient prefetch (front rows -6 .. L+3 of the first / last band) stays inside
+    // the allocation.
+    const int64_t pad = ((h->world > 1 || h->transport == 2) && pl != HW_PL_EP) ? 2 * G : 0;
     std::vector<double> ext;
     if (pad) {
         static const int PLANE_FIELD[HW_NPLANES] = {F_VX, F_VS, F_VM, F_P, F_SXX, F_SXX, F_SXX, F_SXS, F_SXX};
@@ -939,99 +939,138 @@ void release_handle(hw_solver* h) {
 }
 
 // ---------------------------------------------------------------- halo exchange
-// Phase 0 (after the velocity kernels) ships the velocity fields with slow-axis
-// derivatives, phase 1 (after the pressure / stress kernels) the rest.  Each field
-// sends its G boundary slabs: bottom rows -> next rank's top ghosts, top rows ->
-// previous rank's bottom ghosts (free surfaces: the global ends keep their images).
-struct Xfer {
-    void* src_bottom;  // rows [n-G, n)
-    void* src_top;     // rows [0, G)
-    void* dst_top;     // ghost rows [-G, 0)
-    void* dst_bottom;  // ghost rows [n, n+G)
-    size_t bytes;
+// The halo plan is computed on the host from the slab geometry alone (no CUDA; exported as
+// hw_exchange_plan) and executed by both transports.  Kinds:
+//   HW_PLAN_VEL    after the velocity kernels: the velocities with slow-axis derivatives;
+//   HW_PLAN_STRESS after the pressure / stress kernels: the rest of the ghosted fields;
+//   HW_PLAN_FUSED  once per step of the fused 2D acoustic kernel on slabs: p (its redundant vy
+//                  halo rows read p rows -3 .. L+2), vy and rvy (old values of those rows), G rows.
+// Per field the phase kinds move the slow-axis stencil reach (1 row at 2nd order, 2 at 4th):
+// bottom rows -> next rank's top ghosts and top rows -> previous rank's bottom ghosts, in a
+// canonical order (every field's bottom-going pair, then every field's top-going pair) so that
+// paired send/recv match even when previous == next (N = 2, periodic) or both are the rank
+// itself (one-rank NCCL self exchange).  Free surfaces: the global ends keep their images.
+struct PlanGeom {
+    int ac, d3, fs, order, world, rank, nsol;
+    int64_t ns_loc;
+    const int* ext;
 };
 
-// Ghost rows the phase kernels read across a slab edge: the slow-axis stencil reach
-// (1 row at 2nd order, 2 at 4th), not the full G-deep ghost slabs.
-std::vector<Xfer> xfers(const hw_solver* h, int phase) {
-    std::vector<Xfer> out;
-    const size_t esz = lane_bytes(h->LU);
-    const int64_t depth = h->d.order == 2 ? 1 : 2;
-    for (int j = 0; j < h->nsol; j++) {
-        const int f = h->ext[j];
-        if (!needs_ghosts(h, f) || is_velocity(f) != (phase == 0)) continue;
-        const FieldView& fv = h->fv[f];
-        const size_t row = (size_t)h->g.slab * esz;
-        char* b = (char*)fv.base;
-        out.push_back(Xfer{b + (fv.rows - depth) * row, b, b - depth * row, b + fv.rows * row, depth * row});
+PlanGeom plan_geom(const hw_solver* h) {
+    return PlanGeom{h->ac ? 1 : 0, h->d3 ? 1 : 0, h->fs ? 1 : 0, h->d.order, h->world, h->rank, h->nsol, h->ns_loc,
+                    h->ext};
+}
+
+int64_t pg_rows(const PlanGeom& g, int f) {
+    return g.ns_loc + ((g.fs && !HALF_S[f] && g.rank == g.world - 1) ? 1 : 0);
+}
+bool pg_ghosts(const PlanGeom& g, int f) {
+    if (g.ac) return f == F_P || f == F_VS;
+    return f == F_VX || f == F_VS || f == F_VM || f == F_SXS || f == F_SSS || f == F_SMS;
+}
+int pg_prev(const PlanGeom& g) { return g.rank > 0 ? g.rank - 1 : (g.fs ? -1 : g.world - 1); }
+int pg_next(const PlanGeom& g) { return g.rank < g.world - 1 ? g.rank + 1 : (g.fs ? -1 : 0); }
+
+std::vector<hw_xfer> halo_plan(const PlanGeom& g, int kind) {
+    std::vector<int> js;   // external field indices, in external order
+    int64_t depth = 0;
+    if (kind == HW_PLAN_FUSED) {
+        js = {0, 2, 5};  // p, vy, rvy of p vx vy rp rvx rvy
+        depth = G;
+    } else {
+        for (int j = 0; j < g.nsol; j++) {
+            const int f = g.ext[j];
+            if (pg_ghosts(g, f) && is_velocity(f) == (kind == HW_PLAN_VEL)) js.push_back(j);
+        }
+        depth = g.order == 2 ? 1 : 2;
+    }
+    const int pv = pg_prev(g), nx_ = pg_next(g);
+    std::vector<hw_xfer> out;
+    for (int j : js) {
+        const int64_t n = pg_rows(g, g.ext[j % g.nsol]);
+        if (nx_ >= 0) out.push_back(hw_xfer{j, nx_, 1, 0, n - depth, depth});
+        if (pv >= 0) out.push_back(hw_xfer{j, pv, 0, 0, -depth, depth});
+    }
+    for (int j : js) {
+        const int64_t n = pg_rows(g, g.ext[j % g.nsol]);
+        if (pv >= 0) out.push_back(hw_xfer{j, pv, 1, 0, 0, depth});
+        if (nx_ >= 0) out.push_back(hw_xfer{j, nx_, 0, 0, n, depth});
     }
     return out;
 }
 
-// Ghost plan of the fused 2D kernel's buffer `buf` (0 = A, 1 = B): p (3 rows each way:
-// its redundant vy halo reads p rows -3 .. L+2), vy and rvy (the old values of those vy
-// halo rows); one exchange per step.
-std::vector<Xfer> xfers_fused(const hw_solver* h, int buf) {
-    std::vector<Xfer> out;
-    const size_t row = (size_t)h->g.slab * 2;
-    for (int j : {0, 2, 5}) {  // p, vy, rvy in the external order p vx vy rp rvx rvy
-        char* b = (char*)(buf ? h->mem_b[j] : h->mem[j]) + G * row;
-        const int64_t n = h->ns_loc;
-        out.push_back(Xfer{b + (n - G) * row, b, b - G * row, b + n * row, G * row});
-    }
-    return out;
+// Device address of local row `row` of external field j for a plan kind (buf: fused 2D
+// ping-pong buffer, 0 = A, 1 = B).
+char* plan_row(const hw_solver* h, int kind, int buf, int j, int64_t row) {
+    const size_t rb = (size_t)h->g.slab * lane_bytes(h->LU);
+    char* base;
+    if (kind == HW_PLAN_FUSED) base = (char*)(buf ? h->mem_b[j] : h->mem[j]) + G * rb;
+    else base = (char*)(j < h->nsol ? h->fv : h->rv)[h->ext[j % h->nsol]].base;
+    return base + row * (int64_t)rb;
 }
 
-int exchange_nccl_list(hw_solver* h, const std::vector<Xfer>& xs) {
-    const int pv = prev_rank(h), nx_ = next_rank(h);
+int exchange_nccl_plan(hw_solver* h, int kind, int buf) {
+    const size_t rb = (size_t)h->g.slab * lane_bytes(h->LU);
     NC(g_nccl.GroupStart());
-    for (const Xfer& x : xs) {  // canonical order: bottom->next / top ghost<-prev, then the reverse
-        if (nx_ >= 0) NC(g_nccl.Send(x.src_bottom, x.bytes, ncclInt8, nx_, h->nccl, h->st));
-        if (pv >= 0) NC(g_nccl.Recv(x.dst_top, x.bytes, ncclInt8, pv, h->nccl, h->st));
-    }
-    for (const Xfer& x : xs) {
-        if (pv >= 0) NC(g_nccl.Send(x.src_top, x.bytes, ncclInt8, pv, h->nccl, h->st));
-        if (nx_ >= 0) NC(g_nccl.Recv(x.dst_bottom, x.bytes, ncclInt8, nx_, h->nccl, h->st));
+    for (const hw_xfer& x : halo_plan(plan_geom(h), kind)) {
+        void* p = plan_row(h, kind, buf, x.field, x.row0);
+        if (x.send) NC(g_nccl.Send(p, x.nrows * rb, ncclInt8, x.peer, h->nccl, h->st));
+        else NC(g_nccl.Recv(p, x.nrows * rb, ncclInt8, x.peer, h->nccl, h->st));
     }
     NC(g_nccl.GroupEnd());
+    if (kind != HW_PLAN_VEL) {
+        // every rank learns the first failing step of every rank before its next step's kernels
+        // (they exit at entry past it): the state of every rank stops exactly after the global
+        // first failing step (acoustic.py:208-229); the overlapped fused 2D path may run one
+        // interior band further into the other ping-pong buffer, which the copy-back discards
+        NC(g_nccl.AllReduce(&h->ctrl->fail_step, &h->ctrl->gfail_step, 1, ncclInt64, ncclMin, h->nccl, h->st));
+    }
     return HW_OK;
 }
 
-int exchange_nccl(hw_solver* h, int phase) { return exchange_nccl_list(h, xfers(h, phase)); }
+int exchange_nccl(hw_solver* h, int phase) { return exchange_nccl_plan(h, phase == 0 ? HW_PLAN_VEL : HW_PLAN_STRESS, 0); }
 
-// In-process slab group: every rank pulls its ghosts from its neighbours' slabs with
-// peer copies ordered by events (works on one GPU or across NVLink peers).
-// plan(h) lists the transfers of rank h (the same fields in the same order on every rank).
-template <typename PLAN>
-int exchange_group_plan(hw_group* grp, PLAN plan) {
+// In-process slab group: every rank pulls its ghosts from its neighbours' slabs with peer
+// copies ordered by events (one GPU or NVLink peers).  The k-th receive of rank b from rank a
+// takes the k-th send of a to b, as NCCL pairs point-to-point operations.
+int exchange_group_plan(hw_group* grp, int kind, int buf) {
     for (hw_solver* h : grp->ranks) {
         CU(cudaSetDevice(h->d.device));
         CU(cudaEventRecord(h->ev_phase, h->st));
     }
+    const size_t rb = (size_t)grp->ranks[0]->g.slab * lane_bytes(grp->ranks[0]->LU);
     for (hw_solver* b : grp->ranks) {
         CU(cudaSetDevice(b->d.device));
-        const int pv = prev_rank(b), nx_ = next_rank(b);
-        std::vector<Xfer> mine = plan(b);
-        if (pv >= 0) {
-            hw_solver* a = grp->ranks[pv];
-            CU(cudaStreamWaitEvent(b->st, a->ev_phase, 0));
-            std::vector<Xfer> theirs = plan(a);
-            for (size_t k = 0; k < mine.size(); k++)
-                CU(cudaMemcpyPeerAsync(mine[k].dst_top, b->d.device, theirs[k].src_bottom, a->d.device, mine[k].bytes, b->st));
-        }
-        if (nx_ >= 0) {
-            hw_solver* a = grp->ranks[nx_];
-            CU(cudaStreamWaitEvent(b->st, a->ev_phase, 0));
-            std::vector<Xfer> theirs = plan(a);
-            for (size_t k = 0; k < mine.size(); k++)
-                CU(cudaMemcpyPeerAsync(mine[k].dst_bottom, b->d.device, theirs[k].src_top, a->d.device, mine[k].bytes, b->st));
+        const std::vector<hw_xfer> mine = halo_plan(plan_geom(b), kind);
+        std::vector<int> waited;
+        for (size_t k = 0; k < mine.size(); k++) {
+            const hw_xfer& r = mine[k];
+            if (r.send) continue;
+            hw_solver* a = grp->ranks[r.peer];
+            if (std::find(waited.begin(), waited.end(), r.peer) == waited.end()) {
+                CU(cudaStreamWaitEvent(b->st, a->ev_phase, 0));
+                waited.push_back(r.peer);
+            }
+            int nth = 0;  // r is the nth receive of b from a
+            for (size_t q = 0; q < k; q++) nth += (!mine[q].send && mine[q].peer == r.peer) ? 1 : 0;
+            const std::vector<hw_xfer> theirs = halo_plan(plan_geom(a), kind);
+            const hw_xfer* s = nullptr;
+            for (const hw_xfer& t : theirs)
+                if (t.send && t.peer == b->rank && nth-- == 0) {
+                    s = &t;
+                    break;
+                }
+            if (!s || s->nrows != r.nrows || s->field != r.field) return fail(HW_EINVAL, "inconsistent halo plan");
+            CU(cudaMemcpyPeerAsync(plan_row(b, kind, buf, r.field, r.row0), b->d.device,
+                                   plan_row(a, kind, buf, s->field, s->row0), a->d.device, r.nrows * rb, b->st));
         }
         CU(cudaEventRecord(b->ev_copied, b->st));
     }
     // a rank may overwrite its boundary rows only after its neighbours copied them
     for (hw_solver* a : grp->ranks) {
         CU(cudaSetDevice(a->d.device));
-        const int pv = prev_rank(a), nx_ = next_rank(a);
+        const PlanGeom g = plan_geom(a);
+        const int pv = pg_prev(g), nx_ = pg_next(g);
         if (pv >= 0) CU(cudaStreamWaitEvent(a->st, grp->ranks[pv]->ev_copied, 0));
         if (nx_ >= 0) CU(cudaStreamWaitEvent(a->st, grp->ranks[nx_]->ev_copied, 0));
     }
@@ -1039,7 +1078,7 @@ int exchange_group_plan(hw_group* grp, PLAN plan) {
 }
 
 int exchange_group(hw_group* grp, int phase) {
-    return exchange_group_plan(grp, [phase](const hw_solver* h) { return xfers(h, phase); });
+    return exchange_group_plan(grp, phase == 0 ? HW_PLAN_VEL : HW_PLAN_STRESS, 0);
 }
 
 int exchange(hw_solver* h, int phase) {
@@ -1226,6 +1265,7 @@ static int run_begin(hw_solver* h, int32_t variant, int64_t nt, bool energy, boo
         c0.fail_step = INT64_MAX;
         c0.fail_mask = 0;
         c0.pad = 0;
+        c0.gfail_step = INT64_MAX;
         CU(cudaMemcpyAsync(h->ctrl, &c0, sizeof(Ctrl), cudaMemcpyHostToDevice, h->st));
     }
     if (variant == HW_NAIVE && nt > 0) {  // untouched non-finite residuals fail step 0
@@ -1431,7 +1471,7 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
     if (rc) return rc;
     const bool fused_slab = h->fused && h->transport == 2;
     if (fused_slab) {  // halos of the uploaded state
-        if ((rc = exchange_nccl_list(h, xfers_fused(h, 0)))) return rc;
+        if ((rc = exchange_nccl_plan(h, HW_PLAN_FUSED, 0))) return rc;
     } else if ((rc = exchange(h, 0)) || (rc = exchange(h, 1))) {
         return rc;
     }
@@ -1495,7 +1535,7 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
             CU(cudaEventRecord(h->ev_int[n & 1], h->st2));
             h->launches += 2;
             cur ^= 1;
-            if ((rc = exchange_nccl_list(h, xfers_fused(h, cur)))) return rc;
+            if ((rc = exchange_nccl_plan(h, HW_PLAN_FUSED, cur))) return rc;
         }
         if (nt > 0) CU(cudaStreamWaitEvent(h->st, h->ev_int[(nt - 1) & 1], 0));
     } else if (h->fused3 || h->fused3_32) {  // one-pass 3D kernel, ping-pong A <-> B: step n reads buffer n % 2
@@ -1568,7 +1608,7 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
             }
             cur ^= 1;
             h->launches++;
-            if (fused_slab && (rc = exchange_nccl_list(h, xfers_fused(h, cur)))) return rc;
+            if (fused_slab && (rc = exchange_nccl_plan(h, HW_PLAN_FUSED, cur))) return rc;
         }
     } else {
         for (int64_t n = 0; n < nt; n++) {
@@ -1627,6 +1667,7 @@ static int tb2_replay(hw_solver* h, int32_t variant, int64_t nt, const double* s
     c0.fail_step = INT64_MAX;
     c0.fail_mask = 0;
     c0.pad = 0;
+    c0.gfail_step = INT64_MAX;
     CU(cudaMemcpyAsync(h->ctrl, &c0, sizeof(Ctrl), cudaMemcpyHostToDevice, h->st));
     for (int64_t j = 0; j < h->n_rec_sorted; j++)  // the pair's second step recorded samples at n+1
         CU(cudaMemsetAsync(h->traces + j * nt + n + 1, 0, (nt - n - 1) * sizeof(double), h->st));
@@ -1677,7 +1718,21 @@ int hw_run(hw_solver* h, int32_t variant, int64_t step0, int64_t nt, const doubl
     const int64_t nrec = h->d.n_receivers;
     const int64_t ne = energy ? 1 + (status == HW_OK ? nt / h->d.energy_every : (done - 1) / h->d.energy_every) : 0;
     if (h->transport == 2) {
-        if (ne > 0) NC(g_nccl.AllReduce(h->evals, h->evals, ne, ncclFloat64, ncclSum, h->nccl, h->st));
+        if (ne > 0) {  // per-rank energy totals gathered, then summed in rank order on every rank
+            double* all = nullptr;
+            CU(cudaMalloc(&all, sizeof(double) * ne * h->world));
+            NC(g_nccl.AllGather(h->evals, all, ne, ncclFloat64, h->nccl, h->st));
+            std::vector<double> hv((size_t)ne * h->world), tot(ne, 0.0);
+            CU(cudaMemcpyAsync(hv.data(), all, sizeof(double) * ne * h->world, cudaMemcpyDeviceToHost, h->st));
+            CU(cudaStreamSynchronize(h->st));
+            cudaFree(all);
+            for (int64_t k = 0; k < ne; k++) {
+                double t = hv[k];
+                for (int r = 1; r < h->world; r++) t += hv[(size_t)r * ne + k];
+                tot[k] = t;
+            }
+            CU(cudaMemcpy(h->evals, tot.data(), sizeof(double) * ne, cudaMemcpyHostToDevice));
+        }
         for (int64_t j = 0; j < nrec && nt > 0; j++) {  // receiver traces from their owning slab
             int owner = 0;
             for (int r = 0; r < h->world; r++) {
@@ -1723,8 +1778,7 @@ int hw_run_group(hw_solver* const* hs, int32_t nslabs, int32_t variant, int64_t 
             for (int k = 0; k < 2; k++)
                 for (int j = 0; j < FUSED_NSTREAM; j++) bufs[h->rank][k][j] = b[k][j];
         }
-        auto plan = [](int buf) { return [buf](const hw_solver* h) { return xfers_fused(h, buf); }; };
-        if ((rc = exchange_group_plan(grp, plan(0)))) return rc;  // halos of the uploaded state
+        if ((rc = exchange_group_plan(grp, HW_PLAN_FUSED, 0))) return rc;  // halos of the uploaded state
         int cur = 0;
         for (int64_t n = 0; n < nt; n++) {
             for (hw_solver* h : grp->ranks) {
@@ -1740,7 +1794,7 @@ int hw_run_group(hw_solver* const* hs, int32_t nslabs, int32_t variant, int64_t 
                 h->launches++;
             }
             cur ^= 1;
-            if ((rc = exchange_group_plan(grp, plan(cur)))) return rc;
+            if ((rc = exchange_group_plan(grp, HW_PLAN_FUSED, cur))) return rc;
         }
     } else {
     if (nslabs > 1) {
@@ -1872,6 +1926,27 @@ int hw_cheap_div_table(int32_t device, uint32_t* bits1024) {
 int hw_plane_div_mode(const hw_solver* h, int32_t plane) {
     if (!h || plane < 0 || plane >= HW_NPLANES) return -1;
     return h->lp[plane].div_mode;
+}
+
+int hw_exchange_plan(const hw_desc* desc, int32_t world, int32_t rank, int32_t kind, hw_xfer* out, int32_t cap,
+                     int32_t* n) {
+    if (!desc || !n || world < 1 || rank < 0 || rank >= world || kind < 0 || kind > 2)
+        return fail(HW_EINVAL, "hw_exchange_plan: bad arguments");
+    PlanGeom g;
+    g.ac = desc->equation == HW_EQ_ACOUSTIC;
+    g.d3 = desc->ndim == 3;
+    g.fs = desc->bc_slow == HW_BC_FREE_SURFACE;
+    g.order = desc->order;
+    g.world = world;
+    g.rank = rank;
+    g.ext = ext_order(desc->equation, desc->ndim, &g.nsol);
+    g.ns_loc = (int64_t)(rank + 1) * desc->ns / world - (int64_t)rank * desc->ns / world;
+    if (kind == HW_PLAN_FUSED && !(g.ac && !g.d3)) return fail(HW_EINVAL, "hw_exchange_plan: fused plan is 2D acoustic");
+    const std::vector<hw_xfer> p = halo_plan(g, kind);
+    *n = (int32_t)p.size();
+    if (out)
+        for (int32_t k = 0; k < *n && k < cap; k++) out[k] = p[k];
+    return HW_OK;
 }
 
 int hw_set_option(const char* name, int64_t value) {

@@ -83,6 +83,8 @@ struct Ctrl {         // device-side run control
     int64_t fail_step;      // first local step index with a non-finite write (INT64_MAX if none)
     unsigned int fail_mask; // external field bits recorded at that step
     unsigned int pad;
+    int64_t gfail_step;     // first failing step of ANY rank known so far (NCCL transport: min-allreduced
+                            // after every step; INT64_MAX otherwise)
 };
 
 template <typename T>
@@ -400,18 +402,24 @@ __device__ __forceinline__ double warp_sum(double a) {
     return a;
 }
 
-// Warp-aggregated failure record: first failing step + external field bits.
+// Warp-aggregated failure record: first failing step + external field bits (the bits of that
+// step only: a record from a later step -- possible only while another rank's failure is in
+// flight -- leaves the mask alone).
 __device__ __forceinline__ void record_failure(Ctrl* ctrl, int64_t n, unsigned int mask) {
     const int nl = warp_lanes();
     unsigned int any = __reduce_or_sync(nl == 32 ? 0xffffffffu : ((1u << nl) - 1u), mask);
     if (any && (threadIdx.x & 31) == 0) {
-        atomicMin(reinterpret_cast<unsigned long long*>(&ctrl->fail_step), (unsigned long long)n);
-        atomicOr(&ctrl->fail_mask, any);
+        const unsigned long long old =
+            atomicMin(reinterpret_cast<unsigned long long*>(&ctrl->fail_step), (unsigned long long)n);
+        if (old >= (unsigned long long)n) atomicOr(&ctrl->fail_mask, any);
     }
 }
 
+// A step kernel exits at entry once any step before it failed on this rank or on any rank.
 __device__ __forceinline__ bool halted(const Ctrl* ctrl, int64_t n) {
-    return *reinterpret_cast<const volatile int64_t*>(&ctrl->fail_step) < n;
+    const int64_t a = *reinterpret_cast<const volatile int64_t*>(&ctrl->fail_step);
+    const int64_t b = *reinterpret_cast<const volatile int64_t*>(&ctrl->gfail_step);
+    return (a < b ? a : b) < n;
 }
 
 // Block-wide fp64 sum of NCOMP components; thread 0 writes the block partial (row idx,

@@ -1,22 +1,24 @@
-"""Slab decomposition of the slow axis (SURVEY §8 e) — the host-side plan.
+"""Slab decomposition of the slow axis (SURVEY §8 e) on host arrays.
 
-Mirrors the arithmetic of csrc/hw_api.cu (`setup_handle`, `xfers`,
-`exchange_nccl`): rank r of N owns global slow rows [r*ns//N, (r+1)*ns//N) (the
-extra free-surface row of integer sub-grids goes to the last rank), keeps G = 2
-ghost slabs on each side, and after every phase sends its G boundary slabs to its
-neighbours in a canonical order (bottom rows -> next / top ghosts <- previous,
-then top rows -> previous / bottom ghosts <- next).  Periodic slow axes wrap rank
-N-1 <-> 0; free surfaces keep image ghosts at the global ends.
+The library computes its halo plan on the host from the slab geometry alone
+(`hw_exchange_plan`, include/halfwave_b200.h; csrc/hw_api.cu `halo_plan`) and both of its
+transports execute exactly that list: NCCL send/recv in issue order (one process per GPU)
+and peer copies inside a slab group (the k-th receive of rank b from rank a takes the k-th
+send of a to b).  `exchange_host` executes the same list over torch.distributed on host
+arrays, so a CPU job (gloo) can check the plan the device runs against the global array
+(tests/test_decomp_gloo.py).
 
-`exchange_halos` runs that plan over torch.distributed on host arrays; it is the
-CPU (gloo) model of the device exchange, used by tests/test_decomp_gloo.py.
+Rank r of N owns global slow rows [r*ns//N, (r+1)*ns//N) (the extra free-surface row of
+integer sub-grids goes to the last rank) and keeps G = 3 ghost slabs on each side.
 """
 
 from __future__ import annotations
 
 import numpy as np
 
-G = 2
+from . import _abi
+
+G = 3  # ghost slabs per side (csrc/hw_common.cuh)
 
 
 def slab_range(ns: int, world: int, rank: int) -> tuple:
@@ -28,12 +30,6 @@ def local_rows(ns: int, world: int, rank: int, extra_row: bool) -> int:
     return (r1 - r0) + (1 if extra_row and rank == world - 1 else 0)
 
 
-def neighbours(world: int, rank: int, periodic: bool) -> tuple:
-    prev = rank - 1 if rank > 0 else (world - 1 if periodic else -1)
-    nxt = rank + 1 if rank < world - 1 else (0 if periodic else -1)
-    return prev, nxt
-
-
 def owner_of_row(ns: int, world: int, row: int) -> int:
     for r in range(world):
         r0, r1 = slab_range(ns, world, r)
@@ -42,38 +38,38 @@ def owner_of_row(ns: int, world: int, row: int) -> int:
     raise ValueError(f"row {row} outside 0..{ns}")
 
 
-def with_ghosts(slab: np.ndarray) -> np.ndarray:
-    """Allocate [rows + 2G, ...] with the slab in the middle (ghosts zero)."""
-    out = np.zeros((slab.shape[0] + 2 * G,) + slab.shape[1:], dtype=slab.dtype)
-    out[G:-G] = slab
+def plan(desc, world: int, rank: int, kind: int) -> list:
+    """The library's halo plan (hw_exchange_plan) for slab `rank` of `world`."""
+    return _abi.exchange_plan(desc, world, rank, kind)
+
+
+def with_ghosts(slab: np.ndarray, fill=0.0) -> np.ndarray:
+    """[rows + 2G, ...] with the slab in the middle (local row r at index r + G)."""
+    out = np.full((slab.shape[0] + 2 * G,) + slab.shape[1:], fill, dtype=slab.dtype)
+    out[G:G + slab.shape[0]] = slab
     return out
 
 
-def exchange_halos(fields: list, world: int, rank: int, periodic: bool) -> None:
-    """Fill the inter-rank ghost slabs of `fields` (arrays from with_ghosts) in place
-    with torch.distributed point-to-point messages, in the library's order."""
+def exchange_host(desc, fields: dict, world: int, rank: int, kind: int) -> list:
+    """Execute the library's plan on host arrays: `fields` maps external field index -> array
+    from with_ghosts.  Returns the plan that ran."""
     import torch
     import torch.distributed as dist
 
-    prev, nxt = neighbours(world, rank, periodic)
-    ops = []
-    recv = []
-    for f in fields:  # phase A: bottom rows -> next, top ghosts <- prev
-        if nxt >= 0:
-            ops.append(dist.P2POp(dist.isend, torch.from_numpy(np.ascontiguousarray(f[-2 * G:-G])), nxt))
-        if prev >= 0:
-            buf = torch.empty(f[:G].shape, dtype=torch.from_numpy(f[:1]).dtype)
-            ops.append(dist.P2POp(dist.irecv, buf, prev))
-            recv.append((f, slice(0, G), buf))
-    for f in fields:  # phase B: top rows -> prev, bottom ghosts <- next
-        if prev >= 0:
-            ops.append(dist.P2POp(dist.isend, torch.from_numpy(np.ascontiguousarray(f[G:2 * G])), prev))
-        if nxt >= 0:
-            buf = torch.empty(f[-G:].shape, dtype=torch.from_numpy(f[:1]).dtype)
-            ops.append(dist.P2POp(dist.irecv, buf, nxt))
-            recv.append((f, slice(f.shape[0] - G, f.shape[0]), buf))
+    p = plan(desc, world, rank, kind)
+    ops, recv = [], []
+    for x in p:
+        a = fields[x["field"]]
+        sl = slice(x["row0"] + G, x["row0"] + G + x["nrows"])
+        if x["send"]:
+            ops.append(dist.P2POp(dist.isend, torch.from_numpy(np.ascontiguousarray(a[sl])), x["peer"]))
+        else:
+            buf = torch.from_numpy(np.empty_like(a[sl]))
+            ops.append(dist.P2POp(dist.irecv, buf, x["peer"]))
+            recv.append((a, sl, buf))
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
-    for f, sl, buf in recv:
-        f[sl] = buf.numpy()
+    for a, sl, buf in recv:
+        a[sl] = buf.numpy()
+    return p
