@@ -405,6 +405,10 @@ struct hw_solver {
     int64_t el3_cm = 0;
     int el3_group = 1;          // its CTA groups of adjacent tiles (hw_elastic3d_fused.cu)
     double* el3_ecoef = nullptr;  // its per-slab energy coefficients (slow-layered media; in plane_mem)
+    bool el3_slab = false;        // ... on a slab of a decomposed domain (ghosts from HW_PLAN_FUSED_EL3)
+    double* el3_eplane = nullptr; // ... energy partials per (slab, tile) unit (in plane_mem)
+    double* el3_etot = nullptr;   // ... energy plane totals per sample
+    int64_t el3_etot_cap = 0;
     bool el3_stream = false;  // streaming 3D elastic phases
     int stream_blocks = 0;
     unsigned int* counter = nullptr;  // CTA arrival counter of the streaming stress kernel
@@ -811,12 +815,13 @@ int setup_handle(hw_solver* h) {
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
             h->ac3_stream = true;
         }
-        // one-pass 3D elastic step (2nd order, single domain, media constant along x)
+        // one-pass 3D elastic step (2nd order, periodic, media constant along x): a single domain, or
+        // one slab of a decomposed domain (ghost rows exchanged once per step, halo velocities
+        // recomputed from them)
         ElParams EP;
         if (!h->ac && h->d3) fill_params(h, EP);
         if (want && opt("fused_el3") == 1 && !h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
-            h->world == 1 && h->transport == 0 &&
-            el3d_fused_eligible(EP, desc->nx, desc->nm, desc->ns, h->g.pitch, desc->order, dev_smem)) {
+            el3d_fused_eligible(EP, desc->nx, desc->nm, field_rows(h, F_SXX), h->g.pitch, desc->order, dev_smem)) {
             for (int j = 0; j < 2 * h->nsol; j++) {
                 int f = h->ext[j % h->nsol];
                 size_t bytes = (size_t)(field_rows(h, f) + 2 * G) * h->g.slab * esz;
@@ -824,15 +829,20 @@ int setup_handle(hw_solver* h) {
                 CU(cudaMemset(h->mem_b[j], 0, bytes));
             }
             if (el3d_fused_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "fused 3D elastic setup failed");
+            h->el3_slab = h->world > 1 || h->transport != 0;
             h->el3_cm = el3d_fused_coef_rows(EP);
-            CU(cudaMalloc(&h->el3_coef, (size_t)max_rows * h->el3_cm * 8 * sizeof(float)));
+            const int64_t lo = h->el3_slab ? G : 0;  // slab: coefficient rows -G .. rows+G (halo velocities)
+            CU(cudaMalloc(&h->el3_coef, (size_t)(max_rows + 2 * lo) * h->el3_cm * 8 * sizeof(float)));
             h->plane_mem.push_back(h->el3_coef);
-            CU(el3d_fused_coef(EP, h->el3_coef, max_rows, h->el3_cm, 0));
+            CU(el3d_fused_coef(EP, h->el3_coef, -lo, max_rows + 2 * lo, h->el3_cm, 0));
+            h->el3_coef += lo * h->el3_cm * 8;  // (plane_mem keeps the allocation base)
             if (el3d_fused_erow(EP)) {
                 CU(cudaMalloc(&h->el3_ecoef, (size_t)max_rows * 8 * sizeof(double)));
                 h->plane_mem.push_back(h->el3_ecoef);
                 CU(el3d_fused_ecoef(EP, h->el3_ecoef, max_rows, 0));
             }
+            CU(cudaMalloc(&h->el3_eplane, (size_t)max_rows * (desc->nm / (2048 / desc->nx)) * NCOMP * sizeof(double)));
+            h->plane_mem.push_back(h->el3_eplane);
             const int64_t units = (desc->nm / (2048 / desc->nx)) * max_rows;
             int64_t nbs = units / 4;
             if (nbs < 1) nbs = 1;
@@ -923,6 +933,7 @@ void release_handle(hw_solver* h) {
     if (h->gbar) cudaFree(h->gbar);
     if (h->src_dev) cudaFree(h->src_dev);
     if (h->partials2) cudaFree(h->partials2);
+    if (h->el3_etot) cudaFree(h->el3_etot);
     for (int k = 0; k < 2; k++) {
         if (h->ev_edge[k]) cudaEventDestroy(h->ev_edge[k]);
         if (h->ev_int[k]) cudaEventDestroy(h->ev_int[k]);
@@ -974,9 +985,15 @@ int pg_next(const PlanGeom& g) { return g.rank < g.world - 1 ? g.rank + 1 : (g.f
 std::vector<hw_xfer> halo_plan(const PlanGeom& g, int kind) {
     std::vector<int> js;   // external field indices, in external order
     int64_t depth = 0;
+    std::vector<int64_t> dep;  // per-field depth (HW_PLAN_FUSED_EL3)
     if (kind == HW_PLAN_FUSED) {
         js = {0, 2, 5};  // p, vy, rvy of p vx vy rp rvx rvy
         depth = G;
+    } else if (kind == HW_PLAN_FUSED_EL3) {
+        // one-pass 3D elastic slab (hw_elastic3d_fused.cu): its halo velocities v(-1), v(L) are
+        // recomputed from stress rows -2 .. L and the old velocities / residuals of rows -1, L
+        js = {3, 4, 5, 6, 7, 8, 0, 1, 2, 9, 10, 11};  // sxx syy szz sxy sxz syz, vx vy vz, rvx rvy rvz
+        dep = {2, 2, 2, 2, 2, 2, 1, 1, 1, 1, 1, 1};
     } else {
         for (int j = 0; j < g.nsol; j++) {
             const int f = g.ext[j];
@@ -986,15 +1003,17 @@ std::vector<hw_xfer> halo_plan(const PlanGeom& g, int kind) {
     }
     const int pv = pg_prev(g), nx_ = pg_next(g);
     std::vector<hw_xfer> out;
-    for (int j : js) {
-        const int64_t n = pg_rows(g, g.ext[j % g.nsol]);
-        if (nx_ >= 0) out.push_back(hw_xfer{j, nx_, 1, 0, n - depth, depth});
-        if (pv >= 0) out.push_back(hw_xfer{j, pv, 0, 0, -depth, depth});
+    for (size_t q = 0; q < js.size(); q++) {
+        const int j = js[q];
+        const int64_t n = pg_rows(g, g.ext[j % g.nsol]), d = dep.empty() ? depth : dep[q];
+        if (nx_ >= 0) out.push_back(hw_xfer{j, nx_, 1, 0, n - d, d});
+        if (pv >= 0) out.push_back(hw_xfer{j, pv, 0, 0, -d, d});
     }
-    for (int j : js) {
-        const int64_t n = pg_rows(g, g.ext[j % g.nsol]);
-        if (pv >= 0) out.push_back(hw_xfer{j, pv, 1, 0, 0, depth});
-        if (nx_ >= 0) out.push_back(hw_xfer{j, nx_, 0, 0, n, depth});
+    for (size_t q = 0; q < js.size(); q++) {
+        const int j = js[q];
+        const int64_t n = pg_rows(g, g.ext[j % g.nsol]), d = dep.empty() ? depth : dep[q];
+        if (pv >= 0) out.push_back(hw_xfer{j, pv, 1, 0, 0, d});
+        if (nx_ >= 0) out.push_back(hw_xfer{j, nx_, 0, 0, n, d});
     }
     return out;
 }
@@ -1004,7 +1023,7 @@ std::vector<hw_xfer> halo_plan(const PlanGeom& g, int kind) {
 char* plan_row(const hw_solver* h, int kind, int buf, int j, int64_t row) {
     const size_t rb = (size_t)h->g.slab * lane_bytes(h->LU);
     char* base;
-    if (kind == HW_PLAN_FUSED) base = (char*)(buf ? h->mem_b[j] : h->mem[j]) + G * rb;
+    if (kind == HW_PLAN_FUSED || kind == HW_PLAN_FUSED_EL3) base = (char*)(buf ? h->mem_b[j] : h->mem[j]) + G * rb;
     else base = (char*)(j < h->nsol ? h->fv : h->rv)[h->ext[j % h->nsol]].base;
     return base + row * (int64_t)rb;
 }
@@ -1085,6 +1104,34 @@ int exchange(hw_solver* h, int phase) {
     if (h->transport == 2) return exchange_nccl(h, phase);
     if (h->world == 1) return HW_OK;
     return HW_OK;  // group ranks are exchanged by the group driver
+}
+
+// Decomposition-invariant energy of the one-pass 3D elastic kernel: E_k = scale * (sum over the
+// global slow planes, in order, of the plane totals T_k[s]) -- bit-identical for any slab count.
+// planes[r] holds rank r's [ne][rows_r] totals.
+void el3_energy_from_planes(const std::vector<std::vector<double>>& planes, const std::vector<int64_t>& rows,
+                            int64_t ne, double scale, double* e_vals) {
+    for (int64_t k = 0; k < ne; k++) {
+        double t = 0.0;
+        bool first = true;
+        for (size_t r = 0; r < planes.size(); r++)
+            for (int64_t sp = 0; sp < rows[r]; sp++) {
+                const double v = planes[r][k * rows[r] + sp];
+                t = first ? v : t + v;
+                first = false;
+            }
+        e_vals[k] = scale * t;
+    }
+}
+
+double C_scale(const hw_solver* h) { return 0.5 * h->d.dx * h->d.dx * (h->d3 ? h->d.dx : 1.0); }
+
+int el3_planes_host(hw_solver* h, int64_t ne, std::vector<double>& out) {
+    out.resize(ne * h->max_rows);
+    CU(cudaSetDevice(h->d.device));
+    CU(cudaStreamSynchronize(h->st));
+    if (ne > 0) CU(cudaMemcpy(out.data(), h->el3_etot, out.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    return HW_OK;
 }
 
 }  // namespace
@@ -1297,11 +1344,21 @@ static int run_begin(hw_solver* h, int32_t variant, int64_t nt, bool energy, boo
     C.every = h->d.energy_every;
     C.energy = energy;
     h->launches = 0;
+    if (h->fused_el3 && energy) {  // energy plane totals per sample (el3_energy_from_planes)
+        int64_t cap = h->el3_etot_cap;
+        if ((rc = ensure(&h->el3_etot, &cap, (1 + nt / h->d.energy_every) * h->max_rows))) return rc;
+        h->el3_etot_cap = cap;
+    }
     if (energy) {  // E(t=0) pairs the state with itself
         if (h->ac) launch_ac_energy(h->LU, h->W, C.A, h->max_rows, h->st);
         else launch_el_energy(h->LU, h->W, C.L, h->max_rows, h->st);
         launch_epilogue(h->LU, C.E, -1, 1, 0, h->st);
         h->launches += 2;
+        if (h->fused_el3) {  // ... and its per-slab totals (one block partial per (x chunk, mid row, slab))
+            const dim3 gr = grid3(h->g, h->W, h->max_rows);
+            launch_plane_totals(h->partials, (int64_t)gr.x * gr.y, h->max_rows, h->el3_etot, h->st);
+            h->launches++;
+        }
     }
     CU(cudaGetLastError());
     return HW_OK;
@@ -1453,6 +1510,18 @@ static void fused_el3_bufs(const hw_solver* h, int cur, ElParams& P, El3In& in) 
     in.div_mode[2] = h->lp[HW_PL_RHO_M].div_mode;
     in.group = h->el3_group;
     in.ecoef = h->el3_ecoef;
+    in.eplane = h->el3_eplane;
+    in.etot = h->el3_etot;
+    in.slab = h->el3_slab ? 1 : 0;
+    in.vsrc = 0;
+    in.vsrc_s = 0;
+    if (h->d.src_kind == HW_SRC_VSLOW) {  // this slab also computes the halo velocity rows -1 and L
+        const int64_t r = h->d.src_s - h->r0;
+        if (r >= -1 && r <= h->ns_loc) {
+            in.vsrc = 1;
+            in.vsrc_s = r;
+        }
+    }
 }
 
 static void fused_bufs(const hw_solver* h, __half* bufs[2][FUSED_NSTREAM]) {
@@ -1470,8 +1539,8 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
     int rc = run_begin(h, variant, nt, energy, true, C);
     if (rc) return rc;
     const bool fused_slab = h->fused && h->transport == 2;
-    if (fused_slab) {  // halos of the uploaded state
-        if ((rc = exchange_nccl_plan(h, HW_PLAN_FUSED, 0))) return rc;
+    if (fused_slab || (h->fused_el3 && h->transport == 2)) {  // halos of the uploaded state
+        if ((rc = exchange_nccl_plan(h, fused_slab ? HW_PLAN_FUSED : HW_PLAN_FUSED_EL3, 0))) return rc;
     } else if ((rc = exchange(h, 0)) || (rc = exchange(h, 1))) {
         return rc;
     }
@@ -1571,6 +1640,7 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
                 h->launches++;
             }
             cur ^= 1;
+            if (h->transport == 2 && (rc = exchange_nccl_plan(h, HW_PLAN_FUSED_EL3, cur))) return rc;
         }
     } else if (h->fused_el) {  // one-pass 2D elastic kernel, ping-pong A <-> B: step n reads buffer n % 2
         const StreamIO IO = stream_io(h, C);
@@ -1718,7 +1788,31 @@ int hw_run(hw_solver* h, int32_t variant, int64_t step0, int64_t nt, const doubl
     const int64_t nrec = h->d.n_receivers;
     const int64_t ne = energy ? 1 + (status == HW_OK ? nt / h->d.energy_every : (done - 1) / h->d.energy_every) : 0;
     if (h->transport == 2) {
-        if (ne > 0) {  // per-rank energy totals gathered, then summed in rank order on every rank
+        if (ne > 0 && h->fused_el3) {  // plane totals of every rank, summed in global plane order
+            std::vector<double> mine;
+            if ((rc = el3_planes_host(h, ne, mine))) return rc;
+            const int64_t lmax = (h->d.ns + h->world - 1) / h->world;
+            std::vector<double> pad((size_t)ne * lmax, 0.0), allh((size_t)ne * lmax * h->world);
+            for (int64_t q = 0; q < ne * h->max_rows; q++) pad[q] = mine[q];
+            double* dev = nullptr;
+            CU(cudaMalloc(&dev, sizeof(double) * ne * lmax * (h->world + 1)));
+            CU(cudaMemcpy(dev, pad.data(), sizeof(double) * ne * lmax, cudaMemcpyHostToDevice));
+            NC(g_nccl.AllGather(dev, dev + ne * lmax, ne * lmax, ncclFloat64, h->nccl, h->st));
+            CU(cudaMemcpyAsync(allh.data(), dev + ne * lmax, sizeof(double) * ne * lmax * h->world,
+                               cudaMemcpyDeviceToHost, h->st));
+            CU(cudaStreamSynchronize(h->st));
+            cudaFree(dev);
+            std::vector<std::vector<double>> planes(h->world);
+            std::vector<int64_t> rows(h->world);
+            for (int r = 0; r < h->world; r++) {
+                rows[r] = (int64_t)(r + 1) * h->d.ns / h->world - (int64_t)r * h->d.ns / h->world;
+                planes[r].resize(ne * rows[r]);
+                for (int64_t k = 0; k < ne * rows[r]; k++) planes[r][k] = allh[(size_t)r * ne * lmax + k];
+            }
+            std::vector<double> tot(ne);
+            el3_energy_from_planes(planes, rows, ne, C_scale(h), tot.data());
+            CU(cudaMemcpy(h->evals, tot.data(), sizeof(double) * ne, cudaMemcpyHostToDevice));
+        } else if (ne > 0) {  // per-rank energy totals gathered, then summed in rank order on every rank
             double* all = nullptr;
             CU(cudaMalloc(&all, sizeof(double) * ne * h->world));
             NC(g_nccl.AllGather(h->evals, all, ne, ncclFloat64, h->nccl, h->st));
@@ -1742,6 +1836,13 @@ int hw_run(hw_solver* h, int32_t variant, int64_t step0, int64_t nt, const doubl
             NC(g_nccl.Broadcast(h->traces + j * nt, h->traces + j * nt, nt, ncclFloat64, owner, h->nccl, h->st));
         }
         CU(cudaStreamSynchronize(h->st));
+    }
+    if (h->fused_el3 && h->transport == 0 && ne > 0) {  // the same plane-ordered sum on one domain
+        std::vector<std::vector<double>> planes(1);
+        if ((rc = el3_planes_host(h, ne, planes[0]))) return rc;
+        std::vector<double> tot(ne);
+        el3_energy_from_planes(planes, {h->max_rows}, ne, C_scale(h), tot.data());
+        CU(cudaMemcpy(h->evals, tot.data(), sizeof(double) * ne, cudaMemcpyHostToDevice));
     }
     if (traces && nrec > 0 && nt > 0) CU(cudaMemcpy(traces, h->traces, nrec * nt * sizeof(double), cudaMemcpyDeviceToHost));
     if (e_vals && ne > 0) CU(cudaMemcpy(e_vals, h->evals, ne * sizeof(double), cudaMemcpyDeviceToHost));
@@ -1796,6 +1897,30 @@ int hw_run_group(hw_solver* const* hs, int32_t nslabs, int32_t variant, int64_t 
             cur ^= 1;
             if ((rc = exchange_group_plan(grp, HW_PLAN_FUSED, cur))) return rc;
         }
+    } else if (grp->ranks[0]->fused_el3) {  // one-pass 3D elastic slabs: one exchange per step
+        if ((rc = exchange_group_plan(grp, HW_PLAN_FUSED_EL3, 0))) return rc;  // halos of the uploaded state
+        int cur = 0;
+        for (int64_t n = 0; n < nt; n++) {
+            for (hw_solver* h : grp->ranks) {
+                cudaSetDevice(h->d.device);
+                RunCtx& Cr = C[h->rank];
+                ElParams P = Cr.L;
+                El3In in;
+                fused_el3_bufs(h, cur, P, in);
+                const int sample = energy && ((n + 1) % Cr.every == 0);
+                launch_el3d_fused(variant, P, in, stream_io(h, Cr), h->stream_blocks, n,
+                                  src_samples ? src_samples[n] : 0.0, sample, (n + 1) / Cr.every, h->st);
+                h->launches++;
+                if (Cr.E.n_rec > 0) {
+                    EpParams E = Cr.E;
+                    E.trace_base = P.vs.base;
+                    launch_epilogue(h->LU, E, n, 0, 0, h->st);
+                    h->launches++;
+                }
+            }
+            cur ^= 1;
+            if ((rc = exchange_group_plan(grp, HW_PLAN_FUSED_EL3, cur))) return rc;
+        }
     } else {
     if (nslabs > 1) {
         if ((rc = exchange_group(grp, 0)) || (rc = exchange_group(grp, 1))) return rc;  // halos of the uploaded state
@@ -1841,7 +1966,15 @@ int hw_run_group(hw_solver* const* hs, int32_t nslabs, int32_t variant, int64_t 
     const int64_t nrec = h0->d.n_receivers;
     const int64_t ne = energy ? 1 + (status == HW_OK ? nt / h0->d.energy_every : (done - 1) / h0->d.energy_every) : 0;
     std::vector<double> tmp;
-    if (e_vals && ne > 0) {  // per-slab energies summed in slab order (fixed)
+    if (e_vals && ne > 0 && h0->fused_el3) {  // plane totals of every slab, in global plane order
+        std::vector<std::vector<double>> planes(nslabs);
+        std::vector<int64_t> rows(nslabs);
+        for (hw_solver* h : grp->ranks) {
+            if ((rc = el3_planes_host(h, ne, planes[h->rank]))) return rc;
+            rows[h->rank] = h->max_rows;
+        }
+        el3_energy_from_planes(planes, rows, ne, C_scale(h0), e_vals);
+    } else if (e_vals && ne > 0) {  // per-slab energies summed in slab order (fixed)
         std::fill(e_vals, e_vals + ne, 0.0);
         tmp.resize(ne);
         for (hw_solver* h : grp->ranks) {
@@ -1930,7 +2063,7 @@ int hw_plane_div_mode(const hw_solver* h, int32_t plane) {
 
 int hw_exchange_plan(const hw_desc* desc, int32_t world, int32_t rank, int32_t kind, hw_xfer* out, int32_t cap,
                      int32_t* n) {
-    if (!desc || !n || world < 1 || rank < 0 || rank >= world || kind < 0 || kind > 2)
+    if (!desc || !n || world < 1 || rank < 0 || rank >= world || kind < 0 || kind > 3)
         return fail(HW_EINVAL, "hw_exchange_plan: bad arguments");
     PlanGeom g;
     g.ac = desc->equation == HW_EQ_ACOUSTIC;
@@ -1942,6 +2075,7 @@ int hw_exchange_plan(const hw_desc* desc, int32_t world, int32_t rank, int32_t k
     g.ext = ext_order(desc->equation, desc->ndim, &g.nsol);
     g.ns_loc = (int64_t)(rank + 1) * desc->ns / world - (int64_t)rank * desc->ns / world;
     if (kind == HW_PLAN_FUSED && !(g.ac && !g.d3)) return fail(HW_EINVAL, "hw_exchange_plan: fused plan is 2D acoustic");
+    if (kind == HW_PLAN_FUSED_EL3 && !(!g.ac && g.d3)) return fail(HW_EINVAL, "hw_exchange_plan: HW_PLAN_FUSED_EL3 is 3D elastic");
     const std::vector<hw_xfer> p = halo_plan(g, kind);
     *n = (int32_t)p.size();
     if (out)

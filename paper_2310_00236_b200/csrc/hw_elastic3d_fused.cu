@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
     const __half dt = lconst<16>(P.k, 4);
     const __half2 dt2 = __half2half2(dt);
     const __half srch = __double2half(src);
-    const bool vsrc = P.src_kind == HW_SRC_VSLOW && src != 0.0;      // CTA-uniform
+    const bool vsrc = in.vsrc && src != 0.0;  // CTA-uniform; its row may be a slab's halo row (-1 or L)
     const bool ssrc = P.src_kind == HW_SRC_EXPLOSIVE && src != 0.0;  // CTA-uniform
     const bool src_col = (vsrc || ssrc) && P.src_x >= x && P.src_x < x + CPT;
     const int sj = (int)((P.src_x - x) >> 1), sln = (int)((P.src_x - x) & 1);
@@ -301,10 +301,13 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
     __half2 acc[9];
 #pragma unroll
     for (int q = 0; q < 9; q++) acc[q] = __float2half2_rn(0.f);
-    double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    __shared__ double ered[32];  // per-warp energy partials of one (tile, slab) unit
     const int cm = (int)in.coef_m;  // coefficient rows per slab: 1 (slow-layered) or nm
 
-    auto wrap = [&](int s) { return s < 0 ? s + ns : (s >= ns ? s - ns : s); };
+    // single periodic domain: slab indices wrap; slab of a decomposed domain: rows -2 .. ns+1 are
+    // ghost rows filled by the halo exchange (HW_PLAN_FUSED_EL3) before every step
+    const bool slabm = in.slab != 0;
+    auto wrap = [&](int s) { return slabm ? s : (s < 0 ? s + ns : (s >= ns ? s - ns : s)); };
     // Work split: groups of `grp` CTAs own `grp` adjacent mid tiles and stream the same slab
     // range side by side, so the halo rows one CTA reads are the rows its neighbour in the
     // group reads (or wrote) at about the same time: L2 hits instead of DRAM re-reads.  The
@@ -389,7 +392,7 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                     addv<PP>(xfv<PP>(c, T1 + (X::O_SXM + 1) * NX, to, tl, tr, true),
                              fv<PP>(c, ldv<PP>(T2 + (X::O_SMS + 1) * NX + to), ldv<PP>(T1 + (X::O_SMS + 1) * NX + to))),
                     fv<PP>(c, ldv<PP>(T1 + (X::O_SMM + 1) * NX + to), ldv<PP>(T1 + (X::O_SMM + 2) * NX + to)));
-                if (vsrc && k == P.src_s && m == P.src_m && src_col) add_srcv<PP>(as.q, sj, sln, srch);
+                if (vsrc && k == in.vsrc_s && m == P.src_m && src_col) add_srcv<PP>(as.q, sj, sln, srch);
                 // the old values are waited for only now: the A slot was refilled during the previous
                 // iteration's stress phase, the stencil sums above overlap the rest of its latency
                 mbar_wait(abar, (uint32_t)((ga0 + i) & 1));
@@ -456,7 +459,7 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                         a = addv<PP>(addv<PP>(xfv<PP>(c, T1 + X::O_SXS * NX + (TM - 2) * NX, to, tl, tr, true),
                                               fv<PP>(c, ldv<PP>(T1 + X::O_SSS * NX + a0), ldv<PP>(T0 + X::O_SSS * NX + a0))),
                                      fv<PP>(c, ldv<PP>(T1 + X::O_SMS * NX + a0), ldv<PP>(T1 + (X::O_SMS + 1) * NX + a0)));
-                        if (vsrc && k == P.src_s && mhi == P.src_m && src_col) add_srcv<PP>(a.q, sj, sln, srch);
+                        if (vsrc && k == in.vsrc_s && mhi == P.src_m && src_col) add_srcv<PP>(a.q, sj, sln, srch);
                     }
 #pragma unroll
                     const int hm = in.div_mode[j == 1 ? 0 : 1];
@@ -535,6 +538,7 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                     if (comp) gst<PP>(*ORS[q], so, edge, s, slab, rr[q]);
                 }
                 if (sample) {  // diagnostics.py:100-162, 3D compliance form (k_el_stress)
+                    double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};  // this (tile, slab) unit's share
                     const EV<PP> vxo = ldv<PP>(vxt + to), vmo = ldv<PP>(vmt + NX + to), vso = ldv<PP>(vst + to);
                     auto f = [&](const EV<PP>& a, int q) { return (double)__half2float(a.q[q >> 1].e[q & 1]); };
                     if (erow) {  // per-slab medium: raw sums per iteration, one coefficient row per slab
@@ -582,6 +586,11 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                             for (int w = 3; w < 6; w++) e[4] += mun > 0.0 ? (f(old[w], q) * f(nw[w], q)) / mun : 0.0;
                         }
                     }
+                    // per-plane partials (decomposition-invariant energy): the thread's share of the
+                    // unit, a warp tree now, the warps' sums combined by lane 0 of warp 0 after the
+                    // end-of-iteration barrier
+                    const double a = warp_sum((((e[0] + e[1]) + e[2]) + e[3]) + e[4]);
+                    if ((tid & 31) == 0) ered[tid >> 5] = a;
                 }
             }
             if (vel) {
@@ -593,6 +602,11 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
             if (tid == 0 && i + 1 < NI && F + 1 - 2 >= sb && F + 1 - 2 < se) {
                 fence_proxy_async_smem();
                 issue_b(i + 1);
+            }
+            if (sample && tid == 0 && s >= sb && s < se) {  // the unit's partial, warps in order
+                double a = ered[0];
+                for (int w = 1; w < X::NT / 32; w++) a += ered[w];
+                in.eplane[(int64_t)s * (nm / TM) + tile] = a;
             }
         }
         gi += NI;
@@ -607,18 +621,36 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
     for (int q = 0; q < 6; q++) mask |= e_nonfinite(acc[3 + q]) << OS[q]->bit;
     record_failure(P.ctrl, n, mask);
     if constexpr (!SAMPLE) return;
-    block_partials(e, P.partials);
     __threadfence();
     __syncthreads();
     __shared__ unsigned int is_last;
     if (tid == 0) is_last = atomicAdd(IO.counter, 1u) == (unsigned int)(gridDim.x - 1);
     __syncthreads();
     if (!is_last) return;
-    const double t = finalize_partials(P.partials, (int)gridDim.x);  // fixed-order fp64 reduction
-    if (tid == 0) {
-        IO.e_vals[eidx] = IO.scale * t;
-        *IO.counter = 0u;
+    // plane totals T[s] = sum_tile partial[s][tile], tiles in order: the host sums the planes of all
+    // slabs in global order (el3_energy_from_planes, hw_api.cu)
+    const int tiles_all = nm / TM;
+    for (int sp = tid; sp < ns; sp += X::NT) {
+        double t = __ldcg(&in.eplane[(int64_t)sp * tiles_all]);
+        for (int t2 = 1; t2 < tiles_all; t2++) t += __ldcg(&in.eplane[(int64_t)sp * tiles_all + t2]);
+        in.etot[eidx * (int64_t)ns + sp] = t;
     }
+    if (tid == 0) *IO.counter = 0u;
+}
+
+// Plane totals of a generic energy launch (k_el_energy: one block partial per (x chunk, mid
+// row, slab), slab-major): T[s] = sum_c (sum_b partial[s][b][c]) -- the same fixed order per
+// slab whatever the decomposition (E(0) of the one-pass kernel's runs).
+__global__ void k_plane_totals(const double* partials, int64_t blocks_per_plane, int64_t nplanes, double* out) {
+    const int64_t sp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (sp >= nplanes) return;
+    double t = 0.0;
+    for (int c = 0; c < NCOMP; c++) {
+        double a = partials[(sp * blocks_per_plane) * NCOMP + c];
+        for (int64_t b = 1; b < blocks_per_plane; b++) a += partials[(sp * blocks_per_plane + b) * NCOMP + c];
+        t += a;
+    }
+    out[sp] = t;
 }
 
 // Medium coefficient table of the one-pass kernel: per (slab, mid row) -- one row per slab
@@ -626,10 +658,10 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
 // (DIV_CHEAP planes) or their values, and the stencil-lane stiff, lam, mu_n, all as binary32
 // (exact: binary16 values / binary32 reciprocals).
 __global__ void k_el3_coef(PlaneView rx, PlaneView rs, PlaneView rm, PlaneView st, PlaneView la, PlaneView mu,
-                           float* out, int64_t ns, int64_t cm) {
+                           float* out, int64_t s0, int64_t ns, int64_t cm) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= ns * cm) return;
-    const int64_t s = i / cm, m = i % cm;
+    const int64_t s = s0 + i / cm, m = i % cm;
     float* o = out + 8 * i;
     const PlaneView* rho[3] = {&rx, &rs, &rm};
     for (int q = 0; q < 3; q++) {
@@ -677,7 +709,7 @@ static size_t x3_bytes(int64_t nx) {
 
 bool el3d_fused_eligible(const ElParams& P, int64_t nx, int64_t nm, int64_t ns, int64_t pitch, int order,
                          int max_smem) {
-    if (order != 2 || (nx != 256 && nx != 512) || pitch != nx || ns < 4) return false;
+    if (order != 2 || P.fs || (nx != 256 && nx != 512) || pitch != nx || ns < 4) return false;
     const int64_t TM = 2048 / nx;
     if (nm % TM != 0 || nm < 2 * TM || x3_bytes(nx) > (size_t)max_smem) return false;
     // densities and moduli constant along x (slow-layered or per (slab, mid) row)
@@ -700,11 +732,16 @@ cudaError_t el3d_fused_ecoef(const ElParams& P, double* out, int64_t ns, cudaStr
     return cudaGetLastError();
 }
 
-cudaError_t el3d_fused_coef(const ElParams& P, float* out, int64_t ns, int64_t cm, cudaStream_t st) {
+cudaError_t el3d_fused_coef(const ElParams& P, float* out, int64_t s0, int64_t ns, int64_t cm, cudaStream_t st) {
     const int64_t cnt = ns * cm;
     k_el3_coef<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(P.rho_x, P.rho_s, P.rho_m, P.stiff, P.lam, P.mu_n, out,
-                                                              ns, cm);
+                                                              s0, ns, cm);
     return cudaGetLastError();
+}
+
+void launch_plane_totals(const double* partials, int64_t blocks_per_plane, int64_t nplanes, double* out,
+                         cudaStream_t st) {
+    k_plane_totals<<<(unsigned)((nplanes + 127) / 128), 128, 0, st>>>(partials, blocks_per_plane, nplanes, out);
 }
 
 template <int NX>

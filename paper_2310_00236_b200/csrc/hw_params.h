@@ -131,13 +131,20 @@ struct El3In {
     int32_t div_mode[3]; // DivMode of rho_x, rho_s, rho_m
     int32_t group;       // CTAs per group of adjacent mid tiles streamed side by side (divides the grid)
     const double* ecoef; // [ns][8] energy coefficients of slow-layered media (k_el3_ecoef), or null
+    double* eplane;      // [ns][tiles] energy partials of the (tile, slab) units (sample steps)
+    double* etot;        // [samples][ns] energy plane totals (sample eidx at etot + eidx * ns)
+    int32_t slab;        // slab of a decomposed domain (ghost rows from the halo exchange), else 0
+    int32_t vsrc;        // a v_slow point source whose row vsrc_s (local, -1 .. ns) this slab computes
+    int64_t vsrc_s;
 };
 bool el3d_fused_eligible(const ElParams& P, int64_t nx, int64_t nm, int64_t ns, int64_t pitch, int order,
                          int max_smem);
 int64_t el3d_fused_coef_rows(const ElParams& P);
 bool el3d_fused_erow(const ElParams& P);
 cudaError_t el3d_fused_ecoef(const ElParams& P, double* out, int64_t ns, cudaStream_t st);
-cudaError_t el3d_fused_coef(const ElParams& P, float* out, int64_t ns, int64_t cm, cudaStream_t st);
+cudaError_t el3d_fused_coef(const ElParams& P, float* out, int64_t s0, int64_t ns, int64_t cm, cudaStream_t st);
+void launch_plane_totals(const double* partials, int64_t blocks_per_plane, int64_t nplanes, double* out,
+                         cudaStream_t st);
 cudaError_t el3d_fused_prepare(int64_t nx);
 void launch_el3d_fused(int variant, const ElParams& P, const El3In& in, const StreamIO& IO, int nblocks, int64_t n,
                        double src, int sample, int64_t eidx, cudaStream_t st);

@@ -64,8 +64,14 @@ def _acoustic3d(**kw):
     return s, st
 
 
+def _elastic3d_onepass(**kw):  # config 5's one-pass kernel on the NCCL transport (HW_PLAN_FUSED_EL3)
+    from test_gpu_el3_slabs import _el3
+
+    return _el3(1, distributed=bool(kw.get("distributed")))
+
+
 @pytest.mark.parametrize("make,variant", [(_acoustic, hw.Variant.OP3), (_elastic, hw.Variant.OP6),
-                                          (_acoustic3d, hw.Variant.OP3)])
+                                          (_acoustic3d, hw.Variant.OP3), (_elastic3d_onepass, hw.Variant.OP6)])
 def test_nccl_transport_equals_single_process(one_rank_job, make, variant):
     a, sa = make()
     oa = a.run(variant, sa)
@@ -75,6 +81,8 @@ def test_nccl_transport_equals_single_process(one_rank_job, make, variant):
     for n in a.FIELDS:
         assert_same_bits(getattr(sb, n).values, getattr(sa, n).values, n)
     np.testing.assert_array_equal(np.array([t.samples for t in ob.traces]), np.array([t.samples for t in oa.traces]))
+    if a.kernel_path() == b.kernel_path() == "fused3d-el":  # plane-ordered energy: identical on any decomposition
+        np.testing.assert_array_equal(ob.energy.values, oa.energy.values)
     np.testing.assert_allclose(ob.energy.values, oa.energy.values, rtol=1e-12)
 
 
