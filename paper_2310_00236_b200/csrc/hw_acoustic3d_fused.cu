@@ -82,14 +82,17 @@ __device__ __forceinline__ void f3_finish_v(const E8& a, bool rm, float rc, cons
     }
 }
 
-template <int V>
+// NXC: the row width as a compile-time constant (512, BASELINE config 3: shared-memory and row
+// offsets fold into immediates) or 0 (runtime width); SAMPLE: energy sample step.
+template <int V, int NXC, bool SAMPLE>
 __global__ void __launch_bounds__(F3T, 1)
-    k_ac3d_fused(AcParams P, Ac3In in, StreamIO IO, int64_t n, double src, int sample, int64_t eidx) {
+    k_ac3d_fused(AcParams P, Ac3In in, StreamIO IO, int64_t n, double src, int64_t eidx) {
+    constexpr bool sample = SAMPLE;
     e_pdl_enter();
     if (halted(P.ctrl, n)) return;
     extern __shared__ __align__(128) unsigned char smem[];
-    const int nx = (int)P.g.nx, nm = (int)P.g.nm, ns = (int)P.p.rows;
-    const int64_t pitch = P.g.pitch, slab = P.g.slab;
+    const int nx = NXC ? NXC : (int)P.g.nx, nm = (int)P.g.nm, ns = (int)P.p.rows;
+    const int64_t pitch = NXC ? NXC : P.g.pitch, slab = (int64_t)nm * pitch;
     const int TM = F3T * ECPT / nx, TPR = nx / ECPT;
     const F3Layout L(smem, TM, pitch);
     const int tid = threadIdx.x, j = tid / TPR, x = (tid % TPR) * ECPT;
@@ -305,7 +308,7 @@ __global__ void __launch_bounds__(F3T, 1)
         mask |= e_nonfinite(acc[7]) << P.rvm.bit;
     }
     record_failure(P.ctrl, n, mask);
-    if (!sample) return;
+    if constexpr (!SAMPLE) return;
     block_partials(e, P.partials);
     __threadfence();
     __syncthreads();
@@ -329,18 +332,34 @@ bool ac3d_fused_eligible(int64_t nx, int64_t nm, int64_t ns, int64_t pitch, int 
     return f3_bytes(nx) <= (size_t)max_smem;
 }
 
+template <int NXC, bool SAMPLE>
+static void f3_attrs(int b) {
+    cudaFuncSetAttribute((void*)k_ac3d_fused<0, NXC, SAMPLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute((void*)k_ac3d_fused<3, NXC, SAMPLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaFuncSetAttribute((void*)k_ac3d_fused<6, NXC, SAMPLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+}
+
 cudaError_t ac3d_fused_prepare(int64_t nx) {
     const int b = (int)f3_bytes(nx);
-    cudaFuncSetAttribute((void*)k_ac3d_fused<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    cudaFuncSetAttribute((void*)k_ac3d_fused<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    cudaFuncSetAttribute((void*)k_ac3d_fused<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    f3_attrs<0, false>(b);
+    f3_attrs<0, true>(b);
+    f3_attrs<512, false>(b);
+    f3_attrs<512, true>(b);
     return cudaGetLastError();
+}
+
+template <int NXC, bool SAMPLE>
+static void* f3_fn(int variant) {
+    return variant == 0 ? (void*)k_ac3d_fused<0, NXC, SAMPLE>
+                        : (variant == 3 ? (void*)k_ac3d_fused<3, NXC, SAMPLE> : (void*)k_ac3d_fused<6, NXC, SAMPLE>);
 }
 
 void launch_ac3d_fused(int variant, const AcParams& P, const Ac3In& in, const StreamIO& IO, int nblocks, int64_t n,
                        double src, int sample, int64_t eidx, cudaStream_t st) {
-    void* fn = variant == 0 ? (void*)k_ac3d_fused<0> : (variant == 3 ? (void*)k_ac3d_fused<3> : (void*)k_ac3d_fused<6>);
-    void* args[] = {(void*)&P, (void*)&in, (void*)&IO, (void*)&n, (void*)&src, (void*)&sample, (void*)&eidx};
+    const bool c512 = P.g.nx == 512 && P.g.pitch == 512;
+    void* fn = c512 ? (sample ? f3_fn<512, true>(variant) : f3_fn<512, false>(variant))
+                    : (sample ? f3_fn<0, true>(variant) : f3_fn<0, false>(variant));
+    void* args[] = {(void*)&P, (void*)&in, (void*)&IO, (void*)&n, (void*)&src, (void*)&eidx};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nblocks);
     cfg.blockDim = dim3(F3T);

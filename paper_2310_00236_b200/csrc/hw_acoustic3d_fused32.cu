@@ -235,10 +235,13 @@ static size_t q3_bytes(int64_t nx) {
 }
 
 // RR: the three density planes are constant along x (constant / layered media): no per-cell
-// density code is compiled in
-template <int V, bool RR>
+// density code is compiled in.  NXC: the row width as a compile-time constant (512, BASELINE
+// config 3: every shared-memory and row offset folds into immediates) or 0 (runtime width).
+// SAMPLE: energy sample step (the fp64 energy code and its registers stay out of the other steps).
+template <int V, bool RR, int NXC, bool SAMPLE>
 __global__ void __launch_bounds__(Q3T, 1)
-    k_ac3d_fused32(AcParams P, Ac3In in_, StreamIO IO, int64_t n, double src, int sample, int64_t eidx) {
+    k_ac3d_fused32(AcParams P, Ac3In in_, StreamIO IO, int64_t n, double src, int64_t eidx) {
+    constexpr bool sample = SAMPLE;
     e_pdl_enter();
     if (halted(P.ctrl, n)) return;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -250,8 +253,8 @@ __global__ void __launch_bounds__(Q3T, 1)
     const float* in_rvx = reinterpret_cast<const float*>(in_.rvx);
     const float* in_rvs = reinterpret_cast<const float*>(in_.rvs);
     const float* in_rvm = reinterpret_cast<const float*>(in_.rvm);
-    const int nx = (int)P.g.nx, nm = (int)P.g.nm, ns = (int)P.p.rows;
-    const int64_t pitch = P.g.pitch, slab = P.g.slab;
+    const int nx = NXC ? NXC : (int)P.g.nx, nm = (int)P.g.nm, ns = (int)P.p.rows;
+    const int64_t pitch = NXC ? NXC : P.g.pitch, slab = (int64_t)nm * pitch;
     const int TM = Q3T * Q3C / nx, TPR = nx / Q3C;
     const int tid = threadIdx.x, j = tid / TPR, x = (tid % TPR) * Q3C;
     constexpr bool comp = V != 0;
@@ -474,7 +477,7 @@ __global__ void __launch_bounds__(Q3T, 1)
         mask |= q_nonfinite(acc[7]) << P.rvm.bit;
     }
     record_failure(P.ctrl, n, mask);
-    if (!sample) return;
+    if constexpr (!SAMPLE) return;
     block_partials(e, P.partials);
     __threadfence();
     __syncthreads();
@@ -498,22 +501,40 @@ bool ac3d_fused32_eligible(int64_t nx, int64_t nm, int64_t ns, int64_t pitch, in
     return q3_bytes(nx) <= (size_t)max_smem;
 }
 
+template <int NXC, bool SAMPLE>
+static void q3_attrs(int b) {
+    void* fns[] = {(void*)k_ac3d_fused32<0, false, NXC, SAMPLE>, (void*)k_ac3d_fused32<3, false, NXC, SAMPLE>,
+                   (void*)k_ac3d_fused32<6, false, NXC, SAMPLE>, (void*)k_ac3d_fused32<0, true, NXC, SAMPLE>,
+                   (void*)k_ac3d_fused32<3, true, NXC, SAMPLE>,  (void*)k_ac3d_fused32<6, true, NXC, SAMPLE>};
+    for (void* fn : fns) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+}
+
 cudaError_t ac3d_fused32_prepare(int64_t nx) {
     const int b = (int)q3_bytes(nx);
-    void* fns[] = {(void*)k_ac3d_fused32<0, false>, (void*)k_ac3d_fused32<3, false>, (void*)k_ac3d_fused32<6, false>,
-                   (void*)k_ac3d_fused32<0, true>, (void*)k_ac3d_fused32<3, true>, (void*)k_ac3d_fused32<6, true>};
-    for (void* fn : fns) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    q3_attrs<0, false>(b);
+    q3_attrs<0, true>(b);
+    q3_attrs<512, false>(b);
+    q3_attrs<512, true>(b);
     return cudaGetLastError();
+}
+
+template <int NXC, bool SAMPLE>
+static void* q3_fn(int variant, bool rr) {
+    return rr ? (variant == 0 ? (void*)k_ac3d_fused32<0, true, NXC, SAMPLE>
+                              : (variant == 3 ? (void*)k_ac3d_fused32<3, true, NXC, SAMPLE>
+                                              : (void*)k_ac3d_fused32<6, true, NXC, SAMPLE>))
+              : (variant == 0 ? (void*)k_ac3d_fused32<0, false, NXC, SAMPLE>
+                              : (variant == 3 ? (void*)k_ac3d_fused32<3, false, NXC, SAMPLE>
+                                              : (void*)k_ac3d_fused32<6, false, NXC, SAMPLE>));
 }
 
 void launch_ac3d_fused32(int variant, const AcParams& P, const Ac3In& in, const StreamIO& IO, int nblocks, int64_t n,
                          double src, int sample, int64_t eidx, cudaStream_t st) {
     const bool rr = P.rho_x.sx == 0 && P.rho_s.sx == 0 && P.rho_m.sx == 0;
-    void* fn = rr ? (variant == 0 ? (void*)k_ac3d_fused32<0, true>
-                                  : (variant == 3 ? (void*)k_ac3d_fused32<3, true> : (void*)k_ac3d_fused32<6, true>))
-                  : (variant == 0 ? (void*)k_ac3d_fused32<0, false>
-                                  : (variant == 3 ? (void*)k_ac3d_fused32<3, false> : (void*)k_ac3d_fused32<6, false>));
-    void* args[] = {(void*)&P, (void*)&in, (void*)&IO, (void*)&n, (void*)&src, (void*)&sample, (void*)&eidx};
+    const bool c512 = P.g.nx == 512 && P.g.pitch == 512;
+    void* fn = c512 ? (sample ? q3_fn<512, true>(variant, rr) : q3_fn<512, false>(variant, rr))
+                    : (sample ? q3_fn<0, true>(variant, rr) : q3_fn<0, false>(variant, rr));
+    void* args[] = {(void*)&P, (void*)&in, (void*)&IO, (void*)&n, (void*)&src, (void*)&eidx};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nblocks);
     cfg.blockDim = dim3(Q3T);
