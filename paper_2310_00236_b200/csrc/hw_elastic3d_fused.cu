@@ -342,10 +342,10 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
             x3_issue_b<NX, TM>(S + X::B0, bbar, in.rsxx, in.rsss, in.rsmm, in.rsxs, in.rsxm, in.rsms,
                                (int64_t)wrap(F0 + i - 2) * slab + (int64_t)m0 * NX);
         };
-        if (tid == 0) {
-            issue_tap(0);
-            issue_a(0);
-        }
+        // the TMA requests are issued by lane 0 of warps 1, 2 and 3 (the tap ring, the A slot, the B
+        // slot): one on each of three SM sub-partitions, so no warp carries all of them into the barriers
+        if (tid == 32) issue_tap(0);
+        if (tid == 64) issue_a(0);
         EV<PP> vs_m1, vs_m2;  // v_slow own rows of slabs F-2, F-3 (new)
         float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);  // (stiff, lam, mu) of the stress slab (previous k)
 #pragma unroll 1
@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
             const __half* T0 = S + s0 * SLOT * NX;
             const __half* T1 = S + s1 * SLOT * NX;
             const __half* T2 = S + s2 * SLOT * NX;
-            if (tid == 0 && i + 1 < NI) {  // slot (i+1) % RING held slab F-3: last read in iteration i-1
+            if (tid == 32 && i + 1 < NI) {  // slot (i+1) % RING held slab F-3: last read in iteration i-1
                 fence_proxy_async_smem();
                 issue_tap(i + 1);
             }
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                 }
             }
             __syncthreads();  // velocity tiles of slab F-1 visible; the A slot and tap slot (i+1) % RING are free
-            if (tid == 0 && i + 1 < NI) {
+            if (tid == 64 && i + 1 < NI) {
                 fence_proxy_async_smem();
                 issue_a(i + 1);
             }
@@ -599,7 +599,7 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                 cs = cn;  // moduli of slab k: the next iteration's stress slab
             }
             __syncthreads();  // the previous velocity generation and the B slot are free
-            if (tid == 0 && i + 1 < NI && F + 1 - 2 >= sb && F + 1 - 2 < se) {
+            if (tid == 96 && i + 1 < NI && F + 1 - 2 >= sb && F + 1 - 2 < se) {
                 fence_proxy_async_smem();
                 issue_b(i + 1);
             }
