@@ -160,16 +160,17 @@ __global__ void __launch_bounds__(F3T, 1)
                 a3_rows(L.orvm(os), in.rvm, slab, s, m0 - 1, m0 + TM, nm, pitch, b);
             }
         };
-        if (tid == 0) {
+        // the TMA requests come from lane 0 of warps 1 and 2 (the tap ring, the own ring): two SM
+        // sub-partitions, so no warp carries all of them into the barriers
+        if (tid == 32)
             for (int i = 0; i < FD && i < NI; i++) issue(i);
-            issue_own(0);
-        }
+        if (tid == 64) issue_own(0);
         int rcur = rec_lower(IO.rec, 0, IO.n_rec, sb * nm + m, INT_MIN);  // receivers: key (s nm + m, x)
         E8 qp0, qp1, vsq;  // p rows F-1, F at the thread's cells; v_slow(s-1)
 #pragma unroll 1
         for (int i = 0; i < NI; i++) {
             const int k = (gi0 + i) % FR, kp = (gi0 + i + FR - 1) % FR;
-            if (tid == 0 && i + FD < NI) {
+            if (tid == 32 && i + FD < NI) {
                 fence_proxy_async_smem();
                 issue(i + FD);
             }
@@ -187,7 +188,7 @@ __global__ void __launch_bounds__(F3T, 1)
             qp1 = e_ld8(L.sl(k) + (int64_t)(j + 1) * pitch + x);
             if (i > 0) {
                 const int s = F0 + i - 1, kr = i - 1, os = (gk0 + kr) & 1;
-                if (tid == 0 && s + 1 < se) {  // that own slot was last read before the previous barrier
+                if (tid == 64 && s + 1 < se) {  // that own slot was last read before the previous barrier
                     fence_proxy_async_smem();
                     issue_own(kr + 1);
                 }
