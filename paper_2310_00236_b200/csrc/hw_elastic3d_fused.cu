@@ -639,18 +639,28 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
 }
 
 // Plane totals of a generic energy launch (k_el_energy: one block partial per (x chunk, mid
-// row, slab), slab-major): T[s] = sum_c (sum_b partial[s][b][c]) -- the same fixed order per
-// slab whatever the decomposition (E(0) of the one-pass kernel's runs).
-__global__ void k_plane_totals(const double* partials, int64_t blocks_per_plane, int64_t nplanes, double* out) {
-    const int64_t sp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (sp >= nplanes) return;
+// row, slab), slab-major): T[s] = sum_c (sum_b partial[s][b][c]) with every order fixed -- per
+// component a thread-strided sum, a warp tree and the warps in order -- so the same for any
+// decomposition (E(0) of the one-pass kernel's runs).  One CTA of 256 threads per slab.
+__global__ void __launch_bounds__(256) k_plane_totals(const double* partials, int64_t blocks_per_plane, double* out) {
+    __shared__ double red[8];
+    const int64_t sp = blockIdx.x;
+    const int tid = threadIdx.x;
     double t = 0.0;
     for (int c = 0; c < NCOMP; c++) {
-        double a = partials[(sp * blocks_per_plane) * NCOMP + c];
-        for (int64_t b = 1; b < blocks_per_plane; b++) a += partials[(sp * blocks_per_plane + b) * NCOMP + c];
-        t += a;
+        double a = 0.0;
+        for (int64_t b = tid; b < blocks_per_plane; b += 256) a += partials[(sp * blocks_per_plane + b) * NCOMP + c];
+        a = warp_sum(a);
+        if ((tid & 31) == 0) red[tid >> 5] = a;
+        __syncthreads();
+        if (tid == 0) {
+            double w = red[0];
+            for (int k = 1; k < 8; k++) w += red[k];
+            t += w;
+        }
+        __syncthreads();
     }
-    out[sp] = t;
+    if (tid == 0) out[sp] = t;
 }
 
 // Medium coefficient table of the one-pass kernel: per (slab, mid row) -- one row per slab
@@ -741,7 +751,7 @@ cudaError_t el3d_fused_coef(const ElParams& P, float* out, int64_t s0, int64_t n
 
 void launch_plane_totals(const double* partials, int64_t blocks_per_plane, int64_t nplanes, double* out,
                          cudaStream_t st) {
-    k_plane_totals<<<(unsigned)((nplanes + 127) / 128), 128, 0, st>>>(partials, blocks_per_plane, nplanes, out);
+    k_plane_totals<<<(unsigned)nplanes, 256, 0, st>>>(partials, blocks_per_plane, out);
 }
 
 template <int NX>
