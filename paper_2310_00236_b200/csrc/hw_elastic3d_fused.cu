@@ -155,18 +155,17 @@ __device__ __forceinline__ void add_srcv(EH2 r[P], int sj, int sln, __half srch)
 
 // store of the thread's cells of slab s at element offset so = s * slab + goff; the periodic
 // ghost slabs are written through on the first / last G slabs only (CTA-uniform branch)
+// (every field of the one-pass kernel has the same ghost policy: write-through periodic copies on a
+// single domain, none on a slab; `gw` = a CTA-uniform "this slab is one of the first / last G and the
+// ghosts are written through", evaluated once per phase)
 template <int P>
-__device__ __forceinline__ void ghost_st(__half* b, int64_t up, int64_t dn, EV<P> v) {
-    if (up) stv<P>(b + up, v);
-    if (dn) stv<P>(b + dn, v);
-}
-template <int P>
-__device__ __forceinline__ void gst(const FieldView& f, int64_t so, bool edge, int s, int64_t slab, const EV<P>& v) {
+__device__ __forceinline__ void gst(const FieldView& f, int64_t so, bool gw, int s, int ns, int64_t slab,
+                                    const EV<P>& v) {
     __half* b = reinterpret_cast<__half*>(f.base) + so;
     stv<P>(b, v);
-    if (edge && f.gtop == GHOST_PERIODIC) {
-        const int nr = (int)f.rows;
-        ghost_st<P>(b, s >= nr - G ? -(int64_t)nr * slab : 0, s < G ? (int64_t)nr * slab : 0, v);
+    if (gw) {
+        if (s >= ns - G) stv<P>(b - (int64_t)ns * slab, v);
+        if (s < G) stv<P>(b + (int64_t)ns * slab, v);
     }
 }
 
@@ -418,17 +417,17 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                 const int sk = F - 1;  // unwrapped: stored only inside the segment
                 if (sk >= sb && sk < se) {
                     const int64_t so = (int64_t)k * slab + goff;
-                    const bool edge = k < G || k >= ns - G;
-                    gst<PP>(P.vx, so, edge, k, slab, vx);
-                    gst<PP>(P.vs, so, edge, k, slab, vsv);
-                    gst<PP>(P.vm, so, edge, k, slab, vm);
+                    const bool gw = !slabm && (k < G || k >= ns - G);
+                    gst<PP>(P.vx, so, gw, k, ns, slab, vx);
+                    gst<PP>(P.vs, so, gw, k, ns, slab, vsv);
+                    gst<PP>(P.vm, so, gw, k, ns, slab, vm);
                     trackv<PP>(acc[0], vx);
                     trackv<PP>(acc[1], vsv);
                     trackv<PP>(acc[2], vm);
                     if (comp) {
-                        gst<PP>(P.rvx, so, edge, k, slab, rvx);
-                        gst<PP>(P.rvs, so, edge, k, slab, rvs);
-                        gst<PP>(P.rvm, so, edge, k, slab, rvm);
+                        gst<PP>(P.rvx, so, gw, k, ns, slab, rvx);
+                        gst<PP>(P.rvs, so, gw, k, ns, slab, rvs);
+                        gst<PP>(P.rvm, so, gw, k, ns, slab, rvm);
                     }
                 }
                 // halo rows (recomputed, not stored): j = 0 -> vm(m0-1), j = 1 -> vx(m0+TM), j = 2 -> vs(m0+TM)
@@ -530,12 +529,12 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                     e2_finish_nd<V>(EO2::mul(mu, EO2::add(sms_a.q[h], sms_b.q[h])), dt2, -1, srch, nw[5].q[h], rr[5].q[h]);
                 }
                 const int64_t so = (int64_t)s * slab + goff;
-                const bool edge = s < G || s >= ns - G;
+                const bool gw = !slabm && (s < G || s >= ns - G);
 #pragma unroll
                 for (int q = 0; q < 6; q++) {
-                    gst<PP>(*OS[q], so, edge, s, slab, nw[q]);
+                    gst<PP>(*OS[q], so, gw, s, ns, slab, nw[q]);
                     trackv<PP>(acc[3 + q], nw[q]);
-                    if (comp) gst<PP>(*ORS[q], so, edge, s, slab, rr[q]);
+                    if (comp) gst<PP>(*ORS[q], so, gw, s, ns, slab, rr[q]);
                 }
                 if (sample) {  // diagnostics.py:100-162, 3D compliance form (k_el_stress)
                     double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};  // this (tile, slab) unit's share
