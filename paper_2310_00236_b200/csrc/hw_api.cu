@@ -114,6 +114,7 @@ LaneConsts make_consts(const double taps[4], double dt_u) {
 // internal field ids (generic axes) and their staggers (half_x, half_m, half_s)
 enum { F_P, F_VX, F_VS, F_VM, F_SXX, F_SSS, F_SMM, F_SXS, F_SXM, F_SMS, F_N };
 const int HALF_S[F_N] = {0, 0, 1, 0, 0, 0, 0, 1, 0, 1};
+constexpr int EL3_EDGE = 2;  // edge slabs per side of an overlapped one-pass 3D elastic slab step
 
 const int EXT_AC2[] = {F_P, F_VX, F_VS};
 const int EXT_AC3[] = {F_P, F_VX, F_VM, F_VS};
@@ -406,6 +407,7 @@ struct hw_solver {
     int el3_group = 1;          // its CTA groups of adjacent tiles (hw_elastic3d_fused.cu)
     double* el3_ecoef = nullptr;  // its per-slab energy coefficients (slow-layered media; in plane_mem)
     bool el3_slab = false;        // ... on a slab of a decomposed domain (ghosts from HW_PLAN_FUSED_EL3)
+    int el3_nb_edge = 0, el3_nb_int = 0;  // ... NCCL slab: CTAs of the edge / interior launches (overlap)
     double* el3_eplane = nullptr; // ... energy partials per (slab, tile) unit (in plane_mem)
     double* el3_etot = nullptr;   // ... energy plane totals per sample
     int64_t el3_etot_cap = 0;
@@ -855,6 +857,23 @@ int setup_handle(hw_solver* h) {
                     break;
                 }
             h->fused_el3 = true;
+            // NCCL slab: edge slabs (every row the exchange sends) + the exchange on st, the interior
+            // slabs on st2; CTAs split so both launches take about as long (an edge segment of
+            // 2 slabs costs ~3 slabs: the ring fill)
+            if (h->transport == 2 && max_rows >= 5 * EL3_EDGE) {
+                CU(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
+                for (int k = 0; k < 2; k++) {
+                    CU(cudaEventCreateWithFlags(&h->ev_edge[k], cudaEventDisableTiming));
+                    CU(cudaEventCreateWithFlags(&h->ev_int[k], cudaEventDisableTiming));
+                }
+                const double we = 3.0 * 2 * EL3_EDGE, wi = (double)(max_rows - 2 * EL3_EDGE);
+                int ne = (int)(nsm * we / (we + wi) + 0.5);
+                ne = ne < 1 ? 1 : (ne > nsm - 1 ? nsm - 1 : ne);
+                int ni = nsm - ne;
+                if (ni % h->el3_group) ni -= ni % h->el3_group;
+                h->el3_nb_edge = ne;
+                h->el3_nb_int = ni;
+            }
         }
         if (want && !h->fused_el3 && !h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
             el3d_stream_eligible(desc->nx, desc->nm, h->g.pitch, dev_smem)) {
@@ -1515,6 +1534,10 @@ static void fused_el3_bufs(const hw_solver* h, int cur, ElParams& P, El3In& in) 
     in.slab = h->el3_slab ? 1 : 0;
     in.vsrc = 0;
     in.vsrc_s = 0;
+    in.band = 0;
+    in.edge = 0;
+    in.nb_total = 0;
+    in.pad2 = 0;
     if (h->d.src_kind == HW_SRC_VSLOW) {  // this slab also computes the halo velocity rows -1 and L
         const int64_t r = h->d.src_s - h->r0;
         if (r >= -1 && r <= h->ns_loc) {
@@ -1622,6 +1645,43 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
             h->launches++;
             cur ^= 1;
         }
+    } else if (h->fused_el3 && h->transport == 2 && h->st2) {
+        // NCCL slab, overlapped (as the fused 2D kernel):
+        //   st : wait interior(n-1) | edge slabs(n) | record E(n) | exchange(n)
+        //   st2: wait edge(n-1)     | interior slabs(n) | [wait E(n) | traces] | record I(n)
+        const StreamIO IO = stream_io(h, C);
+        CU(cudaEventRecord(h->ev_edge[1], h->st));  // st2 starts after everything queued on st
+        int cur = 0;
+        for (int64_t n = 0; n < nt; n++) {
+            ElParams P = C.L;
+            El3In in;
+            fused_el3_bufs(h, cur, P, in);
+            in.edge = EL3_EDGE;
+            in.nb_total = h->el3_nb_edge + h->el3_nb_int;
+            El3In ie = in, ii = in;
+            ie.band = 1;
+            ie.group = 1;
+            ii.band = 2;
+            const int sample = energy && ((n + 1) % C.every == 0);
+            const double sv = src ? src[n] : 0.0;
+            if (n > 0) CU(cudaStreamWaitEvent(h->st, h->ev_int[(n - 1) & 1], 0));
+            launch_el3d_fused(variant, P, ie, IO, h->el3_nb_edge, n, sv, sample, (n + 1) / C.every, h->st);
+            CU(cudaEventRecord(h->ev_edge[n & 1], h->st));
+            CU(cudaStreamWaitEvent(h->st2, h->ev_edge[(n + 1) & 1], 0));  // edge(n-1), or the start
+            launch_el3d_fused(variant, P, ii, IO, h->el3_nb_int, n, sv, sample, (n + 1) / C.every, h->st2);
+            h->launches += 2;
+            if (C.E.n_rec > 0) {  // traces after the step (both bands done), on st2: the exchange goes on
+                CU(cudaStreamWaitEvent(h->st2, h->ev_edge[n & 1], 0));
+                EpParams E = C.E;
+                E.trace_base = P.vs.base;
+                launch_epilogue(h->LU, E, n, 0, 0, h->st2);
+                h->launches++;
+            }
+            CU(cudaEventRecord(h->ev_int[n & 1], h->st2));
+            cur ^= 1;
+            if ((rc = exchange_nccl_plan(h, HW_PLAN_FUSED_EL3, cur))) return rc;
+        }
+        if (nt > 0) CU(cudaStreamWaitEvent(h->st, h->ev_int[(nt - 1) & 1], 0));
     } else if (h->fused_el3) {  // one-pass 3D elastic kernel, ping-pong A <-> B; traces from the epilogue
         const StreamIO IO = stream_io(h, C);
         int cur = 0;

@@ -311,16 +311,25 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
     // range side by side, so the halo rows one CTA reads are the rows its neighbour in the
     // group reads (or wrote) at about the same time: L2 hits instead of DRAM re-reads.  The
     // group's (tile group, slab) units are split evenly over the groups.
+    // Band mode (slab of a decomposed domain, exchange overlapped): 1 = the edge slabs [0, E) and
+    // [ns-E, ns) -- every row the halo exchange sends --, 2 = the interior [E, ns-E) (reads no ghost
+    // row), 0 = every slab.  t indexes the band's slabs; segments never straddle the two edge runs.
+    const int E = in.edge, bm = in.band;
+    const int nsl = bm == 0 ? ns : (bm == 1 ? 2 * E : ns - 2 * E);
+    auto slab_of = [&](int t) { return bm == 0 ? t : (bm == 1 ? (t < E ? t : ns - 2 * E + t) : E + t); };
     const int grp = in.group, ngrp = (int)gridDim.x / grp, gid = (int)blockIdx.x / grp, gr = (int)blockIdx.x % grp;
     const int tiles = nm / TM / grp;  // tile groups
-    const int64_t U = (int64_t)tiles * ns;
+    const int64_t U = (int64_t)tiles * nsl;
     int64_t u = (int64_t)gid * U / ngrp;
     const int64_t u1 = (int64_t)(gid + 1) * U / ngrp;
     int gi = 0, ga = 0, gb = 0;  // running use counters of the tap slots, the A and the B slot
     while (u < u1) {
-        const int tile = (int)(u / ns) * grp + gr, sb = (int)(u % ns);
-        const int se = (int)min((int64_t)ns, sb + (u1 - u));
-        u += se - sb;
+        const int t0 = (int)(u % nsl);
+        int te = (int)min((int64_t)nsl, t0 + (u1 - u));
+        if (bm == 1 && t0 < E) te = min(te, E);
+        const int tile = (int)(u / nsl) * grp + gr, sb = slab_of(t0);
+        const int se = sb + (te - t0);
+        u += te - t0;
         const int m0 = tile * TM, m = m0 + j;
         const int mlo = m0 == 0 ? nm - 1 : m0 - 1, mhi = m0 + TM == nm ? 0 : m0 + TM;  // halo rows (periodic)
         const int mh = j == 0 ? mlo : mhi;            // this thread row's halo row (j < 3)
@@ -623,7 +632,9 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
     __threadfence();
     __syncthreads();
     __shared__ unsigned int is_last;
-    if (tid == 0) is_last = atomicAdd(IO.counter, 1u) == (unsigned int)(gridDim.x - 1);
+    // (edge + interior launches of one step share the counter: in.nb_total CTAs in all)
+    const unsigned int nbt = in.nb_total > 0 ? (unsigned int)in.nb_total : gridDim.x;
+    if (tid == 0) is_last = atomicAdd(IO.counter, 1u) == nbt - 1;
     __syncthreads();
     if (!is_last) return;
     // plane totals T[s] = sum_tile partial[s][tile], tiles in order: the host sums the planes of all

@@ -136,6 +136,9 @@ struct El3In {
     int32_t slab;        // slab of a decomposed domain (ghost rows from the halo exchange), else 0
     int32_t vsrc;        // a v_slow point source whose row vsrc_s (local, -1 .. ns) this slab computes
     int64_t vsrc_s;
+    int32_t band, edge;  // band mode (0 all slabs, 1 edge slabs [0,edge) + [ns-edge,ns), 2 interior)
+    int32_t nb_total;    // CTAs of all launches of one step (edge + interior; 0 = this grid)
+    int32_t pad2;
 };
 bool el3d_fused_eligible(const ElParams& P, int64_t nx, int64_t nm, int64_t ns, int64_t pitch, int order,
                          int max_smem);

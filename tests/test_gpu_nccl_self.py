@@ -112,3 +112,19 @@ def test_nccl_transport_device_resident_run(one_rank_job):
     assert ms > 0 and b.transport() == 2 and b.kernel_path() == "fused2d"
     for n in a.FIELDS:
         assert_same_bits(getattr(sb, n).values, getattr(sa, n).values, n)
+
+
+def test_nccl_el3_overlapped_device_resident_run(one_rank_job):
+    """Config 5's one-pass kernel on the NCCL transport, overlapped: per step the edge slabs and the
+    exchange on one stream, the interior slabs on another (run_device), equals the single process."""
+    from test_gpu_el3_slabs import _el3
+
+    a, sa = _el3(1, nt=11)
+    a.run(hw.Variant.OP6, sa)
+    b, sb = _el3(1, nt=11, distributed=True)
+    b.upload(sb)
+    ms = b.run_device(hw.Variant.OP6, 0, b.grid.nt)
+    b.download(sb)
+    assert ms > 0 and b.transport() == 2 and b.kernel_path() == "fused3d-el"
+    for n in a.FIELDS:
+        assert_same_bits(getattr(sb, n).values, getattr(sa, n).values, n)
