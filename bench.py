@@ -80,7 +80,7 @@ def init_config5(st):
         np.float16)
 
 
-def make_config2(hw, nt=5000):
+def make_config2(hw, nt=5000, distributed=False):
     n = 4096
     dx = 1.0 / n
     med = hw.build_layered_acoustic(n, n, [(0.5, 1.0, 1.0), (1.0, 1.5, 2.25)])
@@ -90,7 +90,7 @@ def make_config2(hw, nt=5000):
         dt = float(np.nextafter(np.float16(dt), np.float16(0)))
     src = hw.SourceSpec(hw.SourceKind.PRESSURE_POINT, n // 2, 8, hw.RickerSpec(f_center=1 / (10 * dx), amplitude=2.0e4))
     return hw.AcousticSolver(hw.GridSpec(n, n, dx, dt, nt), med, src, stencil_precision=hw.Precision.FP16,
-                             receivers=((n // 2, n // 4),), energy_every=10)
+                             receivers=((n // 2, n // 4),), energy_every=10, distributed=distributed)
 
 
 def smooth_velocity(n, seed=3, sigma=8.0):
