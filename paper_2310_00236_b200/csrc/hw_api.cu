@@ -1371,9 +1371,11 @@ static int run_begin(hw_solver* h, int32_t variant, int64_t nt, bool energy, boo
     if (energy) {  // E(t=0) pairs the state with itself
         if (h->ac) launch_ac_energy(h->LU, h->W, C.A, h->max_rows, h->st);
         else launch_el_energy(h->LU, h->W, C.L, h->max_rows, h->st);
-        launch_epilogue(h->LU, C.E, -1, 1, 0, h->st);
-        h->launches += 2;
-        if (h->fused_el3) {  // ... and its per-slab totals (one block partial per (x chunk, mid row, slab))
+        h->launches++;
+        if (!h->fused_el3) {
+            launch_epilogue(h->LU, C.E, -1, 1, 0, h->st);
+            h->launches++;
+        } else {  // ... and its per-slab totals (one block partial per (x chunk, mid row, slab))
             const dim3 gr = grid3(h->g, h->W, h->max_rows);
             launch_plane_totals(h->partials, (int64_t)gr.x * gr.y, h->max_rows, h->el3_etot, h->st);
             h->launches++;

@@ -153,20 +153,12 @@ __device__ __forceinline__ void add_srcv(EH2 r[P], int sj, int sln, __half srch)
         }
 }
 
-// store of the thread's cells of slab s at element offset so = s * slab + goff; the periodic
-// ghost slabs are written through on the first / last G slabs only (CTA-uniform branch)
-// (every field of the one-pass kernel has the same ghost policy: write-through periodic copies on a
-// single domain, none on a slab; `gw` = a CTA-uniform "this slab is one of the first / last G and the
-// ghosts are written through", evaluated once per phase)
+// store of the thread's cells of slab s at element offset so = s * slab + goff.  No ghost rows: the
+// kernel never reads them on a single domain (its slab indices wrap) and a slab's come from the halo
+// exchange, so the write-through copies of the phase kernels are not needed here.
 template <int P>
-__device__ __forceinline__ void gst(const FieldView& f, int64_t so, bool gw, int s, int ns, int64_t slab,
-                                    const EV<P>& v) {
-    __half* b = reinterpret_cast<__half*>(f.base) + so;
-    stv<P>(b, v);
-    if (gw) {
-        if (s >= ns - G) stv<P>(b - (int64_t)ns * slab, v);
-        if (s < G) stv<P>(b + (int64_t)ns * slab, v);
-    }
+__device__ __forceinline__ void gst(const FieldView& f, int64_t so, const EV<P>& v) {
+    stv<P>(reinterpret_cast<__half*>(f.base) + so, v);
 }
 
 // binary16 -> binary64, one conversion (exact)
@@ -426,17 +418,16 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                 const int sk = F - 1;  // unwrapped: stored only inside the segment
                 if (sk >= sb && sk < se) {
                     const int64_t so = (int64_t)k * slab + goff;
-                    const bool gw = !slabm && (k < G || k >= ns - G);
-                    gst<PP>(P.vx, so, gw, k, ns, slab, vx);
-                    gst<PP>(P.vs, so, gw, k, ns, slab, vsv);
-                    gst<PP>(P.vm, so, gw, k, ns, slab, vm);
+                    gst<PP>(P.vx, so, vx);
+                    gst<PP>(P.vs, so, vsv);
+                    gst<PP>(P.vm, so, vm);
                     trackv<PP>(acc[0], vx);
                     trackv<PP>(acc[1], vsv);
                     trackv<PP>(acc[2], vm);
                     if (comp) {
-                        gst<PP>(P.rvx, so, gw, k, ns, slab, rvx);
-                        gst<PP>(P.rvs, so, gw, k, ns, slab, rvs);
-                        gst<PP>(P.rvm, so, gw, k, ns, slab, rvm);
+                        gst<PP>(P.rvx, so, rvx);
+                        gst<PP>(P.rvs, so, rvs);
+                        gst<PP>(P.rvm, so, rvm);
                     }
                 }
                 // halo rows (recomputed, not stored): j = 0 -> vm(m0-1), j = 1 -> vx(m0+TM), j = 2 -> vs(m0+TM)
@@ -538,12 +529,11 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                     e2_finish_nd<V>(EO2::mul(mu, EO2::add(sms_a.q[h], sms_b.q[h])), dt2, -1, srch, nw[5].q[h], rr[5].q[h]);
                 }
                 const int64_t so = (int64_t)s * slab + goff;
-                const bool gw = !slabm && (s < G || s >= ns - G);
 #pragma unroll
                 for (int q = 0; q < 6; q++) {
-                    gst<PP>(*OS[q], so, gw, s, ns, slab, nw[q]);
+                    gst<PP>(*OS[q], so, nw[q]);
                     trackv<PP>(acc[3 + q], nw[q]);
-                    if (comp) gst<PP>(*ORS[q], so, gw, s, ns, slab, rr[q]);
+                    if (comp) gst<PP>(*ORS[q], so, rr[q]);
                 }
                 if (sample) {  // diagnostics.py:100-162, 3D compliance form (k_el_stress)
                     double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};  // this (tile, slab) unit's share
