@@ -553,7 +553,13 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                             sx1 += xn * x1;
                             sdot += xn * x1 + sn * s1 + mn * m1;
                             str += (xn + sn + mn) * (x1 + s1 + m1);
-                            ssh += g(old[3]) * g(nw[3]) + g(old[4]) * g(nw[4]) + g(old[5]) * g(nw[5]);
+                            // shear: products of binary16 pairs are exact in binary32 (22-bit significands,
+                            // no underflow), so each product takes one conversion instead of two
+                            auto hp = [&](int w) {
+                                const __half a1 = old[w].q[q >> 1].e[q & 1], b1 = nw[w].q[q >> 1].e[q & 1];
+                                return (double)__fmul_rn(__half2float(a1), __half2float(b1));
+                            };
+                            ssh += (hp(3) + hp(4)) + hp(5);
                         }
                         // rho_x, rho_s, rho_m, 1/(lam+mu) [mu = 0], 1/(2 mu), lam/(2 mu (3 lam + 2 mu)), 1/mu_n
                         const double* ec = in.ecoef + 8 * (int64_t)s;
