@@ -143,8 +143,9 @@ __global__ void __launch_bounds__(F3T, 1)
             mbar_arrive_expect_tx(&L.bar[k], (uint32_t)(L.slot * sizeof(__half)));
             a3_rows(L.sl(k), in.p, slab, e_row(F), m0 - 1, m0 + TM + 1, nm, pitch, &L.bar[k]);
         };
-        auto issue_own = [&](int kk) {  // slab sb - 1 + kk (periodic: slab -1 is ns - 1; residuals have no ghosts)
-            const int os = (gk0 + kk) & 1, s = sb - 1 + kk < 0 ? ns - 1 : sb - 1 + kk;
+        auto issue_own = [&](int kk) {  // slab sb - 1 + kk (periodic: slab -1 is ns - 1, residuals have no ghosts;
+                                        // a decomposed domain's slab: ghost row -1 from the exchange)
+            const int os = (gk0 + kk) & 1, s = sb - 1 + kk < 0 ? (in.slab ? -1 : ns - 1) : sb - 1 + kk;
             const int64_t off = (int64_t)s * slab + (int64_t)m0 * pitch;
             uint64_t* b = &L.obar[os];
             mbar_arrive_expect_tx(b, own_tx);
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(F3T, 1)
                 issue(i + FD);
             }
             // row-uniform reciprocals of slab s = F - 1, loaded before the waits (latency off the chain)
-            const int sw = F0 + i - 1 < 0 ? ns - 1 : F0 + i - 1;  // periodic: v_slow(-1) is row ns - 1's medium
+            const int sw = F0 + i - 1 < 0 ? (in.slab ? -1 : ns - 1) : F0 + i - 1;  // v_slow(-1): row ns-1's medium (periodic) or the slab's halo row
             float rcx = 0.f, rcs = 0.f, rcm = 0.f, rch = 0.f;
             if (rm && i > 0) {
                 rcs = e_rcp_at(P.rho_s, sw, m);

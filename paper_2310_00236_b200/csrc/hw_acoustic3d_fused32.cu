@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(Q3T, 1)
             q_rows(sl(k), in_p, slab, e_row(F), m0 - 1, m0 + TM + 1, nm, pitch, &bar[k]);
         };
         auto issue_own = [&](int kk) {  // slab sb - 1 + kk (periodic: slab -1 is ns - 1)
-            const int os = (gk0 + kk) & 1, s = sb - 1 + kk < 0 ? ns - 1 : sb - 1 + kk;
+            const int os = (gk0 + kk) & 1, s = sb - 1 + kk < 0 ? (in_.slab ? -1 : ns - 1) : sb - 1 + kk;
             const int64_t off = (int64_t)s * slab + (int64_t)m0 * pitch;
             uint64_t* b = &obar[os];
             mbar_arrive_expect_tx(b, own_tx);
@@ -345,11 +345,11 @@ __global__ void __launch_bounds__(Q3T, 1)
                 fence_proxy_async_smem();
                 issue(i + QD);
             }
-            const int sw = F0 + i - 1 < 0 ? ns - 1 : F0 + i - 1;  // periodic: v_slow(-1) is row ns - 1's medium
+            const int sw = F0 + i - 1 < 0 ? (in_.slab ? -1 : ns - 1) : F0 + i - 1;  // v_slow(-1): row ns-1's medium (periodic) or the slab's halo row
             // row divisors: threads 0-3 stage those of the next iteration's slab (F0 + i) in shared memory
             // (constant / slow-layered planes depend on the slab only; the barriers below order the use)
             if (tid < 4 && i + 1 < NI) {
-                const int sn = F0 + i < 0 ? ns - 1 : F0 + i;
+                const int sn = F0 + i < 0 ? (in_.slab ? -1 : ns - 1) : F0 + i;
                 const PlaneView& pv = tid == 0 ? P.rho_s : (tid == 1 ? P.rho_x : (tid == 2 ? P.rho_m : P.beta));
                 qdiv[((i + 1) & 1) * 4 + tid] = q_pack(q_rowdiv(pv, sn, 0));
             }

@@ -773,11 +773,11 @@ int setup_handle(hw_solver* h) {
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
             h->el_stream = true;
         }
-        // one-pass 3D acoustic step (2nd order, single domain): ping-pong partner buffers
+        // one-pass 3D acoustic step (2nd order; a single domain or a slab of a decomposed one, whose
+        // ghost rows p(-1), p(L), v_slow(-1) come from HW_PLAN_FUSED_AC3 once per step): ping-pong buffers
         const bool f3_ok = opt("fused3") == 1;
-        if (want && f3_ok && h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
-            h->world == 1 && h->transport == 0 &&
-            ac3d_fused_eligible(desc->nx, desc->nm, desc->ns, h->g.pitch, desc->order, dev_smem)) {
+        if (want && f3_ok && h->ac && h->d3 && h->LS == 16 && h->LU == 16 && !h->fs &&
+            ac3d_fused_eligible(desc->nx, desc->nm, field_rows(h, F_P), h->g.pitch, desc->order, dev_smem)) {
             for (int j = 0; j < 2 * h->nsol; j++) {
                 int f = h->ext[j % h->nsol];
                 size_t bytes = (size_t)(field_rows(h, f) + 2 * G) * h->g.slab * esz;
@@ -792,9 +792,8 @@ int setup_handle(hw_solver* h) {
             h->fused3 = true;
         }
         // the one-pass 3D acoustic step in binary32 lanes (BASELINE config 3's fp32 arm)
-        if (want && f3_ok && h->ac && h->d3 && h->LS == 32 && h->LU == 32 &&
-            h->world == 1 && h->transport == 0 &&
-            ac3d_fused32_eligible(desc->nx, desc->nm, desc->ns, h->g.pitch, desc->order, dev_smem)) {
+        if (want && f3_ok && h->ac && h->d3 && h->LS == 32 && h->LU == 32 && !h->fs &&
+            ac3d_fused32_eligible(desc->nx, desc->nm, field_rows(h, F_P), h->g.pitch, desc->order, dev_smem)) {
             for (int j = 0; j < 2 * h->nsol; j++) {
                 int f = h->ext[j % h->nsol];
                 size_t bytes = (size_t)(field_rows(h, f) + 2 * G) * h->g.slab * esz;
@@ -1008,6 +1007,13 @@ std::vector<hw_xfer> halo_plan(const PlanGeom& g, int kind) {
     if (kind == HW_PLAN_FUSED) {
         js = {0, 2, 5};  // p, vy, rvy of p vx vy rp rvx rvy
         depth = G;
+    } else if (kind == HW_PLAN_FUSED_AC3) {
+        // one-pass 3D acoustic slab: p rows -1 and L, v_slow and its residual row -1 (1 row each way)
+        for (int j = 0; j < g.nsol; j++)
+            if (g.ext[j] == F_P || g.ext[j] == F_VS) js.push_back(j);
+        for (int j = 0; j < g.nsol; j++)
+            if (g.ext[j] == F_VS) js.push_back(g.nsol + j);
+        depth = 1;
     } else if (kind == HW_PLAN_FUSED_EL3) {
         // one-pass 3D elastic slab (hw_elastic3d_fused.cu): its halo velocities v(-1), v(L) are
         // recomputed from stress rows -2 .. L and the old velocities / residuals of rows -1, L
@@ -1042,7 +1048,7 @@ std::vector<hw_xfer> halo_plan(const PlanGeom& g, int kind) {
 char* plan_row(const hw_solver* h, int kind, int buf, int j, int64_t row) {
     const size_t rb = (size_t)h->g.slab * lane_bytes(h->LU);
     char* base;
-    if (kind == HW_PLAN_FUSED || kind == HW_PLAN_FUSED_EL3) base = (char*)(buf ? h->mem_b[j] : h->mem[j]) + G * rb;
+    if (kind >= HW_PLAN_FUSED) base = (char*)(buf ? h->mem_b[j] : h->mem[j]) + G * rb;  // ping-pong buffers
     else base = (char*)(j < h->nsol ? h->fv : h->rv)[h->ext[j % h->nsol]].base;
     return base + row * (int64_t)rb;
 }
@@ -1485,6 +1491,8 @@ static void fused3_bufs(const hw_solver* h, int cur, AcParams& P, Ac3In& in) {
     }
     in.p = src[F_P]; in.vx = src[F_VX]; in.vs = src[F_VS]; in.vm = src[F_VM];
     in.rp = src[F_N + F_P]; in.rvx = src[F_N + F_VX]; in.rvs = src[F_N + F_VS]; in.rvm = src[F_N + F_VM];
+    in.slab = (h->world > 1 || h->transport != 0) ? 1 : 0;
+    in.pad = 0;
 }
 
 // The same for the one-pass 2D elastic kernel (external order vx vy sxx syy sxy + residuals).
@@ -1564,8 +1572,9 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
     int rc = run_begin(h, variant, nt, energy, true, C);
     if (rc) return rc;
     const bool fused_slab = h->fused && h->transport == 2;
-    if (fused_slab || (h->fused_el3 && h->transport == 2)) {  // halos of the uploaded state
-        if ((rc = exchange_nccl_plan(h, fused_slab ? HW_PLAN_FUSED : HW_PLAN_FUSED_EL3, 0))) return rc;
+    if (fused_slab || (h->transport == 2 && (h->fused_el3 || h->fused3 || h->fused3_32))) {  // halos of the upload
+        const int kind = fused_slab ? HW_PLAN_FUSED : (h->fused_el3 ? HW_PLAN_FUSED_EL3 : HW_PLAN_FUSED_AC3);
+        if ((rc = exchange_nccl_plan(h, kind, 0))) return rc;
     } else if ((rc = exchange(h, 0)) || (rc = exchange(h, 1))) {
         return rc;
     }
@@ -1646,6 +1655,7 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
             else launch_ac3d_fused(variant, P, in, IO, h->stream_blocks, n, sv, sample, (n + 1) / C.every, h->st);
             h->launches++;
             cur ^= 1;
+            if (h->transport == 2 && (rc = exchange_nccl_plan(h, HW_PLAN_FUSED_AC3, cur))) return rc;
         }
     } else if (h->fused_el3 && h->transport == 2 && h->st2) {
         // NCCL slab, overlapped (as the fused 2D kernel):
@@ -1959,6 +1969,27 @@ int hw_run_group(hw_solver* const* hs, int32_t nslabs, int32_t variant, int64_t 
             cur ^= 1;
             if ((rc = exchange_group_plan(grp, HW_PLAN_FUSED, cur))) return rc;
         }
+    } else if (grp->ranks[0]->fused3 || grp->ranks[0]->fused3_32) {  // one-pass 3D acoustic slabs
+        if ((rc = exchange_group_plan(grp, HW_PLAN_FUSED_AC3, 0))) return rc;  // halos of the uploaded state
+        int cur = 0;
+        for (int64_t n = 0; n < nt; n++) {
+            for (hw_solver* h : grp->ranks) {
+                cudaSetDevice(h->d.device);
+                RunCtx& Cr = C[h->rank];
+                AcParams P = Cr.A;
+                Ac3In in;
+                fused3_bufs(h, cur, P, in);
+                const int sample = energy && ((n + 1) % Cr.every == 0);
+                const double sv = (src_samples && h->d.src_kind == HW_SRC_PRESSURE) ? src_samples[n] : 0.0;
+                if (h->fused3_32)
+                    launch_ac3d_fused32(variant, P, in, stream_io(h, Cr), h->stream_blocks, n, sv, sample, (n + 1) / Cr.every, h->st);
+                else
+                    launch_ac3d_fused(variant, P, in, stream_io(h, Cr), h->stream_blocks, n, sv, sample, (n + 1) / Cr.every, h->st);
+                h->launches++;
+            }
+            cur ^= 1;
+            if ((rc = exchange_group_plan(grp, HW_PLAN_FUSED_AC3, cur))) return rc;
+        }
     } else if (grp->ranks[0]->fused_el3) {  // one-pass 3D elastic slabs: one exchange per step
         if ((rc = exchange_group_plan(grp, HW_PLAN_FUSED_EL3, 0))) return rc;  // halos of the uploaded state
         int cur = 0;
@@ -2125,7 +2156,7 @@ int hw_plane_div_mode(const hw_solver* h, int32_t plane) {
 
 int hw_exchange_plan(const hw_desc* desc, int32_t world, int32_t rank, int32_t kind, hw_xfer* out, int32_t cap,
                      int32_t* n) {
-    if (!desc || !n || world < 1 || rank < 0 || rank >= world || kind < 0 || kind > 3)
+    if (!desc || !n || world < 1 || rank < 0 || rank >= world || kind < 0 || kind > 4)
         return fail(HW_EINVAL, "hw_exchange_plan: bad arguments");
     PlanGeom g;
     g.ac = desc->equation == HW_EQ_ACOUSTIC;
@@ -2138,6 +2169,7 @@ int hw_exchange_plan(const hw_desc* desc, int32_t world, int32_t rank, int32_t k
     g.ns_loc = (int64_t)(rank + 1) * desc->ns / world - (int64_t)rank * desc->ns / world;
     if (kind == HW_PLAN_FUSED && !(g.ac && !g.d3)) return fail(HW_EINVAL, "hw_exchange_plan: fused plan is 2D acoustic");
     if (kind == HW_PLAN_FUSED_EL3 && !(!g.ac && g.d3)) return fail(HW_EINVAL, "hw_exchange_plan: HW_PLAN_FUSED_EL3 is 3D elastic");
+    if (kind == HW_PLAN_FUSED_AC3 && !(g.ac && g.d3)) return fail(HW_EINVAL, "hw_exchange_plan: HW_PLAN_FUSED_AC3 is 3D acoustic");
     const std::vector<hw_xfer> p = halo_plan(g, kind);
     *n = (int32_t)p.size();
     if (out)

@@ -103,6 +103,8 @@ void launch_ac3d_pres_stream(int variant, int order, const AcParams& P, const St
 // buffers (A), state n+1 written through the AcParams field views (B)
 struct Ac3In {
     const __half *p, *vx, *vs, *vm, *rp, *rvx, *rvs, *rvm;
+    int32_t slab;  // slab of a decomposed domain: slab -1 is a ghost row (HW_PLAN_FUSED_AC3), not slab ns-1
+    int32_t pad;
 };
 bool ac3d_fused_eligible(int64_t nx, int64_t nm, int64_t ns, int64_t pitch, int order, int max_smem);
 cudaError_t ac3d_fused_prepare(int64_t nx);

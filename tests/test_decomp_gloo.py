@@ -21,9 +21,10 @@ from paper_2310_00236_b200 import _abi, decomp
 # derivatives after the velocity phase, the slow-derivative stresses / pressure after the other)
 EXPECT = {
     ("ac", 2): {_abi.PLAN_VEL: {"vy"}, _abi.PLAN_STRESS: {"p"}, _abi.PLAN_FUSED: {"p", "vy", "rvy"}},
-    ("ac", 3): {_abi.PLAN_VEL: {"vz"}, _abi.PLAN_STRESS: {"p"}},
+    ("ac", 3): {_abi.PLAN_VEL: {"vz"}, _abi.PLAN_STRESS: {"p"}, _abi.PLAN_FUSED_AC3: {"p", "vz", "rvz"}},
     ("el", 2): {_abi.PLAN_VEL: {"vx", "vy"}, _abi.PLAN_STRESS: {"syy", "sxy"}},
-    ("el", 3): {_abi.PLAN_VEL: {"vx", "vy", "vz"}, _abi.PLAN_STRESS: {"szz", "sxz", "syz"}},
+    ("el", 3): {_abi.PLAN_VEL: {"vx", "vy", "vz"}, _abi.PLAN_STRESS: {"szz", "sxz", "syz"},
+                _abi.PLAN_FUSED_EL3: {"vx", "vy", "vz", "sxx", "syy", "szz", "sxy", "sxz", "syz", "rvx", "rvy", "rvz"}},
 }
 
 
@@ -64,10 +65,11 @@ def _check_case(eq, ndim, s, world, rank):
             fields[j] = decomp.with_ghosts(gl[r0:r0 + n_loc], fill=np.nan)
         p = decomp.exchange_host(desc, fields, world, rank, kind)
         assert {s.FIELDS[x["field"]] for x in p} == want_fields, (kind, p)
-        depth = 3 if kind == _abi.PLAN_FUSED else (1 if desc.order == 2 else 2)
+        depth_of = lambda j: (3 if kind == _abi.PLAN_FUSED else (2 if s.FIELDS[j].startswith("s") else 1)
+                              if kind == _abi.PLAN_FUSED_EL3 else (1 if desc.order == 2 else 2))
         got = {}
         for x in p:
-            assert x["nrows"] == depth
+            assert x["nrows"] == depth_of(x["field"])
             if x["send"]:
                 continue
             a, gl = fields[x["field"]], glob[x["field"]]
@@ -78,6 +80,7 @@ def _check_case(eq, ndim, s, world, rank):
                 np.testing.assert_array_equal(a[r + decomp.G], gl[g])
                 got.setdefault(x["field"], set()).add(r)
         for j in {x["field"] for x in p}:
+            depth = depth_of(j)
             n = fields[j].shape[0] - 2 * decomp.G
             want = set()
             if periodic or rank > 0:
@@ -126,7 +129,7 @@ def test_plan_pairs_match_across_ranks():
     the same field and row count, for every kind and world size 1..8 (1: NCCL self exchange)."""
     for eq, ndim, s in _cases():
         for world in range(1, 9):
-            kinds = [_abi.PLAN_VEL, _abi.PLAN_STRESS] + ([_abi.PLAN_FUSED] if (eq, ndim) == ("ac", 2) else [])
+            kinds = list(EXPECT[(eq, ndim)])
             for kind in kinds:
                 plans = [decomp.plan(s.desc, world, r, kind) for r in range(world)]
                 for b in range(world):

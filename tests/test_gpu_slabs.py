@@ -161,3 +161,35 @@ def test_fused_2d_slabs_receivers_on_slab_edges(slabs):
     ob = b.run(hw.Variant.OP6, sb)
     assert a.kernel_path() == "small2d" and b.kernel_path() == "fused2d" and b.transport() == 1
     _compare(a, sa, oa, b, sb, ob)
+
+
+def _acoustic3d_onepass(slabs, prec=hw.Precision.FP16, nt=13, src_z=None):
+    """Config 3's one-pass kernels (2nd order, nx = 512, per-cell beta) on slabs: p(-1), p(L), v_slow(-1)
+    and its residual arrive by the once-per-step exchange (HW_PLAN_FUSED_AC3)."""
+    nz, ny, nx = 40, 8, 512
+    rng = np.random.default_rng(9)
+    med = hw.build_acoustic_from_velocity(1.5 + 3.0 * rng.random((nz, ny, nx)))
+    dx = 1.0 / nx
+    g = hw.GridSpec(nx, ny, dx, float(np.float16(0.5 * dx / (med.c_max() * np.sqrt(3)))), nt, nz=nz, order=2)
+    src = None if src_z is None else hw.SourceSpec(hw.SourceKind.PRESSURE_POINT, 300, 3, hw.RickerSpec(1 / (10 * dx), amplitude=5.0), iz=src_z)
+    s = hw.AcousticSolver(g, med, src, stencil_precision=prec, slabs=slabs, energy_every=3,
+                          receivers=((5, 5, 30), (511, 7, 0), (300, 3, 19), (17, 2, 39)))
+    st = s.new_state()
+    z, y, x = np.mgrid[0:nz, 0:ny, 0:nx]
+    st.p.values = np.exp(-((x - 256) ** 2 / 2000.0 + (y - 4) ** 2 / 4.0 + (z - 19) ** 2 / 10.0)).astype(st.p.values.dtype)
+    st.vz.values = (0.01 * rng.standard_normal((nz, ny, nx))).astype(st.vz.values.dtype)
+    return s, st
+
+
+@pytest.mark.parametrize("slabs", [2, 3, 5, 8])
+@pytest.mark.parametrize("prec,variant", [(hw.Precision.FP16, hw.Variant.OP3), (hw.Precision.FP32, None)])
+def test_acoustic_3d_onepass_slabs_equal_single_domain(slabs, prec, variant):
+    a, sa, b, sb = _pair(lambda k: _acoustic3d_onepass(k, prec, src_z=20), slabs)
+    ref = oracle.run_solver(a, variant, sa)
+    oa = a.run(variant, sa)
+    ob = b.run(variant, sb)
+    want = "fused3d" if prec == hw.Precision.FP16 else "fused3d-f32"
+    assert a.kernel_path() == b.kernel_path() == want and b.transport() == 1
+    for j, n in enumerate(a.FIELDS):
+        assert_same_bits(getattr(sa, n).values, ref["fields"][j], n)
+    _compare(a, sa, oa, b, sb, ob)
