@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(Q3T, 1)
     float acc[8];
 #pragma unroll
     for (int q = 0; q < 8; q++) acc[q] = 0.f;
-    double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    __shared__ double ered[32];  // per-warp energy partials of one (tile, slab) unit (sample steps)
 
     const int tiles = nm / TM;
     const int64_t U = (int64_t)tiles * ns;
@@ -447,6 +447,7 @@ __global__ void __launch_bounds__(Q3T, 1)
                             },
                             Q3C);
                     if (sample) {  // E = dx^3/2 [sum beta p^n p^{n+1} + sum rho v^2] (diagnostics.py:76-87)
+                        double e[NCOMP] = {0.0, 0.0, 0.0, 0.0, 0.0};  // this (tile, slab) unit's share
                         const F4 vxo = q_ld(xv + ro);
 #pragma unroll
                         for (int q = 0; q < Q3C; q++) {
@@ -457,11 +458,19 @@ __global__ void __launch_bounds__(Q3T, 1)
                             e[2] += p64(P.e_rho_s, s, m, xi) * (b * b);
                             e[3] += p64(P.e_rho_m, s, m, xi) * (g * g);
                         }
+                        // per-plane partials (decomposition-invariant energy, as hw_elastic3d_fused.cu)
+                        const double a = warp_sum(((e[0] + e[1]) + e[2]) + e[3]);
+                        if ((tid & 31) == 0) ered[tid >> 5] = a;
                     }
                 }
                 vsq = vsn;
             }
             __syncthreads();
+            if (sample && tid == 0 && i > 1) {  // the unit's partial (slab F0 + i - 1), warps in order
+                double a = ered[0];
+                for (int w = 1; w < (int)(blockDim.x >> 5); w++) a += ered[w];
+                in_.eplane[(int64_t)(F0 + i - 1) * (nm / TM) + tile] = a;
+            }
         }
         gi += NI;
         gk += se - sb + 1;
@@ -479,18 +488,20 @@ __global__ void __launch_bounds__(Q3T, 1)
     }
     record_failure(P.ctrl, n, mask);
     if constexpr (!SAMPLE) return;
-    block_partials(e, P.partials);
     __threadfence();
     __syncthreads();
     __shared__ unsigned int is_last;
     if (tid == 0) is_last = atomicAdd(IO.counter, 1u) == (unsigned int)(gridDim.x - 1);
     __syncthreads();
     if (!is_last) return;
-    const double t = finalize_partials(P.partials, (int)gridDim.x);  // fixed-order fp64 reduction
-    if (tid == 0) {
-        IO.e_vals[eidx] = IO.scale * t;
-        *IO.counter = 0u;
+    // plane totals T[s] = sum_tile partial[s][tile], tiles in order (el3_energy_from_planes, hw_api.cu)
+    const int tiles_all = nm / TM;
+    for (int sp = tid; sp < ns; sp += (int)blockDim.x) {
+        double t = __ldcg(&in_.eplane[(int64_t)sp * tiles_all]);
+        for (int t2 = 1; t2 < tiles_all; t2++) t += __ldcg(&in_.eplane[(int64_t)sp * tiles_all + t2]);
+        in_.etot[eidx * (int64_t)ns + sp] = t;
     }
+    if (tid == 0) *IO.counter = 0u;
 }
 
 // ---------------------------------------------------------------- host side

@@ -408,9 +408,13 @@ struct hw_solver {
     double* el3_ecoef = nullptr;  // its per-slab energy coefficients (slow-layered media; in plane_mem)
     bool el3_slab = false;        // ... on a slab of a decomposed domain (ghosts from HW_PLAN_FUSED_EL3)
     int el3_nb_edge = 0, el3_nb_int = 0;  // ... NCCL slab: CTAs of the edge / interior launches (overlap)
-    double* el3_eplane = nullptr; // ... energy partials per (slab, tile) unit (in plane_mem)
-    double* el3_etot = nullptr;   // ... energy plane totals per sample
+    // Plane-ordered energy of the one-pass 3D kernels (fused_el3, fused3, fused3_32): per-(slab, tile)
+    // partials, per-slab totals per sample, summed on the host in global slab order -- the same bits
+    // for any decomposition into slabs
+    double* el3_eplane = nullptr; // energy partials per (slab, tile) unit (in plane_mem)
+    double* el3_etot = nullptr;   // energy plane totals per sample
     int64_t el3_etot_cap = 0;
+    bool plane_energy() const { return fused_el3 || fused3 || fused3_32; }
     bool el3_stream = false;  // streaming 3D elastic phases
     int stream_blocks = 0;
     unsigned int* counter = nullptr;  // CTA arrival counter of the streaming stress kernel
@@ -790,6 +794,8 @@ int setup_handle(hw_solver* h) {
             if (nbs < 1) nbs = 1;
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
             h->fused3 = true;
+            CU(cudaMalloc(&h->el3_eplane, (size_t)max_rows * (desc->nm / (4096 / desc->nx)) * sizeof(double)));
+            h->plane_mem.push_back(h->el3_eplane);
         }
         // the one-pass 3D acoustic step in binary32 lanes (BASELINE config 3's fp32 arm)
         if (want && f3_ok && h->ac && h->d3 && h->LS == 32 && h->LU == 32 && !h->fs &&
@@ -806,6 +812,8 @@ int setup_handle(hw_solver* h) {
             if (nbs < 1) nbs = 1;
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
             h->fused3_32 = true;
+            CU(cudaMalloc(&h->el3_eplane, (size_t)max_rows * (desc->nm / (2048 / desc->nx)) * sizeof(double)));
+            h->plane_mem.push_back(h->el3_eplane);
         }
         if (want && !h->fused3 && h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
             ac3d_stream_eligible(desc->nx, desc->nm, h->g.pitch, dev_smem)) {
@@ -842,7 +850,7 @@ int setup_handle(hw_solver* h) {
                 h->plane_mem.push_back(h->el3_ecoef);
                 CU(el3d_fused_ecoef(EP, h->el3_ecoef, max_rows, 0));
             }
-            CU(cudaMalloc(&h->el3_eplane, (size_t)max_rows * (desc->nm / (2048 / desc->nx)) * NCOMP * sizeof(double)));
+            CU(cudaMalloc(&h->el3_eplane, (size_t)max_rows * (desc->nm / (2048 / desc->nx)) * sizeof(double)));
             h->plane_mem.push_back(h->el3_eplane);
             const int64_t units = (desc->nm / (2048 / desc->nx)) * max_rows;
             int64_t nbs = units / 4;
@@ -1369,7 +1377,7 @@ static int run_begin(hw_solver* h, int32_t variant, int64_t nt, bool energy, boo
     C.every = h->d.energy_every;
     C.energy = energy;
     h->launches = 0;
-    if (h->fused_el3 && energy) {  // energy plane totals per sample (el3_energy_from_planes)
+    if (h->plane_energy() && energy) {  // energy plane totals per sample (el3_energy_from_planes)
         int64_t cap = h->el3_etot_cap;
         if ((rc = ensure(&h->el3_etot, &cap, (1 + nt / h->d.energy_every) * h->max_rows))) return rc;
         h->el3_etot_cap = cap;
@@ -1378,7 +1386,7 @@ static int run_begin(hw_solver* h, int32_t variant, int64_t nt, bool energy, boo
         if (h->ac) launch_ac_energy(h->LU, h->W, C.A, h->max_rows, h->st);
         else launch_el_energy(h->LU, h->W, C.L, h->max_rows, h->st);
         h->launches++;
-        if (!h->fused_el3) {
+        if (!h->plane_energy()) {
             launch_epilogue(h->LU, C.E, -1, 1, 0, h->st);
             h->launches++;
         } else {  // ... and its per-slab totals (one block partial per (x chunk, mid row, slab))
@@ -1493,6 +1501,8 @@ static void fused3_bufs(const hw_solver* h, int cur, AcParams& P, Ac3In& in) {
     in.rp = src[F_N + F_P]; in.rvx = src[F_N + F_VX]; in.rvs = src[F_N + F_VS]; in.rvm = src[F_N + F_VM];
     in.slab = (h->world > 1 || h->transport != 0) ? 1 : 0;
     in.pad = 0;
+    in.eplane = h->el3_eplane;
+    in.etot = h->el3_etot;
 }
 
 // The same for the one-pass 2D elastic kernel (external order vx vy sxx syy sxy + residuals).
@@ -1860,7 +1870,7 @@ int hw_run(hw_solver* h, int32_t variant, int64_t step0, int64_t nt, const doubl
     const int64_t nrec = h->d.n_receivers;
     const int64_t ne = energy ? 1 + (status == HW_OK ? nt / h->d.energy_every : (done - 1) / h->d.energy_every) : 0;
     if (h->transport == 2) {
-        if (ne > 0 && h->fused_el3) {  // plane totals of every rank, summed in global plane order
+        if (ne > 0 && h->plane_energy()) {  // plane totals of every rank, summed in global plane order
             std::vector<double> mine;
             if ((rc = el3_planes_host(h, ne, mine))) return rc;
             const int64_t lmax = (h->d.ns + h->world - 1) / h->world;
@@ -1909,7 +1919,7 @@ int hw_run(hw_solver* h, int32_t variant, int64_t step0, int64_t nt, const doubl
         }
         CU(cudaStreamSynchronize(h->st));
     }
-    if (h->fused_el3 && h->transport == 0 && ne > 0) {  // the same plane-ordered sum on one domain
+    if (h->plane_energy() && h->transport == 0 && ne > 0) {  // the same plane-ordered sum on one domain
         std::vector<std::vector<double>> planes(1);
         if ((rc = el3_planes_host(h, ne, planes[0]))) return rc;
         std::vector<double> tot(ne);
@@ -2059,7 +2069,7 @@ int hw_run_group(hw_solver* const* hs, int32_t nslabs, int32_t variant, int64_t 
     const int64_t nrec = h0->d.n_receivers;
     const int64_t ne = energy ? 1 + (status == HW_OK ? nt / h0->d.energy_every : (done - 1) / h0->d.energy_every) : 0;
     std::vector<double> tmp;
-    if (e_vals && ne > 0 && h0->fused_el3) {  // plane totals of every slab, in global plane order
+    if (e_vals && ne > 0 && h0->plane_energy()) {  // plane totals of every slab, in global plane order
         std::vector<std::vector<double>> planes(nslabs);
         std::vector<int64_t> rows(nslabs);
         for (hw_solver* h : grp->ranks) {

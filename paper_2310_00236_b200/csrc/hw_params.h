@@ -105,6 +105,8 @@ struct Ac3In {
     const __half *p, *vx, *vs, *vm, *rp, *rvx, *rvs, *rvm;
     int32_t slab;  // slab of a decomposed domain: slab -1 is a ghost row (HW_PLAN_FUSED_AC3), not slab ns-1
     int32_t pad;
+    double* eplane;  // [ns][tiles] energy partials of the (tile, slab) units (sample steps)
+    double* etot;    // [samples][ns] energy plane totals (sample eidx at etot + eidx * ns)
 };
 bool ac3d_fused_eligible(int64_t nx, int64_t nm, int64_t ns, int64_t pitch, int order, int max_smem);
 cudaError_t ac3d_fused_prepare(int64_t nx);

@@ -193,3 +193,5 @@ def test_acoustic_3d_onepass_slabs_equal_single_domain(slabs, prec, variant):
     for j, n in enumerate(a.FIELDS):
         assert_same_bits(getattr(sa, n).values, ref["fields"][j], n)
     _compare(a, sa, oa, b, sb, ob)
+    np.testing.assert_allclose(oa.energy.values, ref["e_vals"], rtol=1e-12)
+    np.testing.assert_array_equal(ob.energy.values, oa.energy.values)  # plane-ordered: bit-identical for any slabs
