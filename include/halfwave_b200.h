@@ -141,7 +141,9 @@ enum hw_plan_kind {
     HW_PLAN_FUSED = 2,  /* once per step of the fused 2D acoustic kernel: p, vy, rvy (3 rows) */
     HW_PLAN_FUSED_EL3 = 3, /* once per step of the one-pass 3D elastic kernel: the six stresses (2 rows),
                             * the velocities and their residuals (1 row) */
-    HW_PLAN_FUSED_AC3 = 4  /* once per step of the one-pass 3D acoustic kernels: p, v_slow, its residual (1 row) */
+    HW_PLAN_FUSED_AC3 = 4, /* once per step of the one-pass 3D acoustic kernels: p, v_slow, its residual (1 row) */
+    HW_PLAN_FUSED_EL2 = 5  /* once per step of the one-pass 2D elastic kernel: the five fields and the velocity
+                            * residuals (3 rows) */
 };
 typedef struct hw_xfer {
     int32_t field, peer, send, pad;

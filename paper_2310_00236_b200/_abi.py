@@ -48,7 +48,7 @@ EXPORTED = (
 )
 
 # hw_plan_kind
-PLAN_VEL, PLAN_STRESS, PLAN_FUSED, PLAN_FUSED_EL3, PLAN_FUSED_AC3 = 0, 1, 2, 3, 4
+PLAN_VEL, PLAN_STRESS, PLAN_FUSED, PLAN_FUSED_EL3, PLAN_FUSED_AC3, PLAN_FUSED_EL2 = 0, 1, 2, 3, 4, 5
 
 
 class Xfer(ctypes.Structure):

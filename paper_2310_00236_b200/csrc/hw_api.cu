@@ -754,9 +754,10 @@ int setup_handle(hw_solver* h) {
             CU(cudaMalloc(&h->partials2, (size_t)h->small_nb * NCOMP * sizeof(double)));
             h->small_el = true;
         }
-        // one-pass 2D elastic step (single domain): ping-pong partner buffers
+        // one-pass 2D elastic step (a single domain, or a slab of a decomposed one: ghost rows from
+        // HW_PLAN_FUSED_EL2 once per step): ping-pong partner buffers
         if (want && !h->small_el && opt("fused_el") == 1 && !h->ac && !h->d3 && h->LS == 16 &&
-            h->LU == 16 && h->world == 1 && h->transport == 0 && el2d_fused_eligible(desc->nx, desc->ns, dev_smem)) {
+            h->LU == 16 && el2d_fused_eligible(desc->nx, field_rows(h, F_SXS), dev_smem)) {
             for (int j = 0; j < 2 * h->nsol; j++) {
                 int f = h->ext[j % h->nsol];
                 size_t bytes = (size_t)(field_rows(h, f) + 2 * G) * h->g.slab * esz;
@@ -1014,6 +1015,11 @@ std::vector<hw_xfer> halo_plan(const PlanGeom& g, int kind) {
     std::vector<int64_t> dep;  // per-field depth (HW_PLAN_FUSED_EL3)
     if (kind == HW_PLAN_FUSED) {
         js = {0, 2, 5};  // p, vy, rvy of p vx vy rp rvx rvy
+        depth = G;
+    } else if (kind == HW_PLAN_FUSED_EL2) {
+        // one-pass 2D elastic slab (hw_elastic2d_fused.cu): its CTAs stream rows -3 .. L+2 and recompute
+        // the velocity rows of the halo: the five fields and the velocity residuals, G rows each way
+        js = {0, 1, 2, 3, 4, 5, 6};  // vx vy sxx syy sxy rvx rvy
         depth = G;
     } else if (kind == HW_PLAN_FUSED_AC3) {
         // one-pass 3D acoustic slab: p rows -1 and L, v_slow and its residual row -1 (1 row each way)
@@ -1516,6 +1522,18 @@ static void fused_el_bufs(const hw_solver* h, int cur, ElParams& P, El2In& in) {
         out[j]->base = (char*)wr[j] + ghost;
         *src[j] = (const __half*)((const char*)rd[j] + ghost);
     }
+    in.slab = (h->world > 1 || h->transport != 0) ? 1 : 0;
+    in.top = h->rank == 0;
+    in.bot = h->rank == h->world - 1;
+    in.vsrc = 0;
+    in.vsrc_s = 0;
+    if (h->d.src_kind == HW_SRC_VSLOW) {  // this slab also computes the halo velocity rows -3 .. rows + 2
+        const int64_t r = h->d.src_s - h->r0;
+        if (r >= -G && r < field_rows(h, F_VS) + G) {
+            in.vsrc = 1;
+            in.vsrc_s = r;
+        }
+    }
 }
 
 // The same for the one-pass 3D elastic kernel.
@@ -1582,8 +1600,9 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
     int rc = run_begin(h, variant, nt, energy, true, C);
     if (rc) return rc;
     const bool fused_slab = h->fused && h->transport == 2;
-    if (fused_slab || (h->transport == 2 && (h->fused_el3 || h->fused3 || h->fused3_32))) {  // halos of the upload
-        const int kind = fused_slab ? HW_PLAN_FUSED : (h->fused_el3 ? HW_PLAN_FUSED_EL3 : HW_PLAN_FUSED_AC3);
+    if (fused_slab || (h->transport == 2 && (h->fused_el3 || h->fused3 || h->fused3_32 || h->fused_el))) {  // halos
+        const int kind = fused_slab ? HW_PLAN_FUSED
+                                    : (h->fused_el3 ? HW_PLAN_FUSED_EL3 : (h->fused_el ? HW_PLAN_FUSED_EL2 : HW_PLAN_FUSED_AC3));
         if ((rc = exchange_nccl_plan(h, kind, 0))) return rc;
     } else if ((rc = exchange(h, 0)) || (rc = exchange(h, 1))) {
         return rc;
@@ -1736,6 +1755,7 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
                               (n + 1) / C.every, h->st);
             h->launches++;
             cur ^= 1;
+            if (h->transport == 2 && (rc = exchange_nccl_plan(h, HW_PLAN_FUSED_EL2, cur))) return rc;
         }
     } else if (h->fused) {  // fused kernels, ping-pong A <-> B: launch L reads buffer L % 2
         AcFusedParams F = fused_params(h, nt);
@@ -1979,6 +1999,24 @@ int hw_run_group(hw_solver* const* hs, int32_t nslabs, int32_t variant, int64_t 
             cur ^= 1;
             if ((rc = exchange_group_plan(grp, HW_PLAN_FUSED, cur))) return rc;
         }
+    } else if (grp->ranks[0]->fused_el) {  // one-pass 2D elastic slabs: one exchange per step
+        if ((rc = exchange_group_plan(grp, HW_PLAN_FUSED_EL2, 0))) return rc;  // halos of the uploaded state
+        int cur = 0;
+        for (int64_t n = 0; n < nt; n++) {
+            for (hw_solver* h : grp->ranks) {
+                cudaSetDevice(h->d.device);
+                RunCtx& Cr = C[h->rank];
+                ElParams P = Cr.L;
+                El2In in;
+                fused_el_bufs(h, cur, P, in);
+                const int sample = energy && ((n + 1) % Cr.every == 0);
+                launch_el2d_fused(variant, h->d.order, P, in, stream_io(h, Cr), h->stream_blocks, n,
+                                  src_samples ? src_samples[n] : 0.0, sample, (n + 1) / Cr.every, h->st);
+                h->launches++;
+            }
+            cur ^= 1;
+            if ((rc = exchange_group_plan(grp, HW_PLAN_FUSED_EL2, cur))) return rc;
+        }
     } else if (grp->ranks[0]->fused3 || grp->ranks[0]->fused3_32) {  // one-pass 3D acoustic slabs
         if ((rc = exchange_group_plan(grp, HW_PLAN_FUSED_AC3, 0))) return rc;  // halos of the uploaded state
         int cur = 0;
@@ -2166,7 +2204,7 @@ int hw_plane_div_mode(const hw_solver* h, int32_t plane) {
 
 int hw_exchange_plan(const hw_desc* desc, int32_t world, int32_t rank, int32_t kind, hw_xfer* out, int32_t cap,
                      int32_t* n) {
-    if (!desc || !n || world < 1 || rank < 0 || rank >= world || kind < 0 || kind > 4)
+    if (!desc || !n || world < 1 || rank < 0 || rank >= world || kind < 0 || kind > 5)
         return fail(HW_EINVAL, "hw_exchange_plan: bad arguments");
     PlanGeom g;
     g.ac = desc->equation == HW_EQ_ACOUSTIC;
@@ -2180,6 +2218,7 @@ int hw_exchange_plan(const hw_desc* desc, int32_t world, int32_t rank, int32_t k
     if (kind == HW_PLAN_FUSED && !(g.ac && !g.d3)) return fail(HW_EINVAL, "hw_exchange_plan: fused plan is 2D acoustic");
     if (kind == HW_PLAN_FUSED_EL3 && !(!g.ac && g.d3)) return fail(HW_EINVAL, "hw_exchange_plan: HW_PLAN_FUSED_EL3 is 3D elastic");
     if (kind == HW_PLAN_FUSED_AC3 && !(g.ac && g.d3)) return fail(HW_EINVAL, "hw_exchange_plan: HW_PLAN_FUSED_AC3 is 3D acoustic");
+    if (kind == HW_PLAN_FUSED_EL2 && !(!g.ac && !g.d3)) return fail(HW_EINVAL, "hw_exchange_plan: HW_PLAN_FUSED_EL2 is 2D elastic");
     const std::vector<hw_xfer> p = halo_plan(g, kind);
     *n = (int32_t)p.size();
     if (out)

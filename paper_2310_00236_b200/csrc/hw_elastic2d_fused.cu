@@ -101,7 +101,12 @@ __global__ void __launch_bounds__(512, 1)
     const uint32_t rb = (uint32_t)(nx * sizeof(__half));
     // rows outside the domain: periodic -> wrapped; free surface -> clamped (those values
     // are never used: image rows replace them); tap rows with images use the ghost slabs
-    auto orow = [&](int r, int rows) { return fs ? (r < 0 ? 0 : (r >= rows ? rows - 1 : r)) : (r < 0 ? r + rows : (r >= rows ? r - rows : r)); };
+    // (a slab of a decomposed domain: no wrap; clamping only at the global ends it owns)
+    const bool slabm = in.slab != 0, gtop = !slabm || in.top, gbot = !slabm || in.bot;
+    auto orow = [&](int r, int rows) {
+        if (slabm) return fs ? ((r < 0 && gtop) ? 0 : ((r >= rows && gbot) ? rows - 1 : r)) : r;
+        return fs ? (r < 0 ? 0 : (r >= rows ? rows - 1 : r)) : (r < 0 ? r + rows : (r >= rows ? r - rows : r));
+    };
     auto trow = [&](int r, int rows) {  // (free surface: stay inside the G ghost slabs)
         return fs ? (int64_t)(r < -G ? -G : (r > rows + G - 1 ? rows + G - 1 : r)) : (int64_t)orow(r, rows);
     };
@@ -148,7 +153,7 @@ __global__ void __launch_bounds__(512, 1)
     const __half2 dt2 = __half2half2(dt);
     const __half srch = __double2half(src);
     const int xl = x == 0 ? nx - 2 : x - 2, xr = x + ECPT >= nx ? 0 : x + ECPT;
-    const bool vsrc = P.src_kind == HW_SRC_VSLOW && src != 0.0;      // warp-uniform
+    const bool vsrc = in.vsrc && src != 0.0;  // warp-uniform; on a slab its row may be a halo row
     const bool ssrc = P.src_kind == HW_SRC_EXPLOSIVE && src != 0.0;  // warp-uniform
     const bool src_v = vsrc && P.src_x >= x && P.src_x < x + ECPT;
     const bool src_s = ssrc && P.src_x >= x && P.src_x < x + ECPT;
@@ -208,7 +213,8 @@ __global__ void __launch_bounds__(512, 1)
                 const E8 ay = e_xfold<ORDER>(c, S.l(l2, L_SXS), x, xl, xr, true);
                 const E8 dy = e_sfold<ORDER>(c, e_ld8(S.l(l3, L_SSS) + x), e_ld8(S.l(l2, L_SSS) + x),
                                              e_ld8(S.l(l1, L_SSS) + x), e_ld8(S.l(ls, L_SSS) + x));  // syy F-3..F
-                const bool sk = src_v && ryw == P.src_s;  // (periodic halo rows: the wrapped row)
+                const int vrow = slabm ? ry : ryw;  // (single periodic domain: halo rows are the wrapped rows)
+                const bool sk = src_v && vrow == in.vsrc_s;
                 if constexpr (RM) {
                     EH2 hx[4], hy[4];
 #pragma unroll
@@ -216,7 +222,7 @@ __global__ void __launch_bounds__(512, 1)
                         hx[j] = EO2::add(ax.q[j], dx.q[j]);
                         hy[j] = EO2::add(ay.q[j], dy.q[j]);
                     }
-                    if (vsrc && ryw == P.src_s) e2_add_src(hy, sk, sj, sln, srch);
+                    if (vsrc && vrow == in.vsrc_s) e2_add_src(hy, sk, sj, sln, srch);
 #pragma unroll
                     for (int j = 0; j < 4; j++) {
                         e_finish_rc<V>(hx[j], rcx, dt2, -1, srch, v.q[j], rr.q[j]);
@@ -232,11 +238,11 @@ __global__ void __launch_bounds__(512, 1)
                     }
                 }
             }
-            if (fs && rx >= ri) {  // bottom images: rows ri-2, ri-3 (pre-push)
+            if (fs && gbot && rx >= ri) {  // bottom images: rows ri-2, ri-3 (pre-push)
                 if (rx == ri) v = vxq.q2;
                 else v = vxq.q0;
             }
-            if (fs && ry >= rh) {  // bottom images: rows rh-1, rh-2 (pre-push)
+            if (fs && gbot && ry >= rh) {  // bottom images: rows rh-1, rh-2 (pre-push)
                 if (ry == rh) w = vyq.q3;
                 else w = vyq.q1;
             }
@@ -256,9 +262,9 @@ __global__ void __launch_bounds__(512, 1)
             }
             vxq.push(v);
             vyq.push(w);
-            if (fs && rx == 1) vxq.q1 = vxq.q3;  // top images: vx row -1 = row 1
-            if (fs && ry == 0) vyq.q2 = vyq.q3;  //             vy row -1 = row 0
-            if (fs && ry == 1) vyq.q0 = vyq.q3;  //             vy row -2 = row 1
+            if (fs && gtop && rx == 1) vxq.q1 = vxq.q3;  // top images: vx row -1 = row 1
+            if (fs && gtop && ry == 0) vyq.q2 = vyq.q3;  //             vy row -1 = row 0
+            if (fs && gtop && ry == 1) vyq.q0 = vyq.q3;  //             vy row -2 = row 1
         }
         __syncthreads();  // vx / vy rows visible; every read of tap slot (i+1) % LR and of the A rows is done
         if (tid == 0 && i + 1 < NI) {

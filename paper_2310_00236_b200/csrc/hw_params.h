@@ -121,6 +121,11 @@ void launch_ac3d_fused32(int variant, const AcParams& P, const Ac3In& in, const 
 // state n+1 written through the ElParams field views (B)
 struct El2In {
     const __half *vx, *vs, *sxx, *sss, *sxs, *rvx, *rvs, *rsxx, *rsss, *rsxs;
+    // slab of a decomposed domain (ghost rows from HW_PLAN_FUSED_EL2): rows outside the slab are read
+    // from the ghosts, not wrapped; free-surface images only at the global ends this slab owns
+    int32_t slab, top, bot;
+    int32_t vsrc;   // a v_slow point source on local row vsrc_s (-3 .. rows + 2: halo rows included)
+    int64_t vsrc_s;
 };
 bool el2d_fused_eligible(int64_t nx, int64_t ns, int max_smem);
 cudaError_t el2d_fused_prepare(int64_t nx);

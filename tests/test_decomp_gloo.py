@@ -22,7 +22,8 @@ from paper_2310_00236_b200 import _abi, decomp
 EXPECT = {
     ("ac", 2): {_abi.PLAN_VEL: {"vy"}, _abi.PLAN_STRESS: {"p"}, _abi.PLAN_FUSED: {"p", "vy", "rvy"}},
     ("ac", 3): {_abi.PLAN_VEL: {"vz"}, _abi.PLAN_STRESS: {"p"}, _abi.PLAN_FUSED_AC3: {"p", "vz", "rvz"}},
-    ("el", 2): {_abi.PLAN_VEL: {"vx", "vy"}, _abi.PLAN_STRESS: {"syy", "sxy"}},
+    ("el", 2): {_abi.PLAN_VEL: {"vx", "vy"}, _abi.PLAN_STRESS: {"syy", "sxy"},
+                _abi.PLAN_FUSED_EL2: {"vx", "vy", "sxx", "syy", "sxy", "rvx", "rvy"}},
     ("el", 3): {_abi.PLAN_VEL: {"vx", "vy", "vz"}, _abi.PLAN_STRESS: {"szz", "sxz", "syz"},
                 _abi.PLAN_FUSED_EL3: {"vx", "vy", "vz", "sxx", "syy", "szz", "sxy", "sxz", "syz", "rvx", "rvy", "rvz"}},
 }
@@ -65,7 +66,7 @@ def _check_case(eq, ndim, s, world, rank):
             fields[j] = decomp.with_ghosts(gl[r0:r0 + n_loc], fill=np.nan)
         p = decomp.exchange_host(desc, fields, world, rank, kind)
         assert {s.FIELDS[x["field"]] for x in p} == want_fields, (kind, p)
-        depth_of = lambda j: (3 if kind == _abi.PLAN_FUSED else (2 if s.FIELDS[j].startswith("s") else 1)
+        depth_of = lambda j: (3 if kind in (_abi.PLAN_FUSED, _abi.PLAN_FUSED_EL2) else (2 if s.FIELDS[j].startswith("s") else 1)
                               if kind == _abi.PLAN_FUSED_EL3 else (1 if desc.order == 2 else 2))
         got = {}
         for x in p:

@@ -80,7 +80,18 @@ def _acoustic3d_onepass(**kw):  # config 3's one-pass kernel on the NCCL transpo
     return s, st
 
 
+def _elastic2d_onepass(**kw):  # config 4's one-pass kernel on the NCCL transport (HW_PLAN_FUSED_EL2)
+    from test_gpu_slabs import _elastic2d_onepass as mk
+
+    s, st = mk(1)
+    if kw.get("distributed"):
+        s = hw.ElasticSolver(s.grid, s.medium, s.source, stencil_precision=s.stencil_precision,
+                             receivers=s.receivers, energy_every=s.energy_every, distributed=True)
+    return s, st
+
+
 @pytest.mark.parametrize("make,variant", [(_acoustic, hw.Variant.OP3), (_elastic, hw.Variant.OP6),
+                                          (_elastic2d_onepass, hw.Variant.OP6),
                                           (_acoustic3d, hw.Variant.OP3), (_elastic3d_onepass, hw.Variant.OP6),
                                           (_acoustic3d_onepass, hw.Variant.OP3)])
 def test_nccl_transport_equals_single_process(one_rank_job, make, variant):

@@ -195,3 +195,38 @@ def test_acoustic_3d_onepass_slabs_equal_single_domain(slabs, prec, variant):
     _compare(a, sa, oa, b, sb, ob)
     np.testing.assert_allclose(oa.energy.values, ref["e_vals"], rtol=1e-12)
     np.testing.assert_array_equal(ob.energy.values, oa.energy.values)  # plane-ordered: bit-identical for any slabs
+
+
+def _elastic2d_onepass(slabs, fs=True, nt=23, kind=hw.SourceKind.VY_POINT, src_y=45):
+    """Config 4's one-pass kernel on slabs (HW_PLAN_FUSED_EL2: five fields + velocity residuals, 3 rows):
+    the CTAs at a slab edge recompute the halo velocity rows from the ghosts; free-surface images only at
+    the global ends."""
+    nx, ny = 256, 120
+    med = hw.build_layered_elastic(nx, ny, [(0.4, 2.0, 2.0, 1.0), (1.0, 2.3, 2.8, 1.4)])
+    g = hw.GridSpec(nx, ny, 1.0 / nx, float(np.float16(0.3 / nx / med.c_max())), nt,
+                    bc_y=hw.Boundary.FREE_SURFACE if fs else hw.Boundary.PERIODIC)
+    src = hw.SourceSpec(kind, 100, src_y, hw.RickerSpec(1 / (10 / nx), amplitude=20.0))
+    s = hw.ElasticSolver(g, med, src, stencil_precision=hw.Precision.FP16, energy_every=4, slabs=slabs,
+                         receivers=((100, src_y), (10, 0), (250, 119), (7, 44), (8, 46), (9, 15)))
+    st = s.new_state()
+    rng = np.random.default_rng(13)
+    st.sxx.values = rng.uniform(-0.1, 0.1, st.sxx.values.shape).astype(np.float16)
+    st.vy.values = rng.uniform(-0.01, 0.01, st.vy.values.shape).astype(np.float16)
+    st.sxy.values = rng.uniform(-0.02, 0.02, st.sxy.values.shape).astype(np.float16)
+    return s, st
+
+
+@pytest.mark.parametrize("slabs", [2, 3, 5, 8])
+@pytest.mark.parametrize("fs", [True, False])
+@pytest.mark.parametrize("kind,src_y", [(hw.SourceKind.VY_POINT, 45), (hw.SourceKind.VY_POINT, 44),
+                                        (hw.SourceKind.EXPLOSIVE, 46)])
+def test_elastic_2d_onepass_slabs_equal_single_domain(hwopt, slabs, fs, kind, src_y):
+    hwopt(small=0)
+    a, sa, b, sb = _pair(lambda k: _elastic2d_onepass(k, fs, kind=kind, src_y=src_y), slabs)
+    ref = oracle.run_solver(a, hw.Variant.OP6, sa)
+    oa = a.run(hw.Variant.OP6, sa)
+    ob = b.run(hw.Variant.OP6, sb)
+    assert a.kernel_path() == b.kernel_path() == "fused2d-el" and b.transport() == 1
+    for j, n in enumerate(a.FIELDS):
+        assert_same_bits(getattr(sa, n).values, ref["fields"][j], n)
+    _compare(a, sa, oa, b, sb, ob)
