@@ -229,6 +229,7 @@ int hw_plane_div_mode(const hw_solver* h, int32_t plane);
  *   "fused3"    1 one-pass 3D acoustic kernels | 0 two-phase kernels
  *   "fused_el3" 1 one-pass 3D elastic kernel (2nd order, media constant along x) | 0 two-phase
  *   "el3_group" 4 at most this many CTAs of the one-pass 3D elastic kernel stream adjacent tiles
+ *   "ac3_group" 4 the same for the one-pass 3D acoustic kernels (binary16 and binary32)
  *   "nccl_self" 0 | 1 a one-rank job given an NCCL id takes the NCCL transport (tests)
  * HW_EINVAL for an unknown name or an out-of-range value. */
 int hw_set_option(const char* name, int64_t value);

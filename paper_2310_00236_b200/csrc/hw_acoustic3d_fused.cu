@@ -125,13 +125,17 @@ __global__ void __launch_bounds__(F3T, 1)
     for (int q = 0; q < 8; q++) acc[q] = __float2half2_rn(0.f);
     __shared__ double ered[32];  // per-warp energy partials of one (tile, slab) unit (sample steps)
 
-    const int tiles = nm / TM;
+    // groups of `grp` CTAs own `grp` adjacent mid tiles and stream the same slab range side by side:
+    // the halo rows one CTA reads are rows its neighbour in the group reads at about the same time
+    // (L2 hits instead of DRAM re-reads); the (tile group, slab) units are split evenly over the groups
+    const int grp = in.group, ngrp = (int)gridDim.x / grp, gid = (int)blockIdx.x / grp, gr = (int)blockIdx.x % grp;
+    const int tiles = nm / TM / grp;  // tile groups
     const int64_t U = (int64_t)tiles * ns;
-    int64_t u = (int64_t)blockIdx.x * U / gridDim.x;
-    const int64_t u1 = (int64_t)(blockIdx.x + 1) * U / gridDim.x;
+    int64_t u = (int64_t)gid * U / ngrp;
+    const int64_t u1 = (int64_t)(gid + 1) * U / ngrp;
     int gi = 0, gk = 0;  // running tap / own use counters (slot and parity continue across segments)
     while (u < u1) {
-        const int tile = (int)(u / ns), sb = (int)(u % ns);
+        const int tile = (int)(u / ns) * grp + gr, sb = (int)(u % ns);
         const int se = (int)min((int64_t)ns, sb + (u1 - u));
         u += se - sb;
         const int m0 = tile * TM, m = m0 + j;

@@ -44,6 +44,7 @@ Option g_opts[] = {
     {"fused3", 1, 0, 1, "one-pass 3D acoustic kernels (binary16 and binary32 lanes)"},
     {"fused_el3", 1, 0, 1, "one-pass 3D elastic kernel (2nd order, media constant along x) | 0 two-phase kernels"},
     {"el3_group", 4, 1, 4, "one-pass 3D elastic kernel: at most this many CTAs stream adjacent tiles side by side"},
+    {"ac3_group", 4, 1, 4, "one-pass 3D acoustic kernels: at most this many CTAs stream adjacent tiles side by side"},
     {"nccl_self", 0, 0, 1, "a one-rank job with an NCCL id takes the NCCL transport (self exchange: tests)"},
 };
 int64_t opt(const char* name) {
@@ -404,7 +405,7 @@ struct hw_solver {
     bool fused_el3 = false;   // one-pass 3D elastic step (2nd order), ping-pong A <-> B
     float* el3_coef = nullptr;  // its medium coefficient table ([ns][el3_cm][8], in plane_mem)
     int64_t el3_cm = 0;
-    int el3_group = 1;          // its CTA groups of adjacent tiles (hw_elastic3d_fused.cu)
+    int el3_group = 1;          // CTA groups of adjacent tiles of the one-pass 3D kernels (elastic and acoustic)
     double* el3_ecoef = nullptr;  // its per-slab energy coefficients (slow-layered media; in plane_mem)
     bool el3_slab = false;        // ... on a slab of a decomposed domain (ghosts from HW_PLAN_FUSED_EL3)
     int el3_nb_edge = 0, el3_nb_int = 0;  // ... NCCL slab: CTAs of the edge / interior launches (overlap)
@@ -790,10 +791,16 @@ int setup_handle(hw_solver* h) {
                 CU(cudaMemset(h->mem_b[j], 0, bytes));
             }
             if (ac3d_fused_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "fused 3D kernel setup failed");
-            const int64_t units = (desc->nm / (4096 / desc->nx)) * max_rows;
+            const int64_t tiles = desc->nm / (4096 / desc->nx), units = tiles * max_rows;
             int64_t nbs = units / 4;
             if (nbs < 1) nbs = 1;
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
+            for (int g : {4, 2, 1})  // CTA groups of adjacent tiles (halo rows shared through L2)
+                if (g <= opt("ac3_group") && h->stream_blocks % g == 0 && tiles % g == 0 &&
+                    (tiles / g) * max_rows >= h->stream_blocks / g) {
+                    h->el3_group = g;
+                    break;
+                }
             h->fused3 = true;
             CU(cudaMalloc(&h->el3_eplane, (size_t)max_rows * (desc->nm / (4096 / desc->nx)) * sizeof(double)));
             h->plane_mem.push_back(h->el3_eplane);
@@ -808,10 +815,16 @@ int setup_handle(hw_solver* h) {
                 CU(cudaMemset(h->mem_b[j], 0, bytes));
             }
             if (ac3d_fused32_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "fused 3D fp32 kernel setup failed");
-            const int64_t units = (desc->nm / (2048 / desc->nx)) * max_rows;
+            const int64_t tiles = desc->nm / (2048 / desc->nx), units = tiles * max_rows;
             int64_t nbs = units / 4;
             if (nbs < 1) nbs = 1;
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
+            for (int g : {4, 2, 1})  // CTA groups of adjacent tiles (halo rows shared through L2)
+                if (g <= opt("ac3_group") && h->stream_blocks % g == 0 && tiles % g == 0 &&
+                    (tiles / g) * max_rows >= h->stream_blocks / g) {
+                    h->el3_group = g;
+                    break;
+                }
             h->fused3_32 = true;
             CU(cudaMalloc(&h->el3_eplane, (size_t)max_rows * (desc->nm / (2048 / desc->nx)) * sizeof(double)));
             h->plane_mem.push_back(h->el3_eplane);
@@ -1506,7 +1519,7 @@ static void fused3_bufs(const hw_solver* h, int cur, AcParams& P, Ac3In& in) {
     in.p = src[F_P]; in.vx = src[F_VX]; in.vs = src[F_VS]; in.vm = src[F_VM];
     in.rp = src[F_N + F_P]; in.rvx = src[F_N + F_VX]; in.rvs = src[F_N + F_VS]; in.rvm = src[F_N + F_VM];
     in.slab = (h->world > 1 || h->transport != 0) ? 1 : 0;
-    in.pad = 0;
+    in.group = h->el3_group;
     in.eplane = h->el3_eplane;
     in.etot = h->el3_etot;
 }

@@ -104,7 +104,7 @@ void launch_ac3d_pres_stream(int variant, int order, const AcParams& P, const St
 struct Ac3In {
     const __half *p, *vx, *vs, *vm, *rp, *rvx, *rvs, *rvm;
     int32_t slab;  // slab of a decomposed domain: slab -1 is a ghost row (HW_PLAN_FUSED_AC3), not slab ns-1
-    int32_t pad;
+    int32_t group;  // CTAs per group of adjacent tiles (divides the grid and the tile count)
     double* eplane;  // [ns][tiles] energy partials of the (tile, slab) units (sample steps)
     double* etot;    // [samples][ns] energy plane totals (sample eidx at etot + eidx * ns)
 };
