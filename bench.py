@@ -111,14 +111,14 @@ def smooth_velocity(n, seed=3, sigma=8.0):
     return 1.5 + 3.0 * (f.astype(np.float64) - lo) / (hi - lo)
 
 
-def make_config3(hw, prec, nt=1000, c=None):
+def make_config3(hw, prec, nt=1000, c=None, **kw):
     n = 512
     c = smooth_velocity(n) if c is None else c
     med = hw.build_acoustic_from_velocity(c)
     dx = 1.0 / n
     dt = float(np.float16(0.5 * dx / (4.5 * np.sqrt(3))))  # CFL <= 1/sqrt(3) at the config's c_max 4.5
     g = hw.GridSpec(n, n, dx, dt, nt, nz=c.shape[0], order=2)
-    return hw.AcousticSolver(g, med, stencil_precision=prec, energy_every=10)
+    return hw.AcousticSolver(g, med, stencil_precision=prec, energy_every=10, **kw)
 
 
 def init_config3(st):
@@ -129,13 +129,14 @@ def init_config3(st):
         st.p.values.dtype)
 
 
-def make_config4(hw, nt=5000):
+def make_config4(hw, nt=5000, periodic=False, **kw):
     n = 4096
     dx = 1.0 / n
     med = hw.build_layered_elastic(n, n, [(1.0, 1.0, 2.0, 1.0)])  # lambda = 2, mu = 1, rho = 1
-    g = hw.GridSpec(n, n, dx, float(np.float16(0.4 * dx / 2)), nt, bc_y=hw.Boundary.FREE_SURFACE)
+    g = hw.GridSpec(n, n, dx, float(np.float16(0.4 * dx / 2)), nt,
+                    bc_y=hw.Boundary.PERIODIC if periodic else hw.Boundary.FREE_SURFACE)
     src = hw.SourceSpec(hw.SourceKind.EXPLOSIVE, n // 2, 16, hw.RickerSpec(1 / (10 * dx), amplitude=3.0e4))
-    return hw.ElasticSolver(g, med, src, stencil_precision=hw.Precision.FP16, energy_every=10)
+    return hw.ElasticSolver(g, med, src, stencil_precision=hw.Precision.FP16, energy_every=10, **kw)
 
 
 def make_config1(hw, prec, nt=2000):

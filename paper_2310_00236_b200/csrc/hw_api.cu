@@ -770,6 +770,17 @@ int setup_handle(hw_solver* h) {
             if (nbs < 1) nbs = 1;
             h->stream_blocks = (int)(nbs < nsm ? nbs : nsm);
             h->fused_el = true;
+            // NCCL slab: the two edge bands + the exchange on st, the interior bands on st2 (as the
+            // fused 2D acoustic kernel)
+            if (h->transport == 2 && field_rows(h, F_SXS) >= 5 * FUSED_EDGE) {
+                CU(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
+                for (int k = 0; k < 2; k++) {
+                    CU(cudaEventCreateWithFlags(&h->ev_edge[k], cudaEventDisableTiming));
+                    CU(cudaEventCreateWithFlags(&h->ev_int[k], cudaEventDisableTiming));
+                }
+                int64_t ni = (field_rows(h, F_SXS) - 2 * FUSED_EDGE) / 4;
+                h->nb_int = (int)(ni < nsm - 2 ? ni : nsm - 2);
+            }
         }
         if (want && !h->small_el && !h->fused_el && !h->ac && !h->d3 && h->LS == 16 && h->LU == 16 &&
             el2d_stream_eligible(desc->nx, desc->ns, dev_smem)) {
@@ -1540,6 +1551,7 @@ static void fused_el_bufs(const hw_solver* h, int cur, ElParams& P, El2In& in) {
     in.bot = h->rank == h->world - 1;
     in.vsrc = 0;
     in.vsrc_s = 0;
+    in.band = in.edge = in.nb_total = in.pad = 0;
     if (h->d.src_kind == HW_SRC_VSLOW) {  // this slab also computes the halo velocity rows -3 .. rows + 2
         const int64_t r = h->d.src_s - h->r0;
         if (r >= -G && r < field_rows(h, F_VS) + G) {
@@ -1756,6 +1768,35 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
             cur ^= 1;
             if (h->transport == 2 && (rc = exchange_nccl_plan(h, HW_PLAN_FUSED_EL3, cur))) return rc;
         }
+    } else if (h->fused_el && h->transport == 2 && h->st2) {
+        // NCCL slab, overlapped (as the fused 2D acoustic kernel):
+        //   st : wait interior(n-1) | edge bands(n) | record E(n) | exchange(n)
+        //   st2: wait edge(n-1)     | interior bands(n) | record I(n)
+        const StreamIO IO = stream_io(h, C);
+        CU(cudaEventRecord(h->ev_edge[1], h->st));  // st2 starts after everything queued on st
+        int cur = 0;
+        for (int64_t n = 0; n < nt; n++) {
+            ElParams P = C.L;
+            El2In in;
+            fused_el_bufs(h, cur, P, in);
+            in.edge = FUSED_EDGE;
+            in.nb_total = 2 + h->nb_int;
+            El2In ie = in, ii = in;
+            ie.band = 1;
+            ii.band = 2;
+            const int sample = energy && ((n + 1) % C.every == 0);
+            const double sv = src ? src[n] : 0.0;
+            if (n > 0) CU(cudaStreamWaitEvent(h->st, h->ev_int[(n - 1) & 1], 0));
+            launch_el2d_fused(variant, h->d.order, P, ie, IO, 2, n, sv, sample, (n + 1) / C.every, h->st);
+            CU(cudaEventRecord(h->ev_edge[n & 1], h->st));
+            CU(cudaStreamWaitEvent(h->st2, h->ev_edge[(n + 1) & 1], 0));  // edge(n-1), or the start
+            launch_el2d_fused(variant, h->d.order, P, ii, IO, h->nb_int, n, sv, sample, (n + 1) / C.every, h->st2);
+            CU(cudaEventRecord(h->ev_int[n & 1], h->st2));
+            h->launches += 2;
+            cur ^= 1;
+            if ((rc = exchange_nccl_plan(h, HW_PLAN_FUSED_EL2, cur))) return rc;
+        }
+        if (nt > 0) CU(cudaStreamWaitEvent(h->st, h->ev_int[(nt - 1) & 1], 0));
     } else if (h->fused_el) {  // one-pass 2D elastic kernel, ping-pong A <-> B: step n reads buffer n % 2
         const StreamIO IO = stream_io(h, C);
         int cur = 0;

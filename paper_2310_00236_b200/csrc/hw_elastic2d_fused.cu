@@ -92,8 +92,22 @@ __global__ void __launch_bounds__(512, 1)
     const int64_t pitch = P.g.slab;  // row stride (2D: nm = 1)
     const int nx = (int)P.g.nx;
     const int ri = (int)P.sxx.rows, rh = (int)P.sxs.rows;  // integer / half sub-grid rows
-    const int nb = gridDim.x, b = blockIdx.x;
-    const int y0 = (int)((int64_t)b * ri / nb), y1 = (int)((int64_t)(b + 1) * ri / nb);
+    const int b = blockIdx.x;
+    int y0, y1, pidx = b, nb = gridDim.x;  // this CTA's rows, its energy-partial slot, CTAs of the whole step
+    if (in.band == 1) {  // edge bands: launched ahead of the interior so the halo exchange overlaps it
+        y0 = b == 0 ? 0 : ri - in.edge;
+        y1 = b == 0 ? in.edge : ri;
+        nb = in.nb_total;
+    } else if (in.band == 2) {
+        const int64_t nin = ri - 2 * in.edge;
+        y0 = in.edge + (int)((int64_t)b * nin / gridDim.x);
+        y1 = in.edge + (int)((int64_t)(b + 1) * nin / gridDim.x);
+        pidx = 2 + b;
+        nb = in.nb_total;
+    } else {
+        y0 = (int)((int64_t)b * ri / nb);
+        y1 = (int)((int64_t)(b + 1) * ri / nb);
+    }
     const int F0 = y0 - 3, NI = y1 - y0 + 6;
     const int tid = threadIdx.x, x = tid * ECPT;
     constexpr bool comp = V != 0;
@@ -110,21 +124,27 @@ __global__ void __launch_bounds__(512, 1)
     auto trow = [&](int r, int rows) {  // (free surface: stay inside the G ghost slabs)
         return fs ? (int64_t)(r < -G ? -G : (r > rows + G - 1 ? rows + G - 1 : r)) : (int64_t)orow(r, rows);
     };
+    // row of a TMA load: on a slab the first iterations of the top band ask for rows -4 and -5 (values never
+    // used: no velocity is computed before iteration 3) -- keep the copy inside the G ghost rows
+    auto lrow = [&](int r, int rows) {
+        const int o = orow(r, rows);
+        return (int64_t)(slabm ? (o < -G ? -G : (o > rows + G - 1 ? rows + G - 1 : o)) : o);
+    };
     auto issue_l = [&](int i) {  // tap rows of iteration i (front F0 + i)
         const int F = F0 + i, ls = i % LR;
         mbar_arrive_expect_tx(&S.lbar[ls], L_N * rb);
         tma_load_1d(S.l(ls, L_SXS), in.sxs + trow(F, rh) * pitch, rb, &S.lbar[ls]);
         tma_load_1d(S.l(ls, L_SSS), in.sss + trow(F, ri) * pitch, rb, &S.lbar[ls]);
-        tma_load_1d(S.l(ls, L_SXX), in.sxx + (int64_t)orow(F - 1, ri) * pitch, rb, &S.lbar[ls]);
+        tma_load_1d(S.l(ls, L_SXX), in.sxx + lrow(F - 1, ri) * pitch, rb, &S.lbar[ls]);
     };
     auto issue_a = [&](int i) {  // velocity own rows of iteration i
         const int F = F0 + i;
         mbar_arrive_expect_tx(S.abar(), (comp ? 4 : 2) * rb);
-        tma_load_1d(S.a(A_VX), in.vx + (int64_t)orow(F - 1, ri) * pitch, rb, S.abar());
-        tma_load_1d(S.a(A_VS), in.vs + (int64_t)orow(F - 2, rh) * pitch, rb, S.abar());
+        tma_load_1d(S.a(A_VX), in.vx + lrow(F - 1, ri) * pitch, rb, S.abar());
+        tma_load_1d(S.a(A_VS), in.vs + lrow(F - 2, rh) * pitch, rb, S.abar());
         if (comp) {
-            tma_load_1d(S.a(A_RVX), in.rvx + (int64_t)orow(F - 1, ri) * pitch, rb, S.abar());
-            tma_load_1d(S.a(A_RVS), in.rvs + (int64_t)orow(F - 2, rh) * pitch, rb, S.abar());
+            tma_load_1d(S.a(A_RVX), in.rvx + lrow(F - 1, ri) * pitch, rb, S.abar());
+            tma_load_1d(S.a(A_RVS), in.rvs + lrow(F - 2, rh) * pitch, rb, S.abar());
         }
     };
     // stress residual rows of iteration i (compensated runs; only iterations with an own
@@ -132,9 +152,9 @@ __global__ void __launch_bounds__(512, 1)
     auto issue_b = [&](int i) {
         const int F = F0 + i;
         mbar_arrive_expect_tx(S.bbar(), 3 * rb);
-        tma_load_1d(S.b(B_RSXX), in.rsxx + (int64_t)orow(F - 3, ri) * pitch, rb, S.bbar());
-        tma_load_1d(S.b(B_RSSS), in.rsss + (int64_t)orow(F - 3, ri) * pitch, rb, S.bbar());
-        tma_load_1d(S.b(B_RSXS), in.rsxs + (int64_t)orow(F - 3, rh) * pitch, rb, S.bbar());
+        tma_load_1d(S.b(B_RSXX), in.rsxx + lrow(F - 3, ri) * pitch, rb, S.bbar());
+        tma_load_1d(S.b(B_RSSS), in.rsss + lrow(F - 3, ri) * pitch, rb, S.bbar());
+        tma_load_1d(S.b(B_RSXS), in.rsxs + lrow(F - 3, rh) * pitch, rb, S.bbar());
     };
     if (tid == 0) {
         for (int q = 0; q < LR + 2; q++) mbar_init(&S.lbar[q], 1);
@@ -431,7 +451,7 @@ __global__ void __launch_bounds__(512, 1)
     mask |= e_nonfinite(acc[4]) << P.sxs.bit;
     record_failure(P.ctrl, n, mask);
     if constexpr (!SAMPLE) return;
-    block_partials(e, P.partials);
+    block_partials(e, P.partials, pidx);
     __threadfence();
     __syncthreads();
     __shared__ unsigned int is_last;

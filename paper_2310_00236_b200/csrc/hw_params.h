@@ -126,6 +126,10 @@ struct El2In {
     int32_t slab, top, bot;
     int32_t vsrc;   // a v_slow point source on local row vsrc_s (-3 .. rows + 2: halo rows included)
     int64_t vsrc_s;
+    // overlapped halo exchange (NCCL slab): band 1 = the two edge bands [0, edge) and [rows - edge, rows)
+    // (every row the exchange sends), 2 = the interior (reads no ghost row), 0 = every row;
+    // nb_total = CTAs of the step over both launches (energy partial slots, last-CTA count)
+    int32_t band, edge, nb_total, pad;
 };
 bool el2d_fused_eligible(int64_t nx, int64_t ns, int max_smem);
 cudaError_t el2d_fused_prepare(int64_t nx);

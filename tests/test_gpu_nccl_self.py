@@ -80,10 +80,10 @@ def _acoustic3d_onepass(**kw):  # config 3's one-pass kernel on the NCCL transpo
     return s, st
 
 
-def _elastic2d_onepass(**kw):  # config 4's one-pass kernel on the NCCL transport (HW_PLAN_FUSED_EL2)
+def _elastic2d_onepass(fs=True, **kw):  # config 4's one-pass kernel on the NCCL transport (HW_PLAN_FUSED_EL2)
     from test_gpu_slabs import _elastic2d_onepass as mk
 
-    s, st = mk(1)
+    s, st = mk(1, fs)
     if kw.get("distributed"):
         s = hw.ElasticSolver(s.grid, s.medium, s.source, stencil_precision=s.stencil_precision,
                              receivers=s.receivers, energy_every=s.energy_every, distributed=True)
@@ -92,6 +92,7 @@ def _elastic2d_onepass(**kw):  # config 4's one-pass kernel on the NCCL transpor
 
 @pytest.mark.parametrize("make,variant", [(_acoustic, hw.Variant.OP3), (_elastic, hw.Variant.OP6),
                                           (_elastic2d_onepass, hw.Variant.OP6),
+                                          (lambda **kw: _elastic2d_onepass(False, **kw), hw.Variant.OP6),
                                           (_acoustic3d, hw.Variant.OP3), (_elastic3d_onepass, hw.Variant.OP6),
                                           (_acoustic3d_onepass, hw.Variant.OP3)])
 def test_nccl_transport_equals_single_process(one_rank_job, make, variant):
@@ -150,3 +151,25 @@ def test_nccl_el3_overlapped_device_resident_run(one_rank_job):
     assert ms > 0 and b.transport() == 2 and b.kernel_path() == "fused3d-el"
     for n in a.FIELDS:
         assert_same_bits(getattr(sb, n).values, getattr(sa, n).values, n)
+
+
+@pytest.mark.parametrize("fs", [True, False])
+@pytest.mark.parametrize("variant", [None, hw.Variant.OP6])
+def test_nccl_el2_overlapped_device_resident_run(one_rank_job, fs, variant):
+    """Config 4's one-pass kernel on the NCCL transport, overlapped: per step the two 8-row edge bands
+    and the exchange on one stream, the interior bands on another (two launches per step), equals the
+    single process (free surface: images at the global ends, no exchange; periodic: self exchange)."""
+    a, sa = _elastic2d_onepass(fs)
+    oa = a.run(variant, sa)
+    b, sb = _elastic2d_onepass(fs, distributed=True)
+    b.upload(sb)
+    ms = b.run_device(variant, 0, b.grid.nt)
+    b.download(sb)
+    assert ms > 0 and b.transport() == 2 and b.kernel_path() == "fused2d-el"
+    assert b.last_launch_count() >= 2 * b.grid.nt
+    for n in a.FIELDS:
+        assert_same_bits(getattr(sb, n).values, getattr(sa, n).values, n)
+    _, sc = _elastic2d_onepass(fs)  # the host path (traces, energy) through the same overlapped loop
+    oc = b.run(variant, sc)
+    np.testing.assert_array_equal(np.array([t.samples for t in oc.traces]), np.array([t.samples for t in oa.traces]))
+    np.testing.assert_allclose(oc.energy.values, oa.energy.values, rtol=1e-12)

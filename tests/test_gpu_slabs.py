@@ -197,17 +197,16 @@ def test_acoustic_3d_onepass_slabs_equal_single_domain(slabs, prec, variant):
     np.testing.assert_array_equal(ob.energy.values, oa.energy.values)  # plane-ordered: bit-identical for any slabs
 
 
-def _elastic2d_onepass(slabs, fs=True, nt=23, kind=hw.SourceKind.VY_POINT, src_y=45):
+def _elastic2d_onepass(slabs, fs=True, nt=23, kind=hw.SourceKind.VY_POINT, src_y=45, nx=256, ny=120):
     """Config 4's one-pass kernel on slabs (HW_PLAN_FUSED_EL2: five fields + velocity residuals, 3 rows):
     the CTAs at a slab edge recompute the halo velocity rows from the ghosts; free-surface images only at
     the global ends."""
-    nx, ny = 256, 120
     med = hw.build_layered_elastic(nx, ny, [(0.4, 2.0, 2.0, 1.0), (1.0, 2.3, 2.8, 1.4)])
     g = hw.GridSpec(nx, ny, 1.0 / nx, float(np.float16(0.3 / nx / med.c_max())), nt,
                     bc_y=hw.Boundary.FREE_SURFACE if fs else hw.Boundary.PERIODIC)
     src = hw.SourceSpec(kind, 100, src_y, hw.RickerSpec(1 / (10 / nx), amplitude=20.0))
     s = hw.ElasticSolver(g, med, src, stencil_precision=hw.Precision.FP16, energy_every=4, slabs=slabs,
-                         receivers=((100, src_y), (10, 0), (250, 119), (7, 44), (8, 46), (9, 15)))
+                         receivers=((100, src_y), (10, 0), (250, ny - 1), (7, 44), (8, 46), (9, 15)))
     st = s.new_state()
     rng = np.random.default_rng(13)
     st.sxx.values = rng.uniform(-0.1, 0.1, st.sxx.values.shape).astype(np.float16)
@@ -223,6 +222,23 @@ def _elastic2d_onepass(slabs, fs=True, nt=23, kind=hw.SourceKind.VY_POINT, src_y
 def test_elastic_2d_onepass_slabs_equal_single_domain(hwopt, slabs, fs, kind, src_y):
     hwopt(small=0)
     a, sa, b, sb = _pair(lambda k: _elastic2d_onepass(k, fs, kind=kind, src_y=src_y), slabs)
+    ref = oracle.run_solver(a, hw.Variant.OP6, sa)
+    oa = a.run(hw.Variant.OP6, sa)
+    ob = b.run(hw.Variant.OP6, sb)
+    assert a.kernel_path() == b.kernel_path() == "fused2d-el" and b.transport() == 1
+    for j, n in enumerate(a.FIELDS):
+        assert_same_bits(getattr(sa, n).values, ref["fields"][j], n)
+    _compare(a, sa, oa, b, sb, ob)
+
+
+@pytest.mark.parametrize("nx,ny,slabs", [(1024, 256, 2), (2048, 96, 3), (4096, 64, 2)])
+@pytest.mark.parametrize("fs", [True, False])
+def test_elastic_2d_onepass_slabs_wide_rows(hwopt, nx, ny, slabs, fs):
+    """Wide rows (4 to 16 warps per CTA; the narrow cases above run one warp): the top band's first
+    TMA requests ask for rows -4 and -5, which must stay inside the 3 ghost rows of a slab (they ran
+    off the allocation by up to 16 KB at nx = 4096 -- an illegal address in round 2's first build)."""
+    hwopt(small=0)
+    a, sa, b, sb = _pair(lambda k: _elastic2d_onepass(k, fs, nt=9, nx=nx, ny=ny), slabs)
     ref = oracle.run_solver(a, hw.Variant.OP6, sa)
     oa = a.run(hw.Variant.OP6, sa)
     ob = b.run(hw.Variant.OP6, sb)

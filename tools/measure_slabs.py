@@ -1,8 +1,8 @@
-"""Decomposed-compute efficiency on one B200: BASELINE config 5 (512^3, op6), config 3 (512^3, op3)
-or config 2 (4096^2, op3) run as an in-process slab group of N = 1, 2, 4, 8 slabs on one GPU (the multi-GPU path's
+"""Decomposed-compute efficiency on one B200: BASELINE config 5 (512^3, op6), config 3 (512^3, op3; 3f32: its
+fp32 naive arm), config 4 (4096^2 elastic op6, free surface) or config 2 (4096^2, op3) run as an in-process slab group of N = 1, 2, 4, 8 slabs on one GPU (the multi-GPU path's
 kernels, exchange plan and halo recomputation; the exchange is a peer copy on the same device, not
 overlapped) -- cell-steps/s relative to the single domain.
-python tools/measure_slabs.py [5|3|2] [nt] -> one JSON line per N."""
+python tools/measure_slabs.py [5|3|3f32|4|2] [nt] -> one JSON line per N."""
 import ctypes
 import json
 import sys
@@ -26,14 +26,18 @@ for n in (1, 2, 4, 8):
         st = s.new_state()
         bench.init_config5(st)
         v, cells = hw.Variant.OP6, 512 ** 3
-    elif cfg == "3":
+    elif cfg in ("3", "3f32"):
         if n == 1:
             c3 = bench.smooth_velocity(512)
-        s0 = bench.make_config3(hw, hw.Precision.FP16, nt=nt, c=c3)
-        s = hw.AcousticSolver(s0.grid, s0.medium, stencil_precision=hw.Precision.FP16, energy_every=10, slabs=n)
+        prec = hw.Precision.FP16 if cfg == "3" else hw.Precision.FP32
+        s = bench.make_config3(hw, prec, nt=nt, c=c3, slabs=n)
         st = s.new_state()
         bench.init_config3(st)
-        v, cells = hw.Variant.OP3, 512 ** 3
+        v, cells = (hw.Variant.OP3 if cfg == "3" else None), 512 ** 3
+    elif cfg == "4":
+        s = bench.make_config4(hw, nt=nt, slabs=n)
+        st = s.new_state()
+        v, cells = hw.Variant.OP6, 4096 * 4097
     else:
         s0 = bench.make_config2(hw, nt=nt)
         s = hw.AcousticSolver(s0.grid, s0.medium, s0.source, stencil_precision=hw.Precision.FP16,
