@@ -210,6 +210,11 @@ double hw_last_kernel_ms(const hw_solver* h);
  * *first_pair the first failing (a << 16 | b) bit patterns. */
 int hw_selftest_div16(int32_t device, uint64_t* mismatches, uint32_t* first_pair);
 
+/* Self-test of the guarded allocations (option "guard"): allocates 4096 bytes and reads the byte at
+ * `offset` from a kernel.  With guard = 1, offset -1 faults (HW_ECUDA; the CUDA context is lost, so call
+ * it from a process of its own); with guard = 2, offset 4096 faults; offsets 0 .. 4095 return HW_OK. */
+int hw_selftest_guard(int32_t device, int64_t offset);
+
 /* The exhaustive per-divisor table behind the cheap binary16 division: bit b of
  * the 1024 words is set iff fl16(fl32(a * rcp_rn(b))) == fl16(a / b) for every
  * binary16 a (b = positive finite binary16 bit pattern).  Computed on `device`. */
@@ -230,6 +235,8 @@ int hw_plane_div_mode(const hw_solver* h, int32_t plane);
  *   "fused_el3" 1 one-pass 3D elastic kernel (2nd order, media constant along x) | 0 two-phase
  *   "el3_group" 4 at most this many CTAs of the one-pass 3D elastic kernel stream adjacent tiles
  *   "ac3_group" 4 the same for the one-pass 3D acoustic kernels (binary16 and binary32)
+ *   "guard"     0 | 1 | 2 every device buffer in its own mapping between unmapped pages, starting at the
+ *               mapping's start (1) or ending at its end (2): out-of-bounds accesses fault (tests)
  *   "nccl_self" 0 | 1 a one-rank job given an NCCL id takes the NCCL transport (tests)
  * HW_EINVAL for an unknown name or an out-of-range value. */
 int hw_set_option(const char* name, int64_t value);

@@ -44,7 +44,7 @@ EXPORTED = (
     "hw_get_state", "hw_run", "hw_run_device", "hw_last_launch_count", "hw_kernel_path", "hw_transport",
     "hw_last_kernel_ms", "hw_last_error", "hw_version", "hw_selftest_div16",
     "hw_cheap_div_table", "hw_plane_div_mode", "hw_nccl_unique_id", "hw_create_group", "hw_run_group",
-    "hw_set_option", "hw_get_option", "hw_exchange_plan",
+    "hw_set_option", "hw_get_option", "hw_exchange_plan", "hw_selftest_guard",
 )
 
 # hw_plan_kind
@@ -129,6 +129,8 @@ def load() -> ctypes.CDLL:
     lib.hw_last_error.restype = ctypes.c_char_p
     lib.hw_selftest_div16.argtypes = [i32, P(ctypes.c_uint64), P(ctypes.c_uint32)]
     lib.hw_selftest_div16.restype = ctypes.c_int
+    lib.hw_selftest_guard.argtypes = [i32, ctypes.c_int64]
+    lib.hw_selftest_guard.restype = ctypes.c_int
     lib.hw_cheap_div_table.argtypes = [i32, P(ctypes.c_uint32)]
     lib.hw_cheap_div_table.restype = ctypes.c_int
     lib.hw_plane_div_mode.argtypes = [vp, i32]

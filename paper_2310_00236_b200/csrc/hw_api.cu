@@ -4,6 +4,7 @@
 // One hw_solver per rank/GPU.  The whole time loop of AcousticSolver.run /
 // ElasticSolver.run (acoustic.py:185-236, elastic.py:242-296) is issued from here
 // onto one CUDA stream; the host synchronises once per hw_run.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -15,6 +16,8 @@
 #include <vector>
 #include <algorithm>
 #include <array>
+#include <map>
+#include <mutex>
 
 #include "../../include/halfwave_b200.h"
 #include "hw_params.h"
@@ -45,6 +48,7 @@ Option g_opts[] = {
     {"fused_el3", 1, 0, 1, "one-pass 3D elastic kernel (2nd order, media constant along x) | 0 two-phase kernels"},
     {"el3_group", 4, 1, 4, "one-pass 3D elastic kernel: at most this many CTAs stream adjacent tiles side by side"},
     {"ac3_group", 4, 1, 4, "one-pass 3D acoustic kernels: at most this many CTAs stream adjacent tiles side by side"},
+    {"guard", 0, 0, 2, "device allocations between unmapped pages (tests): 1 = start at a mapping start, 2 = end at a mapping end"},
     {"nccl_self", 0, 0, 1, "a one-rank job with an NCCL id takes the NCCL transport (self exchange: tests)"},
 };
 int64_t opt(const char* name) {
@@ -57,6 +61,95 @@ int fail(int code, const std::string& msg) {
     g_err = msg;
     return code;
 }
+
+// ---------------------------------------------------------------- guarded device allocations
+// Option "guard" (tests; compute-sanitizer's memcheck is not available on every box): every device
+// buffer of the library becomes its own virtual-memory mapping with unmapped pages on both sides,
+// starting at the mapping's first byte (guard = 1: a read or write before the buffer faults) or ending
+// at its last (guard = 2: one past the end faults, to 256-byte rounding).  An out-of-bounds access of
+// any kernel, TMA requests included, then stops the run with an illegal-address error instead of
+// reading a neighbouring allocation unnoticed.  guard = 0 (the default) is plain cudaMalloc.
+struct VmmRec {
+    CUdeviceptr va, mapped;
+    size_t span, msize;
+    CUmemGenericAllocationHandle hnd;
+};
+std::map<void*, VmmRec> g_vmm;
+std::mutex g_vmm_mu;
+
+template <typename F>
+bool drv(const char* name, F* fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || !p) return false;
+    *fn = reinterpret_cast<F>(p);
+    return true;
+}
+
+cudaError_t hw_dev_alloc(void** out, size_t bytes) {
+    const int64_t g = opt("guard");
+    if (g == 0) return ::cudaMalloc(out, bytes);
+    CUresult (*memCreate)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long);
+    CUresult (*memGran)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags);
+    CUresult (*memReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
+    CUresult (*memMap)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
+    CUresult (*memAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+    if (!drv("cuMemCreate", &memCreate) || !drv("cuMemGetAllocationGranularity", &memGran) ||
+        !drv("cuMemAddressReserve", &memReserve) || !drv("cuMemMap", &memMap) || !drv("cuMemSetAccess", &memAccess))
+        return cudaErrorNotSupported;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    cudaFree(nullptr);  // (a context on this device)
+    CUmemAllocationProp prop = {};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = dev;
+    size_t gran = 0;
+    if (memGran(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM) != CUDA_SUCCESS || !gran) return cudaErrorUnknown;
+    const size_t need = ((bytes ? bytes : 1) + 255) / 256 * 256;
+    VmmRec r;
+    r.msize = (need + gran - 1) / gran * gran;
+    r.span = r.msize + 2 * gran;
+    if (memReserve(&r.va, r.span, gran, 0, 0) != CUDA_SUCCESS) return cudaErrorMemoryAllocation;
+    if (memCreate(&r.hnd, r.msize, &prop, 0) != CUDA_SUCCESS) return cudaErrorMemoryAllocation;
+    r.mapped = r.va + gran;
+    if (memMap(r.mapped, r.msize, 0, r.hnd, 0) != CUDA_SUCCESS) return cudaErrorMemoryAllocation;
+    CUmemAccessDesc acc = {};
+    acc.location = prop.location;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    if (memAccess(r.mapped, r.msize, &acc, 1) != CUDA_SUCCESS) return cudaErrorMemoryAllocation;
+    void* p = reinterpret_cast<void*>(g == 1 ? r.mapped : r.mapped + (r.msize - need));
+    std::lock_guard<std::mutex> lk(g_vmm_mu);
+    g_vmm[p] = r;
+    *out = p;
+    return cudaSuccess;
+}
+
+cudaError_t hw_dev_free(void* p) {
+    if (!p) return cudaSuccess;
+    VmmRec r;
+    {
+        std::lock_guard<std::mutex> lk(g_vmm_mu);
+        auto it = g_vmm.find(p);
+        if (it == g_vmm.end()) return ::cudaFree(p);
+        r = it->second;
+        g_vmm.erase(it);
+    }
+    CUresult (*memUnmap)(CUdeviceptr, size_t);
+    CUresult (*memRelease)(CUmemGenericAllocationHandle);
+    CUresult (*memFree)(CUdeviceptr, size_t);
+    if (!drv("cuMemUnmap", &memUnmap) || !drv("cuMemRelease", &memRelease) || !drv("cuMemAddressFree", &memFree))
+        return cudaErrorNotSupported;
+    cudaDeviceSynchronize();
+    memUnmap(r.mapped, r.msize);
+    memRelease(r.hnd);
+    memFree(r.va, r.span);
+    return cudaSuccess;
+}
+// every allocation below goes through the two functions above
+#define cudaMalloc(p, n) hw_dev_alloc((void**)(p), (size_t)(n))
+#define cudaFree(p) hw_dev_free((void*)(p))
 
 #define CU(call)                                                                              \
     do {                                                                                      \
@@ -2220,6 +2313,24 @@ int32_t hw_transport(const hw_solver* h) { return h ? h->transport : -1; }
 double hw_last_kernel_ms(const hw_solver* h) { return h ? h->kernel_ms : 0.0; }
 
 const char* hw_last_error(void) { return g_err.c_str(); }
+
+__global__ void k_selftest_guard(const unsigned char* p, int64_t off, unsigned int* sink) {
+    *sink = p[off];
+}
+
+int hw_selftest_guard(int32_t device, int64_t offset) {
+    CU(cudaSetDevice(device));
+    unsigned char* buf = nullptr;
+    unsigned int* sink = nullptr;
+    CU(cudaMalloc(&buf, 4096));
+    CU(cudaMalloc(&sink, 4));
+    k_selftest_guard<<<1, 1>>>(buf, offset, sink);
+    CU(cudaGetLastError());
+    CU(cudaDeviceSynchronize());  // an unmapped address ends here (the context is lost after that)
+    cudaFree(buf);
+    cudaFree(sink);
+    return HW_OK;
+}
 
 int hw_selftest_div16(int32_t device, uint64_t* mismatches, uint32_t* first_pair) {
     CU(cudaSetDevice(device));
