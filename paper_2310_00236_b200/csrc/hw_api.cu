@@ -730,6 +730,28 @@ int check_desc(const hw_desc* d) {
 }
 
 // The slab's field buffers, ghost policies, medium, source and receivers.
+// Ping-pong partner buffers (B) of the one-pass kernels: same shape as the fields' own buffers (A).
+int alloc_partner_buffers(hw_solver* h) {
+    const int esz = lane_bytes(h->LU);
+    for (int j = 0; j < 2 * h->nsol; j++) {
+        const int f = h->ext[j % h->nsol];
+        const size_t bytes = (size_t)(field_rows(h, f) + 2 * G) * h->g.slab * esz;
+        if (cudaMalloc(&h->mem_b[j], bytes) != cudaSuccess) return fail(HW_ECUDA, "out of memory (B)");
+        CU(cudaMemset(h->mem_b[j], 0, bytes));
+    }
+    return HW_OK;
+}
+
+// Second stream + events of an NCCL slab's overlapped step (edge bands and exchange | interior bands).
+int make_overlap_streams(hw_solver* h) {
+    CU(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; k++) {
+        CU(cudaEventCreateWithFlags(&h->ev_edge[k], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&h->ev_int[k], cudaEventDisableTiming));
+    }
+    return HW_OK;
+}
+
 int setup_handle(hw_solver* h) {
     const hw_desc* desc = &h->d;
     int rc;
@@ -793,23 +815,14 @@ int setup_handle(hw_solver* h) {
         // exchanged once per step; periodic slow axis only, as the acoustic solver)
         if (want && h->ac && !h->d3 && h->LS == 16 && h->LU == 16 && !h->fs && field_rows(h, F_P) >= 8 &&
             fused2d_eligible(desc->nx, dev_smem)) {
-            for (int j = 0; j < 2 * h->nsol; j++) {
-                int f = h->ext[j % h->nsol];
-                size_t bytes = (size_t)(field_rows(h, f) + 2 * G) * h->g.slab * esz;
-                if (cudaMalloc(&h->mem_b[j], bytes) != cudaSuccess) return fail(HW_ECUDA, "out of memory (B)");
-                CU(cudaMemset(h->mem_b[j], 0, bytes));
-            }
+            if ((rc = alloc_partner_buffers(h))) return rc;
             if (fused2d_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "fused kernel setup failed");
             int64_t nbf = field_rows(h, F_P) / 4;
             if (nbf < 1) nbf = 1;
             h->fused_blocks = (int)(nbf < nsm ? nbf : nsm);
             h->fused = true;
             if (h->transport == 2 && field_rows(h, F_P) >= 5 * FUSED_EDGE) {  // overlapped halo exchange
-                CU(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
-                for (int k = 0; k < 2; k++) {
-                    CU(cudaEventCreateWithFlags(&h->ev_edge[k], cudaEventDisableTiming));
-                    CU(cudaEventCreateWithFlags(&h->ev_int[k], cudaEventDisableTiming));
-                }
+                if ((rc = make_overlap_streams(h))) return rc;
                 int64_t ni = (field_rows(h, F_P) - 2 * FUSED_EDGE) / 4;
                 h->nb_int = (int)(ni < nsm - 2 ? ni : nsm - 2);
             }
@@ -852,12 +865,7 @@ int setup_handle(hw_solver* h) {
         // HW_PLAN_FUSED_EL2 once per step): ping-pong partner buffers
         if (want && !h->small_el && opt("fused_el") == 1 && !h->ac && !h->d3 && h->LS == 16 &&
             h->LU == 16 && el2d_fused_eligible(desc->nx, field_rows(h, F_SXS), dev_smem)) {
-            for (int j = 0; j < 2 * h->nsol; j++) {
-                int f = h->ext[j % h->nsol];
-                size_t bytes = (size_t)(field_rows(h, f) + 2 * G) * h->g.slab * esz;
-                if (cudaMalloc(&h->mem_b[j], bytes) != cudaSuccess) return fail(HW_ECUDA, "out of memory (B)");
-                CU(cudaMemset(h->mem_b[j], 0, bytes));
-            }
+            if ((rc = alloc_partner_buffers(h))) return rc;
             if (el2d_fused_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "fused elastic kernel setup failed");
             int64_t nbs = max_rows / 4;
             if (nbs < 1) nbs = 1;
@@ -866,11 +874,7 @@ int setup_handle(hw_solver* h) {
             // NCCL slab: the two edge bands + the exchange on st, the interior bands on st2 (as the
             // fused 2D acoustic kernel)
             if (h->transport == 2 && field_rows(h, F_SXS) >= 5 * FUSED_EDGE) {
-                CU(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
-                for (int k = 0; k < 2; k++) {
-                    CU(cudaEventCreateWithFlags(&h->ev_edge[k], cudaEventDisableTiming));
-                    CU(cudaEventCreateWithFlags(&h->ev_int[k], cudaEventDisableTiming));
-                }
+                if ((rc = make_overlap_streams(h))) return rc;
                 int64_t ni = (field_rows(h, F_SXS) - 2 * FUSED_EDGE) / 4;
                 h->nb_int = (int)(ni < nsm - 2 ? ni : nsm - 2);
             }
@@ -888,12 +892,7 @@ int setup_handle(hw_solver* h) {
         const bool f3_ok = opt("fused3") == 1;
         if (want && f3_ok && h->ac && h->d3 && h->LS == 16 && h->LU == 16 && !h->fs &&
             ac3d_fused_eligible(desc->nx, desc->nm, field_rows(h, F_P), h->g.pitch, desc->order, dev_smem)) {
-            for (int j = 0; j < 2 * h->nsol; j++) {
-                int f = h->ext[j % h->nsol];
-                size_t bytes = (size_t)(field_rows(h, f) + 2 * G) * h->g.slab * esz;
-                if (cudaMalloc(&h->mem_b[j], bytes) != cudaSuccess) return fail(HW_ECUDA, "out of memory (B)");
-                CU(cudaMemset(h->mem_b[j], 0, bytes));
-            }
+            if ((rc = alloc_partner_buffers(h))) return rc;
             if (ac3d_fused_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "fused 3D kernel setup failed");
             const int64_t tiles = desc->nm / (4096 / desc->nx), units = tiles * max_rows;
             int64_t nbs = units / 4;
@@ -912,12 +911,7 @@ int setup_handle(hw_solver* h) {
         // the one-pass 3D acoustic step in binary32 lanes (BASELINE config 3's fp32 arm)
         if (want && f3_ok && h->ac && h->d3 && h->LS == 32 && h->LU == 32 && !h->fs &&
             ac3d_fused32_eligible(desc->nx, desc->nm, field_rows(h, F_P), h->g.pitch, desc->order, dev_smem)) {
-            for (int j = 0; j < 2 * h->nsol; j++) {
-                int f = h->ext[j % h->nsol];
-                size_t bytes = (size_t)(field_rows(h, f) + 2 * G) * h->g.slab * esz;
-                if (cudaMalloc(&h->mem_b[j], bytes) != cudaSuccess) return fail(HW_ECUDA, "out of memory (B)");
-                CU(cudaMemset(h->mem_b[j], 0, bytes));
-            }
+            if ((rc = alloc_partner_buffers(h))) return rc;
             if (ac3d_fused32_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "fused 3D fp32 kernel setup failed");
             const int64_t tiles = desc->nm / (2048 / desc->nx), units = tiles * max_rows;
             int64_t nbs = units / 4;
@@ -949,12 +943,7 @@ int setup_handle(hw_solver* h) {
         if (!h->ac && h->d3) fill_params(h, EP);
         if (want && opt("fused_el3") == 1 && !h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
             el3d_fused_eligible(EP, desc->nx, desc->nm, field_rows(h, F_SXX), h->g.pitch, desc->order, dev_smem)) {
-            for (int j = 0; j < 2 * h->nsol; j++) {
-                int f = h->ext[j % h->nsol];
-                size_t bytes = (size_t)(field_rows(h, f) + 2 * G) * h->g.slab * esz;
-                if (cudaMalloc(&h->mem_b[j], bytes) != cudaSuccess) return fail(HW_ECUDA, "out of memory (B)");
-                CU(cudaMemset(h->mem_b[j], 0, bytes));
-            }
+            if ((rc = alloc_partner_buffers(h))) return rc;
             if (el3d_fused_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "fused 3D elastic setup failed");
             h->el3_slab = h->world > 1 || h->transport != 0;
             h->el3_cm = el3d_fused_coef_rows(EP);
@@ -986,11 +975,7 @@ int setup_handle(hw_solver* h) {
             // slabs on st2; CTAs split so both launches take about as long (an edge segment of
             // 2 slabs costs ~3 slabs: the ring fill)
             if (h->transport == 2 && max_rows >= 5 * EL3_EDGE) {
-                CU(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
-                for (int k = 0; k < 2; k++) {
-                    CU(cudaEventCreateWithFlags(&h->ev_edge[k], cudaEventDisableTiming));
-                    CU(cudaEventCreateWithFlags(&h->ev_int[k], cudaEventDisableTiming));
-                }
+                if ((rc = make_overlap_streams(h))) return rc;
                 const double we = 3.0 * 2 * EL3_EDGE, wi = (double)(max_rows - 2 * EL3_EDGE);
                 int ne = (int)(nsm * we / (we + wi) + 0.5);
                 ne = ne < 1 ? 1 : (ne > nsm - 1 ? nsm - 1 : ne);
