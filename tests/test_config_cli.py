@@ -123,6 +123,23 @@ def test_cli_desk_run_matches_reference_outputs(tmp_path, preset):
     np.testing.assert_allclose(got[:, 1], want[:, 1], rtol=1e-12)
 
 
+@pytest.mark.gpu
+def test_cli_mid_run_range_failure_matches_reference(tmp_path):
+    """A run that passes the static audit and goes non-finite mid-wavelet (reference behaviour:
+    test_cli.py:311-327): same exit code, same failing step and field in summary.json as the
+    reference CLI on the same INI file (tests/golden/cli/range-failure/, make_cli_golden.py)."""
+    import json
+
+    gold = GOLD / "range-failure"
+    r = subprocess.run([sys.executable, "-m", "paper_2310_00236_b200.cli", "run", "--config", str(gold / "case.ini"),
+                        "--out", str(tmp_path)], cwd=ROOT, capture_output=True, text=True)
+    assert r.returncode == int((gold / "exit_code.txt").read_text()) == 1
+    got = json.loads((tmp_path / "overdrive" / "summary.json").read_text())
+    want = json.loads((gold / "summary.json").read_text())
+    assert got["range_failure"] == want["range_failure"] == {"field": "Vy", "step": 83}
+    assert "non-finite" in r.stderr
+
+
 def test_ini_rigid_walls(tmp_path):
     """grid.bc_x / grid.bc_y = rigid (p = 0 walls, extension) parse into a rigid GridSpec."""
     ini = tmp_path / "box.ini"
