@@ -298,14 +298,22 @@ __global__ void __launch_bounds__(Q3T, 1)
     // (L2 hits instead of DRAM re-reads); the (tile group, slab) units are split evenly over the groups
     const int grp = in_.group, ngrp = (int)gridDim.x / grp, gid = (int)blockIdx.x / grp, gr = (int)blockIdx.x % grp;
     const int tiles = nm / TM / grp;  // tile groups
-    const int64_t U = (int64_t)tiles * ns;
+    // Band mode (NCCL slab, exchange overlapped): 1 = the edge slabs 0 and ns-1 (every row the halo
+    // exchange sends; the only slabs that read ghost rows), 2 = the interior [1, ns-1), 0 = every slab.
+    // t indexes the band's slabs; a segment never straddles the two edge slabs.
+    const int E = in_.edge, bm = in_.band;
+    const int nsl = bm == 0 ? ns : (bm == 1 ? 2 * E : ns - 2 * E);
+    auto slab_of = [&](int t) { return bm == 0 ? t : (bm == 1 ? (t < E ? t : ns - 2 * E + t) : E + t); };
+    const int64_t U = (int64_t)tiles * nsl;
     int64_t u = (int64_t)gid * U / ngrp;
     const int64_t u1 = (int64_t)(gid + 1) * U / ngrp;
     int gi = 0, gk = 0;  // running tap / own use counters (slot and parity continue across segments)
     while (u < u1) {
-        const int tile = (int)(u / ns) * grp + gr, sb = (int)(u % ns);
-        const int se = (int)min((int64_t)ns, sb + (u1 - u));
-        u += se - sb;
+        const int t0 = (int)(u % nsl);
+        int te = (int)min((int64_t)nsl, t0 + (u1 - u));
+        if (bm == 1 && t0 < E) te = min(te, E);
+        const int tile = (int)(u / nsl) * grp + gr, sb = slab_of(t0), se = sb + (te - t0);
+        u += te - t0;
         const int m0 = tile * TM, m = m0 + j;
         const int mh = m0 == 0 ? nm - 1 : m0 - 1;  // mid halo row (periodic)
         const int F0 = sb - 1, NI = se - sb + 2;
@@ -495,7 +503,9 @@ __global__ void __launch_bounds__(Q3T, 1)
     __threadfence();
     __syncthreads();
     __shared__ unsigned int is_last;
-    if (tid == 0) is_last = atomicAdd(IO.counter, 1u) == (unsigned int)(gridDim.x - 1);
+    // (edge + interior launches of one step share the counter: nb_total CTAs in all)
+    const unsigned int nbt = in_.nb_total > 0 ? (unsigned int)in_.nb_total : gridDim.x;
+    if (tid == 0) is_last = atomicAdd(IO.counter, 1u) == nbt - 1;
     __syncthreads();
     if (!is_last) return;
     // plane totals T[s] = sum_tile partial[s][tile], tiles in order (el3_energy_from_planes, hw_api.cu)

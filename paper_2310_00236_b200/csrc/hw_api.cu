@@ -501,6 +501,7 @@ struct hw_solver {
     int el3_group = 1;          // CTA groups of adjacent tiles of the one-pass 3D kernels (elastic and acoustic)
     double* el3_ecoef = nullptr;  // its per-slab energy coefficients (slow-layered media; in plane_mem)
     bool el3_slab = false;        // ... on a slab of a decomposed domain (ghosts from HW_PLAN_FUSED_EL3)
+    int ac3_nb_edge = 0, ac3_nb_int = 0;  // one-pass 3D acoustic kernels on an NCCL slab: CTAs of the edge / interior launches
     int el3_nb_edge = 0, el3_nb_int = 0;  // ... NCCL slab: CTAs of the edge / interior launches (overlap)
     // Plane-ordered energy of the one-pass 3D kernels (fused_el3, fused3, fused3_32): per-(slab, tile)
     // partials, per-slab totals per sample, summed on the host in global slab order -- the same bits
@@ -905,6 +906,16 @@ int setup_handle(hw_solver* h) {
                     break;
                 }
             h->fused3 = true;
+            if (h->transport == 2 && max_rows >= 16 && nsm > 8) {  // overlapped halo exchange (edge slabs 0, L-1)
+                if ((rc = make_overlap_streams(h))) return rc;
+                // the edge launch (CTA groups of 1): 2 one-slab units per tile, ~3 ring iterations each -- 4 CTAs
+                // finish them well before the interior launch ends, so the exchange hides behind it
+                const int g = h->el3_group;
+                h->ac3_nb_edge = (int)(2 * tiles < 4 ? 2 * tiles : 4);
+                int64_t ni = (tiles / g) * (max_rows - 2);  // interior (tile group, slab) units
+                if (ni > (nsm - h->ac3_nb_edge) / g) ni = (nsm - h->ac3_nb_edge) / g;
+                h->ac3_nb_int = (int)(ni < 1 ? 1 : ni) * g;
+            }
             CU(cudaMalloc(&h->el3_eplane, (size_t)max_rows * (desc->nm / (4096 / desc->nx)) * sizeof(double)));
             h->plane_mem.push_back(h->el3_eplane);
         }
@@ -924,6 +935,16 @@ int setup_handle(hw_solver* h) {
                     break;
                 }
             h->fused3_32 = true;
+            if (h->transport == 2 && max_rows >= 16 && nsm > 8) {  // overlapped halo exchange (edge slabs 0, L-1)
+                if ((rc = make_overlap_streams(h))) return rc;
+                // the edge launch (CTA groups of 1): 2 one-slab units per tile, ~3 ring iterations each -- 4 CTAs
+                // finish them well before the interior launch ends, so the exchange hides behind it
+                const int g = h->el3_group;
+                h->ac3_nb_edge = (int)(2 * tiles < 4 ? 2 * tiles : 4);
+                int64_t ni = (tiles / g) * (max_rows - 2);  // interior (tile group, slab) units
+                if (ni > (nsm - h->ac3_nb_edge) / g) ni = (nsm - h->ac3_nb_edge) / g;
+                h->ac3_nb_int = (int)(ni < 1 ? 1 : ni) * g;
+            }
             CU(cudaMalloc(&h->el3_eplane, (size_t)max_rows * (desc->nm / (2048 / desc->nx)) * sizeof(double)));
             h->plane_mem.push_back(h->el3_eplane);
         }
@@ -1609,6 +1630,7 @@ static void fused3_bufs(const hw_solver* h, int cur, AcParams& P, Ac3In& in) {
     in.rp = src[F_N + F_P]; in.rvx = src[F_N + F_VX]; in.rvs = src[F_N + F_VS]; in.rvm = src[F_N + F_VM];
     in.slab = (h->world > 1 || h->transport != 0) ? 1 : 0;
     in.group = h->el3_group;
+    in.band = in.edge = in.nb_total = in.pad = 0;
     in.eplane = h->el3_eplane;
     in.etot = h->el3_etot;
 }
@@ -1771,6 +1793,40 @@ static int run_impl(hw_solver* h, int32_t variant, int64_t nt, const double* src
             h->launches += 2;
             cur ^= 1;
             if ((rc = exchange_nccl_plan(h, HW_PLAN_FUSED, cur))) return rc;
+        }
+        if (nt > 0) CU(cudaStreamWaitEvent(h->st, h->ev_int[(nt - 1) & 1], 0));
+    } else if ((h->fused3 || h->fused3_32) && h->transport == 2 && h->st2) {
+        // NCCL slab, overlapped (as the fused 2D kernel): edge slabs 0 and L-1 + the exchange on st,
+        // the interior slabs on st2
+        const StreamIO IO = stream_io(h, C);
+        const int sk = h->d.src_kind;
+        CU(cudaEventRecord(h->ev_edge[1], h->st));  // st2 starts after everything queued on st
+        int cur = 0;
+        for (int64_t n = 0; n < nt; n++) {
+            AcParams P = C.A;
+            Ac3In in;
+            fused3_bufs(h, cur, P, in);
+            in.edge = 1;
+            in.nb_total = h->ac3_nb_edge + h->ac3_nb_int;
+            Ac3In ie = in, ii = in;
+            ie.band = 1;
+            ie.group = 1;
+            ii.band = 2;
+            const int sample = energy && ((n + 1) % C.every == 0);
+            const double sv = (src && sk == HW_SRC_PRESSURE) ? src[n] : 0.0;
+            auto launch = [&](const Ac3In& a, int nb, cudaStream_t st) {
+                if (h->fused3_32) launch_ac3d_fused32(variant, P, a, IO, nb, n, sv, sample, (n + 1) / C.every, st);
+                else launch_ac3d_fused(variant, P, a, IO, nb, n, sv, sample, (n + 1) / C.every, st);
+            };
+            if (n > 0) CU(cudaStreamWaitEvent(h->st, h->ev_int[(n - 1) & 1], 0));
+            launch(ie, h->ac3_nb_edge, h->st);
+            CU(cudaEventRecord(h->ev_edge[n & 1], h->st));
+            CU(cudaStreamWaitEvent(h->st2, h->ev_edge[(n + 1) & 1], 0));  // edge(n-1), or the start
+            launch(ii, h->ac3_nb_int, h->st2);
+            CU(cudaEventRecord(h->ev_int[n & 1], h->st2));
+            h->launches += 2;
+            cur ^= 1;
+            if ((rc = exchange_nccl_plan(h, HW_PLAN_FUSED_AC3, cur))) return rc;
         }
         if (nt > 0) CU(cudaStreamWaitEvent(h->st, h->ev_int[(nt - 1) & 1], 0));
     } else if (h->fused3 || h->fused3_32) {  // one-pass 3D kernel, ping-pong A <-> B: step n reads buffer n % 2

@@ -105,6 +105,9 @@ struct Ac3In {
     const __half *p, *vx, *vs, *vm, *rp, *rvx, *rvs, *rvm;
     int32_t slab;  // slab of a decomposed domain: slab -1 is a ghost row (HW_PLAN_FUSED_AC3), not slab ns-1
     int32_t group;  // CTAs per group of adjacent tiles (divides the grid and the tile count)
+    // overlapped halo exchange (NCCL slab): band 1 = the edge slabs 0 and ns-1, 2 = the interior, 0 = all;
+    // edge = slabs per edge (1); nb_total = CTAs of the step over both launches (last-CTA count)
+    int32_t band, edge, nb_total, pad;
     double* eplane;  // [ns][tiles] energy partials of the (tile, slab) units (sample steps)
     double* etot;    // [samples][ns] energy plane totals (sample eidx at etot + eidx * ns)
 };

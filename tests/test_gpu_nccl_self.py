@@ -173,3 +173,23 @@ def test_nccl_el2_overlapped_device_resident_run(one_rank_job, fs, variant):
     oc = b.run(variant, sc)
     np.testing.assert_array_equal(np.array([t.samples for t in oc.traces]), np.array([t.samples for t in oa.traces]))
     np.testing.assert_allclose(oc.energy.values, oa.energy.values, rtol=1e-12)
+
+
+@pytest.mark.parametrize("prec,variant,ny", [(hw.Precision.FP16, hw.Variant.OP3, 8), (hw.Precision.FP16, hw.Variant.OP3, 64),
+                                             (hw.Precision.FP32, None, 8), (hw.Precision.FP32, hw.Variant.OP3, 32)])
+def test_nccl_ac3_overlapped(one_rank_job, prec, variant, ny):
+    """Config 3's one-pass kernels on the NCCL transport, overlapped: per step the edge slabs 0 and L-1
+    and the exchange on one stream, the interior slabs on another (two launches per step; 1 to 8 tiles,
+    CTA groups of 1 and 4), equal the single process -- fields, traces, energy bit for bit (plane order)."""
+    from test_gpu_slabs import _acoustic3d_onepass as mk
+
+    a, sa = mk(1, prec, src_z=0, ny=ny)
+    oa = a.run(variant, sa)
+    b, sb = mk(1, prec, src_z=0, ny=ny, distributed=True)
+    ob = b.run(variant, sb)
+    assert b.transport() == 2 and b.kernel_path() == a.kernel_path() == ("fused3d" if prec == hw.Precision.FP16 else "fused3d-f32")
+    assert b.last_launch_count() >= 2 * b.grid.nt
+    for n in a.FIELDS:
+        assert_same_bits(getattr(sb, n).values, getattr(sa, n).values, n)
+    np.testing.assert_array_equal(np.array([t.samples for t in ob.traces]), np.array([t.samples for t in oa.traces]))
+    np.testing.assert_array_equal(ob.energy.values, oa.energy.values)

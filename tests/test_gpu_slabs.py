@@ -163,20 +163,20 @@ def test_fused_2d_slabs_receivers_on_slab_edges(slabs):
     _compare(a, sa, oa, b, sb, ob)
 
 
-def _acoustic3d_onepass(slabs, prec=hw.Precision.FP16, nt=13, src_z=None):
+def _acoustic3d_onepass(slabs, prec=hw.Precision.FP16, nt=13, src_z=None, ny=8, distributed=False):
     """Config 3's one-pass kernels (2nd order, nx = 512, per-cell beta) on slabs: p(-1), p(L), v_slow(-1)
     and its residual arrive by the once-per-step exchange (HW_PLAN_FUSED_AC3)."""
-    nz, ny, nx = 40, 8, 512
+    nz, nx = 40, 512
     rng = np.random.default_rng(9)
     med = hw.build_acoustic_from_velocity(1.5 + 3.0 * rng.random((nz, ny, nx)))
     dx = 1.0 / nx
     g = hw.GridSpec(nx, ny, dx, float(np.float16(0.5 * dx / (med.c_max() * np.sqrt(3)))), nt, nz=nz, order=2)
     src = None if src_z is None else hw.SourceSpec(hw.SourceKind.PRESSURE_POINT, 300, 3, hw.RickerSpec(1 / (10 * dx), amplitude=5.0), iz=src_z)
-    s = hw.AcousticSolver(g, med, src, stencil_precision=prec, slabs=slabs, energy_every=3,
-                          receivers=((5, 5, 30), (511, 7, 0), (300, 3, 19), (17, 2, 39)))
+    s = hw.AcousticSolver(g, med, src, stencil_precision=prec, slabs=slabs, energy_every=3, distributed=distributed,
+                          receivers=((5, 5, 30), (511, ny - 1, 0), (300, 3, 19), (17, 2, 39), (100, ny // 2, 1)))
     st = s.new_state()
     z, y, x = np.mgrid[0:nz, 0:ny, 0:nx]
-    st.p.values = np.exp(-((x - 256) ** 2 / 2000.0 + (y - 4) ** 2 / 4.0 + (z - 19) ** 2 / 10.0)).astype(st.p.values.dtype)
+    st.p.values = np.exp(-((x - 256) ** 2 / 2000.0 + (y - ny // 2) ** 2 / 4.0 + (z - 19) ** 2 / 10.0)).astype(st.p.values.dtype)
     st.vz.values = (0.01 * rng.standard_normal((nz, ny, nx))).astype(st.vz.values.dtype)
     return s, st
 
