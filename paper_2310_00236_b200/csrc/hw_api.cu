@@ -1007,8 +1007,8 @@ int setup_handle(hw_solver* h) {
             }
         }
         if (want && !h->fused_el3 && !h->ac && h->d3 && h->LS == 16 && h->LU == 16 &&
-            el3d_stream_eligible(desc->nx, desc->nm, h->g.pitch, dev_smem)) {
-            if (el3d_stream_prepare(desc->nx) != cudaSuccess) return fail(HW_ECUDA, "streaming kernel setup failed");
+            el3d_stream_eligible(desc->nx, desc->nm, h->g.pitch, desc->order, dev_smem)) {
+            if (el3d_stream_prepare(desc->nx, desc->order) != cudaSuccess) return fail(HW_ECUDA, "streaming kernel setup failed");
             const int64_t units = (desc->nm / (2048 / desc->nx)) * max_rows;
             int64_t nbs = units / 4;
             if (nbs < 1) nbs = 1;

@@ -509,11 +509,13 @@ static size_t e3_stress_bytes(int64_t nx, int order) {
     return 128 + ((size_t)QR * (5 * TM + 3 * (2 * H - 1)) + 2 * 12 * TM) * nx * sizeof(__half);
 }
 
-bool el3d_stream_eligible(int64_t nx, int64_t nm, int64_t pitch, int max_smem) {
-    if (nx % 256 != 0 || nx > E3T * ECPT || pitch != nx) return false;
+// (the tile halos are sized by the order: nx = 1024 fits at 2nd order -- the per-GPU slab of BASELINE
+// config 5's 1024^3 / 8-GPU grid -- but not at 4th)
+bool el3d_stream_eligible(int64_t nx, int64_t nm, int64_t pitch, int order, int max_smem) {
+    if (nx % 256 != 0 || nx > E3T * ECPT || pitch != nx || (order != 2 && order != 4)) return false;
     const int64_t TM = E3T * ECPT / nx;
     if (nm % TM != 0) return false;
-    return e3_vel_bytes(nx, 4) <= (size_t)max_smem && e3_stress_bytes(nx, 4) <= (size_t)max_smem;
+    return e3_vel_bytes(nx, order) <= (size_t)max_smem && e3_stress_bytes(nx, order) <= (size_t)max_smem;
 }
 
 template <int V, int O>
@@ -526,9 +528,12 @@ static void e3_attrs(int64_t nx) {
                          (int)e3_stress_bytes(nx, O));
 }
 
-cudaError_t el3d_stream_prepare(int64_t nx) {
-    e3_attrs<0, 2>(nx); e3_attrs<3, 2>(nx); e3_attrs<6, 2>(nx);
-    e3_attrs<0, 4>(nx); e3_attrs<3, 4>(nx); e3_attrs<6, 4>(nx);
+cudaError_t el3d_stream_prepare(int64_t nx, int order) {
+    if (order == 2) {
+        e3_attrs<0, 2>(nx); e3_attrs<3, 2>(nx); e3_attrs<6, 2>(nx);
+    } else {
+        e3_attrs<0, 4>(nx); e3_attrs<3, 4>(nx); e3_attrs<6, 4>(nx);
+    }
     return cudaGetLastError();
 }
 

@@ -168,8 +168,8 @@ cudaError_t el3d_fused_prepare(int64_t nx);
 void launch_el3d_fused(int variant, const ElParams& P, const El3In& in, const StreamIO& IO, int nblocks, int64_t n,
                        double src, int sample, int64_t eidx, cudaStream_t st);
 // streaming 3D elastic phase kernels (hw_elastic3d_stream.cu)
-bool el3d_stream_eligible(int64_t nx, int64_t nm, int64_t pitch, int max_smem);
-cudaError_t el3d_stream_prepare(int64_t nx);
+bool el3d_stream_eligible(int64_t nx, int64_t nm, int64_t pitch, int order, int max_smem);
+cudaError_t el3d_stream_prepare(int64_t nx, int order);
 void launch_el3d_vel_stream(int variant, int order, const ElParams& P, int nblocks, int64_t n, double src,
                             cudaStream_t st);
 void launch_el3d_stress_stream(int variant, int order, const ElParams& P, const StreamIO& IO, int nblocks, int64_t n,

@@ -71,6 +71,25 @@ def test_el3d_stream_tiles_sources_full_media(ny, nz, kind):
     _check(s, st, out, ref)
 
 
+@pytest.mark.parametrize("nx,ny,nz,slabs", [(1024, 10, 9, 1), (1024, 8, 12, 3), (2048, 9, 8, 1)])
+def test_el3d_stream_wide_rows_2nd_order(nx, ny, nz, slabs):
+    """nx = 1024 (TM = 2) and 2048 (TM = 1) at 2nd order: the row width of a GPU's slab of BASELINE
+    config 5's 1024^3 / 8-GPU grid (these widths fit the shared memory at 2nd order only)."""
+    s, st = _case(nx, ny, nz, 7, order=2, kind=hw.SourceKind.VY_POINT, slabs=slabs)
+    ref = oracle.run_solver(s, hw.Variant.OP6, st)
+    out = s.run(hw.Variant.OP6, st)
+    assert s.kernel_path() == "stream3d"
+    _check(s, st, out, ref)
+
+
+def test_el3d_nx1024_4th_order_stays_generic():
+    s, st = _case(1024, 8, 9, 3, order=4)
+    ref = oracle.run_solver(s, hw.Variant.OP6, st)
+    out = s.run(hw.Variant.OP6, st)
+    assert s.kernel_path() == "generic"
+    _check(s, st, out, ref)
+
+
 def test_el3d_stream_nx512_equals_generic(hwopt):
     s1, st1 = _case(512, 12, 16, 8)
     out1 = s1.run(hw.Variant.OP6, st1)
