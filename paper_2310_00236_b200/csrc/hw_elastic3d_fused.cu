@@ -50,7 +50,11 @@ struct X3G {
     static constexpr int O_SXX = 0, O_SXS = R1, O_SSS = 2 * R1, O_SXM = 3 * R1, O_SMS = 3 * R1 + R2,
                          O_SMM = 3 * R1 + 2 * R2;
     static constexpr int SLOT = 3 * R1 + 3 * R2;
-    static constexpr int RING = 4;
+    // 4 tap slots (slabs F-2 .. F+1); rows of 1024 cells (TM = 2: relatively more halo rows per tile) leave
+    // room for 3 only -- then the slab-(F-2) values are carried in registers from the iteration before,
+    // when that slab sat in slot F-1, instead of being read from a fourth slot (CARRY below)
+    static constexpr int RING = NX_ >= 1024 ? 3 : 4;
+    static constexpr bool CARRY = RING == 3;
     // element offsets of the staged slots and the velocity tile generations
     static constexpr int A0 = RING * SLOT * NX;      // vx, vs, vm [rvx, rvs, rvm]: R1 rows each
     static constexpr int B0 = A0 + 6 * R1 * NX;      // rsxx rsss rsmm rsxs rsxm rsms: TM rows each
@@ -330,7 +334,7 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
         const int F0 = sb - 2, NI = se - sb + 4;
         const int gi0 = gi, ga0 = ga, gb0 = gb;
         auto issue_tap = [&](int i) {  // the six stress tiles of slab F0 + i
-            const int sl = (gi0 + i) & 3;
+            const int sl = (gi0 + i) % X::RING;
             x3_issue_tap<NX, TM>(S + sl * SLOT * NX, &bar[sl], in.sxx, in.sxs, in.sss, in.sxm, in.sms, in.smm, slab,
                                  wrap(F0 + i), m0, nm);
         };
@@ -347,11 +351,15 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
         if (tid == 32) issue_tap(0);
         if (tid == 64) issue_a(0);
         EV<PP> vs_m1, vs_m2;  // v_slow own rows of slabs F-2, F-3 (new)
+        // CARRY: the thread's slab-(F-2) stress values (own cells of the six fields; its halo-row cells of
+        // sms / sxs), read from slot F-1 at the end of the previous iteration
+        EV<PP> cold[6], chalo;
         float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);  // (stiff, lam, mu) of the stress slab (previous k)
 #pragma unroll 1
         for (int i = 0; i < NI; i++) {
             const int F = F0 + i;
-            const int s0 = (gi0 + i) & 3, s1 = (gi0 + i + 3) & 3, s2 = (gi0 + i + 2) & 3;  // F, F-1, F-2
+            const int s0 = (gi0 + i) % X::RING, s1 = (gi0 + i + X::RING - 1) % X::RING;  // F, F-1
+            const int s2 = X::CARRY ? s1 : (gi0 + i + 2) % X::RING;  // F-2 (CARRY: never read; its values are in registers)
             const int gen = i & 1;
             const __half* T0 = S + s0 * SLOT * NX;
             const __half* T1 = S + s1 * SLOT * NX;
@@ -364,14 +372,15 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
             const int k = wrap(F - 1);
             // medium coefficients of slab k (loaded before the ring waits)
             float4 cv = make_float4(0.f, 0.f, 0.f, 0.f), cn = cv;
-            float rch = 0.f;
+            float rch = 0.f, rch2 = 0.f;
             if (vel) {
                 const float4* cr = reinterpret_cast<const float4*>(in.coef) + 2 * ((int64_t)k * cm + (cm > 1 ? m : 0));
                 cv = __ldg(cr);
                 cn = __ldg(cr + 1);
                 if (j < 3) rch = __ldg(in.coef + 8 * ((int64_t)k * cm + (cm > 1 ? mh : 0)) + hq);
+                if (TM < 3 && j == 1) rch2 = __ldg(in.coef + 8 * ((int64_t)k * cm + (cm > 1 ? mhi : 0)) + 1);  // rho_s of vs(m0+TM)
             }
-            mbar_wait(&bar[s0], (uint32_t)(((gi0 + i) >> 2) & 1));
+            mbar_wait(&bar[s0], (uint32_t)(((gi0 + i) / X::RING) & 1));
             if (!vel) mbar_wait(abar, (uint32_t)((ga0 + i) & 1));
             EV<PP> vs_new;
             if (vel) {  // ---- velocities of slab k = F-1 (elastic.py:191-205, 3D)
@@ -380,7 +389,7 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                 // vx: fl(fl(ddx sxx + dds sxs) + ddm sxm)
                 const EV<PP> ax =
                     addv<PP>(addv<PP>(xfv<PP>(c, T1 + X::O_SXX * NX, to, tl, tr, false),
-                                      fv<PP>(c, ldv<PP>(T2 + X::O_SXS * NX + to), ldv<PP>(T1 + X::O_SXS * NX + to))),
+                                      fv<PP>(c, X::CARRY ? cold[3] : ldv<PP>(T2 + X::O_SXS * NX + to), ldv<PP>(T1 + X::O_SXS * NX + to))),
                              fv<PP>(c, ldv<PP>(T1 + X::O_SXM * NX + to), ldv<PP>(T1 + (X::O_SXM + 1) * NX + to)));
                 // v_slow: fl(fl(ddx sxs + dds sss) + ddm sms) (+ src)
                 EV<PP> as =
@@ -390,7 +399,7 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                 // v_mid: fl(fl(ddx sxm + dds sms) + ddm smm)
                 const EV<PP> am = addv<PP>(
                     addv<PP>(xfv<PP>(c, T1 + (X::O_SXM + 1) * NX, to, tl, tr, true),
-                             fv<PP>(c, ldv<PP>(T2 + (X::O_SMS + 1) * NX + to), ldv<PP>(T1 + (X::O_SMS + 1) * NX + to))),
+                             fv<PP>(c, X::CARRY ? cold[5] : ldv<PP>(T2 + (X::O_SMS + 1) * NX + to), ldv<PP>(T1 + (X::O_SMS + 1) * NX + to))),
                     fv<PP>(c, ldv<PP>(T1 + (X::O_SMM + 1) * NX + to), ldv<PP>(T1 + (X::O_SMM + 2) * NX + to)));
                 if (vsrc && k == in.vsrc_s && m == P.src_m && src_col) add_srcv<PP>(as.q, sj, sln, srch);
                 // the old values are waited for only now: the A slot was refilled during the previous
@@ -438,33 +447,43 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                     if (comp) rh = ldv<PP>(A + 5 * R1 * NX + a0);
                     const EV<PP> a =
                         addv<PP>(addv<PP>(xfv<PP>(c, T1 + X::O_SXM * NX, to, tl, tr, true),
-                                          fv<PP>(c, ldv<PP>(T2 + X::O_SMS * NX + a0), ldv<PP>(T1 + X::O_SMS * NX + a0))),
+                                          fv<PP>(c, X::CARRY ? chalo : ldv<PP>(T2 + X::O_SMS * NX + a0), ldv<PP>(T1 + X::O_SMS * NX + a0))),
                                  fv<PP>(c, ldv<PP>(T1 + X::O_SMM * NX + a0), ldv<PP>(T1 + (X::O_SMM + 1) * NX + a0)));
 #pragma unroll
                     for (int q = 0; q < PP; q++) x3_finish<V>(a.q[q], rch, x3_rcp(rch), in.div_mode[2], dt2, srch, h.q[q], rh.q[q]);
                     stv<PP>(VT + 2 * R1 * NX + a0, h);
-                } else if (j == 1 || j == 2) {
-                    const int a0 = TM * NX + x;  // row TM of the tiles
-                    const int fo = j == 1 ? 0 : R1 * NX;  // vx or vs in the A slot / the velocity tile
-                    EV<PP> h = ldv<PP>(A + fo + a0);
-                    EV<PP> rh;
-                    if (comp) rh = ldv<PP>(A + 3 * R1 * NX + fo + a0);
-                    EV<PP> a;
-                    if (j == 1) {
-                        a = addv<PP>(addv<PP>(xfv<PP>(c, T1 + X::O_SXX * NX + (TM - 1) * NX, to, tl, tr, false),
-                                              fv<PP>(c, ldv<PP>(T2 + X::O_SXS * NX + a0), ldv<PP>(T1 + X::O_SXS * NX + a0))),
-                                     fv<PP>(c, ldv<PP>(T1 + X::O_SXM * NX + a0), ldv<PP>(T1 + (X::O_SXM + 1) * NX + a0)));
+                } else if (j == 1 || (TM >= 3 && j == 2)) {
+                    // thread row jj's halo row: jj = 1 -> vx(m0+TM), jj = 2 -> vs(m0+TM); a tile of TM = 2 rows has
+                    // no thread row 2, so its row 1 takes both
+                    auto halo_hi = [&](int jj, float rc) {
+                        const int a0 = TM * NX + x;  // row TM of the tiles
+                        const int fo = jj == 1 ? 0 : R1 * NX;  // vx or vs in the A slot / the velocity tile
+                        const int dj = (jj - j) * NX, to_ = to + dj, tl_ = tl + dj, tr_ = tr + dj;
+                        EV<PP> h = ldv<PP>(A + fo + a0);
+                        EV<PP> rh;
+                        if (comp) rh = ldv<PP>(A + 3 * R1 * NX + fo + a0);
+                        EV<PP> a;
+                        if (jj == 1) {
+                            a = addv<PP>(addv<PP>(xfv<PP>(c, T1 + X::O_SXX * NX + (TM - 1) * NX, to_, tl_, tr_, false),
+                                                  fv<PP>(c, X::CARRY ? chalo : ldv<PP>(T2 + X::O_SXS * NX + a0), ldv<PP>(T1 + X::O_SXS * NX + a0))),
+                                         fv<PP>(c, ldv<PP>(T1 + X::O_SXM * NX + a0), ldv<PP>(T1 + (X::O_SXM + 1) * NX + a0)));
+                        } else {
+                            a = addv<PP>(addv<PP>(xfv<PP>(c, T1 + X::O_SXS * NX + (TM - 2) * NX, to_, tl_, tr_, true),
+                                                  fv<PP>(c, ldv<PP>(T1 + X::O_SSS * NX + a0), ldv<PP>(T0 + X::O_SSS * NX + a0))),
+                                         fv<PP>(c, ldv<PP>(T1 + X::O_SMS * NX + a0), ldv<PP>(T1 + (X::O_SMS + 1) * NX + a0)));
+                            if (vsrc && k == in.vsrc_s && mhi == P.src_m && src_col) add_srcv<PP>(a.q, sj, sln, srch);
+                        }
+                        const int hm = in.div_mode[jj == 1 ? 0 : 1];
+#pragma unroll
+                        for (int q = 0; q < PP; q++) x3_finish<V>(a.q[q], rc, x3_rcp(rc), hm, dt2, srch, h.q[q], rh.q[q]);
+                        stv<PP>(VT + fo + a0, h);
+                    };
+                    if constexpr (TM >= 3) {
+                        halo_hi(j, rch);
                     } else {
-                        a = addv<PP>(addv<PP>(xfv<PP>(c, T1 + X::O_SXS * NX + (TM - 2) * NX, to, tl, tr, true),
-                                              fv<PP>(c, ldv<PP>(T1 + X::O_SSS * NX + a0), ldv<PP>(T0 + X::O_SSS * NX + a0))),
-                                     fv<PP>(c, ldv<PP>(T1 + X::O_SMS * NX + a0), ldv<PP>(T1 + (X::O_SMS + 1) * NX + a0)));
-                        if (vsrc && k == in.vsrc_s && mhi == P.src_m && src_col) add_srcv<PP>(a.q, sj, sln, srch);
+                        halo_hi(1, rch);
+                        halo_hi(2, rch2);
                     }
-#pragma unroll
-                    const int hm = in.div_mode[j == 1 ? 0 : 1];
-#pragma unroll
-                    for (int q = 0; q < PP; q++) x3_finish<V>(a.q[q], rch, x3_rcp(rch), hm, dt2, srch, h.q[q], rh.q[q]);
-                    stv<PP>(VT + fo + a0, h);
                 }
             }
             __syncthreads();  // velocity tiles of slab F-1 visible; the A slot and tap slot (i+1) % RING are free
@@ -484,12 +503,17 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                 const EV<PP> dvs = fv<PP>(c, vs_m2, vs_m1);  // v_slow(s-1), v_slow(s) (own rows)
                 const EV<PP> dvm = fv<PP>(c, ldv<PP>(vmt + to), ldv<PP>(vmt + NX + to));
                 EV<PP> old[6], nw[6], rr[6];
-                old[0] = ldv<PP>(T2 + X::O_SXX * NX + to);
-                old[1] = ldv<PP>(T2 + X::O_SSS * NX + to);
-                old[2] = ldv<PP>(T2 + (X::O_SMM + 1) * NX + to);
-                old[3] = ldv<PP>(T2 + X::O_SXS * NX + to);
-                old[4] = ldv<PP>(T2 + (X::O_SXM + 1) * NX + to);
-                old[5] = ldv<PP>(T2 + (X::O_SMS + 1) * NX + to);
+                if constexpr (X::CARRY) {
+#pragma unroll
+                    for (int q = 0; q < 6; q++) old[q] = cold[q];
+                } else {
+                    old[0] = ldv<PP>(T2 + X::O_SXX * NX + to);
+                    old[1] = ldv<PP>(T2 + X::O_SSS * NX + to);
+                    old[2] = ldv<PP>(T2 + (X::O_SMM + 1) * NX + to);
+                    old[3] = ldv<PP>(T2 + X::O_SXS * NX + to);
+                    old[4] = ldv<PP>(T2 + (X::O_SXM + 1) * NX + to);
+                    old[5] = ldv<PP>(T2 + (X::O_SMS + 1) * NX + to);
+                }
 #pragma unroll
                 for (int q = 0; q < 6; q++) nw[q] = old[q];
                 const EH2 stiff = vsplat<16, 2>(__float2half_rn(cs.x)), lam = vsplat<16, 2>(__float2half_rn(cs.y));
@@ -601,6 +625,17 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
                 vs_m2 = vs_m1;
                 vs_m1 = vs_new;
                 cs = cn;  // moduli of slab k: the next iteration's stress slab
+            }
+            if constexpr (X::CARRY) {  // slab F-1 is the next iteration's slab F-2: its slot is refilled then
+                if (i >= 1) {
+                    cold[0] = ldv<PP>(T1 + X::O_SXX * NX + to);
+                    cold[1] = ldv<PP>(T1 + X::O_SSS * NX + to);
+                    cold[2] = ldv<PP>(T1 + (X::O_SMM + 1) * NX + to);
+                    cold[3] = ldv<PP>(T1 + X::O_SXS * NX + to);
+                    cold[4] = ldv<PP>(T1 + (X::O_SXM + 1) * NX + to);
+                    cold[5] = ldv<PP>(T1 + (X::O_SMS + 1) * NX + to);
+                    chalo = ldv<PP>(T1 + (j == 0 ? X::O_SMS * NX : (X::O_SXS + TM) * NX) + x);
+                }
             }
             __syncthreads();  // the previous velocity generation and the B slot are free
             if (tid == 96 && i + 1 < NI && F + 1 - 2 >= sb && F + 1 - 2 < se) {
@@ -720,12 +755,12 @@ __global__ void k_el3_ecoef(Plane64 rx, Plane64 rs, Plane64 rm, Plane64 la, Plan
 constexpr int X3C = HW_X3C;  // cells per thread (4 or 8)
 
 static size_t x3_bytes(int64_t nx) {
-    return nx == 512 ? X3G<512, X3C>::BYTES : X3G<256, X3C>::BYTES;
+    return nx == 1024 ? X3G<1024, X3C>::BYTES : (nx == 512 ? X3G<512, X3C>::BYTES : X3G<256, X3C>::BYTES);
 }
 
 bool el3d_fused_eligible(const ElParams& P, int64_t nx, int64_t nm, int64_t ns, int64_t pitch, int order,
                          int max_smem) {
-    if (order != 2 || P.fs || (nx != 256 && nx != 512) || pitch != nx || ns < 4) return false;
+    if (order != 2 || P.fs || (nx != 256 && nx != 512 && nx != 1024) || pitch != nx || ns < 4) return false;
     const int64_t TM = 2048 / nx;
     if (nm % TM != 0 || nm < 2 * TM || x3_bytes(nx) > (size_t)max_smem) return false;
     // densities and moduli constant along x (slow-layered or per (slab, mid) row)
@@ -770,7 +805,8 @@ static void x3_attrs() {
 }
 
 cudaError_t el3d_fused_prepare(int64_t nx) {
-    if (nx == 512) x3_attrs<512>();
+    if (nx == 1024) x3_attrs<1024>();
+    else if (nx == 512) x3_attrs<512>();
     else x3_attrs<256>();
     return cudaGetLastError();
 }
@@ -786,7 +822,8 @@ static void* x3_fn(int variant, int sample) {
 
 void launch_el3d_fused(int variant, const ElParams& P, const El3In& in, const StreamIO& IO, int nblocks, int64_t n,
                        double src, int sample, int64_t eidx, cudaStream_t st) {
-    void* fn = P.g.nx == 512 ? x3_fn<512>(variant, sample) : x3_fn<256>(variant, sample);
+    void* fn = P.g.nx == 1024 ? x3_fn<1024>(variant, sample)
+                              : (P.g.nx == 512 ? x3_fn<512>(variant, sample) : x3_fn<256>(variant, sample));
     void* args[] = {(void*)&P, (void*)&in, (void*)&IO, (void*)&n, (void*)&src, (void*)&eidx};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(nblocks);

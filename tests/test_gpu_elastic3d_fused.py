@@ -1,5 +1,5 @@
 """The one-pass 3D elastic step (csrc/hw_elastic3d_fused.cu: 2nd order, binary16, single
-periodic domain, ping-pong buffers, nx 256 or 512, media constant along x) against the CPU
+periodic domain, ping-pong buffers, nx 256, 512 or 1024, media constant along x) against the CPU
 oracle and the two-phase streaming kernels: bit-exact fields, traces and failure steps;
 energy within 1e-12."""
 
@@ -37,6 +37,32 @@ def test_el3d_fused_tiles_and_slab_splits(nx, ny, nz):
     # media varying along x (full planes) take the streaming kernels
     assert s.kernel_path() == ("stream3d" if nz == 20 else "fused3d-el")
     _check(s, st, out, ref)
+
+
+@pytest.mark.parametrize("variant", [None, hw.Variant.OP3, hw.Variant.OP6])
+@pytest.mark.parametrize("ny,nz", [(8, 9), (10, 33)])
+def test_el3d_fused_nx1024(variant, ny, nz):
+    """Rows of 1024 cells (the per-GPU slab width of BASELINE config 5's 1024^3 / 8-GPU grid): tiles of
+    TM = 2 rows, a 3-slot tap ring with the slab-(F-2) values carried in registers, thread row 1 taking
+    both upper halo rows."""
+    s, st = _case(1024, ny, nz, 7, kind=hw.SourceKind.VY_POINT if nz == 9 else hw.SourceKind.EXPLOSIVE)
+    ref = oracle.run_solver(s, variant, st)
+    out = s.run(variant, st)
+    assert s.kernel_path() == "fused3d-el"
+    _check(s, st, out, ref)
+
+
+def test_el3d_fused_nx1024_sources_on_tile_edges_and_slabs():
+    for iy, iz, kind, slabs in ((1, 0, hw.SourceKind.VY_POINT, 1), (2, 5, hw.SourceKind.VY_POINT, 2),
+                                (0, 11, hw.SourceKind.EXPLOSIVE, 3), (7, 6, hw.SourceKind.VY_POINT, 4)):
+        s, st = _case(1024, 8, 24, 7)
+        src = hw.SourceSpec(kind, 1023 if iy == 1 else 37, iy, hw.RickerSpec(1 / (10 * s.grid.dx), amplitude=30.0), iz=iz)
+        s = hw.ElasticSolver(s.grid, s.medium, src, stencil_precision=hw.Precision.FP16, slabs=slabs,
+                             receivers=((37, iy, iz), (1, 2, 3), (1023, 7, 23), (0, 0, 12)), energy_every=2)
+        ref = oracle.run_solver(s, hw.Variant.OP6, st)
+        out = s.run(hw.Variant.OP6, st)
+        assert s.kernel_path() == "fused3d-el" and s.transport() == (0 if slabs == 1 else 1)
+        _check(s, st, out, ref)
 
 
 def test_el3d_fused_sources_on_tile_edges():
