@@ -50,11 +50,14 @@ struct X3G {
     static constexpr int O_SXX = 0, O_SXS = R1, O_SSS = 2 * R1, O_SXM = 3 * R1, O_SMS = 3 * R1 + R2,
                          O_SMM = 3 * R1 + 2 * R2;
     static constexpr int SLOT = 3 * R1 + 3 * R2;
-    // 4 tap slots (slabs F-2 .. F+1); rows of 1024 cells (TM = 2: relatively more halo rows per tile) leave
-    // room for 3 only -- then the slab-(F-2) values are carried in registers from the iteration before,
-    // when that slab sat in slot F-1, instead of being read from a fourth slot (CARRY below)
-    static constexpr int RING = NX_ >= 1024 ? 3 : 4;
-    static constexpr bool CARRY = RING == 3;
+    // 3 tap slots (slabs F-1, F, F+1; slab F+1 requested a full iteration ahead).  The slab-(F-2) values a
+    // step needs (slow-axis taps of sxs / sms, the old stresses of the stress phase) are carried in
+    // registers from the iteration before, when that slab sat in slot F-1 (CARRY) -- a fourth slot
+    // holding slab F-2 measured 1.3 % slower at nx = 512 (216 vs 183 KB of shared memory: less L1 left)
+    // and does not fit at nx = 1024 (264 KB); a fourth slot used to prefetch two iterations ahead: 0.6 % slower
+    static constexpr int RING = 3;
+    static constexpr bool CARRY = true;
+    static constexpr int PD = RING - 2;  // tap prefetch distance in iterations
     // element offsets of the staged slots and the velocity tile generations
     static constexpr int A0 = RING * SLOT * NX;      // vx, vs, vm [rvx, rvs, rvm]: R1 rows each
     static constexpr int B0 = A0 + 6 * R1 * NX;      // rsxx rsss rsmm rsxs rsxm rsms: TM rows each
@@ -348,7 +351,10 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
         };
         // the TMA requests are issued by lane 0 of warps 1, 2 and 3 (the tap ring, the A slot, the B
         // slot): one on each of three SM sub-partitions, so no warp carries all of them into the barriers
-        if (tid == 32) issue_tap(0);
+        if (tid == 32) {
+            issue_tap(0);
+            if (X::PD > 1 && NI > 1) issue_tap(1);
+        }
         if (tid == 64) issue_a(0);
         EV<PP> vs_m1, vs_m2;  // v_slow own rows of slabs F-2, F-3 (new)
         // CARRY: the thread's slab-(F-2) stress values (own cells of the six fields; its halo-row cells of
@@ -364,9 +370,9 @@ __global__ void __launch_bounds__(2048 / CPT, 1)
             const __half* T0 = S + s0 * SLOT * NX;
             const __half* T1 = S + s1 * SLOT * NX;
             const __half* T2 = S + s2 * SLOT * NX;
-            if (tid == 32 && i + 1 < NI) {  // slot (i+1) % RING held slab F-3: last read in iteration i-1
+            if (tid == 32 && i + X::PD < NI) {  // slot (i + PD) % RING held slab F-2: last read in iteration i-1
                 fence_proxy_async_smem();
-                issue_tap(i + 1);
+                issue_tap(i + X::PD);
             }
             const bool vel = i >= 2;
             const int k = wrap(F - 1);

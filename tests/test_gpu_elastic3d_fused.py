@@ -1,5 +1,5 @@
 """The one-pass 3D elastic step (csrc/hw_elastic3d_fused.cu: 2nd order, binary16, single
-periodic domain, ping-pong buffers, nx 256, 512 or 1024, media constant along x) against the CPU
+periodic domain or a slab, ping-pong buffers, nx 256, 512 or 1024, media constant along x) against the CPU
 oracle and the two-phase streaming kernels: bit-exact fields, traces and failure steps;
 energy within 1e-12."""
 
