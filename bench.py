@@ -396,6 +396,12 @@ def extra_configs(hw, with_cpu):
                      "4 leapfrog steps at 4096^2 (fp16 op6)")) if with_cpu else None
     res["config4"] = sub_config(hw, "config4", lambda: make_config4(hw), hw.Variant.OP6, 40, 4096 * 4097, 5000,
                                 "k_el2d_fused, free surface (40 B/cell-step)", cpu=cpu4, traffic_key="config4")
+    # the per-GPU slab of config 5's 8-GPU grid (1024^3 over 8 z-slabs), run here as a periodic domain of
+    # that shape: the rate of one GPU's kernels on its slab, without the exchange
+    res["config5_slab_of_1024cubed_over_8"] = sub_config(
+        hw, "config5 1024x1024x128", lambda: make_config5(hw, n=1024, nz=128, nt=200), hw.Variant.OP6, B_ALG5,
+        1024 * 1024 * 128, 200, "k_el3d_fused at nx = 1024 (tiles of 2 rows): one GPU's slab of the 1024^3 / 8-GPU "
+        "grid as a periodic single domain (72 B/cell-step)", init=init_config5)
     res["config1"] = sub_config(hw, "config1", lambda: make_config1(hw, F16), hw.Variant.OP3, 24, 256 * 256, 2000,
                                 "persistent small-grid kernel on the mirrored 512^2 domain (cells counted: the 256^2 "
                                 "box), energy every step: latency-bound, not an HBM roofline config", init=init_config1, repeats=3)
