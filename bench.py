@@ -417,6 +417,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the configs 1-4 sub-objects")
     ap.add_argument("--nt", type=int, default=NT5, help="leapfrog steps per bench step")
+    ap.add_argument("--with-1024cubed", action="store_true",
+                    help="at --gpus 8 also time config 5's 1024^3 global grid (every rank builds ~80 GB of global "
+                         "host arrays first: minutes of host time; off by default so the scaling runs stay short -- "
+                         "the N=1 line carries one GPU's slab of that grid as a sub-config)")
     ap.add_argument("--rank-probe", action="store_true", help=argparse.SUPPRESS)  # spawn test: print rank, exit
     args = ap.parse_args()
     ws, rank, local = dist_env()
@@ -514,7 +518,7 @@ def main():
 
     # ---------------------------------------------------------- 1024^3 over 8 GPUs (the config's global grid)
     extra = {}
-    if ws == 8:
+    if ws == 8 and args.with_1024cubed:
         # every rank builds the global host arrays (medium planes in fp64 + state): ~80 GB per rank at
         # 1024^3; measured only when the host has room for all eight ranks, reported either way
         import psutil
