@@ -11,7 +11,7 @@ the final energy relative to the fp64 arm, the receiver traces' relative L2 dist
 arm (diagnostics.compare_traces), and the device throughput.  Synthetic seeded inputs of the
 BASELINE shapes stand in for any dataset.
 
-    python tools/precision_study.py [configs, default 1,2,3,4,5] > profiles/r1_precision_study.jsonl
+    python tools/precision_study.py [configs, default 1,2,3,4,5] > profiles/r2_precision_study.jsonl
 """
 import json
 import sys
@@ -62,7 +62,7 @@ def config2(prec, upd=None):
     import bench
 
     n = 4096
-    s0 = bench.make_solver(hw, nt=5000)
+    s0 = bench.make_config2(hw, nt=5000)
     s = hw.AcousticSolver(s0.grid, s0.medium, s0.source, stencil_precision=prec, update_precision=upd,
                           receivers=((n // 2, 600), (n // 2 + 400, 400)), energy_every=10)  # source at (n/2, 8)
     return s, None, 2.0 * s0.source.wavelet.delay, n * n
