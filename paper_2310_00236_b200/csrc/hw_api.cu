@@ -49,6 +49,7 @@ Option g_opts[] = {
     {"el3_group", 4, 1, 4, "one-pass 3D elastic kernel: at most this many CTAs stream adjacent tiles side by side"},
     {"ac3_group", 4, 1, 4, "one-pass 3D acoustic kernels: at most this many CTAs stream adjacent tiles side by side"},
     {"guard", 0, 0, 2, "device allocations between unmapped pages (tests): 1 = start at a mapping start, 2 = end at a mapping end"},
+    {"el3_edge_ctas", 0, 0, 64, "one-pass 3D elastic kernel on an NCCL slab: CTAs of the edge launch (0 = automatic)"},
     {"nccl_self", 0, 0, 1, "a one-rank job with an NCCL id takes the NCCL transport (self exchange: tests)"},
 };
 int64_t opt(const char* name) {
@@ -209,6 +210,7 @@ LaneConsts make_consts(const double taps[4], double dt_u) {
 enum { F_P, F_VX, F_VS, F_VM, F_SXX, F_SSS, F_SMM, F_SXS, F_SXM, F_SMS, F_N };
 const int HALF_S[F_N] = {0, 0, 1, 0, 0, 0, 0, 1, 0, 1};
 constexpr int EL3_EDGE = 2;  // edge slabs per side of an overlapped one-pass 3D elastic slab step
+constexpr double EL3_EDGE_SHARE = 1.0;  // CTAs of the edge launch relative to its share of the work
 
 const int EXT_AC2[] = {F_P, F_VX, F_VS};
 const int EXT_AC3[] = {F_P, F_VX, F_VM, F_VS};
@@ -998,11 +1000,11 @@ int setup_handle(hw_solver* h) {
             if (h->transport == 2 && max_rows >= 5 * EL3_EDGE) {
                 if ((rc = make_overlap_streams(h))) return rc;
                 const double we = 3.0 * 2 * EL3_EDGE, wi = (double)(max_rows - 2 * EL3_EDGE);
-                int ne = (int)(nsm * we / (we + wi) + 0.5);
-                ne = ne < 1 ? 1 : (ne > nsm - 1 ? nsm - 1 : ne);
+                int ne = opt("el3_edge_ctas") > 0 ? (int)opt("el3_edge_ctas") : (int)(nsm * EL3_EDGE_SHARE * we / (we + wi) + 0.5);
+                ne = ne < 1 ? 1 : (ne > nsm / 2 ? nsm / 2 : ne);
                 int ni = nsm - ne;
                 if (ni % h->el3_group) ni -= ni % h->el3_group;
-                h->el3_nb_edge = ne;
+                h->el3_nb_edge = nsm - ni;  // (the CTAs the interior's group rounding leaves go to the edges)
                 h->el3_nb_int = ni;
             }
         }
