@@ -1,7 +1,7 @@
 """Strong-scaling proxy on one B200: config 5's 512^3 grid cut into N z-slabs, ONE slab (512 x 512 x 512/N)
 run as a one-rank NCCL job (option nccl_self: edge slabs + exchange to itself overlapped with the interior
 slabs) -- the per-GPU step of an N-GPU run, with the self exchange standing in for NVLink -- against the
-single-domain 512^3 step / N.  python tools/measure_strong_proxy.py [nt] [edge_ctas ...] -> one JSON line per N."""
+single-domain 512^3 step / N.  python tools/measure_strong_proxy.py [--opt name=value ...] [nt] [edge_ctas ...] -> one JSON line per N."""
 import json
 import socket
 import sys
@@ -13,8 +13,14 @@ import torch.distributed as dist  # noqa: E402
 import bench  # noqa: E402
 import paper_2310_00236_b200 as hw  # noqa: E402
 
-nt = int(sys.argv[1]) if len(sys.argv) > 1 else 200
-sweep = [int(a) for a in sys.argv[2:]] or [0]
+args = sys.argv[1:]
+while "--opt" in args:  # --opt name=value: library kernel-path options (hw_set_option)
+    i = args.index("--opt")
+    k, v = args[i + 1].split("=")
+    hw.set_option(k, int(v))
+    del args[i:i + 2]
+nt = int(args[0]) if args else 200
+sweep = [int(a) for a in args[1:]] or [0]
 with socket.socket() as sk:
     sk.bind(("127.0.0.1", 0))
     port = sk.getsockname()[1]
