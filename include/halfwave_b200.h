@@ -235,6 +235,8 @@ int hw_plane_div_mode(const hw_solver* h, int32_t plane);
  *   "fused_el3" 1 one-pass 3D elastic kernel (2nd order, media constant along x) | 0 two-phase
  *   "el3_group" 4 at most this many CTAs of the one-pass 3D elastic kernel stream adjacent tiles
  *   "ac3_group" 4 the same for the one-pass 3D acoustic kernels (binary16 and binary32)
+ *   "el3_overlap_min_rows" 0 | n: NCCL slabs thinner than n slow rows run one launch and exchange in stream order
+ *               (no edge / interior split; for A/B runs on a multi-GPU box)
  *   "el3_edge_ctas" 0 automatic | 1..64 CTAs of the edge launch of the one-pass 3D elastic kernel on an NCCL slab
  *   "guard"     0 | 1 | 2 every device buffer in its own mapping between unmapped pages, starting at the
  *               mapping's start (1) or ending at its end (2): out-of-bounds accesses fault (tests)

@@ -49,6 +49,7 @@ Option g_opts[] = {
     {"el3_group", 4, 1, 4, "one-pass 3D elastic kernel: at most this many CTAs stream adjacent tiles side by side"},
     {"ac3_group", 4, 1, 4, "one-pass 3D acoustic kernels: at most this many CTAs stream adjacent tiles side by side"},
     {"guard", 0, 0, 2, "device allocations between unmapped pages (tests): 1 = start at a mapping start, 2 = end at a mapping end"},
+    {"el3_overlap_min_rows", 0, 0, 1 << 20, "one-pass 3D elastic kernel on an NCCL slab: thinner slabs exchange in stream order after one launch (no edge / interior split)"},
     {"el3_edge_ctas", 0, 0, 64, "one-pass 3D elastic kernel on an NCCL slab: CTAs of the edge launch (0 = automatic)"},
     {"nccl_self", 0, 0, 1, "a one-rank job with an NCCL id takes the NCCL transport (self exchange: tests)"},
 };
@@ -997,7 +998,7 @@ int setup_handle(hw_solver* h) {
             // NCCL slab: edge slabs (every row the exchange sends) + the exchange on st, the interior
             // slabs on st2; CTAs split so both launches take about as long (an edge segment of
             // 2 slabs costs ~3 slabs: the ring fill)
-            if (h->transport == 2 && max_rows >= 5 * EL3_EDGE) {
+            if (h->transport == 2 && max_rows >= 5 * EL3_EDGE && max_rows >= opt("el3_overlap_min_rows")) {
                 if ((rc = make_overlap_streams(h))) return rc;
                 const double we = 3.0 * 2 * EL3_EDGE, wi = (double)(max_rows - 2 * EL3_EDGE);
                 int ne = opt("el3_edge_ctas") > 0 ? (int)opt("el3_edge_ctas") : (int)(nsm * EL3_EDGE_SHARE * we / (we + wi) + 0.5);
